@@ -1,0 +1,205 @@
+/*
+ * mmws_gpu.h -- C ABI of libmmws_gpu, the B200 (sm_100a) implementation of the
+ * reference's dense-matmul hot path (arxiv/paper_1012_2273, "mmws").
+ *
+ * The reference exposes its hot path as inline C++ in namespace mmws (no FFI):
+ *   Matrix matmul_seq(const Matrix&, const Matrix&)            matrix.hpp:112-126
+ *   Matrix matmul_threads(const Matrix&, const Matrix&, unsigned) workshare.hpp:98-113
+ *   std::vector<WorkAssignment> split_rows(int64_t, int)       protocol.hpp:33-46
+ *   std::pair<Matrix,double> master_run(Communicator&, A, B)   protocol.hpp:50-108
+ *   void worker_run(Communicator&)                              protocol.hpp:112-147
+ *   Partition static_partition(size_t, unsigned)               workshare.hpp:33-46
+ *   uint64_t op_count(int64_t)                                  matrix.hpp:130-134
+ * Each entry point below names the one it replaces.  All paths are relative
+ * to the reference tree's proj/ directory.  The C++ drop-in adapter that
+ * restores the reference's signatures and exception types on top of this ABI
+ * is include/mmws_gpu.hpp.
+ *
+ * Conventions: plain pointers and sizes, row-major matrices with explicit
+ * leading dimensions (elements), every function returns an int status
+ * (MMWS_GPU_OK == 0), no exception crosses the ABI, and the message of the
+ * last failure on the calling thread is mmws_gpu_last_error().  A context is
+ * bound to one CUDA device and serialises its callers with a mutex.  There is
+ * no CPU fallback: without a usable sm_100 device mmws_gpu_init fails.
+ */
+#ifndef MMWS_GPU_H_
+#define MMWS_GPU_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MMWS_GPU_ABI_VERSION 1
+
+/* Status codes.  DIMENSION / DOMAIN mirror the reference's DimensionError /
+ * DomainError (error.hpp:9-17); RANK / PROTOCOL mirror RankError /
+ * ProtocolError (error.hpp:20-32); CUDA / NCCL / ALLOC / STATE are device-side
+ * failures the reference cannot have. */
+enum {
+  MMWS_GPU_OK = 0,
+  MMWS_GPU_ERR_DIMENSION = 1,
+  MMWS_GPU_ERR_DOMAIN = 2,
+  MMWS_GPU_ERR_CUDA = 3,
+  MMWS_GPU_ERR_NCCL = 4,
+  MMWS_GPU_ERR_RANK = 5,
+  MMWS_GPU_ERR_PROTOCOL = 6,
+  MMWS_GPU_ERR_STATE = 7,
+  MMWS_GPU_ERR_ALLOC = 8
+};
+
+/* Multiply modes.
+ *   EXACT      per element acc = +0.0, then acc += a*b for k ascending with
+ *              separate roundings: bitwise identical to matmul_seq for every
+ *              NaN-free input (matrix.hpp:118-124).  FP64 pipe, DMUL+DADD.
+ *   DMMA       FP64 tensor path (mma.sync m8n8k4 -> DMMA.8x8x4), 128x128 tiles,
+ *              TMA + mbarrier pipeline.  Bit-exact for integer-valued inputs
+ *              whose partial sums stay below 2^53; normwise <= 1e-12 otherwise.
+ *   DMMA_SMALL same math on 64x64 tiles (more CTAs for N < ~2000).
+ *   AUTO       DMMA or DMMA_SMALL by problem size (fp64); FFMA (fp32).
+ *   FFMA       fp32 register-blocked FFMA GEMM (sgemm only). */
+enum {
+  MMWS_GPU_MODE_AUTO = 0,
+  MMWS_GPU_MODE_EXACT = 1,
+  MMWS_GPU_MODE_DMMA = 2,
+  MMWS_GPU_MODE_DMMA_SMALL = 3,
+  MMWS_GPU_MODE_FFMA = 4
+};
+
+/* Generator distributions over the reference's splitmix64 stream
+ * (matrix.hpp:23-33, random_matrix matrix.hpp:101-107): element i of a
+ * matrix is derived from the (i+1)-th output for `seed`.
+ *   UNIT     (bits>>11) * 2^-53 in [0,1)         == mmws::random_matrix
+ *   UNIFORM  2u - 1 in [-1,1)                     (configs C1, C2, C4)
+ *   INT8     ((bits>>11)*17 >> 53) - 8 in [-8,8]  (config C3, exact)
+ *   NORMAL   Box-Muller from draws 2i, 2i+1       (config C5, fp32)  */
+enum {
+  MMWS_GPU_DIST_UNIT = 0,
+  MMWS_GPU_DIST_UNIFORM = 1,
+  MMWS_GPU_DIST_INT8 = 2,
+  MMWS_GPU_DIST_NORMAL = 3
+};
+
+/* Peak probes (mmws_gpu_peak_probe). */
+enum {
+  MMWS_GPU_PROBE_DMMA = 0,
+  MMWS_GPU_PROBE_DFMA = 1,
+  MMWS_GPU_PROBE_DMUL_DADD = 2,
+  MMWS_GPU_PROBE_FFMA = 3
+};
+
+typedef struct mmws_gpu_ctx mmws_gpu_ctx;
+typedef struct mmws_gpu_graph mmws_gpu_graph;
+
+/* ---------------------------------------------------------------- library */
+int mmws_gpu_abi_version(void);
+/* Message of the last failing call on this thread ("" if none). */
+const char* mmws_gpu_last_error(void);
+
+/* ---------------------------------------------------------------- context */
+int mmws_gpu_init(int device, mmws_gpu_ctx** out);
+int mmws_gpu_destroy(mmws_gpu_ctx* ctx);
+int mmws_gpu_device_info(mmws_gpu_ctx* ctx, int* num_sms, int* cc_major, int* cc_minor,
+                         int* max_clock_khz);
+/* Number of kernels this context has launched so far (launch accounting). */
+uint64_t mmws_gpu_launch_count(const mmws_gpu_ctx* ctx);
+/* The context's own stream (cudaStream_t), used when a call passes NULL. */
+void* mmws_gpu_stream(mmws_gpu_ctx* ctx);
+
+/* ---------------------------------------------------------------- host-only helpers */
+/* split_rows (protocol.hpp:33-46): offset/rows arrays of n_workers entries. */
+int mmws_gpu_split_rows(int64_t n_rows, int n_workers, int64_t* offset, int64_t* rows);
+/* static_partition (workshare.hpp:33-46): start/len arrays of `workers` entries. */
+int mmws_gpu_static_partition(uint64_t iterations, uint32_t workers, uint64_t* start,
+                              uint64_t* len);
+/* op_count (matrix.hpp:130-134): N^2 (2N - 1). */
+int mmws_gpu_op_count(int64_t n, uint64_t* out);
+
+/* ---------------------------------------------------------------- multiply, device pointers */
+/* C[m,n] = A[m,k] . B[k,n] on device memory; replaces the inner loops of
+ * matmul_seq (matrix.hpp:118-124), matmul_threads' body (workshare.hpp:105-111)
+ * and worker_run's body (protocol.hpp:132-141).  Asynchronous on `stream`
+ * (NULL = the context stream).  Zero dimensions are MMWS_GPU_ERR_DIMENSION as
+ * in Matrix's constructor (matrix.hpp:72-78). */
+int mmws_gpu_dgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
+                   int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int mode,
+                   void* stream);
+int mmws_gpu_sgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const float* A,
+                   int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int mode,
+                   void* stream);
+
+/* ---------------------------------------------------------------- multiply, host buffers */
+/* The matmul_seq / matmul_threads replacement for host data: dense row-major
+ * A (m x k), B (k x n) in, C (m x n) out.  Copies in, multiplies, copies out
+ * and synchronises.  *elapsed_s (optional) is the device-measured time of the
+ * whole call (H2D + multiply + D2H).  Pinned host buffers give full PCIe
+ * bandwidth; pageable ones work too. */
+int mmws_gpu_matmul_host(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
+                         const double* B, double* C, int mode, double* elapsed_s);
+int mmws_gpu_matmul_host_f32(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k,
+                             const float* A, const float* B, float* C, int mode,
+                             double* elapsed_s);
+
+/* ---------------------------------------------------------------- generators */
+/* Fill dst[rows, cols] (leading dimension ld, fp64 or fp32) with elements
+ * first .. first + rows*cols - 1 of the seeded stream.  dist NORMAL requires
+ * is_f32 == 1. */
+int mmws_gpu_fill(mmws_gpu_ctx* ctx, int dist, uint64_t seed, void* dst, int64_t rows,
+                  int64_t cols, int64_t ld, int is_f32, uint64_t first, void* stream);
+
+/* ---------------------------------------------------------------- CUDA graphs (small-N path) */
+/* Capture one fp64 multiply on fixed device buffers into a CUDA graph; replay
+ * with mmws_gpu_graph_launch to pay one graph launch instead of the per-call
+ * host work (tensor-map encoding, packing decisions, kernel launches). */
+int mmws_gpu_graph_dgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
+                         int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                         int mode, mmws_gpu_graph** out);
+int mmws_gpu_graph_launch(mmws_gpu_graph* graph, void* stream);
+int mmws_gpu_graph_destroy(mmws_gpu_graph* graph);
+
+/* ---------------------------------------------------------------- measurement */
+/* Runs one pipe-saturating probe kernel and returns its TFLOP/s. */
+int mmws_gpu_peak_probe(mmws_gpu_ctx* ctx, int which, int iters, double* tflops);
+
+/* ---------------------------------------------------------------- row-block distribution */
+/* The master/worker row decomposition of master_run / worker_run
+ * (protocol.hpp:50-147) over NCCL, one rank per GPU.  Bootstrap: rank 0 calls
+ * mmws_gpu_nccl_unique_id and ships the 128 bytes to every rank by any means
+ * (torch.distributed, the reference's launch.hpp control plane, MPI, ...);
+ * every rank then calls mmws_gpu_comm_init. */
+int mmws_gpu_nccl_unique_id(uint8_t out[128]);
+int mmws_gpu_comm_init(mmws_gpu_ctx* ctx, int nranks, int rank, const uint8_t id[128]);
+int mmws_gpu_comm_destroy(mmws_gpu_ctx* ctx);
+
+/* Collective over the context's communicator; every rank calls it with the
+ * same m, n, k, mode.  Rank 0 (master) passes device pointers to dense A
+ * (m x k), B (k x n) and C (m x n); the other ranks pass NULL.  Rows are split
+ * with split_rows(m, nranks); rank r multiplies rows [offset_r, offset_r +
+ * rows_r).  Unlike the reference's master (protocol.hpp:3-4) rank 0 also
+ * computes its own block -- on a GPU box the master's device is a full worker.
+ * Messages: A-slice 0->r (r >= 1), B broadcast from 0, C-slice r->0; ranks
+ * with rows_r == 0 still take part (protocol.hpp:122-123).  *elapsed_s
+ * (rank 0, optional) is first send -> last receive measured on the device
+ * (the bracket of protocol.hpp:63,105).  Synchronous on return. */
+int mmws_gpu_rowblock_dgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k,
+                            const double* A, const double* B, double* C, int mode,
+                            double* elapsed_s);
+int mmws_gpu_rowblock_sgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const float* A,
+                            const float* B, float* C, int mode, double* elapsed_s);
+
+/* The message plan rank 0 executes for (m, k, n, nranks), in issue order --
+ * the analogue of the reference's Communicator traffic log (comm.hpp:24-32)
+ * used by its protocol-shape test (test_protocol.cpp:99-137).  Host-only.
+ * Entry e: peer[e], tag[e] (1 = assign, 2 = result), kind[e] (0 = int64
+ * scalar metadata, 1 = fp64/fp32 array), count[e] (elements), dir[e] (0 sent,
+ * 1 received, 2 broadcast).  *n_entries in: capacity, out: entries needed. */
+int mmws_gpu_rowblock_plan(int64_t m, int64_t n, int64_t k, int nranks, int32_t* peer,
+                           int32_t* tag, int32_t* kind, int64_t* count, int32_t* dir,
+                           int32_t* n_entries);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MMWS_GPU_H_ */

@@ -1,0 +1,299 @@
+"""Python host mirror of the reference's hot-path API over the C ABI.
+
+The reference is C++ (namespace mmws); its drop-in for C++ callers is
+include/mmws_gpu.hpp.  This module is the same surface for Python callers,
+tests and bench.py: reference names (split_rows, static_partition, op_count,
+matmul / master_run analogues), reference error classes, and device tensors
+handed to the CUDA kernels through ctypes.  Every compute call goes to
+libmmws_gpu.so; nothing here computes on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+from . import _abi
+from ._abi import (DIST_INT8, DIST_NORMAL, DIST_UNIFORM, DIST_UNIT, MODE_AUTO, MODE_DMMA,  # noqa: F401
+                   MODE_DMMA_SMALL, MODE_EXACT, MODE_FFMA, PROBE_DFMA, PROBE_DMMA,
+                   PROBE_DMUL_DADD, PROBE_FFMA)
+
+
+# --------------------------------------------------------------------------- errors
+# Names and bases follow the reference's error.hpp:9-53.
+class DimensionError(ValueError):
+    """Invalid matrix shapes (error.hpp:9-12)."""
+
+
+class DomainError(ValueError):
+    """Arguments outside an operation's domain (error.hpp:14-17)."""
+
+
+class RankError(IndexError):
+    """Unaddressable rank (error.hpp:19-22)."""
+
+
+class ProtocolError(RuntimeError):
+    """Row-block exchange failed (error.hpp:29-32)."""
+
+
+class GpuError(RuntimeError):
+    """CUDA / NCCL / allocation failure (no reference counterpart)."""
+
+
+_ERRORS = {
+    _abi.ERR_DIMENSION: DimensionError,
+    _abi.ERR_DOMAIN: DomainError,
+    _abi.ERR_RANK: RankError,
+    _abi.ERR_PROTOCOL: ProtocolError,
+}
+
+
+def _check(rc: int) -> None:
+    if rc != _abi.OK:
+        raise _ERRORS.get(rc, GpuError)(f"[mmws_gpu rc={rc}] {_abi.last_error()}")
+
+
+def _lib():
+    return _abi.load()
+
+
+# --------------------------------------------------------------------------- host-only helpers
+def split_rows(n_rows: int, n_workers: int) -> List[Tuple[int, int]]:
+    """split_rows (protocol.hpp:33-46) -> [(offset, rows)] per worker."""
+    n = max(int(n_workers), 1)
+    off = (C.c_int64 * n)()
+    rows = (C.c_int64 * n)()
+    _check(_lib().mmws_gpu_split_rows(n_rows, n_workers, off, rows))
+    return [(off[i], rows[i]) for i in range(n)]
+
+
+def static_partition(iterations: int, workers: int) -> List[Tuple[int, int]]:
+    """static_partition (workshare.hpp:33-46) -> [(start, len)] per worker."""
+    n = max(int(workers), 1)
+    st = (C.c_uint64 * n)()
+    ln = (C.c_uint64 * n)()
+    _check(_lib().mmws_gpu_static_partition(iterations, workers, st, ln))
+    return [(st[i], ln[i]) for i in range(n)]
+
+
+def op_count(n: int) -> int:
+    """op_count (matrix.hpp:130-134): N^2 (2N - 1)."""
+    out = C.c_uint64()
+    _check(_lib().mmws_gpu_op_count(n, C.byref(out)))
+    return out.value
+
+
+def rowblock_plan(m: int, n: int, k: int, nranks: int):
+    """Rank 0's message plan for the row-block exchange, in issue order:
+    list of dicts(peer, tag, kind, count, dir) with dir in {sent, received, broadcast}."""
+    cnt = C.c_int32(0)
+    _check(_lib().mmws_gpu_rowblock_plan(m, n, k, nranks, None, None, None, None, None,
+                                         C.byref(cnt)))
+    e = cnt.value
+    peer, tag, kind, dirs = ((C.c_int32 * max(e, 1))() for _ in range(4))
+    count = (C.c_int64 * max(e, 1))()
+    _check(_lib().mmws_gpu_rowblock_plan(m, n, k, nranks, peer, tag, kind, count, dirs,
+                                         C.byref(cnt)))
+    names = {0: "sent", 1: "received", 2: "broadcast"}
+    return [dict(peer=peer[i], tag=tag[i], kind=kind[i], count=count[i], dir=names[dirs[i]])
+            for i in range(e)]
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(_lib().mmws_gpu_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+# --------------------------------------------------------------------------- context
+def _ptr(t) -> int:
+    return t.data_ptr()
+
+
+_CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: the default stream torch reports as 0
+
+
+def _stream(stream) -> int:
+    """Launch stream for a call: torch's current stream by default, so the
+    kernels order with surrounding torch work and torch events time them."""
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream().cuda_stream
+    stream = int(stream)
+    return stream if stream else _CUDA_STREAM_LEGACY
+
+
+def _ld(t) -> int:
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise DimensionError("expected a 2-D row-major tensor with unit column stride")
+    return t.stride(0)
+
+
+class Graph:
+    """A captured fp64 multiply (small-N path: one graph launch per call)."""
+
+    def __init__(self, ctx: "Context", handle: int, keep):
+        self._ctx, self._h, self._keep = ctx, handle, keep
+
+    def launch(self, stream=None) -> None:
+        _check(_lib().mmws_gpu_graph_launch(self._h, _stream(stream)))
+
+    def close(self) -> None:
+        if self._h:
+            _lib().mmws_gpu_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Context:
+    """One CUDA device (sm_100a) + its stream, workspaces and NCCL communicator."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        _check(_lib().mmws_gpu_init(device, C.byref(h)))
+        self._h = h.value
+        self.device = device
+        sms, ma, mi, clk = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        _check(_lib().mmws_gpu_device_info(self._h, C.byref(sms), C.byref(ma), C.byref(mi),
+                                           C.byref(clk)))
+        self.num_sms, self.cc, self.max_clock_khz = sms.value, (ma.value, mi.value), clk.value
+
+    # -- lifecycle
+    def close(self) -> None:
+        if self._h:
+            _lib().mmws_gpu_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self) -> int:
+        return self._h
+
+    @property
+    def launches(self) -> int:
+        return int(_lib().mmws_gpu_launch_count(self._h))
+
+    @property
+    def stream(self) -> int:
+        return int(_lib().mmws_gpu_stream(self._h) or 0)
+
+    # -- device-pointer multiply (torch CUDA tensors)
+    def dgemm(self, A, B, C_=None, mode: int = MODE_AUTO, stream=None):
+        import torch
+        if A.dtype != torch.float64 or B.dtype != torch.float64:
+            raise DomainError("dgemm expects float64 tensors")
+        m, k = A.shape
+        k2, n = B.shape
+        if k != k2:
+            raise DimensionError(f"matmul: inner dimensions differ, {k} vs {k2}")
+        if C_ is None:
+            C_ = torch.empty((m, n), dtype=torch.float64, device=A.device)
+        _check(_lib().mmws_gpu_dgemm(self._h, m, n, k, _ptr(A), _ld(A), _ptr(B), _ld(B),
+                                     _ptr(C_), _ld(C_), mode, _stream(stream)))
+        return C_
+
+    def sgemm(self, A, B, C_=None, mode: int = MODE_AUTO, stream=None):
+        import torch
+        if A.dtype != torch.float32 or B.dtype != torch.float32:
+            raise DomainError("sgemm expects float32 tensors")
+        m, k = A.shape
+        k2, n = B.shape
+        if k != k2:
+            raise DimensionError(f"matmul: inner dimensions differ, {k} vs {k2}")
+        if C_ is None:
+            C_ = torch.empty((m, n), dtype=torch.float32, device=A.device)
+        _check(_lib().mmws_gpu_sgemm(self._h, m, n, k, _ptr(A), _ld(A), _ptr(B), _ld(B),
+                                     _ptr(C_), _ld(C_), mode, _stream(stream)))
+        return C_
+
+    # -- host-buffer multiply (the matmul_seq / matmul_threads replacement)
+    def matmul_host(self, a: np.ndarray, b: np.ndarray, mode: int = MODE_AUTO,
+                    out: Optional[np.ndarray] = None) -> Tuple[np.ndarray, float]:
+        if a.ndim != 2 or b.ndim != 2:
+            raise DimensionError("matmul expects 2-D matrices")
+        if a.shape[1] != b.shape[0]:
+            raise DimensionError(f"matmul: inner dimensions differ, {a.shape[1]} vs {b.shape[0]}")
+        f32 = a.dtype == np.float32
+        dt = np.float32 if f32 else np.float64
+        a = np.ascontiguousarray(a, dtype=dt)
+        b = np.ascontiguousarray(b, dtype=dt)
+        m, k = a.shape
+        n = b.shape[1]
+        c = out if out is not None else np.empty((m, n), dtype=dt)
+        el = C.c_double()
+        fn = _lib().mmws_gpu_matmul_host_f32 if f32 else _lib().mmws_gpu_matmul_host
+        _check(fn(self._h, m, n, k, a.ctypes.data, b.ctypes.data, c.ctypes.data, mode,
+                  C.byref(el)))
+        return c, el.value
+
+    # -- generators
+    def fill(self, dist: int, seed: int, rows: int, cols: int, dtype=None, first: int = 0,
+             out=None, stream=None):
+        import torch
+        dtype = dtype or torch.float64
+        t = out if out is not None else torch.empty((rows, cols), dtype=dtype,
+                                                    device=f"cuda:{self.device}")
+        _check(_lib().mmws_gpu_fill(self._h, dist, seed, _ptr(t), rows, cols, _ld(t),
+                                    int(t.dtype == torch.float32), first, _stream(stream)))
+        return t
+
+    # -- graphs
+    def graph_dgemm(self, A, B, C_, mode: int = MODE_AUTO) -> Graph:
+        m, k = A.shape
+        n = B.shape[1]
+        g = C.c_void_p()
+        _check(_lib().mmws_gpu_graph_dgemm(self._h, m, n, k, _ptr(A), _ld(A), _ptr(B), _ld(B),
+                                           _ptr(C_), _ld(C_), mode, C.byref(g)))
+        return Graph(self, g.value, (A, B, C_))
+
+    # -- measurement
+    def peak_probe(self, which: int, iters: int = 4096) -> float:
+        out = C.c_double()
+        _check(_lib().mmws_gpu_peak_probe(self._h, which, iters, C.byref(out)))
+        return out.value
+
+    # -- row-block distribution
+    def comm_init(self, nranks: int, rank: int, uid: bytes) -> None:
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        _check(_lib().mmws_gpu_comm_init(self._h, nranks, rank, buf))
+
+    def comm_destroy(self) -> None:
+        _check(_lib().mmws_gpu_comm_destroy(self._h))
+
+    def rowblock(self, m: int, n: int, k: int, A=None, B=None, C_=None, mode: int = MODE_AUTO,
+                 f32: bool = False) -> float:
+        """Collective master/worker multiply; rank 0 passes A, B, C device tensors."""
+        el = C.c_double(0.0)
+        fn = _lib().mmws_gpu_rowblock_sgemm if f32 else _lib().mmws_gpu_rowblock_dgemm
+        _check(fn(self._h, m, n, k, _ptr(A) if A is not None else None,
+                  _ptr(B) if B is not None else None, _ptr(C_) if C_ is not None else None,
+                  mode, C.byref(el)))
+        return el.value
+
+
+def bootstrap_comm(ctx: Context) -> None:
+    """NCCL communicator for the current torch.distributed world: rank 0 makes
+    the unique id, torch.distributed ships it (plumbing only)."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(), dist.get_world_size()
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    ctx.comm_init(world, rank, obj[0])

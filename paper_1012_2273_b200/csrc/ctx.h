@@ -1,0 +1,66 @@
+// ctx.h -- the context object behind mmws_gpu_ctx (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <mutex>
+#include <string>
+
+#include "kernels.h"
+
+struct mmws_gpu_ctx {
+  int device = 0;
+  int num_sms = 0;
+  int cc_major = 0, cc_minor = 0, clock_khz = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  mmws_impl::EncodeTiledFn encode = nullptr;
+  uint64_t launches = 0;
+  std::mutex mu;
+
+  // packing workspace (device), grown on demand
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  // host-entry staging buffers (device)
+  void* dA = nullptr;
+  void* dB = nullptr;
+  void* dC = nullptr;
+  size_t dA_bytes = 0, dB_bytes = 0, dC_bytes = 0;
+  // probe sink
+  double* sink = nullptr;
+
+  // row-block distribution
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  cudaStream_t comm_stream = nullptr;
+  void* rbA = nullptr;  // worker-side A slice / B copy / C slice
+  void* rbB = nullptr;
+  void* rbC = nullptr;
+  size_t rbA_bytes = 0, rbB_bytes = 0, rbC_bytes = 0;
+
+  mmws_impl::Launch launch(cudaStream_t s) {
+    mmws_impl::Launch L;
+    L.stream = s ? s : stream;
+    L.num_sms = num_sms;
+    L.encode = encode;
+    L.launches = &launches;
+    return L;
+  }
+};
+
+namespace mmws_impl {
+// error plumbing shared by the C-ABI translation units
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+int ok();
+// grow a device buffer to at least `bytes`
+cudaError_t ensure(void** buf, size_t* have, size_t bytes);
+// the fp64 multiply dispatch used by dgemm / host / graph / row-block paths
+int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
+                   int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int mode,
+                   cudaStream_t stream);
+int sgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const float* A,
+                   int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int mode,
+                   cudaStream_t stream);
+}  // namespace mmws_impl

@@ -1,0 +1,264 @@
+// dgemm_dmma.cu -- FP64 GEMM on the sm_100a FP64 tensor path (DMMA.8x8x4).
+//
+// Replaces the inner triple loop of matmul_seq / matmul_threads / worker_run
+// (reference include/mmws/matrix.hpp:118-124, workshare.hpp:105-111,
+// protocol.hpp:132-141) for real-valued fp64 inputs.  Blackwell has no
+// tcgen05 .kind::f64, so the FP64 tensor instruction is warp-level
+// mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4.
+//
+// Structure (one CTA per BMxBN output tile, 1 CTA/SM for the big config):
+//   * warp CONSUMERS (the last warp) is the TMA producer: one elected lane
+//     streams A[BM x 16] and B[16 x BN] k-slices into a STAGES-deep ring of
+//     128B-swizzled shared-memory stages, completion via mbarrier tx-counts;
+//   * CONSUMERS math warps each own a WM x WN sub-tile held as DMMA
+//     accumulator fragments in registers (acc = +0.0 at start; the epilogue
+//     stores the accumulator directly -- no beta*C read);
+//   * fragments are fetched with conflict-free 128-bit LDS thanks to two
+//     index permutations that the 8x8x4 MMA does not care about:
+//       - k: within each 8-wide k-group the lane with k-slot t holds the pair
+//         (2t, 2t+1) and feeds element q to MMA #q (q = 0, 1);
+//       - m: row slot g of an 8-row subtile is physical row sigma(g) =
+//         (g>>1) + 4(g&1), so the two rows a quarter-warp touches sit in
+//         opposite halves of the 128-byte swizzle row;
+//       - n: lane slot g of 16-column box b holds columns (2g, 2g+1) and feeds
+//         element e to MMA (b, e); each lane ends up owning 4 consecutive
+//         output columns, stored as two 16-byte vectors.
+//   * integer-valued inputs (|partial sums| < 2^53) come out bit-exact in any
+//     accumulation order, which is what the N=4099 exactness config checks.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mmws_impl {
+namespace {
+
+using namespace mmws_dev;
+
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_>
+struct Cfg {
+  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_;
+  static constexpr int BK = 16;  // 16 doubles = one 128-byte swizzle row
+  static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
+  static constexpr int CONSUMERS = WARPS_M * WARPS_N;
+  // The producer is a whole warpgroup so setmaxnreg can move its registers to
+  // the math warpgroups (register budgets are per 4-warp group).
+  static constexpr int THREADS = (CONSUMERS + 4) * 32;
+  static constexpr int MATH_REGS = CONSUMERS == 8 ? 232 : 0;  // 0: no setmaxnreg
+  static constexpr int MI = WM / 8;   // 8-row subtiles per warp
+  static constexpr int NB = WN / 16;  // 16-column boxes per warp
+  static constexpr int A_BYTES = BM * BK * 8;
+  static constexpr int B_BYTES = BN * BK * 8;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 1024;
+  static_assert(BM % WM == 0 && BN % WN == 0 && WM % 8 == 0 && WN % 16 == 0, "tile");
+  static_assert(BM <= 256, "TMA box");
+};
+
+using Big = Cfg<128, 128, 64, 32, 6, 1>;   // 8 math warps, 192 KB ring, 1 CTA/SM
+using Small = Cfg<64, 64, 32, 32, 4, 2>;   // 4 math warps, 64 KB ring, 2+ CTAs/SM
+using Mid = Cfg<128, 64, 32, 32, 5, 1>;    // 8 math warps, 160 KB ring
+
+template <class K>
+__global__ void __launch_bounds__(K::THREADS, K::MINB)
+    dgemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA,
+                      const __grid_constant__ CUtensorMap tmB, double* __restrict__ C,
+                      int64_t ldc, int M, int N, int K_, int tiles_m, int tiles_n, int vec_ok) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  // 1024-byte aligned ring (128B-swizzle atoms); offsetting the __shared__
+  // array itself keeps the shared address space visible, so fragment fetches
+  // compile to LDS rather than generic loads.
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + K::STAGES * K::STAGE_BYTES);
+  uint64_t* empty = full + K::STAGES;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  // Grouped rasterisation: GROUP tile-rows advance together so the A panels
+  // and B panels of one wave are shared through L2.
+  constexpr int GROUP = 8;
+  const int tile = blockIdx.x;
+  const int per_group = GROUP * tiles_n;
+  const int first_m = (tile / per_group) * GROUP;
+  const int gm = min(tiles_m - first_m, GROUP);
+  const int tm = first_m + (tile % per_group) % gm;
+  const int tn = (tile % per_group) / gm;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < K::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], K::CONSUMERS);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  const int KT = (K_ + K::BK - 1) / K::BK;
+
+  if (warp >= K::CONSUMERS) {
+    // ---------------- TMA producer ----------------
+    if constexpr (K::MATH_REGS > 0)
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    if (warp == K::CONSUMERS && lane == 0) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+      for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % K::STAGES;
+        if (kt >= K::STAGES) mbar_wait(&empty[s], ((kt / K::STAGES) - 1) & 1);
+        uint8_t* sa = smem + s * K::STAGE_BYTES;
+        uint8_t* sb = sa + K::A_BYTES;
+        mbar_arrive_expect_tx(&full[s], K::STAGE_BYTES);
+        tma_load_2d(sa, &tmA, &full[s], kt * K::BK, tm * K::BM);
+#pragma unroll
+        for (int b = 0; b < K::BN / 16; ++b)
+          tma_load_2d(sb + b * 2048, &tmB, &full[s], tn * K::BN + b * 16, kt * K::BK);
+      }
+    }
+    return;
+  }
+
+  // ---------------- math warps ----------------
+  if constexpr (K::MATH_REGS > 0)
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(K::MATH_REGS));
+  const int wm = warp % K::WARPS_M;
+  const int wn = warp / K::WARPS_M;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int sig = (gid >> 1) + ((gid & 1) << 2);
+
+  // Per-lane byte offsets inside a stage.
+  uint32_t a_off[K::MI];
+#pragma unroll
+  for (int i = 0; i < K::MI; ++i) a_off[i] = (wm * K::WM + i * 8 + sig) * 128;
+  uint32_t a_chunk[2];
+#pragma unroll
+  for (int g8 = 0; g8 < 2; ++g8) a_chunk[g8] = ((g8 * 4 + tig) ^ sig) << 4;
+  uint32_t b_off[2][2];  // [g8][q]: row (k) byte offset + swizzled chunk
+#pragma unroll
+  for (int g8 = 0; g8 < 2; ++g8)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int k = g8 * 8 + 2 * tig + q;
+      b_off[g8][q] = k * 128 + ((gid ^ (k & 7)) << 4);
+    }
+
+  double acc[K::MI][K::NB][2][2];
+#pragma unroll
+  for (int i = 0; i < K::MI; ++i)
+#pragma unroll
+    for (int b = 0; b < K::NB; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) acc[i][b][e][0] = acc[i][b][e][1] = 0.0;
+
+  for (int kt = 0; kt < KT; ++kt) {
+    const int s = kt % K::STAGES;
+    mbar_wait(&full[s], (kt / K::STAGES) & 1);
+    // Release the PREVIOUS stage here, not at the end of its own iteration:
+    // ptxas sinks DMMAs below an arrive placed right after them, so the arrive
+    // could retire while LDS of that stage are still in flight and the next
+    // TMA would overwrite data being read.  Every DMMA of stage kt-1 sits in
+    // the basic block before this wait loop and has issued -- so all of its
+    // LDS have returned -- by the time we get here.
+    if (kt > 0) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[(kt - 1) % K::STAGES]);
+    }
+    const uint8_t* sa = smem + s * K::STAGE_BYTES;
+    const uint8_t* sb = sa + K::A_BYTES + (wn * K::NB) * 2048;
+#pragma unroll
+    for (int g8 = 0; g8 < 2; ++g8) {
+      double2 af[K::MI];
+      double2 bf[K::NB][2];
+#pragma unroll
+      for (int i = 0; i < K::MI; ++i)
+        af[i] = *reinterpret_cast<const double2*>(sa + a_off[i] + a_chunk[g8]);
+#pragma unroll
+      for (int b = 0; b < K::NB; ++b)
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          bf[b][q] = *reinterpret_cast<const double2*>(sb + b * 2048 + b_off[g8][q]);
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int i = 0; i < K::MI; ++i)
+#pragma unroll
+          for (int b = 0; b < K::NB; ++b) {
+            const double a = q ? af[i].y : af[i].x;
+            dmma_8x8x4(acc[i][b][0][0], acc[i][b][0][1], a, q ? bf[b][1].x : bf[b][0].x);
+            dmma_8x8x4(acc[i][b][1][0], acc[i][b][1][1], a, q ? bf[b][1].y : bf[b][0].y);
+          }
+    }
+
+  }
+
+  // ---------------- epilogue: registers -> global ----------------
+  // Lane owns row (.., sigma(gid)) and columns 4*tig .. 4*tig+3 of each box.
+#pragma unroll
+  for (int i = 0; i < K::MI; ++i) {
+    const int row = tm * K::BM + wm * K::WM + i * 8 + sig;
+    if (row >= M) continue;
+    double* crow = C + static_cast<int64_t>(row) * ldc;
+#pragma unroll
+    for (int b = 0; b < K::NB; ++b) {
+      const int col = tn * K::BN + (wn * K::NB + b) * 16 + 4 * tig;
+      const double v0 = acc[i][b][0][0], v1 = acc[i][b][1][0];
+      const double v2 = acc[i][b][0][1], v3 = acc[i][b][1][1];
+      if (vec_ok && col + 3 < N) {
+        reinterpret_cast<double2*>(crow + col)[0] = make_double2(v0, v1);
+        reinterpret_cast<double2*>(crow + col)[1] = make_double2(v2, v3);
+      } else {
+        if (col + 0 < N) crow[col + 0] = v0;
+        if (col + 1 < N) crow[col + 1] = v1;
+        if (col + 2 < N) crow[col + 2] = v2;
+        if (col + 3 < N) crow[col + 3] = v3;
+      }
+    }
+  }
+}
+
+bool make_map(const Launch& L, CUtensorMap* map, const double* base, int64_t inner, int64_t outer,
+              int64_t ld, int box_inner, int box_outer) {
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * sizeof(double)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner),
+                             static_cast<cuuint32_t>(box_outer)};
+  const cuuint32_t estr[2] = {1, 1};
+  return L.encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <class K>
+cudaError_t run(const Launch& L, int64_t M, int64_t N, int64_t Kd, const double* A, int64_t lda,
+                const double* B, int64_t ldb, double* C, int64_t ldc) {
+  CUtensorMap ta, tb;
+  if (!make_map(L, &ta, A, Kd, M, lda, 16, K::BM)) return cudaErrorInvalidValue;
+  if (!make_map(L, &tb, B, N, Kd, ldb, 16, 16)) return cudaErrorInvalidValue;
+  const int smem = K::SMEM;
+  cudaError_t e = cudaFuncSetAttribute(dgemm_dmma_kernel<K>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int tiles_m = static_cast<int>((M + K::BM - 1) / K::BM);
+  const int tiles_n = static_cast<int>((N + K::BN - 1) / K::BN);
+  const int vec_ok = (ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0);
+  dgemm_dmma_kernel<K><<<tiles_m * tiles_n, K::THREADS, smem, L.stream>>>(
+      ta, tb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(Kd), tiles_m,
+      tiles_n, vec_ok);
+  L.count();
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_dgemm_dmma(const Launch& L, int cfg, int64_t M, int64_t N, int64_t K,
+                              const double* A, int64_t lda, const double* B, int64_t ldb,
+                              double* C, int64_t ldc) {
+  switch (cfg) {
+    case DMMA_64x64: return run<Small>(L, M, N, K, A, lda, B, ldb, C, ldc);
+    case DMMA_128x64: return run<Mid>(L, M, N, K, A, lda, B, ldb, C, ldc);
+    default: return run<Big>(L, M, N, K, A, lda, B, ldb, C, ldc);
+  }
+}
+
+}  // namespace mmws_impl

@@ -1,0 +1,60 @@
+// kernels.h -- internal (C++) launch interface between the C-ABI layer
+// (mmws_gpu.cu) and the kernel translation units.  Not installed, not part of
+// the drop-in surface; include/mmws_gpu.h is.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mmws_impl {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+struct Launch {
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  EncodeTiledFn encode = nullptr;
+  uint64_t* launches = nullptr;  // bumped once per kernel launched
+  void count(int n = 1) const {
+    if (launches) *launches += static_cast<uint64_t>(n);
+  }
+};
+
+// DMMA tile configurations (see dgemm_dmma.cu / DESIGN.md s3).
+enum DmmaCfg { DMMA_128x128 = 0, DMMA_64x64 = 1, DMMA_128x64 = 2 };
+
+// C[M,N] = A[M,K] . B[K,N], row-major, accumulators from +0.0.  The TMA path
+// needs lda, ldb even and A, B 16-byte aligned (the caller packs otherwise).
+cudaError_t launch_dgemm_dmma(const Launch& L, int cfg, int64_t M, int64_t N, int64_t K,
+                              const double* A, int64_t lda, const double* B, int64_t ldb,
+                              double* C, int64_t ldc);
+
+// Exact-order SIMT: per element acc = +0.0; for j ascending acc = (acc + a*b)
+// with separate roundings -- bitwise equal to matmul_seq for every input.
+cudaError_t launch_dgemm_exact(const Launch& L, int64_t M, int64_t N, int64_t K,
+                               const double* A, int64_t lda, const double* B, int64_t ldb,
+                               double* C, int64_t ldc);
+
+// Register-blocked FFMA fp32 GEMM with two-level (chunked) accumulation.
+cudaError_t launch_sgemm_ffma(const Launch& L, int64_t M, int64_t N, int64_t K, const float* A,
+                              int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc);
+
+// Pad/pack src[rows, cols] (ld_src) into dst[rows_p, cols_p] (ld_dst), zero fill.
+cudaError_t launch_pack_f64(const Launch& L, const double* src, int64_t rows, int64_t cols,
+                            int64_t ld_src, double* dst, int64_t rows_p, int64_t cols_p,
+                            int64_t ld_dst);
+
+// Counter-based splitmix64 generators (bit-identical to oracle_fill for dist 0..2).
+cudaError_t launch_fill(const Launch& L, int dist, uint64_t seed, void* dst, int64_t rows,
+                        int64_t cols, int64_t ld, int is_f32, uint64_t first);
+
+// Peak probes: FP64 DMMA / DFMA / DMUL+DADD, FP32 FFMA loops (flops written to
+// *flops, elapsed measured by the caller with events on L.stream).
+cudaError_t launch_peak_probe(const Launch& L, int which, int iters, double* sink,
+                              double* flops);
+
+}  // namespace mmws_impl

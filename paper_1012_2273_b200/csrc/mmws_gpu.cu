@@ -1,0 +1,429 @@
+// mmws_gpu.cu -- the C ABI (include/mmws_gpu.h): contexts, multiply dispatch,
+// host-buffer entry points, CUDA-graph capture, generators, peak probes.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "../../include/mmws_gpu.h"
+#include "ctx.h"
+#include "kernels.h"
+#include "nccl_dl.h"
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+namespace mmws_impl {
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(MMWS_GPU_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+int ok() {
+  g_last_error.clear();
+  return MMWS_GPU_OK;
+}
+
+cudaError_t ensure(void** buf, size_t* have, size_t bytes) {
+  if (*have >= bytes && *buf) return cudaSuccess;
+  if (*buf) {
+    cudaError_t e = cudaFree(*buf);
+    if (e != cudaSuccess) return e;
+    *buf = nullptr;
+    *have = 0;
+  }
+  cudaError_t e = cudaMalloc(buf, bytes);
+  if (e == cudaSuccess) *have = bytes;
+  return e;
+}
+
+namespace {
+inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+int check_dims(int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb, int64_t ldc,
+               const void* A, const void* B, const void* C) {
+  if (m <= 0 || n <= 0 || k <= 0)
+    return fail(MMWS_GPU_ERR_DIMENSION, "matmul: dimensions must be positive, got m=" +
+                                            std::to_string(m) + " n=" + std::to_string(n) +
+                                            " k=" + std::to_string(k));
+  if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX)
+    return fail(MMWS_GPU_ERR_DIMENSION, "matmul: dimension exceeds 2^31-1");
+  if (lda < k || ldb < n || ldc < n)
+    return fail(MMWS_GPU_ERR_DIMENSION, "matmul: leading dimension smaller than row length");
+  if (!A || !B || !C) return fail(MMWS_GPU_ERR_DOMAIN, "matmul: null matrix pointer");
+  return MMWS_GPU_OK;
+}
+}  // namespace
+
+int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
+                   int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int mode,
+                   cudaStream_t stream) {
+  if (int rc = check_dims(m, n, k, lda, ldb, ldc, A, B, C)) return rc;
+  const Launch L = ctx->launch(stream);
+  cudaError_t e;
+  if (mode == MMWS_GPU_MODE_EXACT) {
+    e = launch_dgemm_exact(L, m, n, k, A, lda, B, ldb, C, ldc);
+    return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm exact");
+  }
+  if (mode != MMWS_GPU_MODE_AUTO && mode != MMWS_GPU_MODE_DMMA &&
+      mode != MMWS_GPU_MODE_DMMA_SMALL)
+    return fail(MMWS_GPU_ERR_DOMAIN, "dgemm: unknown mode " + std::to_string(mode));
+  int cfg = DMMA_128x128;
+  if (mode == MMWS_GPU_MODE_DMMA_SMALL) {
+    cfg = DMMA_64x64;
+
+  } else if (mode == MMWS_GPU_MODE_AUTO) {
+    const int64_t tiles = ((m + 127) / 128) * ((n + 127) / 128);
+    if (tiles < 2 * static_cast<int64_t>(ctx->num_sms)) cfg = DMMA_64x64;
+  }
+  // TMA needs 16-byte aligned bases and row pitches: pack otherwise.
+  const bool a_ok = lda % 2 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0;
+  const bool b_ok = ldb % 2 == 0 && reinterpret_cast<uintptr_t>(B) % 16 == 0;
+  if (!a_ok || !b_ok) {
+    const int64_t lda_p = round_up(k, 8), ldb_p = round_up(n, 8);
+    const size_t bytes = sizeof(double) * ((a_ok ? 0 : m * lda_p) + (b_ok ? 0 : k * ldb_p));
+    e = ensure(&ctx->ws, &ctx->ws_bytes, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "dgemm pack workspace");
+    double* w = static_cast<double*>(ctx->ws);
+    if (!a_ok) {
+      e = launch_pack_f64(L, A, m, k, lda, w, m, lda_p, lda_p);
+      if (e != cudaSuccess) return cuda_fail(e, "dgemm pack A");
+      A = w;
+      lda = lda_p;
+      w += m * lda_p;
+    }
+    if (!b_ok) {
+      e = launch_pack_f64(L, B, k, n, ldb, w, k, ldb_p, ldb_p);
+      if (e != cudaSuccess) return cuda_fail(e, "dgemm pack B");
+      B = w;
+      ldb = ldb_p;
+    }
+  }
+  e = launch_dgemm_dmma(L, cfg, m, n, k, A, lda, B, ldb, C, ldc);
+  return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm dmma");
+}
+
+int sgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const float* A,
+                   int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int mode,
+                   cudaStream_t stream) {
+  if (int rc = check_dims(m, n, k, lda, ldb, ldc, A, B, C)) return rc;
+  if (mode != MMWS_GPU_MODE_AUTO && mode != MMWS_GPU_MODE_FFMA)
+    return fail(MMWS_GPU_ERR_DOMAIN, "sgemm: unknown mode " + std::to_string(mode));
+  cudaError_t e = launch_sgemm_ffma(ctx->launch(stream), m, n, k, A, lda, B, ldb, C, ldc);
+  return e == cudaSuccess ? ok() : cuda_fail(e, "sgemm ffma");
+}
+
+}  // namespace mmws_impl
+
+using namespace mmws_impl;
+
+struct mmws_gpu_graph {
+  mmws_gpu_ctx* ctx = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  uint64_t kernels = 0;
+};
+
+#define MMWS_CTX_GUARD(ctx)                                                  \
+  if (!(ctx)) return fail(MMWS_GPU_ERR_STATE, "null mmws_gpu_ctx");          \
+  std::lock_guard<std::mutex> guard_((ctx)->mu);                             \
+  if (cudaError_t e_ = cudaSetDevice((ctx)->device); e_ != cudaSuccess)      \
+    return cuda_fail(e_, "cudaSetDevice");
+
+namespace {
+template <class T>
+int matmul_host_impl(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, const T* B,
+                     T* C, int mode, double* elapsed_s) {
+  if (m <= 0 || n <= 0 || k <= 0)
+    return fail(MMWS_GPU_ERR_DIMENSION, "matmul: dimensions must be positive");
+  if (!A || !B || !C) return fail(MMWS_GPU_ERR_DOMAIN, "matmul: null host pointer");
+  const size_t a_b = sizeof(T) * m * k, b_b = sizeof(T) * k * n, c_b = sizeof(T) * m * n;
+  cudaError_t e;
+  if ((e = ensure(&ctx->dA, &ctx->dA_bytes, a_b)) != cudaSuccess ||
+      (e = ensure(&ctx->dB, &ctx->dB_bytes, b_b)) != cudaSuccess ||
+      (e = ensure(&ctx->dC, &ctx->dC_bytes, c_b)) != cudaSuccess)
+    return cuda_fail(e, "matmul_host: device buffers");
+  cudaStream_t s = ctx->stream;
+  cudaEventRecord(ctx->ev0, s);
+  if ((e = cudaMemcpyAsync(ctx->dA, A, a_b, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(ctx->dB, B, b_b, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return cuda_fail(e, "matmul_host: H2D");
+  int rc;
+  if constexpr (sizeof(T) == 8)
+    rc = dgemm_dispatch(ctx, m, n, k, static_cast<const double*>(ctx->dA), k,
+                        static_cast<const double*>(ctx->dB), n, static_cast<double*>(ctx->dC), n,
+                        mode, s);
+  else
+    rc = sgemm_dispatch(ctx, m, n, k, static_cast<const float*>(ctx->dA), k,
+                        static_cast<const float*>(ctx->dB), n, static_cast<float*>(ctx->dC), n,
+                        mode, s);
+  if (rc) return rc;
+  if ((e = cudaMemcpyAsync(C, ctx->dC, c_b, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return cuda_fail(e, "matmul_host: D2H");
+  cudaEventRecord(ctx->ev1, s);
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "matmul_host: sync");
+  if (elapsed_s) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    *elapsed_s = ms * 1e-3;
+  }
+  return ok();
+}
+}  // namespace
+
+extern "C" {
+
+int mmws_gpu_abi_version(void) { return MMWS_GPU_ABI_VERSION; }
+
+const char* mmws_gpu_last_error(void) { return g_last_error.c_str(); }
+
+int mmws_gpu_init(int device, mmws_gpu_ctx** out) {
+  if (!out) return fail(MMWS_GPU_ERR_DOMAIN, "mmws_gpu_init: null out pointer");
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess) return cuda_fail(e, "mmws_gpu_init: no CUDA device");
+  if (device < 0 || device >= count)
+    return fail(MMWS_GPU_ERR_DOMAIN, "mmws_gpu_init: device " + std::to_string(device) +
+                                         " out of range (" + std::to_string(count) + ")");
+  if ((e = cudaSetDevice(device)) != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  cudaDeviceProp prop;
+  if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess)
+    return cuda_fail(e, "cudaGetDeviceProperties");
+  if (prop.major != 10)
+    return fail(MMWS_GPU_ERR_STATE, std::string("mmws_gpu_init: built for sm_100a, device is ") +
+                                        prop.name + " (sm_" + std::to_string(prop.major) +
+                                        std::to_string(prop.minor) + ")");
+  auto* ctx = new (std::nothrow) mmws_gpu_ctx();
+  if (!ctx) return fail(MMWS_GPU_ERR_ALLOC, "mmws_gpu_init: out of host memory");
+  ctx->device = device;
+  ctx->num_sms = prop.multiProcessorCount;
+  ctx->cc_major = prop.major;
+  ctx->cc_minor = prop.minor;
+  int clk = 0;
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, device);
+  ctx->clock_khz = clk;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) {
+    delete ctx;
+    return fail(MMWS_GPU_ERR_CUDA, "mmws_gpu_init: cuTensorMapEncodeTiled unavailable");
+  }
+  ctx->encode = reinterpret_cast<EncodeTiledFn>(fn);
+  if ((e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaEventCreate(&ctx->ev0)) != cudaSuccess ||
+      (e = cudaEventCreate(&ctx->ev1)) != cudaSuccess ||
+      (e = cudaMalloc(&ctx->sink, 4096 * sizeof(double))) != cudaSuccess) {
+    mmws_gpu_destroy(ctx);
+    return cuda_fail(e, "mmws_gpu_init");
+  }
+  *out = ctx;
+  return ok();
+}
+
+int mmws_gpu_destroy(mmws_gpu_ctx* ctx) {
+  if (!ctx) return ok();
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->comm && nccl().ok) nccl().CommDestroy(ctx->comm);
+  for (void* p : {ctx->ws, ctx->dA, ctx->dB, ctx->dC, ctx->rbA, ctx->rbB, ctx->rbC,
+                  static_cast<void*>(ctx->sink)})
+    if (p) cudaFree(p);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+  delete ctx;
+  return ok();
+}
+
+int mmws_gpu_device_info(mmws_gpu_ctx* ctx, int* num_sms, int* cc_major, int* cc_minor,
+                         int* max_clock_khz) {
+  if (!ctx) return fail(MMWS_GPU_ERR_STATE, "null mmws_gpu_ctx");
+  if (num_sms) *num_sms = ctx->num_sms;
+  if (cc_major) *cc_major = ctx->cc_major;
+  if (cc_minor) *cc_minor = ctx->cc_minor;
+  if (max_clock_khz) *max_clock_khz = ctx->clock_khz;
+  return ok();
+}
+
+uint64_t mmws_gpu_launch_count(const mmws_gpu_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+void* mmws_gpu_stream(mmws_gpu_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+// ------------------------------------------------------------------ host-only helpers
+int mmws_gpu_split_rows(int64_t n_rows, int n_workers, int64_t* offset, int64_t* rows) {
+  // protocol.hpp:33-46
+  if (n_workers < 1) return fail(MMWS_GPU_ERR_DOMAIN, "split_rows: need at least one worker");
+  if (n_rows < 0) return fail(MMWS_GPU_ERR_DOMAIN, "split_rows: negative row count");
+  if (!offset || !rows) return fail(MMWS_GPU_ERR_DOMAIN, "split_rows: null output");
+  const int64_t averow = n_rows / n_workers, extra = n_rows % n_workers;
+  int64_t off = 0;
+  for (int w = 0; w < n_workers; ++w) {
+    offset[w] = off;
+    rows[w] = averow + (w < extra ? 1 : 0);
+    off += rows[w];
+  }
+  return ok();
+}
+
+int mmws_gpu_static_partition(uint64_t iterations, uint32_t workers, uint64_t* start,
+                              uint64_t* len) {
+  // workshare.hpp:33-46
+  if (workers == 0)
+    return fail(MMWS_GPU_ERR_DOMAIN, "static_partition: worker count must be >= 1");
+  if (!start || !len) return fail(MMWS_GPU_ERR_DOMAIN, "static_partition: null output");
+  const uint64_t base = iterations / workers, extra = iterations % workers;
+  uint64_t s = 0;
+  for (uint32_t w = 0; w < workers; ++w) {
+    start[w] = s;
+    len[w] = base + (w < extra ? 1 : 0);
+    s += len[w];
+  }
+  return ok();
+}
+
+int mmws_gpu_op_count(int64_t n, uint64_t* out) {
+  // matrix.hpp:130-134
+  if (n < 1) return fail(MMWS_GPU_ERR_DOMAIN, "op_count: N must be >= 1, got " + std::to_string(n));
+  if (!out) return fail(MMWS_GPU_ERR_DOMAIN, "op_count: null output");
+  const uint64_t un = static_cast<uint64_t>(n);
+  *out = un * un * (2 * un - 1);
+  return ok();
+}
+
+// ------------------------------------------------------------------ multiply
+int mmws_gpu_dgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
+                   int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int mode,
+                   void* stream) {
+  MMWS_CTX_GUARD(ctx);
+  return dgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode,
+                        static_cast<cudaStream_t>(stream));
+}
+
+int mmws_gpu_sgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const float* A,
+                   int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int mode,
+                   void* stream) {
+  MMWS_CTX_GUARD(ctx);
+  return sgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode,
+                        static_cast<cudaStream_t>(stream));
+}
+
+
+int mmws_gpu_matmul_host(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
+                         const double* B, double* C, int mode, double* elapsed_s) {
+  MMWS_CTX_GUARD(ctx);
+  return matmul_host_impl(ctx, m, n, k, A, B, C, mode, elapsed_s);
+}
+
+int mmws_gpu_matmul_host_f32(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k,
+                             const float* A, const float* B, float* C, int mode,
+                             double* elapsed_s) {
+  MMWS_CTX_GUARD(ctx);
+  return matmul_host_impl(ctx, m, n, k, A, B, C, mode, elapsed_s);
+}
+
+// ------------------------------------------------------------------ generators
+int mmws_gpu_fill(mmws_gpu_ctx* ctx, int dist, uint64_t seed, void* dst, int64_t rows,
+                  int64_t cols, int64_t ld, int is_f32, uint64_t first, void* stream) {
+  MMWS_CTX_GUARD(ctx);
+  if (rows <= 0 || cols <= 0 || ld < cols)
+    return fail(MMWS_GPU_ERR_DIMENSION, "fill: bad shape");
+  if (dist < 0 || dist > 3 || (dist == MMWS_GPU_DIST_NORMAL && !is_f32) || !dst)
+    return fail(MMWS_GPU_ERR_DOMAIN, "fill: bad distribution / dtype / pointer");
+  cudaError_t e = launch_fill(ctx->launch(static_cast<cudaStream_t>(stream)), dist, seed, dst,
+                              rows, cols, ld, is_f32, first);
+  return e == cudaSuccess ? ok() : cuda_fail(e, "fill");
+}
+
+// ------------------------------------------------------------------ graphs
+int mmws_gpu_graph_dgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
+                         int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                         int mode, mmws_gpu_graph** out) {
+  MMWS_CTX_GUARD(ctx);
+  if (!out) return fail(MMWS_GPU_ERR_DOMAIN, "graph_dgemm: null out");
+  *out = nullptr;
+  // One eager call first: sets kernel attributes and sizes the packing
+  // workspace, so nothing inside the capture allocates.
+  if (int rc = dgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode, ctx->stream)) return rc;
+  cudaError_t e;
+  if ((e = cudaStreamSynchronize(ctx->stream)) != cudaSuccess) return cuda_fail(e, "graph warmup");
+  auto* g = new (std::nothrow) mmws_gpu_graph();
+  if (!g) return fail(MMWS_GPU_ERR_ALLOC, "graph_dgemm: out of host memory");
+  g->ctx = ctx;
+  const uint64_t before = ctx->launches;
+  if ((e = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) {
+    delete g;
+    return cuda_fail(e, "graph capture begin");
+  }
+  const int rc = dgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode, ctx->stream);
+  e = cudaStreamEndCapture(ctx->stream, &g->graph);
+  g->kernels = ctx->launches - before;
+  ctx->launches = before;  // counted on replay
+  if (rc) {
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
+    return rc;
+  }
+  if (e != cudaSuccess) {
+    delete g;
+    return cuda_fail(e, "graph capture end");
+  }
+  if ((e = cudaGraphInstantiate(&g->exec, g->graph, 0)) != cudaSuccess) {
+    cudaGraphDestroy(g->graph);
+    delete g;
+    return cuda_fail(e, "graph instantiate");
+  }
+  *out = g;
+  return ok();
+}
+
+int mmws_gpu_graph_launch(mmws_gpu_graph* g, void* stream) {
+  if (!g) return fail(MMWS_GPU_ERR_STATE, "null graph");
+  mmws_gpu_ctx* ctx = g->ctx;
+  MMWS_CTX_GUARD(ctx);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  cudaError_t e = cudaGraphLaunch(g->exec, s);
+  if (e != cudaSuccess) return cuda_fail(e, "graph launch");
+  ctx->launches += g->kernels;
+  return ok();
+}
+
+int mmws_gpu_graph_destroy(mmws_gpu_graph* g) {
+  if (!g) return ok();
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  delete g;
+  return ok();
+}
+
+// ------------------------------------------------------------------ measurement
+int mmws_gpu_peak_probe(mmws_gpu_ctx* ctx, int which, int iters, double* tflops) {
+  MMWS_CTX_GUARD(ctx);
+  if (which < 0 || which > 3 || iters < 1 || !tflops)
+    return fail(MMWS_GPU_ERR_DOMAIN, "peak_probe: bad arguments");
+  const Launch L = ctx->launch(nullptr);
+  double flops = 0;
+  cudaError_t e = launch_peak_probe(L, which, iters, ctx->sink, &flops);  // warm-up
+  if (e != cudaSuccess) return cuda_fail(e, "peak_probe");
+  cudaEventRecord(ctx->ev0, ctx->stream);
+  e = launch_peak_probe(L, which, iters, ctx->sink, &flops);
+  cudaEventRecord(ctx->ev1, ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "peak_probe");
+  if ((e = cudaStreamSynchronize(ctx->stream)) != cudaSuccess) return cuda_fail(e, "peak_probe");
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+  *tflops = flops / (ms * 1e-3) / 1e12;
+  return ok();
+}
+
+}  // extern "C"

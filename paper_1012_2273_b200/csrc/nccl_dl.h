@@ -1,0 +1,55 @@
+// nccl_dl.h -- NCCL entry points resolved at run time with dlopen.
+//
+// libmmws_gpu.so does not link libnccl: a process that already holds an NCCL
+// (e.g. torch's bundled libnccl.so.2) must keep using that one -- a second,
+// older libnccl.so.2 bound first would break the other library's newer
+// symbols.  dlopen("libnccl.so.2") returns whichever copy the process already
+// loaded, or the system one otherwise.  Only the row-block path needs NCCL.
+#pragma once
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <mutex>
+
+namespace mmws_impl {
+
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+inline const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+#define MMWS_NCCL_SYM(field, name) api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name))
+    MMWS_NCCL_SYM(GetUniqueId, "ncclGetUniqueId");
+    MMWS_NCCL_SYM(CommInitRank, "ncclCommInitRank");
+    MMWS_NCCL_SYM(CommDestroy, "ncclCommDestroy");
+    MMWS_NCCL_SYM(Send, "ncclSend");
+    MMWS_NCCL_SYM(Recv, "ncclRecv");
+    MMWS_NCCL_SYM(Broadcast, "ncclBroadcast");
+    MMWS_NCCL_SYM(GroupStart, "ncclGroupStart");
+    MMWS_NCCL_SYM(GroupEnd, "ncclGroupEnd");
+    MMWS_NCCL_SYM(GetErrorString, "ncclGetErrorString");
+#undef MMWS_NCCL_SYM
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv &&
+             api.Broadcast && api.GroupStart && api.GroupEnd && api.GetErrorString;
+  });
+  return api;
+}
+
+}  // namespace mmws_impl

@@ -1,0 +1,326 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle.
+
+Bar (BASELINE.json north_star): bit-exact for integer-valued inputs and for
+the exact-order mode; fp64 DMMA normwise <= 1e-12, fp32 FFMA normwise <= 1e-5
+against the fp64 oracle of the widened inputs.  Golden fixtures in
+tests/golden/ were produced by the reference itself (gen_golden.py).
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_1012_2273_b200 as P
+
+pytestmark = pytest.mark.gpu
+
+FP64_TOL = 1e-12   # north_star: fp64 normwise relative error
+FP32_TOL = 1e-5    # north_star: fp32 normwise relative error vs fp64 oracle
+FP64_MODES = [P.MODE_EXACT, P.MODE_DMMA, P.MODE_DMMA_SMALL, P.MODE_AUTO]
+
+
+def torch():
+    import torch as T
+    return T
+
+
+def dev(x):
+    T = torch()
+    return T.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def host(t):
+    torch().cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def bits(x):
+    return np.ascontiguousarray(x, dtype=np.float64).view(np.uint64)
+
+
+def from_hex(h, shape):
+    return np.array([int(v, 16) for v in h], dtype=np.uint64).view(np.float64).reshape(shape)
+
+
+def normwise(x, ref):
+    return float(np.linalg.norm(x - ref) / np.linalg.norm(ref))
+
+
+def sha(x):
+    return hashlib.sha256(np.ascontiguousarray(x, dtype=np.float64).tobytes()).hexdigest()
+
+
+# ----------------------------------------------------------------------------- known answers
+@pytest.mark.parametrize("mode", FP64_MODES)
+def test_hand_computed_2x2_and_1x1(ctx, golden_small, mode):
+    # test_matrix.cpp:105-120 (and over msg, test_protocol.cpp:56-67)
+    c = host(ctx.dgemm(dev(np.array([[1., 2], [3, 4]])), dev(np.array([[5., 6], [7, 8]])),
+                       mode=mode))
+    assert c.tolist() == [[19.0, 22.0], [43.0, 50.0]]
+    assert (bits(c).ravel() == bits(from_hex(golden_small["matmul_2x2"], (2, 2))).ravel()).all()
+    c = host(ctx.dgemm(dev(np.array([[3.25]])), dev(np.array([[-2.0]])), mode=mode))
+    assert c[0, 0] == 3.25 * -2.0
+
+
+@pytest.mark.parametrize("mode", FP64_MODES)
+def test_identity_is_bitwise_neutral(ctx, oracle, mode):
+    # test_matrix.cpp:122-141
+    for n in (1, 2, 5, 13, 130):
+        a = oracle.ref_random_matrix(n, n, 1000 + n) if oracle.ref_available() else \
+            oracle.fill(0, 1000 + n, n, n)
+        eye = np.eye(n)
+        assert (bits(host(ctx.dgemm(dev(a), dev(eye), mode=mode))) == bits(a)).all()
+        assert (bits(host(ctx.dgemm(dev(eye), dev(a), mode=mode))) == bits(a)).all()
+
+
+def test_acceptance_products_match_reference_golden(ctx, oracle, golden_small):
+    # acceptance.cpp:90-109 dims, seeds 1000+N / 2000+N; golden = mmws::matmul_seq
+    for n in [int(k[2:]) for k in golden_small["products_unit"] if k.startswith("sq")]:
+        a = oracle.fill(oracle.DIST_UNIT, 1000 + n, n, n)
+        b = oracle.fill(oracle.DIST_UNIT, 2000 + n, n, n)
+        want = from_hex(golden_small["products_unit"][f"sq{n}"], (n, n))
+        got = host(ctx.dgemm(dev(a), dev(b), mode=P.MODE_EXACT))
+        assert (bits(got) == bits(want)).all(), f"exact N={n}"
+        for mode in (P.MODE_DMMA, P.MODE_DMMA_SMALL):
+            got = host(ctx.dgemm(dev(a), dev(b), mode=mode))
+            assert normwise(got, want) <= FP64_TOL, f"mode={mode} N={n}"
+
+
+def test_rectangular_products(ctx, oracle, golden_small):
+    # test_matrix.cpp:148-156, test_workshare.cpp:160-163, test_protocol.cpp:91-97
+    for key, (m, k, n, sa, sb) in {"rect2x5x4": (2, 5, 4, 303, 304),
+                                   "rect4x7x3": (4, 7, 3, 27, 28),
+                                   "rect5x7x4": (5, 7, 4, 31, 32)}.items():
+        a = oracle.fill(oracle.DIST_UNIT, sa, m, k)
+        b = oracle.fill(oracle.DIST_UNIT, sb, k, n)
+        want = from_hex(golden_small["products_unit"][key], (m, n))
+        for mode in FP64_MODES:
+            got = host(ctx.dgemm(dev(a), dev(b), mode=mode))
+            assert got.shape == (m, n)
+            if mode == P.MODE_EXACT:
+                assert (bits(got) == bits(want)).all()
+            else:
+                assert normwise(got, want) <= FP64_TOL
+
+
+# ----------------------------------------------------------------------------- exact mode, any input
+@pytest.mark.parametrize("shape", [(1, 1, 1), (7, 3, 5), (64, 64, 64), (127, 129, 131),
+                                   (200, 33, 257), (300, 1000, 17), (513, 257, 260)])
+def test_exact_mode_bitwise_equals_matmul_seq(ctx, oracle, shape):
+    m, k, n = shape
+    a = oracle.fill(oracle.DIST_UNIFORM, 11, m, k)
+    b = oracle.fill(oracle.DIST_UNIFORM, 12, k, n)
+    want = oracle.matmul_seq(a, b)
+    got = host(ctx.dgemm(dev(a), dev(b), mode=P.MODE_EXACT))
+    assert oracle.first_difference(got, want) is None
+
+
+def test_exact_mode_signed_zeros_and_specials(ctx, oracle):
+    # -0 handling: acc starts at +0, so all-zero rows give +0 (matrix.hpp:120)
+    a = np.array([[-0.0, 0.0], [1e308, 1e308], [1.0, -1.0]])
+    b = np.array([[0.0, -0.0], [-0.0, 3.0]])
+    want = oracle.matmul_seq(a, b)
+    for mode in FP64_MODES:
+        got = host(ctx.dgemm(dev(a), dev(b), mode=mode))
+        if mode == P.MODE_EXACT:
+            assert oracle.first_difference(got, want) is None
+        assert (np.signbit(got[0]) == np.signbit(want[0])).all()
+
+
+# ----------------------------------------------------------------------------- integer inputs: bit-exact everywhere
+@pytest.mark.parametrize("mode", FP64_MODES)
+@pytest.mark.parametrize("n", [1, 2, 3, 17, 100, 129, 255, 1001])
+def test_integer_inputs_bit_exact_all_modes(ctx, oracle, mode, n):
+    a = oracle.fill(oracle.DIST_INT8, 0, n, n)
+    b = oracle.fill(oracle.DIST_INT8, 1, n, n)
+    want = oracle.matmul_threads(a, b)
+    got = host(ctx.dgemm(dev(a), dev(b), mode=mode))
+    assert oracle.first_difference(got, want) is None
+
+
+def test_config_c3_n4099_integer_bit_exact(ctx, oracle, golden_big):
+    # BASELINE configs[2]: odd, non-tile-aligned N, DMMA path packs for TMA.
+    n = 4099
+    A = ctx.fill(P.DIST_INT8, 0, n, n)
+    B = ctx.fill(P.DIST_INT8, 1, n, n)
+    for mode in (P.MODE_AUTO, P.MODE_DMMA, P.MODE_EXACT):
+        c = host(ctx.dgemm(A, B, mode=mode))
+        assert sha(c) == golden_big["n4099_int8_sha256"], f"mode {mode}"
+
+
+# ----------------------------------------------------------------------------- real inputs: tolerance
+def test_config_c1_n1000(ctx, oracle, golden_big):
+    n = 1000
+    A = ctx.fill(P.DIST_UNIFORM, 0, n, n)
+    B = ctx.fill(P.DIST_UNIFORM, 1, n, n)
+    exact = host(ctx.dgemm(A, B, mode=P.MODE_EXACT))
+    assert sha(exact) == golden_big["n1000_uniform_sha256"]
+    for mode in (P.MODE_AUTO, P.MODE_DMMA, P.MODE_DMMA_SMALL):
+        assert normwise(host(ctx.dgemm(A, B, mode=mode)), exact) <= FP64_TOL
+
+
+@pytest.mark.parametrize("n", [10, 50, 100, 250, 500, 1500, 2000])
+def test_config_c2_sweep(ctx, oracle, n):
+    a = oracle.fill(oracle.DIST_UNIFORM, 0, n, n)
+    b = oracle.fill(oracle.DIST_UNIFORM, 1, n, n)
+    rows = sorted({0, n // 3, n // 2, n - 1})
+    want = oracle.matmul_rows(rows, a, b)
+    A, B = dev(a), dev(b)
+    got = host(ctx.dgemm(A, B, mode=P.MODE_EXACT))
+    assert (bits(got[rows]) == bits(want)).all()
+    for mode in (P.MODE_AUTO, P.MODE_DMMA, P.MODE_DMMA_SMALL):
+        assert normwise(host(ctx.dgemm(A, B, mode=mode))[rows], want) <= FP64_TOL
+    # graph replay (small-N latency path) gives the same bits as an eager call
+    C1 = ctx.dgemm(A, B, mode=P.MODE_AUTO)
+    C2 = torch().full_like(C1, float("nan"))
+    g = ctx.graph_dgemm(A, B, C2, mode=P.MODE_AUTO)
+    g.launch()
+    g.launch()
+    assert (bits(host(C1)) == bits(host(C2))).all()
+    g.close()
+
+
+def test_config_c4_n16384_sampled_rows(ctx, oracle, golden_big):
+    n = 16384
+    rows = golden_big["n16384_rows"]
+    A = ctx.fill(P.DIST_UNIFORM, 0, n, n)
+    B = ctx.fill(P.DIST_UNIFORM, 1, n, n)
+    a_rows = host(A[rows])
+    b = host(B)
+    # oracle rows on the box, pinned against the reference's own rows (sha256)
+    want = oracle.matmul_rows(list(range(len(rows))), a_rows, b)
+    assert [sha(want[i]) for i in range(len(rows))] == golden_big["n16384_rows_sha256"]
+    C = ctx.dgemm(A, B, mode=P.MODE_AUTO)
+    got = host(C[rows])
+    assert normwise(got, want) <= FP64_TOL
+    for i in range(len(rows)):
+        assert normwise(got[i], want[i]) <= FP64_TOL
+    exact = host(ctx.dgemm(A, B, mode=P.MODE_EXACT)[rows])
+    assert (bits(exact) == bits(want)).all()
+
+
+def test_config_c5_n32768_fp32_sampled_rows(ctx, oracle):
+    n = 32768
+    T = torch()
+    A = ctx.fill(P.DIST_NORMAL, 0, n, n, dtype=T.float32)
+    B = ctx.fill(P.DIST_NORMAL, 1, n, n, dtype=T.float32)
+    rows = [0, 1, 4095, 4096, 16383, 16384, 24575, 32767]
+    C = ctx.sgemm(A, B)
+    got = host(C[rows]).astype(np.float64)
+    a_rows = host(A[rows])
+    b = host(B)
+    want = oracle.matmul_rows(list(range(len(rows))), a_rows, b)
+    err = normwise(got, want)
+    assert err <= FP32_TOL, err
+
+
+def test_fp32_small_shapes(ctx, oracle):
+    for (m, k, n) in [(1, 1, 1), (3, 5, 7), (128, 128, 128), (129, 1000, 131), (1000, 37, 999)]:
+        a = oracle.fill(oracle.DIST_NORMAL, 3, m, k, dtype=np.float32)
+        b = oracle.fill(oracle.DIST_NORMAL, 4, k, n, dtype=np.float32)
+        want = oracle.matmul_rows(list(range(m)), a, b)
+        got = host(ctx.sgemm(dev(a), dev(b))).astype(np.float64)
+        assert normwise(got, want) <= FP32_TOL
+
+
+# ----------------------------------------------------------------------------- row-block semantics on one GPU
+@pytest.mark.parametrize("P_", [2, 3, 4, 8])
+def test_rowblock_slices_bitwise_equal_full_product(ctx, P_):
+    # split_rows blocks multiplied separately == 1-GPU product, bitwise: the
+    # property that makes P-GPU results identical to 1-GPU results.
+    n = 1031
+    A = ctx.fill(P.DIST_UNIFORM, 0, n, n)
+    B = ctx.fill(P.DIST_UNIFORM, 1, n, n)
+    for mode in (P.MODE_AUTO, P.MODE_DMMA, P.MODE_EXACT):
+        full = host(ctx.dgemm(A, B, mode=mode))
+        for off, rows in P.split_rows(n, P_):
+            if rows == 0:
+                continue
+            part = host(ctx.dgemm(A[off:off + rows].contiguous(), B, mode=mode))
+            assert (bits(part) == bits(full[off:off + rows])).all()
+
+
+def test_rowblock_single_rank_entry(ctx, oracle):
+    n = 300
+    A = ctx.fill(P.DIST_UNIFORM, 0, n, n)
+    B = ctx.fill(P.DIST_UNIFORM, 1, n, n)
+    C = torch().empty_like(A)
+    el = ctx.rowblock(n, n, n, A, B, C, mode=P.MODE_EXACT)
+    assert el > 0
+    want = oracle.matmul_seq(host(A), host(B))
+    assert oracle.first_difference(host(C), want) is None
+
+
+# ----------------------------------------------------------------------------- boundary behaviour
+def test_host_entry_matches_device_entry(ctx, oracle):
+    a = oracle.fill(oracle.DIST_UNIFORM, 5, 257, 300)
+    b = oracle.fill(oracle.DIST_UNIFORM, 6, 300, 129)
+    for mode in FP64_MODES:
+        c, el = ctx.matmul_host(a, b, mode=mode)
+        assert el > 0
+        assert (bits(c) == bits(host(ctx.dgemm(dev(a), dev(b), mode=mode)))).all()
+    c, _ = ctx.matmul_host(a, b, mode=P.MODE_EXACT)
+    assert oracle.first_difference(c, oracle.matmul_seq(a, b)) is None
+    af, bf = a.astype(np.float32), b.astype(np.float32)
+    cf, _ = ctx.matmul_host(af, bf)
+    assert normwise(cf.astype(np.float64), oracle.matmul_rows(list(range(257)), af, bf)) <= FP32_TOL
+
+
+def test_strided_views_and_unaligned_leading_dims(ctx, oracle):
+    T = torch()
+    big_a = ctx.fill(P.DIST_UNIFORM, 7, 300, 301)
+    big_b = ctx.fill(P.DIST_UNIFORM, 8, 211, 259)
+    A = big_a[3:203, 1:212]   # odd offset -> misaligned base, lda = 301
+    B = big_b[:, 2:201]       # ldb = 259
+    a, b = host(A.contiguous()), host(B.contiguous())
+    want = oracle.matmul_seq(a, b)
+    Cbig = T.zeros((200, 205), dtype=T.float64, device="cuda")
+    Cv = Cbig[:, 3:202]
+    for mode in FP64_MODES:
+        ctx.dgemm(A, B, Cv, mode=mode)
+        got = host(Cv.contiguous())
+        if mode == P.MODE_EXACT:
+            assert oracle.first_difference(got, want) is None
+        else:
+            assert normwise(got, want) <= FP64_TOL
+        cb = host(Cbig)
+        assert (cb[:, :3] == 0).all() and (cb[:, 202:] == 0).all()
+
+
+def test_errors_map_to_reference_types(ctx):
+    T = torch()
+    a = T.zeros((2, 3), dtype=T.float64, device="cuda")
+    b = T.zeros((2, 2), dtype=T.float64, device="cuda")
+    with pytest.raises(P.DimensionError):
+        ctx.dgemm(a, b)                       # inner mismatch (matrix.hpp:113-116)
+    with pytest.raises(P.DomainError):
+        ctx.dgemm(a, a.t().contiguous(), mode=99)
+    with pytest.raises(P.DimensionError):
+        ctx.matmul_host(np.zeros((2, 3)), np.zeros((2, 2)))
+
+
+def test_device_generators_match_oracle(ctx, oracle):
+    for dist in (oracle.DIST_UNIT, oracle.DIST_UNIFORM, oracle.DIST_INT8):
+        for (r, c, first) in [(1, 1, 0), (17, 23, 0), (64, 100, 12345)]:
+            want = oracle.fill(dist, 42, r, c, first=first)
+            got = host(ctx.fill(dist, 42, r, c, first=first))
+            assert (bits(got) == bits(want)).all()
+    T = torch()
+    got = host(ctx.fill(P.DIST_NORMAL, 3, 50, 70, dtype=T.float32))
+    want = oracle.fill(oracle.DIST_NORMAL, 3, 50, 70, dtype=np.float32)
+    assert np.allclose(got, want, rtol=1e-6, atol=1e-6)
+
+
+def test_launch_accounting(ctx):
+    before = ctx.launches
+    T = torch()
+    a = T.ones((64, 64), dtype=T.float64, device="cuda")
+    ctx.dgemm(a, a, mode=P.MODE_DMMA)
+    ctx.dgemm(a, a, mode=P.MODE_EXACT)
+    assert ctx.launches - before == 2
+
+
+def test_peak_probes_run(ctx):
+    for which in (P.PROBE_DMMA, P.PROBE_DFMA, P.PROBE_DMUL_DADD, P.PROBE_FFMA):
+        tf = ctx.peak_probe(which, 256)
+        assert 0.5 < tf < 200, (which, tf)
