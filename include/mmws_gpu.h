@@ -188,6 +188,21 @@ int mmws_gpu_rowblock_dgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k,
 int mmws_gpu_rowblock_sgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const float* A,
                             const float* B, float* C, int mode, double* elapsed_s);
 
+/* master_run (protocol.hpp:50-108) for host matrices: rank 0 passes dense host
+ * A (m x k), B (k x n) and receives C (m x n); other ranks pass NULL.  The
+ * H2D copies of A and B, the round above and the D2H copy of C are all inside
+ * *elapsed_s (rank 0).  With no communicator (or nranks == 1) this is the
+ * single-GPU host-buffer multiply. */
+int mmws_gpu_master_run_host(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k,
+                             const double* A, const double* B, double* C, int mode,
+                             double* elapsed_s);
+int mmws_gpu_master_run_host_f32(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k,
+                                 const float* A, const float* B, float* C, int mode,
+                                 double* elapsed_s);
+/* Device time (ms, CUDA events on the launch stream) of this rank's multiply
+ * kernel(s) in the most recent row-block / master_run call. */
+int mmws_gpu_last_kernel_ms(mmws_gpu_ctx* ctx, double* ms);
+
 /* The message plan rank 0 executes for (m, k, n, nranks), in issue order --
  * the analogue of the reference's Communicator traffic log (comm.hpp:24-32)
  * used by its protocol-shape test (test_protocol.cpp:99-137).  Host-only.

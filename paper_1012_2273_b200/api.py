@@ -289,6 +289,39 @@ class Context:
         return el.value
 
 
+def _master_run_host(self, a=None, b=None, out=None, mode: int = MODE_AUTO, m=None, n=None,
+                     k=None, f32: bool = False):
+    """master_run (protocol.hpp:50-108) with host matrices on rank 0 (numpy
+    arrays, pinned for full PCIe bandwidth); other ranks pass nothing but the
+    shape.  Returns (C or None, elapsed_s)."""
+    if a is not None:
+        if a.shape[1] != b.shape[0]:
+            raise DimensionError(f"master_run: inner dimensions disagree, {a.shape[1]} vs {b.shape[0]}")
+        m, k = a.shape
+        n = b.shape[1]
+        f32 = a.dtype == np.float32
+        if out is None:
+            out = np.empty((m, n), dtype=a.dtype)
+        for x in (a, b, out):
+            if not x.flags["C_CONTIGUOUS"]:
+                raise DimensionError("master_run: host matrices must be C-contiguous")
+    el = C.c_double()
+    fn = _lib().mmws_gpu_master_run_host_f32 if f32 else _lib().mmws_gpu_master_run_host
+    ptr = (lambda x: x.ctypes.data if x is not None else None)
+    _check(fn(self._h, m, n, k, ptr(a), ptr(b), ptr(out), mode, C.byref(el)))
+    return out, el.value
+
+
+def _last_kernel_ms(self) -> float:
+    out = C.c_double()
+    _check(_lib().mmws_gpu_last_kernel_ms(self._h, C.byref(out)))
+    return out.value
+
+
+Context.master_run_host = _master_run_host
+Context.last_kernel_ms = property(_last_kernel_ms)
+
+
 def bootstrap_comm(ctx: Context) -> None:
     """NCCL communicator for the current torch.distributed world: rank 0 makes
     the unique id, torch.distributed ships it (plumbing only)."""

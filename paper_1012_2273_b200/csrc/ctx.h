@@ -15,6 +15,8 @@ struct mmws_gpu_ctx {
   int cc_major = 0, cc_minor = 0, clock_khz = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t evk0 = nullptr, evk1 = nullptr;  // around the row-block multiply
+  double last_kernel_ms = 0.0;
   mmws_impl::EncodeTiledFn encode = nullptr;
   uint64_t launches = 0;
   std::mutex mu;

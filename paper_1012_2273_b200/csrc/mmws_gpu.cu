@@ -222,6 +222,8 @@ int mmws_gpu_init(int device, mmws_gpu_ctx** out) {
       (e = cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaEventCreate(&ctx->ev0)) != cudaSuccess ||
       (e = cudaEventCreate(&ctx->ev1)) != cudaSuccess ||
+      (e = cudaEventCreate(&ctx->evk0)) != cudaSuccess ||
+      (e = cudaEventCreate(&ctx->evk1)) != cudaSuccess ||
       (e = cudaMalloc(&ctx->sink, 4096 * sizeof(double))) != cudaSuccess) {
     mmws_gpu_destroy(ctx);
     return cuda_fail(e, "mmws_gpu_init");
@@ -240,6 +242,8 @@ int mmws_gpu_destroy(mmws_gpu_ctx* ctx) {
     if (p) cudaFree(p);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->evk0) cudaEventDestroy(ctx->evk0);
+  if (ctx->evk1) cudaEventDestroy(ctx->evk1);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   delete ctx;

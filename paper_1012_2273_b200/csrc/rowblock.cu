@@ -38,6 +38,8 @@ int nccl_fail(ncclResult_t r, const char* what) {
 #define NCCL_REQUIRE()                                                          \
   if (!nccl().ok) return fail(MMWS_GPU_ERR_NCCL, "libnccl.so.2 could not be loaded");
 
+
+
 #define NCCL_TRY(call, what)                                   \
   do {                                                         \
     ncclResult_t r_ = (call);                                  \
@@ -45,14 +47,22 @@ int nccl_fail(ncclResult_t r, const char* what) {
   } while (0)
 
 template <class T>
-int rowblock(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, const T* B, T* C,
-             int mode, double* elapsed_s) {
+T* as_mut(const T* p) {
+  return const_cast<T*>(p);
+}
+
+// Enqueue one master/worker round on ctx->stream (no synchronisation).  Rank
+// 0 passes device A, B, C; other ranks pass nulls and use library buffers.
+template <class T>
+int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, const T* B,
+                     T* C, int mode) {
   if (m <= 0 || n <= 0 || k <= 0)
     return fail(MMWS_GPU_ERR_DIMENSION, "rowblock: dimensions must be positive");
   const int P = ctx->comm ? ctx->nranks : 1;
   const int me = ctx->comm ? ctx->rank : 0;
   if (me == 0 && (!A || !B || !C))
     return fail(MMWS_GPU_ERR_DOMAIN, "rowblock: rank 0 needs A, B and C");
+  if (P > 1) NCCL_REQUIRE();
   std::vector<int64_t> off(P), rows(P);
   if (int rc = mmws_gpu_split_rows(m, P, off.data(), rows.data())) return rc;
 
@@ -73,8 +83,6 @@ int rowblock(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, con
     c_loc = static_cast<T*>(ctx->rbC);
   }
 
-  if (me == 0) cudaEventRecord(ctx->ev0, s);  // first send
-
   if (P > 1) {
     // tag 1: A-slices (protocol.hpp:70-72) ...
     NCCL_TRY(nccl().GroupStart(), "ncclGroupStart");
@@ -83,15 +91,16 @@ int rowblock(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, con
         if (rows[r] > 0)
           NCCL_TRY(nccl().Send(A + off[r] * k, rows[r] * k, dt, r, ctx->comm, s), "send A-slice");
     } else if (rows[me] > 0) {
-      NCCL_TRY(nccl().Recv(const_cast<T*>(a_loc), rows[me] * k, dt, 0, ctx->comm, s), "recv A-slice");
+      NCCL_TRY(nccl().Recv(as_mut(a_loc), rows[me] * k, dt, 0, ctx->comm, s), "recv A-slice");
     }
     NCCL_TRY(nccl().GroupEnd(), "ncclGroupEnd");
     // ... and all of B (protocol.hpp:73), once, as a broadcast.
-    void* bbuf = me == 0 ? const_cast<T*>(B) : const_cast<T*>(b_loc);
+    void* bbuf = me == 0 ? as_mut(B) : as_mut(b_loc);
     NCCL_TRY(nccl().Broadcast(bbuf, bbuf, k * n, dt, 0, ctx->comm, s), "broadcast B");
   }
 
-  // worker body (protocol.hpp:132-141) on this rank's rows
+  // worker body (protocol.hpp:132-141) on this rank's rows, timed on its stream
+  cudaEventRecord(ctx->evk0, s);
   if (rows[me] > 0) {
     int rc;
     if constexpr (sizeof(T) == 8)
@@ -100,6 +109,7 @@ int rowblock(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, con
       rc = sgemm_dispatch(ctx, rows[me], n, k, a_loc, k, b_loc, n, c_loc, n, mode, s);
     if (rc) return rc;
   }
+  cudaEventRecord(ctx->evk1, s);
 
   if (P > 1) {
     // tag 2: C-slices back into C's row blocks, rank order (protocol.hpp:85-103)
@@ -113,15 +123,61 @@ int rowblock(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, con
     }
     NCCL_TRY(nccl().GroupEnd(), "ncclGroupEnd");
   }
+  return MMWS_GPU_OK;
+}
 
-  if (me == 0) cudaEventRecord(ctx->ev1, s);  // last receive
-  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "rowblock: sync");
-  if (me == 0 && elapsed_s) {
-    float ms = 0.f;
+int finish(mmws_gpu_ctx* ctx, bool timed, double* elapsed_s) {
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "rowblock: sync");
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, ctx->evk0, ctx->evk1) == cudaSuccess) ctx->last_kernel_ms = ms;
+  if (timed && elapsed_s) {
     cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
     *elapsed_s = ms * 1e-3;
   }
   return ok();
+}
+
+template <class T>
+int rowblock(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, const T* B, T* C,
+             int mode, double* elapsed_s) {
+  const bool root = !ctx->comm || ctx->rank == 0;
+  if (root) cudaEventRecord(ctx->ev0, ctx->stream);  // first send
+  if (int rc = rowblock_enqueue(ctx, m, n, k, A, B, C, mode)) return rc;
+  if (root) cudaEventRecord(ctx->ev1, ctx->stream);  // last receive
+  return finish(ctx, root, elapsed_s);
+}
+
+// master_run with host matrices on rank 0: H2D of A and B, the round, D2H of
+// C, all inside the elapsed bracket (the reference's master holds host data).
+template <class T>
+int master_run_host(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, const T* B,
+                    T* C, int mode, double* elapsed_s) {
+  const bool root = !ctx->comm || ctx->rank == 0;
+  if (!root) return rowblock(ctx, m, n, k, static_cast<const T*>(nullptr),
+                             static_cast<const T*>(nullptr), static_cast<T*>(nullptr), mode,
+                             elapsed_s);
+  if (m <= 0 || n <= 0 || k <= 0)
+    return fail(MMWS_GPU_ERR_DIMENSION, "master_run: dimensions must be positive");
+  if (!A || !B || !C) return fail(MMWS_GPU_ERR_DOMAIN, "master_run: null host matrix");
+  const size_t a_b = sizeof(T) * m * k, b_b = sizeof(T) * k * n, c_b = sizeof(T) * m * n;
+  cudaError_t e;
+  if ((e = ensure(&ctx->dA, &ctx->dA_bytes, a_b)) != cudaSuccess ||
+      (e = ensure(&ctx->dB, &ctx->dB_bytes, b_b)) != cudaSuccess ||
+      (e = ensure(&ctx->dC, &ctx->dC_bytes, c_b)) != cudaSuccess)
+    return cuda_fail(e, "master_run: device buffers");
+  cudaStream_t s = ctx->stream;
+  cudaEventRecord(ctx->ev0, s);
+  if ((e = cudaMemcpyAsync(ctx->dA, A, a_b, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(ctx->dB, B, b_b, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return cuda_fail(e, "master_run: H2D");
+  if (int rc = rowblock_enqueue(ctx, m, n, k, static_cast<const T*>(ctx->dA),
+                                static_cast<const T*>(ctx->dB), static_cast<T*>(ctx->dC), mode))
+    return rc;
+  if ((e = cudaMemcpyAsync(C, ctx->dC, c_b, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return cuda_fail(e, "master_run: D2H");
+  cudaEventRecord(ctx->ev1, s);
+  return finish(ctx, true, elapsed_s);
 }
 
 }  // namespace
@@ -183,6 +239,26 @@ int mmws_gpu_rowblock_sgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, 
                             const float* B, float* C, int mode, double* elapsed_s) {
   MMWS_CTX_GUARD(ctx);
   return rowblock<float>(ctx, m, n, k, A, B, C, mode, elapsed_s);
+}
+
+int mmws_gpu_master_run_host(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k,
+                             const double* A, const double* B, double* C, int mode,
+                             double* elapsed_s) {
+  MMWS_CTX_GUARD(ctx);
+  return master_run_host<double>(ctx, m, n, k, A, B, C, mode, elapsed_s);
+}
+
+int mmws_gpu_master_run_host_f32(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k,
+                                 const float* A, const float* B, float* C, int mode,
+                                 double* elapsed_s) {
+  MMWS_CTX_GUARD(ctx);
+  return master_run_host<float>(ctx, m, n, k, A, B, C, mode, elapsed_s);
+}
+
+int mmws_gpu_last_kernel_ms(mmws_gpu_ctx* ctx, double* ms) {
+  if (!ctx || !ms) return fail(MMWS_GPU_ERR_DOMAIN, "last_kernel_ms: null argument");
+  *ms = ctx->last_kernel_ms;
+  return ok();
 }
 
 int mmws_gpu_rowblock_plan(int64_t m, int64_t n, int64_t k, int nranks, int32_t* peer,
