@@ -1,0 +1,277 @@
+// mmws_gpu.hpp -- header-only C++ drop-in for the reference's hot-path API,
+// implemented on top of the C ABI in mmws_gpu.h (libmmws_gpu.so, sm_100a).
+//
+// Reference surface (namespace mmws, /root/reference/proj/include/mmws/):
+//   Matrix matmul_seq(const Matrix&, const Matrix&)                matrix.hpp:112-126
+//   Matrix matmul_threads(const Matrix&, const Matrix&, unsigned)  workshare.hpp:98-113
+//   std::vector<WorkAssignment> split_rows(int64_t, int)           protocol.hpp:33-46
+//   std::pair<Matrix,double> master_run(Communicator&, a, b)       protocol.hpp:50-108
+//   void worker_run(Communicator&)                                  protocol.hpp:112-147
+//   Partition static_partition(size_t, unsigned)                   workshare.hpp:33-46
+//   uint64_t op_count(int64_t)                                      matrix.hpp:130-134
+// Here they live in namespace mmws::gpu with the same names, argument
+// meaning and exception types, plus a Context (the device, its stream and --
+// for master_run -- its NCCL communicator) as first argument.
+//
+// Matrix type: any row-major fp64/fp32 matrix with rows(), cols(), data()
+// (contiguous, rows*cols elements) and a (rows, cols, std::vector<T>)
+// constructor -- i.e. the reference's mmws::Matrix itself when its headers are
+// on the include path, or mmws::gpu::HostMatrix<T> (MatrixF32 for the fp32
+// configuration, which the reference has no type for).
+//
+// Errors: DimensionError / DomainError / RankError / ProtocolError are the
+// reference's own types (error.hpp) when available, identical stand-ins
+// otherwise; CUDA / NCCL failures throw mmws::gpu::GpuError.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "mmws_gpu.h"
+
+#if __has_include(<mmws/error.hpp>)
+#include <mmws/error.hpp>
+#else
+namespace mmws {
+struct DimensionError : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct DomainError : std::domain_error {
+  using std::domain_error::domain_error;
+};
+struct RankError : std::out_of_range {
+  using std::out_of_range::out_of_range;
+};
+struct ProtocolError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+}  // namespace mmws
+#endif
+
+namespace mmws {
+namespace gpu {
+
+struct GpuError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+enum class Mode : int {
+  automatic = MMWS_GPU_MODE_AUTO,   // DMMA tensor path, tile size by problem size
+  exact = MMWS_GPU_MODE_EXACT,      // bitwise identical to mmws::matmul_seq
+  dmma = MMWS_GPU_MODE_DMMA,
+  dmma_small = MMWS_GPU_MODE_DMMA_SMALL,
+  ffma = MMWS_GPU_MODE_FFMA,
+};
+
+inline void check(int rc) {
+  if (rc == MMWS_GPU_OK) return;
+  const std::string msg = mmws_gpu_last_error();
+  switch (rc) {
+    case MMWS_GPU_ERR_DIMENSION: throw DimensionError(msg);
+    case MMWS_GPU_ERR_DOMAIN: throw DomainError(msg);
+    case MMWS_GPU_ERR_RANK: throw RankError(msg);
+    case MMWS_GPU_ERR_PROTOCOL: throw ProtocolError(msg);
+    default: throw GpuError(msg);
+  }
+}
+
+// ---------------------------------------------------------------- host matrix
+template <class T>
+class HostMatrix {
+ public:
+  HostMatrix(std::size_t r, std::size_t c) : rows_(r), cols_(c), data_(checked(r, c), T(0)) {}
+  HostMatrix(std::size_t r, std::size_t c, std::vector<T> v)
+      : rows_(r), cols_(c), data_(std::move(v)) {
+    if (data_.size() != checked(r, c))
+      throw DimensionError("HostMatrix: value buffer has " + std::to_string(data_.size()) +
+                           " elements, expected " + std::to_string(r * c));
+  }
+  std::size_t rows() const { return rows_; }
+  std::size_t cols() const { return cols_; }
+  std::size_t size() const { return data_.size(); }
+  T operator()(std::size_t i, std::size_t j) const { return data_[i * cols_ + j]; }
+  T& operator()(std::size_t i, std::size_t j) { return data_[i * cols_ + j]; }
+  const std::vector<T>& data() const { return data_; }
+  std::vector<T>& data() { return data_; }
+
+ private:
+  static std::size_t checked(std::size_t r, std::size_t c) {
+    if (r == 0 || c == 0)
+      throw DimensionError("HostMatrix: dimensions must be positive, got " + std::to_string(r) +
+                           "x" + std::to_string(c));
+    return r * c;
+  }
+  std::size_t rows_, cols_;
+  std::vector<T> data_;
+};
+using MatrixF64 = HostMatrix<double>;
+using MatrixF32 = HostMatrix<float>;
+
+// ---------------------------------------------------------------- context
+class Context {
+ public:
+  explicit Context(int device = 0) { check(mmws_gpu_init(device, &ctx_)); }
+  ~Context() {
+    if (ctx_) mmws_gpu_destroy(ctx_);
+  }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  Context(Context&& o) noexcept : ctx_(o.ctx_), rank_(o.rank_), world_(o.world_) {
+    o.ctx_ = nullptr;
+  }
+
+  mmws_gpu_ctx* handle() const { return ctx_; }
+  int rank() const { return rank_; }
+  int world_size() const { return world_; }
+  std::uint64_t launches() const { return mmws_gpu_launch_count(ctx_); }
+
+  // NCCL world for master_run/worker_run; rank 0 creates the id
+  // (unique_id()) and ships it to every rank by any control plane.
+  static std::vector<std::uint8_t> unique_id() {
+    std::vector<std::uint8_t> id(128);
+    check(mmws_gpu_nccl_unique_id(id.data()));
+    return id;
+  }
+  void comm_init(int world_size, int rank, const std::vector<std::uint8_t>& id) {
+    if (id.size() != 128) throw DomainError("comm_init: unique id must be 128 bytes");
+    check(mmws_gpu_comm_init(ctx_, world_size, rank, id.data()));
+    rank_ = rank;
+    world_ = world_size;
+  }
+
+ private:
+  mmws_gpu_ctx* ctx_ = nullptr;
+  int rank_ = 0, world_ = 1;
+};
+
+// ---------------------------------------------------------------- partitions
+struct WorkAssignment {
+  std::int64_t offset = 0;
+  std::int64_t rows = 0;
+  bool operator==(const WorkAssignment&) const = default;
+};
+
+inline std::vector<WorkAssignment> split_rows(std::int64_t n_rows, int n_workers) {
+  std::vector<std::int64_t> off(n_workers > 0 ? n_workers : 1), rows(off.size());
+  check(mmws_gpu_split_rows(n_rows, n_workers, off.data(), rows.data()));
+  std::vector<WorkAssignment> out(off.size());
+  for (std::size_t i = 0; i < off.size(); ++i) out[i] = {off[i], rows[i]};
+  return out;
+}
+
+struct Range {
+  std::size_t start = 0;
+  std::size_t len = 0;
+  bool operator==(const Range&) const = default;
+};
+
+inline std::vector<Range> static_partition(std::size_t iterations, unsigned workers) {
+  std::vector<std::uint64_t> st(workers ? workers : 1), ln(st.size());
+  check(mmws_gpu_static_partition(iterations, workers, st.data(), ln.data()));
+  std::vector<Range> out(st.size());
+  for (std::size_t i = 0; i < st.size(); ++i) out[i] = {st[i], ln[i]};
+  return out;
+}
+
+inline std::uint64_t op_count(std::int64_t n) {
+  std::uint64_t out = 0;
+  check(mmws_gpu_op_count(n, &out));
+  return out;
+}
+
+// ---------------------------------------------------------------- multiply
+namespace detail {
+template <class M>
+auto element_type(const M& m) -> std::decay_t<decltype(*m.data().data())>;
+
+template <class M>
+M multiply(Context& ctx, const M& a, const M& b, Mode mode, const char* who) {
+  using T = decltype(element_type(a));
+  static_assert(sizeof(T) == 8 || sizeof(T) == 4, "fp64 or fp32 matrices");
+  if (a.cols() != b.rows())
+    throw DimensionError(std::string(who) + ": inner dimensions differ, " +
+                         std::to_string(a.cols()) + " vs " + std::to_string(b.rows()));
+  std::vector<T> out(a.rows() * b.cols());
+  const auto m = static_cast<std::int64_t>(a.rows());
+  const auto n = static_cast<std::int64_t>(b.cols());
+  const auto k = static_cast<std::int64_t>(a.cols());
+  if constexpr (sizeof(T) == 8)
+    check(mmws_gpu_matmul_host(ctx.handle(), m, n, k, a.data().data(), b.data().data(),
+                               out.data(), static_cast<int>(mode), nullptr));
+  else
+    check(mmws_gpu_matmul_host_f32(ctx.handle(), m, n, k, a.data().data(), b.data().data(),
+                                   out.data(), static_cast<int>(mode), nullptr));
+  return M(a.rows(), b.cols(), std::move(out));
+}
+}  // namespace detail
+
+// General entry: DMMA tensor path by default (normwise <= 1e-12 vs the
+// sequential order; bit-exact for integer-valued inputs), Mode::exact for the
+// reference's bitwise contract.
+template <class M>
+M matmul(Context& ctx, const M& a, const M& b, Mode mode = Mode::automatic) {
+  return detail::multiply(ctx, a, b, mode, "matmul");
+}
+
+// matmul_seq (matrix.hpp:112-126): bitwise identical result, on the GPU.
+template <class M>
+M matmul_seq(Context& ctx, const M& a, const M& b) {
+  return detail::multiply(ctx, a, b, Mode::exact, "matmul");
+}
+
+// matmul_threads (workshare.hpp:98-113): the whole GPU is the worker team; the
+// result is bitwise matmul_seq's, as the reference guarantees for its threads.
+template <class M>
+M matmul_threads(Context& ctx, const M& a, const M& b, unsigned workers) {
+  if (a.cols() != b.rows())
+    throw DimensionError("matmul_threads: inner dimensions differ, " + std::to_string(a.cols()) +
+                         " vs " + std::to_string(b.rows()));
+  if (workers == 0) throw DomainError("matmul_threads: worker count must be >= 1");
+  return detail::multiply(ctx, a, b, Mode::exact, "matmul_threads");
+}
+
+// master_run (protocol.hpp:50-108) on rank 0 of the context's NCCL world:
+// row blocks of A by split_rows over all ranks (rank 0 computes too), B
+// broadcast, C gathered.  Returns (C, elapsed first send -> last receive,
+// including the host<->device copies of A, B and C).
+template <class M>
+std::pair<M, double> master_run(Context& ctx, const M& a, const M& b,
+                                Mode mode = Mode::automatic) {
+  using T = decltype(detail::element_type(a));
+  if (ctx.rank() != 0) throw RankError("master_run must be called by rank 0");
+  if (a.cols() != b.rows()) throw DimensionError("master_run: inner dimensions disagree");
+  std::vector<T> out(a.rows() * b.cols());
+  double elapsed = 0.0;
+  const auto m = static_cast<std::int64_t>(a.rows());
+  const auto n = static_cast<std::int64_t>(b.cols());
+  const auto k = static_cast<std::int64_t>(a.cols());
+  if constexpr (sizeof(T) == 8)
+    check(mmws_gpu_master_run_host(ctx.handle(), m, n, k, a.data().data(), b.data().data(),
+                                   out.data(), static_cast<int>(mode), &elapsed));
+  else
+    check(mmws_gpu_master_run_host_f32(ctx.handle(), m, n, k, a.data().data(),
+                                       b.data().data(), out.data(), static_cast<int>(mode),
+                                       &elapsed));
+  return {M(a.rows(), b.cols(), std::move(out)), elapsed};
+}
+
+// worker_run (protocol.hpp:112-147) on ranks >= 1.  The reference learns the
+// shapes from the messages; NCCL collectives need them up front, so the
+// worker passes (m, n, k) -- every rank derives its rows from split_rows.
+inline void worker_run(Context& ctx, std::int64_t m, std::int64_t n, std::int64_t k,
+                       Mode mode = Mode::automatic, bool f32 = false) {
+  if (ctx.rank() == 0) throw RankError("worker_run must not be called by rank 0");
+  if (f32)
+    check(mmws_gpu_master_run_host_f32(ctx.handle(), m, n, k, nullptr, nullptr, nullptr,
+                                       static_cast<int>(mode), nullptr));
+  else
+    check(mmws_gpu_master_run_host(ctx.handle(), m, n, k, nullptr, nullptr, nullptr,
+                                   static_cast<int>(mode), nullptr));
+}
+
+}  // namespace gpu
+}  // namespace mmws

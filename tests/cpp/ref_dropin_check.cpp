@@ -1,0 +1,15 @@
+// Compile-only proof that include/mmws_gpu.hpp is a drop-in for the
+// reference's own types: instantiated with mmws::Matrix from the unmodified
+// reference headers (built here only, where /root/reference exists).
+#include <mmws/matrix.hpp>
+#include <mmws/workshare.hpp>
+
+#include "mmws_gpu.hpp"
+
+mmws::Matrix via_gpu(mmws::gpu::Context& ctx, const mmws::Matrix& a, const mmws::Matrix& b) {
+  mmws::Matrix s = mmws::gpu::matmul_seq(ctx, a, b);
+  mmws::Matrix t = mmws::gpu::matmul_threads(ctx, a, b, mmws::default_workers());
+  auto [c, elapsed] = mmws::gpu::master_run(ctx, a, b);
+  (void)elapsed;
+  return mmws::bitwise_equal(s, t) ? c : mmws::gpu::matmul(ctx, a, b);
+}

@@ -1,0 +1,145 @@
+"""CPU tests of the drop-in boundary: the C-ABI library loads, exports every
+symbol include/mmws_gpu.h declares, its host-only logic matches the reference
+(split_rows, static_partition, op_count, the row-block message plan), the C++
+adapter compiles against the reference's own Matrix type, and there is no CPU
+fallback (no compute calls here)."""
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_1012_2273_b200 as P
+from paper_1012_2273_b200 import _abi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF_INC = "/root/reference/proj/include"
+
+
+def header_functions():
+    with open(os.path.join(ROOT, "include", "mmws_gpu.h")) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"^\s*(?:const char\*|int|uint64_t|void\*)\s+(mmws_gpu_\w+)\(",
+                                 text, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _abi.load()
+    declared = header_functions()
+    assert len(declared) >= 25
+    nm = subprocess.run(["nm", "-D", "--defined-only", _abi.LIB_PATH], capture_output=True,
+                        text=True, check=True).stdout
+    exported = set(re.findall(r" T (mmws_gpu_\w+)", nm))
+    assert set(declared) <= exported, set(declared) - exported
+    assert set(declared) == set(_abi.SIGNATURES), set(declared) ^ set(_abi.SIGNATURES)
+    for name in declared:
+        assert getattr(lib, name) is not None
+    assert lib.mmws_gpu_abi_version() == 1
+
+
+def test_library_is_sm100a_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", _abi.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    archs = set(re.findall(r"sm_\d+a?", out))
+    assert archs == {"sm_100a"}, archs
+
+
+def test_no_cpu_fallback_without_gpu():
+    # No GPU in this container: creating a context must fail loudly.
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("a GPU is present")
+    except ImportError:
+        pass
+    with pytest.raises(P.GpuError):
+        P.Context(0)
+
+
+def test_split_rows_matches_reference(oracle, golden_small):
+    for key, want in golden_small["split_rows"].items():
+        n, w = (int(x) for x in key.split(","))
+        assert [list(x) for x in P.split_rows(n, w)] == want
+    assert P.split_rows(4, 3) == [(0, 2), (2, 1), (3, 1)]
+    assert P.split_rows(2, 3) == [(0, 1), (1, 1), (2, 0)]
+    for n in range(0, 201, 13):
+        for w in range(1, 17):
+            assert P.split_rows(n, w) == oracle.split_rows(n, w)
+    with pytest.raises(P.DomainError):
+        P.split_rows(4, 0)
+    with pytest.raises(P.DomainError):
+        P.split_rows(-1, 2)
+
+
+def test_static_partition_and_op_count_match_reference(golden_small):
+    for key, want in golden_small["static_partition"].items():
+        n, w = (int(x) for x in key.split(","))
+        assert [list(x) for x in P.static_partition(n, w)] == want
+    with pytest.raises(P.DomainError):
+        P.static_partition(3, 0)
+    for n, want in golden_small["op_count"].items():
+        assert P.op_count(int(n)) == want
+    with pytest.raises(P.DomainError):
+        P.op_count(0)
+    with pytest.raises(P.DomainError):
+        P.op_count(-5)
+
+
+def test_rowblock_plan_shape():
+    # The reference's protocol shape test (test_protocol.cpp:99-137) on a 4x4
+    # problem over 2 workers; here rank 0 also computes, so 3 ranks = rank 0 +
+    # 2 remote workers, metadata is derived locally (no scalar messages), and B
+    # is one broadcast instead of per-worker copies.
+    plan = P.rowblock_plan(4, 4, 4, 3)
+    assert [(e["dir"], e["tag"], e["peer"], e["count"]) for e in plan] == [
+        ("sent", 1, 1, 4), ("sent", 1, 2, 4), ("broadcast", 1, -1, 16),
+        ("received", 2, 1, 4), ("received", 2, 2, 4)]
+    # idle ranks (P > N) exchange nothing but still join the collectives
+    plan = P.rowblock_plan(2, 2, 2, 5)
+    assert [e["peer"] for e in plan if e["dir"] == "sent"] == [1]
+    assert P.rowblock_plan(7, 7, 7, 1) == []
+    # total traffic: A slices (m - rows_0) k, B once, C slices (m - rows_0) n
+    m, n, k, world = 16384, 16384, 16384, 8
+    plan = P.rowblock_plan(m, n, k, world)
+    rows0 = P.split_rows(m, world)[0][1]
+    assert sum(e["count"] for e in plan if e["dir"] == "sent") == (m - rows0) * k
+    assert sum(e["count"] for e in plan if e["dir"] == "received") == (m - rows0) * n
+    with pytest.raises(P.DimensionError):
+        P.rowblock_plan(0, 4, 4, 2)
+
+
+def _compile_adapter(tmp_path):
+    exe = tmp_path / "test_adapter"
+    subprocess.run(["g++", "-std=c++20", "-O2", "-Wall", "-Wextra", "-Werror",
+                    f"-I{ROOT}/include", f"{ROOT}/tests/cpp/test_adapter.cpp", "-o", str(exe),
+                    f"-L{ROOT}/paper_1012_2273_b200", "-lmmws_gpu",
+                    f"-Wl,-rpath,{ROOT}/paper_1012_2273_b200"], check=True)
+    return exe
+
+
+def test_cpp_adapter_host_checks(tmp_path):
+    try:
+        import torch
+        gpu = torch.cuda.is_available()
+    except ImportError:
+        gpu = False
+    exe = _compile_adapter(tmp_path)
+    if gpu:
+        pytest.skip("host-only variant asserts that no GPU is present")
+    r = subprocess.run([str(exe), "cpu"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(REF_INC, "mmws", "matrix.hpp")),
+                    reason="reference headers not present (GPU box)")
+def test_cpp_adapter_is_dropin_for_reference_matrix():
+    subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Wextra", "-Werror",
+                    f"-I{REF_INC}", f"-I{ROOT}/include",
+                    f"{ROOT}/tests/cpp/ref_dropin_check.cpp"], check=True)
+
+
+@pytest.mark.gpu
+def test_cpp_adapter_gpu_checks(tmp_path):
+    exe = _compile_adapter(tmp_path)
+    r = subprocess.run([str(exe), "gpu"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr

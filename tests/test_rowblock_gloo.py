@@ -1,0 +1,98 @@
+"""Multi-process (gloo, CPU) test of the row-block master/worker host logic.
+
+The GPU engine (csrc/rowblock.cu) executes, on every rank, split_rows(m, P)
+and rank 0's message plan (mmws_gpu_rowblock_plan): A-slices out, one B
+broadcast, C-slices back into C's row blocks.  Only one GPU is available to
+this build, so the N > 1 path is exercised here with real processes: the same
+plan from the product library, the exchange over torch.distributed gloo, and
+the oracle's worker_block (protocol.hpp:132-141) standing in for the GPU
+kernel.  Mirrors the reference's msg-vs-seq matrix (acceptance.cpp:112-133,
+test_protocol.cpp:76-89): bitwise equal to matmul_seq, idle workers included.
+"""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _rank_main(rank, world, port, cases, failures):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import torch
+    import torch.distributed as dist
+
+    import oracle as O
+    import paper_1012_2273_b200 as P
+
+    dist.init_process_group("gloo", rank=rank, world_size=world,
+                            init_method=f"tcp://127.0.0.1:{port}")
+    try:
+        for (m, k, n, sa, sb) in cases:
+            parts = P.split_rows(m, world)
+            off, rows = parts[rank]
+            if rank == 0:
+                a = O.fill(O.DIST_UNIT, sa, m, k)
+                b = O.fill(O.DIST_UNIT, sb, k, n)
+                c = np.full((m, n), np.nan)
+                plan = P.rowblock_plan(m, n, k, world)
+                for e in plan:                       # tag 1: A-slices, then B
+                    if e["dir"] == "sent":
+                        o, r = parts[e["peer"]]
+                        assert e["count"] == r * k
+                        dist.send(torch.from_numpy(np.ascontiguousarray(a[o:o + r])), e["peer"])
+                    elif e["dir"] == "broadcast":
+                        assert e["count"] == k * n
+                        dist.broadcast(torch.from_numpy(b), 0)
+                if world > 1 and not any(e["dir"] == "broadcast" for e in plan):
+                    raise AssertionError("plan without B broadcast")
+                c[off:off + rows] = O.worker_block(a[off:off + rows], b) if rows else c[0:0]
+                for e in plan:                       # tag 2: C-slices, rank order
+                    if e["dir"] == "received":
+                        o, r = parts[e["peer"]]
+                        buf = torch.empty((r, n), dtype=torch.float64)
+                        dist.recv(buf, e["peer"])
+                        c[o:o + r] = buf.numpy()
+                want = O.matmul_seq(a, b)
+                if O.first_difference(c, want) is not None:
+                    failures.append(f"m={m} k={k} n={n} world={world}")
+            else:
+                a_slice = torch.empty((rows, k), dtype=torch.float64)
+                if rows:
+                    dist.recv(a_slice, 0)
+                b = torch.empty((k, n), dtype=torch.float64)
+                dist.broadcast(b, 0)
+                if rows:
+                    c_slice = O.worker_block(a_slice.numpy(), b.numpy())
+                    dist.send(torch.from_numpy(c_slice), 0)
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, cases):
+    import torch.multiprocessing as mp
+    mgr = mp.Manager()
+    failures = mgr.list()
+    port = _free_port()
+    mp.spawn(_rank_main, args=(world, port, cases, failures), nprocs=world, join=True)
+    return list(failures)
+
+
+ACCEPT = [(n, n, n, 3000 + n, 4000 + n) for n in (1, 2, 3, 4, 8, 16, 33)]
+RECT = [(5, 7, 4, 31, 32), (2, 2, 2, 61, 62), (513, 67, 129, 7, 8)]
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_rowblock_gloo_bitwise_equals_seq(world):
+    assert _run(world, ACCEPT + RECT) == []
