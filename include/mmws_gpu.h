@@ -86,7 +86,8 @@ enum {
   MMWS_GPU_PROBE_DMMA = 0,
   MMWS_GPU_PROBE_DFMA = 1,
   MMWS_GPU_PROBE_DMUL_DADD = 2,
-  MMWS_GPU_PROBE_FFMA = 3
+  MMWS_GPU_PROBE_FFMA = 3,
+  MMWS_GPU_PROBE_FFMA2 = 4
 };
 
 typedef struct mmws_gpu_ctx mmws_gpu_ctx;

@@ -6,6 +6,7 @@
 
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "kernels.h"
 
@@ -13,7 +14,9 @@ struct mmws_gpu_ctx {
   int device = 0;
   int num_sms = 0;
   int cc_major = 0, cc_minor = 0, clock_khz = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;                       // compute
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;  // host-entry PCIe copies
+  std::vector<cudaEvent_t> pool;                       // host-pipeline ordering events
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t evk0 = nullptr, evk1 = nullptr;  // around the row-block multiply
   double last_kernel_ms = 0.0;
@@ -62,6 +65,10 @@ cudaError_t ensure(void** buf, size_t* have, size_t bytes);
 int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
                    int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int mode,
                    cudaStream_t stream);
+// Host-buffer multiply with PCIe copies overlapped (host_pipeline.cu).
+template <class T>
+int host_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, const T* B,
+                  T* C, int mode, double* elapsed_s);
 int sgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const float* A,
                    int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int mode,
                    cudaStream_t stream);

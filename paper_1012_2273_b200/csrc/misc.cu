@@ -61,7 +61,7 @@ __global__ void pack_f64_kernel(const double* __restrict__ src, int64_t rows, in
 }
 
 // ---------------------------------------------------------------- peak probes
-// 0: DMMA.8x8x4 (FP64 tensor)  1: DFMA  2: DMUL+DADD  3: FFMA (fp32)
+// 0: DMMA.8x8x4 (FP64 tensor)  1: DFMA  2: DMUL+DADD  3: FFMA (fp32)  4: FFMA2 (fp32x2)
 template <int WHICH>
 __global__ void __launch_bounds__(256) probe_kernel(int iters, double* sink) {
   const double x = 1.0 + threadIdx.x * 1e-9, y = 1.0 - threadIdx.x * 1e-9;
@@ -88,6 +88,21 @@ __global__ void __launch_bounds__(256) probe_kernel(int iters, double* sink) {
 #pragma unroll
     for (int c = 0; c < 8; ++c) s += d[c];
     if (s == 12345.0) sink[threadIdx.x] = s;
+  } else if (WHICH == 4) {
+    unsigned long long d[8];
+    const float xf = static_cast<float>(x), yf = static_cast<float>(y);
+    unsigned long long xx, yy;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(xx) : "f"(xf));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(yy) : "f"(yf));
+#pragma unroll
+    for (int c = 0; c < 8; ++c) d[c] = static_cast<unsigned long long>(c);
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) asm volatile("fma.rn.f32x2 %0, %1, %0, %2;" : "+l"(d[c]) : "l"(xx), "l"(yy));
+    unsigned long long s = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) s ^= d[c];
+    if (s == 12345ull) sink[threadIdx.x] = static_cast<double>(s);
   } else {
     float d[16];
     const float xf = static_cast<float>(x), yf = static_cast<float>(y);
@@ -145,9 +160,13 @@ cudaError_t launch_peak_probe(const Launch& L, int which, int iters, double* sin
       probe_kernel<2><<<blocks, threads, 0, L.stream>>>(iters, sink);
       *flops = thr * 8.0 * iters * 2.0;
       break;
-    default:
+    case 3:
       probe_kernel<3><<<blocks, threads, 0, L.stream>>>(iters, sink);
       *flops = thr * 16.0 * iters * 2.0;
+      break;
+    default:
+      probe_kernel<4><<<blocks, threads, 0, L.stream>>>(iters, sink);
+      *flops = thr * 8.0 * iters * 4.0;  // 8 chains x 2 lanes x 2 flops
       break;
   }
   L.count();

@@ -137,46 +137,6 @@ struct mmws_gpu_graph {
   if (cudaError_t e_ = cudaSetDevice((ctx)->device); e_ != cudaSuccess)      \
     return cuda_fail(e_, "cudaSetDevice");
 
-namespace {
-template <class T>
-int matmul_host_impl(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, const T* B,
-                     T* C, int mode, double* elapsed_s) {
-  if (m <= 0 || n <= 0 || k <= 0)
-    return fail(MMWS_GPU_ERR_DIMENSION, "matmul: dimensions must be positive");
-  if (!A || !B || !C) return fail(MMWS_GPU_ERR_DOMAIN, "matmul: null host pointer");
-  const size_t a_b = sizeof(T) * m * k, b_b = sizeof(T) * k * n, c_b = sizeof(T) * m * n;
-  cudaError_t e;
-  if ((e = ensure(&ctx->dA, &ctx->dA_bytes, a_b)) != cudaSuccess ||
-      (e = ensure(&ctx->dB, &ctx->dB_bytes, b_b)) != cudaSuccess ||
-      (e = ensure(&ctx->dC, &ctx->dC_bytes, c_b)) != cudaSuccess)
-    return cuda_fail(e, "matmul_host: device buffers");
-  cudaStream_t s = ctx->stream;
-  cudaEventRecord(ctx->ev0, s);
-  if ((e = cudaMemcpyAsync(ctx->dA, A, a_b, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
-      (e = cudaMemcpyAsync(ctx->dB, B, b_b, cudaMemcpyHostToDevice, s)) != cudaSuccess)
-    return cuda_fail(e, "matmul_host: H2D");
-  int rc;
-  if constexpr (sizeof(T) == 8)
-    rc = dgemm_dispatch(ctx, m, n, k, static_cast<const double*>(ctx->dA), k,
-                        static_cast<const double*>(ctx->dB), n, static_cast<double*>(ctx->dC), n,
-                        mode, s);
-  else
-    rc = sgemm_dispatch(ctx, m, n, k, static_cast<const float*>(ctx->dA), k,
-                        static_cast<const float*>(ctx->dB), n, static_cast<float*>(ctx->dC), n,
-                        mode, s);
-  if (rc) return rc;
-  if ((e = cudaMemcpyAsync(C, ctx->dC, c_b, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-    return cuda_fail(e, "matmul_host: D2H");
-  cudaEventRecord(ctx->ev1, s);
-  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "matmul_host: sync");
-  if (elapsed_s) {
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
-    *elapsed_s = ms * 1e-3;
-  }
-  return ok();
-}
-}  // namespace
 
 extern "C" {
 
@@ -220,6 +180,8 @@ int mmws_gpu_init(int device, mmws_gpu_ctx** out) {
   ctx->encode = reinterpret_cast<EncodeTiledFn>(fn);
   if ((e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaEventCreate(&ctx->ev0)) != cudaSuccess ||
       (e = cudaEventCreate(&ctx->ev1)) != cudaSuccess ||
       (e = cudaEventCreate(&ctx->evk0)) != cudaSuccess ||
@@ -246,6 +208,9 @@ int mmws_gpu_destroy(mmws_gpu_ctx* ctx) {
   if (ctx->evk1) cudaEventDestroy(ctx->evk1);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+  if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
+  if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
+  for (cudaEvent_t ev : ctx->pool) cudaEventDestroy(ev);
   delete ctx;
   return ok();
 }
@@ -326,14 +291,14 @@ int mmws_gpu_sgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const flo
 int mmws_gpu_matmul_host(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
                          const double* B, double* C, int mode, double* elapsed_s) {
   MMWS_CTX_GUARD(ctx);
-  return matmul_host_impl(ctx, m, n, k, A, B, C, mode, elapsed_s);
+  return host_multiply(ctx, m, n, k, A, B, C, mode, elapsed_s);
 }
 
 int mmws_gpu_matmul_host_f32(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k,
                              const float* A, const float* B, float* C, int mode,
                              double* elapsed_s) {
   MMWS_CTX_GUARD(ctx);
-  return matmul_host_impl(ctx, m, n, k, A, B, C, mode, elapsed_s);
+  return host_multiply(ctx, m, n, k, A, B, C, mode, elapsed_s);
 }
 
 // ------------------------------------------------------------------ generators
@@ -413,7 +378,7 @@ int mmws_gpu_graph_destroy(mmws_gpu_graph* g) {
 // ------------------------------------------------------------------ measurement
 int mmws_gpu_peak_probe(mmws_gpu_ctx* ctx, int which, int iters, double* tflops) {
   MMWS_CTX_GUARD(ctx);
-  if (which < 0 || which > 3 || iters < 1 || !tflops)
+  if (which < 0 || which > 4 || iters < 1 || !tflops)
     return fail(MMWS_GPU_ERR_DOMAIN, "peak_probe: bad arguments");
   const Launch L = ctx->launch(nullptr);
   double flops = 0;

@@ -157,6 +157,8 @@ int master_run_host(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T*
   if (!root) return rowblock(ctx, m, n, k, static_cast<const T*>(nullptr),
                              static_cast<const T*>(nullptr), static_cast<T*>(nullptr), mode,
                              elapsed_s);
+  if (!ctx->comm || ctx->nranks == 1)  // one GPU: copies overlapped with the multiply
+    return host_multiply(ctx, m, n, k, A, B, C, mode, elapsed_s);
   if (m <= 0 || n <= 0 || k <= 0)
     return fail(MMWS_GPU_ERR_DIMENSION, "master_run: dimensions must be positive");
   if (!A || !B || !C) return fail(MMWS_GPU_ERR_DOMAIN, "master_run: null host matrix");

@@ -7,8 +7,9 @@
 //
 // 128x128 CTA tile, 256 threads, 8x8 outputs per thread (rows 4*ty + 64v + h,
 // cols 4*tx + 64v + h so fragment fetches are 128-bit broadcast / conflict-free
-// LDS), A staged k-major (transposed) in shared memory, global->register->
-// shared double buffering over 8-wide k-tiles.
+// LDS) held as packed fp32 pairs and updated with FFMA2 (the a-value is the
+// broadcast operand), A staged k-major (transposed) in shared memory,
+// global->register->shared double buffering over 8-wide k-tiles.
 //
 // Accuracy: a single fp32 chain over K = 32768 terms has an expected normwise
 // error of ~5e-6, uncomfortably close to the 1e-5 bound.  The
@@ -18,6 +19,27 @@
 // ~sqrt(KC) + sqrt(K / KC) for one extra FADD per KC FFMAs.
 #include "common.cuh"
 #include "kernels.h"
+
+// Packed fp32 pairs (Blackwell FFMA2 / FADD2): one instruction does two
+// multiply-adds, halving issue pressure; ptxas folds a {x, x} pair of a scalar
+// into the instruction's broadcast operand (no MOV).
+#define MMWS_F2 unsigned long long
+__device__ __forceinline__ MMWS_F2 pack2(float lo, float hi) {
+  MMWS_F2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 unpack2(MMWS_F2 v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ void ffma2(MMWS_F2& d, MMWS_F2 a, MMWS_F2 b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ void fadd2(MMWS_F2& d, MMWS_F2 a) {
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(d) : "l"(a));
+}
 
 namespace mmws_impl {
 namespace {
@@ -77,11 +99,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     *reinterpret_cast<float4*>(&Bs[buf][b_k][b_c]) = make_float4(rb[0], rb[1], rb[2], rb[3]);
   };
 
-  float acc[8][8], part[8][8];
+  // acc[i][p] holds columns (2p, 2p+1) of row i of the thread's 8x8 block
+  MMWS_F2 acc[8][4], part[8][4];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = part[i][j] = 0.f;
+    for (int p = 0; p < 4; ++p) acc[i][p] = part[i][p] = 0ull;
 
   const int KT = (K + BK - 1) / BK;
   load_tile(0);
@@ -93,27 +116,29 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (kt + 1 < KT) load_tile(kt + 1);
 #pragma unroll
     for (int k = 0; k < BK; ++k) {
-      float a[8], b[8];
+      float a[8];
       const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][k][ty * 4]);
       const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][k][ty * 4 + 64]);
       const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][k][tx * 4]);
       const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][k][tx * 4 + 64]);
       a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
       a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
-      b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
-      b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+      const MMWS_F2 b2[4] = {pack2(b0.x, b0.y), pack2(b0.z, b0.w), pack2(b1.x, b1.y),
+                             pack2(b1.z, b1.w)};
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < 8; ++i) {
+        const MMWS_F2 aa = pack2(a[i], a[i]);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) part[i][j] = fmaf(a[i], b[j], part[i][j]);
+        for (int p = 0; p < 4; ++p) ffma2(part[i][p], aa, b2[p]);
+      }
     }
     if ((kt % KC_TILES) == KC_TILES - 1 || kt + 1 == KT) {
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          acc[i][j] += part[i][j];
-          part[i][j] = 0.f;
+        for (int p = 0; p < 4; ++p) {
+          fadd2(acc[i][p], part[i][p]);
+          part[i][p] = 0ull;
         }
     }
     if (kt + 1 < KT) store_tile(buf ^ 1);
@@ -128,13 +153,14 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int c = col0 + tx * 4 + 64 * h;
+      const float2 lo = unpack2(acc[i][2 * h]), hi = unpack2(acc[i][2 * h + 1]);
+      const float v[4] = {lo.x, lo.y, hi.x, hi.y};
       if (vec_c && c + 3 < N) {
-        *reinterpret_cast<float4*>(crow + c) =
-            make_float4(acc[i][4 * h], acc[i][4 * h + 1], acc[i][4 * h + 2], acc[i][4 * h + 3]);
+        *reinterpret_cast<float4*>(crow + c) = make_float4(v[0], v[1], v[2], v[3]);
       } else {
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          if (c + j < N) crow[c + j] = acc[i][4 * h + j];
+          if (c + j < N) crow[c + j] = v[j];
       }
     }
   }

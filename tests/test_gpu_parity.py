@@ -266,6 +266,29 @@ def test_host_entry_matches_device_entry(ctx, oracle):
     assert normwise(cf.astype(np.float64), oracle.matmul_rows(list(range(257)), af, bf)) <= FP32_TOL
 
 
+@pytest.mark.parametrize("shape", [(1301, 1299, 1303), (2048, 1024, 4096)])
+def test_host_pipeline_bitwise_equals_device(ctx, oracle, shape):
+    # big enough to take the overlapped (row-panel x column-block) host path
+    T = torch()
+    m, k, n = shape
+    a = oracle.fill(oracle.DIST_UNIFORM, 21, m, k)
+    b = oracle.fill(oracle.DIST_UNIFORM, 22, k, n)
+    ap = T.from_numpy(a).pin_memory().numpy()
+    bp = T.from_numpy(b).pin_memory().numpy()
+    for mode in (P.MODE_AUTO, P.MODE_EXACT):
+        want = host(ctx.dgemm(dev(a), dev(b), mode=mode))
+        for (x, y) in ((a, b), (ap, bp)):
+            c, el = ctx.matmul_host(x, y, mode=mode)
+            assert el > 0 and (bits(c) == bits(want)).all()
+        c, el = ctx.master_run_host(ap, bp, mode=mode)
+        assert (bits(c) == bits(want)).all()
+    rows = [0, m // 2, m - 1]
+    assert oracle.first_difference(c[rows], oracle.matmul_rows(rows, a, b)) is None
+    af, bf = a.astype(np.float32), b.astype(np.float32)
+    cf, _ = ctx.matmul_host(af, bf)
+    assert (cf == host(ctx.sgemm(dev(af), dev(bf)))).all()
+
+
 def test_strided_views_and_unaligned_leading_dims(ctx, oracle):
     T = torch()
     big_a = ctx.fill(P.DIST_UNIFORM, 7, 300, 301)
@@ -321,6 +344,6 @@ def test_launch_accounting(ctx):
 
 
 def test_peak_probes_run(ctx):
-    for which in (P.PROBE_DMMA, P.PROBE_DFMA, P.PROBE_DMUL_DADD, P.PROBE_FFMA):
+    for which in (P.PROBE_DMMA, P.PROBE_DFMA, P.PROBE_DMUL_DADD, P.PROBE_FFMA, P.PROBE_FFMA2):
         tf = ctx.peak_probe(which, 256)
         assert 0.5 < tf < 200, (which, tf)

@@ -28,7 +28,7 @@ def main():
     ctx = P.Context(0)
     out = {"num_sms": ctx.num_sms, "max_clock_khz": ctx.max_clock_khz}
     for name, w in [("dmma", P.PROBE_DMMA), ("dfma", P.PROBE_DFMA), ("dmul_dadd", P.PROBE_DMUL_DADD),
-                    ("ffma", P.PROBE_FFMA)]:
+                    ("ffma", P.PROBE_FFMA), ("ffma2", P.PROBE_FFMA2)]:
         out["probe_" + name] = [ctx.peak_probe(w, 20000) for _ in range(3)]
     print(json.dumps(out), flush=True)
     sizes = [int(x) for x in (sys.argv[1:] or ["16384"])]

@@ -1,0 +1,28 @@
+"""One launch of each kernel family (for ncu -k regex:... captures)."""
+import sys
+import torch
+sys.path.insert(0, ".")
+import paper_1012_2273_b200 as P
+
+ctx = P.Context(0)
+which = sys.argv[1] if len(sys.argv) > 1 else "all"
+if which in ("all", "ffma"):
+    n = 8192
+    A = ctx.fill(P.DIST_NORMAL, 0, n, n, dtype=torch.float32)
+    B = ctx.fill(P.DIST_NORMAL, 1, n, n, dtype=torch.float32)
+    for _ in range(2):
+        ctx.sgemm(A, B)
+if which in ("all", "exact"):
+    n = 4096
+    A = ctx.fill(P.DIST_UNIFORM, 0, n, n)
+    B = ctx.fill(P.DIST_UNIFORM, 1, n, n)
+    for _ in range(2):
+        ctx.dgemm(A, B, mode=P.MODE_EXACT)
+if which in ("all", "small"):
+    n = 1000
+    A = ctx.fill(P.DIST_UNIFORM, 0, n, n)
+    B = ctx.fill(P.DIST_UNIFORM, 1, n, n)
+    for _ in range(2):
+        ctx.dgemm(A, B, mode=P.MODE_AUTO)
+torch.cuda.synchronize()
+print("ok")
