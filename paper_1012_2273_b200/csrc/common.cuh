@@ -105,3 +105,38 @@ MMWS_DEVICE void dmma_8x8x4(double& d0, double& d1, double a, double b) {
 
 
 }  // namespace mmws_dev
+
+namespace mmws_dev {
+
+// cp.async copy of a ROWS x COLS tile of a row-major matrix g (leading
+// dimension ld) starting at (row0, col0) into shared memory s (row pitch SLD
+// elements).  Elements outside [0, nrows) x [0, ncols) are zero-filled.
+// VEC: 16-byte chunks -- requires a 16-byte aligned base, ld and ncols that
+// are multiples of the chunk, so a chunk is either wholly inside or wholly
+// outside the matrix.  !VEC: element-sized copies (any alignment).  Every
+// thread of the CTA must call it.
+template <typename T, int ROWS, int COLS, int SLD, int THREADS, bool VEC>
+MMWS_DEVICE void load_tile_async(T* s, const T* __restrict__ g, int64_t ld, int row0, int col0,
+                                 int nrows, int ncols) {
+  constexpr int CH = VEC ? 16 / sizeof(T) : 1;  // elements per copy
+  static_assert(COLS % CH == 0, "tile width must be a whole number of chunks");
+  constexpr int CPR = COLS / CH;
+  constexpr int TOTAL = ROWS * CPR;
+#pragma unroll
+  for (int it = 0; it < (TOTAL + THREADS - 1) / THREADS; ++it) {
+    const int i = it * THREADS + threadIdx.x;
+    if (TOTAL % THREADS != 0 && i >= TOTAL) break;
+    const int r = i / CPR, c = (i % CPR) * CH;
+    const int gr = row0 + r, gc = col0 + c;
+    const bool ok = gr < nrows && gc < ncols;
+    const T* src = ok ? g + static_cast<int64_t>(gr) * ld + gc : g;
+    if constexpr (VEC)
+      cp_async_16(s + r * SLD + c, src, ok);
+    else if constexpr (sizeof(T) == 8)
+      cp_async_8(s + r * SLD + c, src, ok);
+    else
+      cp_async_4(s + r * SLD + c, src, ok);
+  }
+}
+
+}  // namespace mmws_dev

@@ -5,66 +5,58 @@
 //     acc = +0.0;  for j = 0 .. K-1 ascending:  acc = RN(acc + RN(a(i,j)*b(j,k)))
 // This kernel keeps exactly that chain per thread-owned element: DMUL then
 // DADD (__dmul_rn / __dadd_rn are never contracted into DFMA), k ascending
-// through the smem k-tiles, accumulator initialised to +0.0 and stored as is.
-// Out-of-range k is zero-filled in BOTH operands, which appends (+0)*(+0) = +0
-// terms; acc is never -0 (it starts at +0 and RN(x + -x) = +0), so acc + +0 ==
-// acc bit-for-bit.  Hence C is bitwise matmul_seq(A, B) for every input
-// without NaNs (NaN payload propagation is hardware-specific on both sides).
+// through the shared-memory k-tiles, accumulator initialised to +0.0 and
+// stored as is.  Out-of-range k is zero-filled in BOTH operands, which appends
+// (+0)*(+0) = +0 terms; acc is never -0 (it starts at +0 and RN(x + -x) = +0),
+// so acc + +0 == acc bit-for-bit.  Hence C is bitwise matmul_seq(A, B) for
+// every input without NaNs (NaN payload propagation is hardware-specific on
+// both sides).
 //
 // Layout: 128x128 CTA tile, 256 threads, 8x8 register block per thread with
-// rows {2*ty + 32v + h} and cols {2*tx + 32v + h} (v < 4, h < 2) so every
-// fragment fetch is a conflict-free / broadcast 128-bit LDS; A is staged
-// transposed (k-major) in shared memory, B as is; global->register->shared
-// double buffering over 8-wide k-tiles.  Bound: FP64 pipe at one DMUL + one
-// DADD per multiply-add, i.e. half of the DFMA peak.
+// rows {2*ty + 32v + h} and cols {2*tx + 32v + h} (v < 4, h < 2).  A and B
+// k-tiles (16 wide) stream through a 3-stage cp.async ring in their natural
+// row-major layout; a lane fetches A as (k, k+1) pairs of one row (broadcast
+// LDS.128) and B as column pairs (conflict-free LDS.128).  Bound: FP64 pipe
+// at one DMUL + one DADD per multiply-add, i.e. half of the DFMA peak.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace mmws_impl {
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 8, THREADS = 256;
-constexpr int AV = BM * BK / THREADS;  // A elements staged per thread (4)
-constexpr int BV = BN * BK / THREADS;  // B elements staged per thread (4)
-constexpr int LDA_S = BM + 2;  // padded k-major A rows (keeps 16-byte alignment)
+using namespace mmws_dev;
 
+constexpr int BM = 128, BN = 128, BK = 16, THREADS = 256, STAGES = 3;
+constexpr int SLA = BK + 2;   // A row pitch (doubles): keeps 16-byte alignment, spreads banks
+constexpr int SLB = BN;       // B row pitch
+constexpr int A_ELEMS = BM * SLA, B_ELEMS = BK * SLB;
+constexpr int SMEM = STAGES * (A_ELEMS + B_ELEMS) * sizeof(double);
+
+template <bool VA, bool VB>
 __global__ void __launch_bounds__(THREADS, 1)
     dgemm_exact_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
                        int64_t ldb, double* __restrict__ C, int64_t ldc, int M, int N, int K,
-                       int tiles_n) {
-  __shared__ __align__(16) double As[2][BK][LDA_S];
-  __shared__ __align__(16) double Bs[2][BK][BN];
+                       int tiles_m, int tiles_n) {
+  extern __shared__ __align__(16) double smem_d[];
+  double* As = smem_d;                       // [STAGES][BM][SLA]
+  double* Bs = smem_d + STAGES * A_ELEMS;    // [STAGES][BK][SLB]
 
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
-  const int tm = blockIdx.x / tiles_n, tn = blockIdx.x % tiles_n;
+  constexpr int GROUP = 8;
+  const int tile = blockIdx.x;
+  const int per_group = GROUP * tiles_n;
+  const int first_m = (tile / per_group) * GROUP;
+  const int gm = min(tiles_m - first_m, GROUP);
+  const int tm = first_m + (tile % per_group) % gm;
+  const int tn = (tile % per_group) / gm;
   const int row0 = tm * BM, col0 = tn * BN;
+  const int KT = (K + BK - 1) / BK;
 
-  // global staging coordinates
-  const int a_r = tid / (BK / AV), a_k = (tid % (BK / AV)) * AV;  // A: row a_r, k a_k..+AV
-  const int b_k = tid / (BN / BV), b_c = (tid % (BN / BV)) * BV;  // B: k-row b_k, cols b_c..+BV
-  const bool a_row_ok = row0 + a_r < M;
-  const double* a_src = A + static_cast<int64_t>(row0 + a_r) * lda;
-
-  double ra[AV], rb[BV];
-  auto load_tile = [&](int kt) {
-    const int k0 = kt * BK;
-#pragma unroll
-    for (int j = 0; j < AV; ++j) {
-      const int k = k0 + a_k + j;
-      ra[j] = (a_row_ok && k < K) ? a_src[k] : 0.0;
-    }
-    const int kb = k0 + b_k;
-    const double* b_src = B + static_cast<int64_t>(kb) * ldb + col0 + b_c;
-#pragma unroll
-    for (int j = 0; j < BV; ++j) rb[j] = (kb < K && col0 + b_c + j < N) ? b_src[j] : 0.0;
-  };
-  auto store_tile = [&](int buf) {
-#pragma unroll
-    for (int j = 0; j < AV; ++j) As[buf][a_k + j][a_r] = ra[j];
-#pragma unroll
-    for (int j = 0; j < BV; j += 2)
-      *reinterpret_cast<double2*>(&Bs[buf][b_k][b_c + j]) = make_double2(rb[j], rb[j + 1]);
+  auto load_stage = [&](int kt) {
+    const int s = kt % STAGES;
+    load_tile_async<double, BM, BK, SLA, THREADS, VA>(As + s * A_ELEMS, A, lda, row0, kt * BK, M, K);
+    load_tile_async<double, BK, BN, SLB, THREADS, VB>(Bs + s * B_ELEMS, B, ldb, kt * BK, col0, K, N);
   };
 
   double acc[8][8];
@@ -73,33 +65,42 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
 
-  const int KT = (K + BK - 1) / BK;
-  load_tile(0);
-  store_tile(0);
-  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_stage(s);
+    cp_async_commit();
+  }
 
   for (int kt = 0; kt < KT; ++kt) {
-    const int buf = kt & 1;
-    if (kt + 1 < KT) load_tile(kt + 1);
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();  // stage kt landed for everyone; stage kt-1 fully consumed
+    if (kt + STAGES - 1 < KT) load_stage(kt + STAGES - 1);
+    cp_async_commit();
+    const double* as = As + (kt % STAGES) * A_ELEMS;
+    const double* bs = Bs + (kt % STAGES) * B_ELEMS;
 #pragma unroll
-    for (int k = 0; k < BK; ++k) {
-      double a[8], b[8];
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const double2 av = *reinterpret_cast<const double2*>(&As[buf][k][ty * 2 + 32 * v]);
-        const double2 bv = *reinterpret_cast<const double2*>(&Bs[buf][k][tx * 2 + 32 * v]);
-        a[2 * v] = av.x;
-        a[2 * v + 1] = av.y;
-        b[2 * v] = bv.x;
-        b[2 * v + 1] = bv.y;
-      }
+    for (int k = 0; k < BK; k += 2) {
+      double2 a2[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i)
+        a2[i] = *reinterpret_cast<const double2*>(as + (ty * 2 + 32 * (i >> 1) + (i & 1)) * SLA + k);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(a[i], b[j]));
+      for (int kk = 0; kk < 2; ++kk) {
+        double b[8];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const double2 bv = *reinterpret_cast<const double2*>(bs + (k + kk) * SLB + tx * 2 + 32 * v);
+          b[2 * v] = bv.x;
+          b[2 * v + 1] = bv.y;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const double a = kk ? a2[i].y : a2[i].x;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(a, b[j]));
+        }
+      }
     }
-    if (kt + 1 < KT) store_tile(buf ^ 1);
-    __syncthreads();
   }
 
 #pragma unroll
@@ -122,9 +123,16 @@ cudaError_t launch_dgemm_exact(const Launch& L, int64_t M, int64_t N, int64_t K,
                                int64_t ldc) {
   const int tiles_m = static_cast<int>((M + BM - 1) / BM);
   const int tiles_n = static_cast<int>((N + BN - 1) / BN);
-  dgemm_exact_kernel<<<tiles_m * tiles_n, THREADS, 0, L.stream>>>(
-      A, lda, B, ldb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K),
-      tiles_n);
+  // 16-byte cp.async when a whole chunk is always in or out of the matrix
+  const bool va = lda % 2 == 0 && K % 2 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0;
+  const bool vb = ldb % 2 == 0 && N % 2 == 0 && reinterpret_cast<uintptr_t>(B) % 16 == 0;
+  auto kern = va ? (vb ? dgemm_exact_kernel<true, true> : dgemm_exact_kernel<true, false>)
+                 : (vb ? dgemm_exact_kernel<false, true> : dgemm_exact_kernel<false, false>);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  if (e != cudaSuccess) return e;
+  kern<<<tiles_m * tiles_n, THREADS, SMEM, L.stream>>>(A, lda, B, ldb, C, ldc,
+                                                       static_cast<int>(M), static_cast<int>(N),
+                                                       static_cast<int>(K), tiles_m, tiles_n);
   L.count();
   return cudaGetLastError();
 }

@@ -5,55 +5,64 @@
 // this is the same C = A.B contraction in fp32, checked normwise against the
 // fp64 oracle of the widened inputs (tolerance 1e-5, tests/test_gpu_parity.py).
 //
-// 128x128 CTA tile, 256 threads, 8x8 outputs per thread (rows 4*ty + 64v + h,
-// cols 4*tx + 64v + h so fragment fetches are 128-bit broadcast / conflict-free
-// LDS) held as packed fp32 pairs and updated with FFMA2 (the a-value is the
-// broadcast operand), A staged k-major (transposed) in shared memory,
-// global->register->shared double buffering over 8-wide k-tiles.
+// 192x128 CTA tile, 384 threads (12 warps, 1 CTA/SM, <= 168 registers each),
+// 8x8 outputs per thread (rows 4*ty + 96v + h, cols 4*tx + 64v + h) held as
+// packed fp32 pairs and updated with Blackwell's FFMA2 (two multiply-adds per
+// instruction; the A value is the instruction's broadcast operand).  A and B
+// k-tiles (16 wide) stream through a 3-stage cp.async ring in natural layout;
+// a lane fetches A as (k, k+1) pairs of one row (broadcast LDS.64) and B as
+// 4-column vectors (conflict-free LDS.128).
 //
 // Accuracy: a single fp32 chain over K = 32768 terms has an expected normwise
 // error of ~5e-6, uncomfortably close to the 1e-5 bound.  The
-// kernel therefore sums each KC-long k-chunk into a fresh partial and adds the
-// partial into the running total once per chunk (two-level / blocked
-// summation), which shrinks the error growth from ~sqrt(K) to
-// ~sqrt(KC) + sqrt(K / KC) for one extra FADD per KC FFMAs.
+// kernel therefore sums each KC-long k-chunk into a fresh register partial and
+// adds the partial into a running total kept in shared memory (96 KB: 64
+// floats per thread) once per chunk -- two-level (blocked) summation, error
+// growth ~sqrt(KC) + sqrt(K / KC) instead of ~sqrt(K), for ~1% extra
+// instructions and without doubling the accumulator registers.
 #include "common.cuh"
 #include "kernels.h"
-
-// Packed fp32 pairs (Blackwell FFMA2 / FADD2): one instruction does two
-// multiply-adds, halving issue pressure; ptxas folds a {x, x} pair of a scalar
-// into the instruction's broadcast operand (no MOV).
-#define MMWS_F2 unsigned long long
-__device__ __forceinline__ MMWS_F2 pack2(float lo, float hi) {
-  MMWS_F2 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-__device__ __forceinline__ float2 unpack2(MMWS_F2 v) {
-  float2 r;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
-  return r;
-}
-__device__ __forceinline__ void ffma2(MMWS_F2& d, MMWS_F2 a, MMWS_F2 b) {
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
-}
-__device__ __forceinline__ void fadd2(MMWS_F2& d, MMWS_F2 a) {
-  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(d) : "l"(a));
-}
 
 namespace mmws_impl {
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 8, THREADS = 256;
-constexpr int KC_TILES = 16;  // partial-sum chunk = 16 k-tiles = 128 k
-constexpr int LDA_S = BM + 4;
+using namespace mmws_dev;
 
+// Packed fp32 pairs (FFMA2): ptxas folds a {x, x} pair of a scalar into the
+// instruction's broadcast operand, so no MOV is emitted.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pack2(float lo, float hi) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 unpack2(f32x2 v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ void ffma2(f32x2& d, f32x2 a, f32x2 b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+}
+
+constexpr int BM = 192, BN = 128, BK = 16, THREADS = 384, STAGES = 3;
+constexpr int RSTEP = BM / 2;  // row stride between a thread's two 4-row groups
+constexpr int KC_TILES = 16;  // partial-sum chunk = 16 k-tiles = 256 k
+constexpr int SLA = BK + 4;   // A row pitch (floats)
+constexpr int SLB = BN;       // B row pitch
+constexpr int A_ELEMS = BM * SLA, B_ELEMS = BK * SLB;
+constexpr int TOT_FLOATS = THREADS * 64;
+constexpr int SMEM = (STAGES * (A_ELEMS + B_ELEMS) + TOT_FLOATS) * sizeof(float);
+
+template <bool VA, bool VB>
 __global__ void __launch_bounds__(THREADS, 1)
     sgemm_ffma_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B,
                       int64_t ldb, float* __restrict__ C, int64_t ldc, int M, int N, int K,
-                      int tiles_m, int tiles_n, int vec_a, int vec_b, int vec_c) {
-  __shared__ __align__(16) float As[2][BK][LDA_S];
-  __shared__ __align__(16) float Bs[2][BK][BN];
+                      int tiles_m, int tiles_n, int vec_c) {
+  extern __shared__ __align__(16) float smem_f[];
+  float* As = smem_f;                               // [STAGES][BM][SLA]
+  float* Bs = smem_f + STAGES * A_ELEMS;            // [STAGES][BK][SLB]
+  float4* tot = reinterpret_cast<float4*>(Bs + STAGES * B_ELEMS);  // [16][THREADS]
 
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
@@ -66,102 +75,93 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int tm = first_m + (tile % per_group) % gm;
   const int tn = (tile % per_group) / gm;
   const int row0 = tm * BM, col0 = tn * BN;
+  const int KT = (K + BK - 1) / BK;
 
-  const int a_r = tid >> 1, a_k = (tid & 1) * 4;   // A: row a_r, k a_k .. a_k+3
-  const int b_k = tid >> 5, b_c = (tid & 31) * 4;  // B: k-row b_k, cols b_c .. b_c+3
-  const bool a_row_ok = row0 + a_r < M;
-  const float* a_src = A + static_cast<int64_t>(row0 + a_r) * lda;
-
-  float ra[4], rb[4];
-  auto load_tile = [&](int kt) {
-    const int k0 = kt * BK;
-    const int ka = k0 + a_k;
-    if (vec_a && a_row_ok && ka + 3 < K) {
-      const float4 v = *reinterpret_cast<const float4*>(a_src + ka);
-      ra[0] = v.x; ra[1] = v.y; ra[2] = v.z; ra[3] = v.w;
-    } else {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) ra[j] = (a_row_ok && ka + j < K) ? a_src[ka + j] : 0.f;
-    }
-    const int kb = k0 + b_k;
-    const float* b_src = B + static_cast<int64_t>(kb) * ldb + col0 + b_c;
-    if (vec_b && kb < K && col0 + b_c + 3 < N) {
-      const float4 v = *reinterpret_cast<const float4*>(b_src);
-      rb[0] = v.x; rb[1] = v.y; rb[2] = v.z; rb[3] = v.w;
-    } else {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) rb[j] = (kb < K && col0 + b_c + j < N) ? b_src[j] : 0.f;
-    }
-  };
-  auto store_tile = [&](int buf) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) As[buf][a_k + j][a_r] = ra[j];
-    *reinterpret_cast<float4*>(&Bs[buf][b_k][b_c]) = make_float4(rb[0], rb[1], rb[2], rb[3]);
+  auto load_stage = [&](int kt) {
+    const int s = kt % STAGES;
+    load_tile_async<float, BM, BK, SLA, THREADS, VA>(As + s * A_ELEMS, A, lda, row0, kt * BK, M, K);
+    load_tile_async<float, BK, BN, SLB, THREADS, VB>(Bs + s * B_ELEMS, B, ldb, kt * BK, col0, K, N);
   };
 
-  // acc[i][p] holds columns (2p, 2p+1) of row i of the thread's 8x8 block
-  MMWS_F2 acc[8][4], part[8][4];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) tot[q * THREADS + tid] = make_float4(0.f, 0.f, 0.f, 0.f);
+
+  // part[i][p]: columns (2p, 2p+1) of row i of the thread's 8x8 block
+  f32x2 part[8][4];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int p = 0; p < 4; ++p) acc[i][p] = part[i][p] = 0ull;
+    for (int p = 0; p < 4; ++p) part[i][p] = 0ull;
 
-  const int KT = (K + BK - 1) / BK;
-  load_tile(0);
-  store_tile(0);
-  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_stage(s);
+    cp_async_commit();
+  }
 
   for (int kt = 0; kt < KT; ++kt) {
-    const int buf = kt & 1;
-    if (kt + 1 < KT) load_tile(kt + 1);
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    if (kt + STAGES - 1 < KT) load_stage(kt + STAGES - 1);
+    cp_async_commit();
+    const float* as = As + (kt % STAGES) * A_ELEMS;
+    const float* bs = Bs + (kt % STAGES) * B_ELEMS;
 #pragma unroll
-    for (int k = 0; k < BK; ++k) {
-      float a[8];
-      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][k][ty * 4]);
-      const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][k][ty * 4 + 64]);
-      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][k][tx * 4]);
-      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][k][tx * 4 + 64]);
-      a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
-      a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
-      const MMWS_F2 b2[4] = {pack2(b0.x, b0.y), pack2(b0.z, b0.w), pack2(b1.x, b1.y),
+    for (int k = 0; k < BK; k += 2) {
+      float2 a2[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        a2[i] = *reinterpret_cast<const float2*>(as + (ty * 4 + RSTEP * (i >> 2) + (i & 3)) * SLA + k);
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const float4 b0 = *reinterpret_cast<const float4*>(bs + (k + kk) * SLB + tx * 4);
+        const float4 b1 = *reinterpret_cast<const float4*>(bs + (k + kk) * SLB + tx * 4 + 64);
+        const f32x2 b2[4] = {pack2(b0.x, b0.y), pack2(b0.z, b0.w), pack2(b1.x, b1.y),
                              pack2(b1.z, b1.w)};
+        // p outer / i inner: consecutive FFMA2s share the B pair (operand
+        // reuse cache), so each reads only the broadcast A value and the
+        // accumulator pair from the register file
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const MMWS_F2 aa = pack2(a[i], a[i]);
+        for (int p = 0; p < 4; ++p)
 #pragma unroll
-        for (int p = 0; p < 4; ++p) ffma2(part[i][p], aa, b2[p]);
+          for (int i = 0; i < 8; ++i) {
+            const float a = kk ? a2[i].y : a2[i].x;
+            ffma2(part[i][p], pack2(a, a), b2[p]);
+          }
       }
     }
     if ((kt % KC_TILES) == KC_TILES - 1 || kt + 1 == KT) {
+      // fold the chunk partial into the shared-memory running total
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int p = 0; p < 4; ++p) {
-          fadd2(acc[i][p], part[i][p]);
-          part[i][p] = 0ull;
-        }
+      for (int q = 0; q < 16; ++q) {
+        const int i = q >> 1, p = (q & 1) * 2;
+        float4 t = tot[q * THREADS + tid];
+        const float2 lo = unpack2(part[i][p]), hi = unpack2(part[i][p + 1]);
+        t.x += lo.x;
+        t.y += lo.y;
+        t.z += hi.x;
+        t.w += hi.y;
+        tot[q * THREADS + tid] = t;
+        part[i][p] = part[i][p + 1] = 0ull;
+      }
     }
-    if (kt + 1 < KT) store_tile(buf ^ 1);
-    __syncthreads();
   }
 
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int r = row0 + ty * 4 + 64 * (i >> 2) + (i & 3);
+  for (int q = 0; q < 16; ++q) {
+    const int i = q >> 1, h = q & 1;
+    const int r = row0 + ty * 4 + RSTEP * (i >> 2) + (i & 3);
     if (r >= M) continue;
+    const int c = col0 + tx * 4 + 64 * h;
+    const float4 v = tot[q * THREADS + tid];
     float* crow = C + static_cast<int64_t>(r) * ldc;
+    if (vec_c && c + 3 < N) {
+      *reinterpret_cast<float4*>(crow + c) = v;
+    } else {
+      const float w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int c = col0 + tx * 4 + 64 * h;
-      const float2 lo = unpack2(acc[i][2 * h]), hi = unpack2(acc[i][2 * h + 1]);
-      const float v[4] = {lo.x, lo.y, hi.x, hi.y};
-      if (vec_c && c + 3 < N) {
-        *reinterpret_cast<float4*>(crow + c) = make_float4(v[0], v[1], v[2], v[3]);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (c + j < N) crow[c + j] = v[j];
-      }
+      for (int j = 0; j < 4; ++j)
+        if (c + j < N) crow[c + j] = w[j];
     }
   }
 }
@@ -172,12 +172,18 @@ cudaError_t launch_sgemm_ffma(const Launch& L, int64_t M, int64_t N, int64_t K, 
                               int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc) {
   const int tiles_m = static_cast<int>((M + BM - 1) / BM);
   const int tiles_n = static_cast<int>((N + BN - 1) / BN);
-  const int vec_a = (lda % 4 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0);
-  const int vec_b = (ldb % 4 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0);
+  // 16-byte cp.async when a whole chunk is always in or out of the matrix
+  const bool va = lda % 4 == 0 && K % 4 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0;
+  const bool vb = ldb % 4 == 0 && N % 4 == 0 && reinterpret_cast<uintptr_t>(B) % 16 == 0;
   const int vec_c = (ldc % 4 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0);
-  sgemm_ffma_kernel<<<tiles_m * tiles_n, THREADS, 0, L.stream>>>(
-      A, lda, B, ldb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K),
-      tiles_m, tiles_n, vec_a, vec_b, vec_c);
+  auto kern = va ? (vb ? sgemm_ffma_kernel<true, true> : sgemm_ffma_kernel<true, false>)
+                 : (vb ? sgemm_ffma_kernel<false, true> : sgemm_ffma_kernel<false, false>);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  if (e != cudaSuccess) return e;
+  kern<<<tiles_m * tiles_n, THREADS, SMEM, L.stream>>>(A, lda, B, ldb, C, ldc,
+                                                       static_cast<int>(M), static_cast<int>(N),
+                                                       static_cast<int>(K), tiles_m, tiles_n,
+                                                       vec_c);
   L.count();
   return cudaGetLastError();
 }

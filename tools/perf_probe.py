@@ -44,7 +44,7 @@ def main():
             print(json.dumps({"n": n, "mode": mname, "t_min": tmin, "t_med": tmed,
                               "tflops": 2 * n**3 / tmin / 1e12}), flush=True)
         del A, B, C
-    for n in [8192, 16384]:
+    for n in [8192, 16384, 32768]:
         A = ctx.fill(P.DIST_NORMAL, 0, n, n, dtype=torch.float32)
         B = ctx.fill(P.DIST_NORMAL, 1, n, n, dtype=torch.float32)
         C = torch.empty_like(A)
