@@ -207,12 +207,17 @@ int mmws_gpu_last_kernel_ms(mmws_gpu_ctx* ctx, double* ms);
 /* The message plan rank 0 executes for (m, k, n, nranks), in issue order --
  * the analogue of the reference's Communicator traffic log (comm.hpp:24-32)
  * used by its protocol-shape test (test_protocol.cpp:99-137).  Host-only.
- * Entry e: peer[e], tag[e] (1 = assign, 2 = result), kind[e] (0 = int64
- * scalar metadata, 1 = fp64/fp32 array), count[e] (elements), dir[e] (0 sent,
- * 1 received, 2 broadcast).  *n_entries in: capacity, out: entries needed. */
+ * Order: one B broadcast, then the A-slices sub-block by sub-block, then the
+ * C-slices sub-block by sub-block (offsets/row counts are derived from
+ * split_rows on every rank, so there are no scalar metadata messages).
+ * Entry e: peer[e] (-1 = all ranks), tag[e] (1 = assign, 2 = result),
+ * kind[e] (1 = fp64/fp32 array), count[e] (elements), row0[e] (first row of
+ * A or C the slice covers, -1 for B), dir[e] (0 sent, 1 received,
+ * 2 broadcast).  *n_entries in: capacity, out: entries needed; any output
+ * array may be NULL. */
 int mmws_gpu_rowblock_plan(int64_t m, int64_t n, int64_t k, int nranks, int32_t* peer,
-                           int32_t* tag, int32_t* kind, int64_t* count, int32_t* dir,
-                           int32_t* n_entries);
+                           int32_t* tag, int32_t* kind, int64_t* count, int64_t* row0,
+                           int32_t* dir, int32_t* n_entries);
 
 #ifdef __cplusplus
 }

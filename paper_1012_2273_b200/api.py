@@ -86,19 +86,19 @@ def op_count(n: int) -> int:
 
 
 def rowblock_plan(m: int, n: int, k: int, nranks: int):
-    """Rank 0's message plan for the row-block exchange, in issue order:
-    list of dicts(peer, tag, kind, count, dir) with dir in {sent, received, broadcast}."""
+    """Rank 0's message plan for the row-block exchange, in issue order: list of
+    dicts(peer, tag, kind, count, row0, dir) with dir in {sent, received, broadcast}."""
     cnt = C.c_int32(0)
-    _check(_lib().mmws_gpu_rowblock_plan(m, n, k, nranks, None, None, None, None, None,
+    _check(_lib().mmws_gpu_rowblock_plan(m, n, k, nranks, None, None, None, None, None, None,
                                          C.byref(cnt)))
     e = cnt.value
     peer, tag, kind, dirs = ((C.c_int32 * max(e, 1))() for _ in range(4))
-    count = (C.c_int64 * max(e, 1))()
-    _check(_lib().mmws_gpu_rowblock_plan(m, n, k, nranks, peer, tag, kind, count, dirs,
+    count, row0 = ((C.c_int64 * max(e, 1))() for _ in range(2))
+    _check(_lib().mmws_gpu_rowblock_plan(m, n, k, nranks, peer, tag, kind, count, row0, dirs,
                                          C.byref(cnt)))
     names = {0: "sent", 1: "received", 2: "broadcast"}
-    return [dict(peer=peer[i], tag=tag[i], kind=kind[i], count=count[i], dir=names[dirs[i]])
-            for i in range(e)]
+    return [dict(peer=peer[i], tag=tag[i], kind=kind[i], count=count[i], row0=row0[i],
+                 dir=names[dirs[i]]) for i in range(e)]
 
 
 def nccl_unique_id() -> bytes:

@@ -51,24 +51,99 @@ T* as_mut(const T* p) {
   return const_cast<T*>(p);
 }
 
-// Enqueue one master/worker round on ctx->stream (no synchronisation).  Rank
-// 0 passes device A, B, C; other ranks pass nulls and use library buffers.
+template <class T>
+int gemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, int64_t lda, const T* B,
+         int64_t ldb, T* C, int64_t ldc, int mode, cudaStream_t s) {
+  if constexpr (sizeof(T) == 8)
+    return dgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode, s);
+  else
+    return sgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode, s);
+}
+
+cudaError_t event_pool(mmws_gpu_ctx* ctx, size_t need) {
+  while (ctx->pool.size() < need) {
+    cudaEvent_t ev;
+    cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+    ctx->pool.push_back(ev);
+  }
+  return cudaSuccess;
+}
+
+// Who holds which rows, and the sub-block cut of every rank's rows -- derived
+// by every rank from split_rows (protocol.hpp:33-46), so no metadata messages
+// are needed.  S = 2 for the big configs: each sub-block is a whole number of
+// 128-row bands, so a sub-block launch loses <2% to wave quantisation on 148
+// SMs while half of the C gather hides behind the second multiply.
+struct Schedule {
+  int P = 1, S = 1;
+  std::vector<int64_t> off, rows;
+  std::vector<std::vector<int64_t>> soff, srows;  // [rank][sub-block], offsets within the rank
+};
+
+Schedule make_schedule(int64_t m, int P) {
+  Schedule sc;
+  sc.P = P;
+  sc.off.resize(P);
+  sc.rows.resize(P);
+  mmws_gpu_split_rows(m, P, sc.off.data(), sc.rows.data());
+  sc.S = P > 1 && m / P >= 1024 ? 2 : 1;
+  sc.soff.assign(P, std::vector<int64_t>(sc.S));
+  sc.srows.assign(P, std::vector<int64_t>(sc.S));
+  for (int r = 0; r < P; ++r)
+    mmws_gpu_split_rows(sc.rows[r], sc.S, sc.soff[r].data(), sc.srows[r].data());
+  return sc;
+}
+
+// Enqueue one master/worker round (no host synchronisation).  Rank 0 passes
+// device A, B, C; other ranks pass nulls and use library buffers.  On return
+// ctx->ev1 (rank 0) is recorded after the last C-slice has landed.
+//
+// P == 1: one multiply.  P > 1 (one rank per GPU, NCCL on ctx->comm_stream,
+// multiplies on ctx->stream), pipelined so transfers hide behind the math:
+//   * comm order, identical on every rank: B (one broadcast -- all of it is
+//     needed before any output element can finish), then every rank's A-slice
+//     in S sub-blocks (grouped send/recv), then per sub-block s the C-slice
+//     gather (grouped send/recv straight into C's row block on rank 0);
+//   * a worker multiplies sub-block s as soon as B and A sub-block s have
+//     landed and ships its C rows while it multiplies sub-block s+1;
+//   * rank 0 multiplies its own rows meanwhile (it holds A and B already).
+// Every launch
+// computes each element with the same kernel and k-order as a 1-GPU launch,
+// so the assembled C is bitwise the 1-GPU result.
 template <class T>
 int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, const T* B,
-                     T* C, int mode) {
+                     T* C, int mode, bool bracket = true) {
   if (m <= 0 || n <= 0 || k <= 0)
     return fail(MMWS_GPU_ERR_DIMENSION, "rowblock: dimensions must be positive");
   const int P = ctx->comm ? ctx->nranks : 1;
   const int me = ctx->comm ? ctx->rank : 0;
   if (me == 0 && (!A || !B || !C))
     return fail(MMWS_GPU_ERR_DOMAIN, "rowblock: rank 0 needs A, B and C");
-  if (P > 1) NCCL_REQUIRE();
-  std::vector<int64_t> off(P), rows(P);
-  if (int rc = mmws_gpu_split_rows(m, P, off.data(), rows.data())) return rc;
-
-  const ncclDataType_t dt = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
-  cudaStream_t s = ctx->stream;
+  cudaStream_t comp = ctx->stream, comm = ctx->comm_stream;
   cudaError_t e;
+
+  if (P == 1) {
+    if (bracket) cudaEventRecord(ctx->ev0, comp);
+    cudaEventRecord(ctx->evk0, comp);
+    if (int rc = gemm<T>(ctx, m, n, k, A, k, B, n, C, n, mode, comp)) return rc;
+    cudaEventRecord(ctx->evk1, comp);
+    if (bracket) cudaEventRecord(ctx->ev1, comp);
+    return MMWS_GPU_OK;
+  }
+  NCCL_REQUIRE();
+  const Schedule sc = make_schedule(m, P);
+  const int S = sc.S;
+  const auto& off = sc.off;
+  const auto& rows = sc.rows;
+  const auto& soff = sc.soff;
+  const auto& srows = sc.srows;
+  const ncclDataType_t dt = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
+
+  if ((e = event_pool(ctx, 2 * S + 3)) != cudaSuccess) return cuda_fail(e, "rowblock: events");
+  cudaEvent_t* evA = ctx->pool.data();
+  cudaEvent_t* evC = evA + S;
+  cudaEvent_t evB = evC[S], evStart = evC[S + 1], evJoin = evC[S + 2];
 
   const T* a_loc = A;
   const T* b_loc = B;
@@ -83,46 +158,67 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
     c_loc = static_cast<T*>(ctx->rbC);
   }
 
-  if (P > 1) {
-    // tag 1: A-slices (protocol.hpp:70-72) ...
+  // the exchange starts after everything already queued on the compute stream
+  // (e.g. the H2D copies of master_run_host)
+  if (me == 0 && bracket) cudaEventRecord(ctx->ev0, comp);  // first send
+  cudaEventRecord(evStart, comp);
+  cudaStreamWaitEvent(comm, evStart, 0);
+
+  // ---- comm stream, part 1: all of B (protocol.hpp:73), once, as a broadcast ...
+  void* bbuf = as_mut(b_loc);
+  NCCL_TRY(nccl().Broadcast(bbuf, bbuf, k * n, dt, 0, ctx->comm, comm), "broadcast B");
+  cudaEventRecord(evB, comm);
+  // ... then the A-slices (protocol.hpp:70-72), sub-block by sub-block
+  for (int s = 0; s < S; ++s) {
     NCCL_TRY(nccl().GroupStart(), "ncclGroupStart");
     if (me == 0) {
       for (int r = 1; r < P; ++r)
-        if (rows[r] > 0)
-          NCCL_TRY(nccl().Send(A + off[r] * k, rows[r] * k, dt, r, ctx->comm, s), "send A-slice");
-    } else if (rows[me] > 0) {
-      NCCL_TRY(nccl().Recv(as_mut(a_loc), rows[me] * k, dt, 0, ctx->comm, s), "recv A-slice");
+        if (srows[r][s] > 0)
+          NCCL_TRY(nccl().Send(A + (off[r] + soff[r][s]) * k, srows[r][s] * k, dt, r, ctx->comm,
+                               comm), "send A-slice");
+    } else if (srows[me][s] > 0) {
+      NCCL_TRY(nccl().Recv(as_mut(a_loc) + soff[me][s] * k, srows[me][s] * k, dt, 0, ctx->comm,
+                           comm), "recv A-slice");
     }
     NCCL_TRY(nccl().GroupEnd(), "ncclGroupEnd");
-    // ... and all of B (protocol.hpp:73), once, as a broadcast.
-    void* bbuf = me == 0 ? as_mut(B) : as_mut(b_loc);
-    NCCL_TRY(nccl().Broadcast(bbuf, bbuf, k * n, dt, 0, ctx->comm, s), "broadcast B");
+    cudaEventRecord(evA[s], comm);
   }
 
-  // worker body (protocol.hpp:132-141) on this rank's rows, timed on its stream
-  cudaEventRecord(ctx->evk0, s);
-  if (rows[me] > 0) {
-    int rc;
-    if constexpr (sizeof(T) == 8)
-      rc = dgemm_dispatch(ctx, rows[me], n, k, a_loc, k, b_loc, n, c_loc, n, mode, s);
-    else
-      rc = sgemm_dispatch(ctx, rows[me], n, k, a_loc, k, b_loc, n, c_loc, n, mode, s);
-    if (rc) return rc;
+  // ---- compute stream: this rank's rows (worker_run's body, protocol.hpp:132-141)
+  cudaEventRecord(ctx->evk0, comp);
+  if (me != 0) cudaStreamWaitEvent(comp, evB, 0);
+  for (int s = 0; s < S; ++s) {
+    const int64_t r0 = soff[me][s], rs = srows[me][s];
+    if (me != 0) cudaStreamWaitEvent(comp, evA[s], 0);
+    if (rs > 0)
+      if (int rc = gemm<T>(ctx, rs, n, k, a_loc + r0 * k, k, b_loc, n, c_loc + r0 * n, n, mode,
+                           comp))
+        return rc;
+    cudaEventRecord(evC[s], comp);
   }
-  cudaEventRecord(ctx->evk1, s);
+  cudaEventRecord(ctx->evk1, comp);
 
-  if (P > 1) {
-    // tag 2: C-slices back into C's row blocks, rank order (protocol.hpp:85-103)
+  // ---- comm stream, part 2: C-slices back into C's row blocks, rank order
+  // (protocol.hpp:85-103), one grouped exchange per sub-block
+  for (int s = 0; s < S; ++s) {
+    if (me != 0) cudaStreamWaitEvent(comm, evC[s], 0);
     NCCL_TRY(nccl().GroupStart(), "ncclGroupStart");
     if (me == 0) {
       for (int r = 1; r < P; ++r)
-        if (rows[r] > 0)
-          NCCL_TRY(nccl().Recv(C + off[r] * n, rows[r] * n, dt, r, ctx->comm, s), "recv C-slice");
-    } else if (rows[me] > 0) {
-      NCCL_TRY(nccl().Send(c_loc, rows[me] * n, dt, 0, ctx->comm, s), "send C-slice");
+        if (srows[r][s] > 0)
+          NCCL_TRY(nccl().Recv(C + (off[r] + soff[r][s]) * n, srows[r][s] * n, dt, r, ctx->comm,
+                               comm), "recv C-slice");
+    } else if (srows[me][s] > 0) {
+      NCCL_TRY(nccl().Send(c_loc + soff[me][s] * n, srows[me][s] * n, dt, 0, ctx->comm, comm),
+               "send C-slice");
     }
     NCCL_TRY(nccl().GroupEnd(), "ncclGroupEnd");
   }
+  // join: the compute stream waits for the exchange, so the caller only
+  // needs to synchronise ctx->stream
+  cudaEventRecord(evJoin, comm);
+  cudaStreamWaitEvent(comp, evJoin, 0);
+  if (me == 0 && bracket) cudaEventRecord(ctx->ev1, comp);  // last receive
   return MMWS_GPU_OK;
 }
 
@@ -142,9 +238,7 @@ template <class T>
 int rowblock(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, const T* B, T* C,
              int mode, double* elapsed_s) {
   const bool root = !ctx->comm || ctx->rank == 0;
-  if (root) cudaEventRecord(ctx->ev0, ctx->stream);  // first send
   if (int rc = rowblock_enqueue(ctx, m, n, k, A, B, C, mode)) return rc;
-  if (root) cudaEventRecord(ctx->ev1, ctx->stream);  // last receive
   return finish(ctx, root, elapsed_s);
 }
 
@@ -174,7 +268,8 @@ int master_run_host(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T*
       (e = cudaMemcpyAsync(ctx->dB, B, b_b, cudaMemcpyHostToDevice, s)) != cudaSuccess)
     return cuda_fail(e, "master_run: H2D");
   if (int rc = rowblock_enqueue(ctx, m, n, k, static_cast<const T*>(ctx->dA),
-                                static_cast<const T*>(ctx->dB), static_cast<T*>(ctx->dC), mode))
+                                static_cast<const T*>(ctx->dB), static_cast<T*>(ctx->dC), mode,
+                                false))
     return rc;
   if ((e = cudaMemcpyAsync(C, ctx->dC, c_b, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
     return cuda_fail(e, "master_run: D2H");
@@ -264,22 +359,25 @@ int mmws_gpu_last_kernel_ms(mmws_gpu_ctx* ctx, double* ms) {
 }
 
 int mmws_gpu_rowblock_plan(int64_t m, int64_t n, int64_t k, int nranks, int32_t* peer,
-                           int32_t* tag, int32_t* kind, int64_t* count, int32_t* dir,
-                           int32_t* n_entries) {
+                           int32_t* tag, int32_t* kind, int64_t* count, int64_t* row0,
+                           int32_t* dir, int32_t* n_entries) {
   if (!n_entries) return fail(MMWS_GPU_ERR_DOMAIN, "rowblock_plan: null n_entries");
   if (m <= 0 || n <= 0 || k <= 0)
     return fail(MMWS_GPU_ERR_DIMENSION, "rowblock_plan: dimensions must be positive");
   if (nranks < 1) return fail(MMWS_GPU_ERR_DOMAIN, "rowblock_plan: nranks must be >= 1");
-  std::vector<int64_t> off(nranks), rows(nranks);
-  mmws_gpu_split_rows(m, nranks, off.data(), rows.data());
-  struct E { int32_t peer, tag, kind; int64_t count; int32_t dir; };
-  std::vector<E> plan;
+  const Schedule sc = make_schedule(m, nranks);
+  struct E { int32_t peer, tag, kind; int64_t count, row0; int32_t dir; };
+  std::vector<E> plan;  // the order rowblock_enqueue issues on rank 0
   if (nranks > 1) {
-    for (int r = 1; r < nranks; ++r)
-      if (rows[r] > 0) plan.push_back({r, 1, 1, rows[r] * k, 0});
-    plan.push_back({-1, 1, 1, k * n, 2});
-    for (int r = 1; r < nranks; ++r)
-      if (rows[r] > 0) plan.push_back({r, 2, 1, rows[r] * n, 1});
+    plan.push_back({-1, 1, 1, k * n, -1, 2});
+    for (int s = 0; s < sc.S; ++s)
+      for (int r = 1; r < nranks; ++r)
+        if (sc.srows[r][s] > 0)
+          plan.push_back({r, 1, 1, sc.srows[r][s] * k, sc.off[r] + sc.soff[r][s], 0});
+    for (int s = 0; s < sc.S; ++s)
+      for (int r = 1; r < nranks; ++r)
+        if (sc.srows[r][s] > 0)
+          plan.push_back({r, 2, 1, sc.srows[r][s] * n, sc.off[r] + sc.soff[r][s], 1});
   }
   const int32_t cap = *n_entries;
   *n_entries = static_cast<int32_t>(plan.size());
@@ -289,6 +387,7 @@ int mmws_gpu_rowblock_plan(int64_t m, int64_t n, int64_t k, int nranks, int32_t*
     if (tag) tag[i] = plan[i].tag;
     if (kind) kind[i] = plan[i].kind;
     if (count) count[i] = plan[i].count;
+    if (row0) row0[i] = plan[i].row0;
     if (dir) dir[i] = plan[i].dir;
   }
   return ok();

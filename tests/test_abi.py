@@ -89,21 +89,29 @@ def test_rowblock_plan_shape():
     # The reference's protocol shape test (test_protocol.cpp:99-137) on a 4x4
     # problem over 2 workers; here rank 0 also computes, so 3 ranks = rank 0 +
     # 2 remote workers, metadata is derived locally (no scalar messages), and B
-    # is one broadcast instead of per-worker copies.
+    # is one broadcast (first: nothing can finish without all of B) instead of
+    # per-worker copies.
     plan = P.rowblock_plan(4, 4, 4, 3)
-    assert [(e["dir"], e["tag"], e["peer"], e["count"]) for e in plan] == [
-        ("sent", 1, 1, 4), ("sent", 1, 2, 4), ("broadcast", 1, -1, 16),
-        ("received", 2, 1, 4), ("received", 2, 2, 4)]
-    # idle ranks (P > N) exchange nothing but still join the collectives
+    assert [(e["dir"], e["tag"], e["peer"], e["count"], e["row0"]) for e in plan] == [
+        ("broadcast", 1, -1, 16, -1), ("sent", 1, 1, 4, 2), ("sent", 1, 2, 4, 3),
+        ("received", 2, 1, 4, 2), ("received", 2, 2, 4, 3)]
+    # idle ranks (P > N) exchange nothing but still join the broadcast
     plan = P.rowblock_plan(2, 2, 2, 5)
     assert [e["peer"] for e in plan if e["dir"] == "sent"] == [1]
     assert P.rowblock_plan(7, 7, 7, 1) == []
-    # total traffic: A slices (m - rows_0) k, B once, C slices (m - rows_0) n
+    # N=16384 over 8 GPUs: two sub-blocks per rank; A and C slices tile rows
+    # 2048..16383 exactly once each, B goes out once
     m, n, k, world = 16384, 16384, 16384, 8
     plan = P.rowblock_plan(m, n, k, world)
     rows0 = P.split_rows(m, world)[0][1]
-    assert sum(e["count"] for e in plan if e["dir"] == "sent") == (m - rows0) * k
-    assert sum(e["count"] for e in plan if e["dir"] == "received") == (m - rows0) * n
+    assert [e["dir"] for e in plan].count("broadcast") == 1
+    for d, width in (("sent", k), ("received", n)):
+        spans = sorted((e["row0"], e["row0"] + e["count"] // width) for e in plan if e["dir"] == d)
+        assert len(spans) == 2 * (world - 1)
+        assert spans[0][0] == rows0 and spans[-1][1] == m
+        assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    # every sub-block is a whole number of 128-row bands (wave quantisation)
+    assert all(e["count"] // k % 128 == 0 for e in plan if e["dir"] == "sent")
     with pytest.raises(P.DimensionError):
         P.rowblock_plan(0, 4, 4, 2)
 

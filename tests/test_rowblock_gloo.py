@@ -40,42 +40,51 @@ def _rank_main(rank, world, port, cases, failures):
                             init_method=f"tcp://127.0.0.1:{port}")
     try:
         for (m, k, n, sa, sb) in cases:
-            parts = P.split_rows(m, world)
-            off, rows = parts[rank]
+            # rank 0's plan is the single schedule; a worker follows the
+            # entries addressed to it, in order (as the NCCL engine does)
+            plan = P.rowblock_plan(m, n, k, world)
+            off, rows = P.split_rows(m, world)[rank]
             if rank == 0:
                 a = O.fill(O.DIST_UNIT, sa, m, k)
                 b = O.fill(O.DIST_UNIT, sb, k, n)
                 c = np.full((m, n), np.nan)
-                plan = P.rowblock_plan(m, n, k, world)
-                for e in plan:                       # tag 1: A-slices, then B
-                    if e["dir"] == "sent":
-                        o, r = parts[e["peer"]]
-                        assert e["count"] == r * k
-                        dist.send(torch.from_numpy(np.ascontiguousarray(a[o:o + r])), e["peer"])
-                    elif e["dir"] == "broadcast":
+                if rows:
+                    c[off:off + rows] = O.worker_block(a[off:off + rows], b)
+                for e in plan:
+                    if e["dir"] == "broadcast":
                         assert e["count"] == k * n
                         dist.broadcast(torch.from_numpy(b), 0)
-                if world > 1 and not any(e["dir"] == "broadcast" for e in plan):
-                    raise AssertionError("plan without B broadcast")
-                c[off:off + rows] = O.worker_block(a[off:off + rows], b) if rows else c[0:0]
-                for e in plan:                       # tag 2: C-slices, rank order
-                    if e["dir"] == "received":
-                        o, r = parts[e["peer"]]
-                        buf = torch.empty((r, n), dtype=torch.float64)
+                    elif e["dir"] == "sent":               # tag 1: A sub-slice
+                        r0, nr = e["row0"], e["count"] // k
+                        dist.send(torch.from_numpy(np.ascontiguousarray(a[r0:r0 + nr])), e["peer"])
+                    else:                                  # tag 2: C sub-slice
+                        r0, nr = e["row0"], e["count"] // n
+                        buf = torch.empty((nr, n), dtype=torch.float64)
                         dist.recv(buf, e["peer"])
-                        c[o:o + r] = buf.numpy()
+                        c[r0:r0 + nr] = buf.numpy()
                 want = O.matmul_seq(a, b)
                 if O.first_difference(c, want) is not None:
                     failures.append(f"m={m} k={k} n={n} world={world}")
+                covered = sum(e["count"] // n for e in plan if e["dir"] == "received") + rows
+                if world > 1 and covered != m:
+                    failures.append(f"coverage m={m} world={world}")
             else:
-                a_slice = torch.empty((rows, k), dtype=torch.float64)
-                if rows:
-                    dist.recv(a_slice, 0)
+                a_loc = np.zeros((rows, k))
                 b = torch.empty((k, n), dtype=torch.float64)
-                dist.broadcast(b, 0)
-                if rows:
-                    c_slice = O.worker_block(a_slice.numpy(), b.numpy())
-                    dist.send(torch.from_numpy(c_slice), 0)
+                for e in plan:
+                    if e["dir"] == "broadcast":
+                        dist.broadcast(b, 0)
+                    elif e["peer"] != rank:
+                        continue
+                    elif e["dir"] == "sent":
+                        r0, nr = e["row0"] - off, e["count"] // k
+                        buf = torch.empty((nr, k), dtype=torch.float64)
+                        dist.recv(buf, 0)
+                        a_loc[r0:r0 + nr] = buf.numpy()
+                    else:                                  # multiply the sub-block, reply
+                        r0, nr = e["row0"] - off, e["count"] // n
+                        c_sub = O.worker_block(a_loc[r0:r0 + nr], b.numpy())
+                        dist.send(torch.from_numpy(c_sub), 0)
     finally:
         dist.destroy_process_group()
 
@@ -91,8 +100,9 @@ def _run(world, cases):
 
 ACCEPT = [(n, n, n, 3000 + n, 4000 + n) for n in (1, 2, 3, 4, 8, 16, 33)]
 RECT = [(5, 7, 4, 31, 32), (2, 2, 2, 61, 62), (513, 67, 129, 7, 8)]
+SUBBLOCKS = [(2048 * 5 + 3, 7, 5, 9, 10)]   # >= 1024 rows per rank: two sub-blocks each
 
 
 @pytest.mark.parametrize("world", [2, 3, 5])
 def test_rowblock_gloo_bitwise_equals_seq(world):
-    assert _run(world, ACCEPT + RECT) == []
+    assert _run(world, ACCEPT + RECT + SUBBLOCKS) == []
