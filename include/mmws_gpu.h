@@ -57,7 +57,11 @@ enum {
  *              TMA + mbarrier pipeline.  Bit-exact for integer-valued inputs
  *              whose partial sums stay below 2^53; normwise <= 1e-12 otherwise.
  *   DMMA_SMALL same math on 64x64 tiles (more CTAs for N < ~2000).
- *   AUTO       DMMA or DMMA_SMALL by problem size (fp64); FFMA (fp32).
+ *   AUTO       fp64: the latency path (32x32 tiles, one DFMA chain per
+ *              element, no TMA) when n <= 256 and k <= 256, else DMMA or
+ *              DMMA_SMALL by tile count -- the choice never depends on m, so
+ *              row slices of a problem get the whole problem's bits; fp32: FFMA.
+ *              EXACT also switches to 32x32 tiles for small problems.
  *   FFMA       fp32 register-blocked FFMA GEMM (sgemm only). */
 enum {
   MMWS_GPU_MODE_AUTO = 0,

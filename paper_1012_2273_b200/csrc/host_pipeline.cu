@@ -68,7 +68,9 @@ int host_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A
   const double work = static_cast<double>(m) * n * k;
   const int64_t R = work < 2.0e9 ? m : std::max<int64_t>(128, ((m + 7) / 8 + 127) / 128 * 128);
   const int64_t panels = (m + R - 1) / R;
-  const int64_t W = panels > 1 ? std::min<int64_t>(n, R) : n;
+  // column blocks never narrower than 512 unless n itself is: a block then
+  // takes the same kernel as the whole problem (see dgemm_dispatch)
+  const int64_t W = panels > 1 ? std::min<int64_t>(n, std::max<int64_t>(R, 512)) : n;
   const int64_t blocks = (n + W - 1) / W;
   if ((e = event_pool(ctx, panels * 2 + blocks)) != cudaSuccess)
     return cuda_fail(e, "matmul_host: events");

@@ -39,6 +39,12 @@ cudaError_t launch_dgemm_exact(const Launch& L, int64_t M, int64_t N, int64_t K,
                                const double* A, int64_t lda, const double* B, int64_t ldb,
                                double* C, int64_t ldc);
 
+// Latency path: 32x32 tiles, plain loads, no TMA.  exact: DMUL+DADD chain
+// (bitwise matmul_seq); otherwise one DFMA per step.
+cudaError_t launch_dgemm_small(const Launch& L, bool exact, int64_t M, int64_t N, int64_t K,
+                               const double* A, int64_t lda, const double* B, int64_t ldb,
+                               double* C, int64_t ldc);
+
 // Register-blocked FFMA fp32 GEMM with two-level (chunked) accumulation.
 cudaError_t launch_sgemm_ffma(const Launch& L, int64_t M, int64_t N, int64_t K, const float* A,
                               int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc);

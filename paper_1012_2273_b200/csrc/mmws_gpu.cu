@@ -68,21 +68,27 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
   if (int rc = check_dims(m, n, k, lda, ldb, ldc, A, B, C)) return rc;
   const Launch L = ctx->launch(stream);
   cudaError_t e;
+  const int64_t tiles128 = ((m + 127) / 128) * ((n + 127) / 128);
   if (mode == MMWS_GPU_MODE_EXACT) {
-    e = launch_dgemm_exact(L, m, n, k, A, lda, B, ldb, C, ldc);
+    // exact order: 32x32 tiles while 128x128 tiles would leave SMs idle
+    e = tiles128 < 2 * static_cast<int64_t>(ctx->num_sms)
+            ? launch_dgemm_small(L, true, m, n, k, A, lda, B, ldb, C, ldc)
+            : launch_dgemm_exact(L, m, n, k, A, lda, B, ldb, C, ldc);
     return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm exact");
   }
   if (mode != MMWS_GPU_MODE_AUTO && mode != MMWS_GPU_MODE_DMMA &&
       mode != MMWS_GPU_MODE_DMMA_SMALL)
     return fail(MMWS_GPU_ERR_DOMAIN, "dgemm: unknown mode " + std::to_string(mode));
-  int cfg = DMMA_128x128;
-  if (mode == MMWS_GPU_MODE_DMMA_SMALL) {
-    cfg = DMMA_64x64;
-
-  } else if (mode == MMWS_GPU_MODE_AUTO) {
-    const int64_t tiles = ((m + 127) / 128) * ((n + 127) / 128);
-    if (tiles < 2 * static_cast<int64_t>(ctx->num_sms)) cfg = DMMA_64x64;
+  if (mode == MMWS_GPU_MODE_AUTO && n <= 256 && k <= 256) {
+    // latency path; chosen from (n, k) only, so every row slice of a problem
+    // (row-block ranks, host-pipeline panels) takes the same kernel as the
+    // whole problem and gets the same bits
+    e = launch_dgemm_small(L, false, m, n, k, A, lda, B, ldb, C, ldc);
+    return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm small");
   }
+  int cfg = DMMA_128x128;
+  if (mode == MMWS_GPU_MODE_DMMA_SMALL || (mode == MMWS_GPU_MODE_AUTO && tiles128 < 2 * static_cast<int64_t>(ctx->num_sms)))
+    cfg = DMMA_64x64;
   // TMA needs 16-byte aligned bases and row pitches: pack otherwise.
   const bool a_ok = lda % 2 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0;
   const bool b_ok = ldb % 2 == 0 && reinterpret_cast<uintptr_t>(B) % 16 == 0;

@@ -18,6 +18,13 @@ if which in ("all", "exact"):
     B = ctx.fill(P.DIST_UNIFORM, 1, n, n)
     for _ in range(2):
         ctx.dgemm(A, B, mode=P.MODE_EXACT)
+if which == "tiny":
+    for n in (10, 64, 250, 500):
+        A = ctx.fill(P.DIST_UNIFORM, 0, n, n)
+        B = ctx.fill(P.DIST_UNIFORM, 1, n, n)
+        for _ in range(2):
+            ctx.dgemm(A, B, mode=P.MODE_AUTO)
+            ctx.dgemm(A, B, mode=P.MODE_EXACT)
 if which in ("all", "small"):
     n = 1000
     A = ctx.fill(P.DIST_UNIFORM, 0, n, n)
