@@ -144,6 +144,18 @@ struct mmws_gpu_graph {
     return cuda_fail(e_, "cudaSetDevice");
 
 
+namespace {
+// The NCCL stream gets the highest priority so its CTAs are scheduled ahead of
+// pending GEMM CTAs whenever an SM frees up -- otherwise the C gather of a
+// finished sub-block would wait for the whole next multiply.
+cudaError_t create_comm_stream(cudaStream_t* s) {
+  int least = 0, greatest = 0;
+  cudaError_t e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  if (e != cudaSuccess) return e;
+  return cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, greatest);
+}
+}  // namespace
+
 extern "C" {
 
 int mmws_gpu_abi_version(void) { return MMWS_GPU_ABI_VERSION; }
@@ -185,7 +197,7 @@ int mmws_gpu_init(int device, mmws_gpu_ctx** out) {
   }
   ctx->encode = reinterpret_cast<EncodeTiledFn>(fn);
   if ((e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess ||
-      (e = cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = create_comm_stream(&ctx->comm_stream)) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaEventCreate(&ctx->ev0)) != cudaSuccess ||
