@@ -80,6 +80,8 @@ def ref():
         L.ref_static_partition.argtypes = [_u64, C.c_uint, _pu64, _pu64]
         L.ref_op_count.argtypes = [_i64, _pu64]
         L.ref_split_rows.argtypes = [_i64, C.c_int, _pi64, _pi64]
+        L.ref_derive_seed.argtypes = [_u64, _i64, C.c_int, _pu64]
+        L.ref_mflops.argtypes = [_i64, C.c_double, C.POINTER(C.c_double)]
         _ref = L
     return _ref
 
@@ -264,6 +266,22 @@ def ref_op_count(n: int) -> int:
     rc = ref().ref_op_count(n, C.byref(out))
     if rc:
         raise ValueError(f"ref_op_count rc={rc}")
+    return out.value
+
+
+def ref_derive_seed(seed: int, n: int, which: int) -> int:
+    out = C.c_uint64()
+    rc = ref().ref_derive_seed(seed, n, which, C.byref(out))
+    if rc:
+        raise ValueError(f"ref_derive_seed rc={rc}")
+    return out.value
+
+
+def ref_mflops(n: int, elapsed: float) -> float:
+    out = C.c_double()
+    rc = ref().ref_mflops(n, elapsed, C.byref(out))
+    if rc:
+        raise ValueError(f"ref_mflops rc={rc}")
     return out.value
 
 

@@ -20,6 +20,7 @@
 #include "mmws/matrix.hpp"
 #include "mmws/workshare.hpp"
 #ifdef MMWS_REF_WITH_PROTOCOL
+#include "mmws/bench.hpp"
 #include "mmws/protocol.hpp"
 #endif
 
@@ -170,6 +171,32 @@ int ref_split_rows(std::int64_t n_rows, int n_workers, std::int64_t* offset,
   }
 #else
   (void)n_rows; (void)n_workers; (void)offset; (void)rows;
+  return 9;
+#endif
+}
+
+// bench.hpp:83-86 (derive_seed) and :70-78 (mflops); 9 when the harness
+// header could not be built.
+int ref_derive_seed(std::uint64_t seed, std::int64_t n, int which, std::uint64_t* out) {
+#ifdef MMWS_REF_WITH_PROTOCOL
+  *out = mmws::detail::derive_seed(seed, n, which);
+  return 0;
+#else
+  (void)seed; (void)n; (void)which; (void)out;
+  return 9;
+#endif
+}
+
+int ref_mflops(std::int64_t n, double elapsed, double* out) {
+#ifdef MMWS_REF_WITH_PROTOCOL
+  try {
+    *out = mmws::mflops(n, elapsed);
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+#else
+  (void)n; (void)elapsed; (void)out;
   return 9;
 #endif
 }

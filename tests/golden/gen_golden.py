@@ -73,6 +73,11 @@ def small(out_path: str) -> None:
     g["static_partition"] = {f"{n},{w}": O.ref_static_partition(n, w)
                              for n in (0, 3, 8, 50, 1000) for w in (1, 2, 4, 9)}
     g["op_count"] = {str(n): O.ref_op_count(n) for n in (1, 100, 1000, 4099, 16384, 32768)}
+    # bench.hpp harness pieces: derive_seed (:83-86) and mflops (:70-73)
+    g["derive_seed"] = {f"{s},{n},{w}": O.ref_derive_seed(s, n, w)
+                        for s in (0, 42, 2**63 + 5) for n in (1, 100, 1000, 16384) for w in (0, 1)}
+    g["mflops"] = {f"{n},{t}": O.ref_mflops(n, t)
+                   for n in (100, 500, 1000, 2000) for t in (0.03, 2.09, 22.52, 240.97)}
     with open(out_path, "w") as f:
         json.dump(g, f, indent=1, sort_keys=True)
 

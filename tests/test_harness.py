@@ -1,0 +1,62 @@
+"""The benchmark harness with GPU models (include/mmws_gpu_bench.hpp,
+tools/mmws_gpu_bench.cpp): host-side pieces pinned against the reference's own
+bench.hpp values (golden), and an end-to-end sweep on the GPU with the
+correctness gate."""
+import json
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF_INC = "/root/reference/proj/include"
+LIB = ["-L" + os.path.join(ROOT, "paper_1012_2273_b200"), "-lmmws_gpu",
+       "-Wl,-rpath," + os.path.join(ROOT, "paper_1012_2273_b200")]
+
+
+def _build(src, out, extra=()):
+    subprocess.run(["g++", "-std=c++20", "-O2", "-Wall", "-Wextra", "-Werror",
+                    "-I" + os.path.join(ROOT, "include"), *extra, src, "-o", str(out), *LIB],
+                   check=True)
+    return str(out)
+
+
+def test_harness_host_pieces_match_reference(tmp_path, golden_small):
+    exe = _build(os.path.join(ROOT, "tests", "cpp", "test_harness.cpp"), tmp_path / "th")
+    got = json.loads(subprocess.run([exe], capture_output=True, text=True, check=True).stdout)
+    assert {k: int(v) for k, v in got["derive_seed"].items()} == golden_small["derive_seed"]
+    for key, want in golden_small["mflops"].items():
+        n, t = key.split(",")
+        assert got["mflops"][f"{n},{float(t):.6g}"] == want
+    assert got["random0"] == 0.88331080821364261
+    assert got["csv"] == ("model,n,workers,elapsed_s,mflops,speedup|"
+                          "gpu,1000,1,0.000123457,16191.2,|gpu-exact,1000,1,0.5,3998,2.5|")
+    assert got["mflops_zero_throws"] is True
+
+
+def test_cli_builds_standalone_and_against_reference(tmp_path):
+    _build(os.path.join(ROOT, "tools", "mmws_gpu_bench.cpp"), tmp_path / "b1")
+    if os.path.exists(os.path.join(REF_INC, "mmws", "matrix.hpp")):
+        _build(os.path.join(ROOT, "tools", "mmws_gpu_bench.cpp"), tmp_path / "b2",
+               extra=("-I" + REF_INC,))
+
+
+@pytest.mark.gpu
+def test_cli_sweep_with_gate(tmp_path):
+    exe = _build(os.path.join(ROOT, "tools", "mmws_gpu_bench.cpp"), tmp_path / "b")
+    csv = tmp_path / "out.csv"
+    r = subprocess.run([exe, "--dims", "10,100,257,1000", "--models", "gpu,gpu-exact,gpu-rowblock",
+                        "--repeats", "2", "--csv", str(csv)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    lines = csv.read_text().splitlines()
+    assert lines[0] == "model,n,workers,elapsed_s,mflops,speedup"
+    assert len(lines) == 1 + 12
+    models = [ln.split(",")[0] for ln in lines[1:]]
+    assert models == ["gpu"] * 4 + ["gpu-exact"] * 4 + ["gpu-rowblock"] * 4
+    for ln in lines[1:]:
+        f = ln.split(",")
+        assert float(f[3]) > 0 and float(f[4]) > 0 and f[5] == ""
+    # an impossible tolerance trips the normwise gate: exit code 2 (bench_main.cpp:175-177)
+    r = subprocess.run([exe, "--dims", "300", "--models", "gpu", "--tolerance", "0"],
+                       capture_output=True, text=True)
+    assert r.returncode == 2 and "correctness gate" in r.stderr
