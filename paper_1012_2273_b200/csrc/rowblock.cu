@@ -99,8 +99,9 @@ Schedule make_schedule(int64_t m, int P) {
 // device A, B, C; other ranks pass nulls and use library buffers.  On return
 // ctx->ev1 (rank 0) is recorded after the last C-slice has landed.
 //
-// P == 1: one multiply.  P > 1 (one rank per GPU, NCCL on ctx->comm_stream,
-// multiplies on ctx->stream), pipelined so transfers hide behind the math:
+// Without a communicator: one multiply.  With one (one rank per GPU, NCCL on
+// ctx->comm_stream, multiplies on ctx->stream -- a 1-rank world takes this
+// path too), pipelined so transfers hide behind the math:
 //   * comm order, identical on every rank: B (one broadcast -- all of it is
 //     needed before any output element can finish), then every rank's A-slice
 //     in S sub-blocks (grouped send/recv), then per sub-block s the C-slice
@@ -123,7 +124,7 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
   cudaStream_t comp = ctx->stream, comm = ctx->comm_stream;
   cudaError_t e;
 
-  if (P == 1) {
+  if (!ctx->comm) {  // no communicator: one multiply
     if (bracket) cudaEventRecord(ctx->ev0, comp);
     cudaEventRecord(ctx->evk0, comp);
     if (int rc = gemm<T>(ctx, m, n, k, A, k, B, n, C, n, mode, comp)) return rc;
@@ -251,7 +252,7 @@ int master_run_host(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T*
   if (!root) return rowblock(ctx, m, n, k, static_cast<const T*>(nullptr),
                              static_cast<const T*>(nullptr), static_cast<T*>(nullptr), mode,
                              elapsed_s);
-  if (!ctx->comm || ctx->nranks == 1)  // one GPU: copies overlapped with the multiply
+  if (!ctx->comm)  // one GPU: copies overlapped with the multiply
     return host_multiply(ctx, m, n, k, A, B, C, mode, elapsed_s);
   if (m <= 0 || n <= 0 || k <= 0)
     return fail(MMWS_GPU_ERR_DIMENSION, "master_run: dimensions must be positive");

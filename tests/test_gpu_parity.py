@@ -251,6 +251,31 @@ def test_rowblock_single_rank_entry(ctx, oracle):
     assert oracle.first_difference(host(C), want) is None
 
 
+def test_rowblock_nccl_path_single_rank(oracle):
+    # The NCCL engine (dlopen of the process's libnccl, communicator, broadcast,
+    # grouped exchanges, two sub-blocks, stream joins) in a 1-rank world -- the
+    # only multi-rank code this one-GPU box can execute.  Bitwise equal to the
+    # plain multiply.
+    T = torch()
+    c2 = P.Context(0)
+    try:
+        c2.comm_init(1, 0, P.nccl_unique_id())
+        n = 2304  # >= 1024 rows per rank: two sub-blocks
+        A = c2.fill(P.DIST_UNIFORM, 0, n, n)
+        B = c2.fill(P.DIST_UNIFORM, 1, n, n)
+        C = T.empty_like(A)
+        for mode in (P.MODE_AUTO, P.MODE_EXACT):
+            el = c2.rowblock(n, n, n, A, B, C, mode=mode)
+            assert el > 0
+            want = host(c2.dgemm(A, B, mode=mode))
+            assert (bits(host(C)) == bits(want)).all()
+            c, el = c2.master_run_host(host(A), host(B), mode=mode)
+            assert el > 0 and (bits(c) == bits(want)).all()
+        c2.comm_destroy()
+    finally:
+        c2.close()
+
+
 # ----------------------------------------------------------------------------- boundary behaviour
 def test_host_entry_matches_device_entry(ctx, oracle):
     a = oracle.fill(oracle.DIST_UNIFORM, 5, 257, 300)
