@@ -49,14 +49,17 @@ __global__ void fill_kernel(int dist, uint64_t seed, void* dst, int64_t rows, in
 }
 
 // ---------------------------------------------------------------- packing
+// One CTA row-strip per (row, 1024-column chunk): no 64-bit division per
+// element, coalesced reads and writes.
 __global__ void pack_f64_kernel(const double* __restrict__ src, int64_t rows, int64_t cols,
                                 int64_t ld_src, double* __restrict__ dst, int64_t rows_p,
                                 int64_t cols_p, int64_t ld_dst) {
-  const int64_t total = rows_p * cols_p;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t r = e / cols_p, c = e % cols_p;
-    dst[r * ld_dst + c] = (r < rows && c < cols) ? src[r * ld_src + c] : 0.0;
+  for (int64_t r = blockIdx.y; r < rows_p; r += gridDim.y) {
+    const double* s = src + r * ld_src;
+    double* d = dst + r * ld_dst;
+    for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < cols_p;
+         c += static_cast<int64_t>(gridDim.x) * blockDim.x)
+      d[c] = (r < rows && c < cols) ? s[c] : 0.0;
   }
 }
 
@@ -137,8 +140,10 @@ cudaError_t launch_fill(const Launch& L, int dist, uint64_t seed, void* dst, int
 cudaError_t launch_pack_f64(const Launch& L, const double* src, int64_t rows, int64_t cols,
                             int64_t ld_src, double* dst, int64_t rows_p, int64_t cols_p,
                             int64_t ld_dst) {
-  pack_f64_kernel<<<grid_for(L, rows_p * cols_p), 256, 0, L.stream>>>(src, rows, cols, ld_src,
-                                                                       dst, rows_p, cols_p, ld_dst);
+  const dim3 grid(static_cast<unsigned>((cols_p + 255) / 256 < 8 ? (cols_p + 255) / 256 : 8),
+                  static_cast<unsigned>(rows_p < 65535 ? rows_p : 65535));
+  pack_f64_kernel<<<grid, 256, 0, L.stream>>>(src, rows, cols, ld_src, dst, rows_p, cols_p,
+                                              ld_dst);
   L.count();
   return cudaGetLastError();
 }

@@ -18,6 +18,29 @@ if which in ("all", "exact"):
     B = ctx.fill(P.DIST_UNIFORM, 1, n, n)
     for _ in range(2):
         ctx.dgemm(A, B, mode=P.MODE_EXACT)
+if which == "families":
+    # one launch per kernel family at its representative size
+    n = 8192
+    A = ctx.fill(P.DIST_NORMAL, 0, n, n, dtype=torch.float32)
+    B = ctx.fill(P.DIST_NORMAL, 1, n, n, dtype=torch.float32)
+    ctx.sgemm(A, B)
+    del A, B
+    n = 4096
+    A = ctx.fill(P.DIST_UNIFORM, 0, n, n)
+    B = ctx.fill(P.DIST_UNIFORM, 1, n, n)
+    ctx.dgemm(A, B, mode=P.MODE_EXACT)
+    n = 1000
+    A = ctx.fill(P.DIST_UNIFORM, 0, n, n)
+    B = ctx.fill(P.DIST_UNIFORM, 1, n, n)
+    ctx.dgemm(A, B, mode=P.MODE_AUTO)
+    n = 250
+    A = ctx.fill(P.DIST_UNIFORM, 0, n, n)
+    B = ctx.fill(P.DIST_UNIFORM, 1, n, n)
+    ctx.dgemm(A, B, mode=P.MODE_AUTO)
+    n = 4099
+    A = ctx.fill(P.DIST_INT8, 0, n, n)
+    B = ctx.fill(P.DIST_INT8, 1, n, n)
+    ctx.dgemm(A, B, mode=P.MODE_AUTO)   # pack_f64_kernel x2 + DMMA
 if which == "tiny":
     for n in (10, 64, 250, 500):
         A = ctx.fill(P.DIST_UNIFORM, 0, n, n)
