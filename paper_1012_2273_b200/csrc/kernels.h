@@ -49,6 +49,12 @@ cudaError_t launch_dgemm_small(const Launch& L, bool exact, int64_t M, int64_t N
 cudaError_t launch_sgemm_ffma(const Launch& L, int64_t M, int64_t N, int64_t K, const float* A,
                               int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc);
 
+// TMA-fed, warp-specialised FFMA2 fp32 GEMM (needs lda, ldb % 4 == 0 and
+// 16-byte aligned A, B).
+bool sgemm_tma_supported(int64_t lda, int64_t ldb, const float* A, const float* B);
+cudaError_t launch_sgemm_tma(const Launch& L, int64_t M, int64_t N, int64_t K, const float* A,
+                             int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc);
+
 // Pad/pack src[rows, cols] (ld_src) into dst[rows_p, cols_p] (ld_dst), zero fill.
 cudaError_t launch_pack_f64(const Launch& L, const double* src, int64_t rows, int64_t cols,
                             int64_t ld_src, double* dst, int64_t rows_p, int64_t cols_p,

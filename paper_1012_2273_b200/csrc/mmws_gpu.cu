@@ -122,7 +122,10 @@ int sgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const flo
   if (int rc = check_dims(m, n, k, lda, ldb, ldc, A, B, C)) return rc;
   if (mode != MMWS_GPU_MODE_AUTO && mode != MMWS_GPU_MODE_FFMA)
     return fail(MMWS_GPU_ERR_DOMAIN, "sgemm: unknown mode " + std::to_string(mode));
-  cudaError_t e = launch_sgemm_ffma(ctx->launch(stream), m, n, k, A, lda, B, ldb, C, ldc);
+  const Launch L = ctx->launch(stream);
+  cudaError_t e = sgemm_tma_supported(lda, ldb, A, B)
+                      ? launch_sgemm_tma(L, m, n, k, A, lda, B, ldb, C, ldc)
+                      : launch_sgemm_ffma(L, m, n, k, A, lda, B, ldb, C, ldc);
   return e == cudaSuccess ? ok() : cuda_fail(e, "sgemm ffma");
 }
 

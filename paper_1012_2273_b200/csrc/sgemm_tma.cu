@@ -1,0 +1,215 @@
+// sgemm_tma.cu -- FP32 GEMM on the FFMA2 pipe, TMA-fed and warp-specialised.
+//
+// Same contraction and accuracy scheme as sgemm_ffma.cu (two-level summation
+// with the running totals in shared memory, see there), restructured like the
+// DMMA kernel so the math warps do nothing but LDS + FFMA2:
+//   * a producer warpgroup (one elected lane) streams A[128 x 16] and
+//     B[16 x 256] k-slices with TMA into a 3-stage mbarrier ring and gives its
+//     registers to the math warps (setmaxnreg 40 / 232);
+//   * 8 math warps, each lane owning 8 rows x 16 columns (64 packed fp32 pairs)
+//     -- 64 FFMA2 per k against 6 LDS.128 (A as 4-k vectors of one row,
+//     broadcast; B as 4-column vectors 64 columns apart, conflict-free);
+//   * stages are released one iteration late (after the next stage's full
+//     barrier), the ptxas-proof ordering dgemm_dmma.cu documents.
+// Used when A and B meet TMA's 16-byte alignment rules; sgemm_ffma.cu
+// (cp.async) covers every other layout.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mmws_impl {
+namespace {
+
+using namespace mmws_dev;
+
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pack2(float lo, float hi) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 unpack2(f32x2 v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ void ffma2(f32x2& d, f32x2 a, f32x2 b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+}
+
+constexpr int BM = 128, BN = 256, BK = 16, STAGES = 3, CONSUMERS = 8;
+constexpr int THREADS = (CONSUMERS + 4) * 32;
+constexpr int KC_STAGES = 16;  // partial-sum chunk = 16 stages = 256 k
+constexpr int A_BYTES = BM * BK * 4, B_BYTES = BK * BN * 4;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int TOT_BYTES = CONSUMERS * 32 * 128 * 4;  // 128 floats per math lane
+constexpr int SMEM = STAGES * STAGE_BYTES + TOT_BYTES + 2 * STAGES * 8 + 128;
+
+__global__ void __launch_bounds__(THREADS, 1)
+    sgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA,
+                     const __grid_constant__ CUtensorMap tmB, float* __restrict__ C, int64_t ldc,
+                     int M, int N, int K, int tiles_m, int tiles_n, int vec_c) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  float4* tot = reinterpret_cast<float4*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + TOT_BYTES);
+  uint64_t* empty = full + STAGES;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int GROUP = 8;
+  const int tile = blockIdx.x;
+  const int per_group = GROUP * tiles_n;
+  const int first_m = (tile / per_group) * GROUP;
+  const int gm = min(tiles_m - first_m, GROUP);
+  const int tm = first_m + (tile % per_group) % gm;
+  const int tn = (tile % per_group) / gm;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CONSUMERS);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int KT = (K + BK - 1) / BK;
+
+  if (warp >= CONSUMERS) {
+    // ---------------- TMA producer ----------------
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    if (warp == CONSUMERS && lane == 0) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+      for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % STAGES;
+        if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
+        uint8_t* sa = smem + s * STAGE_BYTES;
+        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+        tma_load_2d(sa, &tmA, &full[s], kt * BK, tm * BM);
+        tma_load_2d(sa + A_BYTES, &tmB, &full[s], tn * BN, kt * BK);
+      }
+    }
+    return;
+  }
+
+  // ---------------- math warps ----------------
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+  const int g = lane >> 4, c = lane & 15;
+  const int row_base = warp * 16 + g * 8;  // rows row_base + i, i < 8
+  const int tid = threadIdx.x;             // < 256
+
+#pragma unroll
+  for (int q = 0; q < 32; ++q) tot[q * 256 + tid] = make_float4(0.f, 0.f, 0.f, 0.f);
+
+  f32x2 part[8][8];  // [row i][pair p]: columns c*4 + 64*(p>>1) + 2*(p&1) + {0,1}
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int p = 0; p < 8; ++p) part[i][p] = 0ull;
+
+  for (int kt = 0; kt < KT; ++kt) {
+    const int s = kt % STAGES;
+    mbar_wait(&full[s], (kt / STAGES) & 1);
+    if (kt > 0) {  // release the previous stage (see header)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[(kt - 1) % STAGES]);
+    }
+    const float* as = reinterpret_cast<const float*>(smem + s * STAGE_BYTES);
+    const float* bs = as + BM * BK;
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      float4 a4[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        a4[i] = *reinterpret_cast<const float4*>(as + (row_base + i) * BK + k4);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        f32x2 b2[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 b = *reinterpret_cast<const float4*>(bs + (k4 + kk) * BN + c * 4 + 64 * j);
+          b2[2 * j] = pack2(b.x, b.y);
+          b2[2 * j + 1] = pack2(b.z, b.w);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float a = kk == 0 ? a4[i].x : kk == 1 ? a4[i].y : kk == 2 ? a4[i].z : a4[i].w;
+          const f32x2 aa = pack2(a, a);
+#pragma unroll
+          for (int p = 0; p < 8; ++p) ffma2(part[i][p], aa, b2[p]);
+        }
+      }
+    }
+    if ((kt % KC_STAGES) == KC_STAGES - 1 || kt + 1 == KT) {
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {  // q = i*4 + j: row i, column group j
+        const int i = q >> 2, j = q & 3;
+        float4 t = tot[q * 256 + tid];
+        const float2 lo = unpack2(part[i][2 * j]), hi = unpack2(part[i][2 * j + 1]);
+        t.x += lo.x;
+        t.y += lo.y;
+        t.z += hi.x;
+        t.w += hi.y;
+        tot[q * 256 + tid] = t;
+        part[i][2 * j] = part[i][2 * j + 1] = 0ull;
+      }
+    }
+  }
+
+#pragma unroll
+  for (int q = 0; q < 32; ++q) {
+    const int i = q >> 2, j = q & 3;
+    const int r = tm * BM + row_base + i;
+    if (r >= M) continue;
+    const int col = tn * BN + c * 4 + 64 * j;
+    const float4 v = tot[q * 256 + tid];
+    float* crow = C + static_cast<int64_t>(r) * ldc;
+    if (vec_c && col + 3 < N) {
+      *reinterpret_cast<float4*>(crow + col) = v;
+    } else {
+      const float w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (col + e < N) crow[col + e] = w[e];
+    }
+  }
+}
+
+bool make_map_f32(const Launch& L, CUtensorMap* map, const float* base, int64_t inner,
+                  int64_t outer, int64_t ld, int box_inner, int box_outer) {
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * sizeof(float)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner),
+                             static_cast<cuuint32_t>(box_outer)};
+  const cuuint32_t estr[2] = {1, 1};
+  return L.encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool sgemm_tma_supported(int64_t lda, int64_t ldb, const float* A, const float* B) {
+  return lda % 4 == 0 && ldb % 4 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0 &&
+         reinterpret_cast<uintptr_t>(B) % 16 == 0;
+}
+
+cudaError_t launch_sgemm_tma(const Launch& L, int64_t M, int64_t N, int64_t K, const float* A,
+                             int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc) {
+  CUtensorMap ta, tb;
+  if (!make_map_f32(L, &ta, A, K, M, lda, BK, BM)) return cudaErrorInvalidValue;
+  if (!make_map_f32(L, &tb, B, N, K, ldb, BN, BK)) return cudaErrorInvalidValue;
+  cudaError_t e =
+      cudaFuncSetAttribute(sgemm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  if (e != cudaSuccess) return e;
+  const int tiles_m = static_cast<int>((M + BM - 1) / BM);
+  const int tiles_n = static_cast<int>((N + BN - 1) / BN);
+  const int vec_c = (ldc % 4 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0);
+  sgemm_tma_kernel<<<tiles_m * tiles_n, THREADS, SMEM, L.stream>>>(
+      ta, tb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), tiles_m,
+      tiles_n, vec_c);
+  L.count();
+  return cudaGetLastError();
+}
+
+}  // namespace mmws_impl

@@ -215,7 +215,9 @@ def test_config_c5_n32768_fp32_sampled_rows(ctx, oracle):
 
 
 def test_fp32_small_shapes(ctx, oracle):
-    for (m, k, n) in [(1, 1, 1), (3, 5, 7), (128, 128, 128), (129, 1000, 131), (1000, 37, 999)]:
+    # aligned shapes take the TMA kernel, the others the cp.async kernel
+    for (m, k, n) in [(1, 1, 1), (3, 5, 7), (128, 128, 128), (129, 1000, 131), (1000, 37, 999),
+                      (200, 1000, 1004), (257, 36, 260), (1, 4, 4)]:
         a = oracle.fill(oracle.DIST_NORMAL, 3, m, k, dtype=np.float32)
         b = oracle.fill(oracle.DIST_NORMAL, 4, k, n, dtype=np.float32)
         want = oracle.matmul_rows(list(range(m)), a, b)
