@@ -26,6 +26,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -147,6 +148,38 @@ class Context {
   mmws_gpu_ctx* ctx_ = nullptr;
   int rank_ = 0, world_ = 1;
 };
+
+// ---------------------------------------------------------------- device communicator
+// Ship rank 0's 128-byte NCCL id over any reference-style control plane that
+// offers my_rank(), world_size(), send_i64(dest, tag, v) and recv_i64(src, tag)
+// -- e.g. the reference's own mmws::Communicator from connect_from_env()
+// (launch.hpp:247-302), so existing launch scripts keep working.  Returns the
+// id on every rank.
+template <class Comm>
+std::vector<std::uint8_t> share_unique_id(Comm& comm, std::uint32_t tag = 0x4E43434Cu) {
+  std::vector<std::uint8_t> id(128);
+  if (comm.my_rank() == 0) {
+    id = Context::unique_id();
+    for (int r = 1; r < comm.world_size(); ++r)
+      for (int i = 0; i < 16; ++i) {
+        std::int64_t w;
+        std::memcpy(&w, id.data() + 8 * i, 8);
+        comm.send_i64(r, tag, w);
+      }
+  } else {
+    for (int i = 0; i < 16; ++i) {
+      const std::int64_t w = comm.recv_i64(0, tag);
+      std::memcpy(id.data() + 8 * i, &w, 8);
+    }
+  }
+  return id;
+}
+
+// One call per rank: the context's NCCL world mirrors the control plane's.
+template <class Comm>
+void comm_init_from(Context& ctx, Comm& comm) {
+  ctx.comm_init(comm.world_size(), comm.my_rank(), share_unique_id(comm));
+}
 
 // ---------------------------------------------------------------- partitions
 struct WorkAssignment {

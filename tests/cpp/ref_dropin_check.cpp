@@ -1,6 +1,7 @@
 // Compile-only proof that include/mmws_gpu.hpp is a drop-in for the
 // reference's own types: instantiated with mmws::Matrix from the unmodified
 // reference headers (built here only, where /root/reference exists).
+#include <mmws/comm.hpp>
 #include <mmws/matrix.hpp>
 #include <mmws/workshare.hpp>
 
@@ -12,4 +13,9 @@ mmws::Matrix via_gpu(mmws::gpu::Context& ctx, const mmws::Matrix& a, const mmws:
   auto [c, elapsed] = mmws::gpu::master_run(ctx, a, b);
   (void)elapsed;
   return mmws::bitwise_equal(s, t) ? c : mmws::gpu::matmul(ctx, a, b);
+}
+
+// the reference's own control plane bootstraps the NCCL world
+void bootstrap(mmws::gpu::Context& ctx, mmws::Communicator& comm) {
+  mmws::gpu::comm_init_from(ctx, comm);
 }

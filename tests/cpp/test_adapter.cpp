@@ -67,6 +67,18 @@ static bool bitwise_equal(const MatrixF64& x, const MatrixF64& y) {
          std::memcmp(x.data().data(), y.data().data(), x.size() * sizeof(double)) == 0;
 }
 
+// In-process two-rank control plane with the reference Communicator's
+// send_i64/recv_i64 surface (comm.hpp:49-77), for share_unique_id.
+struct FakeComm {
+  int rank, world;
+  std::vector<std::int64_t>* wire;  // rank 0 -> rank 1, FIFO
+  std::size_t* cursor;
+  int my_rank() const { return rank; }
+  int world_size() const { return world; }
+  void send_i64(int, std::uint32_t, std::int64_t v) { wire->push_back(v); }
+  std::int64_t recv_i64(int, std::uint32_t) { return (*wire)[(*cursor)++]; }
+};
+
 static void cpu_checks() {
   CHECK((G::split_rows(4, 3) == std::vector<G::WorkAssignment>{{0, 2}, {2, 1}, {3, 1}}));
   CHECK((G::split_rows(6, 3) == std::vector<G::WorkAssignment>{{0, 2}, {2, 2}, {4, 2}}));
@@ -83,6 +95,13 @@ static void cpu_checks() {
   CHECK_THROWS_AS(MatrixF64(2, 2, {1, 2, 3}), mmws::DimensionError);
   // no CPU fallback: without an sm_100 device the context cannot be created
   CHECK_THROWS_AS(G::Context(0), G::GpuError);
+  // the 128-byte NCCL id travels as 16 int64 scalars over the control plane
+  std::vector<std::int64_t> wire;
+  std::size_t cursor = 0;
+  FakeComm root{0, 2, &wire, &cursor}, worker{1, 2, &wire, &cursor};
+  const auto id0 = G::share_unique_id(root);
+  const auto id1 = G::share_unique_id(worker);
+  CHECK(wire.size() == 16 && id0.size() == 128 && id0 == id1);
 }
 
 static void gpu_checks() {

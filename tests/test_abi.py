@@ -141,8 +141,10 @@ def test_cpp_adapter_host_checks(tmp_path):
 @pytest.mark.skipif(not os.path.exists(os.path.join(REF_INC, "mmws", "matrix.hpp")),
                     reason="reference headers not present (GPU box)")
 def test_cpp_adapter_is_dropin_for_reference_matrix():
+    json_dir = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "print-json-dir"],
+                              capture_output=True, text=True).stdout.strip()
     subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Wextra", "-Werror",
-                    f"-I{REF_INC}", f"-I{ROOT}/include",
+                    f"-I{REF_INC}", f"-I{json_dir}", f"-I{ROOT}/include",
                     f"{ROOT}/tests/cpp/ref_dropin_check.cpp"], check=True)
 
 
