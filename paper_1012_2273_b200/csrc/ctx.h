@@ -21,6 +21,14 @@ struct mmws_gpu_ctx {
   cudaEvent_t evk0 = nullptr, evk1 = nullptr;  // around the row-block multiply
   double last_kernel_ms = 0.0;
   mmws_impl::EncodeTiledFn encode = nullptr;
+  // stream memory operations (cuStreamWriteValue32 / cuStreamWaitValue32) for
+  // the streamed host path; null if the driver does not offer them
+  CUresult (*write_value)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+  CUresult (*wait_value)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+  // streamed host path: [tile order | ready_a | ready_b | done] on the device
+  void* sched = nullptr;
+  size_t sched_bytes = 0;
+  int64_t sched_m = -1, sched_n = -1;  // shape the uploaded tile order belongs to
   uint64_t launches = 0;
   std::mutex mu;
 

@@ -59,11 +59,29 @@ using Big = Cfg<128, 128, 64, 32, 6, 1>;   // 8 math warps, 192 KB ring, 1 CTA/S
 using Small = Cfg<64, 64, 32, 32, 4, 2>;   // 4 math warps, 64 KB ring, 2+ CTAs/SM
 using Mid = Cfg<128, 64, 32, 32, 5, 1>;    // 8 math warps, 160 KB ring
 
-template <class K>
+// Poll an arrival flag (written by a cuStreamWriteValue32 behind an H2D copy).
+MMWS_DEVICE void wait_flag(const int* f) {
+  for (;;) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    if (v) return;
+    __nanosleep(200);
+  }
+}
+
+// STREAM = false: one CTA per tile, grouped rasterisation (the device-pointer
+// path).  STREAM = true: persistent CTAs walk a host-ordered tile list
+// (CTA b takes entries b, b + grid, ...), the producer waits for the A row
+// band and B column band of each tile to have arrived (flags), and the math
+// warps count finished tiles per tile row so a copy stream can ship C rows
+// back while the rest computes (host_pipeline.cu).  The per-element
+// arithmetic is the same either way.
+template <class K, bool STREAM>
 __global__ void __launch_bounds__(K::THREADS, K::MINB)
     dgemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB, double* __restrict__ C,
-                      int64_t ldc, int M, int N, int K_, int tiles_m, int tiles_n, int vec_ok) {
+                      int64_t ldc, int M, int N, int K_, int tiles_m, int tiles_n, int vec_ok,
+                      DmmaStream st) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   // 1024-byte aligned ring (128B-swizzle atoms); offsetting the __shared__
   // array itself keeps the shared address space visible, so fragment fetches
@@ -75,15 +93,27 @@ __global__ void __launch_bounds__(K::THREADS, K::MINB)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  // Grouped rasterisation: GROUP tile-rows advance together so the A panels
-  // and B panels of one wave are shared through L2.
-  constexpr int GROUP = 8;
-  const int tile = blockIdx.x;
-  const int per_group = GROUP * tiles_n;
-  const int first_m = (tile / per_group) * GROUP;
-  const int gm = min(tiles_m - first_m, GROUP);
-  const int tm = first_m + (tile % per_group) % gm;
-  const int tn = (tile % per_group) / gm;
+  // Tile coordinates.  One-shot: grouped rasterisation (GROUP tile-rows advance
+  // together so the A and B panels of one wave are shared through L2).
+  // Streamed: the host's arrival-ordered list.
+  auto tile_at = [&](int idx, int& tm, int& tn) {
+    if constexpr (STREAM) {
+      const int t = st.order[idx];
+      tm = t / tiles_n;
+      tn = t % tiles_n;
+    } else {
+      constexpr int GROUP = 8;
+      const int tile = blockIdx.x;
+      const int per_group = GROUP * tiles_n;
+      const int first_m = (tile / per_group) * GROUP;
+      const int gm = min(tiles_m - first_m, GROUP);
+      tm = first_m + (tile % per_group) % gm;
+      tn = (tile % per_group) / gm;
+    }
+  };
+  const int idx0 = STREAM ? static_cast<int>(blockIdx.x) : 0;
+  const int n_idx = STREAM ? st.count : 1;
+  const int idx_step = STREAM ? static_cast<int>(gridDim.x) : 1;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < K::STAGES; ++s) {
@@ -103,16 +133,26 @@ __global__ void __launch_bounds__(K::THREADS, K::MINB)
     if (warp == K::CONSUMERS && lane == 0) {
       tma_prefetch_desc(&tmA);
       tma_prefetch_desc(&tmB);
-      for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % K::STAGES;
-        if (kt >= K::STAGES) mbar_wait(&empty[s], ((kt / K::STAGES) - 1) & 1);
-        uint8_t* sa = smem + s * K::STAGE_BYTES;
-        uint8_t* sb = sa + K::A_BYTES;
-        mbar_arrive_expect_tx(&full[s], K::STAGE_BYTES);
-        tma_load_2d(sa, &tmA, &full[s], kt * K::BK, tm * K::BM);
+      int kg = 0;  // stage counter, continuous across tiles
+      for (int idx = idx0; idx < n_idx; idx += idx_step) {
+        int tm, tn;
+        tile_at(idx, tm, tn);
+        if constexpr (STREAM) {
+          wait_flag(st.ready_a + tm / st.band);
+          wait_flag(st.ready_b + tn / st.band);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        for (int kt = 0; kt < KT; ++kt, ++kg) {
+          const int s = kg % K::STAGES;
+          if (kg >= K::STAGES) mbar_wait(&empty[s], ((kg / K::STAGES) - 1) & 1);
+          uint8_t* sa = smem + s * K::STAGE_BYTES;
+          uint8_t* sb = sa + K::A_BYTES;
+          mbar_arrive_expect_tx(&full[s], K::STAGE_BYTES);
+          tma_load_2d(sa, &tmA, &full[s], kt * K::BK, tm * K::BM);
 #pragma unroll
-        for (int b = 0; b < K::BN / 16; ++b)
-          tma_load_2d(sb + b * 2048, &tmB, &full[s], tn * K::BN + b * 16, kt * K::BK);
+          for (int b = 0; b < K::BN / 16; ++b)
+            tma_load_2d(sb + b * 2048, &tmB, &full[s], tn * K::BN + b * 16, kt * K::BK);
+        }
       }
     }
     return;
@@ -142,75 +182,88 @@ __global__ void __launch_bounds__(K::THREADS, K::MINB)
       b_off[g8][q] = k * 128 + ((gid ^ (k & 7)) << 4);
     }
 
-  double acc[K::MI][K::NB][2][2];
-#pragma unroll
-  for (int i = 0; i < K::MI; ++i)
-#pragma unroll
-    for (int b = 0; b < K::NB; ++b)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) acc[i][b][e][0] = acc[i][b][e][1] = 0.0;
-
-  for (int kt = 0; kt < KT; ++kt) {
-    const int s = kt % K::STAGES;
-    mbar_wait(&full[s], (kt / K::STAGES) & 1);
-    // Release the PREVIOUS stage here, not at the end of its own iteration:
-    // ptxas sinks DMMAs below an arrive placed right after them, so the arrive
-    // could retire while LDS of that stage are still in flight and the next
-    // TMA would overwrite data being read.  Every DMMA of stage kt-1 sits in
-    // the basic block before this wait loop and has issued -- so all of its
-    // LDS have returned -- by the time we get here.
-    if (kt > 0) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[(kt - 1) % K::STAGES]);
-    }
-    const uint8_t* sa = smem + s * K::STAGE_BYTES;
-    const uint8_t* sb = sa + K::A_BYTES + (wn * K::NB) * 2048;
-#pragma unroll
-    for (int g8 = 0; g8 < 2; ++g8) {
-      double2 af[K::MI];
-      double2 bf[K::NB][2];
-#pragma unroll
-      for (int i = 0; i < K::MI; ++i)
-        af[i] = *reinterpret_cast<const double2*>(sa + a_off[i] + a_chunk[g8]);
-#pragma unroll
+  int kg = 0;  // stage counter, continuous across tiles
+  for (int idx = idx0; idx < n_idx; idx += idx_step) {
+    int tm, tn;
+    tile_at(idx, tm, tn);
+    double acc[K::MI][K::NB][2][2];
+  #pragma unroll
+    for (int i = 0; i < K::MI; ++i)
+  #pragma unroll
       for (int b = 0; b < K::NB; ++b)
-#pragma unroll
-        for (int q = 0; q < 2; ++q)
-          bf[b][q] = *reinterpret_cast<const double2*>(sb + b * 2048 + b_off[g8][q]);
-#pragma unroll
-      for (int q = 0; q < 2; ++q)
-#pragma unroll
+  #pragma unroll
+        for (int e = 0; e < 2; ++e) acc[i][b][e][0] = acc[i][b][e][1] = 0.0;
+
+    for (int kt = 0; kt < KT; ++kt, ++kg) {
+      const int s = kg % K::STAGES;
+      mbar_wait(&full[s], (kg / K::STAGES) & 1);
+      // Release the PREVIOUS stage here, not at the end of its own iteration:
+      // ptxas sinks DMMAs below an arrive placed right after them, so the arrive
+      // could retire while LDS of that stage are still in flight and the next
+      // TMA would overwrite data being read.  Every DMMA of stage kt-1 sits in
+      // the basic block before this wait loop and has issued -- so all of its
+      // LDS have returned -- by the time we get here.
+      if (kg > 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[(kg - 1) % K::STAGES]);
+      }
+      const uint8_t* sa = smem + s * K::STAGE_BYTES;
+      const uint8_t* sb = sa + K::A_BYTES + (wn * K::NB) * 2048;
+  #pragma unroll
+      for (int g8 = 0; g8 < 2; ++g8) {
+        double2 af[K::MI];
+        double2 bf[K::NB][2];
+  #pragma unroll
         for (int i = 0; i < K::MI; ++i)
-#pragma unroll
-          for (int b = 0; b < K::NB; ++b) {
-            const double a = q ? af[i].y : af[i].x;
-            dmma_8x8x4(acc[i][b][0][0], acc[i][b][0][1], a, q ? bf[b][1].x : bf[b][0].x);
-            dmma_8x8x4(acc[i][b][1][0], acc[i][b][1][1], a, q ? bf[b][1].y : bf[b][0].y);
-          }
+          af[i] = *reinterpret_cast<const double2*>(sa + a_off[i] + a_chunk[g8]);
+  #pragma unroll
+        for (int b = 0; b < K::NB; ++b)
+  #pragma unroll
+          for (int q = 0; q < 2; ++q)
+            bf[b][q] = *reinterpret_cast<const double2*>(sb + b * 2048 + b_off[g8][q]);
+  #pragma unroll
+        for (int q = 0; q < 2; ++q)
+  #pragma unroll
+          for (int i = 0; i < K::MI; ++i)
+  #pragma unroll
+            for (int b = 0; b < K::NB; ++b) {
+              const double a = q ? af[i].y : af[i].x;
+              dmma_8x8x4(acc[i][b][0][0], acc[i][b][0][1], a, q ? bf[b][1].x : bf[b][0].x);
+              dmma_8x8x4(acc[i][b][1][0], acc[i][b][1][1], a, q ? bf[b][1].y : bf[b][0].y);
+            }
+      }
+
     }
 
-  }
-
-  // ---------------- epilogue: registers -> global ----------------
-  // Lane owns row (.., sigma(gid)) and columns 4*tig .. 4*tig+3 of each box.
-#pragma unroll
-  for (int i = 0; i < K::MI; ++i) {
-    const int row = tm * K::BM + wm * K::WM + i * 8 + sig;
-    if (row >= M) continue;
-    double* crow = C + static_cast<int64_t>(row) * ldc;
-#pragma unroll
-    for (int b = 0; b < K::NB; ++b) {
-      const int col = tn * K::BN + (wn * K::NB + b) * 16 + 4 * tig;
-      const double v0 = acc[i][b][0][0], v1 = acc[i][b][1][0];
-      const double v2 = acc[i][b][0][1], v3 = acc[i][b][1][1];
-      if (vec_ok && col + 3 < N) {
-        reinterpret_cast<double2*>(crow + col)[0] = make_double2(v0, v1);
-        reinterpret_cast<double2*>(crow + col)[1] = make_double2(v2, v3);
-      } else {
-        if (col + 0 < N) crow[col + 0] = v0;
-        if (col + 1 < N) crow[col + 1] = v1;
-        if (col + 2 < N) crow[col + 2] = v2;
-        if (col + 3 < N) crow[col + 3] = v3;
+    // ---------------- epilogue: registers -> global ----------------
+    // Lane owns row (.., sigma(gid)) and columns 4*tig .. 4*tig+3 of each box.
+  #pragma unroll
+    for (int i = 0; i < K::MI; ++i) {
+      const int row = tm * K::BM + wm * K::WM + i * 8 + sig;
+      if (row >= M) continue;
+      double* crow = C + static_cast<int64_t>(row) * ldc;
+  #pragma unroll
+      for (int b = 0; b < K::NB; ++b) {
+        const int col = tn * K::BN + (wn * K::NB + b) * 16 + 4 * tig;
+        const double v0 = acc[i][b][0][0], v1 = acc[i][b][1][0];
+        const double v2 = acc[i][b][0][1], v3 = acc[i][b][1][1];
+        if (vec_ok && col + 3 < N) {
+          reinterpret_cast<double2*>(crow + col)[0] = make_double2(v0, v1);
+          reinterpret_cast<double2*>(crow + col)[1] = make_double2(v2, v3);
+        } else {
+          if (col + 0 < N) crow[col + 0] = v0;
+          if (col + 1 < N) crow[col + 1] = v1;
+          if (col + 2 < N) crow[col + 2] = v2;
+          if (col + 3 < N) crow[col + 3] = v3;
+        }
+      }
+    }
+    if constexpr (STREAM) {
+      // all math warps' stores of this tile are issued -> count the tile
+      asm volatile("bar.sync 1, %0;" ::"n"(K::CONSUMERS * 32) : "memory");
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(st.done + tm, 1);
       }
     }
   }
@@ -236,20 +289,40 @@ cudaError_t run(const Launch& L, int64_t M, int64_t N, int64_t Kd, const double*
   if (!make_map(L, &ta, A, Kd, M, lda, 16, K::BM)) return cudaErrorInvalidValue;
   if (!make_map(L, &tb, B, N, Kd, ldb, 16, 16)) return cudaErrorInvalidValue;
   const int smem = K::SMEM;
-  cudaError_t e = cudaFuncSetAttribute(dgemm_dmma_kernel<K>,
+  cudaError_t e = cudaFuncSetAttribute(dgemm_dmma_kernel<K, false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int tiles_m = static_cast<int>((M + K::BM - 1) / K::BM);
   const int tiles_n = static_cast<int>((N + K::BN - 1) / K::BN);
   const int vec_ok = (ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0);
-  dgemm_dmma_kernel<K><<<tiles_m * tiles_n, K::THREADS, smem, L.stream>>>(
+  dgemm_dmma_kernel<K, false><<<tiles_m * tiles_n, K::THREADS, smem, L.stream>>>(
       ta, tb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(Kd), tiles_m,
-      tiles_n, vec_ok);
+      tiles_n, vec_ok, DmmaStream{});
   L.count();
   return cudaGetLastError();
 }
 
 }  // namespace
+
+cudaError_t launch_dgemm_dmma_stream(const Launch& L, int64_t M, int64_t N, int64_t Kd,
+                                     const double* A, int64_t lda, const double* B, int64_t ldb,
+                                     double* C, int64_t ldc, const DmmaStream& st, int grid) {
+  using K = Big;
+  CUtensorMap ta, tb;
+  if (!make_map(L, &ta, A, Kd, M, lda, 16, K::BM)) return cudaErrorInvalidValue;
+  if (!make_map(L, &tb, B, N, Kd, ldb, 16, 16)) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(dgemm_dmma_kernel<K, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
+  if (e != cudaSuccess) return e;
+  const int tiles_m = static_cast<int>((M + K::BM - 1) / K::BM);
+  const int tiles_n = static_cast<int>((N + K::BN - 1) / K::BN);
+  const int vec_ok = (ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0);
+  dgemm_dmma_kernel<K, true><<<grid, K::THREADS, K::SMEM, L.stream>>>(
+      ta, tb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(Kd), tiles_m,
+      tiles_n, vec_ok, st);
+  L.count();
+  return cudaGetLastError();
+}
 
 cudaError_t launch_dgemm_dmma(const Launch& L, int cfg, int64_t M, int64_t N, int64_t K,
                               const double* A, int64_t lda, const double* B, int64_t ldb,

@@ -20,6 +20,7 @@
 
 #include "../../include/mmws_gpu.h"
 #include "ctx.h"
+#include "kernels.h"
 
 namespace mmws_impl {
 
@@ -44,6 +45,130 @@ int gemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, int64_t
     return sgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode, s);
 }
 
+// Streamed variant (fp64 DMMA, big problems): one persistent GEMM over the
+// whole C that starts on tiles whose A rows and B columns have already
+// crossed PCIe.  Copy-in interleaves 1024-row bands of A and 1024-column bands
+// of B, each followed by a cuStreamWriteValue32 flag; the kernel walks its
+// tiles in arrival order; a per-tile-row completion counter, awaited with
+// cuStreamWaitValue32, releases each finished 1024-row band of C to the
+// copy-out stream.  No launch-size wave quantisation, no panel-0 stall.
+int host_multiply_streamed(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
+                           const double* B, double* C, double* elapsed_s) {
+  constexpr int TILE = 128, BAND = 8;
+  const int64_t tiles_m = (m + TILE - 1) / TILE, tiles_n = (n + TILE - 1) / TILE;
+  const int64_t nba = (tiles_m + BAND - 1) / BAND, nbb = (tiles_n + BAND - 1) / BAND;
+  const int64_t T = tiles_m * tiles_n;
+  const size_t flag_ints = nba + nbb + tiles_m;
+  cudaError_t e;
+  if ((e = ensure(&ctx->sched, &ctx->sched_bytes, sizeof(int) * (T + flag_ints))) != cudaSuccess)
+    return cuda_fail(e, "matmul_host: schedule buffer");
+  int* order = static_cast<int*>(ctx->sched);
+  int* ready_a = order + T;
+  int* ready_b = ready_a + nba;
+  int* done = ready_b + nbb;
+
+  // Copy order: A band 0, then B bands two at a time interleaved with A bands
+  // until all of B has landed, then the remaining A bands.  Every tile needs
+  // all of its row's B columns to finish, so once B is complete each further
+  // A band unlocks -- and lets the kernel finish -- a whole band of C rows,
+  // which the copy-out stream ships while the next band computes.
+  std::vector<int64_t> seq_a(nba), seq_b(nbb);
+  std::vector<std::pair<char, int64_t>> copies;
+  auto push = [&](char w, int64_t i) {
+    (w == 'A' ? seq_a : seq_b)[i] = static_cast<int64_t>(copies.size());
+    copies.push_back({w, i});
+  };
+  int64_t ia = 0, ib = 0;
+  push('A', ia++);
+  while (ib < nbb) {
+    push('B', ib++);
+    if (ib < nbb) push('B', ib++);
+    if (ib < nbb && ia < nba) push('A', ia++);
+  }
+  while (ia < nba) push('A', ia++);
+  if (ctx->sched_m != m || ctx->sched_n != n) {  // tile order: by arrival, then row-major
+    std::vector<int64_t> key(T);
+    std::vector<int> ord(T);
+    for (int64_t t = 0; t < T; ++t) {
+      const int64_t tm = t / tiles_n, tn = t % tiles_n;
+      key[t] = std::max(seq_a[tm / BAND], seq_b[tn / BAND]) * T + t;
+      ord[t] = static_cast<int>(t);
+    }
+    std::sort(ord.begin(), ord.end(), [&](int x, int y) { return key[x] < key[y]; });
+    if ((e = cudaMemcpy(order, ord.data(), sizeof(int) * T, cudaMemcpyHostToDevice)))
+      return cuda_fail(e, "matmul_host: tile order");
+    ctx->sched_m = m;
+    ctx->sched_n = n;
+  }
+
+  cudaStream_t in = ctx->copy_in, comp = ctx->stream, out = ctx->copy_out;
+  if ((e = event_pool(ctx, 1)) != cudaSuccess) return cuda_fail(e, "matmul_host: events");
+  cudaEvent_t ev_reset = ctx->pool[0];
+  double* dA = static_cast<double*>(ctx->dA);
+  double* dB = static_cast<double*>(ctx->dB);
+  double* dC = static_cast<double*>(ctx->dC);
+  auto dptr = [](const void* p) { return static_cast<CUdeviceptr>(reinterpret_cast<uintptr_t>(p)); };
+
+  cudaEventRecord(ctx->ev0, comp);
+  if ((e = cudaMemsetAsync(ready_a, 0, sizeof(int) * flag_ints, comp)))
+    return cuda_fail(e, "matmul_host: reset flags");
+  cudaEventRecord(ev_reset, comp);
+  cudaStreamWaitEvent(in, ev_reset, 0);
+  cudaStreamWaitEvent(out, ev_reset, 0);
+  // ---- copy-in, each band followed by its arrival flag
+  for (const auto& [which, i] : copies) {
+    if (which == 'A') {
+      const int64_t r0 = i * BAND * TILE, rows = std::min<int64_t>(BAND * TILE, m - r0);
+      if ((e = cudaMemcpyAsync(dA + r0 * k, A + r0 * k, sizeof(double) * rows * k,
+                               cudaMemcpyHostToDevice, in)))
+        return cuda_fail(e, "matmul_host: H2D A");
+      if (ctx->write_value(in, dptr(ready_a + i), 1, 0) != CUDA_SUCCESS)
+        return fail(MMWS_GPU_ERR_CUDA, "matmul_host: cuStreamWriteValue32 failed");
+    } else {
+      const int64_t c0 = i * BAND * TILE, w = std::min<int64_t>(BAND * TILE, n - c0);
+      if ((e = cudaMemcpy2DAsync(dB + c0, sizeof(double) * n, B + c0, sizeof(double) * n,
+                                 sizeof(double) * w, k, cudaMemcpyHostToDevice, in)))
+        return cuda_fail(e, "matmul_host: H2D B");
+      if (ctx->write_value(in, dptr(ready_b + i), 1, 0) != CUDA_SUCCESS)
+        return fail(MMWS_GPU_ERR_CUDA, "matmul_host: cuStreamWriteValue32 failed");
+    }
+  }
+  // ---- one persistent multiply
+  DmmaStream st;
+  st.order = order;
+  st.count = static_cast<int>(T);
+  st.ready_a = ready_a;
+  st.ready_b = ready_b;
+  st.band = BAND;
+  st.done = done;
+  const int grid = static_cast<int>(std::min<int64_t>(T, ctx->num_sms));
+  if ((e = launch_dgemm_dmma_stream(ctx->launch(comp), m, n, k, dA, k, dB, n, dC, n, st, grid)))
+    return cuda_fail(e, "matmul_host: streamed dgemm");
+  // ---- copy-out: each 1024-row band once all its tiles are counted
+  for (int64_t i = 0; i < nba; ++i) {
+    const int64_t t0 = i * BAND, t1 = std::min<int64_t>(tiles_m, t0 + BAND);
+    for (int64_t tm = t0; tm < t1; ++tm)
+      if (ctx->wait_value(out, dptr(done + tm), static_cast<cuuint32_t>(tiles_n),
+                          CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+        return fail(MMWS_GPU_ERR_CUDA, "matmul_host: cuStreamWaitValue32 failed");
+    const int64_t r0 = t0 * TILE, rows = std::min<int64_t>(m, t1 * TILE) - r0;
+    if ((e = cudaMemcpyAsync(C + r0 * n, dC + r0 * n, sizeof(double) * rows * n,
+                             cudaMemcpyDeviceToHost, out)))
+      return cuda_fail(e, "matmul_host: D2H");
+  }
+  cudaEventRecord(ctx->ev1, out);
+  if ((e = cudaStreamSynchronize(out)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(comp)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(in)) != cudaSuccess)
+    return cuda_fail(e, "matmul_host: sync");
+  if (elapsed_s) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    *elapsed_s = ms * 1e-3;
+  }
+  return ok();
+}
+
 }  // namespace
 
 template <class T>
@@ -58,6 +183,14 @@ int host_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A
       (e = ensure(&ctx->dB, &ctx->dB_bytes, b_b)) != cudaSuccess ||
       (e = ensure(&ctx->dC, &ctx->dC_bytes, c_b)) != cudaSuccess)
     return cuda_fail(e, "matmul_host: device buffers");
+  if constexpr (sizeof(T) == 8) {
+    // big fp64 tensor-path problems whose dense device copies TMA can read
+    const int64_t tiles128 = ((m + 127) / 128) * ((n + 127) / 128);
+    if ((mode == MMWS_GPU_MODE_AUTO || mode == MMWS_GPU_MODE_DMMA) && ctx->write_value &&
+        ctx->wait_value && tiles128 >= 2 * static_cast<int64_t>(ctx->num_sms) && k % 2 == 0 &&
+        n % 2 == 0 && (n > 256 || k > 256))
+      return host_multiply_streamed(ctx, m, n, k, A, B, C, elapsed_s);
+  }
   T* dA = static_cast<T*>(ctx->dA);
   T* dB = static_cast<T*>(ctx->dB);
   T* dC = static_cast<T*>(ctx->dC);

@@ -27,6 +27,21 @@ struct Launch {
 // DMMA tile configurations (see dgemm_dmma.cu / DESIGN.md s3).
 enum DmmaCfg { DMMA_128x128 = 0, DMMA_64x64 = 1, DMMA_128x64 = 2 };
 
+// Streamed (persistent) DMMA schedule: tile list in arrival order, per-band
+// arrival flags, per-tile-row completion counters (see dgemm_dmma.cu).
+struct DmmaStream {
+  const int* order = nullptr;    // tm * tiles_n + tn, processed in this order
+  int count = 0;                 // entries in order
+  const int* ready_a = nullptr;  // [tile-row band] != 0 once A's rows have landed
+  const int* ready_b = nullptr;  // [tile-col band] != 0 once B's columns have landed
+  int band = 1;                  // tiles per band
+  int* done = nullptr;           // [tile row] finished tiles
+};
+// 128x128 tiles only; grid = number of persistent CTAs.
+cudaError_t launch_dgemm_dmma_stream(const Launch& L, int64_t M, int64_t N, int64_t K,
+                                     const double* A, int64_t lda, const double* B, int64_t ldb,
+                                     double* C, int64_t ldc, const DmmaStream& st, int grid);
+
 // C[M,N] = A[M,K] . B[K,N], row-major, accumulators from +0.0.  The TMA path
 // needs lda, ldb even and A, B 16-byte aligned (the caller packs otherwise).
 cudaError_t launch_dgemm_dmma(const Launch& L, int cfg, int64_t M, int64_t N, int64_t K,

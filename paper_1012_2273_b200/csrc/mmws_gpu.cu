@@ -199,6 +199,15 @@ int mmws_gpu_init(int device, mmws_gpu_ctx** out) {
     return fail(MMWS_GPU_ERR_CUDA, "mmws_gpu_init: cuTensorMapEncodeTiled unavailable");
   }
   ctx->encode = reinterpret_cast<EncodeTiledFn>(fn);
+  void* wr = nullptr;
+  void* wt = nullptr;
+  if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &wr, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess &&
+      cudaGetDriverEntryPoint("cuStreamWaitValue32", &wt, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess && wr && wt) {
+    ctx->write_value = reinterpret_cast<decltype(ctx->write_value)>(wr);
+    ctx->wait_value = reinterpret_cast<decltype(ctx->wait_value)>(wt);
+  }
   if ((e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = create_comm_stream(&ctx->comm_stream)) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking)) != cudaSuccess ||
@@ -220,7 +229,7 @@ int mmws_gpu_destroy(mmws_gpu_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->comm && nccl().ok) nccl().CommDestroy(ctx->comm);
-  for (void* p : {ctx->ws, ctx->dA, ctx->dB, ctx->dC, ctx->rbA, ctx->rbB, ctx->rbC,
+  for (void* p : {ctx->ws, ctx->dA, ctx->dB, ctx->dC, ctx->rbA, ctx->rbB, ctx->rbC, ctx->sched,
                   static_cast<void*>(ctx->sink)})
     if (p) cudaFree(p);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);

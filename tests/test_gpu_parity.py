@@ -293,7 +293,7 @@ def test_host_entry_matches_device_entry(ctx, oracle):
     assert normwise(cf.astype(np.float64), oracle.matmul_rows(list(range(257)), af, bf)) <= FP32_TOL
 
 
-@pytest.mark.parametrize("shape", [(1301, 1299, 1303), (2048, 1024, 4096)])
+@pytest.mark.parametrize("shape", [(1301, 1299, 1303), (2048, 1024, 4096), (2100, 1000, 2500)])
 def test_host_pipeline_bitwise_equals_device(ctx, oracle, shape):
     # big enough to take the overlapped (row-panel x column-block) host path
     T = torch()
