@@ -163,6 +163,17 @@ int mmws_gpu_graph_dgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, con
 int mmws_gpu_graph_launch(mmws_gpu_graph* graph, void* stream);
 int mmws_gpu_graph_destroy(mmws_gpu_graph* graph);
 
+/* ---------------------------------------------------------------- IPC (same-node peers) */
+/* Block until everything queued on the context stream has finished. */
+int mmws_gpu_synchronize(mmws_gpu_ctx* ctx);
+/* Export the device allocation holding `ptr` to another process on this node:
+ * 72 bytes = CUDA IPC handle (64) + byte offset of ptr in the allocation (8).
+ * Fails for memory that CUDA IPC cannot export (e.g. VMM allocations). */
+int mmws_gpu_ipc_export(mmws_gpu_ctx* ctx, const void* ptr, uint8_t out[72]);
+/* Map an exported pointer into this process (peer access enabled, mapping
+ * cached per allocation until the context is destroyed). */
+int mmws_gpu_ipc_open(mmws_gpu_ctx* ctx, const uint8_t in[72], void** ptr);
+
 /* ---------------------------------------------------------------- measurement */
 /* Runs one pipe-saturating probe kernel and returns its TFLOP/s. */
 int mmws_gpu_peak_probe(mmws_gpu_ctx* ctx, int which, int iters, double* tflops);
@@ -183,8 +194,11 @@ int mmws_gpu_comm_destroy(mmws_gpu_ctx* ctx);
  * with split_rows(m, nranks); rank r multiplies rows [offset_r, offset_r +
  * rows_r).  Unlike the reference's master (protocol.hpp:3-4) rank 0 also
  * computes its own block -- on a GPU box the master's device is a full worker.
- * Messages: A-slice 0->r (r >= 1), B broadcast from 0, C-slice r->0; ranks
- * with rows_r == 0 still take part (protocol.hpp:122-123).  *elapsed_s
+ * Data movement: B broadcast from 0, A-slices 0->r (r >= 1), and each
+ * worker's C rows into rank 0's C -- stored directly by the worker's GEMM
+ * epilogue through a CUDA IPC mapping of rank 0's C over NVLink (fused
+ * gather), or as NCCL C-slice messages when the allocation cannot be
+ * IPC-exported; ranks with rows_r == 0 still take part (protocol.hpp:122-123).  *elapsed_s
  * (rank 0, optional) is first send -> last receive measured on the device
  * (the bracket of protocol.hpp:63,105).  Synchronous on return. */
 int mmws_gpu_rowblock_dgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k,

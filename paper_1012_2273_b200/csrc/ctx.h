@@ -25,6 +25,14 @@ struct mmws_gpu_ctx {
   // the streamed host path; null if the driver does not offer them
   CUresult (*write_value)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
   CUresult (*wait_value)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+  // CUDA IPC (fused C gather of the row-block path)
+  CUresult (*mem_range)(CUdeviceptr*, size_t*, CUdeviceptr) = nullptr;
+  struct IpcMap {
+    unsigned char handle[64];
+    void* base;
+  };
+  std::vector<IpcMap> ipc_cache;
+  void* ipc_stage = nullptr;  // 256-byte device staging for the handle broadcast / barrier
   // streamed host path: [tile order | ready_a | ready_b | done] on the device
   void* sched = nullptr;
   size_t sched_bytes = 0;
@@ -73,6 +81,9 @@ cudaError_t ensure(void** buf, size_t* have, size_t bytes);
 int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
                    int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int mode,
                    cudaStream_t stream);
+// CUDA IPC: 64-byte handle of the allocation holding ptr + 8-byte offset.
+int ipc_export(mmws_gpu_ctx* ctx, const void* ptr, uint8_t out[72]);
+int ipc_open(mmws_gpu_ctx* ctx, const uint8_t in[72], void** ptr);
 // Host-buffer multiply with PCIe copies overlapped (host_pipeline.cu).
 template <class T>
 int host_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, const T* B,

@@ -129,6 +129,46 @@ int sgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const flo
   return e == cudaSuccess ? ok() : cuda_fail(e, "sgemm ffma");
 }
 
+int ipc_export(mmws_gpu_ctx* ctx, const void* ptr, uint8_t out[72]) {
+  if (!ptr || !out) return fail(MMWS_GPU_ERR_DOMAIN, "ipc_export: null argument");
+  if (!ctx->mem_range) return fail(MMWS_GPU_ERR_STATE, "ipc_export: cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (ctx->mem_range(&base, &size, static_cast<CUdeviceptr>(reinterpret_cast<uintptr_t>(ptr))) !=
+      CUDA_SUCCESS)
+    return fail(MMWS_GPU_ERR_CUDA, "ipc_export: pointer is not a device allocation");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(static_cast<uintptr_t>(base)));
+  if (e != cudaSuccess) return cuda_fail(e, "ipc_export: cudaIpcGetMemHandle");
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  const uint64_t offset = reinterpret_cast<uintptr_t>(ptr) - static_cast<uintptr_t>(base);
+  std::memcpy(out, &h, 64);
+  std::memcpy(out + 64, &offset, 8);
+  return ok();
+}
+
+int ipc_open(mmws_gpu_ctx* ctx, const uint8_t in[72], void** ptr) {
+  if (!in || !ptr) return fail(MMWS_GPU_ERR_DOMAIN, "ipc_open: null argument");
+  uint64_t offset = 0;
+  std::memcpy(&offset, in + 64, 8);
+  for (const auto& mp : ctx->ipc_cache)
+    if (std::memcmp(mp.handle, in, 64) == 0) {
+      *ptr = static_cast<char*>(mp.base) + offset;
+      return ok();
+    }
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, in, 64);
+  void* base = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_fail(e, "ipc_open: cudaIpcOpenMemHandle");
+  mmws_gpu_ctx::IpcMap mp;
+  std::memcpy(mp.handle, in, 64);
+  mp.base = base;
+  ctx->ipc_cache.push_back(mp);
+  *ptr = static_cast<char*>(base) + offset;
+  return ok();
+}
+
 }  // namespace mmws_impl
 
 using namespace mmws_impl;
@@ -199,6 +239,10 @@ int mmws_gpu_init(int device, mmws_gpu_ctx** out) {
     return fail(MMWS_GPU_ERR_CUDA, "mmws_gpu_init: cuTensorMapEncodeTiled unavailable");
   }
   ctx->encode = reinterpret_cast<EncodeTiledFn>(fn);
+  void* mr = nullptr;
+  if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &mr, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess)
+    ctx->mem_range = reinterpret_cast<decltype(ctx->mem_range)>(mr);
   void* wr = nullptr;
   void* wt = nullptr;
   if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &wr, cudaEnableDefault, &q) == cudaSuccess &&
@@ -216,7 +260,8 @@ int mmws_gpu_init(int device, mmws_gpu_ctx** out) {
       (e = cudaEventCreate(&ctx->ev1)) != cudaSuccess ||
       (e = cudaEventCreate(&ctx->evk0)) != cudaSuccess ||
       (e = cudaEventCreate(&ctx->evk1)) != cudaSuccess ||
-      (e = cudaMalloc(&ctx->sink, 4096 * sizeof(double))) != cudaSuccess) {
+      (e = cudaMalloc(&ctx->sink, 4096 * sizeof(double))) != cudaSuccess ||
+      (e = cudaMalloc(&ctx->ipc_stage, 256)) != cudaSuccess) {
     mmws_gpu_destroy(ctx);
     return cuda_fail(e, "mmws_gpu_init");
   }
@@ -229,7 +274,9 @@ int mmws_gpu_destroy(mmws_gpu_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->comm && nccl().ok) nccl().CommDestroy(ctx->comm);
+  for (auto& mp : ctx->ipc_cache) cudaIpcCloseMemHandle(mp.base);
   for (void* p : {ctx->ws, ctx->dA, ctx->dB, ctx->dC, ctx->rbA, ctx->rbB, ctx->rbC, ctx->sched,
+                  ctx->ipc_stage,
                   static_cast<void*>(ctx->sink)})
     if (p) cudaFree(p);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -403,6 +450,23 @@ int mmws_gpu_graph_destroy(mmws_gpu_graph* g) {
   if (g->graph) cudaGraphDestroy(g->graph);
   delete g;
   return ok();
+}
+
+// ------------------------------------------------------------------ IPC
+int mmws_gpu_synchronize(mmws_gpu_ctx* ctx) {
+  MMWS_CTX_GUARD(ctx);
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  return e == cudaSuccess ? ok() : cuda_fail(e, "synchronize");
+}
+
+int mmws_gpu_ipc_export(mmws_gpu_ctx* ctx, const void* ptr, uint8_t out[72]) {
+  MMWS_CTX_GUARD(ctx);
+  return ipc_export(ctx, ptr, out);
+}
+
+int mmws_gpu_ipc_open(mmws_gpu_ctx* ctx, const uint8_t in[72], void** ptr) {
+  MMWS_CTX_GUARD(ctx);
+  return ipc_open(ctx, in, ptr);
 }
 
 // ------------------------------------------------------------------ measurement

@@ -22,6 +22,8 @@ struct NcclApi {
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -42,12 +44,13 @@ inline const NcclApi& nccl() {
     MMWS_NCCL_SYM(Send, "ncclSend");
     MMWS_NCCL_SYM(Recv, "ncclRecv");
     MMWS_NCCL_SYM(Broadcast, "ncclBroadcast");
+    MMWS_NCCL_SYM(AllReduce, "ncclAllReduce");
     MMWS_NCCL_SYM(GroupStart, "ncclGroupStart");
     MMWS_NCCL_SYM(GroupEnd, "ncclGroupEnd");
     MMWS_NCCL_SYM(GetErrorString, "ncclGetErrorString");
 #undef MMWS_NCCL_SYM
     api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv &&
-             api.Broadcast && api.GroupStart && api.GroupEnd && api.GetErrorString;
+             api.Broadcast && api.AllReduce && api.GroupStart && api.GroupEnd && api.GetErrorString;
   });
   return api;
 }

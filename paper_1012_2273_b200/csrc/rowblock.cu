@@ -165,6 +165,42 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
   cudaEventRecord(evStart, comp);
   cudaStreamWaitEvent(comm, evStart, 0);
 
+  // ---- fused gather: map rank 0's C into every worker (CUDA IPC, NVLink peer
+  // memory); the workers' GEMM epilogues then store their rows straight into
+  // it and the C-slice messages disappear.  All ranks agree (allreduce-min of
+  // "export/open worked") before anything is queued; otherwise the C-slices
+  // travel as NCCL messages below.
+  unsigned char hbuf[128] = {0};
+  int fused = 0;
+  T* c_peer = nullptr;
+  {
+    unsigned char* stage = static_cast<unsigned char*>(ctx->ipc_stage);
+    if (me == 0) {
+      hbuf[72] = ipc_export(ctx, C, hbuf) == MMWS_GPU_OK ? 1 : 0;
+      if ((e = cudaMemcpyAsync(stage, hbuf, 80, cudaMemcpyHostToDevice, comm)))
+        return cuda_fail(e, "rowblock: stage IPC handle");
+    }
+    NCCL_TRY(nccl().Broadcast(stage, stage, 80, ncclUint8, 0, ctx->comm, comm), "broadcast C handle");
+    if ((e = cudaMemcpyAsync(hbuf, stage, 80, cudaMemcpyDeviceToHost, comm)) ||
+        (e = cudaStreamSynchronize(comm)))
+      return cuda_fail(e, "rowblock: fetch IPC handle");
+    int ok_here = hbuf[72];
+    if (me != 0 && ok_here) {
+      void* p = nullptr;
+      ok_here = ipc_open(ctx, hbuf, &p) == MMWS_GPU_OK ? 1 : 0;
+      c_peer = static_cast<T*>(p);
+    }
+    int* vote = reinterpret_cast<int*>(stage + 128);
+    if ((e = cudaMemcpyAsync(vote, &ok_here, sizeof(int), cudaMemcpyHostToDevice, comm)))
+      return cuda_fail(e, "rowblock: vote");
+    NCCL_TRY(nccl().AllReduce(vote, vote, 1, ncclInt32, ncclMin, ctx->comm, comm), "agree on fused gather");
+    if ((e = cudaMemcpyAsync(&fused, vote, sizeof(int), cudaMemcpyDeviceToHost, comm)) ||
+        (e = cudaStreamSynchronize(comm)))
+      return cuda_fail(e, "rowblock: vote result");
+    ok();  // a failed export/open only selects the NCCL gather
+  }
+  T* c_dst = me == 0 ? C : (fused ? c_peer + off[me] * n : c_loc);
+
   // ---- comm stream, part 1: all of B (protocol.hpp:73), once, as a broadcast ...
   void* bbuf = as_mut(b_loc);
   NCCL_TRY(nccl().Broadcast(bbuf, bbuf, k * n, dt, 0, ctx->comm, comm), "broadcast B");
@@ -192,16 +228,25 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
     const int64_t r0 = soff[me][s], rs = srows[me][s];
     if (me != 0) cudaStreamWaitEvent(comp, evA[s], 0);
     if (rs > 0)
-      if (int rc = gemm<T>(ctx, rs, n, k, a_loc + r0 * k, k, b_loc, n, c_loc + r0 * n, n, mode,
+      if (int rc = gemm<T>(ctx, rs, n, k, a_loc + r0 * k, k, b_loc, n, c_dst + r0 * n, n, mode,
                            comp))
         return rc;
     cudaEventRecord(evC[s], comp);
   }
   cudaEventRecord(ctx->evk1, comp);
 
-  // ---- comm stream, part 2: C-slices back into C's row blocks, rank order
-  // (protocol.hpp:85-103), one grouped exchange per sub-block
-  for (int s = 0; s < S; ++s) {
+  // ---- comm stream, part 2 (fused): the C rows are already in rank 0's C; one
+  // 4-byte allreduce after every rank's last multiply is the completion
+  // barrier (kernel completion makes the peer stores visible).
+  if (fused) {
+    cudaStreamWaitEvent(comm, evC[S - 1], 0);
+    int* token = reinterpret_cast<int*>(static_cast<unsigned char*>(ctx->ipc_stage) + 192);
+    NCCL_TRY(nccl().AllReduce(token, token, 1, ncclInt32, ncclSum, ctx->comm, comm),
+             "completion barrier");
+  }
+  // ---- comm stream, part 2 (fallback): C-slices back into C's row blocks, rank
+  // order (protocol.hpp:85-103), one grouped exchange per sub-block
+  for (int s = 0; !fused && s < S; ++s) {
     if (me != 0) cudaStreamWaitEvent(comm, evC[s], 0);
     NCCL_TRY(nccl().GroupStart(), "ncclGroupStart");
     if (me == 0) {

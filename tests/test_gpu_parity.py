@@ -278,6 +278,55 @@ def test_rowblock_nccl_path_single_rank(oracle):
         c2.close()
 
 
+def _ipc_child(conn):
+    import ctypes
+    import paper_1012_2273_b200 as P2
+    handle, m, n, k = conn.recv()
+    ctx = P2.Context(0)
+    lib = P2._abi.load()
+    ptr = ctypes.c_void_p()
+    buf = (ctypes.c_uint8 * 72).from_buffer_copy(handle)
+    assert lib.mmws_gpu_ipc_open(ctx.handle, buf, ctypes.byref(ptr)) == 0, P2._abi.last_error()
+    A = ctx.fill(P2.DIST_UNIFORM, 5, m, k)
+    B = ctx.fill(P2.DIST_UNIFORM, 6, k, n)
+    import torch as T
+    T.cuda.synchronize()
+    # this process's GEMM stores straight into the other process's buffer
+    assert lib.mmws_gpu_dgemm(ctx.handle, m, n, k, A.data_ptr(), k, B.data_ptr(), n, ptr.value,
+                              n, P2.MODE_AUTO, None) == 0, P2._abi.last_error()
+    assert lib.mmws_gpu_synchronize(ctx.handle) == 0
+    conn.send("done")
+    ctx.close()
+
+
+def test_ipc_peer_stores_from_another_process(ctx):
+    # The fused C gather of the row-block path: a worker's GEMM epilogue writes
+    # its rows into rank 0's C through a CUDA IPC mapping.  Two processes on one
+    # GPU exercise the same export/open/store path (no kernel waits on another).
+    import ctypes
+    import multiprocessing as mp
+    T = torch()
+    m, n, k = 700, 900, 500
+    Cbig = T.zeros((m + 8, n), dtype=T.float64, device="cuda")
+    out = (ctypes.c_uint8 * 72)()
+    lib = P._abi.load()
+    assert lib.mmws_gpu_ipc_export(ctx.handle, Cbig[4:].data_ptr(), out) == 0, P._abi.last_error()
+    mpc = mp.get_context("spawn")
+    a, b = mpc.Pipe()
+    proc = mpc.Process(target=_ipc_child, args=(b,))
+    proc.start()
+    a.send((bytes(out), m, n, k))
+    assert a.poll(240) and a.recv() == "done"
+    proc.join(60)
+    assert proc.exitcode == 0
+    A = ctx.fill(P.DIST_UNIFORM, 5, m, k)
+    B = ctx.fill(P.DIST_UNIFORM, 6, k, n)
+    want = host(ctx.dgemm(A, B))
+    got = host(Cbig)
+    assert (bits(got[4:4 + m]) == bits(want)).all()
+    assert (got[:4] == 0).all() and (got[4 + m:] == 0).all()
+
+
 # ----------------------------------------------------------------------------- boundary behaviour
 def test_host_entry_matches_device_entry(ctx, oracle):
     a = oracle.fill(oracle.DIST_UNIFORM, 5, 257, 300)
