@@ -95,23 +95,28 @@ Schedule make_schedule(int64_t m, int P) {
   return sc;
 }
 
-// Enqueue one master/worker round (no host synchronisation).  Rank 0 passes
-// device A, B, C; other ranks pass nulls and use library buffers.  On return
-// ctx->ev1 (rank 0) is recorded after the last C-slice has landed.
+// Enqueue one master/worker round.  Rank 0 passes device A, B, C (dense); the
+// other ranks pass nulls and use library buffers.  On return ctx->ev1 (rank 0)
+// is recorded after the last C row has landed.
 //
 // Without a communicator: one multiply.  With one (one rank per GPU, NCCL on
 // ctx->comm_stream, multiplies on ctx->stream -- a 1-rank world takes this
-// path too), pipelined so transfers hide behind the math:
-//   * comm order, identical on every rank: B (one broadcast -- all of it is
-//     needed before any output element can finish), then every rank's A-slice
-//     in S sub-blocks (grouped send/recv), then per sub-block s the C-slice
-//     gather (grouped send/recv straight into C's row block on rank 0);
-//   * a worker multiplies sub-block s as soon as B and A sub-block s have
-//     landed and ships its C rows while it multiplies sub-block s+1;
+// path too):
+//   * fused gather: rank 0's C is mapped into every worker (CUDA IPC over
+//     NVLink) and each worker's GEMM epilogue stores its rows straight into
+//     it; a 4-byte allreduce after the last multiply is the completion
+//     barrier.  The 80-byte handle is broadcast every call; whether the
+//     mapping works is voted on (allreduce-min) only when the handle changed,
+//     so a steady-state call needs no host round trip on rank 0;
+//   * comm order, identical on every rank: handle, [vote], B (one broadcast --
+//     all of it is needed before any output element can finish), then every
+//     rank's A-slice in S sub-blocks (grouped send/recv); without the fused
+//     gather, per sub-block s the C-slice messages (grouped send/recv into C's
+//     row block on rank 0);
+//   * a worker multiplies sub-block s as soon as B and A sub-block s landed;
 //   * rank 0 multiplies its own rows meanwhile (it holds A and B already).
-// Every launch
-// computes each element with the same kernel and k-order as a 1-GPU launch,
-// so the assembled C is bitwise the 1-GPU result.
+// Every launch computes each element with the same kernel and k-order as a
+// 1-GPU launch, so the assembled C is bitwise the 1-GPU result.
 template <class T>
 int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, const T* B,
                      T* C, int mode, bool bracket = true) {
@@ -146,60 +151,60 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
   cudaEvent_t* evC = evA + S;
   cudaEvent_t evB = evC[S], evStart = evC[S + 1], evJoin = evC[S + 2];
 
-  const T* a_loc = A;
-  const T* b_loc = B;
-  T* c_loc = C;
-  if (me != 0) {
-    if ((e = ensure(&ctx->rbA, &ctx->rbA_bytes, sizeof(T) * (rows[me] * k + 1))) != cudaSuccess ||
-        (e = ensure(&ctx->rbB, &ctx->rbB_bytes, sizeof(T) * k * n)) != cudaSuccess ||
-        (e = ensure(&ctx->rbC, &ctx->rbC_bytes, sizeof(T) * (rows[me] * n + 1))) != cudaSuccess)
-      return cuda_fail(e, "rowblock: worker buffers");
-    a_loc = static_cast<const T*>(ctx->rbA);
-    b_loc = static_cast<const T*>(ctx->rbB);
-    c_loc = static_cast<T*>(ctx->rbC);
-  }
-
   // the exchange starts after everything already queued on the compute stream
   // (e.g. the H2D copies of master_run_host)
   if (me == 0 && bracket) cudaEventRecord(ctx->ev0, comp);  // first send
   cudaEventRecord(evStart, comp);
   cudaStreamWaitEvent(comm, evStart, 0);
 
-  // ---- fused gather: map rank 0's C into every worker (CUDA IPC, NVLink peer
-  // memory); the workers' GEMM epilogues then store their rows straight into
-  // it and the C-slice messages disappear.  All ranks agree (allreduce-min of
-  // "export/open worked") before anything is queued; otherwise the C-slices
-  // travel as NCCL messages below.
-  unsigned char hbuf[128] = {0};
-  int fused = 0;
+  // ---- fused gather set-up (see above)
+  unsigned char* stage = static_cast<unsigned char*>(ctx->ipc_stage);
+  unsigned char hbuf[80] = {0};
+  if (me == 0) {
+    hbuf[72] = ipc_export(ctx, C, hbuf) == MMWS_GPU_OK ? 1 : 0;
+    if ((e = cudaMemcpyAsync(stage, hbuf, 80, cudaMemcpyHostToDevice, comm)))
+      return cuda_fail(e, "rowblock: stage IPC handle");
+  }
+  NCCL_TRY(nccl().Broadcast(stage, stage, 80, ncclUint8, 0, ctx->comm, comm), "broadcast C handle");
+  if (me != 0 && ((e = cudaMemcpyAsync(hbuf, stage, 80, cudaMemcpyDeviceToHost, comm)) ||
+                  (e = cudaStreamSynchronize(comm))))
+    return cuda_fail(e, "rowblock: fetch IPC handle");
   T* c_peer = nullptr;
-  {
-    unsigned char* stage = static_cast<unsigned char*>(ctx->ipc_stage);
-    if (me == 0) {
-      hbuf[72] = ipc_export(ctx, C, hbuf) == MMWS_GPU_OK ? 1 : 0;
-      if ((e = cudaMemcpyAsync(stage, hbuf, 80, cudaMemcpyHostToDevice, comm)))
-        return cuda_fail(e, "rowblock: stage IPC handle");
-    }
-    NCCL_TRY(nccl().Broadcast(stage, stage, 80, ncclUint8, 0, ctx->comm, comm), "broadcast C handle");
-    if ((e = cudaMemcpyAsync(hbuf, stage, 80, cudaMemcpyDeviceToHost, comm)) ||
-        (e = cudaStreamSynchronize(comm)))
-      return cuda_fail(e, "rowblock: fetch IPC handle");
-    int ok_here = hbuf[72];
-    if (me != 0 && ok_here) {
-      void* p = nullptr;
-      ok_here = ipc_open(ctx, hbuf, &p) == MMWS_GPU_OK ? 1 : 0;
-      c_peer = static_cast<T*>(p);
-    }
+  int ok_here = hbuf[72];
+  if (me != 0 && ok_here) {
+    void* p = nullptr;
+    ok_here = ipc_open(ctx, hbuf, &p) == MMWS_GPU_OK ? 1 : 0;
+    c_peer = static_cast<T*>(p);
+  }
+  int fused = ctx->last_fused;
+  if (fused < 0 || std::memcmp(hbuf, ctx->last_handle, 80) != 0) {  // new handle: vote
     int* vote = reinterpret_cast<int*>(stage + 128);
     if ((e = cudaMemcpyAsync(vote, &ok_here, sizeof(int), cudaMemcpyHostToDevice, comm)))
       return cuda_fail(e, "rowblock: vote");
-    NCCL_TRY(nccl().AllReduce(vote, vote, 1, ncclInt32, ncclMin, ctx->comm, comm), "agree on fused gather");
+    NCCL_TRY(nccl().AllReduce(vote, vote, 1, ncclInt32, ncclMin, ctx->comm, comm),
+             "agree on fused gather");
     if ((e = cudaMemcpyAsync(&fused, vote, sizeof(int), cudaMemcpyDeviceToHost, comm)) ||
         (e = cudaStreamSynchronize(comm)))
       return cuda_fail(e, "rowblock: vote result");
-    ok();  // a failed export/open only selects the NCCL gather
+    std::memcpy(ctx->last_handle, hbuf, 80);
+    ctx->last_fused = fused;
   }
-  T* c_dst = me == 0 ? C : (fused ? c_peer + off[me] * n : c_loc);
+  ok();  // a failed export/open only selects the NCCL gather
+
+  const T* a_loc = A;
+  const T* b_loc = B;
+  T* c_loc = C;
+  if (me != 0) {
+    if ((e = ensure(&ctx->rbA, &ctx->rbA_bytes, sizeof(T) * (rows[me] * k + 1))) != cudaSuccess ||
+        (e = ensure(&ctx->rbB, &ctx->rbB_bytes, sizeof(T) * k * n)) != cudaSuccess ||
+        (!fused &&
+         (e = ensure(&ctx->rbC, &ctx->rbC_bytes, sizeof(T) * (rows[me] * n + 1))) != cudaSuccess))
+      return cuda_fail(e, "rowblock: worker buffers");
+    a_loc = static_cast<const T*>(ctx->rbA);
+    b_loc = static_cast<const T*>(ctx->rbB);
+    c_loc = fused ? c_peer + off[me] * n : static_cast<T*>(ctx->rbC);
+  }
+  T* c_dst = c_loc;  // rank 0: C; workers: rank 0's C (fused) or the local slice
 
   // ---- comm stream, part 1: all of B (protocol.hpp:73), once, as a broadcast ...
   void* bbuf = as_mut(b_loc);
@@ -255,7 +260,7 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
           NCCL_TRY(nccl().Recv(C + (off[r] + soff[r][s]) * n, srows[r][s] * n, dt, r, ctx->comm,
                                comm), "recv C-slice");
     } else if (srows[me][s] > 0) {
-      NCCL_TRY(nccl().Send(c_loc + soff[me][s] * n, srows[me][s] * n, dt, 0, ctx->comm, comm),
+      NCCL_TRY(nccl().Send(c_dst + soff[me][s] * n, srows[me][s] * n, dt, 0, ctx->comm, comm),
                "send C-slice");
     }
     NCCL_TRY(nccl().GroupEnd(), "ncclGroupEnd");
@@ -357,6 +362,7 @@ int mmws_gpu_comm_init(mmws_gpu_ctx* ctx, int nranks, int rank, const uint8_t id
   NCCL_TRY(nccl().CommInitRank(&ctx->comm, nranks, uid, rank), "ncclCommInitRank");
   ctx->nranks = nranks;
   ctx->rank = rank;
+  ctx->last_fused = -1;
   return ok();
 }
 
@@ -368,6 +374,7 @@ int mmws_gpu_comm_destroy(mmws_gpu_ctx* ctx) {
   }
   ctx->nranks = 1;
   ctx->rank = 0;
+  ctx->last_fused = -1;
   return ok();
 }
 
