@@ -47,7 +47,8 @@ def metric_name() -> str:
 def workload_config(n: int, n_gpus: int, mode: str) -> dict:
     return {
         "workload": f"configs[3]: square fp64 GEMM N={n}, row-block master/worker over {n_gpus} GPU(s), "
-                    "B broadcast + C gather via NCCL (A,B resident on rank 0)",
+                    "B broadcast + A scatter via NCCL, C rows stored by the GEMM epilogue into rank 0 "
+                    "over NVLink (A,B resident on rank 0)",
         "n": n, "mode": mode, "parallelism": f"rowblock{n_gpus}",
         "l2": "no flush: inputs are 3 x 8N^2 = %.1f GB >> 126 MB L2" % (3 * 8 * n * n / 1e9),
     }
@@ -283,6 +284,11 @@ def run_ours(args) -> None:
         s = cpu_reference_sample(n)
         cpu = {k: s[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
+    if root and world > 1:  # cost model of this schedule at the measured 1-GPU kernel rate
+        t_model, _, _ = P.rowblock_cost(n, n, n, world, 8, 770e9, 2.0 * rows0 * n * n / (kern_avg_ms / 1e3))
+        model = {"predicted_ms_per_step": t_model * 1e3, "link_GBps": 770}
+    else:
+        model = None
     if root:
         line = {
             "metric": metric_name(), "value": value, "unit": "GFLOP/s", "n_gpus": world,
@@ -305,6 +311,7 @@ def run_ours(args) -> None:
                     "seconds_per_step": e2e_s,
                     "entry": "mmws_gpu_master_run_host (C ABI, pinned host A/B/C)"},
             "gpu_launches": launches_total,
+            "cost_model": model,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

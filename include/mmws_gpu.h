@@ -222,6 +222,14 @@ int mmws_gpu_master_run_host_f32(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_
  * kernel(s) in the most recent row-block / master_run call. */
 int mmws_gpu_last_kernel_ms(mmws_gpu_ctx* ctx, double* ms);
 
+/* Cost model of one row-block round (the analogue of the reference's
+ * cost_model.hpp:36-70): predicted seconds given the NVLink bandwidth per
+ * direction and the per-GPU multiply rate, plus rank 0's egress (B once + the
+ * workers' A rows) and ingress (the workers' C rows) in bytes.  Host-only. */
+int mmws_gpu_rowblock_cost(int64_t m, int64_t n, int64_t k, int nranks, int elem_bytes,
+                           double link_bytes_per_s, double gemm_flops_per_s, double* seconds,
+                           double* root_egress_bytes, double* root_ingress_bytes);
+
 /* The message plan rank 0 executes for (m, k, n, nranks), in issue order --
  * the analogue of the reference's Communicator traffic log (comm.hpp:24-32)
  * used by its protocol-shape test (test_protocol.cpp:99-137).  Host-only.

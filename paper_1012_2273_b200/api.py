@@ -101,6 +101,17 @@ def rowblock_plan(m: int, n: int, k: int, nranks: int):
                  dir=names[dirs[i]]) for i in range(e)]
 
 
+def rowblock_cost(m: int, n: int, k: int, nranks: int, elem_bytes: int = 8,
+                  link_bytes_per_s: float = 770e9, gemm_flops_per_s: float = 36.4e12):
+    """Predicted row-block round (seconds, rank 0 egress bytes, ingress bytes);
+    defaults: measured B200 peer-copy bandwidth per direction
+    (B200_PROFILING.md) and the measured 1-GPU fp64 DMMA rate."""
+    t, eg, ing = C.c_double(), C.c_double(), C.c_double()
+    _check(_lib().mmws_gpu_rowblock_cost(m, n, k, nranks, elem_bytes, link_bytes_per_s,
+                                         gemm_flops_per_s, C.byref(t), C.byref(eg), C.byref(ing)))
+    return t.value, eg.value, ing.value
+
+
 def nccl_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     _check(_lib().mmws_gpu_nccl_unique_id(buf))

@@ -411,6 +411,41 @@ int mmws_gpu_last_kernel_ms(mmws_gpu_ctx* ctx, double* ms) {
   return ok();
 }
 
+int mmws_gpu_rowblock_cost(int64_t m, int64_t n, int64_t k, int nranks, int elem_bytes,
+                           double link_bytes_per_s, double gemm_flops_per_s, double* seconds,
+                           double* root_egress_bytes, double* root_ingress_bytes) {
+  // The analogue of the reference's cost model (cost_model.hpp:36-70, paper
+  // s3.1.1: ((P-1)N^2 + 2N)(tc + tf) datums through the master) for this
+  // schedule.  Rank 0's NVLink egress carries B once (broadcast) plus the
+  // workers' A rows; its ingress carries the workers' C rows (peer stores).
+  // Time = B broadcast + the largest first A sub-block + the slowest rank's
+  // multiply; the C rows land while tiles finish (fused gather), so there is
+  // no gather tail.  Per-op latencies are ignored (microseconds vs ms).
+  if (m <= 0 || n <= 0 || k <= 0)
+    return fail(MMWS_GPU_ERR_DIMENSION, "rowblock_cost: dimensions must be positive");
+  if (nranks < 1 || (elem_bytes != 4 && elem_bytes != 8) || !(link_bytes_per_s > 0) ||
+      !(gemm_flops_per_s > 0))
+    return fail(MMWS_GPU_ERR_DOMAIN, "rowblock_cost: bad nranks / element size / rates");
+  const Schedule sc = make_schedule(m, nranks);
+  const double eb = elem_bytes;
+  int64_t rows_max = 0, a_rows = 0, a0_max = 0;
+  for (int r = 0; r < nranks; ++r) {
+    rows_max = std::max(rows_max, sc.rows[r]);
+    if (r > 0) {
+      a_rows += sc.rows[r];
+      a0_max = std::max(a0_max, sc.srows[r][0]);
+    }
+  }
+  const double egress = nranks > 1 ? eb * (static_cast<double>(k) * n + static_cast<double>(a_rows) * k) : 0.0;
+  const double ingress = nranks > 1 ? eb * static_cast<double>(a_rows) * n : 0.0;
+  double t = 2.0 * static_cast<double>(rows_max) * n * k / gemm_flops_per_s;
+  if (nranks > 1) t += eb * (static_cast<double>(k) * n + static_cast<double>(a0_max) * k) / link_bytes_per_s;
+  if (seconds) *seconds = t;
+  if (root_egress_bytes) *root_egress_bytes = egress;
+  if (root_ingress_bytes) *root_ingress_bytes = ingress;
+  return ok();
+}
+
 int mmws_gpu_rowblock_plan(int64_t m, int64_t n, int64_t k, int nranks, int32_t* peer,
                            int32_t* tag, int32_t* kind, int64_t* count, int64_t* row0,
                            int32_t* dir, int32_t* n_entries) {

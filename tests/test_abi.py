@@ -153,3 +153,28 @@ def test_cpp_adapter_gpu_checks(tmp_path):
     exe = _compile_adapter(tmp_path)
     r = subprocess.run([str(exe), "gpu"], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_rowblock_cost_model():
+    # The reference's cost-model checks (test_cost_model.cpp / acceptance.cpp:172-202)
+    # transposed to this schedule: traffic formulas, monotone in N and P.
+    n, bw, fl = 16384, 770e9, 36.4e12
+    t1, e1, i1 = P.rowblock_cost(n, n, n, 1, 8, bw, fl)
+    assert t1 == pytest.approx(2 * n ** 3 / fl) and e1 == 0 and i1 == 0
+    for p in (2, 4, 8):
+        t, eg, ing = P.rowblock_cost(n, n, n, p, 8, bw, fl)
+        rows0 = P.split_rows(n, p)[0][1]
+        assert eg == 8 * (n * n + (n - rows0) * n)       # B once + the workers' A rows
+        assert ing == 8 * (n - rows0) * n                # the workers' C rows
+        assert t < t1 and t1 / (p * t) > 0.85            # >= 85% efficiency target
+    prev = 0.0
+    for nn in (1000, 2000, 4096, 8192):
+        t, _, _ = P.rowblock_cost(nn, nn, nn, 8, 8, bw, fl)
+        assert t > prev
+        prev = t
+    # fp32 halves the bytes
+    _, eg64, _ = P.rowblock_cost(4096, 4096, 4096, 4, 8, bw, fl)
+    _, eg32, _ = P.rowblock_cost(4096, 4096, 4096, 4, 4, bw, fl)
+    assert eg32 * 2 == eg64
+    with pytest.raises(P.DomainError):
+        P.rowblock_cost(10, 10, 10, 2, 3, bw, fl)
