@@ -4,8 +4,9 @@
 Workload (BASELINE.json configs[3], the config the metric's "1/2/4/8 B200" and
 the >=70%-of-FP64-peak target are quoted on): square fp64 GEMM C = A.B at
 N = 16384, A and B uniform [-1,1) from splitmix64 seeds 0/1, row-block
-(master/worker) partition of A over the n_gpus ranks, B broadcast and C
-gathered to rank 0 over NCCL -- the reference's master_run / worker_run
+(master/worker) partition of A over the n_gpus ranks, B broadcast and A
+scattered over NCCL, each worker's C rows stored by its GEMM epilogue straight
+into rank 0's C over NVLink (CUDA IPC) -- the reference's master_run / worker_run
 (protocol.hpp:50-147) on B200s.  One step = one master/worker round with A, B
 resident in rank 0's HBM (first send -> last receive, protocol.hpp:63,105).
 Total work is fixed as n_gpus grows ("strong" scaling).
