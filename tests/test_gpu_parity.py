@@ -386,6 +386,32 @@ def test_strided_views_and_unaligned_leading_dims(ctx, oracle):
         assert (cb[:, :3] == 0).all() and (cb[:, 202:] == 0).all()
 
 
+@pytest.mark.parametrize("shape", [(1, 1, 1), (5, 3, 7), (129, 200, 131), (300, 17, 257),
+                                   (1000, 64, 1001), (2400, 300, 2500)])
+def test_no_writes_outside_c(ctx, shape):
+    # canary frame around a strided C view: every mode must write exactly C
+    T = torch()
+    m, k, n = shape
+    A = ctx.fill(P.DIST_UNIFORM, 1, m, k)
+    B = ctx.fill(P.DIST_UNIFORM, 2, k, n)
+    for mode in FP64_MODES:
+        buf = T.full((m + 2, n + 3), -7.5, dtype=T.float64, device="cuda")
+        C = buf[1:m + 1, 1:n + 1]
+        ctx.dgemm(A, B, C, mode=mode)
+        b = host(buf)
+        assert (b[0] == -7.5).all() and (b[m + 1] == -7.5).all(), mode
+        assert (b[:, 0] == -7.5).all() and (b[:, n + 1:] == -7.5).all(), mode
+        assert not np.isnan(b[1:m + 1, 1:n + 1]).any()
+    Af, Bf = A.float(), B.float()
+    for sl in (slice(None), slice(0, k)):
+        buf = T.full((m + 2, n + 5), -7.5, dtype=T.float32, device="cuda")
+        C = buf[1:m + 1, 4:n + 4]
+        ctx.sgemm(Af[:, sl], Bf[sl], C)
+        b = host(buf)
+        assert (b[0] == -7.5).all() and (b[m + 1] == -7.5).all()
+        assert (b[:, :4] == -7.5).all() and (b[:, n + 4:] == -7.5).all()
+
+
 def test_errors_map_to_reference_types(ctx):
     T = torch()
     a = T.zeros((2, 3), dtype=T.float64, device="cuda")
