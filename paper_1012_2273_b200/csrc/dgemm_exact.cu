@@ -116,6 +116,129 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-fed, warp-specialised variant (same per-thread arithmetic and layout):
+// a producer warpgroup streams A[128 x 16] and B[16 x 128] k-slices with TMA
+// into a 4-stage mbarrier ring and donates its registers to the 8 math warps
+// (setmaxnreg 40 / 232), so the math warps issue nothing but LDS, DMUL and
+// DADD -- no cp.async address arithmetic, no __syncthreads per k-tile.  Stages
+// are released one iteration late (see dgemm_dmma.cu).  Zero-filled TMA
+// out-of-bounds boxes are the (+0)*(+0) padding discussed above.
+constexpr int T_STAGES = 4, T_CONSUMERS = 8, T_THREADS = (T_CONSUMERS + 4) * 32;
+constexpr int T_A_BYTES = BM * BK * 8, T_B_BYTES = BK * BN * 8;
+constexpr int T_STAGE = T_A_BYTES + T_B_BYTES;
+constexpr int T_SMEM = T_STAGES * T_STAGE + 2 * T_STAGES * 8 + 128;
+
+__global__ void __launch_bounds__(T_THREADS, 1)
+    dgemm_exact_tma_kernel(const __grid_constant__ CUtensorMap tmA,
+                           const __grid_constant__ CUtensorMap tmB, double* __restrict__ C,
+                           int64_t ldc, int M, int N, int K, int tiles_m, int tiles_n) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + T_STAGES * T_STAGE);
+  uint64_t* empty = full + T_STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int GROUP = 8;
+  const int tile = blockIdx.x;
+  const int per_group = GROUP * tiles_n;
+  const int first_m = (tile / per_group) * GROUP;
+  const int gm = min(tiles_m - first_m, GROUP);
+  const int tm = first_m + (tile % per_group) % gm;
+  const int tn = (tile % per_group) / gm;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < T_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], T_CONSUMERS);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int KT = (K + BK - 1) / BK;
+
+  if (warp >= T_CONSUMERS) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    if (warp == T_CONSUMERS && lane == 0) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+      for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % T_STAGES;
+        if (kt >= T_STAGES) mbar_wait(&empty[s], ((kt / T_STAGES) - 1) & 1);
+        uint8_t* sa = smem + s * T_STAGE;
+        mbar_arrive_expect_tx(&full[s], T_STAGE);
+        tma_load_2d(sa, &tmA, &full[s], kt * BK, tm * BM);
+        tma_load_2d(sa + T_A_BYTES, &tmB, &full[s], tn * BN, kt * BK);
+      }
+    }
+    return;
+  }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  double acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+
+  for (int kt = 0; kt < KT; ++kt) {
+    const int s = kt % T_STAGES;
+    mbar_wait(&full[s], (kt / T_STAGES) & 1);
+    if (kt > 0) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[(kt - 1) % T_STAGES]);
+    }
+    const double* as = reinterpret_cast<const double*>(smem + s * T_STAGE);  // [BM][BK]
+    const double* bs = as + BM * BK;                                          // [BK][BN]
+#pragma unroll
+    for (int k = 0; k < BK; k += 2) {
+      double2 a2[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        a2[i] = *reinterpret_cast<const double2*>(as + (ty * 2 + 32 * (i >> 1) + (i & 1)) * BK + k);
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        double b[8];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const double2 bv = *reinterpret_cast<const double2*>(bs + (k + kk) * BN + tx * 2 + 32 * v);
+          b[2 * v] = bv.x;
+          b[2 * v + 1] = bv.y;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const double a = kk ? a2[i].y : a2[i].x;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(a, b[j]));
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = tm * BM + ty * 2 + 32 * (i >> 1) + (i & 1);
+    if (r >= M) continue;
+    double* crow = C + static_cast<int64_t>(r) * ldc;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = tn * BN + tx * 2 + 32 * (j >> 1) + (j & 1);
+      if (c < N) crow[c] = acc[i][j];
+    }
+  }
+}
+
+bool make_map_f64(const Launch& L, CUtensorMap* map, const double* base, int64_t inner,
+                  int64_t outer, int64_t ld, int box_inner, int box_outer) {
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * sizeof(double)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner),
+                             static_cast<cuuint32_t>(box_outer)};
+  const cuuint32_t estr[2] = {1, 1};
+  return L.encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 cudaError_t launch_dgemm_exact(const Launch& L, int64_t M, int64_t N, int64_t K, const double* A,
@@ -123,6 +246,20 @@ cudaError_t launch_dgemm_exact(const Launch& L, int64_t M, int64_t N, int64_t K,
                                int64_t ldc) {
   const int tiles_m = static_cast<int>((M + BM - 1) / BM);
   const int tiles_n = static_cast<int>((N + BN - 1) / BN);
+  if (lda % 2 == 0 && ldb % 2 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0 &&
+      reinterpret_cast<uintptr_t>(B) % 16 == 0) {  // TMA can describe both operands
+    CUtensorMap ta, tb;
+    if (!make_map_f64(L, &ta, A, K, M, lda, BK, BM) || !make_map_f64(L, &tb, B, N, K, ldb, BN, BK))
+      return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(dgemm_exact_tma_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, T_SMEM);
+    if (e != cudaSuccess) return e;
+    dgemm_exact_tma_kernel<<<tiles_m * tiles_n, T_THREADS, T_SMEM, L.stream>>>(
+        ta, tb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), tiles_m,
+        tiles_n);
+    L.count();
+    return cudaGetLastError();
+  }
   // 16-byte cp.async when a whole chunk is always in or out of the matrix
   const bool va = lda % 2 == 0 && K % 2 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0;
   const bool vb = ldb % 2 == 0 && N % 2 == 0 && reinterpret_cast<uintptr_t>(B) % 16 == 0;
