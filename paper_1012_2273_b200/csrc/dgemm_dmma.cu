@@ -60,12 +60,21 @@ using Small = Cfg<64, 64, 32, 32, 4, 2>;   // 4 math warps, 64 KB ring, 2+ CTAs/
 using Mid = Cfg<128, 64, 32, 32, 5, 1>;    // 8 math warps, 160 KB ring
 
 // Poll an arrival flag (written by a cuStreamWriteValue32 behind an H2D copy).
+// A flag that never arrives is a host-side bug; trap after 60 s so the
+// context fails loudly instead of hanging the device.
+MMWS_DEVICE uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 MMWS_DEVICE void wait_flag(const int* f) {
+  const uint64_t t0 = global_ns();
   for (;;) {
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
     if (v) return;
     __nanosleep(200);
+    if (global_ns() - t0 > 60ull * 1000000000ull) __trap();
   }
 }
 
