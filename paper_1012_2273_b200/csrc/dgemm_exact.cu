@@ -124,15 +124,26 @@ __global__ void __launch_bounds__(THREADS, 1)
 // DADD -- no cp.async address arithmetic, no __syncthreads per k-tile.  Stages
 // are released one iteration late (see dgemm_dmma.cu).  Zero-filled TMA
 // out-of-bounds boxes are the (+0)*(+0) padding discussed above.
+// TBM x TBN tiles (128x128, or 64x64 for problems that would leave SMs idle);
+// each of the 256 math threads owns (TBM/16) x (TBN/16) outputs at rows
+// 2*ty + 32v + h and columns 2*tx + 32v + h.
 constexpr int T_STAGES = 4, T_CONSUMERS = 8, T_THREADS = (T_CONSUMERS + 4) * 32;
-constexpr int T_A_BYTES = BM * BK * 8, T_B_BYTES = BK * BN * 8;
-constexpr int T_STAGE = T_A_BYTES + T_B_BYTES;
-constexpr int T_SMEM = T_STAGES * T_STAGE + 2 * T_STAGES * 8 + 128;
+template <int TBM, int TBN>
+struct ExactTma {
+  static constexpr int A_BYTES = TBM * BK * 8, B_BYTES = BK * TBN * 8;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int SMEM = T_STAGES * STAGE + 2 * T_STAGES * 8 + 128;
+  static constexpr int TM = TBM / 16, TN = TBN / 16;  // outputs per thread
+  static constexpr int MINB = TBM == 128 ? 1 : 2;
+};
 
-__global__ void __launch_bounds__(T_THREADS, 1)
+template <int TBM, int TBN>
+__global__ void __launch_bounds__(T_THREADS, ExactTma<TBM, TBN>::MINB)
     dgemm_exact_tma_kernel(const __grid_constant__ CUtensorMap tmA,
                            const __grid_constant__ CUtensorMap tmB, double* __restrict__ C,
                            int64_t ldc, int M, int N, int K, int tiles_m, int tiles_n) {
+  using X = ExactTma<TBM, TBN>;
+  constexpr int T_A_BYTES = X::A_BYTES, T_STAGE = X::STAGE, TM = X::TM, TN = X::TN;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + T_STAGES * T_STAGE);
@@ -156,7 +167,7 @@ __global__ void __launch_bounds__(T_THREADS, 1)
   const int KT = (K + BK - 1) / BK;
 
   if (warp >= T_CONSUMERS) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    if constexpr (TBM == 128) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
     if (warp == T_CONSUMERS && lane == 0) {
       tma_prefetch_desc(&tmA);
       tma_prefetch_desc(&tmB);
@@ -165,20 +176,20 @@ __global__ void __launch_bounds__(T_THREADS, 1)
         if (kt >= T_STAGES) mbar_wait(&empty[s], ((kt / T_STAGES) - 1) & 1);
         uint8_t* sa = smem + s * T_STAGE;
         mbar_arrive_expect_tx(&full[s], T_STAGE);
-        tma_load_2d(sa, &tmA, &full[s], kt * BK, tm * BM);
-        tma_load_2d(sa + T_A_BYTES, &tmB, &full[s], tn * BN, kt * BK);
+        tma_load_2d(sa, &tmA, &full[s], kt * BK, tm * TBM);
+        tma_load_2d(sa + T_A_BYTES, &tmB, &full[s], tn * TBN, kt * BK);
       }
     }
     return;
   }
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+  if constexpr (TBM == 128) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
-  double acc[8][8];
+  double acc[TM][TN];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
 
   for (int kt = 0; kt < KT; ++kt) {
     const int s = kt % T_STAGES;
@@ -187,40 +198,41 @@ __global__ void __launch_bounds__(T_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[(kt - 1) % T_STAGES]);
     }
-    const double* as = reinterpret_cast<const double*>(smem + s * T_STAGE);  // [BM][BK]
-    const double* bs = as + BM * BK;                                          // [BK][BN]
+    const double* as = reinterpret_cast<const double*>(smem + s * T_STAGE);  // [TBM][BK]
+    const double* bs = as + TBM * BK;                                         // [BK][TBN]
 #pragma unroll
     for (int k = 0; k < BK; k += 2) {
-      double2 a2[8];
+      double2 a2[TM];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < TM; ++i)
         a2[i] = *reinterpret_cast<const double2*>(as + (ty * 2 + 32 * (i >> 1) + (i & 1)) * BK + k);
 #pragma unroll
       for (int kk = 0; kk < 2; ++kk) {
-        double b[8];
+        double b[TN];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const double2 bv = *reinterpret_cast<const double2*>(bs + (k + kk) * BN + tx * 2 + 32 * v);
+        for (int v = 0; v < TN / 2; ++v) {
+          const double2 bv =
+              *reinterpret_cast<const double2*>(bs + (k + kk) * TBN + tx * 2 + 32 * v);
           b[2 * v] = bv.x;
           b[2 * v + 1] = bv.y;
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < TM; ++i) {
           const double a = kk ? a2[i].y : a2[i].x;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(a, b[j]));
+          for (int j = 0; j < TN; ++j) acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(a, b[j]));
         }
       }
     }
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int r = tm * BM + ty * 2 + 32 * (i >> 1) + (i & 1);
+  for (int i = 0; i < TM; ++i) {
+    const int r = tm * TBM + ty * 2 + 32 * (i >> 1) + (i & 1);
     if (r >= M) continue;
     double* crow = C + static_cast<int64_t>(r) * ldc;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int c = tn * BN + tx * 2 + 32 * (j >> 1) + (j & 1);
+    for (int j = 0; j < TN; ++j) {
+      const int c = tn * TBN + tx * 2 + 32 * (j >> 1) + (j & 1);
       if (c < N) crow[c] = acc[i][j];
     }
   }
@@ -239,6 +251,25 @@ bool make_map_f64(const Launch& L, CUtensorMap* map, const double* base, int64_t
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+template <int TBM, int TBN>
+cudaError_t run_exact_tma(const Launch& L, int64_t M, int64_t N, int64_t K, const double* A,
+                          int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc) {
+  using X = ExactTma<TBM, TBN>;
+  CUtensorMap ta, tb;
+  if (!make_map_f64(L, &ta, A, K, M, lda, BK, TBM) || !make_map_f64(L, &tb, B, N, K, ldb, TBN, BK))
+    return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(dgemm_exact_tma_kernel<TBM, TBN>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, X::SMEM);
+  if (e != cudaSuccess) return e;
+  const int tiles_m = static_cast<int>((M + TBM - 1) / TBM);
+  const int tiles_n = static_cast<int>((N + TBN - 1) / TBN);
+  dgemm_exact_tma_kernel<TBM, TBN><<<tiles_m * tiles_n, T_THREADS, X::SMEM, L.stream>>>(
+      ta, tb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), tiles_m,
+      tiles_n);
+  L.count();
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t launch_dgemm_exact(const Launch& L, int64_t M, int64_t N, int64_t K, const double* A,
@@ -248,17 +279,10 @@ cudaError_t launch_dgemm_exact(const Launch& L, int64_t M, int64_t N, int64_t K,
   const int tiles_n = static_cast<int>((N + BN - 1) / BN);
   if (lda % 2 == 0 && ldb % 2 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0 &&
       reinterpret_cast<uintptr_t>(B) % 16 == 0) {  // TMA can describe both operands
-    CUtensorMap ta, tb;
-    if (!make_map_f64(L, &ta, A, K, M, lda, BK, BM) || !make_map_f64(L, &tb, B, N, K, ldb, BN, BK))
-      return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(dgemm_exact_tma_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, T_SMEM);
-    if (e != cudaSuccess) return e;
-    dgemm_exact_tma_kernel<<<tiles_m * tiles_n, T_THREADS, T_SMEM, L.stream>>>(
-        ta, tb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), tiles_m,
-        tiles_n);
-    L.count();
-    return cudaGetLastError();
+    // 64x64 tiles while 128x128 ones would not give every SM two CTAs
+    return tiles_m * tiles_n < 2 * L.num_sms
+               ? run_exact_tma<64, 64>(L, M, N, K, A, lda, B, ldb, C, ldc)
+               : run_exact_tma<128, 128>(L, M, N, K, A, lda, B, ldb, C, ldc);
   }
   // 16-byte cp.async when a whole chunk is always in or out of the matrix
   const bool va = lda % 2 == 0 && K % 2 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0;

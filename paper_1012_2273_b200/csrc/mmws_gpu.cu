@@ -70,8 +70,9 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
   cudaError_t e;
   const int64_t tiles128 = ((m + 127) / 128) * ((n + 127) / 128);
   if (mode == MMWS_GPU_MODE_EXACT) {
-    // exact order: 32x32 tiles while 128x128 tiles would leave most SMs idle
-    e = tiles128 <= 64
+    // exact order: the 32x32 latency kernel for tiny problems, else the
+    // 64x64 / 128x128 TMA kernels (every variant gives matmul_seq's bits)
+    e = n <= 256 && k <= 256
             ? launch_dgemm_small(L, true, m, n, k, A, lda, B, ldb, C, ldc)
             : launch_dgemm_exact(L, m, n, k, A, lda, B, ldb, C, ldc);
     return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm exact");
