@@ -273,6 +273,11 @@ def test_rowblock_nccl_path_single_rank(oracle):
             assert (bits(host(C)) == bits(want)).all()
             c, el = c2.master_run_host(host(A), host(B), mode=mode)
             assert el > 0 and (bits(c) == bits(want)).all()
+        # fp32 through the same engine
+        Af, Bf = A.float(), B.float()
+        Cf = T.empty_like(Af)
+        c2.rowblock(n, n, n, Af, Bf, Cf, f32=True)
+        assert (host(Cf) == host(c2.sgemm(Af, Bf))).all()
         c2.comm_destroy()
     finally:
         c2.close()
