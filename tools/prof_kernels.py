@@ -18,6 +18,11 @@ if which in ("all", "exact"):
     B = ctx.fill(P.DIST_UNIFORM, 1, n, n)
     for _ in range(2):
         ctx.dgemm(A, B, mode=P.MODE_EXACT)
+if which == "none":
+    n = 16384
+    A = ctx.fill(P.DIST_UNIFORM, 0, n, n)
+    B = ctx.fill(P.DIST_UNIFORM, 1, n, n)
+    ctx.dgemm(A, B, mode=P.MODE_DMMA)
 if which == "families":
     # one launch per kernel family at its representative size
     n = 8192
