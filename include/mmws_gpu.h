@@ -163,6 +163,22 @@ int mmws_gpu_graph_dgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, con
 int mmws_gpu_graph_launch(mmws_gpu_graph* graph, void* stream);
 int mmws_gpu_graph_destroy(mmws_gpu_graph* graph);
 
+/* ---------------------------------------------------------------- latency server (N <= 96) */
+/* A resident single-CTA kernel serving tiny fp64 multiplies through pinned,
+ * mapped host memory: no launch, copy or stream synchronisation per call.
+ * Results are bitwise those of mmws_gpu_dgemm in the same mode (AUTO or
+ * EXACT).  The kernel holds MMWS_GPU_SERVER_CTAS SMs (default 8) until
+ * mmws_gpu_server_stop (or destroy); while it runs, a device-wide synchronize
+ * (cudaDeviceSynchronize, torch.cuda.synchronize) waits for it -- synchronise
+ * streams instead. */
+int mmws_gpu_server_start(mmws_gpu_ctx* ctx);
+/* Host matrices (any memory); m, n, k <= 96.  *elapsed_s = host wall time of
+ * the call (copy in, compute, copy out). */
+int mmws_gpu_server_dgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
+                          int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                          int mode, double* elapsed_s);
+int mmws_gpu_server_stop(mmws_gpu_ctx* ctx);
+
 /* ---------------------------------------------------------------- IPC (same-node peers) */
 /* Block until everything queued on the context stream has finished. */
 int mmws_gpu_synchronize(mmws_gpu_ctx* ctx);

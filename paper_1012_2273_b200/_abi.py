@@ -42,6 +42,9 @@ SIGNATURES = {
     "mmws_gpu_graph_dgemm": (_i, [_v, _i64, _i64, _i64, _v, _i64, _v, _i64, _v, _i64, _i, _p(_v)]),
     "mmws_gpu_graph_launch": (_i, [_v, _v]),
     "mmws_gpu_graph_destroy": (_i, [_v]),
+    "mmws_gpu_server_start": (_i, [_v]),
+    "mmws_gpu_server_dgemm": (_i, [_v, _i64, _i64, _i64, _v, _i64, _v, _i64, _v, _i64, _i, _p(_d)]),
+    "mmws_gpu_server_stop": (_i, [_v]),
     "mmws_gpu_synchronize": (_i, [_v]),
     "mmws_gpu_ipc_export": (_i, [_v, _v, _p(C.c_uint8)]),
     "mmws_gpu_ipc_open": (_i, [_v, _p(C.c_uint8), _p(_v)]),

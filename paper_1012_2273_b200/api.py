@@ -323,6 +323,35 @@ def _master_run_host(self, a=None, b=None, out=None, mode: int = MODE_AUTO, m=No
     return out, el.value
 
 
+def _server_start(self) -> None:
+    """Start the resident latency server (tiny multiplies, m, n, k <= 96)."""
+    _check(_lib().mmws_gpu_server_start(self._h))
+
+
+def _server_matmul(self, a: np.ndarray, b: np.ndarray, mode: int = MODE_AUTO,
+                   out: Optional[np.ndarray] = None) -> Tuple[np.ndarray, float]:
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if a.shape[1] != b.shape[0]:
+        raise DimensionError(f"matmul: inner dimensions differ, {a.shape[1]} vs {b.shape[0]}")
+    m, k = a.shape
+    n = b.shape[1]
+    c = out if out is not None else np.empty((m, n), dtype=np.float64)
+    el = C.c_double()
+    _check(_lib().mmws_gpu_server_dgemm(self._h, m, n, k, a.ctypes.data, k, b.ctypes.data, n,
+                                        c.ctypes.data, n, mode, C.byref(el)))
+    return c, el.value
+
+
+def _server_stop(self) -> None:
+    _check(_lib().mmws_gpu_server_stop(self._h))
+
+
+Context.server_start = _server_start
+Context.server_matmul = _server_matmul
+Context.server_stop = _server_stop
+
+
 def _last_kernel_ms(self) -> float:
     out = C.c_double()
     _check(_lib().mmws_gpu_last_kernel_ms(self._h, C.byref(out)))

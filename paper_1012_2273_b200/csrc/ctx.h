@@ -25,6 +25,7 @@ struct mmws_gpu_ctx {
   // the streamed host path; null if the driver does not offer them
   CUresult (*write_value)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
   CUresult (*wait_value)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+  void* server = nullptr;  // latency server state (server.cu), null when not running
   // CUDA IPC (fused C gather of the row-block path)
   CUresult (*mem_range)(CUdeviceptr*, size_t*, CUdeviceptr) = nullptr;
   struct IpcMap {
@@ -83,6 +84,8 @@ cudaError_t ensure(void** buf, size_t* have, size_t bytes);
 int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
                    int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int mode,
                    cudaStream_t stream);
+// Stop the latency server (if running) and free its resources.
+void server_destroy(mmws_gpu_ctx* ctx);
 // CUDA IPC: 64-byte handle of the allocation holding ptr + 8-byte offset.
 int ipc_export(mmws_gpu_ctx* ctx, const void* ptr, uint8_t out[72]);
 int ipc_open(mmws_gpu_ctx* ctx, const uint8_t in[72], void** ptr);

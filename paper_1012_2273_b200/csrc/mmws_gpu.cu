@@ -273,6 +273,7 @@ int mmws_gpu_init(int device, mmws_gpu_ctx** out) {
 int mmws_gpu_destroy(mmws_gpu_ctx* ctx) {
   if (!ctx) return ok();
   cudaSetDevice(ctx->device);
+  server_destroy(ctx);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->comm && nccl().ok) nccl().CommDestroy(ctx->comm);
   for (auto& mp : ctx->ipc_cache) cudaIpcCloseMemHandle(mp.base);

@@ -347,6 +347,59 @@ def test_host_entry_matches_device_entry(ctx, oracle):
     assert normwise(cf.astype(np.float64), oracle.matmul_rows(list(range(257)), af, bf)) <= FP32_TOL
 
 
+@pytest.mark.timeout(180, method="thread")
+@pytest.mark.parametrize("ctas", [None, "1", "3"])
+def test_latency_server_bitwise_equals_device_entry(oracle, monkeypatch, ctas):
+    # While the resident server kernel runs, a device-wide synchronize
+    # (torch.cuda.synchronize) would wait for it forever: the expected results
+    # are computed before server_start, and only stream-ordered copies are used.
+    if ctas is not None:
+        monkeypatch.setenv("MMWS_GPU_SERVER_CTAS", ctas)
+    shapes = [(1, 1, 1), (2, 3, 4), (10, 10, 10), (17, 96, 5), (50, 50, 50), (96, 96, 96),
+              (96, 1, 96), (64, 96, 80), (95, 93, 91), (3, 96, 96)]
+    c = P.Context(0)
+    try:
+        cases = []
+        for seed, (m, k, n) in enumerate(shapes):
+            a = oracle.fill(oracle.DIST_UNIFORM, 100 + seed, m, k)
+            b = oracle.fill(oracle.DIST_UNIFORM, 200 + seed, k, n)
+            want = {mode: host(c.dgemm(dev(a), dev(b), mode=mode))
+                    for mode in (P.MODE_AUTO, P.MODE_EXACT)}
+            cases.append((a, b, want))
+        with pytest.raises(P.GpuError):
+            c.server_matmul(np.ones((2, 2)), np.ones((2, 2)))       # not started
+        c.server_start()
+        c.server_start()                                             # idempotent
+        for a, b, want in cases:
+            for mode in (P.MODE_AUTO, P.MODE_EXACT):
+                got, el = c.server_matmul(a, b, mode=mode)
+                assert el > 0
+                assert (bits(got) == bits(want[mode])).all(), (a.shape, b.shape, mode)
+            got, _ = c.server_matmul(a, b, mode=P.MODE_EXACT)
+            assert oracle.first_difference(got, oracle.matmul_seq(a, b)) is None
+        a = oracle.fill(oracle.DIST_UNIFORM, 1, 50, 50)
+        first, _ = c.server_matmul(a, a)
+        for _ in range(200):                                         # repeated requests
+            again, _ = c.server_matmul(a, a)
+        assert (bits(again) == bits(first)).all()
+        # the server does not block stream-ordered work of the same context
+        x = dev(a)
+        y = c.dgemm(x, x, mode=P.MODE_EXACT).cpu().numpy()
+        assert oracle.first_difference(y, oracle.matmul_seq(a, a)) is None
+        with pytest.raises(P.DimensionError):
+            c.server_matmul(np.ones((97, 2)), np.ones((2, 2)))
+        with pytest.raises(P.DimensionError):
+            c.server_matmul(np.ones((2, 3)), np.ones((2, 2)))
+        with pytest.raises(P.DomainError):
+            c.server_matmul(a, a, mode=P.MODE_DMMA)
+        c.server_stop()
+        c.server_start()                                             # restart after stop
+        got, _ = c.server_matmul(a, a, mode=P.MODE_EXACT)
+        assert oracle.first_difference(got, oracle.matmul_seq(a, a)) is None
+    finally:
+        c.close()                                                    # stops the server too
+
+
 @pytest.mark.parametrize("shape", [(1301, 1299, 1303), (2048, 1024, 4096), (2100, 1000, 2500)])
 def test_host_pipeline_bitwise_equals_device(ctx, oracle, shape):
     # big enough to take the overlapped (row-panel x column-block) host path

@@ -1,7 +1,8 @@
 """configs[1] sweep: square fp64 GEMM at N in {10..2000}, uniform [-1,1) seeds
 0/1, one GPU.  Per N: device time of one multiply (CUDA events, min over
 reps) for eager launches and for CUDA-graph replay, the host-buffer call
-(H2D + multiply + D2H through the C ABI), and the reference CPU time
+(H2D + multiply + D2H through the C ABI), the resident latency server for
+N <= 96 (host buffers, min and median of 200 calls), and the reference CPU time
 (oracle/_ref matmul_seq on 1 thread and matmul_threads on all threads, full
 product, time_model bracket) where it finishes quickly.  Writes one JSON line
 per N to stdout."""
@@ -55,7 +56,7 @@ def wall_time(fn, reps):
 def main():
     ctx = P.Context(0)
     cores = len(os.sched_getaffinity(0))
-    ns = [int(x) for x in sys.argv[1:]] or [10, 50, 100, 250, 500, 1000, 1500, 2000]
+    ns = [int(x) for x in sys.argv[1:]] or [10, 50, 96, 100, 250, 500, 1000, 1500, 2000]
     for n in ns:
         A = ctx.fill(P.DIST_UNIFORM, 0, n, n)
         B = ctx.fill(P.DIST_UNIFORM, 1, n, n)
@@ -79,6 +80,16 @@ def main():
         a, b = A.cpu().numpy(), B.cpu().numpy()
         th = min(ctx.matmul_host(a, b)[1] for _ in range(5))
         rec["host_entry_s"] = th
+        if n <= 96:
+            # resident latency server: host buffers in, host buffers out, no launch
+            ctx.server_start()
+            for mode_name, mode in (("server_auto_s", P.MODE_AUTO), ("server_exact_s", P.MODE_EXACT)):
+                for _ in range(20):
+                    ctx.server_matmul(a, b, mode=mode)
+                ts = sorted(ctx.server_matmul(a, b, mode=mode)[1] for _ in range(200))
+                rec[mode_name] = ts[0]
+                rec[mode_name.replace("_s", "_median_s")] = ts[len(ts) // 2]
+            ctx.server_stop()
         if O.ref_available() and n <= 2000:
             reps_cpu = 3 if n <= 1000 else 1
             if n <= 1500:
