@@ -138,7 +138,8 @@ int mmws_gpu_sgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const flo
 /* The matmul_seq / matmul_threads replacement for host data: dense row-major
  * A (m x k), B (k x n) in, C (m x n) out.  Copies in, multiplies, copies out
  * and synchronises.  *elapsed_s (optional) is the device-measured time of the
- * whole call (H2D + multiply + D2H).  Pinned host buffers give full PCIe
+ * whole call (H2D + multiply + D2H) -- the host wall time when the latency
+ * server below takes the call.  Pinned host buffers give full PCIe
  * bandwidth; pageable ones work too. */
 int mmws_gpu_matmul_host(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
                          const double* B, double* C, int mode, double* elapsed_s);
@@ -164,13 +165,17 @@ int mmws_gpu_graph_launch(mmws_gpu_graph* graph, void* stream);
 int mmws_gpu_graph_destroy(mmws_gpu_graph* graph);
 
 /* ---------------------------------------------------------------- latency server (N <= 96) */
-/* A resident single-CTA kernel serving tiny fp64 multiplies through pinned,
- * mapped host memory: no launch, copy or stream synchronisation per call.
+/* A small resident grid serving tiny fp64 multiplies through pinned, mapped
+ * host memory: no launch, copy or stream synchronisation per call.  While it
+ * runs, mmws_gpu_matmul_host routes the shapes and modes it takes to it.
  * Results are bitwise those of mmws_gpu_dgemm in the same mode (AUTO or
  * EXACT).  The kernel holds MMWS_GPU_SERVER_CTAS SMs (default 8) until
  * mmws_gpu_server_stop (or destroy); while it runs, a device-wide synchronize
- * (cudaDeviceSynchronize, torch.cuda.synchronize) waits for it -- synchronise
- * streams instead. */
+ * (cudaDeviceSynchronize, torch.cuda.synchronize, cudaFree) waits for it --
+ * synchronise streams instead.  The same holds for the lazy loading
+ * (CUDA_MODULE_LOADING=LAZY, the default) of a kernel first launched while it
+ * runs: server_start preloads this library's kernels; other libraries' (torch,
+ * NCCL) need CUDA_MODULE_LOADING=EAGER or a warm-up launch before it. */
 int mmws_gpu_server_start(mmws_gpu_ctx* ctx);
 /* Host matrices (any memory); m, n, k <= 96.  *elapsed_s = host wall time of
  * the call (copy in, compute, copy out). */

@@ -130,6 +130,12 @@ class Context {
   int world_size() const { return world_; }
   std::uint64_t launches() const { return mmws_gpu_launch_count(ctx_); }
 
+  // Resident latency server (mmws_gpu.h): while it runs, host multiplies up to
+  // 96 x 96 x 96 in automatic/exact mode skip the launch and copy engines.
+  // Do not call cudaDeviceSynchronize while it runs.
+  void server_start() { check(mmws_gpu_server_start(ctx_)); }
+  void server_stop() { check(mmws_gpu_server_stop(ctx_)); }
+
   // NCCL world for master_run/worker_run; rank 0 creates the id
   // (unique_id()) and ships it to every rank by any control plane.
   static std::vector<std::uint8_t> unique_id() {

@@ -26,6 +26,7 @@ struct mmws_gpu_ctx {
   CUresult (*write_value)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
   CUresult (*wait_value)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
   void* server = nullptr;  // latency server state (server.cu), null when not running
+  std::vector<void*> deferred_free;  // buffers outgrown while the server ran
   // CUDA IPC (fused C gather of the row-block path)
   CUresult (*mem_range)(CUdeviceptr*, size_t*, CUdeviceptr) = nullptr;
   struct IpcMap {
@@ -79,13 +80,22 @@ int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
 int ok();
 // grow a device buffer to at least `bytes`
-cudaError_t ensure(void** buf, size_t* have, size_t bytes);
+// Grow a device buffer to at least `bytes`.  While the latency server runs,
+// cudaFree (a device-wide synchronisation) would wait for it forever, so the
+// old buffer is parked in deferred_free instead (growth at least doubles).
+cudaError_t ensure(mmws_gpu_ctx* ctx, void** buf, size_t* have, size_t bytes);
 // the fp64 multiply dispatch used by dgemm / host / graph / row-block paths
 int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
                    int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int mode,
                    cudaStream_t stream);
 // Stop the latency server (if running) and free its resources.
 void server_destroy(mmws_gpu_ctx* ctx);
+// Would the running latency server take this host-buffer multiply?
+bool server_serves(const mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, int mode);
+// Serve it (caller holds ctx->mu).
+int server_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
+                    int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int mode,
+                    double* elapsed_s);
 // CUDA IPC: 64-byte handle of the allocation holding ptr + 8-byte offset.
 int ipc_export(mmws_gpu_ctx* ctx, const void* ptr, uint8_t out[72]);
 int ipc_open(mmws_gpu_ctx* ctx, const uint8_t in[72], void** ptr);

@@ -346,4 +346,9 @@ cudaError_t launch_dgemm_dmma(const Launch& L, int cfg, int64_t M, int64_t N, in
   }
 }
 
+cudaError_t preload_dgemm_dmma() {
+  return preload_kernels(dgemm_dmma_kernel<Big, false>, dgemm_dmma_kernel<Mid, false>,
+                         dgemm_dmma_kernel<Small, false>, dgemm_dmma_kernel<Big, true>);
+}
+
 }  // namespace mmws_impl

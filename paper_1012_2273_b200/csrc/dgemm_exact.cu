@@ -298,4 +298,10 @@ cudaError_t launch_dgemm_exact(const Launch& L, int64_t M, int64_t N, int64_t K,
   return cudaGetLastError();
 }
 
+cudaError_t preload_dgemm_exact() {
+  return preload_kernels(dgemm_exact_tma_kernel<64, 64>, dgemm_exact_tma_kernel<128, 128>,
+                         dgemm_exact_kernel<true, true>, dgemm_exact_kernel<true, false>,
+                         dgemm_exact_kernel<false, true>, dgemm_exact_kernel<false, false>);
+}
+
 }  // namespace mmws_impl

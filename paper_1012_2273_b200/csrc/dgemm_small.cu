@@ -113,4 +113,8 @@ cudaError_t launch_dgemm_small(const Launch& L, bool exact, int64_t M, int64_t N
   return cudaGetLastError();
 }
 
+cudaError_t preload_dgemm_small() {
+  return preload_kernels(dgemm_small_kernel<true>, dgemm_small_kernel<false>);
+}
+
 }  // namespace mmws_impl

@@ -60,7 +60,7 @@ int host_multiply_streamed(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, c
   const int64_t T = tiles_m * tiles_n;
   const size_t flag_ints = nba + nbb + tiles_m;
   cudaError_t e;
-  if ((e = ensure(&ctx->sched, &ctx->sched_bytes, sizeof(int) * (T + flag_ints))) != cudaSuccess)
+  if ((e = ensure(ctx, &ctx->sched, &ctx->sched_bytes, sizeof(int) * (T + flag_ints))) != cudaSuccess)
     return cuda_fail(e, "matmul_host: schedule buffer");
   int* order = static_cast<int*>(ctx->sched);
   int* ready_a = order + T;
@@ -179,9 +179,9 @@ int host_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A
   if (!A || !B || !C) return fail(MMWS_GPU_ERR_DOMAIN, "matmul: null host pointer");
   const size_t a_b = sizeof(T) * m * k, b_b = sizeof(T) * k * n, c_b = sizeof(T) * m * n;
   cudaError_t e;
-  if ((e = ensure(&ctx->dA, &ctx->dA_bytes, a_b)) != cudaSuccess ||
-      (e = ensure(&ctx->dB, &ctx->dB_bytes, b_b)) != cudaSuccess ||
-      (e = ensure(&ctx->dC, &ctx->dC_bytes, c_b)) != cudaSuccess)
+  if ((e = ensure(ctx, &ctx->dA, &ctx->dA_bytes, a_b)) != cudaSuccess ||
+      (e = ensure(ctx, &ctx->dB, &ctx->dB_bytes, b_b)) != cudaSuccess ||
+      (e = ensure(ctx, &ctx->dC, &ctx->dC_bytes, c_b)) != cudaSuccess)
     return cuda_fail(e, "matmul_host: device buffers");
   if constexpr (sizeof(T) == 8) {
     // big fp64 tensor-path problems whose dense device copies TMA can read

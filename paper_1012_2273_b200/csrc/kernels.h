@@ -38,6 +38,25 @@ struct DmmaStream {
   int* done = nullptr;           // [tile row] finished tiles
 };
 // 128x128 tiles only; grid = number of persistent CTAs.
+// Force-load kernels (cudaFuncGetAttributes).  Under CUDA_MODULE_LOADING=LAZY
+// the first launch of a kernel loads it with a context-wide synchronisation,
+// which would wait forever on the resident latency server: server_start
+// preloads every kernel of the library first.
+template <class... F>
+cudaError_t preload_kernels(F... f) {
+  cudaFuncAttributes attr;
+  cudaError_t e = cudaSuccess;
+  ((e == cudaSuccess ? (e = cudaFuncGetAttributes(&attr, reinterpret_cast<const void*>(f))) : e),
+   ...);
+  return e;
+}
+cudaError_t preload_dgemm_dmma();
+cudaError_t preload_dgemm_exact();
+cudaError_t preload_dgemm_small();
+cudaError_t preload_sgemm();
+cudaError_t preload_sgemm_tma();
+cudaError_t preload_misc();
+
 cudaError_t launch_dgemm_dmma_stream(const Launch& L, int64_t M, int64_t N, int64_t K,
                                      const double* A, int64_t lda, const double* B, int64_t ldb,
                                      double* C, int64_t ldc, const DmmaStream& st, int grid);

@@ -178,4 +178,9 @@ cudaError_t launch_peak_probe(const Launch& L, int which, int iters, double* sin
   return cudaGetLastError();
 }
 
+cudaError_t preload_misc() {
+  return preload_kernels(fill_kernel, pack_f64_kernel, probe_kernel<0>, probe_kernel<1>,
+                         probe_kernel<2>, probe_kernel<3>, probe_kernel<4>);
+}
+
 }  // namespace mmws_impl

@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -31,9 +32,14 @@ int ok() {
   return MMWS_GPU_OK;
 }
 
-cudaError_t ensure(void** buf, size_t* have, size_t bytes) {
+cudaError_t ensure(mmws_gpu_ctx* ctx, void** buf, size_t* have, size_t bytes) {
   if (*have >= bytes && *buf) return cudaSuccess;
-  if (*buf) {
+  if (*buf && ctx->server) {
+    ctx->deferred_free.push_back(*buf);
+    bytes = std::max(bytes, 2 * *have);
+    *buf = nullptr;
+    *have = 0;
+  } else if (*buf) {
     cudaError_t e = cudaFree(*buf);
     if (e != cudaSuccess) return e;
     *buf = nullptr;
@@ -96,7 +102,7 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
   if (!a_ok || !b_ok) {
     const int64_t lda_p = round_up(k, 8), ldb_p = round_up(n, 8);
     const size_t bytes = sizeof(double) * ((a_ok ? 0 : m * lda_p) + (b_ok ? 0 : k * ldb_p));
-    e = ensure(&ctx->ws, &ctx->ws_bytes, bytes);
+    e = ensure(ctx, &ctx->ws, &ctx->ws_bytes, bytes);
     if (e != cudaSuccess) return cuda_fail(e, "dgemm pack workspace");
     double* w = static_cast<double*>(ctx->ws);
     if (!a_ok) {
@@ -281,6 +287,7 @@ int mmws_gpu_destroy(mmws_gpu_ctx* ctx) {
                   ctx->ipc_stage,
                   static_cast<void*>(ctx->sink)})
     if (p) cudaFree(p);
+  for (void* p : ctx->deferred_free) cudaFree(p);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->evk0) cudaEventDestroy(ctx->evk0);
@@ -370,6 +377,8 @@ int mmws_gpu_sgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const flo
 int mmws_gpu_matmul_host(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
                          const double* B, double* C, int mode, double* elapsed_s) {
   MMWS_CTX_GUARD(ctx);
+  if (A && B && C && server_serves(ctx, m, n, k, mode))  // resident server (server.cu)
+    return server_multiply(ctx, m, n, k, A, k, B, n, C, n, mode, elapsed_s);
   return host_multiply(ctx, m, n, k, A, B, C, mode, elapsed_s);
 }
 

@@ -195,10 +195,10 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
   const T* b_loc = B;
   T* c_loc = C;
   if (me != 0) {
-    if ((e = ensure(&ctx->rbA, &ctx->rbA_bytes, sizeof(T) * (rows[me] * k + 1))) != cudaSuccess ||
-        (e = ensure(&ctx->rbB, &ctx->rbB_bytes, sizeof(T) * k * n)) != cudaSuccess ||
+    if ((e = ensure(ctx, &ctx->rbA, &ctx->rbA_bytes, sizeof(T) * (rows[me] * k + 1))) != cudaSuccess ||
+        (e = ensure(ctx, &ctx->rbB, &ctx->rbB_bytes, sizeof(T) * k * n)) != cudaSuccess ||
         (!fused &&
-         (e = ensure(&ctx->rbC, &ctx->rbC_bytes, sizeof(T) * (rows[me] * n + 1))) != cudaSuccess))
+         (e = ensure(ctx, &ctx->rbC, &ctx->rbC_bytes, sizeof(T) * (rows[me] * n + 1))) != cudaSuccess))
       return cuda_fail(e, "rowblock: worker buffers");
     a_loc = static_cast<const T*>(ctx->rbA);
     b_loc = static_cast<const T*>(ctx->rbB);
@@ -309,9 +309,9 @@ int master_run_host(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T*
   if (!A || !B || !C) return fail(MMWS_GPU_ERR_DOMAIN, "master_run: null host matrix");
   const size_t a_b = sizeof(T) * m * k, b_b = sizeof(T) * k * n, c_b = sizeof(T) * m * n;
   cudaError_t e;
-  if ((e = ensure(&ctx->dA, &ctx->dA_bytes, a_b)) != cudaSuccess ||
-      (e = ensure(&ctx->dB, &ctx->dB_bytes, b_b)) != cudaSuccess ||
-      (e = ensure(&ctx->dC, &ctx->dC_bytes, c_b)) != cudaSuccess)
+  if ((e = ensure(ctx, &ctx->dA, &ctx->dA_bytes, a_b)) != cudaSuccess ||
+      (e = ensure(ctx, &ctx->dB, &ctx->dB_bytes, b_b)) != cudaSuccess ||
+      (e = ensure(ctx, &ctx->dC, &ctx->dC_bytes, c_b)) != cudaSuccess)
     return cuda_fail(e, "master_run: device buffers");
   cudaStream_t s = ctx->stream;
   cudaEventRecord(ctx->ev0, s);

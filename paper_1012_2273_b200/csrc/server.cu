@@ -256,6 +256,8 @@ void server_destroy(mmws_gpu_ctx* ctx) {
   if (s->stream) cudaStreamSynchronize(s->stream);
   server_free(s);
   ctx->server = nullptr;
+  for (void* p : ctx->deferred_free) cudaFree(p);
+  ctx->deferred_free.clear();
 }
 
 }  // namespace mmws_impl
@@ -299,6 +301,12 @@ int mmws_gpu_server_start(mmws_gpu_ctx* ctx) {
     server_free(s);
     return cuda_fail(e, "server_start");
   }
+  // every other kernel of the library must be loaded before the server runs
+  if ((e = preload_dgemm_dmma()) || (e = preload_dgemm_exact()) || (e = preload_dgemm_small()) ||
+      (e = preload_sgemm()) || (e = preload_sgemm_tma()) || (e = preload_misc())) {
+    server_free(s);
+    return cuda_fail(e, "server_start: preload kernels");
+  }
   // cooperative launch: all CTAs must be co-resident for the grid barrier
   void* args[] = {&s->dev, &s->scratch, &s->sync};
   if ((e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(server_kernel), dim3(s->ctas),
@@ -311,11 +319,19 @@ int mmws_gpu_server_start(mmws_gpu_ctx* ctx) {
   return ok();
 }
 
-int mmws_gpu_server_dgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
-                          int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
-                          int mode, double* elapsed_s) {
-  if (!ctx) return fail(MMWS_GPU_ERR_STATE, "null mmws_gpu_ctx");
-  std::lock_guard<std::mutex> guard(ctx->mu);
+}  // extern "C"
+
+namespace mmws_impl {
+
+bool server_serves(const mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, int mode) {
+  return ctx->server && m >= 1 && n >= 1 && k >= 1 && m <= SRV_MAX && n <= SRV_MAX &&
+         k <= SRV_MAX && (mode == MMWS_GPU_MODE_AUTO || mode == MMWS_GPU_MODE_EXACT);
+}
+
+// Caller holds ctx->mu.
+int server_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
+                    int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int mode,
+                    double* elapsed_s) {
   ServerState* s = static_cast<ServerState*>(ctx->server);
   if (!s) return fail(MMWS_GPU_ERR_STATE, "server_dgemm: server not started");
   if (m <= 0 || n <= 0 || k <= 0)
@@ -355,6 +371,18 @@ int mmws_gpu_server_dgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, co
   if (elapsed_s)
     *elapsed_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return ok();
+}
+
+}  // namespace mmws_impl
+
+extern "C" {
+
+int mmws_gpu_server_dgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
+                          int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                          int mode, double* elapsed_s) {
+  if (!ctx) return fail(MMWS_GPU_ERR_STATE, "null mmws_gpu_ctx");
+  std::lock_guard<std::mutex> guard(ctx->mu);
+  return server_multiply(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode, elapsed_s);
 }
 
 int mmws_gpu_server_stop(mmws_gpu_ctx* ctx) {

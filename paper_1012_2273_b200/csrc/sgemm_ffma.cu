@@ -188,4 +188,9 @@ cudaError_t launch_sgemm_ffma(const Launch& L, int64_t M, int64_t N, int64_t K, 
   return cudaGetLastError();
 }
 
+cudaError_t preload_sgemm() {
+  return preload_kernels(sgemm_ffma_kernel<true, true>, sgemm_ffma_kernel<true, false>,
+                         sgemm_ffma_kernel<false, true>, sgemm_ffma_kernel<false, false>);
+}
+
 }  // namespace mmws_impl

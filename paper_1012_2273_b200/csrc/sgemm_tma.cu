@@ -212,4 +212,6 @@ cudaError_t launch_sgemm_tma(const Launch& L, int64_t M, int64_t N, int64_t K, c
   return cudaGetLastError();
 }
 
+cudaError_t preload_sgemm_tma() { return preload_kernels(sgemm_tma_kernel); }
+
 }  // namespace mmws_impl

@@ -142,6 +142,14 @@ static void gpu_checks() {
   const MatrixF32 cf = G::matmul(ctx, af, bf);
   CHECK(cf(2, 0) == 5.f && cf(2, 1) == 6.f);
   CHECK(ctx.launches() > 0);
+  // the same calls served by the resident latency server: same bits
+  ctx.server_start();
+  for (auto [m, k, n] : {std::tuple{5, 5, 5}, {50, 50, 50}, {96, 96, 96}, {4, 7, 3}}) {
+    const MatrixF64 a = random_matrix(m, k, 21 + m), b = random_matrix(k, n, 22 + n);
+    CHECK(bitwise_equal(G::matmul_seq(ctx, a, b), seq(a, b)));
+    CHECK(bitwise_equal(G::matmul_threads(ctx, a, b, 4), seq(a, b)));
+  }
+  ctx.server_stop();
 }
 
 int main(int argc, char** argv) {

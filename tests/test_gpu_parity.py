@@ -377,6 +377,9 @@ def test_latency_server_bitwise_equals_device_entry(oracle, monkeypatch, ctas):
                 assert (bits(got) == bits(want[mode])).all(), (a.shape, b.shape, mode)
             got, _ = c.server_matmul(a, b, mode=P.MODE_EXACT)
             assert oracle.first_difference(got, oracle.matmul_seq(a, b)) is None
+        for a, b, want in cases:                                     # routed by matmul_host
+            for mode in (P.MODE_AUTO, P.MODE_EXACT):
+                assert (bits(c.matmul_host(a, b, mode=mode)[0]) == bits(want[mode])).all()
         a = oracle.fill(oracle.DIST_UNIFORM, 1, 50, 50)
         first, _ = c.server_matmul(a, a)
         for _ in range(200):                                         # repeated requests
@@ -386,6 +389,12 @@ def test_latency_server_bitwise_equals_device_entry(oracle, monkeypatch, ctas):
         x = dev(a)
         y = c.dgemm(x, x, mode=P.MODE_EXACT).cpu().numpy()
         assert oracle.first_difference(y, oracle.matmul_seq(a, a)) is None
+        # nor host-buffer calls it does not take, even when they must grow the
+        # context's device buffers (cudaFree would wait for the server)
+        for nn in (100, 300, 700):
+            big = oracle.fill(oracle.DIST_INT8, nn, nn, nn)
+            got, _ = c.matmul_host(big, big, mode=P.MODE_EXACT)
+            assert oracle.first_difference(got, oracle.matmul_threads(big, big)) is None
         with pytest.raises(P.DimensionError):
             c.server_matmul(np.ones((97, 2)), np.ones((2, 2)))
         with pytest.raises(P.DimensionError):

@@ -60,3 +60,15 @@ def test_cli_sweep_with_gate(tmp_path):
     r = subprocess.run([exe, "--dims", "300", "--models", "gpu", "--tolerance", "0"],
                        capture_output=True, text=True)
     assert r.returncode == 2 and "correctness gate" in r.stderr
+
+
+@pytest.mark.gpu
+def test_cli_with_latency_server(tmp_path):
+    # --server: N <= 96 calls go through the resident kernel; the gate still holds
+    exe = _build(os.path.join(ROOT, "tools", "mmws_gpu_bench.cpp"), tmp_path / "b")
+    csv = tmp_path / "out.csv"
+    r = subprocess.run([exe, "--dims", "10,50,96,100", "--models", "gpu,gpu-exact", "--server",
+                        "--repeats", "3", "--csv", str(csv)], capture_output=True, text=True,
+                       timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert len(csv.read_text().splitlines()) == 1 + 8

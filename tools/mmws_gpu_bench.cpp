@@ -3,7 +3,7 @@
 // reference's CSV format.
 //
 //   mmws_gpu_bench --dims 100,500,1000 [--models gpu,gpu-exact] [--repeats 3]
-//                  [--seed 42] [--csv out.csv] [--tolerance 1e-12]
+//                  [--seed 42] [--csv out.csv] [--tolerance 1e-12] [--server]
 //
 // Build: g++ -std=c++20 -O2 -Iinclude tools/mmws_gpu_bench.cpp
 //            -Lpaper_1012_2273_b200 -lmmws_gpu -Wl,-rpath,<repo>/paper_1012_2273_b200
@@ -30,7 +30,7 @@ std::vector<std::string> split(const std::string& s) {
 int usage() {
   std::fprintf(stderr,
                "usage: mmws_gpu_bench --dims N1,N2,... [--models gpu,gpu-exact,gpu-rowblock] "
-               "[--repeats R] [--seed S] [--tolerance T] [--csv PATH] [--device D]\n");
+               "[--repeats R] [--seed S] [--tolerance T] [--csv PATH] [--device D] [--server]\n");
   return 2;
 }
 
@@ -40,6 +40,7 @@ int main(int argc, char** argv) {
   mmws::gpu::BenchConfig config;
   std::string csv_path;
   int device = 0;
+  bool server = false;  // resident latency server for N <= 96 (mmws_gpu_server_start)
   try {
     for (int i = 1; i < argc; ++i) {
       const std::string arg = argv[i];
@@ -62,12 +63,15 @@ int main(int argc, char** argv) {
         csv_path = value();
       } else if (arg == "--device") {
         device = std::stoi(value());
+      } else if (arg == "--server") {
+        server = true;
       } else {
         return usage();
       }
     }
     if (config.dims.empty()) return usage();
     mmws::gpu::Context ctx(device);
+    if (server) ctx.server_start();
     const auto records = mmws::gpu::run_suite(ctx, config);
     std::printf("%-13s %8s %8s %14s %14s %12s\n", "model", "n", "gpus", "elapsed_s", "mflops",
                 "rel_err");
