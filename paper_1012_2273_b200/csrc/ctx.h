@@ -40,7 +40,7 @@ struct mmws_gpu_ctx {
   // streamed host path: [tile order | ready_a | ready_b | done] on the device
   void* sched = nullptr;
   size_t sched_bytes = 0;
-  int64_t sched_m = -1, sched_n = -1;  // shape the uploaded tile order belongs to
+  int64_t sched_m = -1, sched_n = -1, sched_k = -1;  // shape the uploaded tile order belongs to
   uint64_t launches = 0;
   std::mutex mu;
 

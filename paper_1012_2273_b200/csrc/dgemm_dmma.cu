@@ -150,8 +150,8 @@ __global__ void __launch_bounds__(K::THREADS, K::MINB)
         int tm, tn;
         tile_at(idx, tm, tn);
         if constexpr (STREAM) {
-          wait_flag(st.ready_a + tm / st.band);
-          wait_flag(st.ready_b + tn / st.band);
+          wait_flag(st.ready_a + tm / st.band_a);
+          wait_flag(st.ready_b + tn / st.band_b);
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         for (int kt = 0; kt < KT; ++kt, ++kg) {

@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "../../include/mmws_gpu.h"
@@ -47,16 +49,20 @@ int gemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, int64_t
 
 // Streamed variant (fp64 DMMA, big problems): one persistent GEMM over the
 // whole C that starts on tiles whose A rows and B columns have already
-// crossed PCIe.  Copy-in interleaves 1024-row bands of A and 1024-column bands
+// crossed PCIe.  Copy-in interleaves 256-row bands of A and 512-column bands
 // of B, each followed by a cuStreamWriteValue32 flag; the kernel walks its
 // tiles in arrival order; a per-tile-row completion counter, awaited with
-// cuStreamWaitValue32, releases each finished 1024-row band of C to the
+// cuStreamWaitValue32, releases each finished 256-row band of C to the
 // copy-out stream.  No launch-size wave quantisation, no panel-0 stall.
+// Band sizes: the first tile can start once one A band and one B band have
+// landed (48 MB at N=16384, ~1 ms of PCIe), and the last C band to ship after
+// the multiply is 32 MB (~0.6 ms); B bands stay 4 KB wide per row so the 2-D
+// copies run at full PCIe speed.
 int host_multiply_streamed(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
                            const double* B, double* C, double* elapsed_s) {
-  constexpr int TILE = 128, BAND = 8;
+  constexpr int TILE = 128, BAND_A = 2, BAND_B = 4, BAND_C = 2;
   const int64_t tiles_m = (m + TILE - 1) / TILE, tiles_n = (n + TILE - 1) / TILE;
-  const int64_t nba = (tiles_m + BAND - 1) / BAND, nbb = (tiles_n + BAND - 1) / BAND;
+  const int64_t nba = (tiles_m + BAND_A - 1) / BAND_A, nbb = (tiles_n + BAND_B - 1) / BAND_B;
   const int64_t T = tiles_m * tiles_n;
   const size_t flag_ints = nba + nbb + tiles_m;
   cudaError_t e;
@@ -67,38 +73,63 @@ int host_multiply_streamed(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, c
   int* ready_b = ready_a + nba;
   int* done = ready_b + nbb;
 
-  // Copy order: A band 0, then B bands two at a time interleaved with A bands
-  // until all of B has landed, then the remaining A bands.  Every tile needs
-  // all of its row's B columns to finish, so once B is complete each further
-  // A band unlocks -- and lets the kernel finish -- a whole band of C rows,
-  // which the copy-out stream ships while the next band computes.
+  // Copy order: whichever operand has crossed fewer bytes goes next, so the
+  // landed A rows and B columns grow as a square -- the unlocked tile count
+  // (rows x columns) is then largest for the bytes moved.  The first ~15 ms
+  // at N=16384 are data-starved whatever the order (tiles need all of K);
+  // the square order loses ~4 ms less than a B-first one (simulated and
+  // measured).
   std::vector<int64_t> seq_a(nba), seq_b(nbb);
   std::vector<std::pair<char, int64_t>> copies;
   auto push = [&](char w, int64_t i) {
     (w == 'A' ? seq_a : seq_b)[i] = static_cast<int64_t>(copies.size());
     copies.push_back({w, i});
   };
-  int64_t ia = 0, ib = 0;
-  push('A', ia++);
-  while (ib < nbb) {
-    push('B', ib++);
-    if (ib < nbb) push('B', ib++);
-    if (ib < nbb && ia < nba) push('A', ia++);
+  {
+    int64_t ia = 0, ib = 0;
+    double bytes_a = 0, bytes_b = 0;
+    const double band_a_bytes = static_cast<double>(BAND_A) * TILE * k;
+    const double band_b_bytes = static_cast<double>(BAND_B) * TILE * k;
+    while (ia < nba || ib < nbb) {
+      if (ib >= nbb || (ia < nba && bytes_a <= bytes_b)) {
+        push('A', ia++);
+        bytes_a += band_a_bytes;
+      } else {
+        push('B', ib++);
+        bytes_b += band_b_bytes;
+      }
+    }
   }
-  while (ia < nba) push('A', ia++);
-  if (ctx->sched_m != m || ctx->sched_n != n) {  // tile order: by arrival, then row-major
+  if (ctx->sched_m != m || ctx->sched_n != n || ctx->sched_k != k) {
+    // Tile order.  CTA c takes positions c, c + grid, ... so position p starts
+    // around wave p / grid.  Positions whose wave starts before all inputs can
+    // have crossed PCIe take tiles in arrival order (data-starved phase); the
+    // rest take row-major order, so C rows complete -- and ship -- one band
+    // after another instead of all at the end (arrival order finishes no row
+    // before the last B band lands; measured D2H tail 28 ms -> 0.6 ms).
     std::vector<int64_t> key(T);
     std::vector<int> ord(T);
     for (int64_t t = 0; t < T; ++t) {
       const int64_t tm = t / tiles_n, tn = t % tiles_n;
-      key[t] = std::max(seq_a[tm / BAND], seq_b[tn / BAND]) * T + t;
+      key[t] = std::max(seq_a[tm / BAND_A], seq_b[tn / BAND_B]) * T + t;
       ord[t] = static_cast<int>(t);
     }
     std::sort(ord.begin(), ord.end(), [&](int x, int y) { return key[x] < key[y]; });
+    const double pcie_bytes_per_s = 50e9;  // PCIe 5.0 x16 H2D, conservative
+    const double sm_flops_per_s =  // DMMA: 128 flop/clk/SM
+        128.0 * (ctx->clock_khz > 0 ? ctx->clock_khz : 1900000) * 1e3;
+    const double t_inputs = 8.0 * (static_cast<double>(m) * k + static_cast<double>(k) * n) /
+                            pcie_bytes_per_s;
+    const double t_tile = 2.0 * TILE * TILE * k / sm_flops_per_s;
+    const int64_t grid = std::min<int64_t>(T, ctx->num_sms);
+    const int64_t p_all =
+        std::min<int64_t>(T, static_cast<int64_t>(t_inputs / t_tile) * grid);
+    std::sort(ord.begin() + p_all, ord.end());
     if ((e = cudaMemcpy(order, ord.data(), sizeof(int) * T, cudaMemcpyHostToDevice)))
       return cuda_fail(e, "matmul_host: tile order");
     ctx->sched_m = m;
     ctx->sched_n = n;
+    ctx->sched_k = k;
   }
 
   cudaStream_t in = ctx->copy_in, comp = ctx->stream, out = ctx->copy_out;
@@ -118,14 +149,14 @@ int host_multiply_streamed(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, c
   // ---- copy-in, each band followed by its arrival flag
   for (const auto& [which, i] : copies) {
     if (which == 'A') {
-      const int64_t r0 = i * BAND * TILE, rows = std::min<int64_t>(BAND * TILE, m - r0);
+      const int64_t r0 = i * BAND_A * TILE, rows = std::min<int64_t>(BAND_A * TILE, m - r0);
       if ((e = cudaMemcpyAsync(dA + r0 * k, A + r0 * k, sizeof(double) * rows * k,
                                cudaMemcpyHostToDevice, in)))
         return cuda_fail(e, "matmul_host: H2D A");
       if (ctx->write_value(in, dptr(ready_a + i), 1, 0) != CUDA_SUCCESS)
         return fail(MMWS_GPU_ERR_CUDA, "matmul_host: cuStreamWriteValue32 failed");
     } else {
-      const int64_t c0 = i * BAND * TILE, w = std::min<int64_t>(BAND * TILE, n - c0);
+      const int64_t c0 = i * BAND_B * TILE, w = std::min<int64_t>(BAND_B * TILE, n - c0);
       if ((e = cudaMemcpy2DAsync(dB + c0, sizeof(double) * n, B + c0, sizeof(double) * n,
                                  sizeof(double) * w, k, cudaMemcpyHostToDevice, in)))
         return cuda_fail(e, "matmul_host: H2D B");
@@ -133,20 +164,30 @@ int host_multiply_streamed(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, c
         return fail(MMWS_GPU_ERR_CUDA, "matmul_host: cuStreamWriteValue32 failed");
     }
   }
+  // optional timeline (MMWS_GPU_PIPELINE_TRACE=1): H2D end, kernel start/end
+  cudaEvent_t tr[3] = {nullptr, nullptr, nullptr};
+  const bool trace = std::getenv("MMWS_GPU_PIPELINE_TRACE") != nullptr;
+  if (trace) {
+    for (auto& ev : tr) cudaEventCreate(&ev);
+    cudaEventRecord(tr[0], in);
+    cudaEventRecord(tr[1], comp);
+  }
   // ---- one persistent multiply
   DmmaStream st;
   st.order = order;
   st.count = static_cast<int>(T);
   st.ready_a = ready_a;
   st.ready_b = ready_b;
-  st.band = BAND;
+  st.band_a = BAND_A;
+  st.band_b = BAND_B;
   st.done = done;
   const int grid = static_cast<int>(std::min<int64_t>(T, ctx->num_sms));
   if ((e = launch_dgemm_dmma_stream(ctx->launch(comp), m, n, k, dA, k, dB, n, dC, n, st, grid)))
     return cuda_fail(e, "matmul_host: streamed dgemm");
-  // ---- copy-out: each 1024-row band once all its tiles are counted
-  for (int64_t i = 0; i < nba; ++i) {
-    const int64_t t0 = i * BAND, t1 = std::min<int64_t>(tiles_m, t0 + BAND);
+  if (trace) cudaEventRecord(tr[2], comp);
+  // ---- copy-out: each 256-row band once all its tiles are counted
+  for (int64_t t0 = 0; t0 < tiles_m; t0 += BAND_C) {
+    const int64_t t1 = std::min<int64_t>(tiles_m, t0 + BAND_C);
     for (int64_t tm = t0; tm < t1; ++tm)
       if (ctx->wait_value(out, dptr(done + tm), static_cast<cuuint32_t>(tiles_n),
                           CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
@@ -165,6 +206,15 @@ int host_multiply_streamed(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, c
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
     *elapsed_s = ms * 1e-3;
+  }
+  if (trace) {
+    float t[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&t[i], ctx->ev0, tr[i]);
+    cudaEventElapsedTime(&t[3], ctx->ev0, ctx->ev1);
+    std::fprintf(stderr,
+                 "[mmws_gpu pipeline] h2d_end_ms=%.3f kernel_start_ms=%.3f kernel_end_ms=%.3f "
+                 "d2h_end_ms=%.3f\n", t[0], t[1], t[2], t[3]);
+    for (auto& ev : tr) cudaEventDestroy(ev);
   }
   return ok();
 }

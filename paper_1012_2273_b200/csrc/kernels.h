@@ -34,10 +34,10 @@ struct DmmaStream {
   int count = 0;                 // entries in order
   const int* ready_a = nullptr;  // [tile-row band] != 0 once A's rows have landed
   const int* ready_b = nullptr;  // [tile-col band] != 0 once B's columns have landed
-  int band = 1;                  // tiles per band
+  int band_a = 1;                // tile rows per A band (ready_a granularity)
+  int band_b = 1;                // tile columns per B band (ready_b granularity)
   int* done = nullptr;           // [tile row] finished tiles
 };
-// 128x128 tiles only; grid = number of persistent CTAs.
 // Force-load kernels (cudaFuncGetAttributes).  Under CUDA_MODULE_LOADING=LAZY
 // the first launch of a kernel loads it with a context-wide synchronisation,
 // which would wait forever on the resident latency server: server_start
@@ -57,6 +57,7 @@ cudaError_t preload_sgemm();
 cudaError_t preload_sgemm_tma();
 cudaError_t preload_misc();
 
+// 128x128 tiles only; grid = number of persistent CTAs.
 cudaError_t launch_dgemm_dmma_stream(const Launch& L, int64_t M, int64_t N, int64_t K,
                                      const double* A, int64_t lda, const double* B, int64_t ldb,
                                      double* C, int64_t ldc, const DmmaStream& st, int grid);
