@@ -219,6 +219,9 @@ def run_ours(args) -> None:
     for _ in range(args.warmup):
         ctx.rowblock(n, n, n, A, B, C, mode=mode)
     barrier()
+    # cost-model calibration: NCCL broadcast bandwidth out of rank 0 (collective)
+    link_bw = ctx.link_probe(1 << 28, 5) if world > 1 else None
+    barrier()
 
     sampler = ClockSampler(local) if root else None
     if sampler:
@@ -286,8 +289,10 @@ def run_ours(args) -> None:
         cpu = {k: s[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
     if root and world > 1:  # cost model of this schedule at the measured 1-GPU kernel rate
-        t_model, _, _ = P.rowblock_cost(n, n, n, world, 8, 770e9, 2.0 * rows0 * n * n / (kern_avg_ms / 1e3))
-        model = {"predicted_ms_per_step": t_model * 1e3, "link_GBps": 770}
+        t_model, _, _ = P.rowblock_cost(n, n, n, world, 8, link_bw,
+                                        2.0 * rows0 * n * n / (kern_avg_ms / 1e3))
+        model = {"predicted_ms_per_step": t_model * 1e3, "link_GBps": link_bw / 1e9,
+                 "link_source": "mmws_gpu_link_probe: 5 x 256 MiB NCCL broadcasts from rank 0"}
     else:
         model = None
     if root:

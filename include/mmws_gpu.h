@@ -198,6 +198,12 @@ int mmws_gpu_ipc_open(mmws_gpu_ctx* ctx, const uint8_t in[72], void** ptr);
 /* ---------------------------------------------------------------- measurement */
 /* Runs one pipe-saturating probe kernel and returns its TFLOP/s. */
 int mmws_gpu_peak_probe(mmws_gpu_ctx* ctx, int which, int iters, double* tflops);
+/* Calibration of the row-block cost model (the analogue of the reference's
+ * `bench calibrate`, bench_main.cpp:64-93, which fits tc/tf to its TCP link):
+ * mmws_gpu_gemm_probe times `iters` device-resident n x n multiplies in `mode`
+ * (inputs generated on the device, CUDA events) and returns the rate in
+ * FLOP/s (2n^3 per multiply). */
+int mmws_gpu_gemm_probe(mmws_gpu_ctx* ctx, int64_t n, int mode, int iters, double* flops_per_s);
 
 /* ---------------------------------------------------------------- row-block distribution */
 /* The master/worker row decomposition of master_run / worker_run
@@ -247,6 +253,11 @@ int mmws_gpu_last_kernel_ms(mmws_gpu_ctx* ctx, double* ms);
  * cost_model.hpp:36-70): predicted seconds given the NVLink bandwidth per
  * direction and the per-GPU multiply rate, plus rank 0's egress (B once + the
  * workers' A rows) and ingress (the workers' C rows) in bytes.  Host-only. */
+/* Collective over the context's communicator: `iters` broadcasts of `bytes`
+ * from rank 0 (the B broadcast of a round), timed with CUDA events on the
+ * communication stream; *bytes_per_s = bytes / time per broadcast on this
+ * rank.  Needs mmws_gpu_comm_init. */
+int mmws_gpu_link_probe(mmws_gpu_ctx* ctx, int64_t bytes, int iters, double* bytes_per_s);
 int mmws_gpu_rowblock_cost(int64_t m, int64_t n, int64_t k, int nranks, int elem_bytes,
                            double link_bytes_per_s, double gemm_flops_per_s, double* seconds,
                            double* root_egress_bytes, double* root_ingress_bytes);

@@ -50,6 +50,9 @@ struct RankError : std::out_of_range {
 struct ProtocolError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+struct IoError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
 }  // namespace mmws
 #endif
 

@@ -6,7 +6,11 @@
 // Mirrors bench.hpp: model names and parsing (:30-46), the record and config
 // (:48-67), mflops / speedup (:70-78), derive_seed (:83-86), time_model's
 // min-of-repeats bracket (:92-129), run_suite's correctness gate (:161-168)
-// and the CSV format (:190-212).  The gate is bitwise for gpu-exact and
+// and the CSV format (:190-212); plus the SVG charts of plots.hpp (:145-198:
+// runtime / mflops / speedup vs N, one series per model, machine-checkable
+// data-series / data-points attributes, dashed cost-model overlay) and the
+// `bench calibrate` step (bench_main.cpp:64-93) re-aimed at the row-block
+// cost model's two rates.  The gate is bitwise for gpu-exact and
 // normwise (config.tolerance, default 1e-12) for the tensor-path models, whose
 // accumulation order differs from matmul_seq's; the gate's reference product
 // is mmws::matmul_seq itself when the reference headers are on the include
@@ -14,12 +18,15 @@
 // matmul_seq by construction, tests/test_gpu_parity.py).
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <filesystem>
 #include <fstream>
 #include <optional>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -234,9 +241,199 @@ inline std::string csv(const std::vector<BenchRecord>& records) {
 
 inline void emit_csv(const std::vector<BenchRecord>& records, const std::string& path) {
   std::ofstream f(path);
-  if (!f) throw std::runtime_error("cannot write " + path);
+  if (!f) throw IoError("cannot write " + path);
   f << csv(records);
-  if (!f.flush()) throw std::runtime_error("short write to " + path);
+  if (!f.flush()) throw IoError("short write to " + path);
+}
+
+// ---------------------------------------------------------------- calibration
+// The reference's `bench calibrate` fits tc / tf (seconds per datum moved over
+// its TCP link) for cost_model.hpp.  The GPU row-block round has two rates:
+// the NVLink broadcast bandwidth out of rank 0 and the per-GPU multiply rate
+// (mmws_gpu_rowblock_cost).  Collective when the context has a communicator
+// of more than one rank (every rank must call it); otherwise the link rate is
+// NVLink 5's nominal 900 GB/s per direction and marked as not measured.
+struct CostFit {
+  double link_bytes_per_s = 900e9;
+  double gemm_flops_per_s = 0.0;
+  bool link_measured = false;
+};
+
+inline CostFit calibrate(Context& ctx, std::int64_t gemm_n = 4096,
+                         std::int64_t link_bytes = std::int64_t{1} << 28) {
+  CostFit fit;
+  check(mmws_gpu_gemm_probe(ctx.handle(), gemm_n, MMWS_GPU_MODE_AUTO, 3, &fit.gemm_flops_per_s));
+  if (ctx.world_size() > 1) {
+    check(mmws_gpu_link_probe(ctx.handle(), link_bytes, 5, &fit.link_bytes_per_s));
+    fit.link_measured = true;
+  }
+  return fit;
+}
+
+// Predicted seconds of one gpu-rowblock round of an n x n fp64 multiply.
+inline double predicted_seconds(const CostFit& fit, std::int64_t n, int workers) {
+  double t = 0.0;
+  check(mmws_gpu_rowblock_cost(n, n, n, workers, 8, fit.link_bytes_per_s, fit.gemm_flops_per_s,
+                               &t, nullptr, nullptr));
+  return t;
+}
+
+// ---------------------------------------------------------------- plots
+struct PlotSeries {
+  std::string name;
+  std::string color;
+  bool dashed = false;
+  std::vector<std::pair<double, double>> points;  // (N, value), ascending N
+};
+
+namespace plot_detail {
+
+inline std::string num(double v) { return bench_detail::format_g6(v); }
+
+// One linear-axis line chart: title, y label, every series as a polyline
+// carrying data-series="name" and data-points="n:v;n:v" (the values, not the
+// pixels), a marker per point and a legend; x ticks at the measured N.
+inline std::string line_chart(const std::string& title, const std::string& y_label,
+                              const std::vector<PlotSeries>& series,
+                              const std::string& comment) {
+  const double W = 720, H = 480, left = 80, right = 24, top = 48, bottom = 56;
+  const double pw = W - left - right, ph = H - top - bottom;
+  std::vector<double> xs;
+  double ymax = 0.0;
+  for (const auto& s : series)
+    for (const auto& [x, y] : s.points) {
+      xs.push_back(x);
+      ymax = std::max(ymax, y);
+    }
+  std::sort(xs.begin(), xs.end());
+  xs.erase(std::unique(xs.begin(), xs.end()), xs.end());
+  const double x0 = xs.empty() ? 0.0 : xs.front();
+  const double x1 = xs.empty() || xs.back() == x0 ? x0 + 1.0 : xs.back();
+  ymax = ymax > 0.0 ? ymax * 1.08 : 1.0;
+  auto X = [&](double x) { return left + (x - x0) / (x1 - x0) * pw; };
+  auto Y = [&](double y) { return top + ph * (1.0 - y / ymax); };
+  auto text = [](std::ostringstream& o, double x, double y, const char* anchor, int size,
+                 const std::string& body, const std::string& extra = {}) {
+    o << "<text x=\"" << x << "\" y=\"" << y << "\" text-anchor=\"" << anchor
+      << "\" font-size=\"" << size << "\" font-family=\"sans-serif\"" << extra << ">" << body
+      << "</text>\n";
+  };
+  std::ostringstream o;
+  o << "<svg xmlns=\"http://www.w3.org/2000/svg\" width=\"" << W << "\" height=\"" << H
+    << "\" viewBox=\"0 0 " << W << ' ' << H << "\">\n";
+  if (!comment.empty()) o << "<!-- " << comment << " -->\n";
+  o << "<rect width=\"100%\" height=\"100%\" fill=\"white\"/>\n";
+  text(o, W / 2, 26, "middle", 16, title);
+  o << "<path d=\"M" << left << ' ' << top << "V" << top + ph << "H" << left + pw
+    << "\" fill=\"none\" stroke=\"black\"/>\n";
+  for (int t = 0; t <= 5; ++t) {
+    const double v = ymax * t / 5.0;
+    o << "<path d=\"M" << left - 4 << ' ' << Y(v) << "H" << left << "\" stroke=\"black\"/>\n";
+    text(o, left - 8, Y(v) + 4, "end", 11, num(v));
+  }
+  for (double x : xs) {
+    o << "<path d=\"M" << X(x) << ' ' << top + ph << "V" << top + ph + 4
+      << "\" stroke=\"black\"/>\n";
+    text(o, X(x), top + ph + 18, "middle", 11, num(x));
+  }
+  text(o, W / 2, H - 12, "middle", 12, "matrix dimension N");
+  std::ostringstream rot;
+  rot << " transform=\"rotate(-90 18 " << top + ph / 2 << ")\"";
+  text(o, 18, top + ph / 2, "middle", 12, y_label, rot.str());
+  double ly = top + 10;
+  for (const auto& s : series) {
+    std::string data, pts;
+    for (const auto& [x, y] : s.points) {
+      data += (data.empty() ? "" : ";") + num(x) + ":" + num(y);
+      std::ostringstream p;
+      p << (pts.empty() ? "" : " ") << X(x) << ',' << Y(y);
+      pts += p.str();
+    }
+    const std::string dash = s.dashed ? " stroke-dasharray=\"6 3\"" : "";
+    o << "<polyline fill=\"none\" stroke=\"" << s.color << "\" stroke-width=\"2\"" << dash
+      << " data-series=\"" << s.name << "\" data-points=\"" << data << "\" points=\"" << pts
+      << "\"/>\n";
+    for (const auto& [x, y] : s.points)
+      o << "<circle cx=\"" << X(x) << "\" cy=\"" << Y(y) << "\" r=\"3\" fill=\"" << s.color
+        << "\"/>\n";
+    o << "<path d=\"M" << left + pw - 150 << ' ' << ly << "h24\" stroke=\"" << s.color
+      << "\" stroke-width=\"2\"" << dash << "/>\n";
+    text(o, left + pw - 120, ly + 4, "start", 12, s.name);
+    ly += 18;
+  }
+  o << "</svg>\n";
+  return o.str();
+}
+
+inline void write_file(const std::string& path, const std::string& body) {
+  std::ofstream f(path);
+  if (!f) throw IoError("cannot write " + path);
+  f << body;
+  if (!f.flush()) throw IoError("short write to " + path);
+}
+
+inline const char* model_color(const std::string& model) {
+  if (model == "gpu") return "#1f77b4";
+  if (model == "gpu-exact") return "#555555";
+  if (model == "gpu-rowblock") return "#d62728";
+  return "#000000";
+}
+
+}  // namespace plot_detail
+
+// emit_plots (plots.hpp:145-198): runtime.svg, mflops.svg and speedup.svg in
+// `dir`, one series per model in gpu / gpu-exact / gpu-rowblock order.  With
+// a CostFit and gpu-rowblock records, runtime.svg gains the dashed
+// "cost-model" series of predicted round times.
+inline void emit_plots(const std::vector<BenchRecord>& records, const std::string& dir,
+                       const std::optional<CostFit>& fit = std::nullopt) {
+  if (records.empty()) throw DomainError("emit_plots: no records");
+  std::error_code ec;
+  std::filesystem::create_directories(dir, ec);
+  if (ec) throw IoError("cannot create " + dir + ": " + ec.message());
+  auto series_of = [&](auto value_of) {
+    std::vector<PlotSeries> out;
+    for (const char* name : {"gpu", "gpu-exact", "gpu-rowblock"}) {
+      PlotSeries s{name, plot_detail::model_color(name), false, {}};
+      for (const auto& r : records)
+        if (r.model == name)
+          if (const std::optional<double> v = value_of(r))
+            s.points.emplace_back(static_cast<double>(r.n), *v);
+      std::sort(s.points.begin(), s.points.end());
+      if (!s.points.empty()) out.push_back(std::move(s));
+    }
+    return out;
+  };
+  auto runtime = series_of([](const BenchRecord& r) { return std::optional<double>(r.elapsed); });
+  std::string comment;
+  if (fit) {
+    PlotSeries model{"cost-model", "#2ca02c", true, {}};
+    for (const auto& r : records)
+      if (r.model == "gpu-rowblock")
+        model.points.emplace_back(static_cast<double>(r.n), predicted_seconds(*fit, r.n, r.workers));
+    std::sort(model.points.begin(), model.points.end());
+    if (!model.points.empty()) {
+      runtime.push_back(std::move(model));
+      comment = "cost-model overlay: link=" + plot_detail::num(fit->link_bytes_per_s) +
+                " B/s (" + (fit->link_measured ? "measured" : "nominal") +
+                "), gemm=" + plot_detail::num(fit->gemm_flops_per_s) +
+                " FLOP/s; predicted seconds = mmws_gpu_rowblock_cost";
+    }
+  }
+  plot_detail::write_file(dir + "/runtime.svg",
+                          plot_detail::line_chart("Running time vs matrix dimension",
+                                                  "elapsed seconds", runtime, comment));
+  plot_detail::write_file(
+      dir + "/mflops.svg",
+      plot_detail::line_chart("Throughput vs matrix dimension", "MFLOPS",
+                              series_of([](const BenchRecord& r) {
+                                return std::optional<double>(r.mflops);
+                              }),
+                              {}));
+  plot_detail::write_file(
+      dir + "/speedup.svg",
+      plot_detail::line_chart("Speedup over sequential vs matrix dimension", "speedup",
+                              series_of([](const BenchRecord& r) { return r.speedup; }), {}));
 }
 
 }  // namespace gpu

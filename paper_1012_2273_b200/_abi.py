@@ -49,6 +49,8 @@ SIGNATURES = {
     "mmws_gpu_ipc_export": (_i, [_v, _v, _p(C.c_uint8)]),
     "mmws_gpu_ipc_open": (_i, [_v, _p(C.c_uint8), _p(_v)]),
     "mmws_gpu_peak_probe": (_i, [_v, _i, _i, _p(_d)]),
+    "mmws_gpu_gemm_probe": (_i, [_v, _i64, _i, _i, _p(_d)]),
+    "mmws_gpu_link_probe": (_i, [_v, _i64, _i, _p(_d)]),
     "mmws_gpu_nccl_unique_id": (_i, [_p(C.c_uint8)]),
     "mmws_gpu_comm_init": (_i, [_v, _i, _i, _p(C.c_uint8)]),
     "mmws_gpu_comm_destroy": (_i, [_v]),

@@ -281,6 +281,18 @@ class Context:
         _check(_lib().mmws_gpu_peak_probe(self._h, which, iters, C.byref(out)))
         return out.value
 
+    def gemm_probe(self, n: int = 4096, mode: int = MODE_AUTO, iters: int = 3) -> float:
+        """Device-resident n x n multiply rate in FLOP/s (cost-model calibration)."""
+        out = C.c_double()
+        _check(_lib().mmws_gpu_gemm_probe(self._h, n, mode, iters, C.byref(out)))
+        return out.value
+
+    def link_probe(self, nbytes: int = 1 << 28, iters: int = 5) -> float:
+        """Collective: broadcast bandwidth from rank 0 in bytes/s (needs comm_init)."""
+        out = C.c_double()
+        _check(_lib().mmws_gpu_link_probe(self._h, nbytes, iters, C.byref(out)))
+        return out.value
+
     # -- row-block distribution
     def comm_init(self, nranks: int, rank: int, uid: bytes) -> None:
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)

@@ -500,4 +500,42 @@ int mmws_gpu_peak_probe(mmws_gpu_ctx* ctx, int which, int iters, double* tflops)
   return ok();
 }
 
+int mmws_gpu_gemm_probe(mmws_gpu_ctx* ctx, int64_t n, int mode, int iters, double* flops_per_s) {
+  MMWS_CTX_GUARD(ctx);
+  if (n < 1 || n > 65536 || iters < 1 || !flops_per_s)
+    return fail(MMWS_GPU_ERR_DOMAIN, "gemm_probe: bad arguments");
+  const size_t bytes = sizeof(double) * n * n;
+  void* buf = nullptr;
+  cudaError_t e = cudaMalloc(&buf, 3 * bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "gemm_probe: buffers");
+  double* A = static_cast<double*>(buf);
+  double* B = A + n * n;
+  double* C = B + n * n;
+  const Launch L = ctx->launch(nullptr);
+  int rc = MMWS_GPU_OK;
+  if ((e = launch_fill(L, MMWS_GPU_DIST_UNIFORM, 0, A, n, n, n, 0, 0)) ||
+      (e = launch_fill(L, MMWS_GPU_DIST_UNIFORM, 1, B, n, n, n, 0, 0))) {
+    rc = cuda_fail(e, "gemm_probe: fill");
+  } else if ((rc = dgemm_dispatch(ctx, n, n, n, A, n, B, n, C, n, mode, ctx->stream)) ==
+             MMWS_GPU_OK) {  // warm-up
+    cudaEventRecord(ctx->ev0, ctx->stream);
+    for (int i = 0; i < iters && rc == MMWS_GPU_OK; ++i)
+      rc = dgemm_dispatch(ctx, n, n, n, A, n, B, n, C, n, mode, ctx->stream);
+    cudaEventRecord(ctx->ev1, ctx->stream);
+    if (rc == MMWS_GPU_OK) {
+      if ((e = cudaStreamSynchronize(ctx->stream)) != cudaSuccess) {
+        rc = cuda_fail(e, "gemm_probe");
+      } else {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+        *flops_per_s = 2.0 * static_cast<double>(n) * n * n * iters / (ms * 1e-3);
+      }
+    }
+  }
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->server) ctx->deferred_free.push_back(buf);  // cudaFree would wait for the server
+  else cudaFree(buf);
+  return rc == MMWS_GPU_OK ? ok() : rc;
+}
+
 }  // extern "C"

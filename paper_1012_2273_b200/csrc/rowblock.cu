@@ -411,6 +411,30 @@ int mmws_gpu_last_kernel_ms(mmws_gpu_ctx* ctx, double* ms) {
   return ok();
 }
 
+int mmws_gpu_link_probe(mmws_gpu_ctx* ctx, int64_t bytes, int iters, double* bytes_per_s) {
+  MMWS_CTX_GUARD(ctx);
+  if (bytes < 1 || iters < 1 || !bytes_per_s)
+    return fail(MMWS_GPU_ERR_DOMAIN, "link_probe: bad arguments");
+  if (!ctx->comm) return fail(MMWS_GPU_ERR_STATE, "link_probe: no communicator (comm_init)");
+  NCCL_REQUIRE();
+  cudaError_t e;
+  if ((e = ensure(ctx, &ctx->rbB, &ctx->rbB_bytes, static_cast<size_t>(bytes))) != cudaSuccess)
+    return cuda_fail(e, "link_probe: buffer");
+  cudaStream_t s = ctx->comm_stream;
+  NCCL_TRY(nccl().Broadcast(ctx->rbB, ctx->rbB, bytes, ncclUint8, 0, ctx->comm, s),
+           "link_probe warm-up");
+  cudaEventRecord(ctx->ev0, s);
+  for (int i = 0; i < iters; ++i)
+    NCCL_TRY(nccl().Broadcast(ctx->rbB, ctx->rbB, bytes, ncclUint8, 0, ctx->comm, s),
+             "link_probe broadcast");
+  cudaEventRecord(ctx->ev1, s);
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "link_probe");
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+  *bytes_per_s = static_cast<double>(bytes) * iters / (ms * 1e-3);
+  return ok();
+}
+
 int mmws_gpu_rowblock_cost(int64_t m, int64_t n, int64_t k, int nranks, int elem_bytes,
                            double link_bytes_per_s, double gemm_flops_per_s, double* seconds,
                            double* root_egress_bytes, double* root_ingress_bytes) {

@@ -5,12 +5,44 @@
 #include <cinttypes>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "mmws_gpu_bench.hpp"
 
 namespace G = mmws::gpu;
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1) {  // emit_plots on fixed records (plots.hpp:145-198 analogue)
+    std::vector<G::BenchRecord> recs = {
+        {"gpu", 500, 1, 0.002, 1.0e5, 30.0, 0.0},
+        {"gpu", 100, 1, 0.0001, 2.0e4, 4.0, 0.0},
+        {"gpu-exact", 100, 1, 0.0002, 1.0e4, std::nullopt, 0.0},
+        {"gpu-rowblock", 4096, 4, 0.01, 1.3e7, std::nullopt, 0.0},
+        {"gpu-rowblock", 2048, 4, 0.003, 5.7e6, std::nullopt, 0.0}};
+    G::CostFit fit;
+    fit.link_bytes_per_s = 500e9;
+    fit.gemm_flops_per_s = 3.0e13;
+    G::emit_plots(recs, argv[1], fit);
+    bool threw = false;
+    try {
+      G::emit_plots({}, argv[1]);
+    } catch (const mmws::DomainError&) {
+      threw = true;
+    }
+    // a regular file where the directory should be: IoError (test_plots.cpp:204-212)
+    const std::string blocker = std::string(argv[1]) + "/blocker";
+    { std::FILE* f = std::fopen(blocker.c_str(), "w"); if (f) std::fclose(f); }
+    bool io_threw = false;
+    try {
+      G::emit_plots(recs, blocker + "/sub");
+    } catch (const mmws::IoError&) {
+      io_threw = true;
+    }
+    std::remove(blocker.c_str());
+    std::printf("{\"empty_throws\": %s, \"io_error\": %s}\n", threw ? "true" : "false",
+                io_threw ? "true" : "false");
+    return 0;
+  }
   std::printf("{\"derive_seed\": {");
   bool first = true;
   for (std::uint64_t s : {0ULL, 42ULL, (1ULL << 63) + 5})

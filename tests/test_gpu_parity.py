@@ -278,9 +278,21 @@ def test_rowblock_nccl_path_single_rank(oracle):
         Cf = T.empty_like(Af)
         c2.rowblock(n, n, n, Af, Bf, Cf, f32=True)
         assert (host(Cf) == host(c2.sgemm(Af, Bf))).all()
+        # cost-model calibration probes (bench_main.cpp:64-93 analogue)
+        assert c2.link_probe(1 << 24, 3) > 1e9
         c2.comm_destroy()
+        with pytest.raises(P.GpuError):
+            c2.link_probe(1 << 20, 1)                                 # needs a communicator
     finally:
         c2.close()
+
+
+def test_gemm_probe_rate(ctx):
+    r = ctx.gemm_probe(2048, P.MODE_AUTO, 3)
+    assert 5e12 < r < 40e12                       # FP64 tensor pipe: <= 37.2 TFLOP/s
+    assert ctx.gemm_probe(512, P.MODE_EXACT, 2) < r
+    with pytest.raises(P.DomainError):
+        ctx.gemm_probe(0)
 
 
 def _ipc_child(conn):

@@ -34,6 +34,41 @@ def test_harness_host_pieces_match_reference(tmp_path, golden_small):
     assert got["mflops_zero_throws"] is True
 
 
+def _series(svg_path):
+    import re
+    text = open(svg_path).read()
+    out = {}
+    for name, pts, rest in re.findall(r'data-series="([^"]+)" data-points="([^"]*)"( [^>]*)?', text):
+        out[name] = [tuple(float(v) for v in p.split(":")) for p in pts.split(";")]
+        out[name + "#dashed"] = "stroke-dasharray" in text.split(f'data-series="{name}"')[0].rsplit("<polyline", 1)[1]
+    return text, out
+
+
+def test_plots_series_and_cost_overlay(tmp_path):
+    import paper_1012_2273_b200 as P
+    exe = _build(os.path.join(ROOT, "tests", "cpp", "test_harness.cpp"), tmp_path / "th")
+    d = tmp_path / "plots"
+    got = json.loads(subprocess.run([exe, str(d)], capture_output=True, text=True,
+                                    check=True).stdout)
+    assert got["empty_throws"] is True and got["io_error"] is True
+    assert sorted(os.listdir(d)) == ["mflops.svg", "runtime.svg", "speedup.svg"]
+    text, s = _series(d / "runtime.svg")
+    assert text.startswith("<svg") and "Running time vs matrix dimension" in text
+    assert s["gpu"] == [(100.0, 0.0001), (500.0, 0.002)]           # sorted by N
+    assert s["gpu-exact"] == [(100.0, 0.0002)]
+    assert s["gpu-rowblock"] == [(2048.0, 0.003), (4096.0, 0.01)]
+    want = [(float(n), P.rowblock_cost(n, n, n, 4, 8, 500e9, 3e13)[0]) for n in (2048, 4096)]
+    assert [x for x, _ in s["cost-model"]] == [x for x, _ in want]
+    for (_, a), (_, b) in zip(s["cost-model"], want):
+        assert abs(a - b) <= 1e-5 * b                                  # %.6g in the attribute
+    assert s["cost-model#dashed"] and not s["gpu#dashed"]
+    assert "cost-model overlay: link=5e+11 B/s (nominal)" in text
+    _, m = _series(d / "mflops.svg")
+    assert m["gpu-rowblock"] == [(2048.0, 5.7e6), (4096.0, 1.3e7)] and "cost-model" not in m
+    _, sp = _series(d / "speedup.svg")
+    assert sp == {"gpu": [(100.0, 4.0), (500.0, 30.0)], "gpu#dashed": False}
+
+
 def test_cli_builds_standalone_and_against_reference(tmp_path):
     _build(os.path.join(ROOT, "tools", "mmws_gpu_bench.cpp"), tmp_path / "b1")
     if os.path.exists(os.path.join(REF_INC, "mmws", "matrix.hpp")):
@@ -46,13 +81,18 @@ def test_cli_sweep_with_gate(tmp_path):
     exe = _build(os.path.join(ROOT, "tools", "mmws_gpu_bench.cpp"), tmp_path / "b")
     csv = tmp_path / "out.csv"
     r = subprocess.run([exe, "--dims", "10,100,257,1000", "--models", "gpu,gpu-exact,gpu-rowblock",
-                        "--repeats", "2", "--csv", str(csv)], capture_output=True, text=True)
+                        "--repeats", "2", "--csv", str(csv), "--plots", str(tmp_path / "svg"),
+                        "--calibrate"], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
     lines = csv.read_text().splitlines()
     assert lines[0] == "model,n,workers,elapsed_s,mflops,speedup"
     assert len(lines) == 1 + 12
     models = [ln.split(",")[0] for ln in lines[1:]]
     assert models == ["gpu"] * 4 + ["gpu-exact"] * 4 + ["gpu-rowblock"] * 4
+    assert "calibration: link 9e+11 B/s (nominal NVLink 5), gemm" in r.stdout
+    _, s = _series(tmp_path / "svg" / "runtime.svg")
+    assert [x for x, _ in s["cost-model"]] == [10.0, 100.0, 257.0, 1000.0]
+    assert [x for x, _ in s["gpu-rowblock"]] == [10.0, 100.0, 257.0, 1000.0]
     for ln in lines[1:]:
         f = ln.split(",")
         assert float(f[3]) > 0 and float(f[4]) > 0 and f[5] == ""

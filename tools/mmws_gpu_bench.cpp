@@ -4,6 +4,7 @@
 //
 //   mmws_gpu_bench --dims 100,500,1000 [--models gpu,gpu-exact] [--repeats 3]
 //                  [--seed 42] [--csv out.csv] [--tolerance 1e-12] [--server]
+//                  [--plots DIR] [--calibrate]
 //
 // Build: g++ -std=c++20 -O2 -Iinclude tools/mmws_gpu_bench.cpp
 //            -Lpaper_1012_2273_b200 -lmmws_gpu -Wl,-rpath,<repo>/paper_1012_2273_b200
@@ -30,7 +31,7 @@ std::vector<std::string> split(const std::string& s) {
 int usage() {
   std::fprintf(stderr,
                "usage: mmws_gpu_bench --dims N1,N2,... [--models gpu,gpu-exact,gpu-rowblock] "
-               "[--repeats R] [--seed S] [--tolerance T] [--csv PATH] [--device D] [--server]\n");
+               "[--repeats R] [--seed S] [--tolerance T] [--csv PATH] [--device D] [--server] [--plots DIR] [--calibrate]\n");
   return 2;
 }
 
@@ -38,7 +39,8 @@ int usage() {
 
 int main(int argc, char** argv) {
   mmws::gpu::BenchConfig config;
-  std::string csv_path;
+  std::string csv_path, plots_dir;
+  bool calibrate = false;  // bench_main.cpp:64-93 analogue: fit the row-block cost model
   int device = 0;
   bool server = false;  // resident latency server for N <= 96 (mmws_gpu_server_start)
   try {
@@ -63,6 +65,10 @@ int main(int argc, char** argv) {
         csv_path = value();
       } else if (arg == "--device") {
         device = std::stoi(value());
+      } else if (arg == "--plots") {
+        plots_dir = value();
+      } else if (arg == "--calibrate") {
+        calibrate = true;
       } else if (arg == "--server") {
         server = true;
       } else {
@@ -79,6 +85,13 @@ int main(int argc, char** argv) {
       std::printf("%-13s %8lld %8d %14.6g %14.6g %12.3g\n", r.model.c_str(),
                   static_cast<long long>(r.n), r.workers, r.elapsed, r.mflops, r.rel_err);
     if (!csv_path.empty()) mmws::gpu::emit_csv(records, csv_path);
+    std::optional<mmws::gpu::CostFit> fit;
+    if (calibrate) {
+      fit = mmws::gpu::calibrate(ctx);
+      std::printf("calibration: link %.6g B/s (%s), gemm %.6g FLOP/s\n", fit->link_bytes_per_s,
+                  fit->link_measured ? "measured" : "nominal NVLink 5", fit->gemm_flops_per_s);
+    }
+    if (!plots_dir.empty()) mmws::gpu::emit_plots(records, plots_dir, fit);
   } catch (const mmws::gpu::GateError& e) {
     std::fprintf(stderr, "mmws_gpu_bench: %s\n", e.what());
     return 2;  // bench_main.cpp:175-177
