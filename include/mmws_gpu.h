@@ -174,8 +174,8 @@ int mmws_gpu_graph_destroy(mmws_gpu_graph* graph);
  * (cudaDeviceSynchronize, torch.cuda.synchronize, cudaFree) waits for it --
  * synchronise streams instead.  The same holds for the lazy loading
  * (CUDA_MODULE_LOADING=LAZY, the default) of a kernel first launched while it
- * runs: server_start preloads this library's kernels; other libraries' (torch,
- * NCCL) need CUDA_MODULE_LOADING=EAGER or a warm-up launch before it. */
+ * runs: mmws_gpu_init loads all of this library's kernels; other libraries'
+ * (torch, NCCL) need CUDA_MODULE_LOADING=EAGER or a warm-up launch first. */
 int mmws_gpu_server_start(mmws_gpu_ctx* ctx);
 /* Host matrices (any memory); m, n, k <= 96.  *elapsed_s = host wall time of
  * the call (copy in, compute, copy out). */

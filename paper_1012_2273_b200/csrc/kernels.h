@@ -40,8 +40,8 @@ struct DmmaStream {
 };
 // Force-load kernels (cudaFuncGetAttributes).  Under CUDA_MODULE_LOADING=LAZY
 // the first launch of a kernel loads it with a context-wide synchronisation,
-// which would wait forever on the resident latency server: server_start
-// preloads every kernel of the library first.
+// which would wait forever on the resident latency server (and costs tens of
+// ms inside a timed call): mmws_gpu_init preloads every kernel of the library.
 template <class... F>
 cudaError_t preload_kernels(F... f) {
   cudaFuncAttributes attr;

@@ -229,6 +229,13 @@ int mmws_gpu_init(int device, mmws_gpu_ctx** out) {
     return fail(MMWS_GPU_ERR_STATE, std::string("mmws_gpu_init: built for sm_100a, device is ") +
                                         prop.name + " (sm_" + std::to_string(prop.major) +
                                         std::to_string(prop.minor) + ")");
+  // Load every kernel of the library now: under CUDA_MODULE_LOADING=LAZY (the
+  // default) a kernel's first launch would otherwise pay its module load
+  // inside the caller's timed region (~70 ms on the first streamed host
+  // multiply at N=16384), and the latency server relies on it (server.cu).
+  if ((e = preload_dgemm_dmma()) || (e = preload_dgemm_exact()) || (e = preload_dgemm_small()) ||
+      (e = preload_sgemm()) || (e = preload_sgemm_tma()) || (e = preload_misc()))
+    return cuda_fail(e, "mmws_gpu_init: load kernels");
   auto* ctx = new (std::nothrow) mmws_gpu_ctx();
   if (!ctx) return fail(MMWS_GPU_ERR_ALLOC, "mmws_gpu_init: out of host memory");
   ctx->device = device;

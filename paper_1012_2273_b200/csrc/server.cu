@@ -301,12 +301,7 @@ int mmws_gpu_server_start(mmws_gpu_ctx* ctx) {
     server_free(s);
     return cuda_fail(e, "server_start");
   }
-  // every other kernel of the library must be loaded before the server runs
-  if ((e = preload_dgemm_dmma()) || (e = preload_dgemm_exact()) || (e = preload_dgemm_small()) ||
-      (e = preload_sgemm()) || (e = preload_sgemm_tma()) || (e = preload_misc())) {
-    server_free(s);
-    return cuda_fail(e, "server_start: preload kernels");
-  }
+  // (every other kernel of the library was loaded by mmws_gpu_init)
   // cooperative launch: all CTAs must be co-resident for the grid barrier
   void* args[] = {&s->dev, &s->scratch, &s->sync};
   if ((e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(server_kernel), dim3(s->ctas),
