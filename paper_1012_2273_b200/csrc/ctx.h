@@ -79,7 +79,6 @@ namespace mmws_impl {
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
 int ok();
-// grow a device buffer to at least `bytes`
 // Grow a device buffer to at least `bytes`.  While the latency server runs,
 // cudaFree (a device-wide synchronisation) would wait for it forever, so the
 // old buffer is parked in deferred_free instead (growth at least doubles).
@@ -106,4 +105,33 @@ int host_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A
 int sgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const float* A,
                    int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int mode,
                    cudaStream_t stream);
+
+// fp64 / fp32 multiply through the matching dispatch
+template <class T>
+int gemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, int64_t lda, const T* B,
+         int64_t ldb, T* C, int64_t ldc, int mode, cudaStream_t s) {
+  if constexpr (sizeof(T) == 8)
+    return dgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode, s);
+  else
+    return sgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode, s);
+}
+
+// at least `need` ordering events (timing disabled) in ctx->pool
+inline cudaError_t event_pool(mmws_gpu_ctx* ctx, size_t need) {
+  while (ctx->pool.size() < need) {
+    cudaEvent_t ev;
+    cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+    ctx->pool.push_back(ev);
+  }
+  return cudaSuccess;
+}
 }  // namespace mmws_impl
+
+// Entry guard of every C-ABI function taking a context: null check, the
+// context's mutex for the rest of the call, its device made current.
+#define MMWS_CTX_GUARD(ctx)                                                  \
+  if (!(ctx)) return mmws_impl::fail(MMWS_GPU_ERR_STATE, "null mmws_gpu_ctx"); \
+  std::lock_guard<std::mutex> guard_((ctx)->mu);                             \
+  if (cudaError_t e_ = cudaSetDevice((ctx)->device); e_ != cudaSuccess)      \
+    return mmws_impl::cuda_fail(e_, "cudaSetDevice");

@@ -28,25 +28,6 @@ namespace mmws_impl {
 
 namespace {
 
-cudaError_t event_pool(mmws_gpu_ctx* ctx, size_t need) {
-  while (ctx->pool.size() < need) {
-    cudaEvent_t ev;
-    cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    if (e != cudaSuccess) return e;
-    ctx->pool.push_back(ev);
-  }
-  return cudaSuccess;
-}
-
-template <class T>
-int gemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, int64_t lda, const T* B,
-         int64_t ldb, T* C, int64_t ldc, int mode, cudaStream_t s) {
-  if constexpr (sizeof(T) == 8)
-    return dgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode, s);
-  else
-    return sgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode, s);
-}
-
 // Streamed variant (fp64 DMMA, big problems): one persistent GEMM over the
 // whole C that starts on tiles whose A rows and B columns have already
 // crossed PCIe.  Copy-in interleaves 256-row bands of A and 512-column bands

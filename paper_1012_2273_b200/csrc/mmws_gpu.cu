@@ -187,13 +187,6 @@ struct mmws_gpu_graph {
   uint64_t kernels = 0;
 };
 
-#define MMWS_CTX_GUARD(ctx)                                                  \
-  if (!(ctx)) return fail(MMWS_GPU_ERR_STATE, "null mmws_gpu_ctx");          \
-  std::lock_guard<std::mutex> guard_((ctx)->mu);                             \
-  if (cudaError_t e_ = cudaSetDevice((ctx)->device); e_ != cudaSuccess)      \
-    return cuda_fail(e_, "cudaSetDevice");
-
-
 namespace {
 // The NCCL stream gets the highest priority so its CTAs are scheduled ahead of
 // pending GEMM CTAs whenever an SM frees up -- otherwise the C gather of a
@@ -379,7 +372,6 @@ int mmws_gpu_sgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const flo
   return sgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode,
                         static_cast<cudaStream_t>(stream));
 }
-
 
 int mmws_gpu_matmul_host(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
                          const double* B, double* C, int mode, double* elapsed_s) {

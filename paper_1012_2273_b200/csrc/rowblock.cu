@@ -38,8 +38,6 @@ int nccl_fail(ncclResult_t r, const char* what) {
 #define NCCL_REQUIRE()                                                          \
   if (!nccl().ok) return fail(MMWS_GPU_ERR_NCCL, "libnccl.so.2 could not be loaded");
 
-
-
 #define NCCL_TRY(call, what)                                   \
   do {                                                         \
     ncclResult_t r_ = (call);                                  \
@@ -49,25 +47,6 @@ int nccl_fail(ncclResult_t r, const char* what) {
 template <class T>
 T* as_mut(const T* p) {
   return const_cast<T*>(p);
-}
-
-template <class T>
-int gemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, int64_t lda, const T* B,
-         int64_t ldb, T* C, int64_t ldc, int mode, cudaStream_t s) {
-  if constexpr (sizeof(T) == 8)
-    return dgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode, s);
-  else
-    return sgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode, s);
-}
-
-cudaError_t event_pool(mmws_gpu_ctx* ctx, size_t need) {
-  while (ctx->pool.size() < need) {
-    cudaEvent_t ev;
-    cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    if (e != cudaSuccess) return e;
-    ctx->pool.push_back(ev);
-  }
-  return cudaSuccess;
 }
 
 // Who holds which rows, and the sub-block cut of every rank's rows -- derived
@@ -329,12 +308,6 @@ int master_run_host(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T*
 }
 
 }  // namespace
-
-#define MMWS_CTX_GUARD(ctx)                                              \
-  if (!(ctx)) return fail(MMWS_GPU_ERR_STATE, "null mmws_gpu_ctx");      \
-  std::lock_guard<std::mutex> guard_((ctx)->mu);                         \
-  if (cudaError_t e_ = cudaSetDevice((ctx)->device); e_ != cudaSuccess)  \
-    return cuda_fail(e_, "cudaSetDevice");
 
 extern "C" {
 

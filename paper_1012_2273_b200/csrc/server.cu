@@ -264,12 +264,6 @@ void server_destroy(mmws_gpu_ctx* ctx) {
 
 using namespace mmws_impl;
 
-#define MMWS_CTX_GUARD(ctx)                                              \
-  if (!(ctx)) return fail(MMWS_GPU_ERR_STATE, "null mmws_gpu_ctx");      \
-  std::lock_guard<std::mutex> guard_((ctx)->mu);                         \
-  if (cudaError_t e_ = cudaSetDevice((ctx)->device); e_ != cudaSuccess)  \
-    return cuda_fail(e_, "cudaSetDevice");
-
 extern "C" {
 
 int mmws_gpu_server_start(mmws_gpu_ctx* ctx) {
