@@ -47,6 +47,14 @@ struct mmws_gpu_ctx {
   // packing workspace (device), grown on demand
   void* ws = nullptr;
   size_t ws_bytes = 0;
+  // stream-K workspaces, one per launch stream (fixed size, never moved):
+  // (num_sms + 1) accumulator slots of 128 x 128 doubles + their flags
+  struct SkSpace {
+    cudaStream_t stream;
+    void* mem;
+  };
+  std::vector<SkSpace> sk_spaces;
+  bool allow_streamk = true;  // false while a row-block round overlaps NCCL with multiplies
   // host-entry staging buffers (device)
   void* dA = nullptr;
   void* dB = nullptr;

@@ -77,20 +77,36 @@ MMWS_DEVICE void wait_flag(const int* f) {
     if (global_ns() - t0 > 60ull * 1000000000ull) __trap();
   }
 }
+MMWS_DEVICE void set_flag(int* f, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+}
 
-// STREAM = false: one CTA per tile, grouped rasterisation (the device-pointer
-// path).  STREAM = true: persistent CTAs walk a host-ordered tile list
-// (CTA b takes entries b, b + grid, ...), the producer waits for the A row
-// band and B column band of each tile to have arrived (flags), and the math
-// warps count finished tiles per tile row so a copy stream can ship C rows
-// back while the rest computes (host_pipeline.cu).  The per-element
-// arithmetic is the same either way.
-template <class K, bool STREAM>
+// MODE 0 (one-shot): one CTA per tile, grouped rasterisation (the
+// device-pointer path).
+// MODE 1 (streamed): persistent CTAs walk a host-ordered tile list (CTA b
+// takes entries b, b + grid, ...), the producer waits for the A row band and
+// B column band of each tile to have arrived (flags), and the math warps
+// count finished tiles per tile row so a copy stream can ship C rows back
+// while the rest computes (host_pipeline.cu).
+// MODE 2 (stream-K, in-order fix-up): one persistent CTA per SM; CTA b owns
+// the global k-iterations [W*b/G, W*(b+1)/G) of the W = tiles*KT iteration
+// space, so every SM gets the same work whatever the tile count (no
+// partial last wave).  A tile cut by a range boundary is finished by the
+// upper CTA *continuing* the lower CTA's accumulators: the lower CTA walks
+// its range top-down, so the tile's first k-iterations are its first unit;
+// it parks the fp64 accumulators in a workspace slot and raises a flag; the
+// upper CTA's last unit waits for the flag, reloads them and carries on with
+// the next k.  Every element still sees one DMMA chain in ascending k from
+// +0.0, so the result is bitwise the one-shot kernel's.  Needs each range to
+// hold at least one tile's K (W/G >= KT), so a tile spans at most two CTAs.
+// The per-element arithmetic is the same in all modes.
+template <class K, int MODE>
 __global__ void __launch_bounds__(K::THREADS, K::MINB)
     dgemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB, double* __restrict__ C,
                       int64_t ldc, int M, int N, int K_, int tiles_m, int tiles_n, int vec_ok,
                       DmmaStream st) {
+  constexpr bool STREAM = MODE == 1, SK = MODE == 2;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   // 1024-byte aligned ring (128B-swizzle atoms); offsetting the __shared__
   // array itself keeps the shared address space visible, so fragment fetches
@@ -105,11 +121,24 @@ __global__ void __launch_bounds__(K::THREADS, K::MINB)
   // Tile coordinates.  One-shot: grouped rasterisation (GROUP tile-rows advance
   // together so the A and B panels of one wave are shared through L2).
   // Streamed: the host's arrival-ordered list.
+  auto raster = [&](int tile, int& tm, int& tn) {
+    // 12 tile-rows per group: a 148-CTA wave covers ~12 x 12 tiles, the
+    // squarest footprint (fewest distinct A+B panels per wave); measured at
+    // N=16384: 48.6 GB DRAM reads vs 52.2 (8 rows) / 78.3 (4 rows), same time
+    constexpr int GROUP = 12;
+    const int per_group = GROUP * tiles_n;
+    const int first_m = (tile / per_group) * GROUP;
+    const int gm = min(tiles_m - first_m, GROUP);
+    tm = first_m + (tile % per_group) % gm;
+    tn = (tile % per_group) / gm;
+  };
   auto tile_at = [&](int idx, int& tm, int& tn) {
     if constexpr (STREAM) {
       const int t = st.order[idx];
       tm = t / tiles_n;
       tn = t % tiles_n;
+    } else if constexpr (SK) {
+      raster(idx, tm, tn);
     } else {
       // 12 tile-rows per group: a 148-CTA wave covers ~12 x 12 tiles, the
       // squarest footprint (fewest distinct A+B panels per wave); measured at
@@ -138,6 +167,34 @@ __global__ void __launch_bounds__(K::THREADS, K::MINB)
 
   const int KT = (K_ + K::BK - 1) / K::BK;
 
+  // Work units: (tile, k-iterations [k0, k1)).  Modes 0/1: whole tiles in
+  // list order.  Mode 2: this CTA's iteration range, top-down.
+  const long long sk_w = static_cast<long long>(tiles_m) * tiles_n * KT;
+  const long long sk_lo = SK ? sk_w * blockIdx.x / gridDim.x : 0;
+  struct Cursor {
+    int idx;
+    long long pos;
+  };
+  auto next_unit = [&](Cursor& cur, int& tile, int& k0, int& k1) -> bool {
+    if constexpr (SK) {
+      if (cur.pos <= sk_lo) return false;
+      tile = static_cast<int>((cur.pos - 1) / KT);
+      const long long base = static_cast<long long>(tile) * KT;
+      k0 = static_cast<int>((sk_lo > base ? sk_lo : base) - base);
+      k1 = static_cast<int>(cur.pos - base);
+      cur.pos = base + k0;
+      return true;
+    } else {
+      if (cur.idx >= n_idx) return false;
+      tile = cur.idx;
+      cur.idx += idx_step;
+      k0 = 0;
+      k1 = KT;
+      return true;
+    }
+  };
+  const Cursor cur0{idx0, SK ? sk_w * (blockIdx.x + 1) / gridDim.x : 0};
+
   if (warp >= K::CONSUMERS) {
     // ---------------- TMA producer ----------------
     if constexpr (K::MATH_REGS > 0)
@@ -146,7 +203,9 @@ __global__ void __launch_bounds__(K::THREADS, K::MINB)
       tma_prefetch_desc(&tmA);
       tma_prefetch_desc(&tmB);
       int kg = 0;  // stage counter, continuous across tiles
-      for (int idx = idx0; idx < n_idx; idx += idx_step) {
+      Cursor cur = cur0;
+      int idx, k0, k1;
+      while (next_unit(cur, idx, k0, k1)) {
         int tm, tn;
         tile_at(idx, tm, tn);
         if constexpr (STREAM) {
@@ -154,7 +213,7 @@ __global__ void __launch_bounds__(K::THREADS, K::MINB)
           wait_flag(st.ready_b + tn / st.band_b);
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
-        for (int kt = 0; kt < KT; ++kt, ++kg) {
+        for (int kt = k0; kt < k1; ++kt, ++kg) {
           const int s = kg % K::STAGES;
           if (kg >= K::STAGES) mbar_wait(&empty[s], ((kg / K::STAGES) - 1) & 1);
           uint8_t* sa = smem + s * K::STAGE_BYTES;
@@ -195,7 +254,13 @@ __global__ void __launch_bounds__(K::THREADS, K::MINB)
     }
 
   int kg = 0;  // stage counter, continuous across tiles
-  for (int idx = idx0; idx < n_idx; idx += idx_step) {
+  Cursor cur = cur0;
+  int idx, k0, k1;
+  // stream-K workspace slot of this thread's accumulators (slot s holds the
+  // tile cut by the boundary between CTAs s-1 and s)
+  constexpr int ACC_PER_THREAD = K::MI * K::NB * 4;
+  constexpr int MATH_THREADS = K::CONSUMERS * 32;
+  while (next_unit(cur, idx, k0, k1)) {
     int tm, tn;
     tile_at(idx, tm, tn);
     double acc[K::MI][K::NB][2][2];
@@ -205,8 +270,19 @@ __global__ void __launch_bounds__(K::THREADS, K::MINB)
       for (int b = 0; b < K::NB; ++b)
   #pragma unroll
         for (int e = 0; e < 2; ++e) acc[i][b][e][0] = acc[i][b][e][1] = 0.0;
+    if constexpr (SK) {
+      if (k0 > 0) {  // continue the lower CTA's accumulators for this tile
+        if (threadIdx.x == 0) wait_flag(st.flags + blockIdx.x);
+        asm volatile("bar.sync 1, %0;" ::"n"(MATH_THREADS) : "memory");
+        const double* src = st.partial + static_cast<size_t>(blockIdx.x) * ACC_PER_THREAD * MATH_THREADS;
+        double* a = &acc[0][0][0][0];
+  #pragma unroll
+        for (int j = 0; j < ACC_PER_THREAD; ++j) a[j] = __ldcg(src + j * MATH_THREADS + threadIdx.x);
+        if (threadIdx.x == 0) st.flags[blockIdx.x] = 0;  // consumed: ready for the next launch
+      }
+    }
 
-    for (int kt = 0; kt < KT; ++kt, ++kg) {
+    for (int kt = k0; kt < k1; ++kt, ++kg) {
       const int s = kg % K::STAGES;
       mbar_wait(&full[s], (kg / K::STAGES) & 1);
       // Release the PREVIOUS stage here, not at the end of its own iteration:
@@ -245,6 +321,22 @@ __global__ void __launch_bounds__(K::THREADS, K::MINB)
             }
       }
 
+    }
+
+    if constexpr (SK) {
+      if (k1 < KT) {  // first part of a tile the upper CTA finishes: park it
+        double* dst =
+            st.partial + static_cast<size_t>(blockIdx.x + 1) * ACC_PER_THREAD * MATH_THREADS;
+        const double* a = &acc[0][0][0][0];
+  #pragma unroll
+        for (int j = 0; j < ACC_PER_THREAD; ++j) __stcg(dst + j * MATH_THREADS + threadIdx.x, a[j]);
+        asm volatile("bar.sync 1, %0;" ::"n"(MATH_THREADS) : "memory");
+        if (threadIdx.x == 0) {
+          __threadfence();
+          set_flag(st.flags + blockIdx.x + 1, 1);
+        }
+        continue;
+      }
     }
 
     // ---------------- epilogue: registers -> global ----------------
@@ -301,13 +393,13 @@ cudaError_t run(const Launch& L, int64_t M, int64_t N, int64_t Kd, const double*
   if (!make_map(L, &ta, A, Kd, M, lda, 16, K::BM)) return cudaErrorInvalidValue;
   if (!make_map(L, &tb, B, N, Kd, ldb, 16, 16)) return cudaErrorInvalidValue;
   const int smem = K::SMEM;
-  cudaError_t e = cudaFuncSetAttribute(dgemm_dmma_kernel<K, false>,
+  cudaError_t e = cudaFuncSetAttribute(dgemm_dmma_kernel<K, 0>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int tiles_m = static_cast<int>((M + K::BM - 1) / K::BM);
   const int tiles_n = static_cast<int>((N + K::BN - 1) / K::BN);
   const int vec_ok = (ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0);
-  dgemm_dmma_kernel<K, false><<<tiles_m * tiles_n, K::THREADS, smem, L.stream>>>(
+  dgemm_dmma_kernel<K, 0><<<tiles_m * tiles_n, K::THREADS, smem, L.stream>>>(
       ta, tb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(Kd), tiles_m,
       tiles_n, vec_ok, DmmaStream{});
   L.count();
@@ -323,13 +415,36 @@ cudaError_t launch_dgemm_dmma_stream(const Launch& L, int64_t M, int64_t N, int6
   CUtensorMap ta, tb;
   if (!make_map(L, &ta, A, Kd, M, lda, 16, K::BM)) return cudaErrorInvalidValue;
   if (!make_map(L, &tb, B, N, Kd, ldb, 16, 16)) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(dgemm_dmma_kernel<K, true>,
+  cudaError_t e = cudaFuncSetAttribute(dgemm_dmma_kernel<K, 1>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
   if (e != cudaSuccess) return e;
   const int tiles_m = static_cast<int>((M + K::BM - 1) / K::BM);
   const int tiles_n = static_cast<int>((N + K::BN - 1) / K::BN);
   const int vec_ok = (ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0);
-  dgemm_dmma_kernel<K, true><<<grid, K::THREADS, K::SMEM, L.stream>>>(
+  dgemm_dmma_kernel<K, 1><<<grid, K::THREADS, K::SMEM, L.stream>>>(
+      ta, tb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(Kd), tiles_m,
+      tiles_n, vec_ok, st);
+  L.count();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dgemm_dmma_sk(const Launch& L, int64_t M, int64_t N, int64_t Kd,
+                                 const double* A, int64_t lda, const double* B, int64_t ldb,
+                                 double* C, int64_t ldc, double* partial, int* flags, int grid) {
+  using K = Big;
+  CUtensorMap ta, tb;
+  if (!make_map(L, &ta, A, Kd, M, lda, 16, K::BM)) return cudaErrorInvalidValue;
+  if (!make_map(L, &tb, B, N, Kd, ldb, 16, 16)) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(dgemm_dmma_kernel<K, 2>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
+  if (e != cudaSuccess) return e;
+  const int tiles_m = static_cast<int>((M + K::BM - 1) / K::BM);
+  const int tiles_n = static_cast<int>((N + K::BN - 1) / K::BN);
+  const int vec_ok = (ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0);
+  DmmaStream st;
+  st.partial = partial;
+  st.flags = flags;
+  dgemm_dmma_kernel<K, 2><<<grid, K::THREADS, K::SMEM, L.stream>>>(
       ta, tb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(Kd), tiles_m,
       tiles_n, vec_ok, st);
   L.count();
@@ -347,8 +462,9 @@ cudaError_t launch_dgemm_dmma(const Launch& L, int cfg, int64_t M, int64_t N, in
 }
 
 cudaError_t preload_dgemm_dmma() {
-  return preload_kernels(dgemm_dmma_kernel<Big, false>, dgemm_dmma_kernel<Mid, false>,
-                         dgemm_dmma_kernel<Small, false>, dgemm_dmma_kernel<Big, true>);
+  return preload_kernels(dgemm_dmma_kernel<Big, 0>, dgemm_dmma_kernel<Mid, 0>,
+                         dgemm_dmma_kernel<Small, 0>, dgemm_dmma_kernel<Big, 1>,
+                         dgemm_dmma_kernel<Big, 2>);
 }
 
 }  // namespace mmws_impl

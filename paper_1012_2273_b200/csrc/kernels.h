@@ -37,6 +37,10 @@ struct DmmaStream {
   int band_a = 1;                // tile rows per A band (ready_a granularity)
   int band_b = 1;                // tile columns per B band (ready_b granularity)
   int* done = nullptr;           // [tile row] finished tiles
+  // stream-K (launch_dgemm_dmma_sk): accumulator slots and their flags,
+  // grid + 1 of each (slot b = the tile cut between CTAs b-1 and b)
+  double* partial = nullptr;
+  int* flags = nullptr;
 };
 // Force-load kernels (cudaFuncGetAttributes).  Under CUDA_MODULE_LOADING=LAZY
 // the first launch of a kernel loads it with a context-wide synchronisation,
@@ -57,6 +61,15 @@ cudaError_t preload_sgemm();
 cudaError_t preload_sgemm_tma();
 cudaError_t preload_misc();
 
+// Stream-K, 128x128 tiles, one persistent CTA per SM (grid CTAs): every CTA
+// gets the same number of k-iterations; bitwise the one-shot result.  Needs
+// tiles * ceil(K/16) >= grid * ceil(K/16), i.e. tiles >= grid.  partial:
+// (grid + 1) * 128 * 128 doubles; flags: grid + 1 ints, zero before the first
+// launch (the kernel leaves them zero).  Launches sharing a workspace must
+// not overlap.
+cudaError_t launch_dgemm_dmma_sk(const Launch& L, int64_t M, int64_t N, int64_t K,
+                                 const double* A, int64_t lda, const double* B, int64_t ldb,
+                                 double* C, int64_t ldc, double* partial, int* flags, int grid);
 // 128x128 tiles only; grid = number of persistent CTAs.
 cudaError_t launch_dgemm_dmma_stream(const Launch& L, int64_t M, int64_t N, int64_t K,
                                      const double* A, int64_t lda, const double* B, int64_t ldb,

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -93,8 +94,25 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
     e = launch_dgemm_small(L, false, m, n, k, A, lda, B, ldb, C, ldc);
     return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm small");
   }
+  // Stream-K (128x128, one persistent CTA per SM, equal k-iterations per SM;
+  // bitwise the one-shot result) from one tile per SM up to 32 waves: it beat
+  // the one-shot launch at every size measured there (N=1600: 30.0 vs 27.1
+  // TFLOP/s, 2000: 32.6 vs 28.6, 2500: 33.3 vs 30.2, 4099: 32.7 vs 30.1,
+  // 8192: 36.3 vs 36.0) and lost 0.2 % at N=16384 (110 waves).  Not used
+  //   * inside graph capture (the captured launch would share the stream's
+  //     workspace with later eager launches),
+  //   * while the latency server holds SMs (the grid would not be resident),
+  //   * where the caller overlaps NCCL with the multiply (row-block path):
+  //     persistent CTAs would keep the communication kernels off the SMs.
+  const int64_t G = ctx->num_sms;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(L.stream, &cap);
+  const bool sk = mode != MMWS_GPU_MODE_DMMA_SMALL && tiles128 >= G && tiles128 < 32 * G &&
+                  cap == cudaStreamCaptureStatusNone && !ctx->server && ctx->allow_streamk &&
+                  !std::getenv("MMWS_GPU_NO_STREAMK");
   int cfg = DMMA_128x128;
-  if (mode == MMWS_GPU_MODE_DMMA_SMALL || (mode == MMWS_GPU_MODE_AUTO && tiles128 < 2 * static_cast<int64_t>(ctx->num_sms)))
+  if (!sk && (mode == MMWS_GPU_MODE_DMMA_SMALL ||
+              (mode == MMWS_GPU_MODE_AUTO && tiles128 < 2 * G)))
     cfg = DMMA_64x64;
   // TMA needs 16-byte aligned bases and row pitches: pack otherwise.
   const bool a_ok = lda % 2 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0;
@@ -118,6 +136,25 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
       B = w;
       ldb = ldb_p;
     }
+  }
+  if (sk) {
+    void* mem = nullptr;
+    for (const auto& sp : ctx->sk_spaces)
+      if (sp.stream == L.stream) mem = sp.mem;
+    const size_t slot_bytes = sizeof(double) * 128 * 128;
+    if (!mem) {
+      if ((e = cudaMalloc(&mem, (G + 1) * slot_bytes + sizeof(int) * (G + 1))) ||
+          (e = cudaMemsetAsync(static_cast<char*>(mem) + (G + 1) * slot_bytes, 0,
+                               sizeof(int) * (G + 1), L.stream))) {
+        if (mem) cudaFree(mem);
+        return cuda_fail(e, "dgemm stream-K workspace");
+      }
+      ctx->sk_spaces.push_back({L.stream, mem});
+    }
+    e = launch_dgemm_dmma_sk(L, m, n, k, A, lda, B, ldb, C, ldc, static_cast<double*>(mem),
+                             reinterpret_cast<int*>(static_cast<char*>(mem) + (G + 1) * slot_bytes),
+                             static_cast<int>(G));
+    return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm stream-K");
   }
   e = launch_dgemm_dmma(L, cfg, m, n, k, A, lda, B, ldb, C, ldc);
   return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm dmma");
@@ -288,6 +325,7 @@ int mmws_gpu_destroy(mmws_gpu_ctx* ctx) {
                   static_cast<void*>(ctx->sink)})
     if (p) cudaFree(p);
   for (void* p : ctx->deferred_free) cudaFree(p);
+  for (const auto& sp : ctx->sk_spaces) cudaFree(sp.mem);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->evk0) cudaEventDestroy(ctx->evk0);

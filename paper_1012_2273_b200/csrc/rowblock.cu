@@ -117,6 +117,13 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
     return MMWS_GPU_OK;
   }
   NCCL_REQUIRE();
+  // the multiplies below overlap NCCL transfers: no persistent (stream-K)
+  // launches, which would keep the communication kernels off the SMs
+  struct NoStreamK {
+    mmws_gpu_ctx* c;
+    ~NoStreamK() { c->allow_streamk = true; }
+  } no_sk{ctx};
+  ctx->allow_streamk = false;
   const Schedule sc = make_schedule(m, P);
   const int S = sc.S;
   const auto& off = sc.off;

@@ -148,6 +148,27 @@ def test_config_c3_n4099_integer_bit_exact(ctx, oracle, golden_big):
         assert sha(c) == golden_big["n4099_int8_sha256"], f"mode {mode}"
 
 
+@pytest.mark.parametrize("shape", [(2000, 2000, 2000), (1536, 999, 1664), (1280, 5000, 1920),
+                                   (1536, 16, 1664), (2100, 1001, 2303), (2304, 2304, 2304)])
+def test_stream_k_is_bitwise_the_one_shot_kernel(ctx, oracle, monkeypatch, shape):
+    # 148..1183 tiles of 128x128 with a partial last wave take the stream-K
+    # launch (accumulators of a cut tile continued by the next CTA); it must
+    # reproduce the one-shot kernels' bits exactly.
+    m, k, n = shape
+    A = ctx.fill(P.DIST_UNIFORM, 31, m, k)
+    B = ctx.fill(P.DIST_UNIFORM, 32, k, n)
+    for mode in (P.MODE_AUTO, P.MODE_DMMA):
+        got = host(ctx.dgemm(A, B, mode=mode))
+        monkeypatch.setenv("MMWS_GPU_NO_STREAMK", "1")
+        want = host(ctx.dgemm(A, B, mode=mode))
+        monkeypatch.delenv("MMWS_GPU_NO_STREAMK")
+        assert (bits(got) == bits(want)).all(), (shape, mode)
+    again = host(ctx.dgemm(A, B))                 # flags were left clean for the next launch
+    assert (bits(again) == bits(got)).all()
+    rows = [0, m // 2, m - 1]
+    assert normwise(got[rows], oracle.matmul_rows(rows, host(A), host(B))) <= FP64_TOL
+
+
 # ----------------------------------------------------------------------------- real inputs: tolerance
 def test_config_c1_n1000(ctx, oracle, golden_big):
     n = 1000
