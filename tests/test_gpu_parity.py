@@ -169,6 +169,44 @@ def test_stream_k_is_bitwise_the_one_shot_kernel(ctx, oracle, monkeypatch, shape
     assert normwise(got[rows], oracle.matmul_rows(rows, host(A), host(B))) <= FP64_TOL
 
 
+@pytest.mark.parametrize("seed", range(4))
+def test_random_shapes_and_strides(ctx, oracle, seed):
+    # Seeded fuzz over shapes (1..420), leading dimensions (dense or padded
+    # views, odd pitches that force packing / the cp.async fallbacks) and all
+    # modes: EXACT bitwise matmul_seq, tensor modes <= 1e-12 normwise and
+    # bit-exact on integer inputs, fp32 <= 1e-5.
+    T = torch()
+    rng = np.random.default_rng(1000 + seed)
+    for case in range(12):
+        m, k, n = (int(v) for v in rng.integers(1, 421, size=3))
+        pa, pb = (int(v) for v in rng.integers(0, 5, size=2))
+        dist = oracle.DIST_INT8 if case % 3 == 0 else oracle.DIST_UNIFORM
+        a = oracle.fill(dist, 7 * seed + case, m, k)
+        b = oracle.fill(dist, 7 * seed + case + 100, k, n)
+        A = T.zeros((m, k + pa), dtype=T.float64, device="cuda")[:, :k]
+        B = T.zeros((k, n + pb), dtype=T.float64, device="cuda")[:, :n]
+        A.copy_(T.from_numpy(a))
+        B.copy_(T.from_numpy(b))
+        want = oracle.matmul_seq(a, b)
+        for mode in FP64_MODES:
+            got = host(ctx.dgemm(A, B, mode=mode))
+            if mode == P.MODE_EXACT or dist == oracle.DIST_INT8:
+                assert oracle.first_difference(got, want) is None, (m, k, n, pa, pb, mode)
+            else:
+                assert normwise(got, want) <= FP64_TOL, (m, k, n, pa, pb, mode)
+        af, bf = a.astype(np.float32), b.astype(np.float32)
+        Af = T.zeros((m, k + pa), dtype=T.float32, device="cuda")[:, :k]
+        Bf = T.zeros((k, n + pb), dtype=T.float32, device="cuda")[:, :n]
+        Af.copy_(T.from_numpy(af))
+        Bf.copy_(T.from_numpy(bf))
+        gotf = host(ctx.sgemm(Af, Bf)).astype(np.float64)
+        wantf = oracle.matmul_rows(list(range(m)), af, bf)
+        if dist == oracle.DIST_INT8:   # |sums| < 2^24: exact in fp32 too
+            assert (gotf == wantf).all(), (m, k, n, pa, pb)
+        else:
+            assert normwise(gotf, wantf) <= FP32_TOL, (m, k, n, pa, pb)
+
+
 # ----------------------------------------------------------------------------- real inputs: tolerance
 def test_config_c1_n1000(ctx, oracle, golden_big):
     n = 1000
