@@ -137,11 +137,33 @@ struct ExactTma {
   static constexpr int MINB = TBM == 128 ? 1 : 2;
 };
 
-template <int TBM, int TBN>
+// SK = true: stream-K with in-order fix-up, exactly as dgemm_dmma.cu's MODE 2
+// (one persistent CTA per SM, equal k-iteration ranges walked top-down, a cut
+// tile's accumulators parked by the lower CTA and continued by the upper one)
+// -- each element keeps its single ascending-k DMUL+DADD chain, so the result
+// is still bitwise matmul_seq.
+MMWS_DEVICE uint64_t exact_global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+MMWS_DEVICE void exact_wait_flag(const int* f) {
+  const uint64_t t0 = exact_global_ns();
+  for (;;) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    if (v) return;
+    __nanosleep(200);
+    if (exact_global_ns() - t0 > 60ull * 1000000000ull) __trap();
+  }
+}
+
+template <int TBM, int TBN, bool SK = false>
 __global__ void __launch_bounds__(T_THREADS, ExactTma<TBM, TBN>::MINB)
     dgemm_exact_tma_kernel(const __grid_constant__ CUtensorMap tmA,
                            const __grid_constant__ CUtensorMap tmB, double* __restrict__ C,
-                           int64_t ldc, int M, int N, int K, int tiles_m, int tiles_n) {
+                           int64_t ldc, int M, int N, int K, int tiles_m, int tiles_n,
+                           double* partial = nullptr, int* flags = nullptr) {
   using X = ExactTma<TBM, TBN>;
   constexpr int T_A_BYTES = X::A_BYTES, T_STAGE = X::STAGE, TM = X::TM, TN = X::TN;
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -150,12 +172,13 @@ __global__ void __launch_bounds__(T_THREADS, ExactTma<TBM, TBN>::MINB)
   uint64_t* empty = full + T_STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int GROUP = 8;
-  const int tile = blockIdx.x;
-  const int per_group = GROUP * tiles_n;
-  const int first_m = (tile / per_group) * GROUP;
-  const int gm = min(tiles_m - first_m, GROUP);
-  const int tm = first_m + (tile % per_group) % gm;
-  const int tn = (tile % per_group) / gm;
+  auto raster = [&](int tile, int& tm, int& tn) {
+    const int per_group = GROUP * tiles_n;
+    const int first_m = (tile / per_group) * GROUP;
+    const int gm = min(tiles_m - first_m, GROUP);
+    tm = first_m + (tile % per_group) % gm;
+    tn = (tile % per_group) / gm;
+  };
   if (threadIdx.x == 0) {
     for (int s = 0; s < T_STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -165,19 +188,47 @@ __global__ void __launch_bounds__(T_THREADS, ExactTma<TBM, TBN>::MINB)
   }
   __syncthreads();
   const int KT = (K + BK - 1) / BK;
+  // work units (tile, k-iterations [k0, k1)): the CTA's tile, or (SK) its
+  // iteration range top-down
+  const long long w = static_cast<long long>(tiles_m) * tiles_n * KT;
+  const long long lo = SK ? w * blockIdx.x / gridDim.x : 0;
+  const long long hi0 = SK ? w * (blockIdx.x + 1) / gridDim.x : 1;
+  auto next_unit = [&](long long& pos, int& tile, int& k0, int& k1) -> bool {
+    if constexpr (SK) {
+      if (pos <= lo) return false;
+      tile = static_cast<int>((pos - 1) / KT);
+      const long long base = static_cast<long long>(tile) * KT;
+      k0 = static_cast<int>((lo > base ? lo : base) - base);
+      k1 = static_cast<int>(pos - base);
+      pos = base + k0;
+    } else {
+      if (pos == 0) return false;
+      pos = 0;
+      tile = blockIdx.x;
+      k0 = 0;
+      k1 = KT;
+    }
+    return true;
+  };
 
   if (warp >= T_CONSUMERS) {
     if constexpr (TBM == 128) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
     if (warp == T_CONSUMERS && lane == 0) {
       tma_prefetch_desc(&tmA);
       tma_prefetch_desc(&tmB);
-      for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % T_STAGES;
-        if (kt >= T_STAGES) mbar_wait(&empty[s], ((kt / T_STAGES) - 1) & 1);
-        uint8_t* sa = smem + s * T_STAGE;
-        mbar_arrive_expect_tx(&full[s], T_STAGE);
-        tma_load_2d(sa, &tmA, &full[s], kt * BK, tm * TBM);
-        tma_load_2d(sa + T_A_BYTES, &tmB, &full[s], tn * TBN, kt * BK);
+      long long pos = hi0;
+      int tile, k0, k1, kg = 0;  // kg: stage counter, continuous across units
+      while (next_unit(pos, tile, k0, k1)) {
+        int tm, tn;
+        raster(tile, tm, tn);
+        for (int kt = k0; kt < k1; ++kt, ++kg) {
+          const int s = kg % T_STAGES;
+          if (kg >= T_STAGES) mbar_wait(&empty[s], ((kg / T_STAGES) - 1) & 1);
+          uint8_t* sa = smem + s * T_STAGE;
+          mbar_arrive_expect_tx(&full[s], T_STAGE);
+          tma_load_2d(sa, &tmA, &full[s], kt * BK, tm * TBM);
+          tma_load_2d(sa + T_A_BYTES, &tmB, &full[s], tn * TBN, kt * BK);
+        }
       }
     }
     return;
@@ -185,55 +236,91 @@ __global__ void __launch_bounds__(T_THREADS, ExactTma<TBM, TBN>::MINB)
   if constexpr (TBM == 128) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
-  double acc[TM][TN];
+  constexpr int MATH_THREADS = T_CONSUMERS * 32;
+  long long pos = hi0;
+  int tile, k0, k1, kg = 0;
+  while (next_unit(pos, tile, k0, k1)) {
+    int tm, tn;
+    raster(tile, tm, tn);
+    double acc[TM][TN];
 #pragma unroll
-  for (int i = 0; i < TM; ++i)
+    for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
-
-  for (int kt = 0; kt < KT; ++kt) {
-    const int s = kt % T_STAGES;
-    mbar_wait(&full[s], (kt / T_STAGES) & 1);
-    if (kt > 0) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[(kt - 1) % T_STAGES]);
+      for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
+    if constexpr (SK) {
+      if (k0 > 0) {  // continue the lower CTA's chains for this tile
+        if (tid == 0) exact_wait_flag(flags + blockIdx.x);
+        asm volatile("bar.sync 1, %0;" ::"n"(MATH_THREADS) : "memory");
+        const double* src = partial + static_cast<size_t>(blockIdx.x) * TM * TN * MATH_THREADS;
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) acc[i][j] = __ldcg(src + (i * TN + j) * MATH_THREADS + tid);
+        if (tid == 0) flags[blockIdx.x] = 0;
+      }
     }
-    const double* as = reinterpret_cast<const double*>(smem + s * T_STAGE);  // [TBM][BK]
-    const double* bs = as + TBM * BK;                                         // [BK][TBN]
+
+    for (int kt = k0; kt < k1; ++kt, ++kg) {
+      const int s = kg % T_STAGES;
+      mbar_wait(&full[s], (kg / T_STAGES) & 1);
+      if (kg > 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[(kg - 1) % T_STAGES]);
+      }
+      const double* as = reinterpret_cast<const double*>(smem + s * T_STAGE);  // [TBM][BK]
+      const double* bs = as + TBM * BK;                                         // [BK][TBN]
 #pragma unroll
-    for (int k = 0; k < BK; k += 2) {
-      double2 a2[TM];
+      for (int k = 0; k < BK; k += 2) {
+        double2 a2[TM];
 #pragma unroll
-      for (int i = 0; i < TM; ++i)
-        a2[i] = *reinterpret_cast<const double2*>(as + (ty * 2 + 32 * (i >> 1) + (i & 1)) * BK + k);
+        for (int i = 0; i < TM; ++i)
+          a2[i] =
+              *reinterpret_cast<const double2*>(as + (ty * 2 + 32 * (i >> 1) + (i & 1)) * BK + k);
 #pragma unroll
-      for (int kk = 0; kk < 2; ++kk) {
-        double b[TN];
+        for (int kk = 0; kk < 2; ++kk) {
+          double b[TN];
 #pragma unroll
-        for (int v = 0; v < TN / 2; ++v) {
-          const double2 bv =
-              *reinterpret_cast<const double2*>(bs + (k + kk) * TBN + tx * 2 + 32 * v);
-          b[2 * v] = bv.x;
-          b[2 * v + 1] = bv.y;
-        }
+          for (int v = 0; v < TN / 2; ++v) {
+            const double2 bv =
+                *reinterpret_cast<const double2*>(bs + (k + kk) * TBN + tx * 2 + 32 * v);
+            b[2 * v] = bv.x;
+            b[2 * v + 1] = bv.y;
+          }
 #pragma unroll
-        for (int i = 0; i < TM; ++i) {
-          const double a = kk ? a2[i].y : a2[i].x;
+          for (int i = 0; i < TM; ++i) {
+            const double a = kk ? a2[i].y : a2[i].x;
 #pragma unroll
-          for (int j = 0; j < TN; ++j) acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(a, b[j]));
+            for (int j = 0; j < TN; ++j) acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(a, b[j]));
+          }
         }
       }
     }
-  }
+    if constexpr (SK) {
+      if (k1 < KT) {  // first part of a tile the upper CTA finishes: park it
+        double* dst = partial + static_cast<size_t>(blockIdx.x + 1) * TM * TN * MATH_THREADS;
 #pragma unroll
-  for (int i = 0; i < TM; ++i) {
-    const int r = tm * TBM + ty * 2 + 32 * (i >> 1) + (i & 1);
-    if (r >= M) continue;
-    double* crow = C + static_cast<int64_t>(r) * ldc;
+        for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < TN; ++j) {
-      const int c = tn * TBN + tx * 2 + 32 * (j >> 1) + (j & 1);
-      if (c < N) crow[c] = acc[i][j];
+          for (int j = 0; j < TN; ++j) __stcg(dst + (i * TN + j) * MATH_THREADS + tid, acc[i][j]);
+        asm volatile("bar.sync 1, %0;" ::"n"(MATH_THREADS) : "memory");
+        if (tid == 0) {
+          __threadfence();
+          asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flags + blockIdx.x + 1), "r"(1)
+                       : "memory");
+        }
+        continue;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const int r = tm * TBM + ty * 2 + 32 * (i >> 1) + (i & 1);
+      if (r >= M) continue;
+      double* crow = C + static_cast<int64_t>(r) * ldc;
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int c = tn * TBN + tx * 2 + 32 * (j >> 1) + (j & 1);
+        if (c < N) crow[c] = acc[i][j];
+      }
     }
   }
 }
@@ -251,34 +338,46 @@ bool make_map_f64(const Launch& L, CUtensorMap* map, const double* base, int64_t
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int TBM, int TBN>
+template <int TBM, int TBN, bool SK = false>
 cudaError_t run_exact_tma(const Launch& L, int64_t M, int64_t N, int64_t K, const double* A,
-                          int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc) {
+                          int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                          double* partial = nullptr, int* flags = nullptr, int grid = 0) {
   using X = ExactTma<TBM, TBN>;
   CUtensorMap ta, tb;
   if (!make_map_f64(L, &ta, A, K, M, lda, BK, TBM) || !make_map_f64(L, &tb, B, N, K, ldb, TBN, BK))
     return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(dgemm_exact_tma_kernel<TBM, TBN>,
+  cudaError_t e = cudaFuncSetAttribute(dgemm_exact_tma_kernel<TBM, TBN, SK>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, X::SMEM);
   if (e != cudaSuccess) return e;
   const int tiles_m = static_cast<int>((M + TBM - 1) / TBM);
   const int tiles_n = static_cast<int>((N + TBN - 1) / TBN);
-  dgemm_exact_tma_kernel<TBM, TBN><<<tiles_m * tiles_n, T_THREADS, X::SMEM, L.stream>>>(
-      ta, tb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), tiles_m,
-      tiles_n);
+  dgemm_exact_tma_kernel<TBM, TBN, SK><<<SK ? grid : tiles_m * tiles_n, T_THREADS, X::SMEM,
+                                         L.stream>>>(ta, tb, C, ldc, static_cast<int>(M),
+                                                     static_cast<int>(N), static_cast<int>(K),
+                                                     tiles_m, tiles_n, partial, flags);
   L.count();
   return cudaGetLastError();
 }
 
 }  // namespace
 
+bool exact_tma_ok(int64_t lda, int64_t ldb, const double* A, const double* B) {
+  return lda % 2 == 0 && ldb % 2 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0 &&
+         reinterpret_cast<uintptr_t>(B) % 16 == 0;
+}
+
+cudaError_t launch_dgemm_exact_sk(const Launch& L, int64_t M, int64_t N, int64_t K,
+                                  const double* A, int64_t lda, const double* B, int64_t ldb,
+                                  double* C, int64_t ldc, double* partial, int* flags, int grid) {
+  return run_exact_tma<128, 128, true>(L, M, N, K, A, lda, B, ldb, C, ldc, partial, flags, grid);
+}
+
 cudaError_t launch_dgemm_exact(const Launch& L, int64_t M, int64_t N, int64_t K, const double* A,
                                int64_t lda, const double* B, int64_t ldb, double* C,
                                int64_t ldc) {
   const int tiles_m = static_cast<int>((M + BM - 1) / BM);
   const int tiles_n = static_cast<int>((N + BN - 1) / BN);
-  if (lda % 2 == 0 && ldb % 2 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0 &&
-      reinterpret_cast<uintptr_t>(B) % 16 == 0) {  // TMA can describe both operands
+  if (exact_tma_ok(lda, ldb, A, B)) {  // TMA can describe both operands
     // 64x64 tiles while 128x128 ones would not give every SM two CTAs
     return tiles_m * tiles_n < 2 * L.num_sms
                ? run_exact_tma<64, 64>(L, M, N, K, A, lda, B, ldb, C, ldc)
@@ -300,6 +399,7 @@ cudaError_t launch_dgemm_exact(const Launch& L, int64_t M, int64_t N, int64_t K,
 
 cudaError_t preload_dgemm_exact() {
   return preload_kernels(dgemm_exact_tma_kernel<64, 64>, dgemm_exact_tma_kernel<128, 128>,
+                         dgemm_exact_tma_kernel<128, 128, true>,
                          dgemm_exact_kernel<true, true>, dgemm_exact_kernel<true, false>,
                          dgemm_exact_kernel<false, true>, dgemm_exact_kernel<false, false>);
 }

@@ -69,6 +69,32 @@ int check_dims(int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb, int64_
 }
 }  // namespace
 
+// The stream-K workspace of a launch stream: (num_sms + 1) accumulator slots
+// of 128 x 128 doubles and their flags, allocated (flags zeroed on the
+// stream) on first use and kept for the context's lifetime -- fixed size, so
+// a pointer baked into a launch never goes stale.
+int sk_workspace(mmws_gpu_ctx* ctx, cudaStream_t stream, double** partial, int** flags) {
+  const size_t slots = static_cast<size_t>(ctx->num_sms) + 1;
+  const size_t slot_bytes = sizeof(double) * 128 * 128;
+  void* mem = nullptr;
+  for (const auto& sp : ctx->sk_spaces)
+    if (sp.stream == stream) mem = sp.mem;
+  if (!mem) {
+    cudaError_t e;
+    if ((e = cudaMalloc(&mem, slots * slot_bytes + sizeof(int) * slots)) != cudaSuccess)
+      return cuda_fail(e, "stream-K workspace");
+    if ((e = cudaMemsetAsync(static_cast<char*>(mem) + slots * slot_bytes, 0, sizeof(int) * slots,
+                             stream)) != cudaSuccess) {
+      cudaFree(mem);
+      return cuda_fail(e, "stream-K workspace");
+    }
+    ctx->sk_spaces.push_back({stream, mem});
+  }
+  *partial = static_cast<double*>(mem);
+  *flags = reinterpret_cast<int*>(static_cast<char*>(mem) + slots * slot_bytes);
+  return MMWS_GPU_OK;
+}
+
 int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
                    int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int mode,
                    cudaStream_t stream) {
@@ -76,24 +102,6 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
   const Launch L = ctx->launch(stream);
   cudaError_t e;
   const int64_t tiles128 = ((m + 127) / 128) * ((n + 127) / 128);
-  if (mode == MMWS_GPU_MODE_EXACT) {
-    // exact order: the 32x32 latency kernel for tiny problems, else the
-    // 64x64 / 128x128 TMA kernels (every variant gives matmul_seq's bits)
-    e = n <= 256 && k <= 256
-            ? launch_dgemm_small(L, true, m, n, k, A, lda, B, ldb, C, ldc)
-            : launch_dgemm_exact(L, m, n, k, A, lda, B, ldb, C, ldc);
-    return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm exact");
-  }
-  if (mode != MMWS_GPU_MODE_AUTO && mode != MMWS_GPU_MODE_DMMA &&
-      mode != MMWS_GPU_MODE_DMMA_SMALL)
-    return fail(MMWS_GPU_ERR_DOMAIN, "dgemm: unknown mode " + std::to_string(mode));
-  if (mode == MMWS_GPU_MODE_AUTO && n <= 256 && k <= 256) {
-    // latency path; chosen from (n, k) only, so every row slice of a problem
-    // (row-block ranks, host-pipeline panels) takes the same kernel as the
-    // whole problem and gets the same bits
-    e = launch_dgemm_small(L, false, m, n, k, A, lda, B, ldb, C, ldc);
-    return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm small");
-  }
   // Stream-K (128x128, one persistent CTA per SM, equal k-iterations per SM;
   // bitwise the one-shot result) from one tile per SM up to 32 waves: it beat
   // the one-shot launch at every size measured there (N=1600: 30.0 vs 27.1
@@ -110,52 +118,73 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
   const bool sk = mode != MMWS_GPU_MODE_DMMA_SMALL && tiles128 >= G && tiles128 < 32 * G &&
                   cap == cudaStreamCaptureStatusNone && !ctx->server && ctx->allow_streamk &&
                   !std::getenv("MMWS_GPU_NO_STREAMK");
-  int cfg = DMMA_128x128;
-  if (!sk && (mode == MMWS_GPU_MODE_DMMA_SMALL ||
-              (mode == MMWS_GPU_MODE_AUTO && tiles128 < 2 * G)))
-    cfg = DMMA_64x64;
-  // TMA needs 16-byte aligned bases and row pitches: pack otherwise.
-  const bool a_ok = lda % 2 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0;
-  const bool b_ok = ldb % 2 == 0 && reinterpret_cast<uintptr_t>(B) % 16 == 0;
-  if (!a_ok || !b_ok) {
+  // TMA needs 16-byte aligned bases and even row pitches: pack A and/or B into
+  // the workspace otherwise (one HBM-bound pass, zero padding never read).
+  auto pack_operands = [&]() -> int {
+    const bool a_ok = lda % 2 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0;
+    const bool b_ok = ldb % 2 == 0 && reinterpret_cast<uintptr_t>(B) % 16 == 0;
+    if (a_ok && b_ok) return MMWS_GPU_OK;
     const int64_t lda_p = round_up(k, 8), ldb_p = round_up(n, 8);
     const size_t bytes = sizeof(double) * ((a_ok ? 0 : m * lda_p) + (b_ok ? 0 : k * ldb_p));
-    e = ensure(ctx, &ctx->ws, &ctx->ws_bytes, bytes);
-    if (e != cudaSuccess) return cuda_fail(e, "dgemm pack workspace");
+    cudaError_t pe = ensure(ctx, &ctx->ws, &ctx->ws_bytes, bytes);
+    if (pe != cudaSuccess) return cuda_fail(pe, "dgemm pack workspace");
     double* w = static_cast<double*>(ctx->ws);
     if (!a_ok) {
-      e = launch_pack_f64(L, A, m, k, lda, w, m, lda_p, lda_p);
-      if (e != cudaSuccess) return cuda_fail(e, "dgemm pack A");
+      if ((pe = launch_pack_f64(L, A, m, k, lda, w, m, lda_p, lda_p)) != cudaSuccess)
+        return cuda_fail(pe, "dgemm pack A");
       A = w;
       lda = lda_p;
       w += m * lda_p;
     }
     if (!b_ok) {
-      e = launch_pack_f64(L, B, k, n, ldb, w, k, ldb_p, ldb_p);
-      if (e != cudaSuccess) return cuda_fail(e, "dgemm pack B");
+      if ((pe = launch_pack_f64(L, B, k, n, ldb, w, k, ldb_p, ldb_p)) != cudaSuccess)
+        return cuda_fail(pe, "dgemm pack B");
       B = w;
       ldb = ldb_p;
     }
-  }
-  if (sk) {
-    void* mem = nullptr;
-    for (const auto& sp : ctx->sk_spaces)
-      if (sp.stream == L.stream) mem = sp.mem;
-    const size_t slot_bytes = sizeof(double) * 128 * 128;
-    if (!mem) {
-      if ((e = cudaMalloc(&mem, (G + 1) * slot_bytes + sizeof(int) * (G + 1))) ||
-          (e = cudaMemsetAsync(static_cast<char*>(mem) + (G + 1) * slot_bytes, 0,
-                               sizeof(int) * (G + 1), L.stream))) {
-        if (mem) cudaFree(mem);
-        return cuda_fail(e, "dgemm stream-K workspace");
-      }
-      ctx->sk_spaces.push_back({L.stream, mem});
+    return MMWS_GPU_OK;
+  };
+  double* sk_partial = nullptr;
+  int* sk_flags = nullptr;
+  if (mode == MMWS_GPU_MODE_EXACT) {
+    // exact order: the 32x32 latency kernel for tiny problems, the stream-K
+    // form of the 128x128 TMA kernel (operands packed if needed) from one
+    // tile per SM, else the 64x64 / 128x128 TMA kernels or the cp.async
+    // kernel for layouts TMA cannot read -- every variant gives matmul_seq's
+    // bits
+    if (n <= 256 && k <= 256) {
+      e = launch_dgemm_small(L, true, m, n, k, A, lda, B, ldb, C, ldc);
+    } else if (sk) {
+      if (int rc = sk_workspace(ctx, L.stream, &sk_partial, &sk_flags)) return rc;
+      if (int rc = pack_operands()) return rc;
+      e = launch_dgemm_exact_sk(L, m, n, k, A, lda, B, ldb, C, ldc, sk_partial, sk_flags,
+                                static_cast<int>(G));
+    } else {
+      e = launch_dgemm_exact(L, m, n, k, A, lda, B, ldb, C, ldc);
     }
-    e = launch_dgemm_dmma_sk(L, m, n, k, A, lda, B, ldb, C, ldc, static_cast<double*>(mem),
-                             reinterpret_cast<int*>(static_cast<char*>(mem) + (G + 1) * slot_bytes),
+    return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm exact");
+  }
+  if (mode != MMWS_GPU_MODE_AUTO && mode != MMWS_GPU_MODE_DMMA &&
+      mode != MMWS_GPU_MODE_DMMA_SMALL)
+    return fail(MMWS_GPU_ERR_DOMAIN, "dgemm: unknown mode " + std::to_string(mode));
+  if (mode == MMWS_GPU_MODE_AUTO && n <= 256 && k <= 256) {
+    // latency path; chosen from (n, k) only, so every row slice of a problem
+    // (row-block ranks, host-pipeline panels) takes the same kernel as the
+    // whole problem and gets the same bits
+    e = launch_dgemm_small(L, false, m, n, k, A, lda, B, ldb, C, ldc);
+    return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm small");
+  }
+  if (int rc = pack_operands()) return rc;
+  if (sk) {
+    if (int rc = sk_workspace(ctx, L.stream, &sk_partial, &sk_flags)) return rc;
+    e = launch_dgemm_dmma_sk(L, m, n, k, A, lda, B, ldb, C, ldc, sk_partial, sk_flags,
                              static_cast<int>(G));
     return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm stream-K");
   }
+  const int cfg = mode == MMWS_GPU_MODE_DMMA_SMALL ||
+                          (mode == MMWS_GPU_MODE_AUTO && tiles128 < 2 * G)
+                      ? DMMA_64x64
+                      : DMMA_128x128;
   e = launch_dgemm_dmma(L, cfg, m, n, k, A, lda, B, ldb, C, ldc);
   return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm dmma");
 }

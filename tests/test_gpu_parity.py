@@ -166,7 +166,15 @@ def test_stream_k_is_bitwise_the_one_shot_kernel(ctx, oracle, monkeypatch, shape
     again = host(ctx.dgemm(A, B))                 # flags were left clean for the next launch
     assert (bits(again) == bits(got)).all()
     rows = [0, m // 2, m - 1]
-    assert normwise(got[rows], oracle.matmul_rows(rows, host(A), host(B))) <= FP64_TOL
+    want_rows = oracle.matmul_rows(rows, host(A), host(B))
+    assert normwise(got[rows], want_rows) <= FP64_TOL
+    # exact order: stream-K form of the exact kernel, bitwise matmul_seq
+    ex = host(ctx.dgemm(A, B, mode=P.MODE_EXACT))
+    assert (bits(ex[rows]) == bits(want_rows)).all()
+    monkeypatch.setenv("MMWS_GPU_NO_STREAMK", "1")
+    ex1 = host(ctx.dgemm(A, B, mode=P.MODE_EXACT))
+    monkeypatch.delenv("MMWS_GPU_NO_STREAMK")
+    assert (bits(ex) == bits(ex1)).all()
 
 
 @pytest.mark.parametrize("seed", range(4))
