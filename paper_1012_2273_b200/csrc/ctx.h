@@ -26,6 +26,8 @@ struct mmws_gpu_ctx {
   CUresult (*write_value)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
   CUresult (*wait_value)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
   void* server = nullptr;  // latency server state (server.cu), null when not running
+  void* stager = nullptr;  // pinned chunk ring + host copy threads (staging.cu), lazy
+  uint64_t stage_next = 0;  // next pinned chunk (round robin)
   std::vector<void*> deferred_free;  // buffers outgrown while the server ran
   // CUDA IPC (fused C gather of the row-block path)
   CUresult (*mem_range)(CUdeviceptr*, size_t*, CUdeviceptr) = nullptr;
@@ -95,6 +97,38 @@ cudaError_t ensure(mmws_gpu_ctx* ctx, void** buf, size_t* have, size_t bytes);
 int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
                    int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int mode,
                    cudaStream_t stream);
+// Host -> device copy of `rows` rows of `width` bytes (row pitches in bytes),
+// queued on s.  Pageable host memory goes through pinned chunks filled by
+// host threads (staging.cu); pinned memory is copied directly.  Returns once
+// everything is queued (the host buffer is no longer needed).
+cudaError_t copy_h2d(mmws_gpu_ctx* ctx, void* dst, size_t dpitch, const void* src, size_t spitch,
+                     size_t width, size_t rows, cudaStream_t s);
+// Device -> host copies queued on one stream, pageable destinations through
+// the pinned chunk ring with up to 3 chunks in flight across add() calls
+// (a chunk is copied out while the next ones transfer).  Pinned destinations
+// are plain cudaMemcpy2DAsync.  finish() (or the destructor) returns once
+// every staged destination is filled.
+class D2hPump {
+ public:
+  D2hPump(mmws_gpu_ctx* ctx, cudaStream_t s);
+  ~D2hPump();
+  cudaError_t add(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                  size_t rows);
+  cudaError_t finish();
+
+ private:
+  struct Pending {
+    char* dst;
+    size_t dpitch, width, rows;
+    int slot;
+  };
+  cudaError_t drain_one();
+  mmws_gpu_ctx* ctx_;
+  cudaStream_t s_;
+  std::vector<Pending> pending_;
+};
+bool is_pageable(const void* p);
+void staging_destroy(mmws_gpu_ctx* ctx);
 // Stop the latency server (if running) and free its resources.
 void server_destroy(mmws_gpu_ctx* ctx);
 // Would the running latency server take this host-buffer multiply?

@@ -127,33 +127,16 @@ int host_multiply_streamed(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, c
   cudaEventRecord(ev_reset, comp);
   cudaStreamWaitEvent(in, ev_reset, 0);
   cudaStreamWaitEvent(out, ev_reset, 0);
-  // ---- copy-in, each band followed by its arrival flag
-  for (const auto& [which, i] : copies) {
-    if (which == 'A') {
-      const int64_t r0 = i * BAND_A * TILE, rows = std::min<int64_t>(BAND_A * TILE, m - r0);
-      if ((e = cudaMemcpyAsync(dA + r0 * k, A + r0 * k, sizeof(double) * rows * k,
-                               cudaMemcpyHostToDevice, in)))
-        return cuda_fail(e, "matmul_host: H2D A");
-      if (ctx->write_value(in, dptr(ready_a + i), 1, 0) != CUDA_SUCCESS)
-        return fail(MMWS_GPU_ERR_CUDA, "matmul_host: cuStreamWriteValue32 failed");
-    } else {
-      const int64_t c0 = i * BAND_B * TILE, w = std::min<int64_t>(BAND_B * TILE, n - c0);
-      if ((e = cudaMemcpy2DAsync(dB + c0, sizeof(double) * n, B + c0, sizeof(double) * n,
-                                 sizeof(double) * w, k, cudaMemcpyHostToDevice, in)))
-        return cuda_fail(e, "matmul_host: H2D B");
-      if (ctx->write_value(in, dptr(ready_b + i), 1, 0) != CUDA_SUCCESS)
-        return fail(MMWS_GPU_ERR_CUDA, "matmul_host: cuStreamWriteValue32 failed");
-    }
-  }
   // optional timeline (MMWS_GPU_PIPELINE_TRACE=1): H2D end, kernel start/end
   cudaEvent_t tr[3] = {nullptr, nullptr, nullptr};
   const bool trace = std::getenv("MMWS_GPU_PIPELINE_TRACE") != nullptr;
   if (trace) {
     for (auto& ev : tr) cudaEventCreate(&ev);
-    cudaEventRecord(tr[0], in);
     cudaEventRecord(tr[1], comp);
   }
-  // ---- one persistent multiply
+  // ---- one persistent multiply, launched first: it waits on the arrival
+  // flags, so the copy-in below may take as long as it needs (pageable host
+  // buffers are pumped through pinned chunks by the CPU, staging.cu)
   DmmaStream st;
   st.order = order;
   st.count = static_cast<int>(T);
@@ -166,7 +149,27 @@ int host_multiply_streamed(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, c
   if ((e = launch_dgemm_dmma_stream(ctx->launch(comp), m, n, k, dA, k, dB, n, dC, n, st, grid)))
     return cuda_fail(e, "matmul_host: streamed dgemm");
   if (trace) cudaEventRecord(tr[2], comp);
+  // ---- copy-in, each band followed by its arrival flag
+  for (const auto& [which, i] : copies) {
+    if (which == 'A') {
+      const int64_t r0 = i * BAND_A * TILE, rows = std::min<int64_t>(BAND_A * TILE, m - r0);
+      if ((e = copy_h2d(ctx, dA + r0 * k, sizeof(double) * k, A + r0 * k, sizeof(double) * k,
+                        sizeof(double) * k, rows, in)))
+        return cuda_fail(e, "matmul_host: H2D A");
+      if (ctx->write_value(in, dptr(ready_a + i), 1, 0) != CUDA_SUCCESS)
+        return fail(MMWS_GPU_ERR_CUDA, "matmul_host: cuStreamWriteValue32 failed");
+    } else {
+      const int64_t c0 = i * BAND_B * TILE, w = std::min<int64_t>(BAND_B * TILE, n - c0);
+      if ((e = copy_h2d(ctx, dB + c0, sizeof(double) * n, B + c0, sizeof(double) * n,
+                        sizeof(double) * w, k, in)))
+        return cuda_fail(e, "matmul_host: H2D B");
+      if (ctx->write_value(in, dptr(ready_b + i), 1, 0) != CUDA_SUCCESS)
+        return fail(MMWS_GPU_ERR_CUDA, "matmul_host: cuStreamWriteValue32 failed");
+    }
+  }
+  if (trace) cudaEventRecord(tr[0], in);
   // ---- copy-out: each 256-row band once all its tiles are counted
+  D2hPump pump(ctx, out);
   for (int64_t t0 = 0; t0 < tiles_m; t0 += BAND_C) {
     const int64_t t1 = std::min<int64_t>(tiles_m, t0 + BAND_C);
     for (int64_t tm = t0; tm < t1; ++tm)
@@ -174,10 +177,11 @@ int host_multiply_streamed(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, c
                           CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
         return fail(MMWS_GPU_ERR_CUDA, "matmul_host: cuStreamWaitValue32 failed");
     const int64_t r0 = t0 * TILE, rows = std::min<int64_t>(m, t1 * TILE) - r0;
-    if ((e = cudaMemcpyAsync(C + r0 * n, dC + r0 * n, sizeof(double) * rows * n,
-                             cudaMemcpyDeviceToHost, out)))
+    if ((e = pump.add(C + r0 * n, sizeof(double) * n, dC + r0 * n, sizeof(double) * n,
+                      sizeof(double) * n, rows)))
       return cuda_fail(e, "matmul_host: D2H");
   }
+  if ((e = pump.finish())) return cuda_fail(e, "matmul_host: D2H");
   cudaEventRecord(ctx->ev1, out);
   if ((e = cudaStreamSynchronize(out)) != cudaSuccess ||
       (e = cudaStreamSynchronize(comp)) != cudaSuccess ||
@@ -243,47 +247,47 @@ int host_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A
   cudaEvent_t* evB = evC + panels;
 
   cudaEventRecord(ctx->ev0, in);
-  // ---- copy-in
+  // Copy-in and compute are queued in lockstep -- a multiply right after the
+  // copy it needs -- so a pageable copy that the CPU pumps through pinned
+  // chunks (staging.cu) already overlaps the multiplies queued before it.
   auto rows_of = [&](int64_t i) { return std::min(R, m - i * R); };
-  if ((e = cudaMemcpyAsync(dA, A, sizeof(T) * rows_of(0) * k, cudaMemcpyHostToDevice, in)))
+  // panel 0 of A, then B block by block, each block's panel-0 multiply next
+  if ((e = copy_h2d(ctx, dA, sizeof(T) * k, A, sizeof(T) * k, sizeof(T) * k, rows_of(0), in)))
     return cuda_fail(e, "matmul_host: H2D A");
   cudaEventRecord(evA[0], in);
-  for (int64_t j = 0; j < blocks; ++j) {
-    const int64_t w = std::min(W, n - j * W);
-    if ((e = cudaMemcpy2DAsync(dB + j * W, sizeof(T) * n, B + j * W, sizeof(T) * n, sizeof(T) * w,
-                               k, cudaMemcpyHostToDevice, in)))
-      return cuda_fail(e, "matmul_host: H2D B");
-    cudaEventRecord(evB[j], in);
-  }
-  for (int64_t i = 1; i < panels; ++i) {
-    if ((e = cudaMemcpyAsync(dA + i * R * k, A + i * R * k, sizeof(T) * rows_of(i) * k,
-                             cudaMemcpyHostToDevice, in)))
-      return cuda_fail(e, "matmul_host: H2D A");
-    cudaEventRecord(evA[i], in);
-  }
-  // ---- compute
   cudaStreamWaitEvent(comp, evA[0], 0);
   for (int64_t j = 0; j < blocks; ++j) {
-    cudaStreamWaitEvent(comp, evB[j], 0);
     const int64_t w = std::min(W, n - j * W);
+    if ((e = copy_h2d(ctx, dB + j * W, sizeof(T) * n, B + j * W, sizeof(T) * n, sizeof(T) * w, k,
+                      in)))
+      return cuda_fail(e, "matmul_host: H2D B");
+    cudaEventRecord(evB[j], in);
+    cudaStreamWaitEvent(comp, evB[j], 0);
     if (int rc = gemm<T>(ctx, rows_of(0), w, k, dA, k, dB + j * W, n, dC + j * W, n, mode, comp))
       return rc;
   }
   cudaEventRecord(evC[0], comp);
+  // the other A panels, each followed by its full-width multiply
   for (int64_t i = 1; i < panels; ++i) {
+    if ((e = copy_h2d(ctx, dA + i * R * k, sizeof(T) * k, A + i * R * k, sizeof(T) * k,
+                      sizeof(T) * k, rows_of(i), in)))
+      return cuda_fail(e, "matmul_host: H2D A");
+    cudaEventRecord(evA[i], in);
     cudaStreamWaitEvent(comp, evA[i], 0);
     if (int rc = gemm<T>(ctx, rows_of(i), n, k, dA + i * R * k, k, dB, n, dC + i * R * n, n, mode,
                          comp))
       return rc;
     cudaEventRecord(evC[i], comp);
   }
-  // ---- copy-out
+  // ---- copy-out, panel by panel as the multiplies finish
+  D2hPump pump(ctx, out);
   for (int64_t i = 0; i < panels; ++i) {
     cudaStreamWaitEvent(out, evC[i], 0);
-    if ((e = cudaMemcpyAsync(C + i * R * n, dC + i * R * n, sizeof(T) * rows_of(i) * n,
-                             cudaMemcpyDeviceToHost, out)))
+    if ((e = pump.add(C + i * R * n, sizeof(T) * n, dC + i * R * n, sizeof(T) * n, sizeof(T) * n,
+                      rows_of(i))))
       return cuda_fail(e, "matmul_host: D2H");
   }
+  if ((e = pump.finish())) return cuda_fail(e, "matmul_host: D2H");
   cudaEventRecord(ctx->ev1, out);
   if ((e = cudaStreamSynchronize(out)) != cudaSuccess ||
       (e = cudaStreamSynchronize(comp)) != cudaSuccess ||

@@ -355,6 +355,7 @@ int mmws_gpu_destroy(mmws_gpu_ctx* ctx) {
     if (p) cudaFree(p);
   for (void* p : ctx->deferred_free) cudaFree(p);
   for (const auto& sp : ctx->sk_spaces) cudaFree(sp.mem);
+  staging_destroy(ctx);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->evk0) cudaEventDestroy(ctx->evk0);

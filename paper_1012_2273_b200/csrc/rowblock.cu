@@ -301,14 +301,18 @@ int master_run_host(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T*
     return cuda_fail(e, "master_run: device buffers");
   cudaStream_t s = ctx->stream;
   cudaEventRecord(ctx->ev0, s);
-  if ((e = cudaMemcpyAsync(ctx->dA, A, a_b, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
-      (e = cudaMemcpyAsync(ctx->dB, B, b_b, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+  if ((e = copy_h2d(ctx, ctx->dA, sizeof(T) * k, A, sizeof(T) * k, sizeof(T) * k, m, s)) !=
+          cudaSuccess ||
+      (e = copy_h2d(ctx, ctx->dB, sizeof(T) * n, B, sizeof(T) * n, sizeof(T) * n, k, s)) !=
+          cudaSuccess)
     return cuda_fail(e, "master_run: H2D");
   if (int rc = rowblock_enqueue(ctx, m, n, k, static_cast<const T*>(ctx->dA),
                                 static_cast<const T*>(ctx->dB), static_cast<T*>(ctx->dC), mode,
                                 false))
     return rc;
-  if ((e = cudaMemcpyAsync(C, ctx->dC, c_b, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+  D2hPump pump(ctx, s);
+  if ((e = pump.add(C, sizeof(T) * n, ctx->dC, sizeof(T) * n, sizeof(T) * n, m)) != cudaSuccess ||
+      (e = pump.finish()) != cudaSuccess)
     return cuda_fail(e, "master_run: D2H");
   cudaEventRecord(ctx->ev1, s);
   return finish(ctx, true, elapsed_s);

@@ -511,6 +511,28 @@ def test_host_pipeline_bitwise_equals_device(ctx, oracle, shape):
     assert (cf == host(ctx.sgemm(dev(af), dev(bf)))).all()
 
 
+def test_pageable_host_buffers_bigger_than_the_staging_ring(ctx, oracle):
+    # pageable numpy buffers go through the pinned chunk ring (4 x 32 MB):
+    # 128 MB operands wrap it several times; fp64 streamed path, fp32 panel
+    # path, exact panel path -- all bitwise the device-pointer results
+    n = 4096
+    A = ctx.fill(P.DIST_UNIFORM, 41, n, n)
+    B = ctx.fill(P.DIST_UNIFORM, 42, n, n)
+    a, b = host(A), host(B)
+    for mode in (P.MODE_AUTO, P.MODE_EXACT):
+        c, el = ctx.matmul_host(a, b, mode=mode)
+        assert el > 0 and (bits(c) == bits(host(ctx.dgemm(A, B, mode=mode)))).all(), mode
+    af, bf = a.astype(np.float32), b.astype(np.float32)
+    cf, _ = ctx.matmul_host(af, bf)
+    assert (cf == host(ctx.sgemm(dev(af), dev(bf)))).all()
+    # ragged rows / a view with a row pitch (np.ascontiguousarray copies it)
+    a2 = np.ascontiguousarray(a[:4000, :3001])
+    b2 = np.ascontiguousarray(b[:3001, :4093])
+    c2, _ = ctx.matmul_host(a2, b2, mode=P.MODE_EXACT)
+    rows = [0, 1999, 3999]
+    assert oracle.first_difference(c2[rows], oracle.matmul_rows(rows, a2, b2)) is None
+
+
 def test_strided_views_and_unaligned_leading_dims(ctx, oracle):
     T = torch()
     big_a = ctx.fill(P.DIST_UNIFORM, 7, 300, 301)
