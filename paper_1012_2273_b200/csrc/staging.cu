@@ -28,6 +28,17 @@ namespace {
 
 constexpr size_t CHUNK = size_t(32) << 20;  // bytes per pinned chunk
 constexpr int NSLOT = 4;
+// below this a direct pageable cudaMemcpy (the driver's own staging) wins
+// over waking the copy threads
+constexpr size_t STAGE_MIN = size_t(2) << 20;
+
+// rows per chunk: at least four chunks per copy (so the host copy of one
+// overlaps the DMA of the previous even for mid-size matrices), 1 MB to
+// CHUNK bytes each
+size_t rows_per_chunk(size_t width, size_t rows) {
+  const size_t target = std::clamp(width * rows / 4, size_t(1) << 20, CHUNK);
+  return std::clamp<size_t>(target / width, 1, CHUNK / width);
+}
 
 // Row-pitched copy split over a persistent pool of host threads (the calling
 // thread takes part 0).
@@ -170,12 +181,12 @@ void staging_destroy(mmws_gpu_ctx* ctx) {
 cudaError_t copy_h2d(mmws_gpu_ctx* ctx, void* dst, size_t dpitch, const void* src, size_t spitch,
                      size_t width, size_t rows, cudaStream_t s) {
   if (rows == 0 || width == 0) return cudaSuccess;
-  if (!is_pageable(src) || width > CHUNK)
+  if (width * rows < STAGE_MIN || width > CHUNK || !is_pageable(src))
     return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, cudaMemcpyHostToDevice, s);
   Stager* st;
   cudaError_t e = get_stager(ctx, &st);
   if (e != cudaSuccess) return e;
-  const size_t per = std::max<size_t>(1, CHUNK / width);  // rows per chunk
+  const size_t per = rows_per_chunk(width, rows);
   for (size_t r0 = 0; r0 < rows; r0 += per) {
     const size_t nr = std::min(per, rows - r0);
     int k;
@@ -208,12 +219,12 @@ cudaError_t D2hPump::drain_one() {
 cudaError_t D2hPump::add(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
                          size_t rows) {
   if (rows == 0 || width == 0) return cudaSuccess;
-  if (!is_pageable(dst) || width > CHUNK)
+  if (width * rows < STAGE_MIN || width > CHUNK || !is_pageable(dst))
     return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, cudaMemcpyDeviceToHost, s_);
   Stager* st;
   cudaError_t e = get_stager(ctx_, &st);
   if (e != cudaSuccess) return e;
-  const size_t per = std::max<size_t>(1, CHUNK / width);
+  const size_t per = rows_per_chunk(width, rows);
   for (size_t r0 = 0; r0 < rows; r0 += per) {
     // keep NSLOT - 1 chunks in flight: copy the oldest out while the rest move
     if (pending_.size() >= NSLOT - 1 && (e = drain_one()) != cudaSuccess) return e;
