@@ -113,6 +113,14 @@ class CopyPool {
   bool stop_ = false;
 };
 
+// cudaMemcpy2DAsync, as one linear copy when both sides are dense (a 2-D
+// copy from pageable memory is much slower than the 1-D one)
+cudaError_t copy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                   size_t rows, cudaMemcpyKind kind, cudaStream_t s) {
+  if (dpitch == width && spitch == width) return cudaMemcpyAsync(dst, src, width * rows, kind, s);
+  return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, kind, s);
+}
+
 }  // namespace
 
 struct Stager {
@@ -182,7 +190,7 @@ cudaError_t copy_h2d(mmws_gpu_ctx* ctx, void* dst, size_t dpitch, const void* sr
                      size_t width, size_t rows, cudaStream_t s) {
   if (rows == 0 || width == 0) return cudaSuccess;
   if (width * rows < STAGE_MIN || width > CHUNK || !is_pageable(src))
-    return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, cudaMemcpyHostToDevice, s);
+    return copy2d(dst, dpitch, src, spitch, width, rows, cudaMemcpyHostToDevice, s);
   Stager* st;
   cudaError_t e = get_stager(ctx, &st);
   if (e != cudaSuccess) return e;
@@ -193,8 +201,8 @@ cudaError_t copy_h2d(mmws_gpu_ctx* ctx, void* dst, size_t dpitch, const void* sr
     if ((e = st->take(ctx, &k)) != cudaSuccess) return e;
     st->pool.copy(st->slot[k], width, static_cast<const char*>(src) + r0 * spitch, spitch, width,
                   nr);
-    if ((e = cudaMemcpy2DAsync(static_cast<char*>(dst) + r0 * dpitch, dpitch, st->slot[k], width,
-                               width, nr, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+    if ((e = copy2d(static_cast<char*>(dst) + r0 * dpitch, dpitch, st->slot[k], width, width, nr,
+                    cudaMemcpyHostToDevice, s)) != cudaSuccess ||
         (e = cudaEventRecord(st->ev[k], s)) != cudaSuccess)
       return e;
   }
@@ -220,7 +228,7 @@ cudaError_t D2hPump::add(void* dst, size_t dpitch, const void* src, size_t spitc
                          size_t rows) {
   if (rows == 0 || width == 0) return cudaSuccess;
   if (width * rows < STAGE_MIN || width > CHUNK || !is_pageable(dst))
-    return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, cudaMemcpyDeviceToHost, s_);
+    return copy2d(dst, dpitch, src, spitch, width, rows, cudaMemcpyDeviceToHost, s_);
   Stager* st;
   cudaError_t e = get_stager(ctx_, &st);
   if (e != cudaSuccess) return e;
@@ -232,8 +240,8 @@ cudaError_t D2hPump::add(void* dst, size_t dpitch, const void* src, size_t spitc
     int k;
     if ((e = st->take(ctx_, &k)) != cudaSuccess) return e;
     st->held[k] = true;
-    if ((e = cudaMemcpy2DAsync(st->slot[k], width, static_cast<const char*>(src) + r0 * spitch,
-                               spitch, width, nr, cudaMemcpyDeviceToHost, s_)) != cudaSuccess ||
+    if ((e = copy2d(st->slot[k], width, static_cast<const char*>(src) + r0 * spitch, spitch, width,
+                    nr, cudaMemcpyDeviceToHost, s_)) != cudaSuccess ||
         (e = cudaEventRecord(st->ev[k], s_)) != cudaSuccess)
       return e;
     pending_.push_back({static_cast<char*>(dst) + r0 * dpitch, dpitch, width, nr, k});
