@@ -47,7 +47,7 @@ __device__ __forceinline__ void ffma2(f32x2& d, f32x2 a, f32x2 b) {
 
 constexpr int BM = 192, BN = 128, BK = 16, THREADS = 384, STAGES = 3;
 constexpr int RSTEP = BM / 2;  // row stride between a thread's two 4-row groups
-constexpr int KC_TILES = 16;  // partial-sum chunk = 16 k-tiles = 256 k
+constexpr int KC_TILES = 64;  // partial-sum chunk = 64 k-tiles = 1024 k (as sgemm_tma.cu)
 constexpr int SLA = BK + 4;   // A row pitch (floats)
 constexpr int SLB = BN;       // B row pitch
 constexpr int A_ELEMS = BM * SLA, B_ELEMS = BK * SLB;

@@ -4,7 +4,7 @@
 // with the running totals in shared memory, see there), restructured like the
 // DMMA kernel so the math warps do nothing but LDS + FFMA2:
 //   * a producer warpgroup (one elected lane) streams A[128 x 16] and
-//     B[16 x 256] k-slices with TMA into a 3-stage mbarrier ring and gives its
+//     B[16 x 256] k-slices with TMA into a 4-stage mbarrier ring and gives its
 //     registers to the math warps (setmaxnreg 40 / 232);
 //   * 8 math warps, each lane owning 8 rows x 16 columns (64 packed fp32 pairs)
 //     -- 64 FFMA2 per k against 6 LDS.128 (A as 4-k vectors of one row,
@@ -36,9 +36,9 @@ __device__ __forceinline__ void ffma2(f32x2& d, f32x2 a, f32x2 b) {
   asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
 }
 
-constexpr int BM = 128, BN = 256, BK = 16, STAGES = 3, CONSUMERS = 8;
+constexpr int BM = 128, BN = 256, BK = 16, STAGES = 4, CONSUMERS = 8;
 constexpr int THREADS = (CONSUMERS + 4) * 32;
-constexpr int KC_STAGES = 16;  // partial-sum chunk = 16 stages = 256 k
+constexpr int KC_STAGES = 64;  // partial-sum chunk = 64 stages = 1024 k
 constexpr int A_BYTES = BM * BK * 4, B_BYTES = BK * BN * 4;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TOT_BYTES = CONSUMERS * 32 * 128 * 4;  // 128 floats per math lane
