@@ -178,3 +178,24 @@ def test_rowblock_cost_model():
     assert eg32 * 2 == eg64
     with pytest.raises(P.DomainError):
         P.rowblock_cost(10, 10, 10, 2, 3, bw, fl)
+
+
+REF_CP = os.path.join(ROOT, "oracle", "_ref", "ref_control_plane")
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(REF_INC, "mmws", "launch.hpp")),
+                    reason="reference headers not present (GPU box)")
+def test_nccl_id_over_the_reference_control_plane():
+    # the reference's own launcher (launch_with_master /
+    # connect_from_env) and TCP Communicator ship the NCCL id to every rank
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
+    r = subprocess.run([REF_CP, "master", "4"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "4 ranks share one NCCL id" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_master_run_over_a_world_bootstrapped_by_the_reference_launcher():
+    if not os.path.exists(REF_CP):
+        pytest.skip("ref_control_plane not built (needs the reference headers at build time)")
+    r = subprocess.run([REF_CP, "gpu"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok: master_run" in r.stdout, r.stdout + r.stderr
