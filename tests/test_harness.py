@@ -74,6 +74,14 @@ def test_cli_builds_standalone_and_against_reference(tmp_path):
     if os.path.exists(os.path.join(REF_INC, "mmws", "matrix.hpp")):
         _build(os.path.join(ROOT, "tools", "mmws_gpu_bench.cpp"), tmp_path / "b2",
                extra=("-I" + REF_INC,))
+        json_dir = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"),
+                                   "print-json-dir"], capture_output=True, text=True).stdout.strip()
+        exe = _build(os.path.join(ROOT, "tools", "mmws_gpu_bench.cpp"), tmp_path / "b3",
+                     extra=("-I" + REF_INC, "-I" + json_dir, "-pthread"))
+        # --gpus P needs a GPU per rank; without one the context fails loudly
+        r = subprocess.run([exe, "--dims", "64", "--models", "gpu-rowblock", "--gpus", "1"],
+                           capture_output=True, text=True, timeout=120)
+        assert r.returncode != 0 or "gpu-rowblock" in r.stdout
 
 
 @pytest.mark.gpu
@@ -112,3 +120,21 @@ def test_cli_with_latency_server(tmp_path):
                        timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert len(csv.read_text().splitlines()) == 1 + 8
+
+
+@pytest.mark.gpu
+def test_cli_gpus_mode_through_the_reference_launcher(tmp_path):
+    # --gpus P: the reference's launcher spawns ranks 1..P-1 and ships the NCCL
+    # id; on this one-GPU box P = 1 (a 1-rank NCCL world, same code path)
+    exe = os.path.join(ROOT, "oracle", "_ref", "mmws_gpu_bench_ref")
+    if not os.path.exists(exe):
+        pytest.skip("mmws_gpu_bench_ref not built (needs the reference headers at build time)")
+    csv = tmp_path / "out.csv"
+    r = subprocess.run([exe, "--dims", "100,1000", "--models", "gpu-rowblock", "--gpus", "1",
+                        "--repeats", "2", "--csv", str(csv), "--calibrate"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    lines = csv.read_text().splitlines()
+    assert [ln.split(",")[:3] for ln in lines[1:]] == [["gpu-rowblock", "100", "1"],
+                                                       ["gpu-rowblock", "1000", "1"]]
+    assert "calibration: link" in r.stdout   # 1 rank: no link to measure (nominal)

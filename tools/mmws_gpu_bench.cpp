@@ -4,7 +4,15 @@
 //
 //   mmws_gpu_bench --dims 100,500,1000 [--models gpu,gpu-exact] [--repeats 3]
 //                  [--seed 42] [--csv out.csv] [--tolerance 1e-12] [--server]
-//                  [--plots DIR] [--calibrate]
+//                  [--plots DIR] [--calibrate] [--gpus P]
+//
+// --gpus P (gpu-rowblock over P GPUs of this node, one process per GPU): rank
+// 0 spawns ranks 1..P-1 -- this binary in worker mode -- with the reference's
+// own launcher (launch_with_master / connect_from_env, launch.hpp), ships the
+// NCCL id over its TCP Communicator (mmws::gpu::comm_init_from), and every
+// rank then takes part in each gpu-rowblock round (worker_run on ranks >= 1,
+// replaying the master's sweep from the same arguments).  Needs the
+// reference headers at build time.
 //
 // Build: g++ -std=c++20 -O2 -Iinclude tools/mmws_gpu_bench.cpp
 //            -Lpaper_1012_2273_b200 -lmmws_gpu -Wl,-rpath,<repo>/paper_1012_2273_b200
@@ -16,6 +24,11 @@
 #include <vector>
 
 #include "mmws_gpu_bench.hpp"
+
+#if __has_include(<mmws/launch.hpp>) && __has_include(<nlohmann/json.hpp>)
+#include <mmws/launch.hpp>
+#define MMWS_GPU_BENCH_HAVE_LAUNCHER 1
+#endif
 
 namespace {
 
@@ -31,11 +44,28 @@ std::vector<std::string> split(const std::string& s) {
 int usage() {
   std::fprintf(stderr,
                "usage: mmws_gpu_bench --dims N1,N2,... [--models gpu,gpu-exact,gpu-rowblock] "
-               "[--repeats R] [--seed S] [--tolerance T] [--csv PATH] [--device D] [--server] [--plots DIR] [--calibrate]\n");
+               "[--repeats R] [--seed S] [--tolerance T] [--csv PATH] [--device D] [--server] [--plots DIR] [--calibrate] [--gpus P]\n");
   return 2;
 }
 
 }  // namespace
+
+#ifdef MMWS_GPU_BENCH_HAVE_LAUNCHER
+// Rank >= 1 of a --gpus run: the same rounds as the master's gpu-rowblock
+// records (run_suite order: per N, `repeats` timed rounds), as worker_run.
+int run_worker(const mmws::gpu::BenchConfig& config, bool calibrate) {
+  mmws::Communicator comm = mmws::connect_from_env();
+  mmws::gpu::Context ctx(comm.my_rank());
+  mmws::gpu::comm_init_from(ctx, comm);
+  bool rowblock = false;
+  for (auto m : config.models) rowblock = rowblock || m == mmws::gpu::GpuModel::gpu_rowblock;
+  if (rowblock)
+    for (const std::int64_t n : config.dims)
+      for (int r = 0; r < config.repeats; ++r) mmws::gpu::worker_run(ctx, n, n, n);
+  if (calibrate) mmws::gpu::calibrate(ctx);  // its link probe is collective
+  return 0;
+}
+#endif
 
 int main(int argc, char** argv) {
   mmws::gpu::BenchConfig config;
@@ -43,6 +73,8 @@ int main(int argc, char** argv) {
   bool calibrate = false;  // bench_main.cpp:64-93 analogue: fit the row-block cost model
   int device = 0;
   bool server = false;  // resident latency server for N <= 96 (mmws_gpu_server_start)
+  int gpus = 0;  // 0: no --gpus, plain single-context run
+  bool worker = false;
   try {
     for (int i = 1; i < argc; ++i) {
       const std::string arg = argv[i];
@@ -69,6 +101,10 @@ int main(int argc, char** argv) {
         plots_dir = value();
       } else if (arg == "--calibrate") {
         calibrate = true;
+      } else if (arg == "--gpus") {
+        gpus = std::stoi(value());
+      } else if (arg == "--worker") {
+        worker = true;
       } else if (arg == "--server") {
         server = true;
       } else {
@@ -76,7 +112,22 @@ int main(int argc, char** argv) {
       }
     }
     if (config.dims.empty()) return usage();
+#ifdef MMWS_GPU_BENCH_HAVE_LAUNCHER
+    if (worker) return run_worker(config, calibrate);
+    std::optional<mmws::MsgWorld> world;
+    if (gpus >= 1) {  // even P = 1 goes through the launcher and a 1-rank NCCL world
+      std::vector<std::string> child_args(argv + 1, argv + argc);
+      child_args.push_back("--worker");
+      world.emplace(mmws::launch_with_master("/proc/self/exe", child_args, gpus));
+    }
+#else
+    if (gpus > 1 || worker)
+      throw mmws::DomainError("--gpus > 1 needs the reference headers (its launcher) at build time");
+#endif
     mmws::gpu::Context ctx(device);
+#ifdef MMWS_GPU_BENCH_HAVE_LAUNCHER
+    if (world) mmws::gpu::comm_init_from(ctx, world->comm);
+#endif
     if (server) ctx.server_start();
     const auto records = mmws::gpu::run_suite(ctx, config);
     std::printf("%-13s %8s %8s %14s %14s %12s\n", "model", "n", "gpus", "elapsed_s", "mflops",
