@@ -131,12 +131,18 @@ __global__ void __launch_bounds__(THREADS, 1)
           b2[2 * j + 1] = pack2(b.z, b.w);
         }
 #pragma unroll
+        f32x2 aa[8];
+#pragma unroll
         for (int i = 0; i < 8; ++i) {
           const float a = kk == 0 ? a4[i].x : kk == 1 ? a4[i].y : kk == 2 ? a4[i].z : a4[i].w;
-          const f32x2 aa = pack2(a, a);
-#pragma unroll
-          for (int p = 0; p < 8; ++p) ffma2(part[i][p], aa, b2[p]);
+          aa[i] = pack2(a, a);
         }
+        // B pair outer, A inner: consecutive FFMA2s share the B pair (operand
+        // reuse cache) and read one fresh scalar A register each
+#pragma unroll
+        for (int p = 0; p < 8; ++p)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) ffma2(part[i][p], aa[i], b2[p]);
       }
     }
     if ((kt % KC_STAGES) == KC_STAGES - 1 || kt + 1 == KT) {
