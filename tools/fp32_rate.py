@@ -1,5 +1,10 @@
-import os, sys, json
-sys.path.insert(0, os.getcwd())
+"""FP32 FFMA2 multiply rate (TFLOP/s, min of 3 CUDA-event timings) at the given N.
+Usage: python tools/fp32_rate.py [N ...]"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_1012_2273_b200 as P
 ctx = P.Context(0)

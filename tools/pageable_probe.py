@@ -1,5 +1,11 @@
-import os, sys, time, json
-sys.path.insert(0, os.getcwd())
+"""Host-buffer multiply from pageable vs pinned numpy arrays (the staging ring of
+csrc/staging.cu) at N = 2048 / 4096 / 8192, plus single-thread numpy copy speed."""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_1012_2273_b200 as P
 ctx = P.Context(0)

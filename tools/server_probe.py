@@ -1,5 +1,10 @@
-import os, sys, json
-sys.path.insert(0, os.getcwd())
+"""Latency-server wall time per call (min / median) for N in {10..96} and several
+grid sizes.  Usage: python tools/server_probe.py [CTAS ...]"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_1012_2273_b200 as P
 ctx = P.Context(0)

@@ -1,5 +1,9 @@
-import os, sys, json
-sys.path.insert(0, os.getcwd())
+"""Host-entry wall time (min / median of 50) for small pageable multiplies."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_1012_2273_b200 as P
 ctx = P.Context(0)
