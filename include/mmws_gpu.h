@@ -62,13 +62,21 @@ enum {
  *              DMMA_SMALL by tile count -- the choice never depends on m, so
  *              row slices of a problem get the whole problem's bits; fp32: FFMA.
  *              EXACT also switches to 32x32 tiles for small problems.
- *   FFMA       fp32 register-blocked FFMA GEMM (sgemm only). */
+ *   FFMA       fp32 register-blocked FFMA GEMM (sgemm only).
+ *   OZAKI      fp64 emulated exactly on the int8 tensor cores (tcgen05
+ *              .kind::i8): power-of-two row/column scaling to t-bit integers,
+ *              residues mod 14 coprime moduli <= 256, exact int8 GEMMs, CRT
+ *              reconstruction.  Normwise error ~1e-14 for random inputs,
+ *              bit-exact for integer-valued inputs, row-slice invariant;
+ *              finite inputs only (Inf/NaN rows or columns give NaN), k <=
+ *              131072.  Opt-in: AUTO stays on the FP64 tensor path (dgemm). */
 enum {
   MMWS_GPU_MODE_AUTO = 0,
   MMWS_GPU_MODE_EXACT = 1,
   MMWS_GPU_MODE_DMMA = 2,
   MMWS_GPU_MODE_DMMA_SMALL = 3,
-  MMWS_GPU_MODE_FFMA = 4
+  MMWS_GPU_MODE_FFMA = 4,
+  MMWS_GPU_MODE_OZAKI = 5
 };
 
 /* Generator distributions over the reference's splitmix64 stream

@@ -69,6 +69,7 @@ enum class Mode : int {
   dmma = MMWS_GPU_MODE_DMMA,
   dmma_small = MMWS_GPU_MODE_DMMA_SMALL,
   ffma = MMWS_GPU_MODE_FFMA,
+  ozaki = MMWS_GPU_MODE_OZAKI,  // fp64 emulated on the int8 tensor cores (opt-in)
 };
 
 inline void check(int rc) {

@@ -9,5 +9,5 @@ from .api import (Context, DimensionError, DomainError, GpuError, Graph, Protoco
                   RankError, bootstrap_comm, nccl_unique_id, op_count, rowblock_cost, rowblock_plan,
                   split_rows, static_partition)
 from ._abi import (DIST_INT8, DIST_NORMAL, DIST_UNIFORM, DIST_UNIT, MODE_AUTO, MODE_DMMA,  # noqa: F401
-                   MODE_DMMA_SMALL, MODE_EXACT, MODE_FFMA, PROBE_DFMA, PROBE_DMMA,
+                   MODE_DMMA_SMALL, MODE_EXACT, MODE_FFMA, MODE_OZAKI, PROBE_DFMA, PROBE_DMMA,
                    PROBE_DMUL_DADD, PROBE_FFMA, PROBE_FFMA2)

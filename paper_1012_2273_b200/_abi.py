@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(PKG_DIR, "libmmws_gpu.so")
 HEADER = os.path.join(os.path.dirname(PKG_DIR), "include", "mmws_gpu.h")
 
 OK, ERR_DIMENSION, ERR_DOMAIN, ERR_CUDA, ERR_NCCL, ERR_RANK, ERR_PROTOCOL, ERR_STATE, ERR_ALLOC = range(9)
-MODE_AUTO, MODE_EXACT, MODE_DMMA, MODE_DMMA_SMALL, MODE_FFMA = range(5)
+MODE_AUTO, MODE_EXACT, MODE_DMMA, MODE_DMMA_SMALL, MODE_FFMA, MODE_OZAKI = range(6)
 DIST_UNIT, DIST_UNIFORM, DIST_INT8, DIST_NORMAL = range(4)
 PROBE_DMMA, PROBE_DFMA, PROBE_DMUL_DADD, PROBE_FFMA, PROBE_FFMA2 = range(5)
 

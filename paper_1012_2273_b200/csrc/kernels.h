@@ -42,6 +42,13 @@ struct DmmaStream {
   double* partial = nullptr;
   int* flags = nullptr;
 };
+// fp64 GEMM emulated on the int8 tensor cores (ozaki.cu): plan (moduli s,
+// integer bits t) for inner dimension k, workspace bytes, launch (6 kernels).
+void ozaki_plan(int64_t k, int* s, int* t);
+size_t ozaki_workspace_bytes(int64_t m, int64_t n, int64_t k);
+cudaError_t launch_dgemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K, const double* A,
+                               int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                               void* ws);
 // Force-load kernels (cudaFuncGetAttributes).  Under CUDA_MODULE_LOADING=LAZY
 // the first launch of a kernel loads it with a context-wide synchronisation,
 // which would wait forever on the resident latency server (and costs tens of
@@ -55,6 +62,7 @@ cudaError_t preload_kernels(F... f) {
   return e;
 }
 cudaError_t preload_dgemm_dmma();
+cudaError_t preload_ozaki();
 cudaError_t preload_dgemm_exact();
 cudaError_t preload_dgemm_small();
 cudaError_t preload_sgemm();

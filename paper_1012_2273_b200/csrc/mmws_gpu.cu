@@ -164,6 +164,16 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
     }
     return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm exact");
   }
+  if (mode == MMWS_GPU_MODE_OZAKI) {
+    // fp64 emulated on the int8 tensor cores (ozaki.cu); inputs read with
+    // plain loads, so any layout works without packing
+    if (k > 131072)
+      return fail(MMWS_GPU_ERR_DIMENSION, "dgemm ozaki: k must be <= 131072 (int32 accumulation)");
+    if ((e = ensure(ctx, &ctx->ws, &ctx->ws_bytes, ozaki_workspace_bytes(m, n, k))) != cudaSuccess)
+      return cuda_fail(e, "dgemm ozaki workspace");
+    e = launch_dgemm_ozaki(L, m, n, k, A, lda, B, ldb, C, ldc, ctx->ws);
+    return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm ozaki");
+  }
   if (mode != MMWS_GPU_MODE_AUTO && mode != MMWS_GPU_MODE_DMMA &&
       mode != MMWS_GPU_MODE_DMMA_SMALL)
     return fail(MMWS_GPU_ERR_DOMAIN, "dgemm: unknown mode " + std::to_string(mode));
@@ -293,7 +303,8 @@ int mmws_gpu_init(int device, mmws_gpu_ctx** out) {
   // inside the caller's timed region (~70 ms on the first streamed host
   // multiply at N=16384), and the latency server relies on it (server.cu).
   if ((e = preload_dgemm_dmma()) || (e = preload_dgemm_exact()) || (e = preload_dgemm_small()) ||
-      (e = preload_sgemm()) || (e = preload_sgemm_tma()) || (e = preload_misc()))
+      (e = preload_sgemm()) || (e = preload_sgemm_tma()) || (e = preload_misc()) ||
+      (e = preload_ozaki()))
     return cuda_fail(e, "mmws_gpu_init: load kernels");
   auto* ctx = new (std::nothrow) mmws_gpu_ctx();
   if (!ctx) return fail(MMWS_GPU_ERR_ALLOC, "mmws_gpu_init: out of host memory");

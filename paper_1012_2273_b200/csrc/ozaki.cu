@@ -1,0 +1,468 @@
+// ozaki.cu -- fp64 GEMM emulated exactly on the int8 tensor cores
+// (MMWS_GPU_MODE_OZAKI; an opt-in mode, AUTO stays on DMMA).
+//
+// The FP64 tensor pipe (DMMA) peaks at 37 TFLOP/s on B200; the int8 tcgen05
+// pipe at ~4.5 POPS.  The Ozaki scheme (Ozaki, Uchino, Imamura: "Ozaki Scheme
+// II: a GEMM-oriented emulation of floating-point matrix multiplication using
+// an integer modular technique") trades one fp64 GEMM for s exact int8 GEMMs:
+//   1. scale every row of A and column of B by a power of two so its largest
+//      magnitude is just below 2^t and round to integers A', B' (|A'|, |B'| <
+//      2^t; the only rounding of the whole scheme, relative 2^-t per element);
+//   2. for s pairwise-coprime moduli p_l <= 256, take signed residues
+//      A'_l = A' mod p_l, B'_l = B' mod p_l (int8) and compute the exact int32
+//      products A'_l B'_l on the tensor cores (|.| <= k * 128^2 < 2^31), kept
+//      mod p_l as uint8;
+//   3. rebuild C' = A'B' exactly from its residues by the Chinese remainder
+//      theorem (P = prod p_l > 2 k 2^(2t), 128-bit integers) and scale back:
+//      C = C' * 2^-(e_i + f_j), one rounding to double.
+// With s = 14 moduli (P ~ 2^110) and k <= 16384, t = 47: the normwise error is
+// ~1.4 * 2^-47 ~ 1e-14 for random inputs (bound 1e-12), and integer-valued
+// inputs come out bit-exact (C' is then the exact integer product).  Each
+// element's result depends only on its row of A and column of B, so row
+// slices give the same bits as the whole problem.  Inputs must be finite; a
+// row or column holding Inf/NaN yields NaN in the affected outputs.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mmws_impl {
+namespace {
+
+using namespace mmws_dev;
+
+constexpr int OZ_MAX_MODULI = 16;
+constexpr int OZ_NONFINITE = 1 << 20;  // exponent marker: row / column holds Inf or NaN
+
+// pairwise-coprime moduli, largest first (log2 of the product: 8, 16, 24, ...)
+constexpr int kModuli[OZ_MAX_MODULI] = {256, 255, 253, 251, 247, 241, 239, 233,
+                                        229, 227, 223, 211, 199, 197, 193, 191};
+
+struct CrtConst {
+  int p[OZ_MAX_MODULI];
+  int w[OZ_MAX_MODULI];          // (P / p_l)^-1 mod p_l
+  uint64_t m_lo[OZ_MAX_MODULI];  // P / p_l, 128-bit
+  uint64_t m_hi[OZ_MAX_MODULI];
+  uint64_t P_lo, P_hi;
+  double P_d;
+  int s;
+};
+__constant__ CrtConst c_crt;
+
+// ---------------------------------------------------------------- scaling exponents
+// e_i: amax_i * 2^e_i < 2^t for row i of A (frexp: amax = f 2^x, f in [0.5, 1))
+__global__ void row_exponent_kernel(const double* __restrict__ A, int64_t lda, int m, int k, int t,
+                                    int* __restrict__ e) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= m) return;
+  const double* row = A + static_cast<int64_t>(warp) * lda;
+  double amax = 0.0;
+  bool finite = true;
+  for (int j = lane; j < k; j += 32) {
+    const double v = row[j];
+    finite = finite && isfinite(v);
+    amax = fmax(amax, fabs(v));
+  }
+  for (int o = 16; o; o >>= 1) {
+    amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    finite = __all_sync(0xffffffffu, finite);
+  }
+  if (lane == 0) {
+    int x = 0;
+    frexp(amax, &x);
+    e[warp] = !finite ? OZ_NONFINITE : (amax == 0.0 ? 0 : t - x);
+  }
+}
+
+// f_j for column j of B (k x n, row-major): a thread per column, rows walked
+// in order (coalesced across the warp)
+__global__ void col_exponent_kernel(const double* __restrict__ B, int64_t ldb, int k, int n, int t,
+                                    int* __restrict__ f) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double amax = 0.0;
+  bool finite = true;
+  for (int r = 0; r < k; ++r) {
+    const double v = B[static_cast<int64_t>(r) * ldb + j];
+    finite = finite && isfinite(v);
+    amax = fmax(amax, fabs(v));
+  }
+  int x = 0;
+  frexp(amax, &x);
+  f[j] = !finite ? OZ_NONFINITE : (amax == 0.0 ? 0 : t - x);
+}
+
+// signed residue of an integer-valued double (|x| < 2^53): exact
+MMWS_DEVICE int8_t sresidue(double x, int p) {
+  const double pd = static_cast<double>(p);
+  const double q = floor(x * (1.0 / pd));
+  double r = fma(-q, pd, x);  // exact: |q p| ~ |x| < 2^53, result an integer < 2p
+  if (r < 0.0) r += pd;
+  if (r >= pd) r -= pd;
+  int ri = static_cast<int>(r);
+  if (ri >= (p + 1) / 2) ri -= p;
+  return static_cast<int8_t>(ri);
+}
+
+MMWS_DEVICE double scaled_int(double v, int ex) {
+  return ex == OZ_NONFINITE ? 0.0 : rint(ldexp(v, ex));
+}
+
+// residues of A' = rint(A 2^e): res[l][i][j], j < kpad (zero padding)
+__global__ void residue_a_kernel(const double* __restrict__ A, int64_t lda, int m, int k, int kpad,
+                                 const int* __restrict__ e, int8_t* __restrict__ res) {
+  const int64_t total = static_cast<int64_t>(m) * kpad;
+  const int s = c_crt.s;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(idx / kpad), j = static_cast<int>(idx % kpad);
+    const double x = j < k ? scaled_int(A[static_cast<int64_t>(i) * lda + j], e[i]) : 0.0;
+#pragma unroll 4
+    for (int l = 0; l < s; ++l) res[l * total + idx] = sresidue(x, c_crt.p[l]);
+  }
+}
+
+// residues of B' = rint(B 2^f) transposed (K-major operand): res[l][j][r],
+// r < kpad; 32 x 32 tiles through shared memory
+__global__ void residue_bt_kernel(const double* __restrict__ B, int64_t ldb, int k, int n, int kpad,
+                                  const int* __restrict__ f, int8_t* __restrict__ res) {
+  __shared__ double tile[32][33];
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int i = ty; i < 32; i += 8) {
+    const int r = r0 + i, c = c0 + tx;
+    tile[i][tx] = (r < k && c < n) ? scaled_int(B[static_cast<int64_t>(r) * ldb + c], f[c]) : 0.0;
+  }
+  __syncthreads();
+  const int64_t total = static_cast<int64_t>(n) * kpad;
+  const int s = c_crt.s;
+  for (int i = ty; i < 32; i += 8) {
+    const int c = c0 + i, r = r0 + tx;  // output row c (column of B), position r along k
+    if (c >= n || r >= kpad) continue;
+    const double x = tile[tx][i];
+    const int64_t o = static_cast<int64_t>(c) * kpad + r;
+    for (int l = 0; l < s; ++l) res[l * total + o] = sresidue(x, c_crt.p[l]);
+  }
+}
+
+// ---------------------------------------------------------------- int8 tensor-core GEMM
+// C_l = (A_l B_l^T) mod p_l for every modulus l (grid.z), A_l: m x kpad,
+// B_l: n x kpad (both K-major int8), C_l: m x n uint8.  128 x 256 CTA tile,
+// tcgen05.mma.kind::i8 (M=128, N=256, K=32) issued by one thread, operands
+// TMA-staged (128-byte swizzle, 4-stage ring), int32 accumulator in TMEM
+// (256 columns), epilogue tcgen05.ld -> mod p -> 16-byte stores.
+constexpr int IG_BM = 128, IG_BN = 256, IG_BK = 128, IG_STAGES = 4, IG_THREADS = 128;
+constexpr int IG_A_BYTES = IG_BM * IG_BK, IG_B_BYTES = IG_BN * IG_BK;
+constexpr int IG_STAGE = IG_A_BYTES + IG_B_BYTES;
+constexpr int IG_SMEM = IG_STAGES * IG_STAGE + 1024 + 256;
+constexpr uint32_t IG_TMEM_COLS = 256;
+// instruction descriptor: s32 accumulate, s8 x s8, K-major A and B, N = 256, M = 128
+constexpr uint32_t IG_IDESC =
+    (2u << 4) | (1u << 7) | (1u << 10) | ((IG_BN >> 3) << 17) | ((IG_BM >> 4) << 24);
+
+MMWS_DEVICE void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                             int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+// shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row core
+// groups 1024 bytes apart (SBO), sm100 descriptor version 1
+MMWS_DEVICE uint64_t umma_desc(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>(1024 >> 4) << 32) |
+         (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(2) << 61);
+}
+
+MMWS_DEVICE void umma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(IG_IDESC), "r"(accumulate));
+}
+
+MMWS_DEVICE void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(IG_THREADS, 1)
+    igemm_mod_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     uint8_t* __restrict__ C, int m, int n, int kpad, int tiles_m, int tiles_n) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + IG_STAGES * IG_STAGE);
+  uint64_t* empty = full + IG_STAGES;
+  uint64_t* tmem_full = empty + IG_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // grouped rasterisation (8 tile rows): neighbouring CTAs share A and B panels in L2
+  constexpr int GROUP = 8;
+  const int tile = blockIdx.x;
+  const int per_group = GROUP * tiles_n;
+  const int first_m = (tile / per_group) * GROUP;
+  const int gm = min(tiles_m - first_m, GROUP);
+  const int tm = first_m + (tile % per_group) % gm, tn = (tile % per_group) / gm;
+  const int z = blockIdx.z;
+  const int KB = (kpad + IG_BK - 1) / IG_BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < IG_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(IG_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {  // TMA producer
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int kb = 0; kb < KB; ++kb) {
+      const int s = kb % IG_STAGES;
+      if (kb >= IG_STAGES) mbar_wait(&empty[s], ((kb / IG_STAGES) - 1) & 1);
+      uint8_t* sa = smem + s * IG_STAGE;
+      mbar_arrive_expect_tx(&full[s], IG_STAGE);
+      tma_load_3d(sa, &tmA, &full[s], kb * IG_BK, tm * IG_BM, z);
+      tma_load_3d(sa + IG_A_BYTES, &tmB, &full[s], kb * IG_BK, tn * IG_BN, z);
+    }
+  } else if (warp == 1 && lane == 0) {  // MMA issuer
+    for (int kb = 0; kb < KB; ++kb) {
+      const int s = kb % IG_STAGES;
+      mbar_wait(&full[s], (kb / IG_STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t sa = smem_u32(smem + s * IG_STAGE), sb = sa + IG_A_BYTES;
+#pragma unroll
+      for (int kk = 0; kk < IG_BK / 32; ++kk)  // K = 32 bytes per MMA, inside the swizzle row
+        umma_i8(tmem, umma_desc(sa + kk * 32), umma_desc(sb + kk * 32), (kb | kk) != 0);
+      umma_commit(&empty[s]);  // the stage is free once these MMAs have read it
+    }
+    umma_commit(tmem_full);
+  }
+  __syncwarp();
+
+  // epilogue: warp w reads TMEM lanes 32w..32w+31 (= tile rows), 32 columns at a time
+  mbar_wait(tmem_full, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const int row = tm * IG_BM + warp * 32 + lane;
+  const int p = c_crt.p[z];
+  uint8_t* crow = C + (static_cast<size_t>(z) * m + row) * n;
+#pragma unroll 1
+  for (int c0 = 0; c0 < IG_BN; c0 += 32) {
+    uint32_t v[32];
+    const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+        "%28, %29, %30, %31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+          "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+          "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;");
+    const int col = tn * IG_BN + c0;
+    if (row >= m || col >= n) continue;
+    uint32_t packed[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int x = static_cast<int>(v[4 * q + b]);
+        int r = x % p;  // C mod p in [0, p)
+        r += r < 0 ? p : 0;
+        word |= static_cast<uint32_t>(r) << (8 * b);
+      }
+      packed[q] = word;
+    }
+    if (col + 32 <= n && (n % 16) == 0) {
+      uint4* dst = reinterpret_cast<uint4*>(crow + col);
+      dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+      dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+    } else {
+      const uint8_t* bytes = reinterpret_cast<const uint8_t*>(packed);
+      for (int j = 0; j < 32 && col + j < n; ++j) crow[col + j] = bytes[j];
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(IG_TMEM_COLS));
+}
+
+// ---------------------------------------------------------------- reconstruction
+// C'_ij = sum_l ((y_l w_l) mod p_l) (P / p_l)  mod P, lifted to (-P/2, P/2],
+// then C_ij = C' 2^-(e_i + f_j)
+__global__ void crt_kernel(const uint8_t* __restrict__ Cres, int m, int n,
+                           const int* __restrict__ e, const int* __restrict__ f,
+                           double* __restrict__ C, int64_t ldc) {
+  const int64_t total = static_cast<int64_t>(m) * n;
+  const int s = c_crt.s;
+  const unsigned __int128 P =
+      (static_cast<unsigned __int128>(c_crt.P_hi) << 64) | static_cast<unsigned __int128>(c_crt.P_lo);
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(idx / n), j = static_cast<int>(idx % n);
+    double* out = C + static_cast<int64_t>(i) * ldc + j;
+    const int ex = e[i], fx = f[j];
+    if (ex == OZ_NONFINITE || fx == OZ_NONFINITE) {
+      *out = __longlong_as_double(0x7ff8000000000000LL);
+      continue;
+    }
+    unsigned __int128 acc = 0;
+    for (int l = 0; l < s; ++l) {
+      const int p = c_crt.p[l];
+      const int y = Cres[l * total + idx];
+      int z = (y * c_crt.w[l]) % p;  // < 2^16: exact
+      const unsigned __int128 M =
+          (static_cast<unsigned __int128>(c_crt.m_hi[l]) << 64) | c_crt.m_lo[l];
+      acc += static_cast<unsigned __int128>(static_cast<unsigned>(z)) * M;
+    }
+    // acc < s P: reduce mod P with a floating-point quotient estimate
+    const double accd = static_cast<double>(static_cast<uint64_t>(acc >> 64)) * 18446744073709551616.0 +
+                        static_cast<double>(static_cast<uint64_t>(acc));
+    uint64_t q = static_cast<uint64_t>(accd / c_crt.P_d);
+    unsigned __int128 qP = static_cast<unsigned __int128>(q) * P;
+    while (qP > acc) {
+      --q;
+      qP -= P;
+    }
+    unsigned __int128 r = acc - qP;
+    while (r >= P) r -= P;
+    // signed lift and conversion (two roundings at most; exact below 2^53)
+    const bool neg = r > (P >> 1);
+    const unsigned __int128 mag = neg ? P - r : r;
+    double d = static_cast<double>(static_cast<uint64_t>(mag >> 64)) * 18446744073709551616.0 +
+               static_cast<double>(static_cast<uint64_t>(mag));
+    d = neg ? -d : d;
+    *out = ldexp(d, -(ex + fx));
+  }
+}
+
+bool map3_u8(const Launch& L, CUtensorMap* map, const void* base, int64_t kpad, int64_t rows,
+             int64_t batch, int box_rows) {
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(kpad), static_cast<cuuint64_t>(rows),
+                              static_cast<cuuint64_t>(batch)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(kpad),
+                                 static_cast<cuuint64_t>(kpad * rows)};
+  const cuuint32_t box[3] = {IG_BK, static_cast<cuuint32_t>(box_rows), 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return L.encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// host: CRT constants for the first s moduli
+void make_crt(int s, CrtConst* c) {
+  c->s = s;
+  unsigned __int128 P = 1;
+  for (int l = 0; l < s; ++l) P *= static_cast<unsigned>(kModuli[l]);
+  for (int l = 0; l < s; ++l) {
+    const int p = kModuli[l];
+    const unsigned __int128 M = P / static_cast<unsigned>(p);
+    const int mr = static_cast<int>(M % static_cast<unsigned>(p));
+    int w = 1;
+    while ((mr * w) % p != 1) ++w;  // p <= 256: brute force
+    c->p[l] = p;
+    c->w[l] = w;
+    c->m_lo[l] = static_cast<uint64_t>(M);
+    c->m_hi[l] = static_cast<uint64_t>(M >> 64);
+  }
+  c->P_lo = static_cast<uint64_t>(P);
+  c->P_hi = static_cast<uint64_t>(P >> 64);
+  c->P_d = static_cast<double>(c->P_hi) * 18446744073709551616.0 + static_cast<double>(c->P_lo);
+}
+
+}  // namespace
+
+// Plan: number of moduli and integer bits for an inner dimension k.
+void ozaki_plan(int64_t k, int* s_out, int* t_out) {
+  const double logk = std::ceil(std::log2(static_cast<double>(std::max<int64_t>(k, 2))));
+  double logP = 0;
+  int s = 0, t = 0;
+  for (s = 1; s <= OZ_MAX_MODULI; ++s) {
+    logP += std::log2(static_cast<double>(kModuli[s - 1]));
+    t = static_cast<int>(std::floor((logP - 2.0 - logk) / 2.0));
+    if (t >= 46) break;  // ~1.4 * 2^-46 ~ 2e-14 normwise for random inputs
+  }
+  if (s > OZ_MAX_MODULI) s = OZ_MAX_MODULI;
+  *s_out = s;
+  *t_out = std::min(t, 52);
+}
+
+size_t ozaki_workspace_bytes(int64_t m, int64_t n, int64_t k) {
+  int s, t;
+  ozaki_plan(k, &s, &t);
+  const int64_t kpad = (k + 15) / 16 * 16;
+  return static_cast<size_t>(s) * (m * kpad + n * kpad + m * n) + sizeof(int) * (m + n) + 1024;
+}
+
+cudaError_t launch_dgemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K, const double* A,
+                               int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                               void* ws) {
+  int s, t;
+  ozaki_plan(K, &s, &t);
+  CrtConst cc;
+  make_crt(s, &cc);
+  cudaError_t e = cudaMemcpyToSymbolAsync(c_crt, &cc, sizeof(cc), 0, cudaMemcpyHostToDevice, L.stream);
+  if (e != cudaSuccess) return e;
+  const int64_t kpad = (K + 15) / 16 * 16;
+  int8_t* ares = static_cast<int8_t*>(ws);
+  int8_t* bres = ares + s * M * kpad;
+  uint8_t* cres = reinterpret_cast<uint8_t*>(bres + s * N * kpad);
+  int* ex = reinterpret_cast<int*>(reinterpret_cast<uintptr_t>(cres + s * M * N + 15) & ~uintptr_t(15));
+  int* fx = ex + M;
+  const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
+  row_exponent_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, L.stream>>>(A, lda, m, k,
+                                                                                      t, ex);
+  col_exponent_kernel<<<static_cast<unsigned>((N + 255) / 256), 256, 0, L.stream>>>(B, ldb, k, n, t,
+                                                                                   fx);
+  const unsigned grid_e = static_cast<unsigned>(std::min<int64_t>((M * kpad + 255) / 256, L.num_sms * 16));
+  residue_a_kernel<<<grid_e, 256, 0, L.stream>>>(A, lda, m, k, static_cast<int>(kpad), ex, ares);
+  residue_bt_kernel<<<dim3(static_cast<unsigned>((N + 31) / 32), static_cast<unsigned>((kpad + 31) / 32)),
+                      256, 0, L.stream>>>(B, ldb, k, n, static_cast<int>(kpad), fx, bres);
+  CUtensorMap ta, tb;
+  if (!map3_u8(L, &ta, ares, kpad, M, s, IG_BM) || !map3_u8(L, &tb, bres, kpad, N, s, IG_BN))
+    return cudaErrorInvalidValue;
+  if ((e = cudaFuncSetAttribute(igemm_mod_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                IG_SMEM)) != cudaSuccess)
+    return e;
+  const int tiles_m = static_cast<int>((M + IG_BM - 1) / IG_BM);
+  const int tiles_n = static_cast<int>((N + IG_BN - 1) / IG_BN);
+  igemm_mod_kernel<<<dim3(tiles_m * tiles_n, 1, s), IG_THREADS, IG_SMEM, L.stream>>>(
+      ta, tb, cres, m, n, static_cast<int>(kpad), tiles_m, tiles_n);
+  const unsigned grid_c = static_cast<unsigned>(std::min<int64_t>((M * N + 255) / 256, L.num_sms * 16));
+  crt_kernel<<<grid_c, 256, 0, L.stream>>>(cres, m, n, ex, fx, C, ldc);
+  for (int i = 0; i < 6; ++i) L.count();
+  return cudaGetLastError();
+}
+
+cudaError_t preload_ozaki() {
+  return preload_kernels(row_exponent_kernel, col_exponent_kernel, residue_a_kernel,
+                         residue_bt_kernel, igemm_mod_kernel, crt_kernel);
+}
+
+}  // namespace mmws_impl
