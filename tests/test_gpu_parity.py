@@ -215,6 +215,54 @@ def test_random_shapes_and_strides(ctx, oracle, seed):
             assert normwise(gotf, wantf) <= FP32_TOL, (m, k, n, pa, pb)
 
 
+# ----------------------------------------------------------------------------- fp64 on the int8 tensor cores
+@pytest.mark.parametrize("shape", [(1, 1, 1), (7, 3, 5), (128, 128, 128), (129, 1000, 131),
+                                   (300, 17, 257), (1000, 37, 999), (513, 260, 1030),
+                                   (2048, 2048, 2048)])
+def test_ozaki_mode_accuracy_and_integer_exactness(ctx, oracle, shape):
+    m, k, n = shape
+    a = oracle.fill(oracle.DIST_UNIFORM, 51, m, k)
+    b = oracle.fill(oracle.DIST_UNIFORM, 52, k, n)
+    rows = sorted({0, m // 2, m - 1})
+    got = host(ctx.dgemm(dev(a), dev(b), mode=P.MODE_OZAKI))
+    want = oracle.matmul_rows(rows, a, b)
+    assert normwise(got[rows], want) <= 1e-13        # bound 1e-12; expected ~1e-15..1e-14
+    ai = oracle.fill(oracle.DIST_INT8, 53, m, k)
+    bi = oracle.fill(oracle.DIST_INT8, 54, k, n)
+    gi = host(ctx.dgemm(dev(ai), dev(bi), mode=P.MODE_OZAKI))
+    assert oracle.first_difference(gi[rows], oracle.matmul_rows(rows, ai, bi)) is None
+
+
+def test_ozaki_mode_row_slices_strides_scales_and_specials(ctx, oracle):
+    T = torch()
+    m, k, n = 700, 513, 600
+    a = oracle.fill(oracle.DIST_UNIFORM, 61, m, k)
+    b = oracle.fill(oracle.DIST_UNIFORM, 62, k, n)
+    a[3] *= 1e-200                                   # per-row / per-column power-of-two scaling
+    a[5] *= 1e250
+    b[:, 7] *= 3e-300
+    full = host(ctx.dgemm(dev(a), dev(b), mode=P.MODE_OZAKI))
+    for r0, r1 in ((0, 128), (128, 333), (333, 700)):    # row slices: same bits
+        part = host(ctx.dgemm(dev(a[r0:r1]), dev(b), mode=P.MODE_OZAKI))
+        assert (bits(part) == bits(full[r0:r1])).all()
+    rows = [3, 5, 100]
+    want = oracle.matmul_rows(rows, a, b)
+    for i, r in enumerate(rows):                     # row-wise relative accuracy (overflow-safe)
+        scale = np.max(np.abs(want[i]))
+        assert np.linalg.norm((full[r] - want[i]) / scale) <= 1e-13 * np.linalg.norm(want[i] / scale)
+    big = T.zeros((m, k + 3), dtype=T.float64, device="cuda")[:, 1:k + 1]   # misaligned view
+    big.copy_(T.from_numpy(a))
+    assert (bits(host(ctx.dgemm(big, dev(b), mode=P.MODE_OZAKI))) == bits(full)).all()
+    a2 = a.copy()
+    a2[10, 20] = np.inf
+    b2 = b.copy()
+    b2[30, 40] = np.nan
+    g = host(ctx.dgemm(dev(a2), dev(b2), mode=P.MODE_OZAKI))
+    assert np.isnan(g[10]).all() and np.isnan(g[:, 40]).all()
+    assert (bits(np.delete(np.delete(g, 10, 0), 40, 1)) ==
+            bits(np.delete(np.delete(full, 10, 0), 40, 1))).all()
+
+
 # ----------------------------------------------------------------------------- real inputs: tolerance
 def test_config_c1_n1000(ctx, oracle, golden_big):
     n = 1000
