@@ -78,22 +78,39 @@ __global__ void row_exponent_kernel(const double* __restrict__ A, int64_t lda, i
   }
 }
 
-// f_j for column j of B (k x n, row-major): a thread per column, rows walked
-// in order (coalesced across the warp)
-__global__ void col_exponent_kernel(const double* __restrict__ B, int64_t ldb, int k, int n, int t,
-                                    int* __restrict__ f) {
+// f_j for column j of B (k x n, row-major).  |v| as a bit pattern orders
+// like |v| (and Inf < NaN patterns sit above every finite value), so column
+// maxima are atomicMax over 64-bit patterns from a 2-D grid of row blocks;
+// col_exponent_finalize turns them into exponents.
+constexpr int OZ_COL_ROWS = 256;  // rows per block of col_absmax_kernel
+__global__ void col_absmax_kernel(const double* __restrict__ B, int64_t ldb, int k, int n,
+                                  unsigned long long* __restrict__ colmax) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
-  double amax = 0.0;
-  bool finite = true;
-  for (int r = 0; r < k; ++r) {
-    const double v = B[static_cast<int64_t>(r) * ldb + j];
-    finite = finite && isfinite(v);
-    amax = fmax(amax, fabs(v));
+  const int r0 = blockIdx.y * OZ_COL_ROWS, r1 = min(k, r0 + OZ_COL_ROWS);
+  unsigned long long mx = 0;
+  for (int r = r0; r < r1; ++r) {
+    const unsigned long long bits =
+        static_cast<unsigned long long>(__double_as_longlong(B[static_cast<int64_t>(r) * ldb + j])) &
+        0x7fffffffffffffffULL;
+    mx = bits > mx ? bits : mx;
   }
+  atomicMax(colmax + j, mx);
+}
+
+__global__ void col_exponent_finalize(const unsigned long long* __restrict__ colmax, int n, int t,
+                                      int* __restrict__ f) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const unsigned long long bits = colmax[j];
+  if (bits >= 0x7ff0000000000000ULL) {
+    f[j] = OZ_NONFINITE;
+    return;
+  }
+  const double amax = __longlong_as_double(static_cast<long long>(bits));
   int x = 0;
   frexp(amax, &x);
-  f[j] = !finite ? OZ_NONFINITE : (amax == 0.0 ? 0 : t - x);
+  f[j] = amax == 0.0 ? 0 : t - x;
 }
 
 // signed residue of an integer-valued double (|x| < 2^53): exact
@@ -112,22 +129,35 @@ MMWS_DEVICE double scaled_int(double v, int ex) {
   return ex == OZ_NONFINITE ? 0.0 : rint(ldexp(v, ex));
 }
 
-// residues of A' = rint(A 2^e): res[l][i][j], j < kpad (zero padding)
+// residues of A' = rint(A 2^e): res[l][i][j], j < kpad (zero padding).
+// A thread takes 8 consecutive j and stores one 8-byte word per modulus.
 __global__ void residue_a_kernel(const double* __restrict__ A, int64_t lda, int m, int k, int kpad,
                                  const int* __restrict__ e, int8_t* __restrict__ res) {
-  const int64_t total = static_cast<int64_t>(m) * kpad;
+  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (j0 >= kpad) return;
+  for (int i = blockIdx.y; i < m; i += gridDim.y) {
+  const int ex = e[i];
+  const double* row = A + static_cast<int64_t>(i) * lda;
+  double x[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) x[q] = j0 + q < k ? scaled_int(row[j0 + q], ex) : 0.0;
+  const int64_t plane = static_cast<int64_t>(m) * kpad;
+  const int64_t o = static_cast<int64_t>(i) * kpad + j0;
   const int s = c_crt.s;
-  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int i = static_cast<int>(idx / kpad), j = static_cast<int>(idx % kpad);
-    const double x = j < k ? scaled_int(A[static_cast<int64_t>(i) * lda + j], e[i]) : 0.0;
-#pragma unroll 4
-    for (int l = 0; l < s; ++l) res[l * total + idx] = sresidue(x, c_crt.p[l]);
+  for (int l = 0; l < s; ++l) {
+    const int p = c_crt.p[l];
+    unsigned long long w = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      w |= static_cast<unsigned long long>(static_cast<uint8_t>(sresidue(x[q], p))) << (8 * q);
+    *reinterpret_cast<unsigned long long*>(res + l * plane + o) = w;
+  }
   }
 }
 
 // residues of B' = rint(B 2^f) transposed (K-major operand): res[l][j][r],
-// r < kpad; 32 x 32 tiles through shared memory
+// r < kpad; 32 x 32 tiles through shared memory, each thread then packs 4
+// consecutive r of one column into a 4-byte word per modulus
 __global__ void residue_bt_kernel(const double* __restrict__ B, int64_t ldb, int k, int n, int kpad,
                                   const int* __restrict__ f, int8_t* __restrict__ res) {
   __shared__ double tile[32][33];
@@ -138,14 +168,18 @@ __global__ void residue_bt_kernel(const double* __restrict__ B, int64_t ldb, int
     tile[i][tx] = (r < k && c < n) ? scaled_int(B[static_cast<int64_t>(r) * ldb + c], f[c]) : 0.0;
   }
   __syncthreads();
-  const int64_t total = static_cast<int64_t>(n) * kpad;
+  const int c = c0 + tx, rq = r0 + ty * 4;  // column c, rows rq .. rq+3
+  if (c >= n || rq >= kpad) return;
+  const int64_t plane = static_cast<int64_t>(n) * kpad;
+  const int64_t o = static_cast<int64_t>(c) * kpad + rq;
   const int s = c_crt.s;
-  for (int i = ty; i < 32; i += 8) {
-    const int c = c0 + i, r = r0 + tx;  // output row c (column of B), position r along k
-    if (c >= n || r >= kpad) continue;
-    const double x = tile[tx][i];
-    const int64_t o = static_cast<int64_t>(c) * kpad + r;
-    for (int l = 0; l < s; ++l) res[l * total + o] = sresidue(x, c_crt.p[l]);
+  for (int l = 0; l < s; ++l) {
+    const int p = c_crt.p[l];
+    uint32_t w = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      w |= static_cast<uint32_t>(static_cast<uint8_t>(sresidue(tile[ty * 4 + q][tx], p))) << (8 * q);
+    *reinterpret_cast<uint32_t*>(res + l * plane + o) = w;
   }
 }
 
@@ -314,50 +348,67 @@ __global__ void __launch_bounds__(IG_THREADS, 1)
 
 // ---------------------------------------------------------------- reconstruction
 // C'_ij = sum_l ((y_l w_l) mod p_l) (P / p_l)  mod P, lifted to (-P/2, P/2],
-// then C_ij = C' 2^-(e_i + f_j)
+// then C_ij = C' 2^-(e_i + f_j).  Grid (column blocks, rows); a thread takes 4
+// consecutive columns (one 4-byte load per modulus).
+MMWS_DEVICE double u128_to_double(unsigned __int128 v) {  // at most one extra rounding
+  return static_cast<double>(static_cast<uint64_t>(v >> 64)) * 18446744073709551616.0 +
+         static_cast<double>(static_cast<uint64_t>(v));
+}
+
 __global__ void crt_kernel(const uint8_t* __restrict__ Cres, int m, int n,
                            const int* __restrict__ e, const int* __restrict__ f,
                            double* __restrict__ C, int64_t ldc) {
-  const int64_t total = static_cast<int64_t>(m) * n;
+  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (j0 >= n) return;
+  for (int i = blockIdx.y; i < m; i += gridDim.y) {
+  const int64_t plane = static_cast<int64_t>(m) * n;
+  const int64_t base = static_cast<int64_t>(i) * n + j0;
   const int s = c_crt.s;
   const unsigned __int128 P =
       (static_cast<unsigned __int128>(c_crt.P_hi) << 64) | static_cast<unsigned __int128>(c_crt.P_lo);
-  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int i = static_cast<int>(idx / n), j = static_cast<int>(idx % n);
+  const bool vec = (n % 4) == 0;  // 4-byte aligned words (planes and rows)
+  unsigned __int128 acc[4] = {0, 0, 0, 0};
+  for (int l = 0; l < s; ++l) {
+    const int p = c_crt.p[l];
+    const float pf = static_cast<float>(p), inv = 1.0f / pf, wf = static_cast<float>(c_crt.w[l]);
+    uint32_t word = 0;
+    if (vec) {
+      word = *reinterpret_cast<const uint32_t*>(Cres + l * plane + base);
+    } else {
+      for (int q = 0; q < 4 && j0 + q < n; ++q) word |= static_cast<uint32_t>(Cres[l * plane + base + q]) << (8 * q);
+    }
+    const unsigned __int128 M =
+        (static_cast<unsigned __int128>(c_crt.m_hi[l]) << 64) | c_crt.m_lo[l];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float yw = static_cast<float>((word >> (8 * q)) & 0xffu) * wf;  // < 2^16: exact
+      float z = yw - pf * floorf(yw * inv);
+      z += z < 0.f ? pf : 0.f;
+      z -= z >= pf ? pf : 0.f;
+      acc[q] += static_cast<unsigned __int128>(static_cast<uint32_t>(z)) * M;
+    }
+  }
+  const int ex = e[i];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int j = j0 + q;
+    if (j >= n) break;
     double* out = C + static_cast<int64_t>(i) * ldc + j;
-    const int ex = e[i], fx = f[j];
+    const int fx = f[j];
     if (ex == OZ_NONFINITE || fx == OZ_NONFINITE) {
       *out = __longlong_as_double(0x7ff8000000000000LL);
       continue;
     }
-    unsigned __int128 acc = 0;
-    for (int l = 0; l < s; ++l) {
-      const int p = c_crt.p[l];
-      const int y = Cres[l * total + idx];
-      int z = (y * c_crt.w[l]) % p;  // < 2^16: exact
-      const unsigned __int128 M =
-          (static_cast<unsigned __int128>(c_crt.m_hi[l]) << 64) | c_crt.m_lo[l];
-      acc += static_cast<unsigned __int128>(static_cast<unsigned>(z)) * M;
-    }
-    // acc < s P: reduce mod P with a floating-point quotient estimate
-    const double accd = static_cast<double>(static_cast<uint64_t>(acc >> 64)) * 18446744073709551616.0 +
-                        static_cast<double>(static_cast<uint64_t>(acc));
-    uint64_t q = static_cast<uint64_t>(accd / c_crt.P_d);
-    unsigned __int128 qP = static_cast<unsigned __int128>(q) * P;
-    while (qP > acc) {
-      --q;
-      qP -= P;
-    }
-    unsigned __int128 r = acc - qP;
+    // acc < s P: reduce mod P from a floating-point quotient estimate
+    uint64_t qt = static_cast<uint64_t>(u128_to_double(acc[q]) / c_crt.P_d);
+    unsigned __int128 qP = static_cast<unsigned __int128>(qt) * P;
+    while (qP > acc[q]) qP -= P;
+    unsigned __int128 r = acc[q] - qP;
     while (r >= P) r -= P;
-    // signed lift and conversion (two roundings at most; exact below 2^53)
-    const bool neg = r > (P >> 1);
-    const unsigned __int128 mag = neg ? P - r : r;
-    double d = static_cast<double>(static_cast<uint64_t>(mag >> 64)) * 18446744073709551616.0 +
-               static_cast<double>(static_cast<uint64_t>(mag));
-    d = neg ? -d : d;
-    *out = ldexp(d, -(ex + fx));
+    const bool neg = r > (P >> 1);  // signed lift
+    const double d = u128_to_double(neg ? P - r : r);
+    *out = ldexp(neg ? -d : d, -(ex + fx));
+  }
   }
 }
 
@@ -417,7 +468,8 @@ size_t ozaki_workspace_bytes(int64_t m, int64_t n, int64_t k) {
   int s, t;
   ozaki_plan(k, &s, &t);
   const int64_t kpad = (k + 15) / 16 * 16;
-  return static_cast<size_t>(s) * (m * kpad + n * kpad + m * n) + sizeof(int) * (m + n) + 1024;
+  return static_cast<size_t>(s) * (m * kpad + n * kpad + m * n) + sizeof(int) * (m + n + 2) +
+         sizeof(unsigned long long) * n + 1024;
 }
 
 cudaError_t launch_dgemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K, const double* A,
@@ -438,10 +490,17 @@ cudaError_t launch_dgemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K,
   const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
   row_exponent_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, L.stream>>>(A, lda, m, k,
                                                                                       t, ex);
-  col_exponent_kernel<<<static_cast<unsigned>((N + 255) / 256), 256, 0, L.stream>>>(B, ldb, k, n, t,
-                                                                                   fx);
-  const unsigned grid_e = static_cast<unsigned>(std::min<int64_t>((M * kpad + 255) / 256, L.num_sms * 16));
-  residue_a_kernel<<<grid_e, 256, 0, L.stream>>>(A, lda, m, k, static_cast<int>(kpad), ex, ares);
+  unsigned long long* colmax = reinterpret_cast<unsigned long long*>(ex + ((M + N + 1) & ~int64_t(1)));
+  if ((e = cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * N, L.stream)) != cudaSuccess)
+    return e;
+  col_absmax_kernel<<<dim3(static_cast<unsigned>((N + 255) / 256),
+                           static_cast<unsigned>((K + OZ_COL_ROWS - 1) / OZ_COL_ROWS)),
+                      256, 0, L.stream>>>(B, ldb, k, n, colmax);
+  col_exponent_finalize<<<static_cast<unsigned>((N + 255) / 256), 256, 0, L.stream>>>(colmax, n, t,
+                                                                                      fx);
+  const unsigned rows_y = static_cast<unsigned>(std::min<int64_t>(M, 65535));
+  residue_a_kernel<<<dim3(static_cast<unsigned>((kpad / 8 + 127) / 128), rows_y),
+                     128, 0, L.stream>>>(A, lda, m, k, static_cast<int>(kpad), ex, ares);
   residue_bt_kernel<<<dim3(static_cast<unsigned>((N + 31) / 32), static_cast<unsigned>((kpad + 31) / 32)),
                       256, 0, L.stream>>>(B, ldb, k, n, static_cast<int>(kpad), fx, bres);
   CUtensorMap ta, tb;
@@ -454,15 +513,15 @@ cudaError_t launch_dgemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K,
   const int tiles_n = static_cast<int>((N + IG_BN - 1) / IG_BN);
   igemm_mod_kernel<<<dim3(tiles_m * tiles_n, 1, s), IG_THREADS, IG_SMEM, L.stream>>>(
       ta, tb, cres, m, n, static_cast<int>(kpad), tiles_m, tiles_n);
-  const unsigned grid_c = static_cast<unsigned>(std::min<int64_t>((M * N + 255) / 256, L.num_sms * 16));
-  crt_kernel<<<grid_c, 256, 0, L.stream>>>(cres, m, n, ex, fx, C, ldc);
-  for (int i = 0; i < 6; ++i) L.count();
+  crt_kernel<<<dim3(static_cast<unsigned>((N / 4 + 1 + 127) / 128), rows_y), 128, 0,
+               L.stream>>>(cres, m, n, ex, fx, C, ldc);
+  for (int i = 0; i < 7; ++i) L.count();
   return cudaGetLastError();
 }
 
 cudaError_t preload_ozaki() {
-  return preload_kernels(row_exponent_kernel, col_exponent_kernel, residue_a_kernel,
-                         residue_bt_kernel, igemm_mod_kernel, crt_kernel);
+  return preload_kernels(row_exponent_kernel, col_absmax_kernel, col_exponent_finalize,
+                         residue_a_kernel, residue_bt_kernel, igemm_mod_kernel, crt_kernel);
 }
 
 }  // namespace mmws_impl
