@@ -57,6 +57,9 @@ struct mmws_gpu_ctx {
   };
   std::vector<SkSpace> sk_spaces;
   bool allow_streamk = true;  // false while a row-block round overlaps NCCL with multiplies
+  // MODE_OZAKI: second stream for its tensor-core GEMMs + ordering events (lazy)
+  cudaStream_t oz_stream = nullptr;
+  cudaEvent_t oz_ev[8] = {};
   // host-entry staging buffers (device)
   void* dA = nullptr;
   void* dB = nullptr;

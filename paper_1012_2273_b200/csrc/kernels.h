@@ -43,12 +43,15 @@ struct DmmaStream {
   int* flags = nullptr;
 };
 // fp64 GEMM emulated on the int8 tensor cores (ozaki.cu): plan (moduli s,
-// integer bits t) for inner dimension k, workspace bytes, launch (6 kernels).
+// integer bits t) for inner dimension k, workspace bytes, launch.  `aux` is a
+// second stream for the tensor-core GEMMs and `ev` holds at least 5 events
+// (timing disabled); the result is ordered on L.stream.
+constexpr int OZAKI_EVENTS = 5;
 void ozaki_plan(int64_t k, int* s, int* t);
 size_t ozaki_workspace_bytes(int64_t m, int64_t n, int64_t k);
 cudaError_t launch_dgemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K, const double* A,
                                int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
-                               void* ws);
+                               void* ws, cudaStream_t aux, cudaEvent_t* ev);
 // Force-load kernels (cudaFuncGetAttributes).  Under CUDA_MODULE_LOADING=LAZY
 // the first launch of a kernel loads it with a context-wide synchronisation,
 // which would wait forever on the resident latency server (and costs tens of

@@ -171,7 +171,16 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
       return fail(MMWS_GPU_ERR_DIMENSION, "dgemm ozaki: k must be <= 131072 (int32 accumulation)");
     if ((e = ensure(ctx, &ctx->ws, &ctx->ws_bytes, ozaki_workspace_bytes(m, n, k))) != cudaSuccess)
       return cuda_fail(e, "dgemm ozaki workspace");
-    e = launch_dgemm_ozaki(L, m, n, k, A, lda, B, ldb, C, ldc, ctx->ws);
+    if (!ctx->oz_stream) {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      if ((e = cudaStreamCreateWithPriority(&ctx->oz_stream, cudaStreamNonBlocking, lo)) != cudaSuccess)
+        return cuda_fail(e, "dgemm ozaki stream");
+      for (int i = 0; i < OZAKI_EVENTS; ++i)
+        if ((e = cudaEventCreateWithFlags(&ctx->oz_ev[i], cudaEventDisableTiming)) != cudaSuccess)
+          return cuda_fail(e, "dgemm ozaki events");
+    }
+    e = launch_dgemm_ozaki(L, m, n, k, A, lda, B, ldb, C, ldc, ctx->ws, ctx->oz_stream, ctx->oz_ev);
     return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm ozaki");
   }
   if (mode != MMWS_GPU_MODE_AUTO && mode != MMWS_GPU_MODE_DMMA &&
@@ -375,6 +384,9 @@ int mmws_gpu_destroy(mmws_gpu_ctx* ctx) {
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
   if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
+  if (ctx->oz_stream) cudaStreamDestroy(ctx->oz_stream);
+  for (cudaEvent_t ev : ctx->oz_ev)
+    if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : ctx->pool) cudaEventDestroy(ev);
   delete ctx;
   return ok();

@@ -37,6 +37,7 @@ using namespace mmws_dev;
 
 constexpr int OZ_MAX_MODULI = 16;
 constexpr int OZ_NONFINITE = 1 << 20;  // exponent marker: row / column holds Inf or NaN
+constexpr int OZ_GROUPS = 4;           // moduli groups pipelined residues -> GEMMs
 
 // pairwise-coprime moduli, largest first (log2 of the product: 8, 16, 24, ...)
 constexpr int kModuli[OZ_MAX_MODULI] = {256, 255, 253, 251, 247, 241, 239, 233,
@@ -132,7 +133,8 @@ MMWS_DEVICE double scaled_int(double v, int ex) {
 // residues of A' = rint(A 2^e): res[l][i][j], j < kpad (zero padding).
 // A thread takes 8 consecutive j and stores one 8-byte word per modulus.
 __global__ void residue_a_kernel(const double* __restrict__ A, int64_t lda, int m, int k, int kpad,
-                                 const int* __restrict__ e, int8_t* __restrict__ res) {
+                                 const int* __restrict__ e, int8_t* __restrict__ res, int l0,
+                                 int l1) {
   const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (j0 >= kpad) return;
   for (int i = blockIdx.y; i < m; i += gridDim.y) {
@@ -143,8 +145,7 @@ __global__ void residue_a_kernel(const double* __restrict__ A, int64_t lda, int 
   for (int q = 0; q < 8; ++q) x[q] = j0 + q < k ? scaled_int(row[j0 + q], ex) : 0.0;
   const int64_t plane = static_cast<int64_t>(m) * kpad;
   const int64_t o = static_cast<int64_t>(i) * kpad + j0;
-  const int s = c_crt.s;
-  for (int l = 0; l < s; ++l) {
+  for (int l = l0; l < l1; ++l) {
     const int p = c_crt.p[l];
     unsigned long long w = 0;
 #pragma unroll
@@ -159,7 +160,8 @@ __global__ void residue_a_kernel(const double* __restrict__ A, int64_t lda, int 
 // r < kpad; 32 x 32 tiles through shared memory, each thread then packs 4
 // consecutive r of one column into a 4-byte word per modulus
 __global__ void residue_bt_kernel(const double* __restrict__ B, int64_t ldb, int k, int n, int kpad,
-                                  const int* __restrict__ f, int8_t* __restrict__ res) {
+                                  const int* __restrict__ f, int8_t* __restrict__ res, int l0,
+                                  int l1) {
   __shared__ double tile[32][33];
   const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
@@ -172,8 +174,7 @@ __global__ void residue_bt_kernel(const double* __restrict__ B, int64_t ldb, int
   if (c >= n || rq >= kpad) return;
   const int64_t plane = static_cast<int64_t>(n) * kpad;
   const int64_t o = static_cast<int64_t>(c) * kpad + rq;
-  const int s = c_crt.s;
-  for (int l = 0; l < s; ++l) {
+  for (int l = l0; l < l1; ++l) {
     const int p = c_crt.p[l];
     uint32_t w = 0;
 #pragma unroll
@@ -230,7 +231,8 @@ MMWS_DEVICE void umma_commit(uint64_t* bar) {
 
 __global__ void __launch_bounds__(IG_THREADS, 1)
     igemm_mod_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     uint8_t* __restrict__ C, int m, int n, int kpad, int tiles_m, int tiles_n) {
+                     uint8_t* __restrict__ C, int m, int n, int kpad, int tiles_m, int tiles_n,
+                     int z0) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + IG_STAGES * IG_STAGE);
@@ -246,7 +248,7 @@ __global__ void __launch_bounds__(IG_THREADS, 1)
   const int first_m = (tile / per_group) * GROUP;
   const int gm = min(tiles_m - first_m, GROUP);
   const int tm = first_m + (tile % per_group) % gm, tn = (tile % per_group) / gm;
-  const int z = blockIdx.z;
+  const int z = z0 + blockIdx.z;
   const int KB = (kpad + IG_BK - 1) / IG_BK;
 
   if (threadIdx.x == 0) {
@@ -474,7 +476,7 @@ size_t ozaki_workspace_bytes(int64_t m, int64_t n, int64_t k) {
 
 cudaError_t launch_dgemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K, const double* A,
                                int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
-                               void* ws) {
+                               void* ws, cudaStream_t aux, cudaEvent_t* ev) {
   int s, t;
   ozaki_plan(K, &s, &t);
   CrtConst cc;
@@ -487,22 +489,16 @@ cudaError_t launch_dgemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K,
   uint8_t* cres = reinterpret_cast<uint8_t*>(bres + s * N * kpad);
   int* ex = reinterpret_cast<int*>(reinterpret_cast<uintptr_t>(cres + s * M * N + 15) & ~uintptr_t(15));
   int* fx = ex + M;
-  const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
-  row_exponent_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, L.stream>>>(A, lda, m, k,
-                                                                                      t, ex);
   unsigned long long* colmax = reinterpret_cast<unsigned long long*>(ex + ((M + N + 1) & ~int64_t(1)));
-  if ((e = cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * N, L.stream)) != cudaSuccess)
-    return e;
+  const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
+  cudaStream_t st = L.stream;
+  // ---- scaling exponents
+  row_exponent_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(A, lda, m, k, t, ex);
+  if ((e = cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * N, st)) != cudaSuccess) return e;
   col_absmax_kernel<<<dim3(static_cast<unsigned>((N + 255) / 256),
                            static_cast<unsigned>((K + OZ_COL_ROWS - 1) / OZ_COL_ROWS)),
-                      256, 0, L.stream>>>(B, ldb, k, n, colmax);
-  col_exponent_finalize<<<static_cast<unsigned>((N + 255) / 256), 256, 0, L.stream>>>(colmax, n, t,
-                                                                                      fx);
-  const unsigned rows_y = static_cast<unsigned>(std::min<int64_t>(M, 65535));
-  residue_a_kernel<<<dim3(static_cast<unsigned>((kpad / 8 + 127) / 128), rows_y),
-                     128, 0, L.stream>>>(A, lda, m, k, static_cast<int>(kpad), ex, ares);
-  residue_bt_kernel<<<dim3(static_cast<unsigned>((N + 31) / 32), static_cast<unsigned>((kpad + 31) / 32)),
-                      256, 0, L.stream>>>(B, ldb, k, n, static_cast<int>(kpad), fx, bres);
+                      256, 0, st>>>(B, ldb, k, n, colmax);
+  col_exponent_finalize<<<static_cast<unsigned>((N + 255) / 256), 256, 0, st>>>(colmax, n, t, fx);
   CUtensorMap ta, tb;
   if (!map3_u8(L, &ta, ares, kpad, M, s, IG_BM) || !map3_u8(L, &tb, bres, kpad, N, s, IG_BN))
     return cudaErrorInvalidValue;
@@ -511,11 +507,35 @@ cudaError_t launch_dgemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K,
     return e;
   const int tiles_m = static_cast<int>((M + IG_BM - 1) / IG_BM);
   const int tiles_n = static_cast<int>((N + IG_BN - 1) / IG_BN);
-  igemm_mod_kernel<<<dim3(tiles_m * tiles_n, 1, s), IG_THREADS, IG_SMEM, L.stream>>>(
-      ta, tb, cres, m, n, static_cast<int>(kpad), tiles_m, tiles_n);
-  crt_kernel<<<dim3(static_cast<unsigned>((N / 4 + 1 + 127) / 128), rows_y), 128, 0,
-               L.stream>>>(cres, m, n, ex, fx, C, ldc);
-  for (int i = 0; i < 7; ++i) L.count();
+  const unsigned rows_y = static_cast<unsigned>(std::min<int64_t>(M, 65535));
+  // ---- residues and tensor-core GEMMs in moduli groups: the (FP64-ALU bound)
+  // residues of group g+1 run on `st` while the int8 GEMMs of group g run on
+  // `aux`, their blocks sharing the SMs.  Measured: N=4096 3.0 -> 2.0 ms with 4
+  // groups; from N ~ 8192 up the GEMMs fill the SMs and the extra passes over
+  // A and B cost more than the overlap saves (N=16384: 64.5 vs 66.9 ms), so
+  // large problems take one group.
+  const double work = static_cast<double>(M) * N * K;
+  const int groups = work <= 1.4e11 ? std::min(s, OZ_GROUPS) : 1;
+  for (int g = 0; g < groups; ++g) {
+    const int l0 = s * g / groups, l1 = s * (g + 1) / groups;
+    residue_a_kernel<<<dim3(static_cast<unsigned>((kpad / 8 + 127) / 128), rows_y), 128, 0, st>>>(
+        A, lda, m, k, static_cast<int>(kpad), ex, ares, l0, l1);
+    residue_bt_kernel<<<dim3(static_cast<unsigned>((N + 31) / 32),
+                             static_cast<unsigned>((kpad + 31) / 32)),
+                        256, 0, st>>>(B, ldb, k, n, static_cast<int>(kpad), fx, bres, l0, l1);
+    if ((e = cudaEventRecord(ev[g], st)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(aux, ev[g], 0)) != cudaSuccess)
+      return e;
+    igemm_mod_kernel<<<dim3(tiles_m * tiles_n, 1, l1 - l0), IG_THREADS, IG_SMEM, aux>>>(
+        ta, tb, cres, m, n, static_cast<int>(kpad), tiles_m, tiles_n, l0);
+  }
+  // ---- reconstruction after the last GEMM
+  if ((e = cudaEventRecord(ev[groups], aux)) != cudaSuccess ||
+      (e = cudaStreamWaitEvent(st, ev[groups], 0)) != cudaSuccess)
+    return e;
+  crt_kernel<<<dim3(static_cast<unsigned>((N / 4 + 1 + 127) / 128), rows_y), 128, 0, st>>>(
+      cres, m, n, ex, fx, C, ldc);
+  for (int i = 0; i < 4 + 3 * groups; ++i) L.count();
   return cudaGetLastError();
 }
 
