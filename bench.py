@@ -197,7 +197,8 @@ def run_ours(args) -> None:
     ctx = P.Context(local)
     if world > 1:
         P.bootstrap_comm(ctx)
-    mode = {"auto": P.MODE_AUTO, "dmma": P.MODE_DMMA, "exact": P.MODE_EXACT}[args.mode]
+    mode = {"auto": P.MODE_AUTO, "dmma": P.MODE_DMMA, "exact": P.MODE_EXACT,
+            "ozaki": P.MODE_OZAKI}[args.mode]
     n = args.n
     root = rank == 0
 
@@ -260,6 +261,37 @@ def run_ours(args) -> None:
     achieved = 2.0 * rows0 * n * n / (kern_avg_ms / 1e3) / 1e12
     traffic, traffic_src = profiled_traffic(n) if world == 1 else (None, None)
 
+    # The same multiply emulated on the int8 tensor cores (MODE_OZAKI, opt-in;
+    # the headline above stays on the FP64 tensor path): device-resident, CUDA
+    # events, plus its normwise difference from the DMMA product of this run.
+    emulated = None
+    if root and world == 1 and not args.no_emulated:
+        C_oz = torch.empty_like(C)
+        ctx.dgemm(A, B, C_oz, mode=P.MODE_OZAKI)
+        torch.cuda.synchronize()
+        oz_steps = max(3, min(args.steps, 5))
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(oz_steps):
+            ctx.dgemm(A, B, C_oz, mode=P.MODE_OZAKI)
+        f1.record()
+        torch.cuda.synchronize()
+        oz_ms = f0.elapsed_time(f1) / oz_steps
+        diff = float(torch.linalg.norm(C_oz - C) / torch.linalg.norm(C))
+        moduli, _bits = P.ozaki_plan(n)
+        emulated = {
+            "mode": f"ozaki (fp64 emulated exactly on int8 tcgen05 tensor cores, CRT over {moduli} moduli, {_bits}-bit scaling)",
+            "value": flops / (oz_ms / 1e3) / 1e9, "unit": "GFLOP/s", "ms_per_step": oz_ms,
+            "steps": oz_steps, "int8_gemms": moduli,
+            "int8_tops_equivalent": moduli * flops / (oz_ms / 1e3) / 1e12,
+            "int8_tensor_peak_nominal_tops": 4500.0,
+            "normwise_diff_vs_dmma": diff,
+            "note": "opt-in MMWS_GPU_MODE_OZAKI; error ~1e-14 vs the fp64 oracle (tests), "
+                    "integer inputs bit-exact",
+        }
+        del C_oz
+
     # e2e: the public host-buffer entry (master_run with host matrices): H2D of
     # A and B, the round, D2H of C inside the bracket, pinned host buffers.
     e2e_steps = max(2, min(args.steps, 4))
@@ -318,6 +350,7 @@ def run_ours(args) -> None:
                     "entry": "mmws_gpu_master_run_host (C ABI, pinned host A/B/C)"},
             "gpu_launches": launches_total,
             "cost_model": model,
+            "emulated_fp64": emulated,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
@@ -333,7 +366,9 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=16384)
-    ap.add_argument("--mode", choices=["auto", "dmma", "exact"], default="auto")
+    ap.add_argument("--mode", choices=["auto", "dmma", "exact", "ozaki"], default="auto")
+    ap.add_argument("--no-emulated", action="store_true",
+                    help="skip the MODE_OZAKI measurement added to the JSON line")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 0 or args.steps < 1:

@@ -142,6 +142,11 @@ int mmws_gpu_sgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const flo
                    int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int mode,
                    void* stream);
 
+/* MMWS_GPU_MODE_OZAKI plan for inner dimension k: number of int8 tensor-core
+ * GEMMs (moduli) and the integer bits each row of A / column of B is scaled to
+ * (normwise error ~1.4 * 2^-bits for random inputs).  Host-only. */
+int mmws_gpu_ozaki_plan(int64_t k, int* moduli, int* bits);
+
 /* ---------------------------------------------------------------- multiply, host buffers */
 /* The matmul_seq / matmul_threads replacement for host data: dense row-major
  * A (m x k), B (k x n) in, C (m x n) out.  Copies in, multiplies, copies out

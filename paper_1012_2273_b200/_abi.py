@@ -48,6 +48,7 @@ SIGNATURES = {
     "mmws_gpu_synchronize": (_i, [_v]),
     "mmws_gpu_ipc_export": (_i, [_v, _v, _p(C.c_uint8)]),
     "mmws_gpu_ipc_open": (_i, [_v, _p(C.c_uint8), _p(_v)]),
+    "mmws_gpu_ozaki_plan": (_i, [_i64, _p(_i), _p(_i)]),
     "mmws_gpu_peak_probe": (_i, [_v, _i, _i, _p(_d)]),
     "mmws_gpu_gemm_probe": (_i, [_v, _i64, _i, _i, _p(_d)]),
     "mmws_gpu_link_probe": (_i, [_v, _i64, _i, _p(_d)]),

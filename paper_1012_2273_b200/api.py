@@ -112,6 +112,13 @@ def rowblock_cost(m: int, n: int, k: int, nranks: int, elem_bytes: int = 8,
     return t.value, eg.value, ing.value
 
 
+def ozaki_plan(k: int):
+    """MODE_OZAKI plan for inner dimension k: (int8 GEMMs, integer bits)."""
+    s, t = C.c_int(), C.c_int()
+    _check(_lib().mmws_gpu_ozaki_plan(k, C.byref(s), C.byref(t)))
+    return s.value, t.value
+
+
 def nccl_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     _check(_lib().mmws_gpu_nccl_unique_id(buf))

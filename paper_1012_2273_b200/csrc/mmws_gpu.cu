@@ -464,6 +464,13 @@ int mmws_gpu_sgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const flo
                         static_cast<cudaStream_t>(stream));
 }
 
+int mmws_gpu_ozaki_plan(int64_t k, int* moduli, int* bits) {
+  if (k < 1 || k > 131072 || !moduli || !bits)
+    return fail(MMWS_GPU_ERR_DOMAIN, "ozaki_plan: k must be in [1, 131072], outputs non-null");
+  ozaki_plan(k, moduli, bits);
+  return ok();
+}
+
 int mmws_gpu_matmul_host(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
                          const double* B, double* C, int mode, double* elapsed_s) {
   MMWS_CTX_GUARD(ctx);
