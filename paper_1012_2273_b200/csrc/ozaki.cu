@@ -185,16 +185,17 @@ __global__ void residue_bt_kernel(const double* __restrict__ B, int64_t ldb, int
 }
 
 // ---------------------------------------------------------------- int8 tensor-core GEMM
-// C_l = (A_l B_l^T) mod p_l for every modulus l (grid.z), A_l: m x kpad,
-// B_l: n x kpad (both K-major int8), C_l: m x n uint8.  128 x 256 CTA tile,
+// C_l = (A_l B_l^T) mod p_l for every modulus l, A_l: m x kpad, B_l: n x
+// kpad (both K-major int8), C_l: m x n uint8.  128 x 256 tiles,
 // tcgen05.mma.kind::i8 (M=128, N=256, K=32) issued by one thread, operands
-// TMA-staged (128-byte swizzle, 4-stage ring), int32 accumulator in TMEM
-// (256 columns), epilogue tcgen05.ld -> mod p -> 16-byte stores.
-constexpr int IG_BM = 128, IG_BN = 256, IG_BK = 128, IG_STAGES = 4, IG_THREADS = 128;
+// TMA-staged (128-byte swizzle, 4-stage ring), int32 accumulators in TMEM,
+// epilogue tcgen05.ld -> mod p -> 16-byte stores.
+constexpr int IG_BM = 128, IG_BN = 256, IG_BK = 128, IG_STAGES = 4;
+constexpr int IG_EPI_WARPS = 4, IG_THREADS = (2 + IG_EPI_WARPS) * 32;
 constexpr int IG_A_BYTES = IG_BM * IG_BK, IG_B_BYTES = IG_BN * IG_BK;
 constexpr int IG_STAGE = IG_A_BYTES + IG_B_BYTES;
 constexpr int IG_SMEM = IG_STAGES * IG_STAGE + 1024 + 256;
-constexpr uint32_t IG_TMEM_COLS = 256;
+constexpr uint32_t IG_TMEM_COLS = 512;  // two 256-column accumulators
 // instruction descriptor: s32 accumulate, s8 x s8, K-major A and B, N = 256, M = 128
 constexpr uint32_t IG_IDESC =
     (2u << 4) | (1u << 7) | (1u << 10) | ((IG_BN >> 3) << 17) | ((IG_BM >> 4) << 24);
@@ -229,34 +230,47 @@ MMWS_DEVICE void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// Persistent: one CTA per SM walks work items (modulus z, tile) z-major, with
+// grouped rasterisation inside a modulus.  Warp 0 = TMA producer, warp 1 =
+// MMA issuer, warps 2..5 = epilogue (TMEM lane quarter = warp % 4).  Two
+// 256-column TMEM accumulators: the MMAs of item i+1 run while the epilogue
+// drains item i (tmem_full / tmem_empty mbarriers).
 __global__ void __launch_bounds__(IG_THREADS, 1)
     igemm_mod_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      uint8_t* __restrict__ C, int m, int n, int kpad, int tiles_m, int tiles_n,
-                     int z0) {
+                     int z0, int nz) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + IG_STAGES * IG_STAGE);
   uint64_t* empty = full + IG_STAGES;
-  uint64_t* tmem_full = empty + IG_STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tmem_full = empty + IG_STAGES;  // [2]
+  uint64_t* tmem_empty = tmem_full + 2;     // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // grouped rasterisation (8 tile rows): neighbouring CTAs share A and B panels in L2
-  constexpr int GROUP = 8;
-  const int tile = blockIdx.x;
-  const int per_group = GROUP * tiles_n;
-  const int first_m = (tile / per_group) * GROUP;
-  const int gm = min(tiles_m - first_m, GROUP);
-  const int tm = first_m + (tile % per_group) % gm, tn = (tile % per_group) / gm;
-  const int z = z0 + blockIdx.z;
   const int KB = (kpad + IG_BK - 1) / IG_BK;
+  const int tiles = tiles_m * tiles_n;
+  const int items = tiles * nz;
+  auto item_at = [&](int w, int& z, int& tm, int& tn) {
+    z = z0 + w / tiles;
+    const int tile = w % tiles;
+    constexpr int GROUP = 8;  // 8 tile rows advance together (A/B panels shared in L2)
+    const int per_group = GROUP * tiles_n;
+    const int first_m = (tile / per_group) * GROUP;
+    const int gm = min(tiles_m - first_m, GROUP);
+    tm = first_m + (tile % per_group) % gm;
+    tn = (tile % per_group) / gm;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < IG_STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tmem_full[b], 1);
+      mbar_init(&tmem_empty[b], IG_EPI_WARPS);
+    }
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -270,75 +284,101 @@ __global__ void __launch_bounds__(IG_THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {  // TMA producer
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
-    for (int kb = 0; kb < KB; ++kb) {
-      const int s = kb % IG_STAGES;
-      if (kb >= IG_STAGES) mbar_wait(&empty[s], ((kb / IG_STAGES) - 1) & 1);
-      uint8_t* sa = smem + s * IG_STAGE;
-      mbar_arrive_expect_tx(&full[s], IG_STAGE);
-      tma_load_3d(sa, &tmA, &full[s], kb * IG_BK, tm * IG_BM, z);
-      tma_load_3d(sa + IG_A_BYTES, &tmB, &full[s], kb * IG_BK, tn * IG_BN, z);
-    }
-  } else if (warp == 1 && lane == 0) {  // MMA issuer
-    for (int kb = 0; kb < KB; ++kb) {
-      const int s = kb % IG_STAGES;
-      mbar_wait(&full[s], (kb / IG_STAGES) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t sa = smem_u32(smem + s * IG_STAGE), sb = sa + IG_A_BYTES;
-#pragma unroll
-      for (int kk = 0; kk < IG_BK / 32; ++kk)  // K = 32 bytes per MMA, inside the swizzle row
-        umma_i8(tmem, umma_desc(sa + kk * 32), umma_desc(sb + kk * 32), (kb | kk) != 0);
-      umma_commit(&empty[s]);  // the stage is free once these MMAs have read it
-    }
-    umma_commit(tmem_full);
-  }
-  __syncwarp();
-
-  // epilogue: warp w reads TMEM lanes 32w..32w+31 (= tile rows), 32 columns at a time
-  mbar_wait(tmem_full, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const int row = tm * IG_BM + warp * 32 + lane;
-  const int p = c_crt.p[z];
-  uint8_t* crow = C + (static_cast<size_t>(z) * m + row) * n;
-#pragma unroll 1
-  for (int c0 = 0; c0 < IG_BN; c0 += 32) {
-    uint32_t v[32];
-    const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0;
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
-        "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
-        "%28, %29, %30, %31}, [%32];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
-          "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
-          "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;");
-    const int col = tn * IG_BN + c0;
-    if (row >= m || col >= n) continue;
-    uint32_t packed[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      uint32_t word = 0;
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int x = static_cast<int>(v[4 * q + b]);
-        int r = x % p;  // C mod p in [0, p)
-        r += r < 0 ? p : 0;
-        word |= static_cast<uint32_t>(r) << (8 * b);
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+      int kg = 0;  // stage counter across items
+      for (int w = blockIdx.x; w < items; w += gridDim.x) {
+        int z, tm, tn;
+        item_at(w, z, tm, tn);
+        for (int kb = 0; kb < KB; ++kb, ++kg) {
+          const int s = kg % IG_STAGES;
+          if (kg >= IG_STAGES) mbar_wait(&empty[s], ((kg / IG_STAGES) - 1) & 1);
+          uint8_t* sa = smem + s * IG_STAGE;
+          mbar_arrive_expect_tx(&full[s], IG_STAGE);
+          tma_load_3d(sa, &tmA, &full[s], kb * IG_BK, tm * IG_BM, z);
+          tma_load_3d(sa + IG_A_BYTES, &tmB, &full[s], kb * IG_BK, tn * IG_BN, z);
+        }
       }
-      packed[q] = word;
     }
-    if (col + 32 <= n && (n % 16) == 0) {
-      uint4* dst = reinterpret_cast<uint4*>(crow + col);
-      dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-      dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
-    } else {
-      const uint8_t* bytes = reinterpret_cast<const uint8_t*>(packed);
-      for (int j = 0; j < 32 && col + j < n; ++j) crow[col + j] = bytes[j];
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      int kg = 0, it = 0;
+      for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
+        const int b = it & 1;
+        mbar_wait(&tmem_empty[b], ((it >> 1) & 1) ^ 1);  // epilogue has drained buffer b
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t acc = tmem + b * IG_BN;
+        for (int kb = 0; kb < KB; ++kb, ++kg) {
+          const int s = kg % IG_STAGES;
+          mbar_wait(&full[s], (kg / IG_STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t sa = smem_u32(smem + s * IG_STAGE), sb = sa + IG_A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < IG_BK / 32; ++kk)  // K = 32 bytes per MMA, inside the swizzle row
+            umma_i8(acc, umma_desc(sa + kk * 32), umma_desc(sb + kk * 32), (kb | kk) != 0);
+          umma_commit(&empty[s]);  // the stage is free once these MMAs have read it
+        }
+        umma_commit(&tmem_full[b]);
+      }
+    }
+  } else {  // epilogue warps 2..5: TMEM lanes 32*(warp%4) .. +31 = tile rows
+    const int quarter = warp & 3;
+    int it = 0;
+    for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
+      int z, tm, tn;
+      item_at(w, z, tm, tn);
+      const int b = it & 1;
+      mbar_wait(&tmem_full[b], (it >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const int row = tm * IG_BM + quarter * 32 + lane;
+      const int p = c_crt.p[z];
+      uint8_t* crow = C + (static_cast<size_t>(z) * m + row) * n;
+#pragma unroll 1
+      for (int c0 = 0; c0 < IG_BN; c0 += 32) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + b * IG_BN + c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+            "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+            "%28, %29, %30, %31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+              "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+              "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+              "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+              "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        if (c0 + 32 == IG_BN) {  // last read of buffer b: hand it back to the MMA issuer
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tmem_empty[b]);
+        }
+        const int col = tn * IG_BN + c0;
+        if (row >= m || col >= n) continue;
+        uint32_t packed[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          uint32_t word = 0;
+#pragma unroll
+          for (int bb = 0; bb < 4; ++bb) {
+            int r = static_cast<int>(v[4 * q + bb]) % p;  // C mod p in [0, p)
+            r += r < 0 ? p : 0;
+            word |= static_cast<uint32_t>(r) << (8 * bb);
+          }
+          packed[q] = word;
+        }
+        if (col + 32 <= n && (n % 16) == 0) {
+          uint4* dst = reinterpret_cast<uint4*>(crow + col);
+          dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+          dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+        } else {
+          const uint8_t* bytes = reinterpret_cast<const uint8_t*>(packed);
+          for (int j = 0; j < 32 && col + j < n; ++j) crow[col + j] = bytes[j];
+        }
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -526,8 +566,10 @@ cudaError_t launch_dgemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K,
     if ((e = cudaEventRecord(ev[g], st)) != cudaSuccess ||
         (e = cudaStreamWaitEvent(aux, ev[g], 0)) != cudaSuccess)
       return e;
-    igemm_mod_kernel<<<dim3(tiles_m * tiles_n, 1, l1 - l0), IG_THREADS, IG_SMEM, aux>>>(
-        ta, tb, cres, m, n, static_cast<int>(kpad), tiles_m, tiles_n, l0);
+    const int grid = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(tiles_m) * tiles_n * (l1 - l0),
+                                                        L.num_sms));
+    igemm_mod_kernel<<<grid, IG_THREADS, IG_SMEM, aux>>>(ta, tb, cres, m, n, static_cast<int>(kpad),
+                                                         tiles_m, tiles_n, l0, l1 - l0);
   }
   // ---- reconstruction after the last GEMM
   if ((e = cudaEventRecord(ev[groups], aux)) != cudaSuccess ||
