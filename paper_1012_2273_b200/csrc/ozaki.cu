@@ -190,15 +190,20 @@ __global__ void residue_bt_kernel(const double* __restrict__ B, int64_t ldb, int
 // tcgen05.mma.kind::i8 (M=128, N=256, K=32) issued by one thread, operands
 // TMA-staged (128-byte swizzle, 4-stage ring), int32 accumulators in TMEM,
 // epilogue tcgen05.ld -> mod p -> 16-byte stores.
-constexpr int IG_BM = 128, IG_BN = 256, IG_BK = 128, IG_STAGES = 4;
+// 256 x 256 tiles: two M=128 MMAs per k-step share the B operand, so a CTA
+// moves 64 KB per 128-byte k-block for 256x256 outputs (48 KB for 128x256
+// with M=128 tiles): the L2 -> SM operand stream is what limits this kernel.
+constexpr int IG_BM = 256, IG_BN = 256, IG_BK = 128, IG_STAGES = 3;
+constexpr int IG_HALVES = IG_BM / 128;                 // M=128 MMAs per k-step
+constexpr int IG_NBUF = 512 / (IG_HALVES * IG_BN);    // TMEM accumulator buffers
 constexpr int IG_EPI_WARPS = 4, IG_THREADS = (2 + IG_EPI_WARPS) * 32;
 constexpr int IG_A_BYTES = IG_BM * IG_BK, IG_B_BYTES = IG_BN * IG_BK;
 constexpr int IG_STAGE = IG_A_BYTES + IG_B_BYTES;
 constexpr int IG_SMEM = IG_STAGES * IG_STAGE + 1024 + 256;
-constexpr uint32_t IG_TMEM_COLS = 512;  // two 256-column accumulators
+constexpr uint32_t IG_TMEM_COLS = 512;  // all of TMEM: IG_NBUF x IG_HALVES x 256 columns
 // instruction descriptor: s32 accumulate, s8 x s8, K-major A and B, N = 256, M = 128
 constexpr uint32_t IG_IDESC =
-    (2u << 4) | (1u << 7) | (1u << 10) | ((IG_BN >> 3) << 17) | ((IG_BM >> 4) << 24);
+    (2u << 4) | (1u << 7) | (1u << 10) | ((IG_BN >> 3) << 17) | ((128 >> 4) << 24);
 
 MMWS_DEVICE void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
                              int c2) {
@@ -243,9 +248,9 @@ __global__ void __launch_bounds__(IG_THREADS, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + IG_STAGES * IG_STAGE);
   uint64_t* empty = full + IG_STAGES;
-  uint64_t* tmem_full = empty + IG_STAGES;  // [2]
-  uint64_t* tmem_empty = tmem_full + 2;     // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  uint64_t* tmem_full = empty + IG_STAGES;       // [IG_NBUF]
+  uint64_t* tmem_empty = tmem_full + IG_NBUF;   // [IG_NBUF]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + IG_NBUF);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KB = (kpad + IG_BK - 1) / IG_BK;
@@ -267,7 +272,7 @@ __global__ void __launch_bounds__(IG_THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < IG_NBUF; ++b) {
       mbar_init(&tmem_full[b], 1);
       mbar_init(&tmem_empty[b], IG_EPI_WARPS);
     }
@@ -306,10 +311,10 @@ __global__ void __launch_bounds__(IG_THREADS, 1)
     if (lane == 0) {  // MMA issuer
       int kg = 0, it = 0;
       for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
-        const int b = it & 1;
-        mbar_wait(&tmem_empty[b], ((it >> 1) & 1) ^ 1);  // epilogue has drained buffer b
+        const int b = it % IG_NBUF, use = it / IG_NBUF;
+        mbar_wait(&tmem_empty[b], (use & 1) ^ 1);  // epilogue has drained buffer b
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t acc = tmem + b * IG_BN;
+        const uint32_t acc = tmem + b * IG_HALVES * IG_BN;
         for (int kb = 0; kb < KB; ++kb, ++kg) {
           const int s = kg % IG_STAGES;
           mbar_wait(&full[s], (kg / IG_STAGES) & 1);
@@ -317,7 +322,10 @@ __global__ void __launch_bounds__(IG_THREADS, 1)
           const uint32_t sa = smem_u32(smem + s * IG_STAGE), sb = sa + IG_A_BYTES;
 #pragma unroll
           for (int kk = 0; kk < IG_BK / 32; ++kk)  // K = 32 bytes per MMA, inside the swizzle row
-            umma_i8(acc, umma_desc(sa + kk * 32), umma_desc(sb + kk * 32), (kb | kk) != 0);
+#pragma unroll
+            for (int h = 0; h < IG_HALVES; ++h)    // rows 128h.., accumulator columns 256h..
+              umma_i8(acc + h * IG_BN, umma_desc(sa + h * 128 * IG_BK + kk * 32),
+                      umma_desc(sb + kk * 32), (kb | kk) != 0);
           umma_commit(&empty[s]);  // the stage is free once these MMAs have read it
         }
         umma_commit(&tmem_full[b]);
@@ -329,16 +337,19 @@ __global__ void __launch_bounds__(IG_THREADS, 1)
     for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
       int z, tm, tn;
       item_at(w, z, tm, tn);
-      const int b = it & 1;
-      mbar_wait(&tmem_full[b], (it >> 1) & 1);
+      const int b = it % IG_NBUF, use = it / IG_NBUF;
+      mbar_wait(&tmem_full[b], use & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const int row = tm * IG_BM + quarter * 32 + lane;
       const int p = c_crt.p[z];
+#pragma unroll 1
+      for (int h = 0; h < IG_HALVES; ++h) {
+      const int row = tm * IG_BM + h * 128 + quarter * 32 + lane;
       uint8_t* crow = C + (static_cast<size_t>(z) * m + row) * n;
 #pragma unroll 1
       for (int c0 = 0; c0 < IG_BN; c0 += 32) {
         uint32_t v[32];
-        const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + b * IG_BN + c0;
+        const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16) +
+                               (b * IG_HALVES + h) * IG_BN + c0;
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
             "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
@@ -351,7 +362,7 @@ __global__ void __launch_bounds__(IG_THREADS, 1)
               "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;");
-        if (c0 + 32 == IG_BN) {  // last read of buffer b: hand it back to the MMA issuer
+        if (h + 1 == IG_HALVES && c0 + 32 == IG_BN) {  // last read of buffer b: hand it back
           asm volatile("tcgen05.fence::before_thread_sync;");
           __syncwarp();
           if (lane == 0) mbar_arrive(&tmem_empty[b]);
@@ -378,6 +389,7 @@ __global__ void __launch_bounds__(IG_THREADS, 1)
           const uint8_t* bytes = reinterpret_cast<const uint8_t*>(packed);
           for (int j = 0; j < 32 && col + j < n; ++j) crow[col + j] = bytes[j];
         }
+      }
       }
     }
   }
