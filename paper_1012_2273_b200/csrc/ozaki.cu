@@ -49,7 +49,7 @@ struct CrtConst {
   uint64_t m_lo[OZ_MAX_MODULI];  // P / p_l, 128-bit
   uint64_t m_hi[OZ_MAX_MODULI];
   uint64_t P_lo, P_hi;
-  double P_d;
+  double P_d, inv_P;
   int s;
 };
 __constant__ CrtConst c_crt;
@@ -157,30 +157,41 @@ __global__ void residue_a_kernel(const double* __restrict__ A, int64_t lda, int 
 }
 
 // residues of B' = rint(B 2^f) transposed (K-major operand): res[l][j][r],
-// r < kpad; 32 x 32 tiles through shared memory, each thread then packs 4
-// consecutive r of one column into a 4-byte word per modulus
-__global__ void residue_bt_kernel(const double* __restrict__ B, int64_t ldb, int k, int n, int kpad,
-                                  const int* __restrict__ f, int8_t* __restrict__ res, int l0,
-                                  int l1) {
-  __shared__ double tile[32][33];
-  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  for (int i = ty; i < 32; i += 8) {
-    const int r = r0 + i, c = c0 + tx;
-    tile[i][tx] = (r < k && c < n) ? scaled_int(B[static_cast<int64_t>(r) * ldb + c], f[c]) : 0.0;
+// r < kpad.  A block stages a 64 (k) x 32 (column) tile of scaled B through
+// shared memory; thread t then owns column t/8 and 8 consecutive k, so each
+// 8-thread group writes 64 contiguous bytes of one output row per modulus.
+constexpr int OZ_BT_K = 64;
+__global__ void __launch_bounds__(256) residue_bt_kernel(const double* __restrict__ B, int64_t ldb,
+                                                         int k, int n, int kpad,
+                                                         const int* __restrict__ f,
+                                                         int8_t* __restrict__ res, int l0, int l1) {
+  __shared__ double tile[OZ_BT_K][33];
+  const int r0 = blockIdx.y * OZ_BT_K, c0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // load phase: 32 x 8
+  {
+    const int c = c0 + tx;
+    const int fc = c < n ? f[c] : 0;
+    for (int i = ty; i < OZ_BT_K; i += 8) {
+      const int r = r0 + i;
+      tile[i][tx] = (r < k && c < n) ? scaled_int(B[static_cast<int64_t>(r) * ldb + c], fc) : 0.0;
+    }
   }
   __syncthreads();
-  const int c = c0 + tx, rq = r0 + ty * 4;  // column c, rows rq .. rq+3
+  const int col = threadIdx.x >> 3, kq = (threadIdx.x & 7) * 8;  // store phase
+  const int c = c0 + col, rq = r0 + kq;
   if (c >= n || rq >= kpad) return;
+  double x[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) x[q] = tile[kq + q][col];
   const int64_t plane = static_cast<int64_t>(n) * kpad;
   const int64_t o = static_cast<int64_t>(c) * kpad + rq;
   for (int l = l0; l < l1; ++l) {
     const int p = c_crt.p[l];
-    uint32_t w = 0;
+    unsigned long long w = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      w |= static_cast<uint32_t>(static_cast<uint8_t>(sresidue(tile[ty * 4 + q][tx], p))) << (8 * q);
-    *reinterpret_cast<uint32_t*>(res + l * plane + o) = w;
+    for (int q = 0; q < 8; ++q)
+      w |= static_cast<unsigned long long>(static_cast<uint8_t>(sresidue(x[q], p))) << (8 * q);
+    *reinterpret_cast<unsigned long long*>(res + l * plane + o) = w;
   }
 }
 
@@ -421,7 +432,9 @@ __global__ void crt_kernel(const uint8_t* __restrict__ Cres, int m, int n,
   const unsigned __int128 P =
       (static_cast<unsigned __int128>(c_crt.P_hi) << 64) | static_cast<unsigned __int128>(c_crt.P_lo);
   const bool vec = (n % 4) == 0;  // 4-byte aligned words (planes and rows)
-  unsigned __int128 acc[4] = {0, 0, 0, 0};
+  // sum_l z_l (P / p_l), z_l < 256, in four 32-bit limbs of P / p_l: each
+  // limb product is < 2^40, so 64-bit limb sums cannot overflow for s <= 16
+  uint64_t limb[4][4] = {};
   for (int l = 0; l < s; ++l) {
     const int p = c_crt.p[l];
     const float pf = static_cast<float>(p), inv = 1.0f / pf, wf = static_cast<float>(c_crt.w[l]);
@@ -431,17 +444,28 @@ __global__ void crt_kernel(const uint8_t* __restrict__ Cres, int m, int n,
     } else {
       for (int q = 0; q < 4 && j0 + q < n; ++q) word |= static_cast<uint32_t>(Cres[l * plane + base + q]) << (8 * q);
     }
-    const unsigned __int128 M =
-        (static_cast<unsigned __int128>(c_crt.m_hi[l]) << 64) | c_crt.m_lo[l];
+    const uint32_t m0 = static_cast<uint32_t>(c_crt.m_lo[l]), m1 = static_cast<uint32_t>(c_crt.m_lo[l] >> 32);
+    const uint32_t m2 = static_cast<uint32_t>(c_crt.m_hi[l]), m3 = static_cast<uint32_t>(c_crt.m_hi[l] >> 32);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const float yw = static_cast<float>((word >> (8 * q)) & 0xffu) * wf;  // < 2^16: exact
-      float z = yw - pf * floorf(yw * inv);
-      z += z < 0.f ? pf : 0.f;
-      z -= z >= pf ? pf : 0.f;
-      acc[q] += static_cast<unsigned __int128>(static_cast<uint32_t>(z)) * M;
+      float zf = yw - pf * floorf(yw * inv);
+      zf += zf < 0.f ? pf : 0.f;
+      zf -= zf >= pf ? pf : 0.f;
+      const uint32_t z = static_cast<uint32_t>(zf);
+      limb[q][0] += static_cast<uint64_t>(z) * m0;
+      limb[q][1] += static_cast<uint64_t>(z) * m1;
+      limb[q][2] += static_cast<uint64_t>(z) * m2;
+      limb[q][3] += static_cast<uint64_t>(z) * m3;
     }
   }
+  unsigned __int128 acc[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    acc[q] = static_cast<unsigned __int128>(limb[q][0]) +
+             (static_cast<unsigned __int128>(limb[q][1]) << 32) +
+             (static_cast<unsigned __int128>(limb[q][2]) << 64) +
+             (static_cast<unsigned __int128>(limb[q][3]) << 96);
   const int ex = e[i];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -454,7 +478,7 @@ __global__ void crt_kernel(const uint8_t* __restrict__ Cres, int m, int n,
       continue;
     }
     // acc < s P: reduce mod P from a floating-point quotient estimate
-    uint64_t qt = static_cast<uint64_t>(u128_to_double(acc[q]) / c_crt.P_d);
+    uint64_t qt = static_cast<uint64_t>(u128_to_double(acc[q]) * c_crt.inv_P);  // +-1 fixed below
     unsigned __int128 qP = static_cast<unsigned __int128>(qt) * P;
     while (qP > acc[q]) qP -= P;
     unsigned __int128 r = acc[q] - qP;
@@ -499,6 +523,7 @@ void make_crt(int s, CrtConst* c) {
   c->P_lo = static_cast<uint64_t>(P);
   c->P_hi = static_cast<uint64_t>(P >> 64);
   c->P_d = static_cast<double>(c->P_hi) * 18446744073709551616.0 + static_cast<double>(c->P_lo);
+  c->inv_P = 1.0 / c->P_d;
 }
 
 }  // namespace
@@ -573,7 +598,7 @@ cudaError_t launch_dgemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K,
     residue_a_kernel<<<dim3(static_cast<unsigned>((kpad / 8 + 127) / 128), rows_y), 128, 0, st>>>(
         A, lda, m, k, static_cast<int>(kpad), ex, ares, l0, l1);
     residue_bt_kernel<<<dim3(static_cast<unsigned>((N + 31) / 32),
-                             static_cast<unsigned>((kpad + 31) / 32)),
+                             static_cast<unsigned>((kpad + OZ_BT_K - 1) / OZ_BT_K)),
                         256, 0, st>>>(B, ldb, k, n, static_cast<int>(kpad), fx, bres, l0, l1);
     if ((e = cudaEventRecord(ev[g], st)) != cudaSuccess ||
         (e = cudaStreamWaitEvent(aux, ev[g], 0)) != cudaSuccess)
