@@ -448,11 +448,16 @@ __global__ void crt_kernel(const uint8_t* __restrict__ Cres, int m, int n,
     const uint32_t m2 = static_cast<uint32_t>(c_crt.m_hi[l]), m3 = static_cast<uint32_t>(c_crt.m_hi[l] >> 32);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const float yw = static_cast<float>((word >> (8 * q)) & 0xffu) * wf;  // < 2^16: exact
-      float zf = yw - pf * floorf(yw * inv);
+      // (y w) mod p in fp32 without I2F / F2I / FRND (slow multi-function
+      // ops): 2^23-offset tricks for int <-> float, 1.5 * 2^23 add for rint;
+      // every value is an integer < 2^17, so all steps are exact
+      const float y = __int_as_float(0x4B000000 | ((word >> (8 * q)) & 0xffu)) - 8388608.0f;
+      const float yw = y * wf;
+      const float qf = __fsub_rn(__fadd_rn(yw * inv, 12582912.0f), 12582912.0f);
+      float zf = __fmaf_rn(-qf, pf, yw);
       zf += zf < 0.f ? pf : 0.f;
       zf -= zf >= pf ? pf : 0.f;
-      const uint32_t z = static_cast<uint32_t>(zf);
+      const uint32_t z = __float_as_uint(__fadd_rn(zf, 8388608.0f)) & 0x3ffu;
       limb[q][0] += static_cast<uint64_t>(z) * m0;
       limb[q][1] += static_cast<uint64_t>(z) * m1;
       limb[q][2] += static_cast<uint64_t>(z) * m2;
