@@ -233,6 +233,21 @@ def test_ozaki_mode_accuracy_and_integer_exactness(ctx, oracle, shape):
     assert oracle.first_difference(gi[rows], oracle.matmul_rows(rows, ai, bi)) is None
 
 
+def test_ozaki_mode_long_k_and_limits(ctx, oracle):
+    # k beyond the headline (plan: 14 moduli, t = 46 at k = 65536) and the
+    # int32-accumulation limit
+    m, k, n = 64, 65536 + 40, 96
+    A = ctx.fill(P.DIST_UNIFORM, 71, m, k)
+    B = ctx.fill(P.DIST_UNIFORM, 72, k, n)
+    got = host(ctx.dgemm(A, B, mode=P.MODE_OZAKI))
+    rows = [0, 31, 63]
+    assert normwise(got[rows], oracle.matmul_rows(rows, host(A), host(B))) <= 1e-13
+    assert P.ozaki_plan(65536) == (14, 46) and P.ozaki_plan(65576) == (15, 49)
+    with pytest.raises(P.DimensionError):
+        ctx.dgemm(ctx.fill(P.DIST_UNIFORM, 1, 2, 131073), ctx.fill(P.DIST_UNIFORM, 2, 131073, 2),
+                  mode=P.MODE_OZAKI)
+
+
 def test_ozaki_mode_row_slices_strides_scales_and_specials(ctx, oracle):
     T = torch()
     m, k, n = 700, 513, 600
