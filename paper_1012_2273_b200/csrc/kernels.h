@@ -52,6 +52,12 @@ size_t ozaki_workspace_bytes(int64_t m, int64_t n, int64_t k);
 cudaError_t launch_dgemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K, const double* A,
                                int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                                void* ws, cudaStream_t aux, cudaEvent_t* ev);
+// fp32 operands / result through the same scheme (30-bit scaling)
+void ozaki_plan_f32(int64_t k, int* s, int* t);
+size_t ozaki_workspace_bytes_f32(int64_t m, int64_t n, int64_t k);
+cudaError_t launch_sgemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K, const float* A,
+                               int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
+                               void* ws, cudaStream_t aux, cudaEvent_t* ev);
 // Force-load kernels (cudaFuncGetAttributes).  Under CUDA_MODULE_LOADING=LAZY
 // the first launch of a kernel loads it with a context-wide synchronisation,
 // which would wait forever on the resident latency server (and costs tens of

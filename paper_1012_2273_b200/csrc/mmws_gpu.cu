@@ -95,6 +95,20 @@ int sk_workspace(mmws_gpu_ctx* ctx, cudaStream_t stream, double** partial, int**
   return MMWS_GPU_OK;
 }
 
+// MODE_OZAKI's second stream and ordering events (created on first use)
+int ozaki_streams(mmws_gpu_ctx* ctx) {
+  if (ctx->oz_stream) return MMWS_GPU_OK;
+  cudaError_t e;
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  if ((e = cudaStreamCreateWithPriority(&ctx->oz_stream, cudaStreamNonBlocking, lo)) != cudaSuccess)
+    return cuda_fail(e, "ozaki stream");
+  for (int i = 0; i < OZAKI_EVENTS; ++i)
+    if ((e = cudaEventCreateWithFlags(&ctx->oz_ev[i], cudaEventDisableTiming)) != cudaSuccess)
+      return cuda_fail(e, "ozaki events");
+  return MMWS_GPU_OK;
+}
+
 int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
                    int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int mode,
                    cudaStream_t stream) {
@@ -171,15 +185,7 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
       return fail(MMWS_GPU_ERR_DIMENSION, "dgemm ozaki: k must be <= 131072 (int32 accumulation)");
     if ((e = ensure(ctx, &ctx->ws, &ctx->ws_bytes, ozaki_workspace_bytes(m, n, k))) != cudaSuccess)
       return cuda_fail(e, "dgemm ozaki workspace");
-    if (!ctx->oz_stream) {
-      int lo = 0, hi = 0;
-      cudaDeviceGetStreamPriorityRange(&lo, &hi);
-      if ((e = cudaStreamCreateWithPriority(&ctx->oz_stream, cudaStreamNonBlocking, lo)) != cudaSuccess)
-        return cuda_fail(e, "dgemm ozaki stream");
-      for (int i = 0; i < OZAKI_EVENTS; ++i)
-        if ((e = cudaEventCreateWithFlags(&ctx->oz_ev[i], cudaEventDisableTiming)) != cudaSuccess)
-          return cuda_fail(e, "dgemm ozaki events");
-    }
+    if (int rc = ozaki_streams(ctx)) return rc;
     e = launch_dgemm_ozaki(L, m, n, k, A, lda, B, ldb, C, ldc, ctx->ws, ctx->oz_stream, ctx->oz_ev);
     return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm ozaki");
   }
@@ -212,9 +218,19 @@ int sgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const flo
                    int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int mode,
                    cudaStream_t stream) {
   if (int rc = check_dims(m, n, k, lda, ldb, ldc, A, B, C)) return rc;
-  if (mode != MMWS_GPU_MODE_AUTO && mode != MMWS_GPU_MODE_FFMA)
+  if (mode != MMWS_GPU_MODE_AUTO && mode != MMWS_GPU_MODE_FFMA && mode != MMWS_GPU_MODE_OZAKI)
     return fail(MMWS_GPU_ERR_DOMAIN, "sgemm: unknown mode " + std::to_string(mode));
   const Launch L = ctx->launch(stream);
+  if (mode == MMWS_GPU_MODE_OZAKI) {  // fp32 through the int8 tensor-core scheme (ozaki.cu)
+    if (k > 131072)
+      return fail(MMWS_GPU_ERR_DIMENSION, "sgemm ozaki: k must be <= 131072 (int32 accumulation)");
+    cudaError_t e;
+    if ((e = ensure(ctx, &ctx->ws, &ctx->ws_bytes, ozaki_workspace_bytes_f32(m, n, k))) != cudaSuccess)
+      return cuda_fail(e, "sgemm ozaki workspace");
+    if (int rc = ozaki_streams(ctx)) return rc;
+    e = launch_sgemm_ozaki(L, m, n, k, A, lda, B, ldb, C, ldc, ctx->ws, ctx->oz_stream, ctx->oz_ev);
+    return e == cudaSuccess ? ok() : cuda_fail(e, "sgemm ozaki");
+  }
   cudaError_t e = sgemm_tma_supported(lda, ldb, A, B)
                       ? launch_sgemm_tma(L, m, n, k, A, lda, B, ldb, C, ldc)
                       : launch_sgemm_ffma(L, m, n, k, A, lda, B, ldb, C, ldc);

@@ -56,15 +56,16 @@ __constant__ CrtConst c_crt;
 
 // ---------------------------------------------------------------- scaling exponents
 // e_i: amax_i * 2^e_i < 2^t for row i of A (frexp: amax = f 2^x, f in [0.5, 1))
-__global__ void row_exponent_kernel(const double* __restrict__ A, int64_t lda, int m, int k, int t,
+template <class T>
+__global__ void row_exponent_kernel(const T* __restrict__ A, int64_t lda, int m, int k, int t,
                                     int* __restrict__ e) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= m) return;
-  const double* row = A + static_cast<int64_t>(warp) * lda;
+  const T* row = A + static_cast<int64_t>(warp) * lda;
   double amax = 0.0;
   bool finite = true;
   for (int j = lane; j < k; j += 32) {
-    const double v = row[j];
+    const double v = static_cast<double>(row[j]);
     finite = finite && isfinite(v);
     amax = fmax(amax, fabs(v));
   }
@@ -84,7 +85,8 @@ __global__ void row_exponent_kernel(const double* __restrict__ A, int64_t lda, i
 // maxima are atomicMax over 64-bit patterns from a 2-D grid of row blocks;
 // col_exponent_finalize turns them into exponents.
 constexpr int OZ_COL_ROWS = 256;  // rows per block of col_absmax_kernel
-__global__ void col_absmax_kernel(const double* __restrict__ B, int64_t ldb, int k, int n,
+template <class T>
+__global__ void col_absmax_kernel(const T* __restrict__ B, int64_t ldb, int k, int n,
                                   unsigned long long* __restrict__ colmax) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
@@ -92,7 +94,8 @@ __global__ void col_absmax_kernel(const double* __restrict__ B, int64_t ldb, int
   unsigned long long mx = 0;
   for (int r = r0; r < r1; ++r) {
     const unsigned long long bits =
-        static_cast<unsigned long long>(__double_as_longlong(B[static_cast<int64_t>(r) * ldb + j])) &
+        static_cast<unsigned long long>(
+            __double_as_longlong(static_cast<double>(B[static_cast<int64_t>(r) * ldb + j]))) &
         0x7fffffffffffffffULL;
     mx = bits > mx ? bits : mx;
   }
@@ -132,17 +135,19 @@ MMWS_DEVICE double scaled_int(double v, int ex) {
 
 // residues of A' = rint(A 2^e): res[l][i][j], j < kpad (zero padding).
 // A thread takes 8 consecutive j and stores one 8-byte word per modulus.
-__global__ void residue_a_kernel(const double* __restrict__ A, int64_t lda, int m, int k, int kpad,
+template <class T>
+__global__ void residue_a_kernel(const T* __restrict__ A, int64_t lda, int m, int k, int kpad,
                                  const int* __restrict__ e, int8_t* __restrict__ res, int l0,
                                  int l1) {
   const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (j0 >= kpad) return;
   for (int i = blockIdx.y; i < m; i += gridDim.y) {
   const int ex = e[i];
-  const double* row = A + static_cast<int64_t>(i) * lda;
+  const T* row = A + static_cast<int64_t>(i) * lda;
   double x[8];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) x[q] = j0 + q < k ? scaled_int(row[j0 + q], ex) : 0.0;
+  for (int q = 0; q < 8; ++q)
+    x[q] = j0 + q < k ? scaled_int(static_cast<double>(row[j0 + q]), ex) : 0.0;
   const int64_t plane = static_cast<int64_t>(m) * kpad;
   const int64_t o = static_cast<int64_t>(i) * kpad + j0;
   for (int l = l0; l < l1; ++l) {
@@ -161,7 +166,8 @@ __global__ void residue_a_kernel(const double* __restrict__ A, int64_t lda, int 
 // shared memory; thread t then owns column t/8 and 8 consecutive k, so each
 // 8-thread group writes 64 contiguous bytes of one output row per modulus.
 constexpr int OZ_BT_K = 64;
-__global__ void __launch_bounds__(256) residue_bt_kernel(const double* __restrict__ B, int64_t ldb,
+template <class T>
+__global__ void __launch_bounds__(256) residue_bt_kernel(const T* __restrict__ B, int64_t ldb,
                                                          int k, int n, int kpad,
                                                          const int* __restrict__ f,
                                                          int8_t* __restrict__ res, int l0, int l1) {
@@ -173,7 +179,9 @@ __global__ void __launch_bounds__(256) residue_bt_kernel(const double* __restric
     const int fc = c < n ? f[c] : 0;
     for (int i = ty; i < OZ_BT_K; i += 8) {
       const int r = r0 + i;
-      tile[i][tx] = (r < k && c < n) ? scaled_int(B[static_cast<int64_t>(r) * ldb + c], fc) : 0.0;
+      tile[i][tx] =
+          (r < k && c < n) ? scaled_int(static_cast<double>(B[static_cast<int64_t>(r) * ldb + c]), fc)
+                           : 0.0;
     }
   }
   __syncthreads();
@@ -420,9 +428,10 @@ MMWS_DEVICE double u128_to_double(unsigned __int128 v) {  // at most one extra r
          static_cast<double>(static_cast<uint64_t>(v));
 }
 
+template <class TO>
 __global__ void crt_kernel(const uint8_t* __restrict__ Cres, int m, int n,
                            const int* __restrict__ e, const int* __restrict__ f,
-                           double* __restrict__ C, int64_t ldc) {
+                           TO* __restrict__ C, int64_t ldc) {
   const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (j0 >= n) return;
   for (int i = blockIdx.y; i < m; i += gridDim.y) {
@@ -476,10 +485,10 @@ __global__ void crt_kernel(const uint8_t* __restrict__ Cres, int m, int n,
   for (int q = 0; q < 4; ++q) {
     const int j = j0 + q;
     if (j >= n) break;
-    double* out = C + static_cast<int64_t>(i) * ldc + j;
+    TO* out = C + static_cast<int64_t>(i) * ldc + j;
     const int fx = f[j];
     if (ex == OZ_NONFINITE || fx == OZ_NONFINITE) {
-      *out = __longlong_as_double(0x7ff8000000000000LL);
+      *out = static_cast<TO>(__longlong_as_double(0x7ff8000000000000LL));
       continue;
     }
     // acc < s P: reduce mod P from a floating-point quotient estimate
@@ -490,7 +499,7 @@ __global__ void crt_kernel(const uint8_t* __restrict__ Cres, int m, int n,
     while (r >= P) r -= P;
     const bool neg = r > (P >> 1);  // signed lift
     const double d = u128_to_double(neg ? P - r : r);
-    *out = ldexp(neg ? -d : d, -(ex + fx));
+    *out = static_cast<TO>(ldexp(neg ? -d : d, -(ex + fx)));
   }
   }
 }
@@ -533,20 +542,24 @@ void make_crt(int s, CrtConst* c) {
 
 }  // namespace
 
-// Plan: number of moduli and integer bits for an inner dimension k.
-void ozaki_plan(int64_t k, int* s_out, int* t_out) {
+// Plan: number of moduli and integer bits for an inner dimension k; the
+// smallest s whose product leaves at least `target` bits per operand.
+void ozaki_plan_bits(int64_t k, int target, int* s_out, int* t_out) {
   const double logk = std::ceil(std::log2(static_cast<double>(std::max<int64_t>(k, 2))));
   double logP = 0;
   int s = 0, t = 0;
   for (s = 1; s <= OZ_MAX_MODULI; ++s) {
     logP += std::log2(static_cast<double>(kModuli[s - 1]));
     t = static_cast<int>(std::floor((logP - 2.0 - logk) / 2.0));
-    if (t >= 46) break;  // ~1.4 * 2^-46 ~ 2e-14 normwise for random inputs
+    if (t >= target) break;
   }
   if (s > OZ_MAX_MODULI) s = OZ_MAX_MODULI;
   *s_out = s;
   *t_out = std::min(t, 52);
 }
+
+// fp64: t >= 46 (~1.4 * 2^-46 ~ 2e-14 normwise for random inputs)
+void ozaki_plan(int64_t k, int* s, int* t) { ozaki_plan_bits(k, 46, s, t); }
 
 size_t ozaki_workspace_bytes(int64_t m, int64_t n, int64_t k) {
   int s, t;
@@ -556,11 +569,10 @@ size_t ozaki_workspace_bytes(int64_t m, int64_t n, int64_t k) {
          sizeof(unsigned long long) * n + 1024;
 }
 
-cudaError_t launch_dgemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K, const double* A,
-                               int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
-                               void* ws, cudaStream_t aux, cudaEvent_t* ev) {
-  int s, t;
-  ozaki_plan(K, &s, &t);
+template <class T>
+cudaError_t launch_gemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K, const T* A,
+                              int64_t lda, const T* B, int64_t ldb, T* C, int64_t ldc, void* ws,
+                              cudaStream_t aux, cudaEvent_t* ev, int s, int t) {
   CrtConst cc;
   make_crt(s, &cc);
   cudaError_t e = cudaMemcpyToSymbolAsync(c_crt, &cc, sizeof(cc), 0, cudaMemcpyHostToDevice, L.stream);
@@ -575,9 +587,9 @@ cudaError_t launch_dgemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K,
   const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
   cudaStream_t st = L.stream;
   // ---- scaling exponents
-  row_exponent_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(A, lda, m, k, t, ex);
+  row_exponent_kernel<T><<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(A, lda, m, k, t, ex);
   if ((e = cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * N, st)) != cudaSuccess) return e;
-  col_absmax_kernel<<<dim3(static_cast<unsigned>((N + 255) / 256),
+  col_absmax_kernel<T><<<dim3(static_cast<unsigned>((N + 255) / 256),
                            static_cast<unsigned>((K + OZ_COL_ROWS - 1) / OZ_COL_ROWS)),
                       256, 0, st>>>(B, ldb, k, n, colmax);
   col_exponent_finalize<<<static_cast<unsigned>((N + 255) / 256), 256, 0, st>>>(colmax, n, t, fx);
@@ -600,9 +612,9 @@ cudaError_t launch_dgemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K,
   const int groups = work <= 1.4e11 ? std::min(s, OZ_GROUPS) : 1;
   for (int g = 0; g < groups; ++g) {
     const int l0 = s * g / groups, l1 = s * (g + 1) / groups;
-    residue_a_kernel<<<dim3(static_cast<unsigned>((kpad / 8 + 127) / 128), rows_y), 128, 0, st>>>(
+    residue_a_kernel<T><<<dim3(static_cast<unsigned>((kpad / 8 + 127) / 128), rows_y), 128, 0, st>>>(
         A, lda, m, k, static_cast<int>(kpad), ex, ares, l0, l1);
-    residue_bt_kernel<<<dim3(static_cast<unsigned>((N + 31) / 32),
+    residue_bt_kernel<T><<<dim3(static_cast<unsigned>((N + 31) / 32),
                              static_cast<unsigned>((kpad + OZ_BT_K - 1) / OZ_BT_K)),
                         256, 0, st>>>(B, ldb, k, n, static_cast<int>(kpad), fx, bres, l0, l1);
     if ((e = cudaEventRecord(ev[g], st)) != cudaSuccess ||
@@ -617,15 +629,46 @@ cudaError_t launch_dgemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K,
   if ((e = cudaEventRecord(ev[groups], aux)) != cudaSuccess ||
       (e = cudaStreamWaitEvent(st, ev[groups], 0)) != cudaSuccess)
     return e;
-  crt_kernel<<<dim3(static_cast<unsigned>((N / 4 + 1 + 127) / 128), rows_y), 128, 0, st>>>(
+  crt_kernel<T><<<dim3(static_cast<unsigned>((N / 4 + 1 + 127) / 128), rows_y), 128, 0, st>>>(
       cres, m, n, ex, fx, C, ldc);
   for (int i = 0; i < 4 + 3 * groups; ++i) L.count();
   return cudaGetLastError();
 }
 
+cudaError_t launch_dgemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K, const double* A,
+                               int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                               void* ws, cudaStream_t aux, cudaEvent_t* ev) {
+  int s, t;
+  ozaki_plan(K, &s, &t);
+  return launch_gemm_ozaki<double>(L, M, N, K, A, lda, B, ldb, C, ldc, ws, aux, ev, s, t);
+}
+
+// fp32 through the same integer scheme: 30-bit scaling (1.4 * 2^-30 ~ 1e-9,
+// far below the fp32 output rounding) needs ~10 moduli at k = 32768
+void ozaki_plan_f32(int64_t k, int* s, int* t) { ozaki_plan_bits(k, 30, s, t); }
+
+size_t ozaki_workspace_bytes_f32(int64_t m, int64_t n, int64_t k) {
+  int s, t;
+  ozaki_plan_f32(k, &s, &t);
+  const int64_t kpad = (k + 15) / 16 * 16;
+  return static_cast<size_t>(s) * (m * kpad + n * kpad + m * n) + sizeof(int) * (m + n + 2) +
+         sizeof(unsigned long long) * n + 1024;
+}
+
+cudaError_t launch_sgemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K, const float* A,
+                               int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
+                               void* ws, cudaStream_t aux, cudaEvent_t* ev) {
+  int s, t;
+  ozaki_plan_f32(K, &s, &t);
+  return launch_gemm_ozaki<float>(L, M, N, K, A, lda, B, ldb, C, ldc, ws, aux, ev, s, t);
+}
+
 cudaError_t preload_ozaki() {
-  return preload_kernels(row_exponent_kernel, col_absmax_kernel, col_exponent_finalize,
-                         residue_a_kernel, residue_bt_kernel, igemm_mod_kernel, crt_kernel);
+  return preload_kernels(row_exponent_kernel<double>, col_absmax_kernel<double>,
+                         col_exponent_finalize, residue_a_kernel<double>,
+                         residue_bt_kernel<double>, igemm_mod_kernel, crt_kernel<double>,
+                         row_exponent_kernel<float>, col_absmax_kernel<float>,
+                         residue_a_kernel<float>, residue_bt_kernel<float>, crt_kernel<float>);
 }
 
 }  // namespace mmws_impl

@@ -233,6 +233,23 @@ def test_ozaki_mode_accuracy_and_integer_exactness(ctx, oracle, shape):
     assert oracle.first_difference(gi[rows], oracle.matmul_rows(rows, ai, bi)) is None
 
 
+def test_ozaki_mode_fp32(ctx, oracle):
+    # fp32 operands through the same integer scheme (30-bit scaling): error at
+    # the fp32 output rounding (~3e-8), far inside the 1e-5 bound
+    T = torch()
+    for (m, k, n) in [(1, 1, 1), (129, 1000, 131), (1000, 37, 999), (2048, 2048, 2048)]:
+        A = ctx.fill(P.DIST_NORMAL, 81, m, k, dtype=T.float32)
+        B = ctx.fill(P.DIST_NORMAL, 82, k, n, dtype=T.float32)
+        got = host(ctx.sgemm(A, B, mode=P.MODE_OZAKI)).astype(np.float64)
+        rows = sorted({0, m // 2, m - 1})
+        want = oracle.matmul_rows(rows, host(A), host(B))
+        assert normwise(got[rows], want) <= 1e-7, (m, k, n)
+    ai = oracle.fill(oracle.DIST_INT8, 83, 300, 500).astype(np.float32)
+    bi = oracle.fill(oracle.DIST_INT8, 84, 500, 200).astype(np.float32)
+    gi = host(ctx.sgemm(dev(ai), dev(bi), mode=P.MODE_OZAKI))
+    assert (gi.astype(np.float64) == oracle.matmul_rows(list(range(300)), ai, bi)).all()
+
+
 def test_ozaki_mode_long_k_and_limits(ctx, oracle):
     # k beyond the headline (plan: 14 moduli, t = 46 at k = 65536) and the
     # int32-accumulation limit

@@ -49,4 +49,13 @@ for n in [int(x) for x in sys.argv[1:]] or [512, 2048, 4096, 8192, 16384]:
     ci = ctx.dgemm(Ai, Bi, mode=P.MODE_OZAKI).cpu().numpy()[rows]
     wi = O.matmul_rows(rows, Ai.cpu().numpy(), Bi.cpu().numpy())
     rec["int8_bit_exact"] = bool((ci == wi).all())
+    if os.environ.get("OZAKI_PROBE_F32"):
+        Af, Bf = A.float(), B.float()
+        Cf = torch.empty_like(Af)
+        for name, mode in (("f32_ozaki", P.MODE_OZAKI), ("f32_ffma", P.MODE_AUTO)):
+            ms = best_ms(lambda: ctx.sgemm(Af, Bf, Cf, mode=mode))
+            rec[name] = {"ms": ms, "tflops": 2 * n ** 3 / ms / 1e9}
+        ctx.sgemm(Af, Bf, Cf, mode=P.MODE_OZAKI)
+        wf = O.matmul_rows(rows, Af.cpu().numpy(), Bf.cpu().numpy())
+        rec["f32_ozaki_err"] = float(np.linalg.norm(Cf.cpu().numpy()[rows] - wf) / np.linalg.norm(wf))
     print(json.dumps(rec), flush=True)
