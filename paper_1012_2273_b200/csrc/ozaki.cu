@@ -52,7 +52,8 @@ struct CrtConst {
   double P_d, inv_P;
   int s;
 };
-__constant__ CrtConst c_crt;
+// passed to every kernel by value (__grid_constant__): no constant-memory
+// upload, so concurrent calls and CUDA-graph replays each carry their own
 
 // ---------------------------------------------------------------- scaling exponents
 // e_i: amax_i * 2^e_i < 2^t for row i of A (frexp: amax = f 2^x, f in [0.5, 1))
@@ -138,7 +139,7 @@ MMWS_DEVICE double scaled_int(double v, int ex) {
 template <class T>
 __global__ void residue_a_kernel(const T* __restrict__ A, int64_t lda, int m, int k, int kpad,
                                  const int* __restrict__ e, int8_t* __restrict__ res, int l0,
-                                 int l1) {
+                                 int l1, const __grid_constant__ CrtConst c_crt) {
   const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (j0 >= kpad) return;
   for (int i = blockIdx.y; i < m; i += gridDim.y) {
@@ -170,7 +171,8 @@ template <class T>
 __global__ void __launch_bounds__(256) residue_bt_kernel(const T* __restrict__ B, int64_t ldb,
                                                          int k, int n, int kpad,
                                                          const int* __restrict__ f,
-                                                         int8_t* __restrict__ res, int l0, int l1) {
+                                                         int8_t* __restrict__ res, int l0, int l1,
+                                                         const __grid_constant__ CrtConst c_crt) {
   __shared__ double tile[OZ_BT_K][33];
   const int r0 = blockIdx.y * OZ_BT_K, c0 = blockIdx.x * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // load phase: 32 x 8
@@ -262,7 +264,7 @@ MMWS_DEVICE void umma_commit(uint64_t* bar) {
 __global__ void __launch_bounds__(IG_THREADS, 1)
     igemm_mod_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      uint8_t* __restrict__ C, int m, int n, int kpad, int tiles_m, int tiles_n,
-                     int z0, int nz) {
+                     int z0, int nz, const __grid_constant__ CrtConst c_crt) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + IG_STAGES * IG_STAGE);
@@ -431,7 +433,7 @@ MMWS_DEVICE double u128_to_double(unsigned __int128 v) {  // at most one extra r
 template <class TO>
 __global__ void crt_kernel(const uint8_t* __restrict__ Cres, int m, int n,
                            const int* __restrict__ e, const int* __restrict__ f,
-                           TO* __restrict__ C, int64_t ldc) {
+                           TO* __restrict__ C, int64_t ldc, const __grid_constant__ CrtConst c_crt) {
   const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (j0 >= n) return;
   for (int i = blockIdx.y; i < m; i += gridDim.y) {
@@ -575,8 +577,7 @@ cudaError_t launch_gemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K, 
                               cudaStream_t aux, cudaEvent_t* ev, int s, int t) {
   CrtConst cc;
   make_crt(s, &cc);
-  cudaError_t e = cudaMemcpyToSymbolAsync(c_crt, &cc, sizeof(cc), 0, cudaMemcpyHostToDevice, L.stream);
-  if (e != cudaSuccess) return e;
+  cudaError_t e;
   const int64_t kpad = (K + 15) / 16 * 16;
   int8_t* ares = static_cast<int8_t*>(ws);
   int8_t* bres = ares + s * M * kpad;
@@ -613,24 +614,24 @@ cudaError_t launch_gemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K, 
   for (int g = 0; g < groups; ++g) {
     const int l0 = s * g / groups, l1 = s * (g + 1) / groups;
     residue_a_kernel<T><<<dim3(static_cast<unsigned>((kpad / 8 + 127) / 128), rows_y), 128, 0, st>>>(
-        A, lda, m, k, static_cast<int>(kpad), ex, ares, l0, l1);
+        A, lda, m, k, static_cast<int>(kpad), ex, ares, l0, l1, cc);
     residue_bt_kernel<T><<<dim3(static_cast<unsigned>((N + 31) / 32),
                              static_cast<unsigned>((kpad + OZ_BT_K - 1) / OZ_BT_K)),
-                        256, 0, st>>>(B, ldb, k, n, static_cast<int>(kpad), fx, bres, l0, l1);
+                        256, 0, st>>>(B, ldb, k, n, static_cast<int>(kpad), fx, bres, l0, l1, cc);
     if ((e = cudaEventRecord(ev[g], st)) != cudaSuccess ||
         (e = cudaStreamWaitEvent(aux, ev[g], 0)) != cudaSuccess)
       return e;
     const int grid = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(tiles_m) * tiles_n * (l1 - l0),
                                                         L.num_sms));
     igemm_mod_kernel<<<grid, IG_THREADS, IG_SMEM, aux>>>(ta, tb, cres, m, n, static_cast<int>(kpad),
-                                                         tiles_m, tiles_n, l0, l1 - l0);
+                                                         tiles_m, tiles_n, l0, l1 - l0, cc);
   }
   // ---- reconstruction after the last GEMM
   if ((e = cudaEventRecord(ev[groups], aux)) != cudaSuccess ||
       (e = cudaStreamWaitEvent(st, ev[groups], 0)) != cudaSuccess)
     return e;
   crt_kernel<T><<<dim3(static_cast<unsigned>((N / 4 + 1 + 127) / 128), rows_y), 128, 0, st>>>(
-      cres, m, n, ex, fx, C, ldc);
+      cres, m, n, ex, fx, C, ldc, cc);
   for (int i = 0; i < 4 + 3 * groups; ++i) L.count();
   return cudaGetLastError();
 }

@@ -250,6 +250,20 @@ def test_ozaki_mode_fp32(ctx, oracle):
     assert (gi.astype(np.float64) == oracle.matmul_rows(list(range(300)), ai, bi)).all()
 
 
+def test_ozaki_mode_in_a_cuda_graph(ctx):
+    # captured across its two streams; replays give the eager bits
+    T = torch()
+    A = ctx.fill(P.DIST_UNIFORM, 91, 512, 700)
+    B = ctx.fill(P.DIST_UNIFORM, 92, 700, 300)
+    want = host(ctx.dgemm(A, B, mode=P.MODE_OZAKI))
+    C2 = T.full((512, 300), float("nan"), dtype=T.float64, device="cuda")
+    g = ctx.graph_dgemm(A, B, C2, mode=P.MODE_OZAKI)
+    g.launch()
+    g.launch()
+    assert (bits(host(C2)) == bits(want)).all()
+    g.close()
+
+
 def test_ozaki_mode_long_k_and_limits(ctx, oracle):
     # k beyond the headline (plan: 14 moduli, t = 46 at k = 65536) and the
     # int32-accumulation limit
