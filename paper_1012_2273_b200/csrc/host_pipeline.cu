@@ -234,7 +234,10 @@ int host_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A
   // Panels of 1/8 of the rows (multiples of 128) once the problem is big
   // enough for the overlap to matter; one panel otherwise.
   const double work = static_cast<double>(m) * n * k;
-  const int64_t R = work < 2.0e9 ? m : std::max<int64_t>(128, ((m + 7) / 8 + 127) / 128 * 128);
+  // MODE_OZAKI recomputes B's residues per launch, so it takes one panel
+  const int64_t R = (work < 2.0e9 || mode == MMWS_GPU_MODE_OZAKI)
+                        ? m
+                        : std::max<int64_t>(128, ((m + 7) / 8 + 127) / 128 * 128);
   const int64_t panels = (m + R - 1) / R;
   // column blocks never narrower than 512 unless n itself is: a block then
   // takes the same kernel as the whole problem (see dgemm_dispatch)

@@ -250,6 +250,17 @@ def test_ozaki_mode_fp32(ctx, oracle):
     assert (gi.astype(np.float64) == oracle.matmul_rows(list(range(300)), ai, bi)).all()
 
 
+def test_ozaki_mode_host_entry(ctx, oracle):
+    a = oracle.fill(oracle.DIST_UNIFORM, 95, 1500, 1300)
+    b = oracle.fill(oracle.DIST_UNIFORM, 96, 1300, 1700)
+    want = host(ctx.dgemm(dev(a), dev(b), mode=P.MODE_OZAKI))
+    c, el = ctx.matmul_host(a, b, mode=P.MODE_OZAKI)
+    assert el > 0 and (bits(c) == bits(want)).all()
+    cf, _ = ctx.matmul_host(a.astype(np.float32), b.astype(np.float32), mode=P.MODE_OZAKI)
+    assert (cf == host(ctx.sgemm(dev(a.astype(np.float32)), dev(b.astype(np.float32)),
+                                 mode=P.MODE_OZAKI))).all()
+
+
 def test_ozaki_mode_in_a_cuda_graph(ctx):
     # captured across its two streams; replays give the eager bits
     T = torch()
