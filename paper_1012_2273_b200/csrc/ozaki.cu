@@ -13,14 +13,15 @@
 //      products A'_l B'_l on the tensor cores (|.| <= k * 128^2 < 2^31), kept
 //      mod p_l as uint8;
 //   3. rebuild C' = A'B' exactly from its residues by the Chinese remainder
-//      theorem (P = prod p_l > 2 k 2^(2t), 128-bit integers) and scale back:
+//      theorem (P = prod p_l >= 4 k 2^(2t), 128-bit integers) and scale back:
 //      C = C' * 2^-(e_i + f_j), one rounding to double.
 // With s = 14 moduli (P ~ 2^110) and k <= 16384, t = 47: the normwise error is
 // ~1.4 * 2^-47 ~ 1e-14 for random inputs (bound 1e-12), and integer-valued
 // inputs come out bit-exact (C' is then the exact integer product).  Each
 // element's result depends only on its row of A and column of B, so row
 // slices give the same bits as the whole problem.  Inputs must be finite; a
-// row or column holding Inf/NaN yields NaN in the affected outputs.
+// row or column holding Inf/NaN yields NaN in the affected outputs.  fp32
+// operands go through the same kernels with 30-bit scaling (~10 moduli).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -43,6 +44,9 @@ constexpr int OZ_GROUPS = 4;           // moduli groups pipelined residues -> GE
 constexpr int kModuli[OZ_MAX_MODULI] = {256, 255, 253, 251, 247, 241, 239, 233,
                                         229, 227, 223, 211, 199, 197, 193, 191};
 
+// CRT constants, passed to every kernel by value (__grid_constant__) -- no
+// constant-memory upload, so concurrent calls and CUDA-graph replays each
+// carry their own
 struct CrtConst {
   int p[OZ_MAX_MODULI];
   int w[OZ_MAX_MODULI];          // (P / p_l)^-1 mod p_l
@@ -52,8 +56,6 @@ struct CrtConst {
   double P_d, inv_P;
   int s;
 };
-// passed to every kernel by value (__grid_constant__): no constant-memory
-// upload, so concurrent calls and CUDA-graph replays each carry their own
 
 // ---------------------------------------------------------------- scaling exponents
 // e_i: amax_i * 2^e_i < 2^t for row i of A (frexp: amax = f 2^x, f in [0.5, 1))
@@ -143,22 +145,22 @@ __global__ void residue_a_kernel(const T* __restrict__ A, int64_t lda, int m, in
   const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (j0 >= kpad) return;
   for (int i = blockIdx.y; i < m; i += gridDim.y) {
-  const int ex = e[i];
-  const T* row = A + static_cast<int64_t>(i) * lda;
-  double x[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q)
-    x[q] = j0 + q < k ? scaled_int(static_cast<double>(row[j0 + q]), ex) : 0.0;
-  const int64_t plane = static_cast<int64_t>(m) * kpad;
-  const int64_t o = static_cast<int64_t>(i) * kpad + j0;
-  for (int l = l0; l < l1; ++l) {
-    const int p = c_crt.p[l];
-    unsigned long long w = 0;
+    const int ex = e[i];
+    const T* row = A + static_cast<int64_t>(i) * lda;
+    double x[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q)
-      w |= static_cast<unsigned long long>(static_cast<uint8_t>(sresidue(x[q], p))) << (8 * q);
-    *reinterpret_cast<unsigned long long*>(res + l * plane + o) = w;
-  }
+      x[q] = j0 + q < k ? scaled_int(static_cast<double>(row[j0 + q]), ex) : 0.0;
+    const int64_t plane = static_cast<int64_t>(m) * kpad;
+    const int64_t o = static_cast<int64_t>(i) * kpad + j0;
+    for (int l = l0; l < l1; ++l) {
+      const int p = c_crt.p[l];
+      unsigned long long w = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        w |= static_cast<unsigned long long>(static_cast<uint8_t>(sresidue(x[q], p))) << (8 * q);
+      *reinterpret_cast<unsigned long long*>(res + l * plane + o) = w;
+    }
   }
 }
 
@@ -182,8 +184,9 @@ __global__ void __launch_bounds__(256) residue_bt_kernel(const T* __restrict__ B
     for (int i = ty; i < OZ_BT_K; i += 8) {
       const int r = r0 + i;
       tile[i][tx] =
-          (r < k && c < n) ? scaled_int(static_cast<double>(B[static_cast<int64_t>(r) * ldb + c]), fc)
-                           : 0.0;
+          (r < k && c < n)
+              ? scaled_int(static_cast<double>(B[static_cast<int64_t>(r) * ldb + c]), fc)
+              : 0.0;
     }
   }
   __syncthreads();
@@ -207,13 +210,13 @@ __global__ void __launch_bounds__(256) residue_bt_kernel(const T* __restrict__ B
 
 // ---------------------------------------------------------------- int8 tensor-core GEMM
 // C_l = (A_l B_l^T) mod p_l for every modulus l, A_l: m x kpad, B_l: n x
-// kpad (both K-major int8), C_l: m x n uint8.  128 x 256 tiles,
-// tcgen05.mma.kind::i8 (M=128, N=256, K=32) issued by one thread, operands
-// TMA-staged (128-byte swizzle, 4-stage ring), int32 accumulators in TMEM,
-// epilogue tcgen05.ld -> mod p -> 16-byte stores.
-// 256 x 256 tiles: two M=128 MMAs per k-step share the B operand, so a CTA
-// moves 64 KB per 128-byte k-block for 256x256 outputs (48 KB for 128x256
-// with M=128 tiles): the L2 -> SM operand stream is what limits this kernel.
+// kpad (both K-major int8), C_l: m x n uint8.  256 x 256 tiles:
+// tcgen05.mma.kind::i8 (M=128, N=256, K=32) issued by one thread, two per
+// k-step sharing the B operand (64 KB per 128-byte k-block for 256x256
+// outputs; 128x256 tiles needed 48 KB for half the outputs and ran 7 %
+// slower), operands TMA-staged (128-byte swizzle, 3-stage ring), int32
+// accumulators in TMEM (all 512 columns), epilogue tcgen05.ld -> mod p ->
+// 16-byte stores.
 constexpr int IG_BM = 256, IG_BN = 256, IG_BK = 128, IG_STAGES = 3;
 constexpr int IG_HALVES = IG_BM / 128;                 // M=128 MMAs per k-step
 constexpr int IG_NBUF = 512 / (IG_HALVES * IG_BN);    // TMEM accumulator buffers
@@ -262,7 +265,8 @@ MMWS_DEVICE void umma_commit(uint64_t* bar) {
 // 256-column TMEM accumulators: the MMAs of item i+1 run while the epilogue
 // drains item i (tmem_full / tmem_empty mbarriers).
 __global__ void __launch_bounds__(IG_THREADS, 1)
-    igemm_mod_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+    igemm_mod_kernel(const __grid_constant__ CUtensorMap tmA,
+                     const __grid_constant__ CUtensorMap tmB,
                      uint8_t* __restrict__ C, int m, int n, int kpad, int tiles_m, int tiles_n,
                      int z0, int nz, const __grid_constant__ CrtConst c_crt) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -364,53 +368,53 @@ __global__ void __launch_bounds__(IG_THREADS, 1)
       const int p = c_crt.p[z];
 #pragma unroll 1
       for (int h = 0; h < IG_HALVES; ++h) {
-      const int row = tm * IG_BM + h * 128 + quarter * 32 + lane;
-      uint8_t* crow = C + (static_cast<size_t>(z) * m + row) * n;
+        const int row = tm * IG_BM + h * 128 + quarter * 32 + lane;
+        uint8_t* crow = C + (static_cast<size_t>(z) * m + row) * n;
 #pragma unroll 1
-      for (int c0 = 0; c0 < IG_BN; c0 += 32) {
-        uint32_t v[32];
-        const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16) +
-                               (b * IG_HALVES + h) * IG_BN + c0;
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
-            "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
-            "%28, %29, %30, %31}, [%32];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-              "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
-              "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-              "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
-              "=r"(v[31])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;");
-        if (h + 1 == IG_HALVES && c0 + 32 == IG_BN) {  // last read of buffer b: hand it back
-          asm volatile("tcgen05.fence::before_thread_sync;");
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tmem_empty[b]);
-        }
-        const int col = tn * IG_BN + c0;
-        if (row >= m || col >= n) continue;
-        uint32_t packed[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          uint32_t word = 0;
-#pragma unroll
-          for (int bb = 0; bb < 4; ++bb) {
-            int r = static_cast<int>(v[4 * q + bb]) % p;  // C mod p in [0, p)
-            r += r < 0 ? p : 0;
-            word |= static_cast<uint32_t>(r) << (8 * bb);
+        for (int c0 = 0; c0 < IG_BN; c0 += 32) {
+          uint32_t v[32];
+          const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16) +
+                                 (b * IG_HALVES + h) * IG_BN + c0;
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+              "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+              "%28, %29, %30, %31}, [%32];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+                "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+                "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+                "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+                "=r"(v[31])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;");
+          if (h + 1 == IG_HALVES && c0 + 32 == IG_BN) {  // last read of buffer b: hand it back
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tmem_empty[b]);
           }
-          packed[q] = word;
+          const int col = tn * IG_BN + c0;
+          if (row >= m || col >= n) continue;
+          uint32_t packed[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            uint32_t word = 0;
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) {
+              int r = static_cast<int>(v[4 * q + bb]) % p;  // C mod p in [0, p)
+              r += r < 0 ? p : 0;
+              word |= static_cast<uint32_t>(r) << (8 * bb);
+            }
+            packed[q] = word;
+          }
+          if (col + 32 <= n && (n % 16) == 0) {
+            uint4* dst = reinterpret_cast<uint4*>(crow + col);
+            dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+            dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+          } else {
+            const uint8_t* bytes = reinterpret_cast<const uint8_t*>(packed);
+            for (int j = 0; j < 32 && col + j < n; ++j) crow[col + j] = bytes[j];
+          }
         }
-        if (col + 32 <= n && (n % 16) == 0) {
-          uint4* dst = reinterpret_cast<uint4*>(crow + col);
-          dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-          dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
-        } else {
-          const uint8_t* bytes = reinterpret_cast<const uint8_t*>(packed);
-          for (int j = 0; j < 32 && col + j < n; ++j) crow[col + j] = bytes[j];
-        }
-      }
       }
     }
   }
@@ -433,76 +437,81 @@ MMWS_DEVICE double u128_to_double(unsigned __int128 v) {  // at most one extra r
 template <class TO>
 __global__ void crt_kernel(const uint8_t* __restrict__ Cres, int m, int n,
                            const int* __restrict__ e, const int* __restrict__ f,
-                           TO* __restrict__ C, int64_t ldc, const __grid_constant__ CrtConst c_crt) {
+                           TO* __restrict__ C, int64_t ldc,
+                           const __grid_constant__ CrtConst c_crt) {
   const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (j0 >= n) return;
   for (int i = blockIdx.y; i < m; i += gridDim.y) {
-  const int64_t plane = static_cast<int64_t>(m) * n;
-  const int64_t base = static_cast<int64_t>(i) * n + j0;
-  const int s = c_crt.s;
-  const unsigned __int128 P =
-      (static_cast<unsigned __int128>(c_crt.P_hi) << 64) | static_cast<unsigned __int128>(c_crt.P_lo);
-  const bool vec = (n % 4) == 0;  // 4-byte aligned words (planes and rows)
-  // sum_l z_l (P / p_l), z_l < 256, in four 32-bit limbs of P / p_l: each
-  // limb product is < 2^40, so 64-bit limb sums cannot overflow for s <= 16
-  uint64_t limb[4][4] = {};
-  for (int l = 0; l < s; ++l) {
-    const int p = c_crt.p[l];
-    const float pf = static_cast<float>(p), inv = 1.0f / pf, wf = static_cast<float>(c_crt.w[l]);
-    uint32_t word = 0;
-    if (vec) {
-      word = *reinterpret_cast<const uint32_t*>(Cres + l * plane + base);
-    } else {
-      for (int q = 0; q < 4 && j0 + q < n; ++q) word |= static_cast<uint32_t>(Cres[l * plane + base + q]) << (8 * q);
+    const int64_t plane = static_cast<int64_t>(m) * n;
+    const int64_t base = static_cast<int64_t>(i) * n + j0;
+    const int s = c_crt.s;
+    const unsigned __int128 P =
+        (static_cast<unsigned __int128>(c_crt.P_hi) << 64) |
+        static_cast<unsigned __int128>(c_crt.P_lo);
+    const bool vec = (n % 4) == 0;  // 4-byte aligned words (planes and rows)
+    // sum_l z_l (P / p_l), z_l < 256, in four 32-bit limbs of P / p_l: each
+    // limb product is < 2^40, so 64-bit limb sums cannot overflow for s <= 16
+    uint64_t limb[4][4] = {};
+    for (int l = 0; l < s; ++l) {
+      const int p = c_crt.p[l];
+      const float pf = static_cast<float>(p), inv = 1.0f / pf, wf = static_cast<float>(c_crt.w[l]);
+      uint32_t word = 0;
+      if (vec) {
+        word = *reinterpret_cast<const uint32_t*>(Cres + l * plane + base);
+      } else {
+        for (int q = 0; q < 4 && j0 + q < n; ++q)
+          word |= static_cast<uint32_t>(Cres[l * plane + base + q]) << (8 * q);
+      }
+      const uint32_t m0 = static_cast<uint32_t>(c_crt.m_lo[l]);
+      const uint32_t m1 = static_cast<uint32_t>(c_crt.m_lo[l] >> 32);
+      const uint32_t m2 = static_cast<uint32_t>(c_crt.m_hi[l]);
+      const uint32_t m3 = static_cast<uint32_t>(c_crt.m_hi[l] >> 32);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        // (y w) mod p in fp32 without I2F / F2I / FRND (slow multi-function
+        // ops): 2^23-offset tricks for int <-> float, 1.5 * 2^23 add for rint;
+        // every value is an integer < 2^17, so all steps are exact
+        const float y = __int_as_float(0x4B000000 | ((word >> (8 * q)) & 0xffu)) - 8388608.0f;
+        const float yw = y * wf;
+        const float qf = __fsub_rn(__fadd_rn(yw * inv, 12582912.0f), 12582912.0f);
+        float zf = __fmaf_rn(-qf, pf, yw);
+        zf += zf < 0.f ? pf : 0.f;
+        zf -= zf >= pf ? pf : 0.f;
+        const uint32_t z = __float_as_uint(__fadd_rn(zf, 8388608.0f)) & 0x3ffu;
+        limb[q][0] += static_cast<uint64_t>(z) * m0;
+        limb[q][1] += static_cast<uint64_t>(z) * m1;
+        limb[q][2] += static_cast<uint64_t>(z) * m2;
+        limb[q][3] += static_cast<uint64_t>(z) * m3;
+      }
     }
-    const uint32_t m0 = static_cast<uint32_t>(c_crt.m_lo[l]), m1 = static_cast<uint32_t>(c_crt.m_lo[l] >> 32);
-    const uint32_t m2 = static_cast<uint32_t>(c_crt.m_hi[l]), m3 = static_cast<uint32_t>(c_crt.m_hi[l] >> 32);
+    unsigned __int128 acc[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      acc[q] = static_cast<unsigned __int128>(limb[q][0]) +
+               (static_cast<unsigned __int128>(limb[q][1]) << 32) +
+               (static_cast<unsigned __int128>(limb[q][2]) << 64) +
+               (static_cast<unsigned __int128>(limb[q][3]) << 96);
+    const int ex = e[i];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      // (y w) mod p in fp32 without I2F / F2I / FRND (slow multi-function
-      // ops): 2^23-offset tricks for int <-> float, 1.5 * 2^23 add for rint;
-      // every value is an integer < 2^17, so all steps are exact
-      const float y = __int_as_float(0x4B000000 | ((word >> (8 * q)) & 0xffu)) - 8388608.0f;
-      const float yw = y * wf;
-      const float qf = __fsub_rn(__fadd_rn(yw * inv, 12582912.0f), 12582912.0f);
-      float zf = __fmaf_rn(-qf, pf, yw);
-      zf += zf < 0.f ? pf : 0.f;
-      zf -= zf >= pf ? pf : 0.f;
-      const uint32_t z = __float_as_uint(__fadd_rn(zf, 8388608.0f)) & 0x3ffu;
-      limb[q][0] += static_cast<uint64_t>(z) * m0;
-      limb[q][1] += static_cast<uint64_t>(z) * m1;
-      limb[q][2] += static_cast<uint64_t>(z) * m2;
-      limb[q][3] += static_cast<uint64_t>(z) * m3;
+      const int j = j0 + q;
+      if (j >= n) break;
+      TO* out = C + static_cast<int64_t>(i) * ldc + j;
+      const int fx = f[j];
+      if (ex == OZ_NONFINITE || fx == OZ_NONFINITE) {
+        *out = static_cast<TO>(__longlong_as_double(0x7ff8000000000000LL));
+        continue;
+      }
+      // acc < s P: reduce mod P from a floating-point quotient estimate
+      uint64_t qt = static_cast<uint64_t>(u128_to_double(acc[q]) * c_crt.inv_P);  // +-1 fixed below
+      unsigned __int128 qP = static_cast<unsigned __int128>(qt) * P;
+      while (qP > acc[q]) qP -= P;
+      unsigned __int128 r = acc[q] - qP;
+      while (r >= P) r -= P;
+      const bool neg = r > (P >> 1);  // signed lift
+      const double d = u128_to_double(neg ? P - r : r);
+      *out = static_cast<TO>(ldexp(neg ? -d : d, -(ex + fx)));
     }
-  }
-  unsigned __int128 acc[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-    acc[q] = static_cast<unsigned __int128>(limb[q][0]) +
-             (static_cast<unsigned __int128>(limb[q][1]) << 32) +
-             (static_cast<unsigned __int128>(limb[q][2]) << 64) +
-             (static_cast<unsigned __int128>(limb[q][3]) << 96);
-  const int ex = e[i];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int j = j0 + q;
-    if (j >= n) break;
-    TO* out = C + static_cast<int64_t>(i) * ldc + j;
-    const int fx = f[j];
-    if (ex == OZ_NONFINITE || fx == OZ_NONFINITE) {
-      *out = static_cast<TO>(__longlong_as_double(0x7ff8000000000000LL));
-      continue;
-    }
-    // acc < s P: reduce mod P from a floating-point quotient estimate
-    uint64_t qt = static_cast<uint64_t>(u128_to_double(acc[q]) * c_crt.inv_P);  // +-1 fixed below
-    unsigned __int128 qP = static_cast<unsigned __int128>(qt) * P;
-    while (qP > acc[q]) qP -= P;
-    unsigned __int128 r = acc[q] - qP;
-    while (r >= P) r -= P;
-    const bool neg = r > (P >> 1);  // signed lift
-    const double d = u128_to_double(neg ? P - r : r);
-    *out = static_cast<TO>(ldexp(neg ? -d : d, -(ex + fx)));
-  }
   }
 }
 
@@ -582,7 +591,8 @@ cudaError_t launch_gemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K, 
   int8_t* ares = static_cast<int8_t*>(ws);
   int8_t* bres = ares + s * M * kpad;
   uint8_t* cres = reinterpret_cast<uint8_t*>(bres + s * N * kpad);
-  int* ex = reinterpret_cast<int*>(reinterpret_cast<uintptr_t>(cres + s * M * N + 15) & ~uintptr_t(15));
+  int* ex =
+      reinterpret_cast<int*>(reinterpret_cast<uintptr_t>(cres + s * M * N + 15) & ~uintptr_t(15));
   int* fx = ex + M;
   unsigned long long* colmax = reinterpret_cast<unsigned long long*>(ex + ((M + N + 1) & ~int64_t(1)));
   const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
