@@ -261,6 +261,17 @@ def test_ozaki_mode_host_entry(ctx, oracle):
                                  mode=P.MODE_OZAKI))).all()
 
 
+def test_ozaki_mode_tall_and_wide(ctx, oracle):
+    # more rows than a grid dimension holds (row loops) and a 1-column B
+    for (m, k, n) in [(70000, 24, 8), (5, 40, 70001), (70000, 3, 1)]:
+        A = ctx.fill(P.DIST_INT8, 11, m, k)
+        B = ctx.fill(P.DIST_INT8, 12, k, n)
+        got = host(ctx.dgemm(A, B, mode=P.MODE_OZAKI))
+        rows = [0, m // 2, m - 1]
+        want = oracle.matmul_rows(rows, host(A), host(B))
+        assert oracle.first_difference(got[rows], want) is None, (m, k, n)
+
+
 def test_ozaki_mode_in_a_cuda_graph(ctx):
     # captured across its two streams; replays give the eager bits
     T = torch()
