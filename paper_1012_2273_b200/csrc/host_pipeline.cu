@@ -204,6 +204,76 @@ int host_multiply_streamed(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, c
   return ok();
 }
 
+// MODE_OZAKI with host buffers: B crosses PCIe first and is scaled and cut
+// into residues once; A then follows in row panels, each emulated against the
+// prepared B while the next panel is in flight, and each C panel goes back as
+// soon as its reconstruction is done.  Nothing can start before all of B has
+// landed (every output needs a whole column of B), so the floor is B's copy +
+// the emulation + one panel's copy-out rather than copy-in + emulation +
+// copy-out.  Bitwise the one-shot MODE_OZAKI result (each output row depends
+// only on its own row of A).
+template <class T>
+int host_multiply_ozaki(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A,
+                        const T* B, T* C, double* elapsed_s) {
+  if (k > 131072)
+    return fail(MMWS_GPU_ERR_DIMENSION, "matmul ozaki: k must be <= 131072 (int32 accumulation)");
+  const int64_t R = std::max<int64_t>(512, ((m + 7) / 8 + 255) / 256 * 256);
+  const int64_t panels = (m + R - 1) / R;
+  const size_t ws = sizeof(T) == 8 ? ozaki_workspace_bytes(R, n, k) : ozaki_workspace_bytes_f32(R, n, k);
+  cudaError_t e;
+  if ((e = ensure(ctx, &ctx->ws, &ctx->ws_bytes, ws)) != cudaSuccess)
+    return cuda_fail(e, "matmul ozaki: workspace");
+  if ((e = event_pool(ctx, panels * 2 + 1)) != cudaSuccess)
+    return cuda_fail(e, "matmul ozaki: events");
+  cudaEvent_t* evA = ctx->pool.data();
+  cudaEvent_t* evC = evA + panels;
+  cudaEvent_t evB = evC[panels];
+  T* dA = static_cast<T*>(ctx->dA);
+  T* dB = static_cast<T*>(ctx->dB);
+  T* dC = static_cast<T*>(ctx->dC);
+  cudaStream_t in = ctx->copy_in, comp = ctx->stream, out = ctx->copy_out;
+  const Launch L = ctx->launch(comp);
+  auto rows_of = [&](int64_t i) { return std::min(R, m - i * R); };
+
+  cudaEventRecord(ctx->ev0, in);
+  if ((e = copy_h2d(ctx, dB, sizeof(T) * n, B, sizeof(T) * n, sizeof(T) * n, k, in)))
+    return cuda_fail(e, "matmul ozaki: H2D B");
+  cudaEventRecord(evB, in);
+  cudaStreamWaitEvent(comp, evB, 0);
+  if ((e = launch_ozaki_prepare_b(L, n, k, dB, n, ctx->ws)) != cudaSuccess)
+    return cuda_fail(e, "matmul ozaki: prepare B");
+  for (int64_t i = 0; i < panels; ++i) {
+    if ((e = copy_h2d(ctx, dA + i * R * k, sizeof(T) * k, A + i * R * k, sizeof(T) * k,
+                      sizeof(T) * k, rows_of(i), in)))
+      return cuda_fail(e, "matmul ozaki: H2D A");
+    cudaEventRecord(evA[i], in);
+    cudaStreamWaitEvent(comp, evA[i], 0);
+    if ((e = launch_ozaki_panel(L, rows_of(i), n, k, dA + i * R * k, k, dC + i * R * n, n,
+                                ctx->ws)) != cudaSuccess)
+      return cuda_fail(e, "matmul ozaki: panel");
+    cudaEventRecord(evC[i], comp);
+  }
+  D2hPump pump(ctx, out);
+  for (int64_t i = 0; i < panels; ++i) {
+    cudaStreamWaitEvent(out, evC[i], 0);
+    if ((e = pump.add(C + i * R * n, sizeof(T) * n, dC + i * R * n, sizeof(T) * n, sizeof(T) * n,
+                      rows_of(i))))
+      return cuda_fail(e, "matmul ozaki: D2H");
+  }
+  if ((e = pump.finish())) return cuda_fail(e, "matmul ozaki: D2H");
+  cudaEventRecord(ctx->ev1, out);
+  if ((e = cudaStreamSynchronize(out)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(comp)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(in)) != cudaSuccess)
+    return cuda_fail(e, "matmul ozaki: sync");
+  if (elapsed_s) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    *elapsed_s = ms * 1e-3;
+  }
+  return ok();
+}
+
 }  // namespace
 
 template <class T>
@@ -226,6 +296,9 @@ int host_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A
         n % 2 == 0 && (n > 256 || k > 256))
       return host_multiply_streamed(ctx, m, n, k, A, B, C, elapsed_s);
   }
+  // big emulated problems: B prepared once, A streamed in row panels
+  if (mode == MMWS_GPU_MODE_OZAKI && m >= 1024 && static_cast<double>(m) * n * k >= 1.0e10)
+    return host_multiply_ozaki(ctx, m, n, k, A, B, C, elapsed_s);
   T* dA = static_cast<T*>(ctx->dA);
   T* dB = static_cast<T*>(ctx->dB);
   T* dC = static_cast<T*>(ctx->dC);
@@ -234,7 +307,7 @@ int host_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A
   // Panels of 1/8 of the rows (multiples of 128) once the problem is big
   // enough for the overlap to matter; one panel otherwise.
   const double work = static_cast<double>(m) * n * k;
-  // MODE_OZAKI recomputes B's residues per launch, so it takes one panel
+  // small MODE_OZAKI problems would recompute B's residues per launch: one panel
   const int64_t R = (work < 2.0e9 || mode == MMWS_GPU_MODE_OZAKI)
                         ? m
                         : std::max<int64_t>(128, ((m + 7) / 8 + 127) / 128 * 128);

@@ -58,6 +58,18 @@ size_t ozaki_workspace_bytes_f32(int64_t m, int64_t n, int64_t k);
 cudaError_t launch_sgemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K, const float* A,
                                int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
                                void* ws, cudaStream_t aux, cudaEvent_t* ev);
+// Row-panel form (host pipeline): B's scaling and residues once into `ws`
+// (sized by ozaki_workspace_bytes[_f32] for the tallest panel), then any
+// number of A row panels against them, in order on one stream.  Each output
+// row depends only on its own row of A, so panels give the one-shot bits.
+cudaError_t launch_ozaki_prepare_b(const Launch& L, int64_t N, int64_t K, const double* B,
+                                   int64_t ldb, void* ws);
+cudaError_t launch_ozaki_prepare_b(const Launch& L, int64_t N, int64_t K, const float* B,
+                                   int64_t ldb, void* ws);
+cudaError_t launch_ozaki_panel(const Launch& L, int64_t M, int64_t N, int64_t K, const double* A,
+                               int64_t lda, double* C, int64_t ldc, void* ws);
+cudaError_t launch_ozaki_panel(const Launch& L, int64_t M, int64_t N, int64_t K, const float* A,
+                               int64_t lda, float* C, int64_t ldc, void* ws);
 // Force-load kernels (cudaFuncGetAttributes).  Under CUDA_MODULE_LOADING=LAZY
 // the first launch of a kernel loads it with a context-wide synchronisation,
 // which would wait forever on the resident latency server (and costs tens of

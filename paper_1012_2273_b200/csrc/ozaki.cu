@@ -572,106 +572,239 @@ void ozaki_plan_bits(int64_t k, int target, int* s_out, int* t_out) {
 // fp64: t >= 46 (~1.4 * 2^-46 ~ 2e-14 normwise for random inputs)
 void ozaki_plan(int64_t k, int* s, int* t) { ozaki_plan_bits(k, 46, s, t); }
 
-size_t ozaki_workspace_bytes(int64_t m, int64_t n, int64_t k) {
+namespace {
+
+template <class T>
+void plan_for(int64_t k, int* s, int* t) {
+  if constexpr (sizeof(T) == 8)
+    ozaki_plan_bits(k, 46, s, t);  // fp64: t >= 46 (~1.4 * 2^-46 ~ 2e-14 normwise)
+  else
+    ozaki_plan_bits(k, 30, s, t);  // fp32: 1.4 * 2^-30 ~ 1e-9, far below fp32 rounding
+}
+
+template <class T>
+size_t workspace_bytes(int64_t m, int64_t n, int64_t k) {
   int s, t;
-  ozaki_plan(k, &s, &t);
+  plan_for<T>(k, &s, &t);
   const int64_t kpad = (k + 15) / 16 * 16;
-  return static_cast<size_t>(s) * (m * kpad + n * kpad + m * n) + sizeof(int) * (m + n + 2) +
+  return static_cast<size_t>(s) * (m * kpad + n * kpad + m * n) + sizeof(int) * (m + n) +
          sizeof(unsigned long long) * n + 1024;
+}
+
+// Workspace layout.  B's part (residues, column exponents and maxima) comes
+// first and does not depend on m, so one prepared B serves row panels of any
+// height: [bres s*n*kpad | colmax n | fx n | pad to 256] [ares s*m*kpad |
+// cres s*m*n | pad 16 | ex m].  Every TMA base stays 16-byte aligned (kpad is
+// a multiple of 16).
+struct OzWs {
+  int8_t* bres;
+  unsigned long long* colmax;
+  int* fx;
+  int8_t* ares;
+  uint8_t* cres;
+  int* ex;
+};
+
+OzWs layout(void* ws, int64_t m, int64_t n, int64_t kpad, int s) {
+  OzWs w;
+  uintptr_t p = reinterpret_cast<uintptr_t>(ws);
+  w.bres = reinterpret_cast<int8_t*>(p);
+  p += s * n * kpad;
+  p = (p + 15) & ~uintptr_t(15);
+  w.colmax = reinterpret_cast<unsigned long long*>(p);
+  p += sizeof(unsigned long long) * n;
+  w.fx = reinterpret_cast<int*>(p);
+  p += sizeof(int) * n;
+  p = (p + 255) & ~uintptr_t(255);
+  w.ares = reinterpret_cast<int8_t*>(p);
+  p += s * m * kpad;
+  w.cres = reinterpret_cast<uint8_t*>(p);
+  p += s * m * n;
+  p = (p + 15) & ~uintptr_t(15);
+  w.ex = reinterpret_cast<int*>(p);
+  return w;
+}
+
+// B's column exponents; the residue passes take moduli [l0, l1)
+template <class T>
+cudaError_t scale_b(cudaStream_t st, int64_t N, int64_t K, const T* B, int64_t ldb, const OzWs& w,
+                    int t) {
+  const int n = static_cast<int>(N), k = static_cast<int>(K);
+  cudaError_t e = cudaMemsetAsync(w.colmax, 0, sizeof(unsigned long long) * N, st);
+  if (e != cudaSuccess) return e;
+  col_absmax_kernel<T><<<dim3(static_cast<unsigned>((N + 255) / 256),
+                              static_cast<unsigned>((K + OZ_COL_ROWS - 1) / OZ_COL_ROWS)),
+                         256, 0, st>>>(B, ldb, k, n, w.colmax);
+  col_exponent_finalize<<<static_cast<unsigned>((N + 255) / 256), 256, 0, st>>>(w.colmax, n, t,
+                                                                                 w.fx);
+  return cudaSuccess;
+}
+
+template <class T>
+void residues_b(cudaStream_t st, int64_t N, int64_t K, int64_t kpad, const T* B, int64_t ldb,
+                const OzWs& w, int l0, int l1, const CrtConst& cc) {
+  residue_bt_kernel<T><<<dim3(static_cast<unsigned>((N + 31) / 32),
+                              static_cast<unsigned>((kpad + OZ_BT_K - 1) / OZ_BT_K)),
+                         256, 0, st>>>(B, ldb, static_cast<int>(K), static_cast<int>(N),
+                                       static_cast<int>(kpad), w.fx, w.bres, l0, l1, cc);
+}
+
+template <class T>
+void residues_a(cudaStream_t st, int64_t M, int64_t K, int64_t kpad, const T* A, int64_t lda,
+                const OzWs& w, int l0, int l1, const CrtConst& cc) {
+  const unsigned rows_y = static_cast<unsigned>(std::min<int64_t>(M, 65535));
+  residue_a_kernel<T><<<dim3(static_cast<unsigned>((kpad / 8 + 127) / 128), rows_y), 128, 0, st>>>(
+      A, lda, static_cast<int>(M), static_cast<int>(K), static_cast<int>(kpad), w.ex, w.ares, l0,
+      l1, cc);
+}
+
+cudaError_t igemm(const Launch& L, cudaStream_t st, int64_t M, int64_t N, int64_t kpad, int s,
+                  const OzWs& w, int l0, int l1, const CrtConst& cc) {
+  CUtensorMap ta, tb;
+  if (!map3_u8(L, &ta, w.ares, kpad, M, s, IG_BM) || !map3_u8(L, &tb, w.bres, kpad, N, s, IG_BN))
+    return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(igemm_mod_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       IG_SMEM);
+  if (e != cudaSuccess) return e;
+  const int tiles_m = static_cast<int>((M + IG_BM - 1) / IG_BM);
+  const int tiles_n = static_cast<int>((N + IG_BN - 1) / IG_BN);
+  const int grid = static_cast<int>(
+      std::min<int64_t>(static_cast<int64_t>(tiles_m) * tiles_n * (l1 - l0), L.num_sms));
+  igemm_mod_kernel<<<grid, IG_THREADS, IG_SMEM, st>>>(ta, tb, w.cres, static_cast<int>(M),
+                                                      static_cast<int>(N), static_cast<int>(kpad),
+                                                      tiles_m, tiles_n, l0, l1 - l0, cc);
+  return cudaSuccess;
+}
+
+template <class T>
+void crt(cudaStream_t st, int64_t M, int64_t N, const OzWs& w, T* C, int64_t ldc,
+         const CrtConst& cc) {
+  const unsigned rows_y = static_cast<unsigned>(std::min<int64_t>(M, 65535));
+  crt_kernel<T><<<dim3(static_cast<unsigned>((N / 4 + 1 + 127) / 128), rows_y), 128, 0, st>>>(
+      w.cres, static_cast<int>(M), static_cast<int>(N), w.ex, w.fx, C, ldc, cc);
+}
+
+template <class T>
+cudaError_t prepare_b(const Launch& L, int64_t N, int64_t K, const T* B, int64_t ldb, void* ws) {
+  int s, t;
+  plan_for<T>(K, &s, &t);
+  CrtConst cc;
+  make_crt(s, &cc);
+  const int64_t kpad = (K + 15) / 16 * 16;
+  const OzWs w = layout(ws, 0, N, kpad, s);
+  cudaError_t e = scale_b<T>(L.stream, N, K, B, ldb, w, t);
+  if (e != cudaSuccess) return e;
+  residues_b<T>(L.stream, N, K, kpad, B, ldb, w, 0, s, cc);
+  for (int i = 0; i < 3; ++i) L.count();
+  return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t panel(const Launch& L, int64_t M, int64_t N, int64_t K, const T* A, int64_t lda, T* C,
+                  int64_t ldc, void* ws) {
+  int s, t;
+  plan_for<T>(K, &s, &t);
+  CrtConst cc;
+  make_crt(s, &cc);
+  const int64_t kpad = (K + 15) / 16 * 16;
+  const OzWs w = layout(ws, M, N, kpad, s);
+  cudaStream_t st = L.stream;
+  row_exponent_kernel<T><<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(
+      A, lda, static_cast<int>(M), static_cast<int>(K), t, w.ex);
+  residues_a<T>(st, M, K, kpad, A, lda, w, 0, s, cc);
+  cudaError_t e = igemm(L, st, M, N, kpad, s, w, 0, s, cc);
+  if (e != cudaSuccess) return e;
+  crt<T>(st, M, N, w, C, ldc, cc);
+  for (int i = 0; i < 4; ++i) L.count();
+  return cudaGetLastError();
 }
 
 template <class T>
 cudaError_t launch_gemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K, const T* A,
                               int64_t lda, const T* B, int64_t ldb, T* C, int64_t ldc, void* ws,
-                              cudaStream_t aux, cudaEvent_t* ev, int s, int t) {
+                              cudaStream_t aux, cudaEvent_t* ev) {
+  // Large problems: B prepared once, then A's one panel (the GEMMs fill the SMs).
+  // Below ~1.4e11 multiply-adds the residues and tensor-core GEMMs run in
+  // moduli groups: the (FP64-ALU bound) residues of group g+1 on `st` while
+  // the int8 GEMMs of group g run on `aux`, their blocks sharing the SMs.
+  // Measured: N=4096 3.0 -> 2.0 ms with 4 groups; from N ~ 8192 up the extra
+  // passes over A and B cost more than the overlap saves (N=16384: 64.5 vs
+  // 66.9 ms).
+  const double work = static_cast<double>(M) * N * K;
+  int s, t;
+  plan_for<T>(K, &s, &t);
+  const int groups = work <= 1.4e11 ? std::min(s, OZ_GROUPS) : 1;
+  if (groups == 1) {
+    cudaError_t e = prepare_b<T>(L, N, K, B, ldb, ws);
+    return e == cudaSuccess ? panel<T>(L, M, N, K, A, lda, C, ldc, ws) : e;
+  }
   CrtConst cc;
   make_crt(s, &cc);
-  cudaError_t e;
   const int64_t kpad = (K + 15) / 16 * 16;
-  int8_t* ares = static_cast<int8_t*>(ws);
-  int8_t* bres = ares + s * M * kpad;
-  uint8_t* cres = reinterpret_cast<uint8_t*>(bres + s * N * kpad);
-  int* ex =
-      reinterpret_cast<int*>(reinterpret_cast<uintptr_t>(cres + s * M * N + 15) & ~uintptr_t(15));
-  int* fx = ex + M;
-  unsigned long long* colmax = reinterpret_cast<unsigned long long*>(ex + ((M + N + 1) & ~int64_t(1)));
-  const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
+  const OzWs w = layout(ws, M, N, kpad, s);
   cudaStream_t st = L.stream;
-  // ---- scaling exponents
-  row_exponent_kernel<T><<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(A, lda, m, k, t, ex);
-  if ((e = cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * N, st)) != cudaSuccess) return e;
-  col_absmax_kernel<T><<<dim3(static_cast<unsigned>((N + 255) / 256),
-                           static_cast<unsigned>((K + OZ_COL_ROWS - 1) / OZ_COL_ROWS)),
-                      256, 0, st>>>(B, ldb, k, n, colmax);
-  col_exponent_finalize<<<static_cast<unsigned>((N + 255) / 256), 256, 0, st>>>(colmax, n, t, fx);
-  CUtensorMap ta, tb;
-  if (!map3_u8(L, &ta, ares, kpad, M, s, IG_BM) || !map3_u8(L, &tb, bres, kpad, N, s, IG_BN))
-    return cudaErrorInvalidValue;
-  if ((e = cudaFuncSetAttribute(igemm_mod_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                IG_SMEM)) != cudaSuccess)
-    return e;
-  const int tiles_m = static_cast<int>((M + IG_BM - 1) / IG_BM);
-  const int tiles_n = static_cast<int>((N + IG_BN - 1) / IG_BN);
-  const unsigned rows_y = static_cast<unsigned>(std::min<int64_t>(M, 65535));
-  // ---- residues and tensor-core GEMMs in moduli groups: the (FP64-ALU bound)
-  // residues of group g+1 run on `st` while the int8 GEMMs of group g run on
-  // `aux`, their blocks sharing the SMs.  Measured: N=4096 3.0 -> 2.0 ms with 4
-  // groups; from N ~ 8192 up the GEMMs fill the SMs and the extra passes over
-  // A and B cost more than the overlap saves (N=16384: 64.5 vs 66.9 ms), so
-  // large problems take one group.
-  const double work = static_cast<double>(M) * N * K;
-  const int groups = work <= 1.4e11 ? std::min(s, OZ_GROUPS) : 1;
+  cudaError_t e;
+  row_exponent_kernel<T><<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(
+      A, lda, static_cast<int>(M), static_cast<int>(K), t, w.ex);
+  if ((e = scale_b<T>(st, N, K, B, ldb, w, t)) != cudaSuccess) return e;
   for (int g = 0; g < groups; ++g) {
     const int l0 = s * g / groups, l1 = s * (g + 1) / groups;
-    residue_a_kernel<T><<<dim3(static_cast<unsigned>((kpad / 8 + 127) / 128), rows_y), 128, 0, st>>>(
-        A, lda, m, k, static_cast<int>(kpad), ex, ares, l0, l1, cc);
-    residue_bt_kernel<T><<<dim3(static_cast<unsigned>((N + 31) / 32),
-                             static_cast<unsigned>((kpad + OZ_BT_K - 1) / OZ_BT_K)),
-                        256, 0, st>>>(B, ldb, k, n, static_cast<int>(kpad), fx, bres, l0, l1, cc);
+    residues_a<T>(st, M, K, kpad, A, lda, w, l0, l1, cc);
+    residues_b<T>(st, N, K, kpad, B, ldb, w, l0, l1, cc);
     if ((e = cudaEventRecord(ev[g], st)) != cudaSuccess ||
-        (e = cudaStreamWaitEvent(aux, ev[g], 0)) != cudaSuccess)
+        (e = cudaStreamWaitEvent(aux, ev[g], 0)) != cudaSuccess ||
+        (e = igemm(L, aux, M, N, kpad, s, w, l0, l1, cc)) != cudaSuccess)
       return e;
-    const int grid = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(tiles_m) * tiles_n * (l1 - l0),
-                                                        L.num_sms));
-    igemm_mod_kernel<<<grid, IG_THREADS, IG_SMEM, aux>>>(ta, tb, cres, m, n, static_cast<int>(kpad),
-                                                         tiles_m, tiles_n, l0, l1 - l0, cc);
   }
   // ---- reconstruction after the last GEMM
   if ((e = cudaEventRecord(ev[groups], aux)) != cudaSuccess ||
       (e = cudaStreamWaitEvent(st, ev[groups], 0)) != cudaSuccess)
     return e;
-  crt_kernel<T><<<dim3(static_cast<unsigned>((N / 4 + 1 + 127) / 128), rows_y), 128, 0, st>>>(
-      cres, m, n, ex, fx, C, ldc, cc);
+  crt<T>(st, M, N, w, C, ldc, cc);
   for (int i = 0; i < 4 + 3 * groups; ++i) L.count();
   return cudaGetLastError();
 }
 
+}  // namespace
+
+size_t ozaki_workspace_bytes(int64_t m, int64_t n, int64_t k) {
+  return workspace_bytes<double>(m, n, k);
+}
+size_t ozaki_workspace_bytes_f32(int64_t m, int64_t n, int64_t k) {
+  return workspace_bytes<float>(m, n, k);
+}
+
+// fp32 through the same integer scheme: 30-bit scaling needs ~10 moduli at
+// k = 32768
+void ozaki_plan_f32(int64_t k, int* s, int* t) { ozaki_plan_bits(k, 30, s, t); }
+
 cudaError_t launch_dgemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K, const double* A,
                                int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                                void* ws, cudaStream_t aux, cudaEvent_t* ev) {
-  int s, t;
-  ozaki_plan(K, &s, &t);
-  return launch_gemm_ozaki<double>(L, M, N, K, A, lda, B, ldb, C, ldc, ws, aux, ev, s, t);
-}
-
-// fp32 through the same integer scheme: 30-bit scaling (1.4 * 2^-30 ~ 1e-9,
-// far below the fp32 output rounding) needs ~10 moduli at k = 32768
-void ozaki_plan_f32(int64_t k, int* s, int* t) { ozaki_plan_bits(k, 30, s, t); }
-
-size_t ozaki_workspace_bytes_f32(int64_t m, int64_t n, int64_t k) {
-  int s, t;
-  ozaki_plan_f32(k, &s, &t);
-  const int64_t kpad = (k + 15) / 16 * 16;
-  return static_cast<size_t>(s) * (m * kpad + n * kpad + m * n) + sizeof(int) * (m + n + 2) +
-         sizeof(unsigned long long) * n + 1024;
+  return launch_gemm_ozaki<double>(L, M, N, K, A, lda, B, ldb, C, ldc, ws, aux, ev);
 }
 
 cudaError_t launch_sgemm_ozaki(const Launch& L, int64_t M, int64_t N, int64_t K, const float* A,
                                int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
                                void* ws, cudaStream_t aux, cudaEvent_t* ev) {
-  int s, t;
-  ozaki_plan_f32(K, &s, &t);
-  return launch_gemm_ozaki<float>(L, M, N, K, A, lda, B, ldb, C, ldc, ws, aux, ev, s, t);
+  return launch_gemm_ozaki<float>(L, M, N, K, A, lda, B, ldb, C, ldc, ws, aux, ev);
+}
+
+cudaError_t launch_ozaki_prepare_b(const Launch& L, int64_t N, int64_t K, const double* B,
+                                   int64_t ldb, void* ws) {
+  return prepare_b<double>(L, N, K, B, ldb, ws);
+}
+cudaError_t launch_ozaki_prepare_b(const Launch& L, int64_t N, int64_t K, const float* B,
+                                   int64_t ldb, void* ws) {
+  return prepare_b<float>(L, N, K, B, ldb, ws);
+}
+cudaError_t launch_ozaki_panel(const Launch& L, int64_t M, int64_t N, int64_t K, const double* A,
+                               int64_t lda, double* C, int64_t ldc, void* ws) {
+  return panel<double>(L, M, N, K, A, lda, C, ldc, ws);
+}
+cudaError_t launch_ozaki_panel(const Launch& L, int64_t M, int64_t N, int64_t K, const float* A,
+                               int64_t lda, float* C, int64_t ldc, void* ws) {
+  return panel<float>(L, M, N, K, A, lda, C, ldc, ws);
 }
 
 cudaError_t preload_ozaki() {

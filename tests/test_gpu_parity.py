@@ -259,6 +259,17 @@ def test_ozaki_mode_host_entry(ctx, oracle):
     cf, _ = ctx.matmul_host(a.astype(np.float32), b.astype(np.float32), mode=P.MODE_OZAKI)
     assert (cf == host(ctx.sgemm(dev(a.astype(np.float32)), dev(b.astype(np.float32)),
                                  mode=P.MODE_OZAKI))).all()
+    # big enough for the panel pipeline (B prepared once, A in 512-row panels,
+    # a ragged last one): still the one-shot bits, fp64 and fp32
+    for (m, k, n) in [(2500, 4100, 1000), (1100, 3000, 3100)]:
+        a = oracle.fill(oracle.DIST_UNIFORM, 97, m, k)
+        b = oracle.fill(oracle.DIST_UNIFORM, 98, k, n) * 1e-3
+        want = host(ctx.dgemm(dev(a), dev(b), mode=P.MODE_OZAKI))
+        c, el = ctx.matmul_host(a, b, mode=P.MODE_OZAKI)
+        assert el > 0 and (bits(c) == bits(want)).all(), (m, k, n)
+        af, bf = a.astype(np.float32), b.astype(np.float32)
+        cf, _ = ctx.matmul_host(af, bf, mode=P.MODE_OZAKI)
+        assert (cf == host(ctx.sgemm(dev(af), dev(bf), mode=P.MODE_OZAKI))).all(), (m, k, n)
 
 
 def test_ozaki_mode_tall_and_wide(ctx, oracle):
