@@ -318,6 +318,13 @@ def run_ours(args) -> None:
         if i > 0:
             e2e_t.append(max(el, 0.0) if root else wall)
     e2e_s = sum(e2e_t) / len(e2e_t)
+    if emulated is not None:  # the emulated mode through the same host entry
+        oz_e2e = [ctx.master_run_host(a_h, b_h, c_h, mode=P.MODE_OZAKI)[1] for _ in range(3)][1:]
+        oz_s = sum(oz_e2e) / len(oz_e2e)
+        emulated["e2e"] = {"value": flops / oz_s / 1e9, "unit": "GFLOP/s",
+                           "h2d_bytes_per_step": 2 * 8 * n * n, "d2h_bytes_per_step": 8 * n * n,
+                           "seconds_per_step": oz_s,
+                           "entry": "mmws_gpu_master_run_host (C ABI, pinned host A/B/C), MODE_OZAKI"}
 
     cpu = None
     if root and world == 1 and not args.no_cpu_baseline:
