@@ -54,6 +54,12 @@ struct CrtConst {
   uint64_t m_hi[OZ_MAX_MODULI];
   uint64_t P_lo, P_hi;
   double P_d, inv_P;
+  // reconstruction (crt_kernel): fp32 forms of p_l, 1/p_l, w_l and the two
+  // offsets of its (y w) mod p_l step, and D = -256 sum_l P/p_l mod P in
+  // 32-bit limbs (cancels the +256 that keeps every residue term positive)
+  float pf[OZ_MAX_MODULI], invf[OZ_MAX_MODULI], wf[OZ_MAX_MODULI];
+  float c0[OZ_MAX_MODULI], c1[OZ_MAX_MODULI];
+  uint32_t d[4];
   int s;
 };
 
@@ -428,69 +434,90 @@ __global__ void __launch_bounds__(IG_THREADS, 1)
 // ---------------------------------------------------------------- reconstruction
 // C'_ij = sum_l ((y_l w_l) mod p_l) (P / p_l)  mod P, lifted to (-P/2, P/2],
 // then C_ij = C' 2^-(e_i + f_j).  Grid (column blocks, rows); a thread takes 4
-// consecutive columns (one 4-byte load per modulus).
+// consecutive columns (one 4-byte load per modulus, all s loads issued before
+// any arithmetic).
+//
+// Per residue y (a byte), on the FP32 pipe and exact throughout:
+//   Y  = 2^23 + y                     one PRMT (byte into a float's mantissa)
+//   t  = Y w + (2^23 + 256 - 2^23 w)  = y w + 2^23 + 256   (one FFMA, exact)
+//   q ~ rint(t / p - (2^23 + 256) / p) = rint(y w / p)     (error < 0.01)
+//   r  = t - q p                      = 2^23 + 256 + z, z = y w - q p, |z| < p/2 + 2
+//   u  = mantissa(r) & 0x1ff          = z + 256 in [1, 511]
+// and u (P / p_l) is summed in four 32-bit limbs (IMAD.WIDE), D folding the
+// +256 back out.  The sum stays below 44 P (< 2^124 for the s <= 15 the
+// plans use); the nearest multiple of P comes from a double estimate, and the
+// remainder is the signed C' itself (|C'| <= P/4 by the plan).
+// acc += a * b (32 x 32 -> 64 bits) as one IMAD.WIDE.U32: written out so the
+// compiler does not re-associate the four limb products into 64-bit multiplies
+MMWS_DEVICE void mad_wide(uint64_t& acc, uint32_t a, uint32_t b) {
+  asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc) : "r"(a), "r"(b));
+}
+
 MMWS_DEVICE double u128_to_double(unsigned __int128 v) {  // at most one extra rounding
   return static_cast<double>(static_cast<uint64_t>(v >> 64)) * 18446744073709551616.0 +
          static_cast<double>(static_cast<uint64_t>(v));
 }
 
-template <class TO>
-__global__ void crt_kernel(const uint8_t* __restrict__ Cres, int m, int n,
-                           const int* __restrict__ e, const int* __restrict__ f,
-                           TO* __restrict__ C, int64_t ldc,
-                           const __grid_constant__ CrtConst c_crt) {
+// S: the number of moduli as a compile-time count (the plans use 8..15; other
+// counts run as S = 16 with zero terms: make_crt leaves P / p_l = 0 there)
+template <class TO, int S>
+__global__ void __launch_bounds__(128) crt_kernel(const uint8_t* __restrict__ Cres, int m, int n,
+                                                  const int* __restrict__ e,
+                                                  const int* __restrict__ f, TO* __restrict__ C,
+                                                  int64_t ldc,
+                                                  const __grid_constant__ CrtConst c_crt) {
   const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (j0 >= n) return;
+  const int64_t plane = static_cast<int64_t>(m) * n;
+  const int s = c_crt.s;
+  const bool vec = (n % 4) == 0;  // 4-byte aligned words (planes and rows)
+  static_assert(S >= 1 && S <= OZ_MAX_MODULI, "moduli count");
+  const unsigned __int128 P =
+      (static_cast<unsigned __int128>(c_crt.P_hi) << 64) | static_cast<unsigned __int128>(c_crt.P_lo);
   for (int i = blockIdx.y; i < m; i += gridDim.y) {
-    const int64_t plane = static_cast<int64_t>(m) * n;
     const int64_t base = static_cast<int64_t>(i) * n + j0;
-    const int s = c_crt.s;
-    const unsigned __int128 P =
-        (static_cast<unsigned __int128>(c_crt.P_hi) << 64) |
-        static_cast<unsigned __int128>(c_crt.P_lo);
-    const bool vec = (n % 4) == 0;  // 4-byte aligned words (planes and rows)
-    // sum_l z_l (P / p_l), z_l < 256, in four 32-bit limbs of P / p_l: each
-    // limb product is < 2^40, so 64-bit limb sums cannot overflow for s <= 16
-    uint64_t limb[4][4] = {};
-    for (int l = 0; l < s; ++l) {
-      const int p = c_crt.p[l];
-      const float pf = static_cast<float>(p), inv = 1.0f / pf, wf = static_cast<float>(c_crt.w[l]);
-      uint32_t word = 0;
-      if (vec) {
-        word = *reinterpret_cast<const uint32_t*>(Cres + l * plane + base);
-      } else {
-        for (int q = 0; q < 4 && j0 + q < n; ++q)
-          word |= static_cast<uint32_t>(Cres[l * plane + base + q]) << (8 * q);
-      }
-      const uint32_t m0 = static_cast<uint32_t>(c_crt.m_lo[l]);
-      const uint32_t m1 = static_cast<uint32_t>(c_crt.m_lo[l] >> 32);
-      const uint32_t m2 = static_cast<uint32_t>(c_crt.m_hi[l]);
-      const uint32_t m3 = static_cast<uint32_t>(c_crt.m_hi[l] >> 32);
+    uint32_t word[S];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        // (y w) mod p in fp32 without I2F / F2I / FRND (slow multi-function
-        // ops): 2^23-offset tricks for int <-> float, 1.5 * 2^23 add for rint;
-        // every value is an integer < 2^17, so all steps are exact
-        const float y = __int_as_float(0x4B000000 | ((word >> (8 * q)) & 0xffu)) - 8388608.0f;
-        const float yw = y * wf;
-        const float qf = __fsub_rn(__fadd_rn(yw * inv, 12582912.0f), 12582912.0f);
-        float zf = __fmaf_rn(-qf, pf, yw);
-        zf += zf < 0.f ? pf : 0.f;
-        zf -= zf >= pf ? pf : 0.f;
-        const uint32_t z = __float_as_uint(__fadd_rn(zf, 8388608.0f)) & 0x3ffu;
-        limb[q][0] += static_cast<uint64_t>(z) * m0;
-        limb[q][1] += static_cast<uint64_t>(z) * m1;
-        limb[q][2] += static_cast<uint64_t>(z) * m2;
-        limb[q][3] += static_cast<uint64_t>(z) * m3;
+    for (int l = 0; l < S; ++l) {
+      word[l] = 0;
+      if (l < s) {
+        if (vec) {
+          word[l] = __ldcs(reinterpret_cast<const unsigned int*>(Cres + l * plane + base));
+        } else {
+          for (int q = 0; q < 4 && j0 + q < n; ++q)
+            word[l] |= static_cast<uint32_t>(Cres[l * plane + base + q]) << (8 * q);
+        }
       }
     }
-    unsigned __int128 acc[4];
+    uint64_t limb[4][4];
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      acc[q] = static_cast<unsigned __int128>(limb[q][0]) +
-               (static_cast<unsigned __int128>(limb[q][1]) << 32) +
-               (static_cast<unsigned __int128>(limb[q][2]) << 64) +
-               (static_cast<unsigned __int128>(limb[q][3]) << 96);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) limb[q][b] = c_crt.d[b];
+#pragma unroll
+    for (int l = 0; l < S; ++l) {
+      {
+        const float pf = c_crt.pf[l], inv = c_crt.invf[l], wf = c_crt.wf[l];
+        const float c0 = c_crt.c0[l], c1 = c_crt.c1[l];
+        const uint32_t m0 = static_cast<uint32_t>(c_crt.m_lo[l]);
+        const uint32_t m1 = static_cast<uint32_t>(c_crt.m_lo[l] >> 32);
+        const uint32_t m2 = static_cast<uint32_t>(c_crt.m_hi[l]);
+        const uint32_t m3 = static_cast<uint32_t>(c_crt.m_hi[l] >> 32);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          // byte q of the word under exponent byte 0x4B: 2^23 + y
+          const float Y = __uint_as_float(__byte_perm(word[l], 0x4B000000u, 0x7540u + q));
+          const float t = __fmaf_rn(Y, wf, c0);
+          const float qf = __fsub_rn(__fadd_rn(__fmaf_rn(t, inv, -c1), 12582912.0f), 12582912.0f);
+          const float r = __fmaf_rn(-qf, pf, t);
+          const uint32_t u = __float_as_uint(r) & 0x1ffu;
+          mad_wide(limb[q][0], u, m0);
+          mad_wide(limb[q][1], u, m1);
+          mad_wide(limb[q][2], u, m2);
+          mad_wide(limb[q][3], u, m3);
+        }
+      }
+    }
     const int ex = e[i];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -502,15 +529,21 @@ __global__ void crt_kernel(const uint8_t* __restrict__ Cres, int m, int n,
         *out = static_cast<TO>(__longlong_as_double(0x7ff8000000000000LL));
         continue;
       }
-      // acc < s P: reduce mod P from a floating-point quotient estimate
-      uint64_t qt = static_cast<uint64_t>(u128_to_double(acc[q]) * c_crt.inv_P);  // +-1 fixed below
-      unsigned __int128 qP = static_cast<unsigned __int128>(qt) * P;
-      while (qP > acc[q]) qP -= P;
-      unsigned __int128 r = acc[q] - qP;
-      while (r >= P) r -= P;
-      const bool neg = r > (P >> 1);  // signed lift
-      const double d = u128_to_double(neg ? P - r : r);
-      *out = static_cast<TO>(ldexp(neg ? -d : d, -(ex + fx)));
+      const unsigned __int128 acc = static_cast<unsigned __int128>(limb[q][0]) +
+                                    (static_cast<unsigned __int128>(limb[q][1]) << 32) +
+                                    (static_cast<unsigned __int128>(limb[q][2]) << 64) +
+                                    (static_cast<unsigned __int128>(limb[q][3]) << 96);
+      // nearest multiple of P (the quotient is < 64)
+      const uint32_t qt = __double2uint_rn(u128_to_double(acc) * c_crt.inv_P);
+      const __int128 r = static_cast<__int128>(acc - static_cast<unsigned __int128>(qt) * P);
+      const bool neg = r < 0;
+      const double d = u128_to_double(static_cast<unsigned __int128>(neg ? -r : r));
+      const int sh = ex + fx;  // C = C' 2^-sh: one DMUL by an exact power of two when it is normal
+      const double v = neg ? -d : d;
+      const double res = (sh > -1023 && sh < 1023)
+                             ? v * __longlong_as_double(static_cast<long long>(1023 - sh) << 52)
+                             : ldexp(v, -sh);
+      *out = static_cast<TO>(res);
     }
   }
 }
@@ -534,17 +567,32 @@ void make_crt(int s, CrtConst* c) {
   c->s = s;
   unsigned __int128 P = 1;
   for (int l = 0; l < s; ++l) P *= static_cast<unsigned>(kModuli[l]);
-  for (int l = 0; l < s; ++l) {
+  unsigned __int128 sumM = 0;
+  for (int l = 0; l < OZ_MAX_MODULI; ++l) {
     const int p = kModuli[l];
-    const unsigned __int128 M = P / static_cast<unsigned>(p);
-    const int mr = static_cast<int>(M % static_cast<unsigned>(p));
+    const unsigned __int128 M = l < s ? P / static_cast<unsigned>(p) : 0;
     int w = 1;
-    while ((mr * w) % p != 1) ++w;  // p <= 256: brute force
+    if (l < s) {
+      const int mr = static_cast<int>(M % static_cast<unsigned>(p));
+      while ((mr * w) % p != 1) ++w;  // p <= 256: brute force
+      sumM = (sumM + M) % P;
+    }
     c->p[l] = p;
     c->w[l] = w;
     c->m_lo[l] = static_cast<uint64_t>(M);
     c->m_hi[l] = static_cast<uint64_t>(M >> 64);
+    c->pf[l] = static_cast<float>(p);
+    c->invf[l] = 1.0f / static_cast<float>(p);
+    c->wf[l] = static_cast<float>(w);
+    // exact: 256 (2^15 (1 - w) + 1), 24 significant bits at most
+    c->c0[l] = 8388864.0f - 8388608.0f * static_cast<float>(w);
+    c->c1[l] = 8388864.0f * c->invf[l];
   }
+  // D = (-256 sum M_l) mod P
+  unsigned __int128 k256 = sumM;  // 256 sumM mod P by doubling (P < 2^126: no overflow)
+  for (int b = 0; b < 8; ++b) k256 = (k256 * 2u) % P;
+  const unsigned __int128 D = k256 == 0 ? 0 : P - k256;
+  for (int b = 0; b < 4; ++b) c->d[b] = static_cast<uint32_t>(D >> (32 * b));
   c->P_lo = static_cast<uint64_t>(P);
   c->P_hi = static_cast<uint64_t>(P >> 64);
   c->P_d = static_cast<double>(c->P_hi) * 18446744073709551616.0 + static_cast<double>(c->P_lo);
@@ -680,8 +728,25 @@ template <class T>
 void crt(cudaStream_t st, int64_t M, int64_t N, const OzWs& w, T* C, int64_t ldc,
          const CrtConst& cc) {
   const unsigned rows_y = static_cast<unsigned>(std::min<int64_t>(M, 65535));
-  crt_kernel<T><<<dim3(static_cast<unsigned>((N / 4 + 1 + 127) / 128), rows_y), 128, 0, st>>>(
-      w.cres, static_cast<int>(M), static_cast<int>(N), w.ex, w.fx, C, ldc, cc);
+  const dim3 grid(static_cast<unsigned>((N / 4 + 1 + 127) / 128), rows_y);
+  const int m = static_cast<int>(M), n = static_cast<int>(N);
+  switch (cc.s) {
+#define MMWS_CRT_CASE(S_)                                                        \
+  case S_:                                                                       \
+    crt_kernel<T, S_><<<grid, 128, 0, st>>>(w.cres, m, n, w.ex, w.fx, C, ldc, cc); \
+    break;
+    MMWS_CRT_CASE(8)
+    MMWS_CRT_CASE(9)
+    MMWS_CRT_CASE(10)
+    MMWS_CRT_CASE(11)
+    MMWS_CRT_CASE(12)
+    MMWS_CRT_CASE(13)
+    MMWS_CRT_CASE(14)
+    MMWS_CRT_CASE(15)
+#undef MMWS_CRT_CASE
+    default:
+      crt_kernel<T, OZ_MAX_MODULI><<<grid, 128, 0, st>>>(w.cres, m, n, w.ex, w.fx, C, ldc, cc);
+  }
 }
 
 template <class T>
@@ -807,12 +872,22 @@ cudaError_t launch_ozaki_panel(const Launch& L, int64_t M, int64_t N, int64_t K,
   return panel<float>(L, M, N, K, A, lda, C, ldc, ws);
 }
 
+template <class T>
+cudaError_t preload_crt() {
+  return preload_kernels(crt_kernel<T, 8>, crt_kernel<T, 9>, crt_kernel<T, 10>, crt_kernel<T, 11>,
+                         crt_kernel<T, 12>, crt_kernel<T, 13>, crt_kernel<T, 14>,
+                         crt_kernel<T, 15>, crt_kernel<T, OZ_MAX_MODULI>);
+}
+
 cudaError_t preload_ozaki() {
-  return preload_kernels(row_exponent_kernel<double>, col_absmax_kernel<double>,
-                         col_exponent_finalize, residue_a_kernel<double>,
-                         residue_bt_kernel<double>, igemm_mod_kernel, crt_kernel<double>,
-                         row_exponent_kernel<float>, col_absmax_kernel<float>,
-                         residue_a_kernel<float>, residue_bt_kernel<float>, crt_kernel<float>);
+  cudaError_t e = preload_kernels(row_exponent_kernel<double>, col_absmax_kernel<double>,
+                                  col_exponent_finalize, residue_a_kernel<double>,
+                                  residue_bt_kernel<double>, igemm_mod_kernel,
+                                  row_exponent_kernel<float>, col_absmax_kernel<float>,
+                                  residue_a_kernel<float>, residue_bt_kernel<float>);
+  if (e == cudaSuccess) e = preload_crt<double>();
+  if (e == cudaSuccess) e = preload_crt<float>();
+  return e;
 }
 
 }  // namespace mmws_impl
