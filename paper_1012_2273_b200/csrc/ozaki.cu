@@ -60,6 +60,7 @@ struct CrtConst {
   float pf[OZ_MAX_MODULI], invf[OZ_MAX_MODULI], wf[OZ_MAX_MODULI];
   float c0[OZ_MAX_MODULI], c1[OZ_MAX_MODULI];
   uint32_t d[4];
+  double pd[OZ_MAX_MODULI], invd[OZ_MAX_MODULI];  // residue kernels: p_l, fl(1 / p_l)
   int s;
 };
 
@@ -126,20 +127,31 @@ __global__ void col_exponent_finalize(const unsigned long long* __restrict__ col
   f[j] = amax == 0.0 ? 0 : t - x;
 }
 
-// signed residue of an integer-valued double (|x| < 2^53): exact
-MMWS_DEVICE int8_t sresidue(double x, int p) {
-  const double pd = static_cast<double>(p);
-  const double q = floor(x * (1.0 / pd));
-  double r = fma(-q, pd, x);  // exact: |q p| ~ |x| < 2^53, result an integer < 2p
-  if (r < 0.0) r += pd;
-  if (r >= pd) r -= pd;
-  int ri = static_cast<int>(r);
-  if (ri >= (p + 1) / 2) ri -= p;
-  return static_cast<int8_t>(ri);
+// signed residue of an integer-valued double (|x| < 2^52), on the FP64 pipe
+// without conversions: q = rint(x / p) from one DFMA against 1.5 * 2^52
+// (|x / p| < 2^45, so the sum lands where the ulp is 1), r = x - q p exactly
+// (one DFMA), and r's two's-complement low word read off r + 1.5 * 2^52.  The
+// estimate x * fl(1/p) is within 0.006 of x / p, so |r| <= p/2 + 1 and r > 127
+// only for p in {255, 256}: one subtraction of p brings every case into int8.
+// Any representative is fine: the GEMM epilogue reduces mod p.
+constexpr double OZ_MAGIC = 6755399441055744.0;  // 1.5 * 2^52
+MMWS_DEVICE uint32_t sresidue(double x, double pd, double inv) {
+  const double q = __dadd_rn(__fma_rn(x, inv, OZ_MAGIC), -OZ_MAGIC);
+  const double r = __fma_rn(-q, pd, x);
+  int ri = static_cast<int>(__double2loint(__dadd_rn(r, OZ_MAGIC)));
+  ri -= ri > 127 ? static_cast<int>(pd) : 0;
+  return static_cast<uint32_t>(ri) & 0xffu;
 }
 
+// rint(v 2^ex), |result| < 2^52: one DMUL by an exact power of two where it is
+// normal (the product is then exact or, for far-below-one results, rounds to
+// a value whose rint is the same zero), ldexp otherwise
 MMWS_DEVICE double scaled_int(double v, int ex) {
-  return ex == OZ_NONFINITE ? 0.0 : rint(ldexp(v, ex));
+  if (ex == OZ_NONFINITE) return 0.0;
+  const double y = (ex > -1023 && ex < 1024)
+                       ? v * __longlong_as_double(static_cast<long long>(1023 + ex) << 52)
+                       : ldexp(v, ex);
+  return rint(y);
 }
 
 // residues of A' = rint(A 2^e): res[l][i][j], j < kpad (zero padding).
@@ -160,12 +172,14 @@ __global__ void residue_a_kernel(const T* __restrict__ A, int64_t lda, int m, in
     const int64_t plane = static_cast<int64_t>(m) * kpad;
     const int64_t o = static_cast<int64_t>(i) * kpad + j0;
     for (int l = l0; l < l1; ++l) {
-      const int p = c_crt.p[l];
-      unsigned long long w = 0;
+      const double pd = c_crt.pd[l], inv = c_crt.invd[l];
+      uint32_t lo = 0, hi = 0;
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        w |= static_cast<unsigned long long>(static_cast<uint8_t>(sresidue(x[q], p))) << (8 * q);
-      *reinterpret_cast<unsigned long long*>(res + l * plane + o) = w;
+      for (int q = 0; q < 4; ++q) {
+        lo |= sresidue(x[q], pd, inv) << (8 * q);
+        hi |= sresidue(x[q + 4], pd, inv) << (8 * q);
+      }
+      *reinterpret_cast<uint2*>(res + l * plane + o) = make_uint2(lo, hi);
     }
   }
 }
@@ -205,12 +219,14 @@ __global__ void __launch_bounds__(256) residue_bt_kernel(const T* __restrict__ B
   const int64_t plane = static_cast<int64_t>(n) * kpad;
   const int64_t o = static_cast<int64_t>(c) * kpad + rq;
   for (int l = l0; l < l1; ++l) {
-    const int p = c_crt.p[l];
-    unsigned long long w = 0;
+    const double pd = c_crt.pd[l], inv = c_crt.invd[l];
+    uint32_t lo = 0, hi = 0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
-      w |= static_cast<unsigned long long>(static_cast<uint8_t>(sresidue(x[q], p))) << (8 * q);
-    *reinterpret_cast<unsigned long long*>(res + l * plane + o) = w;
+    for (int q = 0; q < 4; ++q) {
+      lo |= sresidue(x[q], pd, inv) << (8 * q);
+      hi |= sresidue(x[q + 4], pd, inv) << (8 * q);
+    }
+    *reinterpret_cast<uint2*>(res + l * plane + o) = make_uint2(lo, hi);
   }
 }
 
@@ -581,6 +597,8 @@ void make_crt(int s, CrtConst* c) {
     c->w[l] = w;
     c->m_lo[l] = static_cast<uint64_t>(M);
     c->m_hi[l] = static_cast<uint64_t>(M >> 64);
+    c->pd[l] = static_cast<double>(p);
+    c->invd[l] = 1.0 / static_cast<double>(p);
     c->pf[l] = static_cast<float>(p);
     c->invf[l] = 1.0f / static_cast<float>(p);
     c->wf[l] = static_cast<float>(w);
