@@ -56,11 +56,12 @@ def workload_config(n: int, n_gpus: int, mode: str) -> dict:
 
 
 # ----------------------------------------------------------------------------- CPU baseline
-def cpu_reference_sample(n: int, repeats: int = 1):
+def cpu_reference_sample(n: int, repeats: int = 1, serial: bool = False):
     """The reference's matmul_threads (all host threads) on a row sample of the
     N x N workload: C[0:r, :] = A[0:r, :] . B with r = #host threads (one row
     per worker, static_partition).  Bitwise the same rows the full product
-    would give.  Returns dict(value GFLOP/s, seconds, cores, kind, sample)."""
+    would give.  Returns dict(value GFLOP/s, seconds, cores, kind, sample), plus
+    the serial matmul_seq on one row ("serial") when asked."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O  # noqa: E402  (test infrastructure: CPU baseline only)
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
@@ -76,11 +77,25 @@ def cpu_reference_sample(n: int, repeats: int = 1):
         O.matmul_threads(a, b, cores)
         best = time.perf_counter() - t0
     flops = 2.0 * rows * n * n
-    return {"value": flops / best / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": kind,
-            "seconds": best,
-            "sample": f"{rows} rows x {n} cols of C = A.B (N={n}, uniform seeds 0/1) via "
-                      f"{'mmws::matmul_threads' if kind == 'reference' else 'oracle_matmul_threads'}"
-                      f"({cores} workers), time_model bracket"}
+    out = {"value": flops / best / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": kind,
+           "seconds": best,
+           "sample": f"{rows} rows x {n} cols of C = A.B (N={n}, uniform seeds 0/1) via "
+                     f"{'mmws::matmul_threads' if kind == 'reference' else 'oracle_matmul_threads'}"
+                     f"({cores} workers), time_model bracket"}
+    if serial:  # the serial path on one core: the first row of the same sample
+        a1 = a[:1]
+        if kind == "reference":
+            t1, _ = O.ref_time_matmul(a1, b, 0, repeats=1)
+        else:
+            t0 = time.perf_counter()
+            O.matmul_seq(a1, b)
+            t1 = time.perf_counter() - t0
+        out["serial"] = {
+            "value": 2.0 * n * n / t1 / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": kind,
+            "seconds": t1,
+            "sample": f"1 row x {n} cols of C = A.B via "
+                      f"{'mmws::matmul_seq' if kind == 'reference' else 'oracle_matmul_seq'}"}
+    return out
 
 
 def run_reference(args) -> None:
@@ -90,7 +105,7 @@ def run_reference(args) -> None:
     times = []
     sample = None
     for step in range(args.warmup + args.steps):
-        sample = cpu_reference_sample(args.n)
+        sample = cpu_reference_sample(args.n, serial=step == args.warmup + args.steps - 1)
         if step >= args.warmup:
             times.append(sample["seconds"])
     rows = sample["cores"]
@@ -104,7 +119,8 @@ def run_reference(args) -> None:
             "generated on the device", "generated on the host"),
         "config": workload_config(args.n, args.gpus, "reference-cpu"),
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": sample["cores"],
-                         "kind": sample["kind"], "sample": sample["sample"]},
+                         "kind": sample["kind"], "sample": sample["sample"],
+                         "serial": sample["serial"]},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -328,8 +344,8 @@ def run_ours(args) -> None:
 
     cpu = None
     if root and world == 1 and not args.no_cpu_baseline:
-        s = cpu_reference_sample(n)
-        cpu = {k: s[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        s = cpu_reference_sample(n, serial=True)
+        cpu = {k: s[k] for k in ("value", "unit", "cores", "kind", "sample", "serial")}
 
     if root and world > 1:  # cost model of this schedule at the measured 1-GPU kernel rate
         t_model, _, _ = P.rowblock_cost(n, n, n, world, 8, link_bw,
