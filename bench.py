@@ -182,16 +182,17 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- our arm
-def profiled_traffic(n: int):
+def profiled_traffic(n: int, plan: str):
     """dram bytes per launch of the dominant kernel from the committed ncu
-    capture (profiles/*_ncu_summary.json), if one matches this N."""
+    capture (profiles/*_ncu_summary*.json), if one matches this N and kernel
+    configuration (ctx.last_plan)."""
     import glob
     for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_summary*.json")), reverse=True):
         try:
             with open(p) as f:
                 d = json.load(f)
             for k in d.get("kernels", []):
-                if k.get("n") == n and k.get("role") == "dominant":
+                if k.get("n") == n and k.get("role") == "dominant" and k.get("plan") == plan:
                     return k.get("dram_bytes"), os.path.relpath(p, ROOT)
         except Exception:
             continue
@@ -253,6 +254,7 @@ def run_ours(args) -> None:
     for _ in range(args.steps):
         ctx.rowblock(n, n, n, A, B, C, mode=mode)
         kern_ms.append(ctx.last_kernel_ms)
+    plan = ctx.last_plan
     e1.record(ext)
     torch.cuda.synchronize()
     launches = ctx.launches - l0
@@ -275,7 +277,7 @@ def run_ours(args) -> None:
     rows0 = P.split_rows(n, world)[0][1]
     kern_avg_ms = sum(kern_ms) / len(kern_ms)
     achieved = 2.0 * rows0 * n * n / (kern_avg_ms / 1e3) / 1e12
-    traffic, traffic_src = profiled_traffic(n) if world == 1 else (None, None)
+    traffic, traffic_src = profiled_traffic(n, plan) if world == 1 else (None, None)
 
     # The same multiply emulated on the int8 tensor cores (MODE_OZAKI, opt-in;
     # the headline above stays on the FP64 tensor path): device-resident, CUDA
@@ -363,7 +365,7 @@ def run_ours(args) -> None:
             "roofline": {
                 "bound": "tensor", "achieved": achieved, "peak": dmma_peak, "unit": "TFLOP/s",
                 "frac": achieved / dmma_peak, "traffic": traffic,
-                "kernel": "dgemm_dmma_kernel<128x128x16, 6 stages> (DMMA.8x8x4)",
+                "kernel": plan + " (DMMA.8x8x4)",
                 "peak_source": "measured live in this run: DMMA.8x8x4 throughput probe "
                                "(FP64 tensor pipe; MEASURED_PEAKS.json has no fp64 figure)",
                 "peak_nominal": NOMINAL_FP64_TFLOPS, "frac_of_nominal": achieved / NOMINAL_FP64_TFLOPS,

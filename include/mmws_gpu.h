@@ -56,9 +56,10 @@ enum {
  *   DMMA       FP64 tensor path (mma.sync m8n8k4 -> DMMA.8x8x4), 128x128 tiles,
  *              TMA + mbarrier pipeline.  Bit-exact for integer-valued inputs
  *              whose partial sums stay below 2^53; normwise <= 1e-12 otherwise.
- *   DMMA_SMALL same math on 64x64 tiles (more CTAs for N < ~2000).
+ *   DMMA_SMALL same math on 32x32 tiles, 6 CTAs per SM (more CTAs for
+ *              N < ~2000); bitwise the DMMA result.
  *   AUTO       fp64: the latency path (32x32 tiles, one DFMA chain per
- *              element, no TMA) when n <= 256 and k <= 256, else DMMA or
+ *              element, no TMA) when n <= 96 and k <= 96, else DMMA or
  *              DMMA_SMALL by tile count -- the choice never depends on m, so
  *              row slices of a problem get the whole problem's bits; fp32: FFMA.
  *              EXACT also switches to 32x32 tiles for small problems.
@@ -263,6 +264,10 @@ int mmws_gpu_master_run_host_f32(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_
 /* Device time (ms, CUDA events on the launch stream) of this rank's multiply
  * kernel(s) in the most recent row-block / master_run call. */
 int mmws_gpu_last_kernel_ms(mmws_gpu_ctx* ctx, double* ms);
+/* Kernel configuration (a static, NUL-terminated string, e.g.
+ * "dgemm_dmma_kernel<64x64, 4 math warps, 3 CTAs/SM>") the most recent
+ * multiply on this context launched; "" before the first one. */
+int mmws_gpu_last_plan(mmws_gpu_ctx* ctx, const char** name);
 
 /* Cost model of one row-block round (the analogue of the reference's
  * cost_model.hpp:36-70): predicted seconds given the NVLink bandwidth per

@@ -60,6 +60,7 @@ SIGNATURES = {
     "mmws_gpu_master_run_host": (_i, [_v, _i64, _i64, _i64, _v, _v, _v, _i, _p(_d)]),
     "mmws_gpu_master_run_host_f32": (_i, [_v, _i64, _i64, _i64, _v, _v, _v, _i, _p(_d)]),
     "mmws_gpu_last_kernel_ms": (_i, [_v, _p(_d)]),
+    "mmws_gpu_last_plan": (_i, [_v, _p(C.c_char_p)]),
     "mmws_gpu_rowblock_cost": (_i, [_i64, _i64, _i64, _i, _i, _d, _d, _p(_d), _p(_d), _p(_d)]),
     "mmws_gpu_rowblock_plan": (_i, [_i64, _i64, _i64, _i, _p(_i32), _p(_i32), _p(_i32), _p(_i64),
                                     _p(_i64), _p(_i32), _p(_i32)]),

@@ -377,8 +377,15 @@ def _last_kernel_ms(self) -> float:
     return out.value
 
 
+def _last_plan(self) -> str:
+    out = C.c_char_p()
+    _check(_lib().mmws_gpu_last_plan(self._h, C.byref(out)))
+    return (out.value or b"").decode()
+
+
 Context.master_run_host = _master_run_host
 Context.last_kernel_ms = property(_last_kernel_ms)
+Context.last_plan = property(_last_plan)
 
 
 def bootstrap_comm(ctx: Context) -> None:

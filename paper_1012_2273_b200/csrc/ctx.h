@@ -20,6 +20,7 @@ struct mmws_gpu_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t evk0 = nullptr, evk1 = nullptr;  // around the row-block multiply
   double last_kernel_ms = 0.0;
+  const char* last_plan = "";  // kernel configuration of the latest multiply (static string)
   mmws_impl::EncodeTiledFn encode = nullptr;
   // stream memory operations (cuStreamWriteValue32 / cuStreamWaitValue32) for
   // the streamed host path; null if the driver does not offer them

@@ -26,6 +26,7 @@
 //   * integer-valued inputs (|partial sums| < 2^53) come out bit-exact in any
 //     accumulation order, which is what the N=4099 exactness config checks.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -35,16 +36,26 @@ namespace {
 
 using namespace mmws_dev;
 
+constexpr int isqrt_round(int x) {
+  int r = 0;
+  while ((r + 1) * (r + 1) <= x) ++r;
+  return (x - r * r > r) ? r + 1 : r;
+}
+static_assert(isqrt_round(148) == 12 && isqrt_round(444) == 21, "raster groups");
+
 template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_>
 struct Cfg {
   static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_;
   static constexpr int BK = 16;  // 16 doubles = one 128-byte swizzle row
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   static constexpr int CONSUMERS = WARPS_M * WARPS_N;
-  // The producer is a whole warpgroup so setmaxnreg can move its registers to
-  // the math warpgroups (register budgets are per 4-warp group).
-  static constexpr int THREADS = (CONSUMERS + 4) * 32;
+  // With 8 math warps the producer is a whole warpgroup so setmaxnreg can move
+  // its registers to the math warpgroups (register budgets are per 4-warp
+  // group); smaller configurations need no register shuffle and use one
+  // producer warp, which leaves registers for more resident CTAs.
   static constexpr int MATH_REGS = CONSUMERS == 8 ? 232 : 0;  // 0: no setmaxnreg
+  static constexpr int PRODUCERS = MATH_REGS > 0 ? 4 : 1;
+  static constexpr int THREADS = (CONSUMERS + PRODUCERS) * 32;
   static constexpr int MI = WM / 8;   // 8-row subtiles per warp
   static constexpr int NB = WN / 16;  // 16-column boxes per warp
   static constexpr int A_BYTES = BM * BK * 8;
@@ -53,11 +64,24 @@ struct Cfg {
   static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 1024;
   static_assert(BM % WM == 0 && BN % WN == 0 && WM % 8 == 0 && WN % 16 == 0, "tile");
   static_assert(BM <= 256, "TMA box");
+  // Raster group (tile rows advancing together).  Default: a wave of 148 x
+  // MINB resident tiles covers a square of C, the fewest distinct A and B
+  // panels per wave (128x128: 12; measured at N=16384: 48.6 GB DRAM reads vs
+  // 52.2 with 8 and 78.3 with 4, same time).  64x64 with 3 CTAs/SM: 10
+  // (N=16384: 116 GB vs 180 GB with the square 21, 133 with 6, 364 with 42;
+  // N=8192: 12.1 vs 14.0 GB; the time does not move, the kernel is bound by
+  // the FP64 tensor pipe either way).
+  static constexpr int GROUP = (BM == 64 && BN == 64 && MINB == 3)
+                                   ? 10
+                                   : isqrt_round(148 * MINB * BN / BM);
 };
 
 using Big = Cfg<128, 128, 64, 32, 6, 1>;   // 8 math warps, 192 KB ring, 1 CTA/SM
-using Small = Cfg<64, 64, 32, 32, 4, 2>;   // 4 math warps, 64 KB ring, 2+ CTAs/SM
+using Small = Cfg<64, 64, 32, 32, 4, 3>;   // 4 math warps, 64 KB ring, 3 CTAs/SM
 using Mid = Cfg<128, 64, 32, 32, 5, 1>;    // 8 math warps, 160 KB ring
+using Small8 = Cfg<64, 64, 32, 16, 6, 1>;  // 8 math warps on a 64x64 tile (stream-K, 1 CTA/SM)
+using Tiny = Cfg<32, 32, 16, 16, 4, 6>;    // 4 math warps, 32 KB ring, 6 CTAs/SM
+using Slim = Cfg<32, 64, 16, 32, 4, 4>;    // 4 math warps, 48 KB ring, 4 CTAs/SM
 
 // Poll an arrival flag (written by a cuStreamWriteValue32 behind an H2D copy).
 // A flag that never arrives is a host-side bug; trap after 60 s so the
@@ -105,7 +129,7 @@ __global__ void __launch_bounds__(K::THREADS, K::MINB)
     dgemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB, double* __restrict__ C,
                       int64_t ldc, int M, int N, int K_, int tiles_m, int tiles_n, int vec_ok,
-                      DmmaStream st) {
+                      int group, DmmaStream st) {
   constexpr bool STREAM = MODE == 1, SK = MODE == 2;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   // 1024-byte aligned ring (128B-swizzle atoms); offsetting the __shared__
@@ -122,13 +146,9 @@ __global__ void __launch_bounds__(K::THREADS, K::MINB)
   // together so the A and B panels of one wave are shared through L2).
   // Streamed: the host's arrival-ordered list.
   auto raster = [&](int tile, int& tm, int& tn) {
-    // 12 tile-rows per group: a 148-CTA wave covers ~12 x 12 tiles, the
-    // squarest footprint (fewest distinct A+B panels per wave); measured at
-    // N=16384: 48.6 GB DRAM reads vs 52.2 (8 rows) / 78.3 (4 rows), same time
-    constexpr int GROUP = 12;
-    const int per_group = GROUP * tiles_n;
-    const int first_m = (tile / per_group) * GROUP;
-    const int gm = min(tiles_m - first_m, GROUP);
+    const int per_group = group * tiles_n;
+    const int first_m = (tile / per_group) * group;
+    const int gm = min(tiles_m - first_m, group);
     tm = first_m + (tile % per_group) % gm;
     tn = (tile % per_group) / gm;
   };
@@ -137,19 +157,8 @@ __global__ void __launch_bounds__(K::THREADS, K::MINB)
       const int t = st.order[idx];
       tm = t / tiles_n;
       tn = t % tiles_n;
-    } else if constexpr (SK) {
-      raster(idx, tm, tn);
     } else {
-      // 12 tile-rows per group: a 148-CTA wave covers ~12 x 12 tiles, the
-      // squarest footprint (fewest distinct A+B panels per wave); measured at
-      // N=16384: 48.6 GB DRAM reads vs 52.2 (8 rows) / 78.3 (4 rows), same time
-      constexpr int GROUP = 12;
-      const int tile = blockIdx.x;
-      const int per_group = GROUP * tiles_n;
-      const int first_m = (tile / per_group) * GROUP;
-      const int gm = min(tiles_m - first_m, GROUP);
-      tm = first_m + (tile % per_group) % gm;
-      tn = (tile % per_group) / gm;
+      raster(SK ? idx : static_cast<int>(blockIdx.x), tm, tn);
     }
   };
   const int idx0 = STREAM ? static_cast<int>(blockIdx.x) : 0;
@@ -373,6 +382,16 @@ __global__ void __launch_bounds__(K::THREADS, K::MINB)
   }
 }
 
+// Raster group of configuration K; MMWS_GPU_RASTER_GROUP overrides it (tuning).
+template <class K>
+int raster_group() {
+  if (const char* g = std::getenv("MMWS_GPU_RASTER_GROUP")) {
+    const int v = std::atoi(g);
+    if (v > 0) return v;
+  }
+  return K::GROUP;
+}
+
 bool make_map(const Launch& L, CUtensorMap* map, const double* base, int64_t inner, int64_t outer,
               int64_t ld, int box_inner, int box_outer) {
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
@@ -393,15 +412,38 @@ cudaError_t run(const Launch& L, int64_t M, int64_t N, int64_t Kd, const double*
   if (!make_map(L, &ta, A, Kd, M, lda, 16, K::BM)) return cudaErrorInvalidValue;
   if (!make_map(L, &tb, B, N, Kd, ldb, 16, 16)) return cudaErrorInvalidValue;
   const int smem = K::SMEM;
+  const int tiles_m = static_cast<int>((M + K::BM - 1) / K::BM);
+  const int tiles_n = static_cast<int>((N + K::BN - 1) / K::BN);
   cudaError_t e = cudaFuncSetAttribute(dgemm_dmma_kernel<K, 0>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int vec_ok = (ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0);
+  dgemm_dmma_kernel<K, 0><<<tiles_m * tiles_n, K::THREADS, smem, L.stream>>>(
+      ta, tb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(Kd), tiles_m,
+      tiles_n, vec_ok, raster_group<K>(), DmmaStream{});
+  L.count();
+  return cudaGetLastError();
+}
+
+template <class K>
+cudaError_t run_sk(const Launch& L, int64_t M, int64_t N, int64_t Kd, const double* A, int64_t lda,
+                   const double* B, int64_t ldb, double* C, int64_t ldc, double* partial,
+                   int* flags, int grid) {
+  CUtensorMap ta, tb;
+  if (!make_map(L, &ta, A, Kd, M, lda, 16, K::BM)) return cudaErrorInvalidValue;
+  if (!make_map(L, &tb, B, N, Kd, ldb, 16, 16)) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(dgemm_dmma_kernel<K, 2>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
   if (e != cudaSuccess) return e;
   const int tiles_m = static_cast<int>((M + K::BM - 1) / K::BM);
   const int tiles_n = static_cast<int>((N + K::BN - 1) / K::BN);
   const int vec_ok = (ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0);
-  dgemm_dmma_kernel<K, 0><<<tiles_m * tiles_n, K::THREADS, smem, L.stream>>>(
+  DmmaStream st;
+  st.partial = partial;
+  st.flags = flags;
+  dgemm_dmma_kernel<K, 2><<<grid, K::THREADS, K::SMEM, L.stream>>>(
       ta, tb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(Kd), tiles_m,
-      tiles_n, vec_ok, DmmaStream{});
+      tiles_n, vec_ok, raster_group<K>(), st);
   L.count();
   return cudaGetLastError();
 }
@@ -423,32 +465,70 @@ cudaError_t launch_dgemm_dmma_stream(const Launch& L, int64_t M, int64_t N, int6
   const int vec_ok = (ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0);
   dgemm_dmma_kernel<K, 1><<<grid, K::THREADS, K::SMEM, L.stream>>>(
       ta, tb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(Kd), tiles_m,
-      tiles_n, vec_ok, st);
+      tiles_n, vec_ok, raster_group<K>(), st);
   L.count();
   return cudaGetLastError();
 }
 
-cudaError_t launch_dgemm_dmma_sk(const Launch& L, int64_t M, int64_t N, int64_t Kd,
+int dmma_tile_rows(int cfg) {
+  switch (cfg) {
+    case DMMA_64x64: case DMMA_64x64_W8: return 64;
+    case DMMA_32x32: case DMMA_32x64: return 32;
+    default: return 128;
+  }
+}
+
+int dmma_tile_cols(int cfg) {
+  switch (cfg) {
+    case DMMA_64x64: case DMMA_64x64_W8: case DMMA_128x64: case DMMA_32x64: return 64;
+    case DMMA_32x32: return 32;
+    default: return 128;
+  }
+}
+
+const char* dmma_plan_name(int cfg, int launch) {
+  // [cfg][launch]: one-shot, stream-K
+  static const char* const names[6][2] = {
+      {"dgemm_dmma_kernel<128x128, 8 math warps, 1 CTA/SM>",
+       "dgemm_dmma_kernel<128x128, 8 math warps, stream-K>"},
+      {"dgemm_dmma_kernel<64x64, 4 math warps, 3 CTAs/SM>",
+       "dgemm_dmma_kernel<64x64, 4 math warps, stream-K>"},
+      {"dgemm_dmma_kernel<128x64, 8 math warps, 1 CTA/SM>",
+       "dgemm_dmma_kernel<128x64, 8 math warps, stream-K>"},
+      {"dgemm_dmma_kernel<64x64, 8 math warps, 1 CTA/SM>",
+       "dgemm_dmma_kernel<64x64, 8 math warps, stream-K>"},
+      {"dgemm_dmma_kernel<32x32, 4 math warps, 6 CTAs/SM>",
+       "dgemm_dmma_kernel<32x32, 4 math warps, stream-K>"},
+      {"dgemm_dmma_kernel<32x64, 4 math warps, 4 CTAs/SM>",
+       "dgemm_dmma_kernel<32x64, 4 math warps, stream-K>"}};
+  if (cfg < 0 || cfg > 5 || launch < 0 || launch > 1) return "dgemm_dmma_kernel<?>";
+  return names[cfg][launch];
+}
+
+
+int dmma_ctas_per_sm(int cfg) {
+  switch (cfg) {
+    case DMMA_64x64: return Small::MINB;
+    case DMMA_128x64: return Mid::MINB;
+    case DMMA_64x64_W8: return Small8::MINB;
+    case DMMA_32x32: return Tiny::MINB;
+    case DMMA_32x64: return Slim::MINB;
+    default: return Big::MINB;
+  }
+}
+
+cudaError_t launch_dgemm_dmma_sk(const Launch& L, int cfg, int64_t M, int64_t N, int64_t Kd,
                                  const double* A, int64_t lda, const double* B, int64_t ldb,
                                  double* C, int64_t ldc, double* partial, int* flags, int grid) {
-  using K = Big;
-  CUtensorMap ta, tb;
-  if (!make_map(L, &ta, A, Kd, M, lda, 16, K::BM)) return cudaErrorInvalidValue;
-  if (!make_map(L, &tb, B, N, Kd, ldb, 16, 16)) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(dgemm_dmma_kernel<K, 2>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
-  if (e != cudaSuccess) return e;
-  const int tiles_m = static_cast<int>((M + K::BM - 1) / K::BM);
-  const int tiles_n = static_cast<int>((N + K::BN - 1) / K::BN);
-  const int vec_ok = (ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0);
-  DmmaStream st;
-  st.partial = partial;
-  st.flags = flags;
-  dgemm_dmma_kernel<K, 2><<<grid, K::THREADS, K::SMEM, L.stream>>>(
-      ta, tb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(Kd), tiles_m,
-      tiles_n, vec_ok, st);
-  L.count();
-  return cudaGetLastError();
+  switch (cfg) {
+    case DMMA_64x64: return run_sk<Small>(L, M, N, Kd, A, lda, B, ldb, C, ldc, partial, flags, grid);
+    case DMMA_128x64: return run_sk<Mid>(L, M, N, Kd, A, lda, B, ldb, C, ldc, partial, flags, grid);
+    case DMMA_64x64_W8:
+      return run_sk<Small8>(L, M, N, Kd, A, lda, B, ldb, C, ldc, partial, flags, grid);
+    case DMMA_32x32: return run_sk<Tiny>(L, M, N, Kd, A, lda, B, ldb, C, ldc, partial, flags, grid);
+    case DMMA_32x64: return run_sk<Slim>(L, M, N, Kd, A, lda, B, ldb, C, ldc, partial, flags, grid);
+    default: return run_sk<Big>(L, M, N, Kd, A, lda, B, ldb, C, ldc, partial, flags, grid);
+  }
 }
 
 cudaError_t launch_dgemm_dmma(const Launch& L, int cfg, int64_t M, int64_t N, int64_t K,
@@ -457,6 +537,9 @@ cudaError_t launch_dgemm_dmma(const Launch& L, int cfg, int64_t M, int64_t N, in
   switch (cfg) {
     case DMMA_64x64: return run<Small>(L, M, N, K, A, lda, B, ldb, C, ldc);
     case DMMA_128x64: return run<Mid>(L, M, N, K, A, lda, B, ldb, C, ldc);
+    case DMMA_64x64_W8: return run<Small8>(L, M, N, K, A, lda, B, ldb, C, ldc);
+    case DMMA_32x32: return run<Tiny>(L, M, N, K, A, lda, B, ldb, C, ldc);
+    case DMMA_32x64: return run<Slim>(L, M, N, K, A, lda, B, ldb, C, ldc);
     default: return run<Big>(L, M, N, K, A, lda, B, ldb, C, ldc);
   }
 }
@@ -464,7 +547,11 @@ cudaError_t launch_dgemm_dmma(const Launch& L, int cfg, int64_t M, int64_t N, in
 cudaError_t preload_dgemm_dmma() {
   return preload_kernels(dgemm_dmma_kernel<Big, 0>, dgemm_dmma_kernel<Mid, 0>,
                          dgemm_dmma_kernel<Small, 0>, dgemm_dmma_kernel<Big, 1>,
-                         dgemm_dmma_kernel<Big, 2>);
+                         dgemm_dmma_kernel<Big, 2>, dgemm_dmma_kernel<Small, 2>,
+                         dgemm_dmma_kernel<Mid, 2>,
+                         dgemm_dmma_kernel<Small8, 0>, dgemm_dmma_kernel<Small8, 2>,
+                         dgemm_dmma_kernel<Tiny, 0>, dgemm_dmma_kernel<Tiny, 2>,
+                         dgemm_dmma_kernel<Slim, 0>, dgemm_dmma_kernel<Slim, 2>);
 }
 
 }  // namespace mmws_impl

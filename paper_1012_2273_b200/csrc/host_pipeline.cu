@@ -146,6 +146,7 @@ int host_multiply_streamed(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, c
   st.band_b = BAND_B;
   st.done = done;
   const int grid = static_cast<int>(std::min<int64_t>(T, ctx->num_sms));
+  ctx->last_plan = "dgemm_dmma_kernel<128x128, 8 math warps, streamed from host>";
   if ((e = launch_dgemm_dmma_stream(ctx->launch(comp), m, n, k, dA, k, dB, n, dC, n, st, grid)))
     return cuda_fail(e, "matmul_host: streamed dgemm");
   if (trace) cudaEventRecord(tr[2], comp);
@@ -240,6 +241,7 @@ int host_multiply_ozaki(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, cons
     return cuda_fail(e, "matmul ozaki: H2D B");
   cudaEventRecord(evB, in);
   cudaStreamWaitEvent(comp, evB, 0);
+  ctx->last_plan = "ozaki (int8 tcgen05 GEMMs + CRT), B prepared once, A in row panels";
   if ((e = launch_ozaki_prepare_b(L, n, k, dB, n, ctx->ws)) != cudaSuccess)
     return cuda_fail(e, "matmul ozaki: prepare B");
   for (int64_t i = 0; i < panels; ++i) {
@@ -293,7 +295,7 @@ int host_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A
     const int64_t tiles128 = ((m + 127) / 128) * ((n + 127) / 128);
     if ((mode == MMWS_GPU_MODE_AUTO || mode == MMWS_GPU_MODE_DMMA) && ctx->write_value &&
         ctx->wait_value && tiles128 >= 2 * static_cast<int64_t>(ctx->num_sms) && k % 2 == 0 &&
-        n % 2 == 0 && (n > 256 || k > 256))
+        n % 2 == 0 && (n > AUTO_SMALL_MAX || k > AUTO_SMALL_MAX))
       return host_multiply_streamed(ctx, m, n, k, A, B, C, elapsed_s);
   }
   // big emulated problems: B prepared once, A streamed in row panels

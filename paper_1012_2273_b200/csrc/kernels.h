@@ -25,7 +25,22 @@ struct Launch {
 };
 
 // DMMA tile configurations (see dgemm_dmma.cu / DESIGN.md s3).
-enum DmmaCfg { DMMA_128x128 = 0, DMMA_64x64 = 1, DMMA_128x64 = 2 };
+enum DmmaCfg {
+  DMMA_128x128 = 0,   // 8 math warps, 1 CTA/SM
+  DMMA_64x64 = 1,     // 4 math warps, 3 CTAs/SM
+  DMMA_128x64 = 2,    // 8 math warps
+  DMMA_64x64_W8 = 3,  // 8 math warps on a 64x64 tile, 1 CTA/SM
+  DMMA_32x32 = 4,     // 4 math warps, 6 CTAs/SM
+  DMMA_32x64 = 5,     // 4 math warps, 4 CTAs/SM
+};
+// AUTO takes the 32x32 DFMA latency kernel when n and k are both <= this
+// (a rule on (n, k) only, so row slices get the whole problem's bits).
+constexpr int64_t AUTO_SMALL_MAX = 96;
+int dmma_tile_rows(int cfg);
+int dmma_tile_cols(int cfg);
+int dmma_ctas_per_sm(int cfg);
+// launch: 0 one-shot, 1 stream-K
+const char* dmma_plan_name(int cfg, int launch);  // resident CTAs per SM the configuration is built for
 
 // Streamed (persistent) DMMA schedule: tile list in arrival order, per-band
 // arrival flags, per-tile-row completion counters (see dgemm_dmma.cu).
@@ -90,13 +105,13 @@ cudaError_t preload_sgemm();
 cudaError_t preload_sgemm_tma();
 cudaError_t preload_misc();
 
-// Stream-K, 128x128 tiles, one persistent CTA per SM (grid CTAs): every CTA
-// gets the same number of k-iterations; bitwise the one-shot result.  Needs
-// tiles * ceil(K/16) >= grid * ceil(K/16), i.e. tiles >= grid.  partial:
-// (grid + 1) * 128 * 128 doubles; flags: grid + 1 ints, zero before the first
-// launch (the kernel leaves them zero).  Launches sharing a workspace must
-// not overlap.
-cudaError_t launch_dgemm_dmma_sk(const Launch& L, int64_t M, int64_t N, int64_t K,
+// Stream-K, tiles of configuration cfg, grid persistent CTAs (all resident):
+// every CTA gets the same number of k-iterations; bitwise the one-shot
+// result.  Needs tiles * ceil(K/16) >= grid * ceil(K/16), i.e. tiles >= grid.
+// partial: (grid + 1) * 128 * 128 doubles; flags: grid + 1 ints, zero before
+// the first launch (the kernel leaves them zero).  Launches sharing a
+// workspace must not overlap.
+cudaError_t launch_dgemm_dmma_sk(const Launch& L, int cfg, int64_t M, int64_t N, int64_t K,
                                  const double* A, int64_t lda, const double* B, int64_t ldb,
                                  double* C, int64_t ldc, double* partial, int* flags, int grid);
 // 128x128 tiles only; grid = number of persistent CTAs.

@@ -73,25 +73,27 @@ int check_dims(int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb, int64_
 // of 128 x 128 doubles and their flags, allocated (flags zeroed on the
 // stream) on first use and kept for the context's lifetime -- fixed size, so
 // a pointer baked into a launch never goes stale.
+// Stream-K workspace of one stream: the flags of up to 4 persistent CTAs per SM
+// (zeroed once; every launch leaves them zero), then accumulator slots --
+// (grid + 1) slots of BM x BN doubles, at most (num_sms + 1) x 128 x 128.
 int sk_workspace(mmws_gpu_ctx* ctx, cudaStream_t stream, double** partial, int** flags) {
-  const size_t slots = static_cast<size_t>(ctx->num_sms) + 1;
-  const size_t slot_bytes = sizeof(double) * 128 * 128;
+  const size_t flag_bytes = round_up(sizeof(int) * (4 * static_cast<size_t>(ctx->num_sms) + 1), 4096);
+  const size_t part_bytes = sizeof(double) * 128 * 128 * (static_cast<size_t>(ctx->num_sms) + 1);
   void* mem = nullptr;
   for (const auto& sp : ctx->sk_spaces)
     if (sp.stream == stream) mem = sp.mem;
   if (!mem) {
     cudaError_t e;
-    if ((e = cudaMalloc(&mem, slots * slot_bytes + sizeof(int) * slots)) != cudaSuccess)
+    if ((e = cudaMalloc(&mem, flag_bytes + part_bytes)) != cudaSuccess)
       return cuda_fail(e, "stream-K workspace");
-    if ((e = cudaMemsetAsync(static_cast<char*>(mem) + slots * slot_bytes, 0, sizeof(int) * slots,
-                             stream)) != cudaSuccess) {
+    if ((e = cudaMemsetAsync(mem, 0, flag_bytes, stream)) != cudaSuccess) {
       cudaFree(mem);
       return cuda_fail(e, "stream-K workspace");
     }
     ctx->sk_spaces.push_back({stream, mem});
   }
-  *partial = static_cast<double*>(mem);
-  *flags = reinterpret_cast<int*>(static_cast<char*>(mem) + slots * slot_bytes);
+  *flags = static_cast<int*>(mem);
+  *partial = reinterpret_cast<double*>(static_cast<char*>(mem) + flag_bytes);
   return MMWS_GPU_OK;
 }
 
@@ -117,10 +119,11 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
   cudaError_t e;
   const int64_t tiles128 = ((m + 127) / 128) * ((n + 127) / 128);
   // Stream-K (128x128, one persistent CTA per SM, equal k-iterations per SM;
-  // bitwise the one-shot result) from one tile per SM up to 32 waves: it beat
-  // the one-shot launch at every size measured there (N=1600: 30.0 vs 27.1
+  // bitwise the one-shot result) from one tile per SM up to 32 waves, for
+  // MODE_DMMA (128x128 tiles) and the exact mode: it beat the one-shot
+  // 128x128 launch at every size measured there (N=1600: 30.0 vs 27.1
   // TFLOP/s, 2000: 32.6 vs 28.6, 2500: 33.3 vs 30.2, 4099: 32.7 vs 30.1,
-  // 8192: 36.3 vs 36.0) and lost 0.2 % at N=16384 (110 waves).  Not used
+  // 8192: 36.3 vs 36.0).  AUTO's small-tile plans beat both (below).  Not used
   //   * inside graph capture (the captured launch would share the stream's
   //     workspace with later eager launches),
   //   * while the latency server holds SMs (the grid would not be resident),
@@ -129,7 +132,8 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
   const int64_t G = ctx->num_sms;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(L.stream, &cap);
-  const bool sk = mode != MMWS_GPU_MODE_DMMA_SMALL && tiles128 >= G && tiles128 < 32 * G &&
+  const bool sk = (mode == MMWS_GPU_MODE_DMMA || mode == MMWS_GPU_MODE_EXACT) && tiles128 >= G &&
+                  tiles128 < 32 * G &&
                   cap == cudaStreamCaptureStatusNone && !ctx->server && ctx->allow_streamk &&
                   !std::getenv("MMWS_GPU_NO_STREAMK");
   // TMA needs 16-byte aligned bases and even row pitches: pack A and/or B into
@@ -168,13 +172,16 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
     // bits
     if (n <= 256 && k <= 256) {
       e = launch_dgemm_small(L, true, m, n, k, A, lda, B, ldb, C, ldc);
+      ctx->last_plan = "dgemm_small_kernel<exact, 32x32>";
     } else if (sk) {
       if (int rc = sk_workspace(ctx, L.stream, &sk_partial, &sk_flags)) return rc;
       if (int rc = pack_operands()) return rc;
       e = launch_dgemm_exact_sk(L, m, n, k, A, lda, B, ldb, C, ldc, sk_partial, sk_flags,
                                 static_cast<int>(G));
+      ctx->last_plan = "dgemm_exact_tma_kernel<128x128, stream-K>";
     } else {
       e = launch_dgemm_exact(L, m, n, k, A, lda, B, ldb, C, ldc);
+      ctx->last_plan = "dgemm_exact (one-shot)";
     }
     return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm exact");
   }
@@ -187,30 +194,70 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
       return cuda_fail(e, "dgemm ozaki workspace");
     if (int rc = ozaki_streams(ctx)) return rc;
     e = launch_dgemm_ozaki(L, m, n, k, A, lda, B, ldb, C, ldc, ctx->ws, ctx->oz_stream, ctx->oz_ev);
+    ctx->last_plan = "ozaki (int8 tcgen05 GEMMs + CRT)";
     return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm ozaki");
   }
   if (mode != MMWS_GPU_MODE_AUTO && mode != MMWS_GPU_MODE_DMMA &&
       mode != MMWS_GPU_MODE_DMMA_SMALL)
     return fail(MMWS_GPU_ERR_DOMAIN, "dgemm: unknown mode " + std::to_string(mode));
-  if (mode == MMWS_GPU_MODE_AUTO && n <= 256 && k <= 256) {
+  if (mode == MMWS_GPU_MODE_AUTO && n <= AUTO_SMALL_MAX && k <= AUTO_SMALL_MAX) {
     // latency path; chosen from (n, k) only, so every row slice of a problem
     // (row-block ranks, host-pipeline panels) takes the same kernel as the
-    // whole problem and gets the same bits
+    // whole problem and gets the same bits.  Above 96 the 32x32 DMMA tiles
+    // are faster (GPU time per call: N=128 6.1 vs 8.2 us, 200 6.2 vs 12.3,
+    // 256 8.2 vs 13.4; tools/dmma_plan_probe.py); up to 96 it stays, so the
+    // latency server (server.cu, N <= 96, same DFMA chain) matches AUTO
     e = launch_dgemm_small(L, false, m, n, k, A, lda, B, ldb, C, ldc);
+    ctx->last_plan = "dgemm_small_kernel<DFMA, 32x32>";
     return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm small");
   }
   if (int rc = pack_operands()) return rc;
-  if (sk) {
+  // DMMA tile plan.  Every configuration computes each element as the same
+  // DMMA chain in ascending k from +0.0, so the choice never changes the bits.
+  // AUTO: 32x32 tiles, 6 CTAs (24 math warps) per SM below three 128x128
+  // tiles per SM; 64x64 tiles, 3 CTAs (12 math warps) per SM up to 64 tiles
+  // per SM; 128x128 above.  GPU time per call, back to back
+  // (tools/dmma_plan_probe.py, profiles/r01_dmma_plans.jsonl), against the
+  // previous plan (64x64 with 2 CTAs/SM below 2 tiles per SM, then 128x128
+  // stream-K / one-shot): N=500 14.4 vs 24.7 us, 1000 70.3 vs 74.6, 1500 205
+  // vs 211, 2200 640 vs 667, 2700 1157 vs 1207, 3500 2461 vs 2508, 4099 4107
+  // vs 4216, 8192 30.20 vs 30.34 ms, 10000 55.4 vs 57.3 ms.  More resident
+  // math warps hide the DMMA and fragment-load latencies better than bigger
+  // register tiles save operand traffic.  At N=16384 the 64x64 plan is only
+  // 0.3-0.5 % faster (240.8 vs 241.9 ms) for 2.3x the DRAM reads (116 vs 50
+  // GB), so the largest problems keep 128x128 tiles.  Stream-K over small
+  // tiles lost to their one-shot launches at every size measured.
+  int cfg = DMMA_128x128;
+  if (mode == MMWS_GPU_MODE_DMMA_SMALL || (mode == MMWS_GPU_MODE_AUTO && tiles128 < 3 * G))
+    cfg = DMMA_32x32;
+  else if (mode == MMWS_GPU_MODE_AUTO && tiles128 < 64 * G)
+    cfg = DMMA_64x64;
+  int sk_grid = sk ? static_cast<int>(G) : 0;
+  if (const char* plan = std::getenv("MMWS_GPU_DMMA_PLAN")) {
+    // tuning override (tools/dmma_plan_probe.py): "<cfg>" one-shot, or
+    // "<cfg>s<CTAs per SM>" stream-K
+    char* end = nullptr;
+    cfg = static_cast<int>(std::strtol(plan, &end, 10));
+    sk_grid = end && *end == 's' ? static_cast<int>(G * std::strtol(end + 1, nullptr, 10)) : 0;
+    const int64_t tiles = ((m + dmma_tile_rows(cfg) - 1) / dmma_tile_rows(cfg)) *
+                          ((n + dmma_tile_cols(cfg) - 1) / dmma_tile_cols(cfg));
+    // stream-K needs every CTA resident (a CTA may wait on its lower
+    // neighbour), a whole tile per CTA, and workspace slots for the grid
+    if (cfg < DMMA_128x128 || cfg > DMMA_32x64 || sk_grid < 0 ||
+        (sk_grid > 0 && (sk_grid > 4 * G || sk_grid > G * dmma_ctas_per_sm(cfg) || tiles < sk_grid ||
+                         static_cast<int64_t>(sk_grid) * dmma_tile_rows(cfg) * dmma_tile_cols(cfg) >
+                             G * 128 * 128)))
+      return fail(MMWS_GPU_ERR_DOMAIN, std::string("MMWS_GPU_DMMA_PLAN not usable here: ") + plan);
+  }
+  if (sk_grid > 0) {
     if (int rc = sk_workspace(ctx, L.stream, &sk_partial, &sk_flags)) return rc;
-    e = launch_dgemm_dmma_sk(L, m, n, k, A, lda, B, ldb, C, ldc, sk_partial, sk_flags,
-                             static_cast<int>(G));
+    e = launch_dgemm_dmma_sk(L, cfg, m, n, k, A, lda, B, ldb, C, ldc, sk_partial, sk_flags,
+                             sk_grid);
+    ctx->last_plan = dmma_plan_name(cfg, 1);
     return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm stream-K");
   }
-  const int cfg = mode == MMWS_GPU_MODE_DMMA_SMALL ||
-                          (mode == MMWS_GPU_MODE_AUTO && tiles128 < 2 * G)
-                      ? DMMA_64x64
-                      : DMMA_128x128;
   e = launch_dgemm_dmma(L, cfg, m, n, k, A, lda, B, ldb, C, ldc);
+  ctx->last_plan = dmma_plan_name(cfg, 0);
   return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm dmma");
 }
 
@@ -229,11 +276,13 @@ int sgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const flo
       return cuda_fail(e, "sgemm ozaki workspace");
     if (int rc = ozaki_streams(ctx)) return rc;
     e = launch_sgemm_ozaki(L, m, n, k, A, lda, B, ldb, C, ldc, ctx->ws, ctx->oz_stream, ctx->oz_ev);
+    ctx->last_plan = "ozaki f32 (int8 tcgen05 GEMMs + CRT)";
     return e == cudaSuccess ? ok() : cuda_fail(e, "sgemm ozaki");
   }
-  cudaError_t e = sgemm_tma_supported(lda, ldb, A, B)
-                      ? launch_sgemm_tma(L, m, n, k, A, lda, B, ldb, C, ldc)
+  const bool tma = sgemm_tma_supported(lda, ldb, A, B);
+  cudaError_t e = tma ? launch_sgemm_tma(L, m, n, k, A, lda, B, ldb, C, ldc)
                       : launch_sgemm_ffma(L, m, n, k, A, lda, B, ldb, C, ldc);
+  ctx->last_plan = tma ? "sgemm_tma_kernel<128x256, FFMA2>" : "sgemm_ffma_kernel<192x128, FFMA2>";
   return e == cudaSuccess ? ok() : cuda_fail(e, "sgemm ffma");
 }
 

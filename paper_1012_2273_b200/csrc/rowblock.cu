@@ -395,6 +395,12 @@ int mmws_gpu_last_kernel_ms(mmws_gpu_ctx* ctx, double* ms) {
   return ok();
 }
 
+int mmws_gpu_last_plan(mmws_gpu_ctx* ctx, const char** name) {
+  if (!ctx || !name) return fail(MMWS_GPU_ERR_DOMAIN, "last_plan: null argument");
+  *name = ctx->last_plan;
+  return ok();
+}
+
 int mmws_gpu_link_probe(mmws_gpu_ctx* ctx, int64_t bytes, int iters, double* bytes_per_s) {
   MMWS_CTX_GUARD(ctx);
   if (bytes < 1 || iters < 1 || !bytes_per_s)

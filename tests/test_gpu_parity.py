@@ -177,6 +177,41 @@ def test_stream_k_is_bitwise_the_one_shot_kernel(ctx, oracle, monkeypatch, shape
     assert (bits(ex) == bits(ex1)).all()
 
 
+@pytest.mark.parametrize("shape", [(1000, 1000, 1000), (777, 513, 1001), (33, 4099, 65),
+                                   (4099, 300, 257), (1600, 1600, 1600)])
+def test_every_dmma_tile_plan_gives_the_same_bits(ctx, oracle, monkeypatch, shape):
+    # AUTO picks among 128x128 / 64x64 / 128x64 / 32x32 / 32x64 tiles, one-shot
+    # or stream-K, by tile count; each element is the same DMMA chain in
+    # ascending k from +0.0 in all of them, so every plan must give the same
+    # bits (odd pitches go through the packing path first).
+    m, k, n = shape
+    A = ctx.fill(P.DIST_UNIFORM, 41, m, k)
+    B = ctx.fill(P.DIST_UNIFORM, 42, k, n)
+    want = host(ctx.dgemm(A, B, mode=P.MODE_DMMA))
+    rows = [0, m // 2, m - 1]
+    assert normwise(want[rows], oracle.matmul_rows(rows, host(A), host(B))) <= FP64_TOL
+    sms = torch().cuda.get_device_properties(0).multi_processor_count
+    tried = 0
+    # (tile rows, tile columns, resident CTAs per SM) of each configuration
+    cfgs = [(128, 128, 1), (64, 64, 3), (128, 64, 1), (64, 64, 1), (32, 32, 6), (32, 64, 4)]
+    for cfg, (bm, bn, per_sm) in enumerate(cfgs):
+        tiles = -(-m // bm) * -(-n // bn)
+        plans = [str(cfg)] + [f"{cfg}s{r}" for r in (1, 2, 3, 4)
+                              if r <= per_sm and tiles >= r * sms and r * bm * bn <= 128 * 128]
+        for plan in plans:
+            monkeypatch.setenv("MMWS_GPU_DMMA_PLAN", plan)
+            got = host(ctx.dgemm(A, B, mode=P.MODE_DMMA))
+            assert (bits(got) == bits(want)).all(), (shape, plan)
+            tried += 1
+    monkeypatch.delenv("MMWS_GPU_DMMA_PLAN")
+    for mode in (P.MODE_AUTO, P.MODE_DMMA_SMALL):
+        assert (bits(host(ctx.dgemm(A, B, mode=mode))) == bits(want)).all(), (shape, mode)
+    assert tried >= 6
+    monkeypatch.setenv("MMWS_GPU_DMMA_PLAN", "0s2")  # more CTAs than can be resident
+    with pytest.raises(P.DomainError):
+        ctx.dgemm(A, B, mode=P.MODE_DMMA)
+
+
 @pytest.mark.parametrize("seed", range(4))
 def test_random_shapes_and_strides(ctx, oracle, seed):
     # Seeded fuzz over shapes (1..420), leading dimensions (dense or padded
@@ -744,3 +779,30 @@ def test_peak_probes_run(ctx):
     for which in (P.PROBE_DMMA, P.PROBE_DFMA, P.PROBE_DMUL_DADD, P.PROBE_FFMA, P.PROBE_FFMA2):
         tf = ctx.peak_probe(which, 256)
         assert 0.5 < tf < 200, (which, tf)
+
+
+def test_auto_tile_plan_by_size(ctx):
+    # AUTO's plan (mmws_gpu_last_plan): the DFMA latency kernel while n, k <= 96,
+    # 32x32 DMMA tiles below three 128x128 tiles per SM, 64x64 tiles up to 64
+    # per SM, 128x128 above;
+    # MODE_DMMA keeps 128x128 tiles (stream-K from one tile per SM).
+    T = torch()
+    sms = T.cuda.get_device_properties(0).multi_processor_count
+    for (m, n, k), want in [((64, 64, 64), "dgemm_small_kernel<DFMA"),
+                            ((96, 96, 96), "dgemm_small_kernel<DFMA"),
+                            ((64, 97, 64), "dgemm_dmma_kernel<32x32"),
+                            ((1000, 1000, 1000), "dgemm_dmma_kernel<32x32"),
+                            ((128 * 3 * sms, 128, 64), "dgemm_dmma_kernel<64x64"),
+                            ((128 * 64 * sms, 128, 16), "dgemm_dmma_kernel<128x128")]:
+        A = T.zeros((m, k), dtype=T.float64, device="cuda")
+        B = T.zeros((k, n), dtype=T.float64, device="cuda")
+        ctx.dgemm(A, B, mode=P.MODE_AUTO)
+        assert ctx.last_plan.startswith(want), ((m, n, k), ctx.last_plan)
+    A = T.zeros((2048, 2048), dtype=T.float64, device="cuda")
+    ctx.dgemm(A, A, mode=P.MODE_DMMA)
+    assert ctx.last_plan == "dgemm_dmma_kernel<128x128, 8 math warps, stream-K>"
+    ctx.dgemm(A, A, mode=P.MODE_DMMA_SMALL)
+    assert ctx.last_plan.startswith("dgemm_dmma_kernel<32x32")
+    ctx.dgemm(A, A, mode=P.MODE_EXACT)
+    assert ctx.last_plan == "dgemm_exact_tma_kernel<128x128, stream-K>"
+    T.cuda.synchronize()
