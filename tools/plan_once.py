@@ -1,5 +1,5 @@
 """One device-pointer multiply per MMWS_GPU_DMMA_PLAN given on the command
-line (for ncu: one kernel launch per plan, after one warm-up multiply).
+line (for ncu: one kernel launch per plan).
 PLAN[:G] also sets the raster group (MMWS_GPU_RASTER_GROUP=G).
 Usage: python tools/plan_once.py N PLAN[:G] [PLAN[:G] ...]"""
 import os

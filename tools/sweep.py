@@ -23,7 +23,8 @@ import paper_1012_2273_b200 as P  # noqa: E402
 
 def dev_time(fn, reps, inner=1):
     """Device time per call: CUDA events around `inner` back-to-back calls
-    (inner > 1 keeps the queue full, so host submission latency is hidden)."""
+    queued behind a sleep kernel, so the host's submission time (Python,
+    ctypes, argument checks) never shows up as idle GPU time between them."""
     s = torch.cuda.current_stream()
     best = 1e9
     for _ in range(3):
@@ -31,6 +32,7 @@ def dev_time(fn, reps, inner=1):
     torch.cuda.synchronize()
     for _ in range(reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(int(inner * 40e-6 * 2e9))  # longer than queuing `inner` calls
         e0.record(s)
         for _ in range(inner):
             fn()
