@@ -274,7 +274,8 @@ def run_ours(args) -> None:
     value = flops * args.steps / (ms / 1e3) / 1e9
 
     # dominant kernel roofline (rank 0's DMMA launch; events on its stream)
-    rows0 = P.split_rows(n, world)[0][1]
+    active = P.rowblock_ranks(n, n, n, world)  # = world at this size
+    rows0 = P.split_rows(n, active)[0][1]
     kern_avg_ms = sum(kern_ms) / len(kern_ms)
     achieved = 2.0 * rows0 * n * n / (kern_avg_ms / 1e3) / 1e12
     traffic, traffic_src = profiled_traffic(n, plan) if world == 1 else (None, None)

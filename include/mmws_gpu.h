@@ -282,12 +282,26 @@ int mmws_gpu_rowblock_cost(int64_t m, int64_t n, int64_t k, int nranks, int elem
                            double link_bytes_per_s, double gemm_flops_per_s, double* seconds,
                            double* root_egress_bytes, double* root_ingress_bytes);
 
+/* Whether a row-block round over nranks GPUs is distributed at all (the north
+ * star's "used only where N is large enough to amortise the transfers"):
+ * *active = nranks when the cost model above, with fixed planning rates
+ * (NVLink 600 GB/s per direction, 33 TFLOP/s fp64 / 55 TFLOP/s fp32 per
+ * GPU, 60 us of collective latency per round), predicts the distributed round
+ * to beat rank 0 multiplying alone, else 1: rank 0 computes every row and the
+ * workers return at once (the reference's idle worker, protocol.hpp:122-123,
+ * with no messages at all).  Every rank computes the same answer from its
+ * arguments, so no agreement round is needed.  MMWS_GPU_ROWBLOCK_RANKS=all
+ * (or =1) in the environment forces the choice.  Host-only. */
+int mmws_gpu_rowblock_ranks(int64_t m, int64_t n, int64_t k, int nranks, int elem_bytes,
+                            int* active);
+
 /* The message plan rank 0 executes for (m, k, n, nranks), in issue order --
  * the analogue of the reference's Communicator traffic log (comm.hpp:24-32)
  * used by its protocol-shape test (test_protocol.cpp:99-137).  Host-only.
  * Order: one B broadcast, then the A-slices sub-block by sub-block, then the
  * C-slices sub-block by sub-block (offsets/row counts are derived from
- * split_rows on every rank, so there are no scalar metadata messages).
+ * split_rows on every rank, so there are no scalar metadata messages).  It
+ * is the plan of a distributed round (see mmws_gpu_rowblock_ranks).
  * Entry e: peer[e] (-1 = all ranks), tag[e] (1 = assign, 2 = result),
  * kind[e] (1 = fp64/fp32 array), count[e] (elements), row0[e] (first row of
  * A or C the slice covers, -1 for B), dir[e] (0 sent, 1 received,

@@ -7,6 +7,7 @@ Python package is the ctypes binding used by tests and bench.py.
 """
 from .api import (Context, DimensionError, DomainError, GpuError, Graph, ProtocolError,  # noqa: F401
                   RankError, bootstrap_comm, nccl_unique_id, op_count, ozaki_plan, rowblock_cost,
+                  rowblock_ranks,
                   rowblock_plan,
                   split_rows, static_partition)
 from ._abi import (DIST_INT8, DIST_NORMAL, DIST_UNIFORM, DIST_UNIT, MODE_AUTO, MODE_DMMA,  # noqa: F401

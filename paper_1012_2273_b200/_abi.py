@@ -62,6 +62,7 @@ SIGNATURES = {
     "mmws_gpu_last_kernel_ms": (_i, [_v, _p(_d)]),
     "mmws_gpu_last_plan": (_i, [_v, _p(C.c_char_p)]),
     "mmws_gpu_rowblock_cost": (_i, [_i64, _i64, _i64, _i, _i, _d, _d, _p(_d), _p(_d), _p(_d)]),
+    "mmws_gpu_rowblock_ranks": (_i, [_i64, _i64, _i64, _i, _i, _p(_i)]),
     "mmws_gpu_rowblock_plan": (_i, [_i64, _i64, _i64, _i, _p(_i32), _p(_i32), _p(_i32), _p(_i64),
                                     _p(_i64), _p(_i32), _p(_i32)]),
 }

@@ -112,6 +112,15 @@ def rowblock_cost(m: int, n: int, k: int, nranks: int, elem_bytes: int = 8,
     return t.value, eg.value, ing.value
 
 
+def rowblock_ranks(m: int, n: int, k: int, nranks: int, elem_bytes: int = 8) -> int:
+    """How many ranks a row-block round over nranks GPUs uses: nranks when
+    the distributed round is predicted to beat rank 0 alone, else 1
+    (mmws_gpu_rowblock_ranks)."""
+    out = C.c_int()
+    _check(_lib().mmws_gpu_rowblock_ranks(m, n, k, nranks, elem_bytes, C.byref(out)))
+    return out.value
+
+
 def ozaki_plan(k: int):
     """MODE_OZAKI plan for inner dimension k: (int8 GEMMs, integer bits)."""
     s, t = C.c_int(), C.c_int()

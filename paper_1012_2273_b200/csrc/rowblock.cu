@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -74,6 +75,26 @@ Schedule make_schedule(int64_t m, int P) {
   return sc;
 }
 
+// Planning rates of mmws_gpu_rowblock_ranks (fixed, so every rank reaches
+// the same decision without exchanging anything).
+constexpr double PLAN_LINK_BPS = 600e9;
+constexpr double PLAN_FP64_FLOPS = 33e12, PLAN_FP32_FLOPS = 55e12;
+constexpr double PLAN_ROUND_LATENCY_S = 60e-6;
+
+int rowblock_active(int64_t m, int64_t n, int64_t k, int P, int elem_bytes) {
+  if (P <= 1) return 1;
+  if (const char* f = std::getenv("MMWS_GPU_ROWBLOCK_RANKS")) {
+    if (std::strcmp(f, "all") == 0) return P;
+    if (std::strcmp(f, "1") == 0) return 1;
+  }
+  double t1 = 0, tp = 0;
+  const double rate = elem_bytes == 8 ? PLAN_FP64_FLOPS : PLAN_FP32_FLOPS;
+  mmws_gpu_rowblock_cost(m, n, k, 1, elem_bytes, PLAN_LINK_BPS, rate, &t1, nullptr, nullptr);
+  mmws_gpu_rowblock_cost(m, n, k, P, elem_bytes, PLAN_LINK_BPS, rate, &tp, nullptr, nullptr);
+  ok();
+  return tp + PLAN_ROUND_LATENCY_S < t1 ? P : 1;
+}
+
 // Enqueue one master/worker round.  Rank 0 passes device A, B, C (dense); the
 // other ranks pass nulls and use library buffers.  On return ctx->ev1 (rank 0)
 // is recorded after the last C row has landed.
@@ -117,6 +138,22 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
     return MMWS_GPU_OK;
   }
   NCCL_REQUIRE();
+  if (P > 1 && rowblock_active(m, n, k, P, sizeof(T)) == 1) {
+    // too small to amortise the exchange: rank 0 multiplies alone, the
+    // workers have nothing to do (every rank takes this branch for the same
+    // arguments, so no collective is left half-matched).  A 1-rank world
+    // still runs the exchange engine below (it is how one GPU tests it).
+    cudaEventRecord(ctx->evk0, comp);
+    if (me != 0) {
+      cudaEventRecord(ctx->evk1, comp);
+      return MMWS_GPU_OK;
+    }
+    if (bracket) cudaEventRecord(ctx->ev0, comp);
+    if (int rc = gemm<T>(ctx, m, n, k, A, k, B, n, C, n, mode, comp)) return rc;
+    cudaEventRecord(ctx->evk1, comp);
+    if (bracket) cudaEventRecord(ctx->ev1, comp);
+    return MMWS_GPU_OK;
+  }
   // the multiplies below overlap NCCL transfers: no persistent (stream-K)
   // launches, which would keep the communication kernels off the SMs
   struct NoStreamK {
@@ -288,7 +325,11 @@ int master_run_host(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T*
   if (!root) return rowblock(ctx, m, n, k, static_cast<const T*>(nullptr),
                              static_cast<const T*>(nullptr), static_cast<T*>(nullptr), mode,
                              elapsed_s);
-  if (!ctx->comm)  // one GPU: copies overlapped with the multiply
+  // one GPU, or a round too small to distribute (rank 0 alone; the workers
+  // return at once from the rowblock call above): copies overlapped with
+  // the multiply
+  if (!ctx->comm || (ctx->nranks > 1 && m > 0 && n > 0 && k > 0 &&
+                     rowblock_active(m, n, k, ctx->nranks, sizeof(T)) == 1))
     return host_multiply(ctx, m, n, k, A, B, C, mode, elapsed_s);
   if (m <= 0 || n <= 0 || k <= 0)
     return fail(MMWS_GPU_ERR_DIMENSION, "master_run: dimensions must be positive");
@@ -457,6 +498,17 @@ int mmws_gpu_rowblock_cost(int64_t m, int64_t n, int64_t k, int nranks, int elem
   if (seconds) *seconds = t;
   if (root_egress_bytes) *root_egress_bytes = egress;
   if (root_ingress_bytes) *root_ingress_bytes = ingress;
+  return ok();
+}
+
+int mmws_gpu_rowblock_ranks(int64_t m, int64_t n, int64_t k, int nranks, int elem_bytes,
+                            int* active) {
+  if (!active) return fail(MMWS_GPU_ERR_DOMAIN, "rowblock_ranks: null active");
+  if (m <= 0 || n <= 0 || k <= 0)
+    return fail(MMWS_GPU_ERR_DIMENSION, "rowblock_ranks: dimensions must be positive");
+  if (nranks < 1 || (elem_bytes != 4 && elem_bytes != 8))
+    return fail(MMWS_GPU_ERR_DOMAIN, "rowblock_ranks: bad nranks / element size");
+  *active = rowblock_active(m, n, k, nranks, elem_bytes);
   return ok();
 }
 

@@ -180,6 +180,38 @@ def test_rowblock_cost_model():
         P.rowblock_cost(10, 10, 10, 2, 3, bw, fl)
 
 
+def test_rowblock_distributes_only_where_it_pays(monkeypatch):
+    # north_star (3): the row-block exchange is used only where N is large
+    # enough to amortise the transfers -- rank 0 alone below that.
+    monkeypatch.delenv("MMWS_GPU_ROWBLOCK_RANKS", raising=False)
+    for n in (10, 100, 500, 1000):
+        assert P.rowblock_ranks(n, n, n, 8) == 1, n
+    for n in (2000, 4096, 16384):
+        assert P.rowblock_ranks(n, n, n, 8) == 8, n
+        assert P.rowblock_ranks(n, n, n, 2, 4) == 2, n
+    assert P.rowblock_ranks(32768, 32768, 32768, 8, 4) == 8
+    assert P.rowblock_ranks(16384, 16384, 16384, 1) == 1
+    # monotone: once distributed, every larger square problem is too
+    seen = False
+    for n in range(200, 4000, 50):
+        d = P.rowblock_ranks(n, n, n, 4) == 4
+        assert d or not seen, n
+        seen = seen or d
+    assert seen
+    # it is the cost model's own comparison (plus the fixed round latency)
+    t1, _, _ = P.rowblock_cost(3000, 3000, 3000, 1, 8, 600e9, 33e12)
+    t8, _, _ = P.rowblock_cost(3000, 3000, 3000, 8, 8, 600e9, 33e12)
+    assert (t8 + 60e-6 < t1) == (P.rowblock_ranks(3000, 3000, 3000, 8) == 8)
+    monkeypatch.setenv("MMWS_GPU_ROWBLOCK_RANKS", "all")
+    assert P.rowblock_ranks(10, 10, 10, 8) == 8
+    monkeypatch.setenv("MMWS_GPU_ROWBLOCK_RANKS", "1")
+    assert P.rowblock_ranks(16384, 16384, 16384, 8) == 1
+    with pytest.raises(P.DimensionError):
+        P.rowblock_ranks(0, 4, 4, 2)
+    with pytest.raises(P.DomainError):
+        P.rowblock_ranks(4, 4, 4, 2, 3)
+
+
 REF_CP = os.path.join(ROOT, "oracle", "_ref", "ref_control_plane")
 
 
