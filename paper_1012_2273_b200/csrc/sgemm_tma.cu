@@ -130,7 +130,6 @@ __global__ void __launch_bounds__(THREADS, 1)
           b2[2 * j] = pack2(b.x, b.y);
           b2[2 * j + 1] = pack2(b.z, b.w);
         }
-#pragma unroll
         f32x2 aa[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {

@@ -200,8 +200,13 @@ def test_every_dmma_tile_plan_gives_the_same_bits(ctx, oracle, monkeypatch, shap
                               if r <= per_sm and tiles >= r * sms and r * bm * bn <= 128 * 128]
         for plan in plans:
             monkeypatch.setenv("MMWS_GPU_DMMA_PLAN", plan)
-            got = host(ctx.dgemm(A, B, mode=P.MODE_DMMA))
-            assert (bits(got) == bits(want)).all(), (shape, plan)
+            # strided C inside a canary frame: the plan writes exactly C
+            buf = torch().full((m + 2, n + 3), -7.5, dtype=torch().float64, device="cuda")
+            ctx.dgemm(A, B, buf[1:m + 1, 1:n + 1], mode=P.MODE_DMMA)
+            b = host(buf)
+            assert (bits(b[1:m + 1, 1:n + 1]) == bits(want)).all(), (shape, plan)
+            assert (b[0] == -7.5).all() and (b[m + 1] == -7.5).all(), (shape, plan)
+            assert (b[:, 0] == -7.5).all() and (b[:, n + 1:] == -7.5).all(), (shape, plan)
             tried += 1
     monkeypatch.delenv("MMWS_GPU_DMMA_PLAN")
     for mode in (P.MODE_AUTO, P.MODE_DMMA_SMALL):
