@@ -366,10 +366,13 @@ bool exact_tma_ok(int64_t lda, int64_t ldb, const double* A, const double* B) {
          reinterpret_cast<uintptr_t>(B) % 16 == 0;
 }
 
-cudaError_t launch_dgemm_exact_sk(const Launch& L, int64_t M, int64_t N, int64_t K,
+cudaError_t launch_dgemm_exact_sk(const Launch& L, int tile, int64_t M, int64_t N, int64_t K,
                                   const double* A, int64_t lda, const double* B, int64_t ldb,
                                   double* C, int64_t ldc, double* partial, int* flags, int grid) {
-  return run_exact_tma<128, 128, true>(L, M, N, K, A, lda, B, ldb, C, ldc, partial, flags, grid);
+  return tile == 64
+             ? run_exact_tma<64, 64, true>(L, M, N, K, A, lda, B, ldb, C, ldc, partial, flags, grid)
+             : run_exact_tma<128, 128, true>(L, M, N, K, A, lda, B, ldb, C, ldc, partial, flags,
+                                             grid);
 }
 
 cudaError_t launch_dgemm_exact(const Launch& L, int64_t M, int64_t N, int64_t K, const double* A,
@@ -399,7 +402,7 @@ cudaError_t launch_dgemm_exact(const Launch& L, int64_t M, int64_t N, int64_t K,
 
 cudaError_t preload_dgemm_exact() {
   return preload_kernels(dgemm_exact_tma_kernel<64, 64>, dgemm_exact_tma_kernel<128, 128>,
-                         dgemm_exact_tma_kernel<128, 128, true>,
+                         dgemm_exact_tma_kernel<128, 128, true>, dgemm_exact_tma_kernel<64, 64, true>,
                          dgemm_exact_kernel<true, true>, dgemm_exact_kernel<true, false>,
                          dgemm_exact_kernel<false, true>, dgemm_exact_kernel<false, false>);
 }

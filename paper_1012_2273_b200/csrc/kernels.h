@@ -127,11 +127,11 @@ cudaError_t launch_dgemm_dmma(const Launch& L, int cfg, int64_t M, int64_t N, in
 
 // Exact-order SIMT: per element acc = +0.0; for j ascending acc = (acc + a*b)
 // with separate roundings -- bitwise equal to matmul_seq for every input.
-// Exact-order stream-K (128x128 TMA kernel, bitwise matmul_seq); same
-// workspace contract as launch_dgemm_dmma_sk.  exact_tma_ok: the layout the
-// TMA kernels (and so this one) accept.
+// Exact-order stream-K (128x128 or 64x64 TMA kernel, `tile`; bitwise
+// matmul_seq); same workspace contract as launch_dgemm_dmma_sk, tiles >= grid.
+// exact_tma_ok: the layout the TMA kernels (and so this one) accept.
 bool exact_tma_ok(int64_t lda, int64_t ldb, const double* A, const double* B);
-cudaError_t launch_dgemm_exact_sk(const Launch& L, int64_t M, int64_t N, int64_t K,
+cudaError_t launch_dgemm_exact_sk(const Launch& L, int tile, int64_t M, int64_t N, int64_t K,
                                   const double* A, int64_t lda, const double* B, int64_t ldb,
                                   double* C, int64_t ldc, double* partial, int* flags, int grid);
 cudaError_t launch_dgemm_exact(const Launch& L, int64_t M, int64_t N, int64_t K,

@@ -132,10 +132,21 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
   const int64_t G = ctx->num_sms;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(L.stream, &cap);
+  const bool sk_ok = cap == cudaStreamCaptureStatusNone && !ctx->server && ctx->allow_streamk &&
+                     !std::getenv("MMWS_GPU_NO_STREAMK");
   const bool sk = (mode == MMWS_GPU_MODE_DMMA || mode == MMWS_GPU_MODE_EXACT) && tiles128 >= G &&
-                  tiles128 < 32 * G &&
-                  cap == cudaStreamCaptureStatusNone && !ctx->server && ctx->allow_streamk &&
-                  !std::getenv("MMWS_GPU_NO_STREAMK");
+                  tiles128 < 32 * G && sk_ok;
+  // Exact order below one 128x128 tile per SM: stream-K over 64x64 tiles
+  // (one CTA of 8 math warps per SM already fills the FP64 pipe) when the
+  // one-shot 64x64 launch would leave the SMs unevenly loaded -- tiles per
+  // SM rounded up more than ~10 % above the average.  GPU time per call
+  // (tools/streamk_probe.py), stream-K vs one-shot: N=800 81.9 vs 122.8 us,
+  // 900 115.5 vs 139.2, 1000 141.3 vs 153.5, 1100 192.5 vs 243.7, 1200 229.2
+  // vs 262.0, 1400 353.1 vs 405.5; balanced sizes stay one-shot (1300 286.7
+  // vs 301.8, 1500 432.1 vs 446.3).
+  const int64_t tiles64 = ((m + 63) / 64) * ((n + 63) / 64);
+  const bool sk64 = mode == MMWS_GPU_MODE_EXACT && tiles128 < G && tiles64 >= G && sk_ok &&
+                    10 * tiles64 < 9 * (((tiles64 + G - 1) / G) * G);
   // TMA needs 16-byte aligned bases and even row pitches: pack A and/or B into
   // the workspace otherwise (one HBM-bound pass, zero padding never read).
   auto pack_operands = [&]() -> int {
@@ -173,12 +184,13 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
     if (n <= 256 && k <= 256) {
       e = launch_dgemm_small(L, true, m, n, k, A, lda, B, ldb, C, ldc);
       ctx->last_plan = "dgemm_small_kernel<exact, 32x32>";
-    } else if (sk) {
+    } else if (sk || sk64) {
       if (int rc = sk_workspace(ctx, L.stream, &sk_partial, &sk_flags)) return rc;
       if (int rc = pack_operands()) return rc;
-      e = launch_dgemm_exact_sk(L, m, n, k, A, lda, B, ldb, C, ldc, sk_partial, sk_flags,
-                                static_cast<int>(G));
-      ctx->last_plan = "dgemm_exact_tma_kernel<128x128, stream-K>";
+      e = launch_dgemm_exact_sk(L, sk ? 128 : 64, m, n, k, A, lda, B, ldb, C, ldc, sk_partial,
+                                sk_flags, static_cast<int>(G));
+      ctx->last_plan = sk ? "dgemm_exact_tma_kernel<128x128, stream-K>"
+                          : "dgemm_exact_tma_kernel<64x64, stream-K>";
     } else {
       e = launch_dgemm_exact(L, m, n, k, A, lda, B, ldb, C, ldc);
       ctx->last_plan = "dgemm_exact (one-shot)";

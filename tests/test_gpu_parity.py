@@ -149,11 +149,13 @@ def test_config_c3_n4099_integer_bit_exact(ctx, oracle, golden_big):
 
 
 @pytest.mark.parametrize("shape", [(2000, 2000, 2000), (1536, 999, 1664), (1280, 5000, 1920),
-                                   (1536, 16, 1664), (2100, 1001, 2303), (2304, 2304, 2304)])
+                                   (1536, 16, 1664), (2100, 1001, 2303), (2304, 2304, 2304),
+                                   (1000, 1000, 1000), (1100, 701, 903)])
 def test_stream_k_is_bitwise_the_one_shot_kernel(ctx, oracle, monkeypatch, shape):
     # 148..1183 tiles of 128x128 with a partial last wave take the stream-K
     # launch (accumulators of a cut tile continued by the next CTA); it must
-    # reproduce the one-shot kernels' bits exactly.
+    # reproduce the one-shot kernels' bits exactly.  The last two shapes have
+    # fewer 128x128 tiles than SMs: the exact mode's 64x64 stream-K.
     m, k, n = shape
     A = ctx.fill(P.DIST_UNIFORM, 31, m, k)
     B = ctx.fill(P.DIST_UNIFORM, 32, k, n)
