@@ -150,7 +150,7 @@ def test_config_c3_n4099_integer_bit_exact(ctx, oracle, golden_big):
 
 @pytest.mark.parametrize("shape", [(2000, 2000, 2000), (1536, 999, 1664), (1280, 5000, 1920),
                                    (1536, 16, 1664), (2100, 1001, 2303), (2304, 2304, 2304),
-                                   (1000, 1000, 1000), (1100, 701, 903)])
+                                   (1000, 1000, 1000), (1100, 701, 1100)])
 def test_stream_k_is_bitwise_the_one_shot_kernel(ctx, oracle, monkeypatch, shape):
     # 148..1183 tiles of 128x128 with a partial last wave take the stream-K
     # launch (accumulators of a cut tile continued by the next CTA); it must
@@ -812,4 +812,10 @@ def test_auto_tile_plan_by_size(ctx):
     assert ctx.last_plan.startswith("dgemm_dmma_kernel<32x32")
     ctx.dgemm(A, A, mode=P.MODE_EXACT)
     assert ctx.last_plan == "dgemm_exact_tma_kernel<128x128, stream-K>"
+    A = T.zeros((1000, 1000), dtype=T.float64, device="cuda")
+    ctx.dgemm(A, A, mode=P.MODE_EXACT)             # 256 tiles of 64x64: uneven one-shot
+    assert ctx.last_plan == "dgemm_exact_tma_kernel<64x64, stream-K>"
+    A = T.zeros((1300, 1300), dtype=T.float64, device="cuda")
+    ctx.dgemm(A, A, mode=P.MODE_EXACT)             # 441 tiles: 2.98 per SM, one-shot
+    assert ctx.last_plan == "dgemm_exact (one-shot)"
     T.cuda.synchronize()
