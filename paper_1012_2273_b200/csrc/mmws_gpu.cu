@@ -178,9 +178,10 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
   if (mode == MMWS_GPU_MODE_EXACT) {
     // exact order: the 32x32 latency kernel for tiny problems, the stream-K
     // form of the 128x128 TMA kernel (operands packed if needed) from one
-    // tile per SM, else the 64x64 / 128x128 TMA kernels or the cp.async
-    // kernel for layouts TMA cannot read -- every variant gives matmul_seq's
-    // bits
+    // tile per SM, of the 64x64 one below that where a one-shot launch would
+    // load the SMs unevenly, else the 64x64 / 128x128 TMA kernels or the
+    // cp.async kernel for layouts TMA cannot read -- every variant gives
+    // matmul_seq's bits
     if (n <= 256 && k <= 256) {
       e = launch_dgemm_small(L, true, m, n, k, A, lda, B, ldb, C, ldc);
       ctx->last_plan = "dgemm_small_kernel<exact, 32x32>";
