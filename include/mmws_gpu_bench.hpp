@@ -373,6 +373,8 @@ inline void write_file(const std::string& path, const std::string& body) {
 }
 
 inline const char* model_color(const std::string& model) {
+  if (model == "seq") return "#9467bd";      // the reference's CPU models
+  if (model == "threads") return "#ff7f0e";
   if (model == "gpu") return "#1f77b4";
   if (model == "gpu-exact") return "#555555";
   if (model == "gpu-rowblock") return "#d62728";
@@ -382,7 +384,8 @@ inline const char* model_color(const std::string& model) {
 }  // namespace plot_detail
 
 // emit_plots (plots.hpp:145-198): runtime.svg, mflops.svg and speedup.svg in
-// `dir`, one series per model in gpu / gpu-exact / gpu-rowblock order.  With
+// `dir`, one series per model in seq / threads (the reference's CPU models,
+// when present) / gpu / gpu-exact / gpu-rowblock order.  With
 // a CostFit and gpu-rowblock records, runtime.svg gains the dashed
 // "cost-model" series of predicted round times.
 inline void emit_plots(const std::vector<BenchRecord>& records, const std::string& dir,
@@ -393,7 +396,7 @@ inline void emit_plots(const std::vector<BenchRecord>& records, const std::strin
   if (ec) throw IoError("cannot create " + dir + ": " + ec.message());
   auto series_of = [&](auto value_of) {
     std::vector<PlotSeries> out;
-    for (const char* name : {"gpu", "gpu-exact", "gpu-rowblock"}) {
+    for (const char* name : {"seq", "threads", "gpu", "gpu-exact", "gpu-rowblock"}) {
       PlotSeries s{name, plot_detail::model_color(name), false, {}};
       for (const auto& r : records)
         if (r.model == name)

@@ -138,3 +138,28 @@ def test_cli_gpus_mode_through_the_reference_launcher(tmp_path):
     assert [ln.split(",")[:3] for ln in lines[1:]] == [["gpu-rowblock", "100", "1"],
                                                        ["gpu-rowblock", "1000", "1"]]
     assert "calibration: link" in r.stdout   # 1 rank: no link to measure (nominal)
+
+
+@pytest.mark.gpu
+def test_cli_cpu_models_through_the_reference_suite(tmp_path):
+    # --cpu-models: the reference's own run_suite times seq / threads first (its
+    # own gate included); their seq times give every GPU record its speedup
+    exe = os.path.join(ROOT, "oracle", "_ref", "mmws_gpu_bench_ref")
+    if not os.path.exists(exe):
+        pytest.skip("mmws_gpu_bench_ref not built (needs the reference headers at build time)")
+    csv = tmp_path / "out.csv"
+    r = subprocess.run([exe, "--dims", "10,200", "--models", "gpu,gpu-exact",
+                        "--cpu-models", "seq,threads", "--csv", str(csv),
+                        "--plots", str(tmp_path / "svg")],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    rows = [ln.split(",") for ln in csv.read_text().splitlines()[1:]]
+    assert [(f[0], f[1]) for f in rows] == [("seq", "10"), ("seq", "200"), ("threads", "10"),
+                                            ("threads", "200"), ("gpu", "10"), ("gpu", "200"),
+                                            ("gpu-exact", "10"), ("gpu-exact", "200")]
+    seq = {f[1]: float(f[3]) for f in rows if f[0] == "seq"}
+    for f in rows:
+        assert f[5] != "", f                              # every record paired with seq
+        assert abs(float(f[5]) - seq[f[1]] / float(f[3])) <= 1e-4 * float(f[5])
+    _, s = _series(tmp_path / "svg" / "speedup.svg")
+    assert {"seq", "threads", "gpu", "gpu-exact"} <= set(k for k in s if "#" not in k)

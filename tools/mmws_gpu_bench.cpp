@@ -5,6 +5,13 @@
 //   mmws_gpu_bench --dims 100,500,1000 [--models gpu,gpu-exact] [--repeats 3]
 //                  [--seed 42] [--csv out.csv] [--tolerance 1e-12] [--server]
 //                  [--plots DIR] [--calibrate] [--gpus P]
+//                  [--cpu-models seq,threads] [--cpu-repeats R]
+//
+// --cpu-models (needs the reference headers): the reference's own run_suite
+// (bench.hpp:133-188) times its seq / threads models on this host first, with
+// its own gate; their records join the CSV / table / plots and the seq times
+// give every GPU record its speedup column -- the paper's comparison in one
+// run.
 //
 // --gpus P (gpu-rowblock over P GPUs of this node, one process per GPU): rank
 // 0 spawns ranks 1..P-1 -- this binary in worker mode -- with the reference's
@@ -25,9 +32,13 @@
 
 #include "mmws_gpu_bench.hpp"
 
-#if __has_include(<mmws/launch.hpp>) && __has_include(<nlohmann/json.hpp>)
+#if __has_include(<mmws/launch.hpp>) && __has_include(<json.hpp>)
 #include <mmws/launch.hpp>
 #define MMWS_GPU_BENCH_HAVE_LAUNCHER 1
+#endif
+#if __has_include(<mmws/bench.hpp>) && __has_include(<json.hpp>)
+#include <mmws/bench.hpp>
+#define MMWS_GPU_BENCH_HAVE_REF_SUITE 1
 #endif
 
 namespace {
@@ -44,7 +55,8 @@ std::vector<std::string> split(const std::string& s) {
 int usage() {
   std::fprintf(stderr,
                "usage: mmws_gpu_bench --dims N1,N2,... [--models gpu,gpu-exact,gpu-rowblock] "
-               "[--repeats R] [--seed S] [--tolerance T] [--csv PATH] [--device D] [--server] [--plots DIR] [--calibrate] [--gpus P]\n");
+               "[--repeats R] [--seed S] [--tolerance T] [--csv PATH] [--device D] [--server] [--plots DIR] [--calibrate] [--gpus P] "
+               "[--cpu-models seq,threads] [--cpu-repeats R]\n");
   return 2;
 }
 
@@ -75,6 +87,8 @@ int main(int argc, char** argv) {
   bool server = false;  // resident latency server for N <= 96 (mmws_gpu_server_start)
   int gpus = 0;  // 0: no --gpus, plain single-context run
   bool worker = false;
+  std::vector<std::string> cpu_models;  // the reference's own seq / threads models
+  int cpu_repeats = 1;
   try {
     for (int i = 1; i < argc; ++i) {
       const std::string arg = argv[i];
@@ -107,6 +121,10 @@ int main(int argc, char** argv) {
         worker = true;
       } else if (arg == "--server") {
         server = true;
+      } else if (arg == "--cpu-models") {
+        cpu_models = split(value());
+      } else if (arg == "--cpu-repeats") {
+        cpu_repeats = std::stoi(value());
       } else {
         return usage();
       }
@@ -129,7 +147,38 @@ int main(int argc, char** argv) {
     if (world) mmws::gpu::comm_init_from(ctx, world->comm);
 #endif
     if (server) ctx.server_start();
-    const auto records = mmws::gpu::run_suite(ctx, config);
+    std::vector<mmws::gpu::BenchRecord> records;
+    std::vector<std::pair<std::int64_t, double>> seq_times;
+    if (!cpu_models.empty()) {
+#ifdef MMWS_GPU_BENCH_HAVE_REF_SUITE
+      mmws::BenchConfig ref;
+      ref.dims = config.dims;
+      ref.models.clear();
+      for (const auto& m : cpu_models) {
+        const mmws::Model model = mmws::model_from_name(m);
+        if (model == mmws::Model::msg)
+          throw mmws::DomainError("--cpu-models: msg is the TCP protocol, not a CPU model here");
+        ref.models.push_back(model);
+      }
+      ref.repeats = cpu_repeats;
+      ref.seed = config.seed;
+      for (const auto& r : mmws::run_suite(ref)) {  // the reference's harness, unchanged
+        mmws::gpu::BenchRecord rec;
+        rec.model = mmws::model_name(r.model);
+        rec.n = r.n;
+        rec.workers = r.workers;
+        rec.elapsed = r.elapsed;
+        rec.mflops = r.mflops;
+        rec.speedup = r.speedup;
+        if (r.model == mmws::Model::seq) seq_times.emplace_back(r.n, r.elapsed);
+        records.push_back(std::move(rec));
+      }
+#else
+      (void)cpu_repeats;
+      throw mmws::DomainError("--cpu-models needs the reference headers at build time");
+#endif
+    }
+    for (auto& r : mmws::gpu::run_suite(ctx, config, seq_times)) records.push_back(std::move(r));
     std::printf("%-13s %8s %8s %14s %14s %12s\n", "model", "n", "gpus", "elapsed_s", "mflops",
                 "rel_err");
     for (const auto& r : records)
