@@ -307,10 +307,17 @@ int host_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A
   cudaStream_t in = ctx->copy_in, comp = ctx->stream, out = ctx->copy_out;
 
   // Panels of 1/8 of the rows (multiples of 128) once the problem is big
-  // enough for the overlap to matter; one panel otherwise.
+  // enough for the overlap to matter; one panel otherwise.  Pinned buffers
+  // pipeline from m*n*k = 1e8 on (host-buffer multiply, min of 25 interleaved
+  // calls: N=750 260.5 vs 292.4 us, 1000 415.2 vs 514.7, 1250 648.5 vs
+  // 818.8); pageable ones only from 2e9, because every panel's copy is
+  // pumped through the pinned staging ring in chunks of its own (N=1000 with
+  // 8 panels: 2.2 ms vs 1.3 ms in one).
   const double work = static_cast<double>(m) * n * k;
+  const bool pinned = !is_pageable(A) && !is_pageable(C);
+  const double min_work = pinned ? 1.0e8 : 2.0e9;
   // small MODE_OZAKI problems would recompute B's residues per launch: one panel
-  const int64_t R = (work < 2.0e9 || mode == MMWS_GPU_MODE_OZAKI)
+  const int64_t R = (work < min_work || mode == MMWS_GPU_MODE_OZAKI)
                         ? m
                         : std::max<int64_t>(128, ((m + 7) / 8 + 127) / 128 * 128);
   const int64_t panels = (m + R - 1) / R;

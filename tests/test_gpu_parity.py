@@ -595,6 +595,26 @@ def test_host_entry_matches_device_entry(ctx, oracle):
     assert normwise(cf.astype(np.float64), oracle.matmul_rows(list(range(257)), af, bf)) <= FP32_TOL
 
 
+def test_host_entry_pinned_panels_match_pageable_and_device(ctx, oracle):
+    # pinned host buffers take the row-panel pipeline from m*n*k = 1e8 on,
+    # pageable ones from 2e9: same bits either way, and the device entry's
+    T = torch()
+    for (m, k, n) in [(700, 600, 900), (1001, 999, 1003), (333, 2000, 700)]:
+        a = oracle.fill(oracle.DIST_UNIFORM, 7, m, k)
+        b = oracle.fill(oracle.DIST_UNIFORM, 8, k, n)
+        want = host(ctx.dgemm(dev(a), dev(b)))
+        ap = T.from_numpy(a).pin_memory().numpy()
+        bp = T.from_numpy(b).pin_memory().numpy()
+        cp = T.empty((m, n), dtype=T.float64).pin_memory().numpy()
+        got, _ = ctx.matmul_host(ap, bp, out=cp)
+        assert (bits(got) == bits(want)).all(), (m, k, n, "pinned")
+        got, _ = ctx.matmul_host(a, b)
+        assert (bits(got) == bits(want)).all(), (m, k, n, "pageable")
+        ex, _ = ctx.matmul_host(ap, bp, mode=P.MODE_EXACT, out=cp)
+        rows = [0, m // 2, m - 1]
+        assert (bits(ex[rows]) == bits(oracle.matmul_rows(rows, a, b))).all()
+
+
 @pytest.mark.timeout(180, method="thread")
 @pytest.mark.parametrize("ctas", [None, "1", "3"])
 def test_latency_server_bitwise_equals_device_entry(oracle, monkeypatch, ctas):
