@@ -31,8 +31,10 @@ namespace {
 constexpr size_t CHUNK = size_t(32) << 20;  // bytes per pinned chunk
 constexpr int NSLOT = 4;
 // below this a direct pageable cudaMemcpy (the driver's own staging) wins
-// over waking the copy threads
-constexpr size_t STAGE_MIN = size_t(2) << 20;
+// over the copy threads.  With spinning workers the cut sits low: pageable
+// host multiply (min of 40 back-to-back calls) N=250 72 vs 112 us with a 2 MB
+// cut, 350 108 vs 207, 500 199 vs 389, 180 51 vs 69
+constexpr size_t STAGE_MIN = size_t(64) << 10;
 
 // rows per chunk: at least four chunks per copy (so the host copy of one
 // overlaps the DMA of the previous even for mid-size matrices), 1 MB to
