@@ -31,10 +31,12 @@ namespace {
 constexpr size_t CHUNK = size_t(32) << 20;  // bytes per pinned chunk
 constexpr int NSLOT = 4;
 // below this a direct pageable cudaMemcpy (the driver's own staging) wins
-// over the copy threads.  With spinning workers the cut sits low: pageable
-// host multiply (min of 40 back-to-back calls) N=250 72 vs 112 us with a 2 MB
-// cut, 350 108 vs 207, 500 199 vs 389, 180 51 vs 69
-constexpr size_t STAGE_MIN = size_t(64) << 10;
+// over a pinned slot.  With spinning workers (and copies up to 128 KB done
+// by the caller alone) the cut sits low: pageable host multiply (min of 40
+// back-to-back calls) N=50 29.8 vs 45.3 us with a 2 MB cut, 180 51 vs 69,
+// 250 72 vs 112, 350 108 vs 207, 500 199 vs 389; at N=10 (800 B) the
+// driver's path is still a little faster
+constexpr size_t STAGE_MIN = size_t(4) << 10;
 
 // rows per chunk: at least four chunks per copy (so the host copy of one
 // overlaps the DMA of the previous even for mid-size matrices), 1 MB to
@@ -69,6 +71,10 @@ class CopyPool {
   // dst/src row-pitched regions of `rows` rows x `width` bytes.
   void copy(char* dst, size_t dpitch, const char* src, size_t spitch, size_t width,
             size_t rows) {
+    if (width * rows <= INLINE_MAX) {  // not worth a hand-off: the caller copies it
+      for (size_t r = 0; r < rows; ++r) std::memcpy(dst + r * dpitch, src + r * spitch, width);
+      return;
+    }
     job_ = {dst, dpitch, src, spitch, width, rows};
     pending_.store(n_ - 1, std::memory_order_relaxed);
     {
@@ -82,6 +88,7 @@ class CopyPool {
 
  private:
   static constexpr int64_t SPIN_NS = 200000;
+  static constexpr size_t INLINE_MAX = size_t(128) << 10;
   struct Job {
     char* dst;
     size_t dpitch;
