@@ -182,6 +182,16 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- our arm
+def measured_hbm_gbs() -> float:
+    """HBM copy bandwidth of this pool (MEASURED_PEAKS.json, driver-written),
+    else the profiling recipe's fallback (6.65 TB/s)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
 def profiled_traffic(n: int, plan: str):
     """dram bytes per launch of the dominant kernel from the committed ncu
     capture (profiles/*_ncu_summary*.json), if one matches this N and kernel
@@ -372,6 +382,14 @@ def run_ours(args) -> None:
                 "peak_nominal": NOMINAL_FP64_TFLOPS, "frac_of_nominal": achieved / NOMINAL_FP64_TFLOPS,
                 "flops_per_launch": 2.0 * rows0 * n * n, "kernel_ms_avg": kern_avg_ms,
                 "traffic_source": traffic_src,
+                "traffic_note": (None if traffic is None else
+                                 "ncu dram bytes per launch vs %.2f GB algorithmic: each wave of "
+                                 "148 tiles streams its ~24 A/B panels (16 MB each) from HBM "
+                                 "again because they exceed the 126 MB L2; %.1f%% of HBM "
+                                 "bandwidth over the launch, the FP64 tensor pipe is the bound"
+                                 % (8.0 * (2 * rows0 * n + n * n) / 1e9,
+                                    100.0 * traffic / (kern_avg_ms / 1e3) / 1e9
+                                    / measured_hbm_gbs())),
             },
             "cpu_baseline": cpu,
             "e2e": {"value": flops / e2e_s / 1e9, "unit": "GFLOP/s",
