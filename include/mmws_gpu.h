@@ -34,9 +34,9 @@ extern "C" {
 #define MMWS_GPU_ABI_VERSION 1
 
 /* Status codes.  DIMENSION / DOMAIN mirror the reference's DimensionError /
- * DomainError (error.hpp:9-17); RANK / PROTOCOL mirror RankError /
- * ProtocolError (error.hpp:20-32); CUDA / NCCL / ALLOC / STATE are device-side
- * failures the reference cannot have. */
+ * DomainError (error.hpp:9-17); RANK / PROTOCOL / TIMEOUT mirror RankError /
+ * ProtocolError / TimeoutError (error.hpp:20-39); CUDA / NCCL / ALLOC / STATE
+ * are device-side failures the reference cannot have. */
 enum {
   MMWS_GPU_OK = 0,
   MMWS_GPU_ERR_DIMENSION = 1,
@@ -46,7 +46,8 @@ enum {
   MMWS_GPU_ERR_RANK = 5,
   MMWS_GPU_ERR_PROTOCOL = 6,
   MMWS_GPU_ERR_STATE = 7,
-  MMWS_GPU_ERR_ALLOC = 8
+  MMWS_GPU_ERR_ALLOC = 8,
+  MMWS_GPU_ERR_TIMEOUT = 9
 };
 
 /* Multiply modes.
@@ -228,6 +229,8 @@ int mmws_gpu_gemm_probe(mmws_gpu_ctx* ctx, int64_t n, int mode, int iters, doubl
  * (torch.distributed, the reference's launch.hpp control plane, MPI, ...);
  * every rank then calls mmws_gpu_comm_init. */
 int mmws_gpu_nccl_unique_id(uint8_t out[128]);
+/* Non-blocking NCCL communicator: returns once all nranks ranks joined, or
+ * MMWS_GPU_ERR_TIMEOUT after the deadline (mmws_gpu_set_timeout). */
 int mmws_gpu_comm_init(mmws_gpu_ctx* ctx, int nranks, int rank, const uint8_t id[128]);
 int mmws_gpu_comm_destroy(mmws_gpu_ctx* ctx);
 
@@ -261,6 +264,20 @@ int mmws_gpu_master_run_host(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k,
 int mmws_gpu_master_run_host_f32(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k,
                                  const float* A, const float* B, float* C, int mode,
                                  double* elapsed_s);
+/* The most recent row-block / master_run call: how many ranks multiplied
+ * (1 = rank 0 alone or no communicator) and how C came back: 0 no exchange,
+ * 1 fused (worker GEMM epilogues stored into rank 0's C over CUDA IPC),
+ * 2 NCCL C-slice messages. */
+int mmws_gpu_last_round(mmws_gpu_ctx* ctx, int* active_ranks, int* gather);
+/* Deadline of one distributed step (communicator bootstrap, a round, a probe):
+ * default 30 s (the reference's receive timeout, comm.hpp:144), or
+ * MMWS_GPU_TIMEOUT_S at mmws_gpu_init.  When it passes -- or NCCL reports a
+ * failed peer -- the communicator is aborted and the call returns
+ * MMWS_GPU_ERR_PROTOCOL naming the worker rank(s) that fell behind (from a
+ * progress board every rank updates over NVLink), or MMWS_GPU_ERR_TIMEOUT
+ * when no rank can be named.  Afterwards every row-block call fails with
+ * MMWS_GPU_ERR_STATE until mmws_gpu_comm_destroy + mmws_gpu_comm_init. */
+int mmws_gpu_set_timeout(mmws_gpu_ctx* ctx, double seconds);
 /* Device time (ms, CUDA events on the launch stream) of this rank's multiply
  * kernel(s) in the most recent row-block / master_run call. */
 int mmws_gpu_last_kernel_ms(mmws_gpu_ctx* ctx, double* ms);
@@ -278,6 +295,11 @@ int mmws_gpu_last_plan(mmws_gpu_ctx* ctx, const char** name);
  * communication stream; *bytes_per_s = bytes / time per broadcast on this
  * rank.  Needs mmws_gpu_comm_init. */
 int mmws_gpu_link_probe(mmws_gpu_ctx* ctx, int64_t bytes, int iters, double* bytes_per_s);
+/* Collective: `iters` point-to-point copies of `bytes` from rank 0 to each
+ * worker in turn (the A-slice / C-slice link), timed on the communication
+ * stream; *bytes_per_s = the slowest peer's rate on rank 0, the rank's own
+ * link on a worker, 0 in a 1-rank world. */
+int mmws_gpu_p2p_probe(mmws_gpu_ctx* ctx, int64_t bytes, int iters, double* bytes_per_s);
 int mmws_gpu_rowblock_cost(int64_t m, int64_t n, int64_t k, int nranks, int elem_bytes,
                            double link_bytes_per_s, double gemm_flops_per_s, double* seconds,
                            double* root_egress_bytes, double* root_ingress_bytes);

@@ -19,9 +19,10 @@
 // on the include path, or mmws::gpu::HostMatrix<T> (MatrixF32 for the fp32
 // configuration, which the reference has no type for).
 //
-// Errors: DimensionError / DomainError / RankError / ProtocolError are the
-// reference's own types (error.hpp) when available, identical stand-ins
-// otherwise; CUDA / NCCL failures throw mmws::gpu::GpuError.
+// Errors: DimensionError / DomainError / RankError / ProtocolError /
+// TimeoutError are the reference's own types (error.hpp) when available,
+// identical stand-ins otherwise; CUDA / NCCL failures throw
+// mmws::gpu::GpuError.
 #pragma once
 
 #include <cstddef>
@@ -48,6 +49,9 @@ struct RankError : std::out_of_range {
   using std::out_of_range::out_of_range;
 };
 struct ProtocolError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct TimeoutError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 struct IoError : std::runtime_error {
@@ -80,6 +84,7 @@ inline void check(int rc) {
     case MMWS_GPU_ERR_DOMAIN: throw DomainError(msg);
     case MMWS_GPU_ERR_RANK: throw RankError(msg);
     case MMWS_GPU_ERR_PROTOCOL: throw ProtocolError(msg);
+    case MMWS_GPU_ERR_TIMEOUT: throw TimeoutError(msg);
     default: throw GpuError(msg);
   }
 }
@@ -146,6 +151,15 @@ class Context {
     std::vector<std::uint8_t> id(128);
     check(mmws_gpu_nccl_unique_id(id.data()));
     return id;
+  }
+  // Deadline of one distributed step (default 30 s, the reference's receive
+  // timeout comm.hpp:144): a round that makes no progress throws
+  // ProtocolError naming the worker rank(s) behind, or TimeoutError.
+  void set_timeout(double seconds) { check(mmws_gpu_set_timeout(ctx_, seconds)); }
+  void comm_destroy() {
+    check(mmws_gpu_comm_destroy(ctx_));
+    rank_ = 0;
+    world_ = 1;
   }
   void comm_init(int world_size, int rank, const std::vector<std::uint8_t>& id) {
     if (id.size() != 128) throw DomainError("comm_init: unique id must be 128 bytes");
@@ -277,13 +291,24 @@ M matmul_threads(Context& ctx, const M& a, const M& b, unsigned workers) {
   return detail::multiply(ctx, a, b, Mode::exact, "matmul_threads");
 }
 
+// The reference's master_run / worker_run return exactly matmul_seq's bits
+// (mm_node --verify checks it with bitwise_equal), so the drop-in defaults to
+// Mode::exact for fp64; fp32 (no reference counterpart) defaults to the FFMA
+// path.  Mode::automatic opts into the FP64 tensor path (normwise <= 1e-12,
+// bit-exact for integer-valued inputs).
+template <class M>
+constexpr Mode contract_mode() {
+  return sizeof(decltype(detail::element_type(std::declval<const M&>()))) == 8 ? Mode::exact
+                                                                                : Mode::ffma;
+}
+
 // master_run (protocol.hpp:50-108) on rank 0 of the context's NCCL world:
 // row blocks of A by split_rows over all ranks (rank 0 computes too), B
 // broadcast, C gathered.  Returns (C, elapsed first send -> last receive,
 // including the host<->device copies of A, B and C).
 template <class M>
 std::pair<M, double> master_run(Context& ctx, const M& a, const M& b,
-                                Mode mode = Mode::automatic) {
+                                Mode mode = contract_mode<M>()) {
   using T = decltype(detail::element_type(a));
   if (ctx.rank() != 0) throw RankError("master_run must be called by rank 0");
   if (a.cols() != b.rows()) throw DimensionError("master_run: inner dimensions disagree");
@@ -305,12 +330,14 @@ std::pair<M, double> master_run(Context& ctx, const M& a, const M& b,
 // worker_run (protocol.hpp:112-147) on ranks >= 1.  The reference learns the
 // shapes from the messages; NCCL collectives need them up front, so the
 // worker passes (m, n, k) -- every rank derives its rows from split_rows.
+// `mode` must be the master's (fp64 default: Mode::exact; fp32: Mode::ffma).
 inline void worker_run(Context& ctx, std::int64_t m, std::int64_t n, std::int64_t k,
-                       Mode mode = Mode::automatic, bool f32 = false) {
+                       Mode mode = Mode::exact, bool f32 = false) {
   if (ctx.rank() == 0) throw RankError("worker_run must not be called by rank 0");
   if (f32)
     check(mmws_gpu_master_run_host_f32(ctx.handle(), m, n, k, nullptr, nullptr, nullptr,
-                                       static_cast<int>(mode), nullptr));
+                                       static_cast<int>(mode == Mode::exact ? Mode::ffma : mode),
+                                       nullptr));
   else
     check(mmws_gpu_master_run_host(ctx.handle(), m, n, k, nullptr, nullptr, nullptr,
                                    static_cast<int>(mode), nullptr));

@@ -13,7 +13,9 @@ PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG_DIR, "libmmws_gpu.so")
 HEADER = os.path.join(os.path.dirname(PKG_DIR), "include", "mmws_gpu.h")
 
-OK, ERR_DIMENSION, ERR_DOMAIN, ERR_CUDA, ERR_NCCL, ERR_RANK, ERR_PROTOCOL, ERR_STATE, ERR_ALLOC = range(9)
+(OK, ERR_DIMENSION, ERR_DOMAIN, ERR_CUDA, ERR_NCCL, ERR_RANK, ERR_PROTOCOL, ERR_STATE, ERR_ALLOC,
+ ERR_TIMEOUT) = range(10)
+GATHER_NONE, GATHER_FUSED, GATHER_NCCL = range(3)
 MODE_AUTO, MODE_EXACT, MODE_DMMA, MODE_DMMA_SMALL, MODE_FFMA, MODE_OZAKI = range(6)
 DIST_UNIT, DIST_UNIFORM, DIST_INT8, DIST_NORMAL = range(4)
 PROBE_DMMA, PROBE_DFMA, PROBE_DMUL_DADD, PROBE_FFMA, PROBE_FFMA2 = range(5)
@@ -52,6 +54,9 @@ SIGNATURES = {
     "mmws_gpu_peak_probe": (_i, [_v, _i, _i, _p(_d)]),
     "mmws_gpu_gemm_probe": (_i, [_v, _i64, _i, _i, _p(_d)]),
     "mmws_gpu_link_probe": (_i, [_v, _i64, _i, _p(_d)]),
+    "mmws_gpu_p2p_probe": (_i, [_v, _i64, _i, _p(_d)]),
+    "mmws_gpu_last_round": (_i, [_v, _p(_i), _p(_i)]),
+    "mmws_gpu_set_timeout": (_i, [_v, _d]),
     "mmws_gpu_nccl_unique_id": (_i, [_p(C.c_uint8)]),
     "mmws_gpu_comm_init": (_i, [_v, _i, _i, _p(C.c_uint8)]),
     "mmws_gpu_comm_destroy": (_i, [_v]),

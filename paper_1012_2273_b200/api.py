@@ -38,6 +38,10 @@ class ProtocolError(RuntimeError):
     """Row-block exchange failed (error.hpp:29-32)."""
 
 
+class TimeoutError(RuntimeError):  # noqa: A001 -- the reference's name (error.hpp:36-39)
+    """A distributed step made no progress within the deadline (error.hpp:36-39)."""
+
+
 class GpuError(RuntimeError):
     """CUDA / NCCL / allocation failure (no reference counterpart)."""
 
@@ -47,6 +51,7 @@ _ERRORS = {
     _abi.ERR_DOMAIN: DomainError,
     _abi.ERR_RANK: RankError,
     _abi.ERR_PROTOCOL: ProtocolError,
+    _abi.ERR_TIMEOUT: TimeoutError,
 }
 
 
@@ -158,6 +163,42 @@ def _ld(t) -> int:
     return t.stride(0)
 
 
+def _device_operands(A, B, C_, dtype, who: str):
+    """Shapes (m, n, k) of C_ = A . B on the device; every tensor must be a
+    2-D CUDA tensor of `dtype`, and C_ (if given) at least m x n."""
+    for name, t in (("A", A), ("B", B), ("C", C_)):
+        if t is None:
+            continue
+        if t.dtype != dtype:
+            raise DomainError(f"{who}: {name} must be {dtype}, got {t.dtype}")
+        if not t.is_cuda:
+            raise DomainError(f"{who}: {name} must be a CUDA tensor")
+        if t.dim() != 2:
+            raise DimensionError(f"{who}: {name} must be 2-D, got {t.dim()}-D")
+    m, k = A.shape
+    k2, n = B.shape
+    if k != k2:
+        raise DimensionError(f"matmul: inner dimensions differ, {k} vs {k2}")
+    if C_ is not None and (C_.shape[0] < m or C_.shape[1] < n):
+        raise DimensionError(f"{who}: C is {tuple(C_.shape)}, needs at least ({m}, {n})")
+    return m, n, k
+
+
+def _host_out(out, m: int, n: int, dt, who: str):
+    """The caller's output array for an (m, n) host result, checked; or a new one."""
+    if out is None:
+        return np.empty((m, n), dtype=dt)
+    if not isinstance(out, np.ndarray):
+        raise DomainError(f"{who}: out must be a numpy array")
+    if out.shape != (m, n):
+        raise DimensionError(f"{who}: out is {out.shape}, expected {(m, n)}")
+    if out.dtype != dt:
+        raise DomainError(f"{who}: out must be {np.dtype(dt)}, got {out.dtype}")
+    if not out.flags["C_CONTIGUOUS"] or not out.flags["WRITEABLE"]:
+        raise DimensionError(f"{who}: out must be C-contiguous and writeable")
+    return out
+
+
 class Graph:
     """A captured fp64 multiply (small-N path: one graph launch per call)."""
 
@@ -225,12 +266,7 @@ class Context:
     # -- device-pointer multiply (torch CUDA tensors)
     def dgemm(self, A, B, C_=None, mode: int = MODE_AUTO, stream=None):
         import torch
-        if A.dtype != torch.float64 or B.dtype != torch.float64:
-            raise DomainError("dgemm expects float64 tensors")
-        m, k = A.shape
-        k2, n = B.shape
-        if k != k2:
-            raise DimensionError(f"matmul: inner dimensions differ, {k} vs {k2}")
+        m, n, k = _device_operands(A, B, C_, torch.float64, "dgemm")
         if C_ is None:
             C_ = torch.empty((m, n), dtype=torch.float64, device=A.device)
         _check(_lib().mmws_gpu_dgemm(self._h, m, n, k, _ptr(A), _ld(A), _ptr(B), _ld(B),
@@ -239,12 +275,7 @@ class Context:
 
     def sgemm(self, A, B, C_=None, mode: int = MODE_AUTO, stream=None):
         import torch
-        if A.dtype != torch.float32 or B.dtype != torch.float32:
-            raise DomainError("sgemm expects float32 tensors")
-        m, k = A.shape
-        k2, n = B.shape
-        if k != k2:
-            raise DimensionError(f"matmul: inner dimensions differ, {k} vs {k2}")
+        m, n, k = _device_operands(A, B, C_, torch.float32, "sgemm")
         if C_ is None:
             C_ = torch.empty((m, n), dtype=torch.float32, device=A.device)
         _check(_lib().mmws_gpu_sgemm(self._h, m, n, k, _ptr(A), _ld(A), _ptr(B), _ld(B),
@@ -264,7 +295,7 @@ class Context:
         b = np.ascontiguousarray(b, dtype=dt)
         m, k = a.shape
         n = b.shape[1]
-        c = out if out is not None else np.empty((m, n), dtype=dt)
+        c = _host_out(out, m, n, dt, "matmul")
         el = C.c_double()
         fn = _lib().mmws_gpu_matmul_host_f32 if f32 else _lib().mmws_gpu_matmul_host
         _check(fn(self._h, m, n, k, a.ctypes.data, b.ctypes.data, c.ctypes.data, mode,
@@ -284,8 +315,10 @@ class Context:
 
     # -- graphs
     def graph_dgemm(self, A, B, C_, mode: int = MODE_AUTO) -> Graph:
-        m, k = A.shape
-        n = B.shape[1]
+        import torch
+        if C_ is None:
+            raise DomainError("graph_dgemm: C must be given (the graph writes into it on every replay)")
+        m, n, k = _device_operands(A, B, C_, torch.float64, "graph_dgemm")
         g = C.c_void_p()
         _check(_lib().mmws_gpu_graph_dgemm(self._h, m, n, k, _ptr(A), _ld(A), _ptr(B), _ld(B),
                                            _ptr(C_), _ld(C_), mode, C.byref(g)))
@@ -309,6 +342,25 @@ class Context:
         _check(_lib().mmws_gpu_link_probe(self._h, nbytes, iters, C.byref(out)))
         return out.value
 
+    def p2p_probe(self, nbytes: int = 1 << 28, iters: int = 5) -> float:
+        """Collective: rank 0 -> each worker point-to-point copy rate in bytes/s
+        (slowest peer on rank 0; 0 in a 1-rank world)."""
+        out = C.c_double()
+        _check(_lib().mmws_gpu_p2p_probe(self._h, nbytes, iters, C.byref(out)))
+        return out.value
+
+    def set_timeout(self, seconds: float) -> None:
+        """Deadline of one distributed step (default 30 s, MMWS_GPU_TIMEOUT_S)."""
+        _check(_lib().mmws_gpu_set_timeout(self._h, float(seconds)))
+
+    @property
+    def last_round(self):
+        """(ranks that multiplied, gather) of the latest row-block call;
+        gather in {"none", "fused-ipc", "nccl"}."""
+        act, g = C.c_int(), C.c_int()
+        _check(_lib().mmws_gpu_last_round(self._h, C.byref(act), C.byref(g)))
+        return act.value, {0: "none", 1: "fused-ipc", 2: "nccl"}[g.value]
+
     # -- row-block distribution
     def comm_init(self, nranks: int, rank: int, uid: bytes) -> None:
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
@@ -319,7 +371,19 @@ class Context:
 
     def rowblock(self, m: int, n: int, k: int, A=None, B=None, C_=None, mode: int = MODE_AUTO,
                  f32: bool = False) -> float:
-        """Collective master/worker multiply; rank 0 passes A, B, C device tensors."""
+        """Collective master/worker multiply; rank 0 passes dense A (m x k), B
+        (k x n), C (m x n) device tensors, the other ranks nothing."""
+        if A is not None or B is not None or C_ is not None:
+            import torch
+            if A is None or B is None or C_ is None:
+                raise DomainError("rowblock: rank 0 passes A, B and C")
+            dt = torch.float32 if f32 else torch.float64
+            _device_operands(A, B, C_, dt, "rowblock")
+            if tuple(A.shape) != (m, k) or tuple(B.shape) != (k, n) or tuple(C_.shape) != (m, n):
+                raise DimensionError(f"rowblock: shapes {tuple(A.shape)} x {tuple(B.shape)} -> "
+                                     f"{tuple(C_.shape)} do not match m={m} n={n} k={k}")
+            if not (A.is_contiguous() and B.is_contiguous() and C_.is_contiguous()):
+                raise DimensionError("rowblock: A, B and C must be dense (contiguous)")
         el = C.c_double(0.0)
         fn = _lib().mmws_gpu_rowblock_sgemm if f32 else _lib().mmws_gpu_rowblock_dgemm
         _check(fn(self._h, m, n, k, _ptr(A) if A is not None else None,
@@ -339,9 +403,10 @@ def _master_run_host(self, a=None, b=None, out=None, mode: int = MODE_AUTO, m=No
         m, k = a.shape
         n = b.shape[1]
         f32 = a.dtype == np.float32
-        if out is None:
-            out = np.empty((m, n), dtype=a.dtype)
-        for x in (a, b, out):
+        if a.dtype not in (np.float32, np.float64) or b.dtype != a.dtype:
+            raise DomainError("master_run: A and B must both be float64 or both float32")
+        out = _host_out(out, m, n, a.dtype, "master_run")
+        for x in (a, b):
             if not x.flags["C_CONTIGUOUS"]:
                 raise DimensionError("master_run: host matrices must be C-contiguous")
     el = C.c_double()
@@ -364,7 +429,7 @@ def _server_matmul(self, a: np.ndarray, b: np.ndarray, mode: int = MODE_AUTO,
         raise DimensionError(f"matmul: inner dimensions differ, {a.shape[1]} vs {b.shape[0]}")
     m, k = a.shape
     n = b.shape[1]
-    c = out if out is not None else np.empty((m, n), dtype=np.float64)
+    c = _host_out(out, m, n, np.float64, "server_matmul")
     el = C.c_double()
     _check(_lib().mmws_gpu_server_dgemm(self._h, m, n, k, a.ctypes.data, k, b.ctypes.data, n,
                                         c.ctypes.data, n, mode, C.byref(el)))

@@ -10,6 +10,23 @@
 
 #include "kernels.h"
 
+namespace mmws_impl {
+// MMWS_GPU_* tuning / test knobs, read once from the environment by
+// mmws_gpu_init (never on a per-call path).
+struct Tuning {
+  bool no_streamk = false;      // MMWS_GPU_NO_STREAMK: never use stream-K launches
+  std::string dmma_plan;        // MMWS_GPU_DMMA_PLAN: "<cfg>" or "<cfg>s<CTAs/SM>" override
+  int raster_group = 0;         // MMWS_GPU_RASTER_GROUP: DMMA tile raster group (0 = built-in)
+  bool pipeline_trace = false;  // MMWS_GPU_PIPELINE_TRACE: host-pipeline timeline on stderr
+  int rowblock_ranks = 0;       // MMWS_GPU_ROWBLOCK_RANKS: 0 cost model, -1 "all", 1 rank 0 alone
+  int server_ctas = 0;          // MMWS_GPU_SERVER_CTAS (0 = default)
+  int copy_threads = 0;         // MMWS_GPU_COPY_THREADS (0 = 3/4 of the host cores, <= 12)
+  double timeout_s = 30.0;      // MMWS_GPU_TIMEOUT_S: deadline of one distributed step
+  bool nccl_gather = false;     // MMWS_GPU_NCCL_GATHER: C-slices as NCCL messages, no fused IPC
+  static Tuning from_env();
+};
+}  // namespace mmws_impl
+
 struct mmws_gpu_ctx {
   int device = 0;
   int num_sms = 0;
@@ -46,10 +63,15 @@ struct mmws_gpu_ctx {
   int64_t sched_m = -1, sched_n = -1, sched_k = -1;  // shape the uploaded tile order belongs to
   uint64_t launches = 0;
   std::mutex mu;
+  mmws_impl::Tuning tune;
 
-  // packing workspace (device), grown on demand
+  // packing / MODE_OZAKI workspace (device), grown on demand.  While a CUDA
+  // graph is built, ws_cur points at that graph's own workspace instead, so a
+  // replay never shares (or outlives) the eager calls' buffer.
   void* ws = nullptr;
   size_t ws_bytes = 0;
+  void** ws_cur = nullptr;
+  size_t* ws_cur_bytes = nullptr;
   // stream-K workspaces, one per launch stream (fixed size, never moved):
   // (num_sms + 1) accumulator slots of 128 x 128 doubles + their flags
   struct SkSpace {
@@ -77,6 +99,14 @@ struct mmws_gpu_ctx {
   void* rbB = nullptr;
   void* rbC = nullptr;
   size_t rbA_bytes = 0, rbB_bytes = 0, rbC_bytes = 0;
+  // failure detection (rowblock.cu): every rank stores its progress through
+  // each round into rank 0's board, one word per rank (round * 8 + stage)
+  unsigned* board = nullptr;       // rank 0: the board (device memory, IPC-exported)
+  unsigned* board_peer = nullptr;  // where this rank's stores go / rank 0's board as seen here
+  uint32_t round = 0;              // rounds started on this communicator
+  bool comm_failed = false;        // a round timed out / a peer failed: communicator aborted
+  int last_gather = 0;             // last round: 0 one GPU, 1 fused IPC stores, 2 NCCL C-slices
+  int last_active = 1;             // last round: ranks that multiplied
 
   mmws_impl::Launch launch(cudaStream_t s) {
     mmws_impl::Launch L;
@@ -84,6 +114,7 @@ struct mmws_gpu_ctx {
     L.num_sms = num_sms;
     L.encode = encode;
     L.launches = &launches;
+    L.raster_group = tune.raster_group;
     return L;
   }
 };
@@ -97,6 +128,15 @@ int ok();
 // cudaFree (a device-wide synchronisation) would wait for it forever, so the
 // old buffer is parked in deferred_free instead (growth at least doubles).
 cudaError_t ensure(mmws_gpu_ctx* ctx, void** buf, size_t* have, size_t bytes);
+// The current multiply workspace (the context's, or the graph's being built),
+// at least `bytes` long.
+inline cudaError_t workspace(mmws_gpu_ctx* ctx, size_t bytes, void** out) {
+  void** buf = ctx->ws_cur ? ctx->ws_cur : &ctx->ws;
+  size_t* have = ctx->ws_cur ? ctx->ws_cur_bytes : &ctx->ws_bytes;
+  const cudaError_t e = ensure(ctx, buf, have, bytes);
+  *out = *buf;
+  return e;
+}
 // the fp64 multiply dispatch used by dgemm / host / graph / row-block paths
 int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
                    int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int mode,

@@ -382,14 +382,11 @@ __global__ void __launch_bounds__(K::THREADS, K::MINB)
   }
 }
 
-// Raster group of configuration K; MMWS_GPU_RASTER_GROUP overrides it (tuning).
+// Raster group of configuration K; MMWS_GPU_RASTER_GROUP (read at init into
+// Launch::raster_group) overrides it (tuning).
 template <class K>
-int raster_group() {
-  if (const char* g = std::getenv("MMWS_GPU_RASTER_GROUP")) {
-    const int v = std::atoi(g);
-    if (v > 0) return v;
-  }
-  return K::GROUP;
+int raster_group(const Launch& L) {
+  return L.raster_group > 0 ? L.raster_group : K::GROUP;
 }
 
 bool make_map(const Launch& L, CUtensorMap* map, const double* base, int64_t inner, int64_t outer,
@@ -420,7 +417,7 @@ cudaError_t run(const Launch& L, int64_t M, int64_t N, int64_t Kd, const double*
   const int vec_ok = (ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0);
   dgemm_dmma_kernel<K, 0><<<tiles_m * tiles_n, K::THREADS, smem, L.stream>>>(
       ta, tb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(Kd), tiles_m,
-      tiles_n, vec_ok, raster_group<K>(), DmmaStream{});
+      tiles_n, vec_ok, raster_group<K>(L), DmmaStream{});
   L.count();
   return cudaGetLastError();
 }
@@ -443,7 +440,7 @@ cudaError_t run_sk(const Launch& L, int64_t M, int64_t N, int64_t Kd, const doub
   st.flags = flags;
   dgemm_dmma_kernel<K, 2><<<grid, K::THREADS, K::SMEM, L.stream>>>(
       ta, tb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(Kd), tiles_m,
-      tiles_n, vec_ok, raster_group<K>(), st);
+      tiles_n, vec_ok, raster_group<K>(L), st);
   L.count();
   return cudaGetLastError();
 }
@@ -465,7 +462,7 @@ cudaError_t launch_dgemm_dmma_stream(const Launch& L, int64_t M, int64_t N, int6
   const int vec_ok = (ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0);
   dgemm_dmma_kernel<K, 1><<<grid, K::THREADS, K::SMEM, L.stream>>>(
       ta, tb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(Kd), tiles_m,
-      tiles_n, vec_ok, raster_group<K>(), st);
+      tiles_n, vec_ok, raster_group<K>(L), st);
   L.count();
   return cudaGetLastError();
 }

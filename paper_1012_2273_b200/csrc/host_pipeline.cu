@@ -129,7 +129,7 @@ int host_multiply_streamed(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, c
   cudaStreamWaitEvent(out, ev_reset, 0);
   // optional timeline (MMWS_GPU_PIPELINE_TRACE=1): H2D end, kernel start/end
   cudaEvent_t tr[3] = {nullptr, nullptr, nullptr};
-  const bool trace = std::getenv("MMWS_GPU_PIPELINE_TRACE") != nullptr;
+  const bool trace = ctx->tune.pipeline_trace;
   if (trace) {
     for (auto& ev : tr) cudaEventCreate(&ev);
     cudaEventRecord(tr[1], comp);
@@ -150,22 +150,32 @@ int host_multiply_streamed(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, c
   if ((e = launch_dgemm_dmma_stream(ctx->launch(comp), m, n, k, dA, k, dB, n, dC, n, st, grid)))
     return cuda_fail(e, "matmul_host: streamed dgemm");
   if (trace) cudaEventRecord(tr[2], comp);
+  // The persistent kernel spins on the arrival flags: if anything below
+  // fails, every flag is raised (on a stream the failed copy did not touch)
+  // and the kernel drained before returning, so no later call queues behind
+  // a kernel that never ends.  Its C is garbage; the call fails.
+  auto abandon = [&](int rc) {
+    cudaMemsetAsync(ready_a, 0x01, sizeof(int) * (nba + nbb), out);
+    cudaStreamSynchronize(out);
+    cudaStreamSynchronize(comp);
+    return rc;
+  };
   // ---- copy-in, each band followed by its arrival flag
   for (const auto& [which, i] : copies) {
     if (which == 'A') {
       const int64_t r0 = i * BAND_A * TILE, rows = std::min<int64_t>(BAND_A * TILE, m - r0);
       if ((e = copy_h2d(ctx, dA + r0 * k, sizeof(double) * k, A + r0 * k, sizeof(double) * k,
                         sizeof(double) * k, rows, in)))
-        return cuda_fail(e, "matmul_host: H2D A");
+        return abandon(cuda_fail(e, "matmul_host: H2D A"));
       if (ctx->write_value(in, dptr(ready_a + i), 1, 0) != CUDA_SUCCESS)
-        return fail(MMWS_GPU_ERR_CUDA, "matmul_host: cuStreamWriteValue32 failed");
+        return abandon(fail(MMWS_GPU_ERR_CUDA, "matmul_host: cuStreamWriteValue32 failed"));
     } else {
       const int64_t c0 = i * BAND_B * TILE, w = std::min<int64_t>(BAND_B * TILE, n - c0);
       if ((e = copy_h2d(ctx, dB + c0, sizeof(double) * n, B + c0, sizeof(double) * n,
                         sizeof(double) * w, k, in)))
-        return cuda_fail(e, "matmul_host: H2D B");
+        return abandon(cuda_fail(e, "matmul_host: H2D B"));
       if (ctx->write_value(in, dptr(ready_b + i), 1, 0) != CUDA_SUCCESS)
-        return fail(MMWS_GPU_ERR_CUDA, "matmul_host: cuStreamWriteValue32 failed");
+        return abandon(fail(MMWS_GPU_ERR_CUDA, "matmul_host: cuStreamWriteValue32 failed"));
     }
   }
   if (trace) cudaEventRecord(tr[0], in);
@@ -322,9 +332,12 @@ int host_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A
                         : std::max<int64_t>(128, ((m + 7) / 8 + 127) / 128 * 128);
   const int64_t panels = (m + R - 1) / R;
   // column blocks never narrower than 512 unless n itself is: a block then
-  // takes the same kernel as the whole problem (see dgemm_dispatch)
+  // takes the same kernel as the whole problem (see dgemm_dispatch).  A
+  // remainder narrower than W is folded into the last block (width in
+  // [W, 2W)), so no block can drop onto the latency kernel.
   const int64_t W = panels > 1 ? std::min<int64_t>(n, std::max<int64_t>(R, 512)) : n;
-  const int64_t blocks = (n + W - 1) / W;
+  const int64_t blocks = std::max<int64_t>(1, n / W);
+  auto width_of = [&](int64_t j) { return j + 1 < blocks ? W : n - j * W; };
   if ((e = event_pool(ctx, panels * 2 + blocks)) != cudaSuccess)
     return cuda_fail(e, "matmul_host: events");
   cudaEvent_t* evA = ctx->pool.data();
@@ -342,7 +355,7 @@ int host_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A
   cudaEventRecord(evA[0], in);
   cudaStreamWaitEvent(comp, evA[0], 0);
   for (int64_t j = 0; j < blocks; ++j) {
-    const int64_t w = std::min(W, n - j * W);
+    const int64_t w = width_of(j);
     if ((e = copy_h2d(ctx, dB + j * W, sizeof(T) * n, B + j * W, sizeof(T) * n, sizeof(T) * w, k,
                       in)))
       return cuda_fail(e, "matmul_host: H2D B");

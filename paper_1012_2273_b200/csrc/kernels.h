@@ -19,6 +19,7 @@ struct Launch {
   int num_sms = 148;
   EncodeTiledFn encode = nullptr;
   uint64_t* launches = nullptr;  // bumped once per kernel launched
+  int raster_group = 0;          // DMMA tile raster group override (0 = the plan's own)
   void count(int n = 1) const {
     if (launches) *launches += static_cast<uint64_t>(n);
   }
@@ -158,6 +159,9 @@ cudaError_t launch_sgemm_tma(const Launch& L, int64_t M, int64_t N, int64_t K, c
 cudaError_t launch_pack_f64(const Launch& L, const double* src, int64_t rows, int64_t cols,
                             int64_t ld_src, double* dst, int64_t rows_p, int64_t cols_p,
                             int64_t ld_dst);
+
+// Store `value` into one progress word (device or peer-mapped), in stream order.
+cudaError_t launch_board_mark(const Launch& L, unsigned* word, unsigned value);
 
 // Counter-based splitmix64 generators (bit-identical to oracle_fill for dist 0..2).
 cudaError_t launch_fill(const Launch& L, int dist, uint64_t seed, void* dst, int64_t rows,

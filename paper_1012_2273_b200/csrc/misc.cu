@@ -48,6 +48,15 @@ __global__ void fill_kernel(int dist, uint64_t seed, void* dst, int64_t rows, in
   }
 }
 
+// ---------------------------------------------------------------- progress board
+// One progress word of the row-block failure detector (rowblock.cu), stored
+// from this GPU into rank 0's board -- local memory on rank 0, a CUDA IPC
+// mapping over NVLink on the workers -- in stream order.
+__global__ void board_mark_kernel(volatile unsigned* word, unsigned value) {
+  *word = value;
+  __threadfence_system();
+}
+
 // ---------------------------------------------------------------- packing
 // One CTA row-strip per (row, 1024-column chunk): no 64-bit division per
 // element, coalesced reads and writes.
@@ -178,8 +187,14 @@ cudaError_t launch_peak_probe(const Launch& L, int which, int iters, double* sin
   return cudaGetLastError();
 }
 
+cudaError_t launch_board_mark(const Launch& L, unsigned* word, unsigned value) {
+  board_mark_kernel<<<1, 1, 0, L.stream>>>(word, value);
+  L.count();
+  return cudaGetLastError();
+}
+
 cudaError_t preload_misc() {
-  return preload_kernels(fill_kernel, pack_f64_kernel, probe_kernel<0>, probe_kernel<1>,
+  return preload_kernels(fill_kernel, pack_f64_kernel, board_mark_kernel, probe_kernel<0>, probe_kernel<1>,
                          probe_kernel<2>, probe_kernel<3>, probe_kernel<4>);
 }
 

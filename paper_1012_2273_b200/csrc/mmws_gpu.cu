@@ -33,6 +33,28 @@ int ok() {
   return MMWS_GPU_OK;
 }
 
+Tuning Tuning::from_env() {
+  Tuning t;
+  auto env = [](const char* name) -> const char* {
+    const char* v = std::getenv(name);
+    return v && *v ? v : nullptr;
+  };
+  t.no_streamk = env("MMWS_GPU_NO_STREAMK") != nullptr;
+  if (const char* v = env("MMWS_GPU_DMMA_PLAN")) t.dmma_plan = v;
+  if (const char* v = env("MMWS_GPU_RASTER_GROUP")) t.raster_group = std::max(0, std::atoi(v));
+  t.pipeline_trace = env("MMWS_GPU_PIPELINE_TRACE") != nullptr;
+  if (const char* v = env("MMWS_GPU_ROWBLOCK_RANKS"))
+    t.rowblock_ranks = std::strcmp(v, "all") == 0 ? -1 : std::strcmp(v, "1") == 0 ? 1 : 0;
+  if (const char* v = env("MMWS_GPU_SERVER_CTAS")) t.server_ctas = std::atoi(v);
+  if (const char* v = env("MMWS_GPU_COPY_THREADS")) t.copy_threads = std::clamp(std::atoi(v), 1, 64);
+  if (const char* v = env("MMWS_GPU_TIMEOUT_S")) {
+    const double s = std::atof(v);
+    if (s > 0) t.timeout_s = s;
+  }
+  t.nccl_gather = env("MMWS_GPU_NCCL_GATHER") != nullptr;
+  return t;
+}
+
 cudaError_t ensure(mmws_gpu_ctx* ctx, void** buf, size_t* have, size_t bytes) {
   if (*have >= bytes && *buf) return cudaSuccess;
   if (*buf && ctx->server) {
@@ -133,7 +155,7 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(L.stream, &cap);
   const bool sk_ok = cap == cudaStreamCaptureStatusNone && !ctx->server && ctx->allow_streamk &&
-                     !std::getenv("MMWS_GPU_NO_STREAMK");
+                     !ctx->tune.no_streamk;
   const bool sk = (mode == MMWS_GPU_MODE_DMMA || mode == MMWS_GPU_MODE_EXACT) && tiles128 >= G &&
                   tiles128 < 32 * G && sk_ok;
   // Exact order below one 128x128 tile per SM: stream-K over 64x64 tiles
@@ -155,9 +177,10 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
     if (a_ok && b_ok) return MMWS_GPU_OK;
     const int64_t lda_p = round_up(k, 8), ldb_p = round_up(n, 8);
     const size_t bytes = sizeof(double) * ((a_ok ? 0 : m * lda_p) + (b_ok ? 0 : k * ldb_p));
-    cudaError_t pe = ensure(ctx, &ctx->ws, &ctx->ws_bytes, bytes);
+    void* wsp = nullptr;
+    cudaError_t pe = workspace(ctx, bytes, &wsp);
     if (pe != cudaSuccess) return cuda_fail(pe, "dgemm pack workspace");
-    double* w = static_cast<double*>(ctx->ws);
+    double* w = static_cast<double*>(wsp);
     if (!a_ok) {
       if ((pe = launch_pack_f64(L, A, m, k, lda, w, m, lda_p, lda_p)) != cudaSuccess)
         return cuda_fail(pe, "dgemm pack A");
@@ -203,10 +226,11 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
     // plain loads, so any layout works without packing
     if (k > 131072)
       return fail(MMWS_GPU_ERR_DIMENSION, "dgemm ozaki: k must be <= 131072 (int32 accumulation)");
-    if ((e = ensure(ctx, &ctx->ws, &ctx->ws_bytes, ozaki_workspace_bytes(m, n, k))) != cudaSuccess)
+    void* wsp = nullptr;
+    if ((e = workspace(ctx, ozaki_workspace_bytes(m, n, k), &wsp)) != cudaSuccess)
       return cuda_fail(e, "dgemm ozaki workspace");
     if (int rc = ozaki_streams(ctx)) return rc;
-    e = launch_dgemm_ozaki(L, m, n, k, A, lda, B, ldb, C, ldc, ctx->ws, ctx->oz_stream, ctx->oz_ev);
+    e = launch_dgemm_ozaki(L, m, n, k, A, lda, B, ldb, C, ldc, wsp, ctx->oz_stream, ctx->oz_ev);
     ctx->last_plan = "ozaki (int8 tcgen05 GEMMs + CRT)";
     return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm ozaki");
   }
@@ -246,7 +270,8 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
   else if (mode == MMWS_GPU_MODE_AUTO && tiles128 < 64 * G)
     cfg = DMMA_64x64;
   int sk_grid = sk ? static_cast<int>(G) : 0;
-  if (const char* plan = std::getenv("MMWS_GPU_DMMA_PLAN")) {
+  if (!ctx->tune.dmma_plan.empty()) {
+    const char* plan = ctx->tune.dmma_plan.c_str();
     // tuning override (tools/dmma_plan_probe.py): "<cfg>" one-shot, or
     // "<cfg>s<CTAs per SM>" stream-K
     char* end = nullptr;
@@ -285,10 +310,11 @@ int sgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const flo
     if (k > 131072)
       return fail(MMWS_GPU_ERR_DIMENSION, "sgemm ozaki: k must be <= 131072 (int32 accumulation)");
     cudaError_t e;
-    if ((e = ensure(ctx, &ctx->ws, &ctx->ws_bytes, ozaki_workspace_bytes_f32(m, n, k))) != cudaSuccess)
+    void* wsp = nullptr;
+    if ((e = workspace(ctx, ozaki_workspace_bytes_f32(m, n, k), &wsp)) != cudaSuccess)
       return cuda_fail(e, "sgemm ozaki workspace");
     if (int rc = ozaki_streams(ctx)) return rc;
-    e = launch_sgemm_ozaki(L, m, n, k, A, lda, B, ldb, C, ldc, ctx->ws, ctx->oz_stream, ctx->oz_ev);
+    e = launch_sgemm_ozaki(L, m, n, k, A, lda, B, ldb, C, ldc, wsp, ctx->oz_stream, ctx->oz_ev);
     ctx->last_plan = "ozaki f32 (int8 tcgen05 GEMMs + CRT)";
     return e == cudaSuccess ? ok() : cuda_fail(e, "sgemm ozaki");
   }
@@ -348,6 +374,8 @@ struct mmws_gpu_graph {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   uint64_t kernels = 0;
+  void* ws = nullptr;  // this graph's own packing / MODE_OZAKI workspace
+  size_t ws_bytes = 0;
 };
 
 namespace {
@@ -396,6 +424,7 @@ int mmws_gpu_init(int device, mmws_gpu_ctx** out) {
   auto* ctx = new (std::nothrow) mmws_gpu_ctx();
   if (!ctx) return fail(MMWS_GPU_ERR_ALLOC, "mmws_gpu_init: out of host memory");
   ctx->device = device;
+  ctx->tune = Tuning::from_env();
   ctx->num_sms = prop.multiProcessorCount;
   ctx->cc_major = prop.major;
   ctx->cc_minor = prop.minor;
@@ -448,7 +477,7 @@ int mmws_gpu_destroy(mmws_gpu_ctx* ctx) {
   if (ctx->comm && nccl().ok) nccl().CommDestroy(ctx->comm);
   for (auto& mp : ctx->ipc_cache) cudaIpcCloseMemHandle(mp.base);
   for (void* p : {ctx->ws, ctx->dA, ctx->dB, ctx->dC, ctx->rbA, ctx->rbB, ctx->rbC, ctx->sched,
-                  ctx->ipc_stage,
+                  ctx->ipc_stage, static_cast<void*>(ctx->board),
                   static_cast<void*>(ctx->sink)})
     if (p) cudaFree(p);
   for (void* p : ctx->deferred_free) cudaFree(p);
@@ -584,14 +613,31 @@ int mmws_gpu_graph_dgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, con
   MMWS_CTX_GUARD(ctx);
   if (!out) return fail(MMWS_GPU_ERR_DOMAIN, "graph_dgemm: null out");
   *out = nullptr;
-  // One eager call first: sets kernel attributes and sizes the packing
-  // workspace, so nothing inside the capture allocates.
-  if (int rc = dgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode, ctx->stream)) return rc;
-  cudaError_t e;
-  if ((e = cudaStreamSynchronize(ctx->stream)) != cudaSuccess) return cuda_fail(e, "graph warmup");
   auto* g = new (std::nothrow) mmws_gpu_graph();
   if (!g) return fail(MMWS_GPU_ERR_ALLOC, "graph_dgemm: out of host memory");
   g->ctx = ctx;
+  // The graph gets its own workspace (a captured pointer into the
+  // context's workspace would dangle once an eager call regrows it, and a
+  // replay would race eager calls on other streams).
+  struct WsRedirect {
+    mmws_gpu_ctx* c;
+    ~WsRedirect() { c->ws_cur = nullptr, c->ws_cur_bytes = nullptr; }
+  } redirect{ctx};
+  ctx->ws_cur = &g->ws;
+  ctx->ws_cur_bytes = &g->ws_bytes;
+  // One eager call first: sets kernel attributes and sizes the graph's
+  // workspace, so nothing inside the capture allocates.
+  cudaError_t e;
+  if (int rc = dgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode, ctx->stream)) {
+    if (g->ws) cudaFree(g->ws);
+    delete g;
+    return rc;
+  }
+  if ((e = cudaStreamSynchronize(ctx->stream)) != cudaSuccess) {
+    if (g->ws) cudaFree(g->ws);
+    delete g;
+    return cuda_fail(e, "graph warmup");
+  }
   const uint64_t before = ctx->launches;
   if ((e = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) {
     delete g;
@@ -601,19 +647,11 @@ int mmws_gpu_graph_dgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, con
   e = cudaStreamEndCapture(ctx->stream, &g->graph);
   g->kernels = ctx->launches - before;
   ctx->launches = before;  // counted on replay
-  if (rc) {
+  if (rc || e != cudaSuccess || (e = cudaGraphInstantiate(&g->exec, g->graph, 0)) != cudaSuccess) {
     if (g->graph) cudaGraphDestroy(g->graph);
+    if (g->ws) cudaFree(g->ws);
     delete g;
-    return rc;
-  }
-  if (e != cudaSuccess) {
-    delete g;
-    return cuda_fail(e, "graph capture end");
-  }
-  if ((e = cudaGraphInstantiate(&g->exec, g->graph, 0)) != cudaSuccess) {
-    cudaGraphDestroy(g->graph);
-    delete g;
-    return cuda_fail(e, "graph instantiate");
+    return rc ? rc : cuda_fail(e, "graph capture / instantiate");
   }
   *out = g;
   return ok();
@@ -632,8 +670,16 @@ int mmws_gpu_graph_launch(mmws_gpu_graph* g, void* stream) {
 
 int mmws_gpu_graph_destroy(mmws_gpu_graph* g) {
   if (!g) return ok();
+  mmws_gpu_ctx* ctx = g->ctx;
+  MMWS_CTX_GUARD(ctx);
   if (g->exec) cudaGraphExecDestroy(g->exec);
   if (g->graph) cudaGraphDestroy(g->graph);
+  if (g->ws) {
+    // a replay may still be running: free after the context's work, or at
+    // server stop while the latency server holds the device
+    if (ctx->server) ctx->deferred_free.push_back(g->ws);
+    else cudaDeviceSynchronize(), cudaFree(g->ws);
+  }
   delete g;
   return ok();
 }

@@ -17,6 +17,9 @@ namespace mmws_impl {
 struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommInitRankConfig)(ncclComm_t*, int, ncclUniqueId, int, ncclConfig_t*) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
@@ -40,6 +43,9 @@ inline const NcclApi& nccl() {
 #define MMWS_NCCL_SYM(field, name) api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name))
     MMWS_NCCL_SYM(GetUniqueId, "ncclGetUniqueId");
     MMWS_NCCL_SYM(CommInitRank, "ncclCommInitRank");
+    MMWS_NCCL_SYM(CommInitRankConfig, "ncclCommInitRankConfig");
+    MMWS_NCCL_SYM(CommGetAsyncError, "ncclCommGetAsyncError");
+    MMWS_NCCL_SYM(CommAbort, "ncclCommAbort");
     MMWS_NCCL_SYM(CommDestroy, "ncclCommDestroy");
     MMWS_NCCL_SYM(Send, "ncclSend");
     MMWS_NCCL_SYM(Recv, "ncclRecv");
@@ -49,7 +55,8 @@ inline const NcclApi& nccl() {
     MMWS_NCCL_SYM(GroupEnd, "ncclGroupEnd");
     MMWS_NCCL_SYM(GetErrorString, "ncclGetErrorString");
 #undef MMWS_NCCL_SYM
-    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv &&
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommInitRankConfig &&
+             api.CommGetAsyncError && api.CommAbort && api.CommDestroy && api.Send && api.Recv &&
              api.Broadcast && api.AllReduce && api.GroupStart && api.GroupEnd && api.GetErrorString;
   });
   return api;

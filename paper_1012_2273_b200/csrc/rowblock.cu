@@ -16,12 +16,27 @@
 // height, so P-GPU results are bitwise the 1-GPU results -- and the C-slices
 // come back as one grouped receive batch into C's row blocks on rank 0.  Rank
 // 0 is master AND worker 0 (its GPU would otherwise idle).
+//
+// Failure detection (the reference's receive deadline, comm.hpp:144 /
+// net.hpp:116-132, and its dead-worker ProtocolError naming the rank,
+// protocol.hpp:74-77,88-101): communicators are created non-blocking
+// (ncclConfig_t.blocking = 0), so no NCCL call parks the host thread; the
+// host waits for a round with a deadline (MMWS_GPU_TIMEOUT_S, default 30 s)
+// while polling ncclCommGetAsyncError.  Every rank stores its progress
+// through a round (joined / inputs landed / multiplied / done) into a board
+// on rank 0 -- one word per rank, mapped into the workers by CUDA IPC -- so
+// when a round fails rank 0 can name the ranks that fell behind.  A failed
+// round aborts the communicator (ncclCommAbort); mmws_gpu_comm_destroy +
+// mmws_gpu_comm_init rebuild it.
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/mmws_gpu.h"
@@ -32,23 +47,146 @@ using namespace mmws_impl;
 
 namespace {
 
-int nccl_fail(ncclResult_t r, const char* what) {
-  return fail(MMWS_GPU_ERR_NCCL, std::string(what) + ": " + nccl().GetErrorString(r));
-}
-
 #define NCCL_REQUIRE()                                                          \
   if (!nccl().ok) return fail(MMWS_GPU_ERR_NCCL, "libnccl.so.2 could not be loaded");
-
-#define NCCL_TRY(call, what)                                   \
-  do {                                                         \
-    ncclResult_t r_ = (call);                                  \
-    if (r_ != ncclSuccess) return nccl_fail(r_, what);         \
-  } while (0)
 
 template <class T>
 T* as_mut(const T* p) {
   return const_cast<T*>(p);
 }
+
+// ---------------------------------------------------------------- failure detection
+using Clock = std::chrono::steady_clock;
+
+struct Deadline {
+  Clock::time_point end;
+  explicit Deadline(double seconds)
+      : end(Clock::now() + std::chrono::duration_cast<Clock::duration>(
+                               std::chrono::duration<double>(seconds))) {}
+  bool passed() const { return Clock::now() >= end; }
+};
+
+// Spin briefly (a round usually completes within microseconds of the event),
+// then back off to 50 us sleeps.
+inline void backoff(int& spins) {
+  if (++spins < 4096) std::this_thread::yield();
+  else std::this_thread::sleep_for(std::chrono::microseconds(50));
+}
+
+enum Stage : unsigned { JOINED = 1, INPUTS = 2, MULTIPLIED = 3, DONE = 4 };
+
+const char* stage_name(unsigned s) {
+  switch (s) {
+    case JOINED: return "joined";
+    case INPUTS: return "received its A rows and B";
+    case MULTIPLIED: return "multiplied";
+    case DONE: return "done";
+    default: return "no round yet";
+  }
+}
+
+// This rank's progress word in rank 0's board, in stream order on s.
+void mark(mmws_gpu_ctx* ctx, cudaStream_t s, unsigned stage) {
+  if (ctx->board_peer)
+    launch_board_mark(ctx->launch(s), ctx->board_peer + ctx->rank, ctx->round * 8u + stage);
+}
+
+// Rank 0: the workers that had not finished round ctx->round, from the board
+// (read on the idle copy stream), lowest progress first.
+std::string laggards(mmws_gpu_ctx* ctx) {
+  if (ctx->rank != 0 || !ctx->board || ctx->nranks < 2) return "";
+  std::vector<unsigned> b(ctx->nranks, 0);
+  if (cudaMemcpyAsync(b.data(), ctx->board, sizeof(unsigned) * ctx->nranks,
+                      cudaMemcpyDeviceToHost, ctx->copy_in) != cudaSuccess ||
+      cudaStreamSynchronize(ctx->copy_in) != cudaSuccess)
+    return "";
+  const unsigned want = ctx->round * 8u + DONE;
+  unsigned low = want;
+  for (int r = 1; r < ctx->nranks; ++r) low = std::min(low, b[r]);
+  if (low >= want) return "";
+  std::string out;
+  for (int r = 1; r < ctx->nranks; ++r) {
+    if (b[r] != low) continue;
+    out += out.empty() ? "worker rank " : ", worker rank ";
+    out += std::to_string(r);
+  }
+  const unsigned rd = low / 8u, st = low % 8u;
+  out += low / 8u == ctx->round
+             ? std::string(" stopped in round ") + std::to_string(rd) + " after it " + stage_name(st)
+             : std::string(" never joined round ") + std::to_string(ctx->round) +
+                   (low == 0 ? std::string(" (no round seen)")
+                             : " (last seen: round " + std::to_string(rd) + ", " +
+                                   stage_name(st) + ")");
+  return out;
+}
+
+// A round (or the bootstrap) failed: name who fell behind, abort the
+// communicator (its kernels exit, so every queued stream drains), report.
+int round_failed(mmws_gpu_ctx* ctx, const char* what, ncclResult_t async, bool timed_out) {
+  std::string who = laggards(ctx);
+  if (ctx->comm) {
+    nccl().CommAbort(ctx->comm);
+    ctx->comm = nullptr;
+  }
+  ctx->comm_failed = true;
+  cudaStreamSynchronize(ctx->comm_stream);
+  cudaStreamSynchronize(ctx->stream);
+  cudaGetLastError();
+  std::string msg = std::string(what) + " (round " + std::to_string(ctx->round) + ", rank " +
+                    std::to_string(ctx->rank) + " of " + std::to_string(ctx->nranks) + "): ";
+  if (!timed_out)
+    msg += std::string("NCCL reported ") + nccl().GetErrorString(async);
+  else
+    msg += "no progress within " + std::to_string(ctx->tune.timeout_s) + " s (deadlock-suspected)";
+  if (!who.empty()) msg += "; " + who;
+  else if (ctx->rank != 0) msg += "; waiting on the master (rank 0) or a peer";
+  msg += "; communicator aborted (mmws_gpu_comm_destroy + mmws_gpu_comm_init to rebuild)";
+  // a named rank that failed is the reference's ProtocolError
+  // (protocol.hpp:74-77,88-101); an anonymous stall its TimeoutError (comm.hpp:144)
+  return fail(!who.empty() || !timed_out ? MMWS_GPU_ERR_PROTOCOL : MMWS_GPU_ERR_TIMEOUT, msg);
+}
+
+// Wait for `ev` with the deadline while watching the communicator.
+int await(mmws_gpu_ctx* ctx, cudaEvent_t ev, const char* what) {
+  const Deadline dl(ctx->tune.timeout_s);
+  for (int spins = 0;; backoff(spins)) {
+    const cudaError_t q = cudaEventQuery(ev);
+    if (q == cudaSuccess) return MMWS_GPU_OK;
+    if (q != cudaErrorNotReady) return cuda_fail(q, what);
+    ncclResult_t a = ncclSuccess;
+    if (ctx->comm && nccl().CommGetAsyncError(ctx->comm, &a) == ncclSuccess && a != ncclSuccess &&
+        a != ncclInProgress)
+      return round_failed(ctx, what, a, false);
+    if (dl.passed()) return round_failed(ctx, what, ncclSuccess, true);
+  }
+}
+
+// Result of an NCCL call on a non-blocking communicator: ncclInProgress
+// means the call is still being set up (connections, ...) -- the next NCCL
+// call may only follow once the communicator reports ncclSuccess.
+int settle(mmws_gpu_ctx* ctx, ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return MMWS_GPU_OK;
+  if (r != ncclInProgress) {
+    ncclResult_t a = ncclSuccess;
+    if (ctx->comm && nccl().CommGetAsyncError(ctx->comm, &a) == ncclSuccess && a != ncclSuccess &&
+        a != ncclInProgress)
+      return round_failed(ctx, what, a, false);
+    return fail(MMWS_GPU_ERR_NCCL, std::string(what) + ": " + nccl().GetErrorString(r));
+  }
+  const Deadline dl(ctx->tune.timeout_s);
+  for (int spins = 0;; backoff(spins)) {
+    ncclResult_t a = ncclInProgress;
+    nccl().CommGetAsyncError(ctx->comm, &a);
+    if (a == ncclSuccess) return MMWS_GPU_OK;
+    if (a != ncclInProgress) return round_failed(ctx, what, a, false);
+    if (dl.passed()) return round_failed(ctx, what, ncclSuccess, true);
+  }
+}
+
+#define NCCL_TRY(call, what)                                  \
+  do {                                                        \
+    if (int rc_ = settle(ctx, (call), what)) return rc_;       \
+  } while (0)
 
 // Who holds which rows, and the sub-block cut of every rank's rows -- derived
 // by every rank from split_rows (protocol.hpp:33-46), so no metadata messages
@@ -76,17 +214,20 @@ Schedule make_schedule(int64_t m, int P) {
 }
 
 // Planning rates of mmws_gpu_rowblock_ranks (fixed, so every rank reaches
-// the same decision without exchanging anything).
-constexpr double PLAN_LINK_BPS = 600e9;
-constexpr double PLAN_FP64_FLOPS = 33e12, PLAN_FP32_FLOPS = 55e12;
+// the same decision without exchanging anything): the measured B200 peer
+// copy bandwidth per direction (B200_PROFILING.md: 770 GB/s) and the
+// measured 1-GPU multiply rates of this library (DMMA 36.3
+// TFLOP/s at N=16384, FFMA2 62 TFLOP/s at N=32768), 60 us of collective
+// latency per round.
+constexpr double PLAN_LINK_BPS = 770e9;
+constexpr double PLAN_FP64_FLOPS = 36.3e12, PLAN_FP32_FLOPS = 62e12;
 constexpr double PLAN_ROUND_LATENCY_S = 60e-6;
 
-int rowblock_active(int64_t m, int64_t n, int64_t k, int P, int elem_bytes) {
+// force: 0 cost model, -1 every rank, 1 rank 0 alone (MMWS_GPU_ROWBLOCK_RANKS)
+int rowblock_active(int64_t m, int64_t n, int64_t k, int P, int elem_bytes, int force) {
   if (P <= 1) return 1;
-  if (const char* f = std::getenv("MMWS_GPU_ROWBLOCK_RANKS")) {
-    if (std::strcmp(f, "all") == 0) return P;
-    if (std::strcmp(f, "1") == 0) return 1;
-  }
+  if (force == -1) return P;
+  if (force == 1) return 1;
   double t1 = 0, tp = 0;
   const double rate = elem_bytes == 8 ? PLAN_FP64_FLOPS : PLAN_FP32_FLOPS;
   mmws_gpu_rowblock_cost(m, n, k, 1, elem_bytes, PLAN_LINK_BPS, rate, &t1, nullptr, nullptr);
@@ -97,7 +238,8 @@ int rowblock_active(int64_t m, int64_t n, int64_t k, int P, int elem_bytes) {
 
 // Enqueue one master/worker round.  Rank 0 passes device A, B, C (dense); the
 // other ranks pass nulls and use library buffers.  On return ctx->ev1 (rank 0)
-// is recorded after the last C row has landed.
+// is recorded after the last C row has landed and *done (if given) after this
+// rank's part of the round.
 //
 // Without a communicator: one multiply.  With one (one rank per GPU, NCCL on
 // ctx->comm_stream, multiplies on ctx->stream -- a 1-rank world takes this
@@ -119,15 +261,23 @@ int rowblock_active(int64_t m, int64_t n, int64_t k, int P, int elem_bytes) {
 // 1-GPU launch, so the assembled C is bitwise the 1-GPU result.
 template <class T>
 int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, const T* B,
-                     T* C, int mode, bool bracket = true) {
+                     T* C, int mode, bool bracket, cudaEvent_t* done) {
   if (m <= 0 || n <= 0 || k <= 0)
     return fail(MMWS_GPU_ERR_DIMENSION, "rowblock: dimensions must be positive");
+  if (ctx->comm_failed)
+    return fail(MMWS_GPU_ERR_STATE, "rowblock: the communicator was aborted after a failed "
+                                    "round; mmws_gpu_comm_destroy + mmws_gpu_comm_init first");
   const int P = ctx->comm ? ctx->nranks : 1;
   const int me = ctx->comm ? ctx->rank : 0;
   if (me == 0 && (!A || !B || !C))
     return fail(MMWS_GPU_ERR_DOMAIN, "rowblock: rank 0 needs A, B and C");
   cudaStream_t comp = ctx->stream, comm = ctx->comm_stream;
   cudaError_t e;
+  if ((e = event_pool(ctx, 1)) != cudaSuccess) return cuda_fail(e, "rowblock: events");
+  cudaEvent_t evDone = ctx->pool[0];
+  if (done) *done = evDone;
+  ctx->last_gather = 0;
+  ctx->last_active = 1;
 
   if (!ctx->comm) {  // no communicator: one multiply
     if (bracket) cudaEventRecord(ctx->ev0, comp);
@@ -135,10 +285,11 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
     if (int rc = gemm<T>(ctx, m, n, k, A, k, B, n, C, n, mode, comp)) return rc;
     cudaEventRecord(ctx->evk1, comp);
     if (bracket) cudaEventRecord(ctx->ev1, comp);
+    cudaEventRecord(evDone, comp);
     return MMWS_GPU_OK;
   }
   NCCL_REQUIRE();
-  if (P > 1 && rowblock_active(m, n, k, P, sizeof(T)) == 1) {
+  if (P > 1 && rowblock_active(m, n, k, P, sizeof(T), ctx->tune.rowblock_ranks) == 1) {
     // too small to amortise the exchange: rank 0 multiplies alone, the
     // workers have nothing to do (every rank takes this branch for the same
     // arguments, so no collective is left half-matched).  A 1-rank world
@@ -146,12 +297,14 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
     cudaEventRecord(ctx->evk0, comp);
     if (me != 0) {
       cudaEventRecord(ctx->evk1, comp);
+      cudaEventRecord(evDone, comp);
       return MMWS_GPU_OK;
     }
     if (bracket) cudaEventRecord(ctx->ev0, comp);
     if (int rc = gemm<T>(ctx, m, n, k, A, k, B, n, C, n, mode, comp)) return rc;
     cudaEventRecord(ctx->evk1, comp);
     if (bracket) cudaEventRecord(ctx->ev1, comp);
+    cudaEventRecord(evDone, comp);
     return MMWS_GPU_OK;
   }
   // the multiplies below overlap NCCL transfers: no persistent (stream-K)
@@ -168,32 +321,38 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
   const auto& soff = sc.soff;
   const auto& srows = sc.srows;
   const ncclDataType_t dt = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
+  ++ctx->round;
+  ctx->last_active = P;
 
-  if ((e = event_pool(ctx, 2 * S + 3)) != cudaSuccess) return cuda_fail(e, "rowblock: events");
-  cudaEvent_t* evA = ctx->pool.data();
+  if ((e = event_pool(ctx, 2 * S + 5)) != cudaSuccess) return cuda_fail(e, "rowblock: events");
+  cudaEvent_t* evA = ctx->pool.data() + 1;
   cudaEvent_t* evC = evA + S;
-  cudaEvent_t evB = evC[S], evStart = evC[S + 1], evJoin = evC[S + 2];
+  cudaEvent_t evB = evC[S], evStart = evC[S + 1], evJoin = evC[S + 2], evHost = evC[S + 3];
 
   // the exchange starts after everything already queued on the compute stream
   // (e.g. the H2D copies of master_run_host)
   if (me == 0 && bracket) cudaEventRecord(ctx->ev0, comp);  // first send
   cudaEventRecord(evStart, comp);
   cudaStreamWaitEvent(comm, evStart, 0);
+  mark(ctx, comm, JOINED);
 
   // ---- fused gather set-up (see above)
   unsigned char* stage = static_cast<unsigned char*>(ctx->ipc_stage);
   unsigned char hbuf[80] = {0};
   if (me == 0) {
-    hbuf[72] = ipc_export(ctx, C, hbuf) == MMWS_GPU_OK ? 1 : 0;
+    hbuf[72] = !ctx->tune.nccl_gather && ipc_export(ctx, C, hbuf) == MMWS_GPU_OK ? 1 : 0;
     if ((e = cudaMemcpyAsync(stage, hbuf, 80, cudaMemcpyHostToDevice, comm)))
       return cuda_fail(e, "rowblock: stage IPC handle");
   }
   NCCL_TRY(nccl().Broadcast(stage, stage, 80, ncclUint8, 0, ctx->comm, comm), "broadcast C handle");
-  if (me != 0 && ((e = cudaMemcpyAsync(hbuf, stage, 80, cudaMemcpyDeviceToHost, comm)) ||
-                  (e = cudaStreamSynchronize(comm))))
-    return cuda_fail(e, "rowblock: fetch IPC handle");
+  if (me != 0) {
+    if ((e = cudaMemcpyAsync(hbuf, stage, 80, cudaMemcpyDeviceToHost, comm)))
+      return cuda_fail(e, "rowblock: fetch IPC handle");
+    cudaEventRecord(evHost, comm);
+    if (int rc = await(ctx, evHost, "rowblock: receive the master's C handle")) return rc;
+  }
   T* c_peer = nullptr;
-  int ok_here = hbuf[72];
+  int ok_here = hbuf[72] && !ctx->tune.nccl_gather;
   if (me != 0 && ok_here) {
     void* p = nullptr;
     ok_here = ipc_open(ctx, hbuf, &p) == MMWS_GPU_OK ? 1 : 0;
@@ -206,13 +365,15 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
       return cuda_fail(e, "rowblock: vote");
     NCCL_TRY(nccl().AllReduce(vote, vote, 1, ncclInt32, ncclMin, ctx->comm, comm),
              "agree on fused gather");
-    if ((e = cudaMemcpyAsync(&fused, vote, sizeof(int), cudaMemcpyDeviceToHost, comm)) ||
-        (e = cudaStreamSynchronize(comm)))
+    if ((e = cudaMemcpyAsync(&fused, vote, sizeof(int), cudaMemcpyDeviceToHost, comm)))
       return cuda_fail(e, "rowblock: vote result");
+    cudaEventRecord(evHost, comm);
+    if (int rc = await(ctx, evHost, "rowblock: agree on the C gather")) return rc;
     std::memcpy(ctx->last_handle, hbuf, 80);
     ctx->last_fused = fused;
   }
   ok();  // a failed export/open only selects the NCCL gather
+  ctx->last_gather = fused ? 1 : 2;
 
   const T* a_loc = A;
   const T* b_loc = B;
@@ -248,6 +409,7 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
     NCCL_TRY(nccl().GroupEnd(), "ncclGroupEnd");
     cudaEventRecord(evA[s], comm);
   }
+  mark(ctx, comm, INPUTS);
 
   // ---- compute stream: this rank's rows (worker_run's body, protocol.hpp:132-141)
   cudaEventRecord(ctx->evk0, comp);
@@ -259,9 +421,12 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
       if (int rc = gemm<T>(ctx, rs, n, k, a_loc + r0 * k, k, b_loc, n, c_dst + r0 * n, n, mode,
                            comp))
         return rc;
+    if (s == S - 1) {
+      cudaEventRecord(ctx->evk1, comp);
+      mark(ctx, comp, MULTIPLIED);  // before evC: the DONE mark below waits on it
+    }
     cudaEventRecord(evC[s], comp);
   }
-  cudaEventRecord(ctx->evk1, comp);
 
   // ---- comm stream, part 2 (fused): the C rows are already in rank 0's C; one
   // 4-byte allreduce after every rank's last multiply is the completion
@@ -288,15 +453,23 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
     }
     NCCL_TRY(nccl().GroupEnd(), "ncclGroupEnd");
   }
+  if (!fused) cudaStreamWaitEvent(comm, evC[S - 1], 0);
+  mark(ctx, comm, DONE);
   // join: the compute stream waits for the exchange, so the caller only
   // needs to synchronise ctx->stream
   cudaEventRecord(evJoin, comm);
   cudaStreamWaitEvent(comp, evJoin, 0);
   if (me == 0 && bracket) cudaEventRecord(ctx->ev1, comp);  // last receive
+  cudaEventRecord(evDone, comp);
   return MMWS_GPU_OK;
 }
 
-int finish(mmws_gpu_ctx* ctx, bool timed, double* elapsed_s) {
+// Wait for this rank's part of the round (with the deadline when peers are
+// involved), then read the kernel and bracket timers.
+int finish(mmws_gpu_ctx* ctx, cudaEvent_t done, bool timed, double* elapsed_s) {
+  if (ctx->comm) {
+    if (int rc = await(ctx, done, "rowblock round")) return rc;
+  }
   cudaError_t e = cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) return cuda_fail(e, "rowblock: sync");
   float ms = 0.f;
@@ -312,8 +485,9 @@ template <class T>
 int rowblock(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, const T* B, T* C,
              int mode, double* elapsed_s) {
   const bool root = !ctx->comm || ctx->rank == 0;
-  if (int rc = rowblock_enqueue(ctx, m, n, k, A, B, C, mode)) return rc;
-  return finish(ctx, root, elapsed_s);
+  cudaEvent_t done = nullptr;
+  if (int rc = rowblock_enqueue(ctx, m, n, k, A, B, C, mode, true, &done)) return rc;
+  return finish(ctx, done, root, elapsed_s);
 }
 
 // master_run with host matrices on rank 0: H2D of A and B, the round, D2H of
@@ -325,12 +499,19 @@ int master_run_host(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T*
   if (!root) return rowblock(ctx, m, n, k, static_cast<const T*>(nullptr),
                              static_cast<const T*>(nullptr), static_cast<T*>(nullptr), mode,
                              elapsed_s);
+  if (ctx->comm_failed)
+    return fail(MMWS_GPU_ERR_STATE, "master_run: the communicator was aborted after a failed "
+                                    "round; mmws_gpu_comm_destroy + mmws_gpu_comm_init first");
   // one GPU, or a round too small to distribute (rank 0 alone; the workers
   // return at once from the rowblock call above): copies overlapped with
   // the multiply
   if (!ctx->comm || (ctx->nranks > 1 && m > 0 && n > 0 && k > 0 &&
-                     rowblock_active(m, n, k, ctx->nranks, sizeof(T)) == 1))
+                     rowblock_active(m, n, k, ctx->nranks, sizeof(T),
+                                     ctx->tune.rowblock_ranks) == 1)) {
+    ctx->last_gather = 0;
+    ctx->last_active = 1;
     return host_multiply(ctx, m, n, k, A, B, C, mode, elapsed_s);
+  }
   if (m <= 0 || n <= 0 || k <= 0)
     return fail(MMWS_GPU_ERR_DIMENSION, "master_run: dimensions must be positive");
   if (!A || !B || !C) return fail(MMWS_GPU_ERR_DOMAIN, "master_run: null host matrix");
@@ -347,17 +528,94 @@ int master_run_host(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T*
       (e = copy_h2d(ctx, ctx->dB, sizeof(T) * n, B, sizeof(T) * n, sizeof(T) * n, k, s)) !=
           cudaSuccess)
     return cuda_fail(e, "master_run: H2D");
+  cudaEvent_t done = nullptr;
   if (int rc = rowblock_enqueue(ctx, m, n, k, static_cast<const T*>(ctx->dA),
                                 static_cast<const T*>(ctx->dB), static_cast<T*>(ctx->dC), mode,
-                                false))
+                                false, &done))
     return rc;
+  // the round must complete (within the deadline) before the copy-out: a
+  // pageable C is pumped by this thread, which would otherwise block on it
+  if (int rc = await(ctx, done, "master_run round")) return rc;
   D2hPump pump(ctx, s);
   if ((e = pump.add(C, sizeof(T) * n, ctx->dC, sizeof(T) * n, sizeof(T) * n, m)) != cudaSuccess ||
       (e = pump.finish()) != cudaSuccess)
     return cuda_fail(e, "master_run: D2H");
   cudaEventRecord(ctx->ev1, s);
-  return finish(ctx, true, elapsed_s);
+  cudaEventRecord(done, s);
+  return finish(ctx, done, true, elapsed_s);
 }
+
+// Non-blocking communicator (see the header): returns once every rank has
+// joined, or fails with MMWS_GPU_ERR_TIMEOUT after the deadline.
+int comm_create(mmws_gpu_ctx* ctx, int nranks, int rank, const ncclUniqueId& uid) {
+  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+  cfg.blocking = 0;
+  ncclComm_t comm = nullptr;
+  ncclResult_t r = nccl().CommInitRankConfig(&comm, nranks, uid, rank, &cfg);
+  if (r != ncclSuccess && r != ncclInProgress) {
+    if (comm) nccl().CommAbort(comm);
+    return fail(MMWS_GPU_ERR_NCCL, std::string("ncclCommInitRankConfig: ") + nccl().GetErrorString(r));
+  }
+  const Deadline dl(ctx->tune.timeout_s);
+  for (int spins = 0;; backoff(spins)) {
+    ncclResult_t a = ncclInProgress;
+    nccl().CommGetAsyncError(comm, &a);
+    if (a == ncclSuccess) break;
+    if (a != ncclInProgress || dl.passed()) {
+      nccl().CommAbort(comm);
+      if (a != ncclInProgress)
+        return fail(MMWS_GPU_ERR_NCCL, std::string("comm_init: ") + nccl().GetErrorString(a));
+      return fail(MMWS_GPU_ERR_TIMEOUT,
+                  "comm_init: rank " + std::to_string(rank) + " waited " +
+                      std::to_string(ctx->tune.timeout_s) + " s for the other " +
+                      std::to_string(nranks - 1) + " rank(s) of the world to join "
+                      "(deadlock-suspected)");
+    }
+  }
+  ctx->comm = comm;
+  ctx->nranks = nranks;
+  ctx->rank = rank;
+  ctx->round = 0;
+  ctx->comm_failed = false;
+  ctx->last_fused = -1;
+  return MMWS_GPU_OK;
+}
+
+// The progress board: rank 0 allocates it and broadcasts its IPC handle;
+// every rank maps it.  Without IPC the deadline still holds, the error just
+// cannot name the rank that fell behind.
+int board_setup(mmws_gpu_ctx* ctx) {
+  cudaError_t e;
+  unsigned char h[80] = {0};
+  if (ctx->rank == 0) {
+    if ((e = cudaMalloc(&ctx->board, 256 + sizeof(unsigned) * ctx->nranks)) != cudaSuccess ||
+        (e = cudaMemset(ctx->board, 0, 256 + sizeof(unsigned) * ctx->nranks)) != cudaSuccess)
+      return cuda_fail(e, "comm_init: progress board");
+    ctx->board_peer = ctx->board;
+    h[72] = ipc_export(ctx, ctx->board, h) == MMWS_GPU_OK ? 1 : 0;
+    ok();
+  }
+  unsigned char* stage = static_cast<unsigned char*>(ctx->ipc_stage);
+  cudaStream_t s = ctx->comm_stream;
+  if ((e = cudaMemcpyAsync(stage, h, 80, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return cuda_fail(e, "comm_init: board handle");
+  NCCL_TRY(nccl().Broadcast(stage, stage, 80, ncclUint8, 0, ctx->comm, s), "comm_init: board handle");
+  if ((e = cudaMemcpyAsync(h, stage, 80, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return cuda_fail(e, "comm_init: board handle");
+  if ((e = event_pool(ctx, 1)) != cudaSuccess) return cuda_fail(e, "comm_init: events");
+  cudaEventRecord(ctx->pool[0], s);
+  if (int rc = await(ctx, ctx->pool[0], "comm_init: board handle")) return rc;
+  if (ctx->rank != 0 && h[72]) {
+    void* p = nullptr;
+    if (ipc_open(ctx, h, &p) == MMWS_GPU_OK) ctx->board_peer = static_cast<unsigned*>(p);
+    ok();
+  }
+  return MMWS_GPU_OK;
+}
+
+// The host-only planning query (no context, not on a per-multiply path)
+// reads the knob at call time.
+Tuning host_tuning() { return Tuning::from_env(); }
 
 }  // namespace
 
@@ -368,7 +626,8 @@ int mmws_gpu_nccl_unique_id(uint8_t out[128]) {
   if (!out) return fail(MMWS_GPU_ERR_DOMAIN, "nccl_unique_id: null out");
   NCCL_REQUIRE();
   ncclUniqueId id;
-  NCCL_TRY(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+  if (ncclResult_t r = nccl().GetUniqueId(&id); r != ncclSuccess)
+    return fail(MMWS_GPU_ERR_NCCL, std::string("ncclGetUniqueId: ") + nccl().GetErrorString(r));
   std::memcpy(out, id.internal, 128);
   return ok();
 }
@@ -381,22 +640,33 @@ int mmws_gpu_comm_init(mmws_gpu_ctx* ctx, int nranks, int rank, const uint8_t id
                                        " outside world of " + std::to_string(nranks));
   if (!id) return fail(MMWS_GPU_ERR_DOMAIN, "comm_init: null unique id");
   if (ctx->comm) return fail(MMWS_GPU_ERR_STATE, "comm_init: communicator already initialised");
+  if (ctx->comm_failed)
+    return fail(MMWS_GPU_ERR_STATE, "comm_init: call mmws_gpu_comm_destroy after a failed round");
   NCCL_REQUIRE();
   ncclUniqueId uid;
   std::memcpy(uid.internal, id, 128);
-  NCCL_TRY(nccl().CommInitRank(&ctx->comm, nranks, uid, rank), "ncclCommInitRank");
-  ctx->nranks = nranks;
-  ctx->rank = rank;
-  ctx->last_fused = -1;
+  if (int rc = comm_create(ctx, nranks, rank, uid)) return rc;
+  if (int rc = board_setup(ctx)) return rc;
   return ok();
 }
 
 int mmws_gpu_comm_destroy(mmws_gpu_ctx* ctx) {
   MMWS_CTX_GUARD(ctx);
   if (ctx->comm) {
-    NCCL_TRY(nccl().CommDestroy(ctx->comm), "ncclCommDestroy");
+    cudaStreamSynchronize(ctx->comm_stream);
+    cudaStreamSynchronize(ctx->stream);
+    const ncclResult_t r = nccl().CommDestroy(ctx->comm);
     ctx->comm = nullptr;
+    if (r != ncclSuccess && r != ncclInProgress)
+      return fail(MMWS_GPU_ERR_NCCL, std::string("ncclCommDestroy: ") + nccl().GetErrorString(r));
   }
+  if (ctx->board) {
+    cudaFree(ctx->board);
+    ctx->board = nullptr;
+  }
+  ctx->board_peer = nullptr;
+  ctx->comm_failed = false;
+  ctx->round = 0;
   ctx->nranks = 1;
   ctx->rank = 0;
   ctx->last_fused = -1;
@@ -451,6 +721,7 @@ int mmws_gpu_link_probe(mmws_gpu_ctx* ctx, int64_t bytes, int iters, double* byt
   cudaError_t e;
   if ((e = ensure(ctx, &ctx->rbB, &ctx->rbB_bytes, static_cast<size_t>(bytes))) != cudaSuccess)
     return cuda_fail(e, "link_probe: buffer");
+  if ((e = event_pool(ctx, 1)) != cudaSuccess) return cuda_fail(e, "link_probe: events");
   cudaStream_t s = ctx->comm_stream;
   NCCL_TRY(nccl().Broadcast(ctx->rbB, ctx->rbB, bytes, ncclUint8, 0, ctx->comm, s),
            "link_probe warm-up");
@@ -459,10 +730,62 @@ int mmws_gpu_link_probe(mmws_gpu_ctx* ctx, int64_t bytes, int iters, double* byt
     NCCL_TRY(nccl().Broadcast(ctx->rbB, ctx->rbB, bytes, ncclUint8, 0, ctx->comm, s),
              "link_probe broadcast");
   cudaEventRecord(ctx->ev1, s);
-  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "link_probe");
+  cudaEventRecord(ctx->pool[0], s);
+  if (int rc = await(ctx, ctx->pool[0], "link_probe")) return rc;
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
   *bytes_per_s = static_cast<double>(bytes) * iters / (ms * 1e-3);
+  return ok();
+}
+
+int mmws_gpu_p2p_probe(mmws_gpu_ctx* ctx, int64_t bytes, int iters, double* bytes_per_s) {
+  MMWS_CTX_GUARD(ctx);
+  if (bytes < 1 || iters < 1 || !bytes_per_s)
+    return fail(MMWS_GPU_ERR_DOMAIN, "p2p_probe: bad arguments");
+  if (!ctx->comm) return fail(MMWS_GPU_ERR_STATE, "p2p_probe: no communicator (comm_init)");
+  NCCL_REQUIRE();
+  *bytes_per_s = 0.0;
+  if (ctx->nranks < 2) return ok();
+  cudaError_t e;
+  if ((e = ensure(ctx, &ctx->rbB, &ctx->rbB_bytes, static_cast<size_t>(bytes))) != cudaSuccess)
+    return cuda_fail(e, "p2p_probe: buffer");
+  if ((e = event_pool(ctx, 1)) != cudaSuccess) return cuda_fail(e, "p2p_probe: events");
+  cudaStream_t s = ctx->comm_stream;
+  // rank 0 -> rank r, one peer at a time (the A-slice / C-slice link); the
+  // slowest peer is reported (rank 0's view; workers report their own link)
+  double worst = 0.0;
+  for (int r = 1; r < ctx->nranks; ++r) {
+    if (ctx->rank != 0 && ctx->rank != r) continue;
+    for (int i = 0; i <= iters; ++i) {  // i == 0: warm-up (connection set-up)
+      if (i == 1) cudaEventRecord(ctx->ev0, s);
+      if (ctx->rank == 0)
+        NCCL_TRY(nccl().Send(ctx->rbB, bytes, ncclUint8, r, ctx->comm, s), "p2p_probe send");
+      else
+        NCCL_TRY(nccl().Recv(ctx->rbB, bytes, ncclUint8, 0, ctx->comm, s), "p2p_probe recv");
+    }
+    cudaEventRecord(ctx->ev1, s);
+    cudaEventRecord(ctx->pool[0], s);
+    if (int rc = await(ctx, ctx->pool[0], "p2p_probe")) return rc;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    const double bw = static_cast<double>(bytes) * iters / (ms * 1e-3);
+    worst = worst == 0.0 ? bw : std::min(worst, bw);
+  }
+  *bytes_per_s = worst;
+  return ok();
+}
+
+int mmws_gpu_last_round(mmws_gpu_ctx* ctx, int* active_ranks, int* gather) {
+  if (!ctx) return fail(MMWS_GPU_ERR_STATE, "null mmws_gpu_ctx");
+  if (active_ranks) *active_ranks = ctx->last_active;
+  if (gather) *gather = ctx->last_gather;
+  return ok();
+}
+
+int mmws_gpu_set_timeout(mmws_gpu_ctx* ctx, double seconds) {
+  MMWS_CTX_GUARD(ctx);
+  if (!(seconds > 0)) return fail(MMWS_GPU_ERR_DOMAIN, "set_timeout: seconds must be > 0");
+  ctx->tune.timeout_s = seconds;
   return ok();
 }
 
@@ -508,7 +831,7 @@ int mmws_gpu_rowblock_ranks(int64_t m, int64_t n, int64_t k, int nranks, int ele
     return fail(MMWS_GPU_ERR_DIMENSION, "rowblock_ranks: dimensions must be positive");
   if (nranks < 1 || (elem_bytes != 4 && elem_bytes != 8))
     return fail(MMWS_GPU_ERR_DOMAIN, "rowblock_ranks: bad nranks / element size");
-  *active = rowblock_active(m, n, k, nranks, elem_bytes);
+  *active = rowblock_active(m, n, k, nranks, elem_bytes, host_tuning().rowblock_ranks);
   return ok();
 }
 

@@ -271,7 +271,7 @@ int mmws_gpu_server_start(mmws_gpu_ctx* ctx) {
   if (ctx->server) return ok();
   auto* s = new ServerState();
   s->ctas = SRV_DEFAULT_CTAS;
-  if (const char* env = std::getenv("MMWS_GPU_SERVER_CTAS")) s->ctas = std::atoi(env);
+  if (ctx->tune.server_ctas != 0) s->ctas = ctx->tune.server_ctas;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
   if (s->ctas < 1 || s->ctas > sms) {

@@ -181,7 +181,7 @@ cudaError_t get_stager(mmws_gpu_ctx* ctx, Stager** out) {
     // 3/4 of the host's cores, at most 12: 16-core box, N=8192 pageable
     // multiply 56 ms with 8 threads, 46 with 12, 44 with 16 (noisy)
     int threads = static_cast<int>(std::clamp(hw * 3 / 4, 1u, 12u));
-    if (const char* env = std::getenv("MMWS_GPU_COPY_THREADS")) threads = std::clamp(std::atoi(env), 1, 64);
+    if (ctx->tune.copy_threads > 0) threads = ctx->tune.copy_threads;
     auto* st = new Stager(threads);
     for (int s = 0; s < NSLOT; ++s) {
       cudaError_t e;

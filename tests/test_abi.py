@@ -199,8 +199,8 @@ def test_rowblock_distributes_only_where_it_pays(monkeypatch):
         seen = seen or d
     assert seen
     # it is the cost model's own comparison (plus the fixed round latency)
-    t1, _, _ = P.rowblock_cost(3000, 3000, 3000, 1, 8, 600e9, 33e12)
-    t8, _, _ = P.rowblock_cost(3000, 3000, 3000, 8, 8, 600e9, 33e12)
+    t1, _, _ = P.rowblock_cost(3000, 3000, 3000, 1, 8, 770e9, 36.3e12)
+    t8, _, _ = P.rowblock_cost(3000, 3000, 3000, 8, 8, 770e9, 36.3e12)
     assert (t8 + 60e-6 < t1) == (P.rowblock_ranks(3000, 3000, 3000, 8) == 8)
     monkeypatch.setenv("MMWS_GPU_ROWBLOCK_RANKS", "all")
     assert P.rowblock_ranks(10, 10, 10, 8) == 8

@@ -73,7 +73,8 @@ int run_worker(const mmws::gpu::BenchConfig& config, bool calibrate) {
   for (auto m : config.models) rowblock = rowblock || m == mmws::gpu::GpuModel::gpu_rowblock;
   if (rowblock)
     for (const std::int64_t n : config.dims)
-      for (int r = 0; r < config.repeats; ++r) mmws::gpu::worker_run(ctx, n, n, n);
+      for (int r = 0; r < config.repeats; ++r)
+        mmws::gpu::worker_run(ctx, n, n, n, mmws::gpu::Mode::automatic);  // the master's mode (time_model)
   if (calibrate) mmws::gpu::calibrate(ctx);  // its link probe is collective
   return 0;
 }
