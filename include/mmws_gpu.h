@@ -123,6 +123,13 @@ int mmws_gpu_device_info(mmws_gpu_ctx* ctx, int* num_sms, int* cc_major, int* cc
 uint64_t mmws_gpu_launch_count(const mmws_gpu_ctx* ctx);
 /* The context's own stream (cudaStream_t), used when a call passes NULL. */
 void* mmws_gpu_stream(mmws_gpu_ctx* ctx);
+/* Tuning / test knobs.  mmws_gpu_init reads them once from the environment
+ * (never per call); this sets one on a live context by the same name (value
+ * NULL or "": the default).  Knobs: MMWS_GPU_NO_STREAMK, MMWS_GPU_DMMA_PLAN,
+ * MMWS_GPU_RASTER_GROUP, MMWS_GPU_PIPELINE_TRACE, MMWS_GPU_ROWBLOCK_RANKS
+ * (all | 1), MMWS_GPU_SERVER_CTAS, MMWS_GPU_COPY_THREADS, MMWS_GPU_TIMEOUT_S,
+ * MMWS_GPU_NCCL_GATHER (C-slices as NCCL messages instead of fused stores). */
+int mmws_gpu_tune(mmws_gpu_ctx* ctx, const char* knob, const char* value);
 
 /* ---------------------------------------------------------------- host-only helpers */
 /* split_rows (protocol.hpp:33-46): offset/rows arrays of n_workers entries. */

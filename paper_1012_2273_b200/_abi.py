@@ -33,6 +33,7 @@ SIGNATURES = {
     "mmws_gpu_device_info": (_i, [_v, _p(_i), _p(_i), _p(_i), _p(_i)]),
     "mmws_gpu_launch_count": (_u64, [_v]),
     "mmws_gpu_stream": (_v, [_v]),
+    "mmws_gpu_tune": (_i, [_v, C.c_char_p, C.c_char_p]),
     "mmws_gpu_split_rows": (_i, [_i64, _i, _p(_i64), _p(_i64)]),
     "mmws_gpu_static_partition": (_i, [_u64, _u32, _p(_u64), _p(_u64)]),
     "mmws_gpu_op_count": (_i, [_i64, _p(_u64)]),

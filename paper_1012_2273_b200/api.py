@@ -259,6 +259,11 @@ class Context:
     def launches(self) -> int:
         return int(_lib().mmws_gpu_launch_count(self._h))
 
+    def tune(self, knob: str, value=None) -> None:
+        """Set one MMWS_GPU_* knob on this context (None: default)."""
+        _check(_lib().mmws_gpu_tune(self._h, knob.encode(),
+                                    None if value is None else str(value).encode()))
+
     @property
     def stream(self) -> int:
         return int(_lib().mmws_gpu_stream(self._h) or 0)

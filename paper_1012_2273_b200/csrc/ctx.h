@@ -24,6 +24,9 @@ struct Tuning {
   double timeout_s = 30.0;      // MMWS_GPU_TIMEOUT_S: deadline of one distributed step
   bool nccl_gather = false;     // MMWS_GPU_NCCL_GATHER: C-slices as NCCL messages, no fused IPC
   static Tuning from_env();
+  // Set one knob by its environment name (value NULL: back to the default);
+  // false for an unknown name.
+  bool set(const char* name, const char* value);
 };
 }  // namespace mmws_impl
 

@@ -33,25 +33,41 @@ int ok() {
   return MMWS_GPU_OK;
 }
 
+bool Tuning::set(const char* name, const char* v) {
+  if (v && !*v) v = nullptr;
+  const Tuning d;
+  if (!std::strcmp(name, "MMWS_GPU_NO_STREAMK")) {
+    no_streamk = v != nullptr;
+  } else if (!std::strcmp(name, "MMWS_GPU_DMMA_PLAN")) {
+    dmma_plan = v ? v : "";
+  } else if (!std::strcmp(name, "MMWS_GPU_RASTER_GROUP")) {
+    raster_group = v ? std::max(0, std::atoi(v)) : d.raster_group;
+  } else if (!std::strcmp(name, "MMWS_GPU_PIPELINE_TRACE")) {
+    pipeline_trace = v != nullptr;
+  } else if (!std::strcmp(name, "MMWS_GPU_ROWBLOCK_RANKS")) {
+    rowblock_ranks = !v ? 0 : std::strcmp(v, "all") == 0 ? -1 : std::strcmp(v, "1") == 0 ? 1 : 0;
+  } else if (!std::strcmp(name, "MMWS_GPU_SERVER_CTAS")) {
+    server_ctas = v ? std::atoi(v) : d.server_ctas;
+  } else if (!std::strcmp(name, "MMWS_GPU_COPY_THREADS")) {
+    copy_threads = v ? std::clamp(std::atoi(v), 1, 64) : d.copy_threads;
+  } else if (!std::strcmp(name, "MMWS_GPU_TIMEOUT_S")) {
+    const double s = v ? std::atof(v) : 0.0;
+    timeout_s = s > 0 ? s : d.timeout_s;
+  } else if (!std::strcmp(name, "MMWS_GPU_NCCL_GATHER")) {
+    nccl_gather = v != nullptr;
+  } else {
+    return false;
+  }
+  return true;
+}
+
 Tuning Tuning::from_env() {
   Tuning t;
-  auto env = [](const char* name) -> const char* {
-    const char* v = std::getenv(name);
-    return v && *v ? v : nullptr;
-  };
-  t.no_streamk = env("MMWS_GPU_NO_STREAMK") != nullptr;
-  if (const char* v = env("MMWS_GPU_DMMA_PLAN")) t.dmma_plan = v;
-  if (const char* v = env("MMWS_GPU_RASTER_GROUP")) t.raster_group = std::max(0, std::atoi(v));
-  t.pipeline_trace = env("MMWS_GPU_PIPELINE_TRACE") != nullptr;
-  if (const char* v = env("MMWS_GPU_ROWBLOCK_RANKS"))
-    t.rowblock_ranks = std::strcmp(v, "all") == 0 ? -1 : std::strcmp(v, "1") == 0 ? 1 : 0;
-  if (const char* v = env("MMWS_GPU_SERVER_CTAS")) t.server_ctas = std::atoi(v);
-  if (const char* v = env("MMWS_GPU_COPY_THREADS")) t.copy_threads = std::clamp(std::atoi(v), 1, 64);
-  if (const char* v = env("MMWS_GPU_TIMEOUT_S")) {
-    const double s = std::atof(v);
-    if (s > 0) t.timeout_s = s;
-  }
-  t.nccl_gather = env("MMWS_GPU_NCCL_GATHER") != nullptr;
+  for (const char* name : {"MMWS_GPU_NO_STREAMK", "MMWS_GPU_DMMA_PLAN", "MMWS_GPU_RASTER_GROUP",
+                           "MMWS_GPU_PIPELINE_TRACE", "MMWS_GPU_ROWBLOCK_RANKS",
+                           "MMWS_GPU_SERVER_CTAS", "MMWS_GPU_COPY_THREADS", "MMWS_GPU_TIMEOUT_S",
+                           "MMWS_GPU_NCCL_GATHER"})
+    if (const char* v = std::getenv(name)) t.set(name, v);
   return t;
 }
 
@@ -512,6 +528,14 @@ int mmws_gpu_device_info(mmws_gpu_ctx* ctx, int* num_sms, int* cc_major, int* cc
 uint64_t mmws_gpu_launch_count(const mmws_gpu_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 void* mmws_gpu_stream(mmws_gpu_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int mmws_gpu_tune(mmws_gpu_ctx* ctx, const char* knob, const char* value) {
+  MMWS_CTX_GUARD(ctx);
+  if (!knob) return fail(MMWS_GPU_ERR_DOMAIN, "tune: null knob name");
+  if (!ctx->tune.set(knob, value))
+    return fail(MMWS_GPU_ERR_DOMAIN, std::string("tune: unknown knob ") + knob);
+  return ok();
+}
 
 // ------------------------------------------------------------------ host-only helpers
 int mmws_gpu_split_rows(int64_t n_rows, int n_workers, int64_t* offset, int64_t* rows) {

@@ -39,3 +39,29 @@ def test_reference_arm_nonzero_rank_exits_quietly():
                         "--n", "64", "--steps", "1", "--warmup", "0"],
                        capture_output=True, text=True, cwd=ROOT, env=env, timeout=120)
     assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+def test_dry_run_self_launches_ranks():
+    """`python bench.py --gpus 3` without torchrun launches 3 ranks itself and
+    prints rank 0's single line with n_gpus 3 and every rank's time (dry
+    mode: gloo, no GPU, no multiply)."""
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--dry-run", "--gpus", "3",
+                        "--n", "96", "--steps", "2", "--warmup", "1"],
+                       capture_output=True, text=True, cwd=ROOT, env=env, timeout=300)
+    assert r.returncode == 0, r.stderr
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 3 and d["dry_run"] is True and len(d["per_rank_ms"]) == 3
+    assert d["config"]["parallelism"] == "rowblock3" and d["steps"] == 2
+    assert d["ms_per_step"] * d["steps"] == pytest.approx(max(d["per_rank_ms"]))
+
+
+def test_world_size_must_match_gpus():
+    env = dict(os.environ, RANK="0", WORLD_SIZE="2", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--dry-run", "--gpus", "3",
+                        "--n", "64", "--steps", "1", "--warmup", "0"],
+                       capture_output=True, text=True, cwd=ROOT, env=env, timeout=120)
+    assert r.returncode != 0 and "WORLD_SIZE=2" in r.stderr

@@ -161,9 +161,9 @@ def test_stream_k_is_bitwise_the_one_shot_kernel(ctx, oracle, monkeypatch, shape
     B = ctx.fill(P.DIST_UNIFORM, 32, k, n)
     for mode in (P.MODE_AUTO, P.MODE_DMMA):
         got = host(ctx.dgemm(A, B, mode=mode))
-        monkeypatch.setenv("MMWS_GPU_NO_STREAMK", "1")
+        ctx.tune("MMWS_GPU_NO_STREAMK", "1")
         want = host(ctx.dgemm(A, B, mode=mode))
-        monkeypatch.delenv("MMWS_GPU_NO_STREAMK")
+        ctx.tune("MMWS_GPU_NO_STREAMK", None)
         assert (bits(got) == bits(want)).all(), (shape, mode)
     again = host(ctx.dgemm(A, B))                 # flags were left clean for the next launch
     assert (bits(again) == bits(got)).all()
@@ -173,9 +173,9 @@ def test_stream_k_is_bitwise_the_one_shot_kernel(ctx, oracle, monkeypatch, shape
     # exact order: stream-K form of the exact kernel, bitwise matmul_seq
     ex = host(ctx.dgemm(A, B, mode=P.MODE_EXACT))
     assert (bits(ex[rows]) == bits(want_rows)).all()
-    monkeypatch.setenv("MMWS_GPU_NO_STREAMK", "1")
+    ctx.tune("MMWS_GPU_NO_STREAMK", "1")
     ex1 = host(ctx.dgemm(A, B, mode=P.MODE_EXACT))
-    monkeypatch.delenv("MMWS_GPU_NO_STREAMK")
+    ctx.tune("MMWS_GPU_NO_STREAMK", None)
     assert (bits(ex) == bits(ex1)).all()
 
 
@@ -201,7 +201,7 @@ def test_every_dmma_tile_plan_gives_the_same_bits(ctx, oracle, monkeypatch, shap
         plans = [str(cfg)] + [f"{cfg}s{r}" for r in (1, 2, 3, 4)
                               if r <= per_sm and tiles >= r * sms and r * bm * bn <= 128 * 128]
         for plan in plans:
-            monkeypatch.setenv("MMWS_GPU_DMMA_PLAN", plan)
+            ctx.tune("MMWS_GPU_DMMA_PLAN", plan)
             # strided C inside a canary frame: the plan writes exactly C
             buf = torch().full((m + 2, n + 3), -7.5, dtype=torch().float64, device="cuda")
             ctx.dgemm(A, B, buf[1:m + 1, 1:n + 1], mode=P.MODE_DMMA)
@@ -210,13 +210,16 @@ def test_every_dmma_tile_plan_gives_the_same_bits(ctx, oracle, monkeypatch, shap
             assert (b[0] == -7.5).all() and (b[m + 1] == -7.5).all(), (shape, plan)
             assert (b[:, 0] == -7.5).all() and (b[:, n + 1:] == -7.5).all(), (shape, plan)
             tried += 1
-    monkeypatch.delenv("MMWS_GPU_DMMA_PLAN")
+    ctx.tune("MMWS_GPU_DMMA_PLAN", None)
     for mode in (P.MODE_AUTO, P.MODE_DMMA_SMALL):
         assert (bits(host(ctx.dgemm(A, B, mode=mode))) == bits(want)).all(), (shape, mode)
     assert tried >= 6
-    monkeypatch.setenv("MMWS_GPU_DMMA_PLAN", "0s2")  # more CTAs than can be resident
-    with pytest.raises(P.DomainError):
-        ctx.dgemm(A, B, mode=P.MODE_DMMA)
+    ctx.tune("MMWS_GPU_DMMA_PLAN", "0s2")  # more CTAs than can be resident
+    try:
+        with pytest.raises(P.DomainError):
+            ctx.dgemm(A, B, mode=P.MODE_DMMA)
+    finally:
+        ctx.tune("MMWS_GPU_DMMA_PLAN", None)
 
 
 @pytest.mark.parametrize("seed", range(4))

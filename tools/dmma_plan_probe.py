@@ -46,12 +46,12 @@ def main():
         B = ctx.fill(P.DIST_UNIFORM, 1, n, n)
         ref = torch.empty_like(A)
         reps = max(5, min(200, int(2e10 / (2 * n ** 3))))
-        os.environ.pop("MMWS_GPU_DMMA_PLAN", None)
+        ctx.tune("MMWS_GPU_DMMA_PLAN", None)
         rec = {"n": n, "reps": reps}
         ms = per_call_ms(lambda: ctx.dgemm(A, B, ref, mode=P.MODE_AUTO), reps)
         rec["auto"] = {"us": ms * 1e3, "tflops": 2 * n ** 3 / ms / 1e9}
         for plan in PLANS:
-            os.environ["MMWS_GPU_DMMA_PLAN"] = plan
+            ctx.tune("MMWS_GPU_DMMA_PLAN", plan)
             C = torch.empty_like(A)
             try:
                 ctx.dgemm(A, B, C, mode=P.MODE_DMMA)
@@ -62,7 +62,7 @@ def main():
             same = bool(torch.equal(C.view(torch.int64), ref.view(torch.int64)))
             ms = per_call_ms(lambda: ctx.dgemm(A, B, C, mode=P.MODE_DMMA), reps)
             rec[plan] = {"us": ms * 1e3, "tflops": 2 * n ** 3 / ms / 1e9, "bitwise": same}
-        os.environ.pop("MMWS_GPU_DMMA_PLAN", None)
+        ctx.tune("MMWS_GPU_DMMA_PLAN", None)
         print(json.dumps(rec), flush=True)
 
 

@@ -17,11 +17,8 @@ B = ctx.fill(P.DIST_UNIFORM, 1, n, n)
 C = torch.empty_like(A)
 for tok in sys.argv[2:]:
     plan, _, group = tok.partition(":")
-    os.environ["MMWS_GPU_DMMA_PLAN"] = plan
-    if group:
-        os.environ["MMWS_GPU_RASTER_GROUP"] = group
-    else:
-        os.environ.pop("MMWS_GPU_RASTER_GROUP", None)
+    ctx.tune("MMWS_GPU_DMMA_PLAN", plan)
+    ctx.tune("MMWS_GPU_RASTER_GROUP", group or None)
     ctx.dgemm(A, B, C, mode=P.MODE_DMMA)
     torch.cuda.synchronize()
     print(tok, ctx.last_plan, flush=True)

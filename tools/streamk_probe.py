@@ -37,9 +37,8 @@ for n in [int(x) for x in sys.argv[1:]] or [1600, 2000, 2048, 2304, 2500, 3000, 
                             ("no_streamk", {"MMWS_GPU_NO_STREAMK": "1"}, P.MODE_AUTO),
                             ("exact", {}, P.MODE_EXACT),
                             ("exact_no_streamk", {"MMWS_GPU_NO_STREAMK": "1"}, P.MODE_EXACT)):
-        os.environ.pop("MMWS_GPU_NO_STREAMK", None)
-        os.environ.update(env)
+        ctx.tune("MMWS_GPU_NO_STREAMK", env.get("MMWS_GPU_NO_STREAMK"))
         ms = best_ms(lambda: ctx.dgemm(A, B, C, mode=mode))
         rec[name] = {"ms": ms, "tflops": 2 * n ** 3 / ms / 1e9}
-    os.environ.pop("MMWS_GPU_NO_STREAMK", None)
+    ctx.tune("MMWS_GPU_NO_STREAMK", None)
     print(json.dumps(rec), flush=True)
