@@ -102,7 +102,6 @@ cudaError_t preload_dgemm_dmma();
 cudaError_t preload_ozaki();
 cudaError_t preload_dgemm_exact();
 cudaError_t preload_dgemm_small();
-cudaError_t preload_sgemm();
 cudaError_t preload_sgemm_tma();
 cudaError_t preload_misc();
 
@@ -145,12 +144,9 @@ cudaError_t launch_dgemm_small(const Launch& L, bool exact, int64_t M, int64_t N
                                const double* A, int64_t lda, const double* B, int64_t ldb,
                                double* C, int64_t ldc);
 
-// Register-blocked FFMA fp32 GEMM with two-level (chunked) accumulation.
-cudaError_t launch_sgemm_ffma(const Launch& L, int64_t M, int64_t N, int64_t K, const float* A,
-                              int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc);
-
-// TMA-fed, warp-specialised FFMA2 fp32 GEMM (needs lda, ldb % 4 == 0 and
-// 16-byte aligned A, B).
+// TMA-fed, warp-specialised FFMA2 fp32 GEMM with two-level (chunked)
+// accumulation (needs lda, ldb % 4 == 0 and 16-byte aligned A, B; the caller
+// packs other layouts).
 bool sgemm_tma_supported(int64_t lda, int64_t ldb, const float* A, const float* B);
 cudaError_t launch_sgemm_tma(const Launch& L, int64_t M, int64_t N, int64_t K, const float* A,
                              int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc);
@@ -162,6 +158,10 @@ cudaError_t launch_pack_f64(const Launch& L, const double* src, int64_t rows, in
 
 // Store `value` into one progress word (device or peer-mapped), in stream order.
 cudaError_t launch_board_mark(const Launch& L, unsigned* word, unsigned value);
+
+cudaError_t launch_pack_f32(const Launch& L, const float* src, int64_t rows, int64_t cols,
+                            int64_t ld_src, float* dst, int64_t rows_p, int64_t cols_p,
+                            int64_t ld_dst);
 
 // Counter-based splitmix64 generators (bit-identical to oracle_fill for dist 0..2).
 cudaError_t launch_fill(const Launch& L, int dist, uint64_t seed, void* dst, int64_t rows,

@@ -60,16 +60,26 @@ __global__ void board_mark_kernel(volatile unsigned* word, unsigned value) {
 // ---------------------------------------------------------------- packing
 // One CTA row-strip per (row, 1024-column chunk): no 64-bit division per
 // element, coalesced reads and writes.
-__global__ void pack_f64_kernel(const double* __restrict__ src, int64_t rows, int64_t cols,
-                                int64_t ld_src, double* __restrict__ dst, int64_t rows_p,
-                                int64_t cols_p, int64_t ld_dst) {
+template <class T>
+__global__ void pack_kernel(const T* __restrict__ src, int64_t rows, int64_t cols, int64_t ld_src,
+                            T* __restrict__ dst, int64_t rows_p, int64_t cols_p, int64_t ld_dst) {
   for (int64_t r = blockIdx.y; r < rows_p; r += gridDim.y) {
-    const double* s = src + r * ld_src;
-    double* d = dst + r * ld_dst;
+    const T* s = src + r * ld_src;
+    T* d = dst + r * ld_dst;
     for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < cols_p;
          c += static_cast<int64_t>(gridDim.x) * blockDim.x)
-      d[c] = (r < rows && c < cols) ? s[c] : 0.0;
+      d[c] = (r < rows && c < cols) ? s[c] : T(0);
   }
+}
+
+template <class T>
+cudaError_t launch_pack(const Launch& L, const T* src, int64_t rows, int64_t cols, int64_t ld_src,
+                        T* dst, int64_t rows_p, int64_t cols_p, int64_t ld_dst) {
+  const dim3 grid(static_cast<unsigned>((cols_p + 255) / 256 < 8 ? (cols_p + 255) / 256 : 8),
+                  static_cast<unsigned>(rows_p < 65535 ? rows_p : 65535));
+  pack_kernel<T><<<grid, 256, 0, L.stream>>>(src, rows, cols, ld_src, dst, rows_p, cols_p, ld_dst);
+  L.count();
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- peak probes
@@ -149,12 +159,13 @@ cudaError_t launch_fill(const Launch& L, int dist, uint64_t seed, void* dst, int
 cudaError_t launch_pack_f64(const Launch& L, const double* src, int64_t rows, int64_t cols,
                             int64_t ld_src, double* dst, int64_t rows_p, int64_t cols_p,
                             int64_t ld_dst) {
-  const dim3 grid(static_cast<unsigned>((cols_p + 255) / 256 < 8 ? (cols_p + 255) / 256 : 8),
-                  static_cast<unsigned>(rows_p < 65535 ? rows_p : 65535));
-  pack_f64_kernel<<<grid, 256, 0, L.stream>>>(src, rows, cols, ld_src, dst, rows_p, cols_p,
-                                              ld_dst);
-  L.count();
-  return cudaGetLastError();
+  return launch_pack(L, src, rows, cols, ld_src, dst, rows_p, cols_p, ld_dst);
+}
+
+cudaError_t launch_pack_f32(const Launch& L, const float* src, int64_t rows, int64_t cols,
+                            int64_t ld_src, float* dst, int64_t rows_p, int64_t cols_p,
+                            int64_t ld_dst) {
+  return launch_pack(L, src, rows, cols, ld_src, dst, rows_p, cols_p, ld_dst);
 }
 
 cudaError_t launch_peak_probe(const Launch& L, int which, int iters, double* sink,
@@ -194,7 +205,7 @@ cudaError_t launch_board_mark(const Launch& L, unsigned* word, unsigned value) {
 }
 
 cudaError_t preload_misc() {
-  return preload_kernels(fill_kernel, pack_f64_kernel, board_mark_kernel, probe_kernel<0>, probe_kernel<1>,
+  return preload_kernels(fill_kernel, pack_kernel<double>, pack_kernel<float>, board_mark_kernel, probe_kernel<0>, probe_kernel<1>,
                          probe_kernel<2>, probe_kernel<3>, probe_kernel<4>);
 }
 

@@ -334,10 +334,35 @@ int sgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const flo
     ctx->last_plan = "ozaki f32 (int8 tcgen05 GEMMs + CRT)";
     return e == cudaSuccess ? ok() : cuda_fail(e, "sgemm ozaki");
   }
-  const bool tma = sgemm_tma_supported(lda, ldb, A, B);
-  cudaError_t e = tma ? launch_sgemm_tma(L, m, n, k, A, lda, B, ldb, C, ldc)
-                      : launch_sgemm_ffma(L, m, n, k, A, lda, B, ldb, C, ldc);
-  ctx->last_plan = tma ? "sgemm_tma_kernel<128x256, FFMA2>" : "sgemm_ffma_kernel<192x128, FFMA2>";
+  // TMA needs 16-byte aligned bases and row pitches that are multiples of 4
+  // floats: other layouts are packed once into the workspace (one HBM-bound
+  // pass, zero padding never read), so every layout runs the same kernel --
+  // and gets the same bits.
+  cudaError_t e;
+  const bool a_aligned = lda % 4 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0;
+  const bool b_aligned = ldb % 4 == 0 && reinterpret_cast<uintptr_t>(B) % 16 == 0;
+  if (!a_aligned || !b_aligned) {
+    const int64_t lda_p = round_up(k, 4), ldb_p = round_up(n, 4);
+    const size_t bytes = sizeof(float) * ((a_aligned ? 0 : m * lda_p) + (b_aligned ? 0 : k * ldb_p));
+    void* wsp = nullptr;
+    if ((e = workspace(ctx, bytes, &wsp)) != cudaSuccess) return cuda_fail(e, "sgemm pack workspace");
+    float* w = static_cast<float*>(wsp);
+    if (!a_aligned) {
+      if ((e = launch_pack_f32(L, A, m, k, lda, w, m, lda_p, lda_p)) != cudaSuccess)
+        return cuda_fail(e, "sgemm pack A");
+      A = w;
+      lda = lda_p;
+      w += m * lda_p;
+    }
+    if (!b_aligned) {
+      if ((e = launch_pack_f32(L, B, k, n, ldb, w, k, ldb_p, ldb_p)) != cudaSuccess)
+        return cuda_fail(e, "sgemm pack B");
+      B = w;
+      ldb = ldb_p;
+    }
+  }
+  e = launch_sgemm_tma(L, m, n, k, A, lda, B, ldb, C, ldc);
+  ctx->last_plan = "sgemm_tma_kernel<128x256, FFMA2>";
   return e == cudaSuccess ? ok() : cuda_fail(e, "sgemm ffma");
 }
 
@@ -434,7 +459,7 @@ int mmws_gpu_init(int device, mmws_gpu_ctx** out) {
   // inside the caller's timed region (~70 ms on the first streamed host
   // multiply at N=16384), and the latency server relies on it (server.cu).
   if ((e = preload_dgemm_dmma()) || (e = preload_dgemm_exact()) || (e = preload_dgemm_small()) ||
-      (e = preload_sgemm()) || (e = preload_sgemm_tma()) || (e = preload_misc()) ||
+      (e = preload_sgemm_tma()) || (e = preload_misc()) ||
       (e = preload_ozaki()))
     return cuda_fail(e, "mmws_gpu_init: load kernels");
   auto* ctx = new (std::nothrow) mmws_gpu_ctx();

@@ -1,8 +1,20 @@
 // sgemm_tma.cu -- FP32 GEMM on the FFMA2 pipe, TMA-fed and warp-specialised.
 //
-// Same contraction and accuracy scheme as sgemm_ffma.cu (two-level summation
-// with the running totals in shared memory, see there), restructured like the
-// DMMA kernel so the math warps do nothing but LDS + FFMA2:
+// The fp32 configuration (BASELINE.json configs[4], N=32768 normal(0,1)) has
+// no counterpart in the reference (its Matrix is fp64 only, matrix.hpp:39-91);
+// this is the same C = A.B contraction as the reference's threaded body
+// (workshare.hpp:98-113) in fp32, checked normwise against the fp64 oracle of
+// the widened inputs (tolerance 1e-5, tests/test_gpu_parity.py).
+//
+// Accuracy: a single fp32 chain over K = 32768 terms has an expected normwise
+// error of ~5e-6, uncomfortably close to the 1e-5 bound.  Each 1024-long
+// k-chunk is therefore summed into a fresh register partial that is added
+// into a running total kept in shared memory once per chunk -- two-level
+// (blocked) summation, error growth ~sqrt(KC) + sqrt(K / KC) instead of
+// ~sqrt(K), without doubling the accumulator registers.
+//
+// Structure (like the DMMA kernel, so the math warps do nothing but LDS +
+// FFMA2):
 //   * a producer warpgroup (one elected lane) streams A[128 x 16] and
 //     B[16 x 256] k-slices with TMA into a 4-stage mbarrier ring and gives its
 //     registers to the math warps (setmaxnreg 40 / 232);
@@ -11,8 +23,13 @@
 //     broadcast; B as 4-column vectors 64 columns apart, conflict-free);
 //   * stages are released one iteration late (after the next stage's full
 //     barrier), the ptxas-proof ordering dgemm_dmma.cu documents.
-// Used when A and B meet TMA's 16-byte alignment rules; sgemm_ffma.cu
-// (cp.async) covers every other layout.
+// Operand pattern: every FFMA2 reads its accumulator pair and the broadcast A
+// scalar from the register file (the B pair comes from the operand reuse
+// cache); a register-only loop of exactly this pattern peaks at ~63 TFLOP/s
+// on B200 against ~69.5 when the scalar is a uniform register
+// (tools/ffma2_uniform_probe.cu, profiles/r02_ffma2_uniform_probe.txt) -- the
+// kernel runs at ~99% of its pattern's ceiling.  Layouts TMA cannot read are
+// packed by the caller (mmws_gpu.cu), so every layout takes this kernel.
 #include "common.cuh"
 #include "kernels.h"
 

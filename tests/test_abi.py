@@ -231,3 +231,31 @@ def test_master_run_over_a_world_bootstrapped_by_the_reference_launcher():
         pytest.skip("ref_control_plane not built (needs the reference headers at build time)")
     r = subprocess.run([REF_CP, "gpu"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok: master_run" in r.stdout, r.stdout + r.stderr
+
+
+def test_python_output_buffer_checks_without_a_gpu():
+    # the wrappers validate outputs before the C ABI
+    # writes m*n elements into them (host heap / device out-of-bounds writes)
+    import numpy as np
+    import torch
+
+    from paper_1012_2273_b200 import api
+    assert api._host_out(None, 3, 4, np.float64, "t").shape == (3, 4)
+    ok = np.empty((3, 4))
+    assert api._host_out(ok, 3, 4, np.float64, "t") is ok
+    with pytest.raises(P.DimensionError):
+        api._host_out(np.empty((3, 3)), 3, 4, np.float64, "t")
+    with pytest.raises(P.DomainError):
+        api._host_out(np.empty((3, 4), dtype=np.float32), 3, 4, np.float64, "t")
+    with pytest.raises(P.DimensionError):
+        api._host_out(np.empty((4, 3)).T, 3, 4, np.float64, "t")
+    ro = np.empty((3, 4))
+    ro.setflags(write=False)
+    with pytest.raises(P.DimensionError):
+        api._host_out(ro, 3, 4, np.float64, "t")
+    a = torch.zeros((3, 2), dtype=torch.float64)
+    b = torch.zeros((2, 4), dtype=torch.float64)
+    with pytest.raises(P.DomainError):            # host tensors are not device operands
+        api._device_operands(a, b, None, torch.float64, "t")
+    with pytest.raises(P.DomainError):
+        api._device_operands(a.float(), b, None, torch.float64, "t")

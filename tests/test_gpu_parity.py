@@ -842,3 +842,105 @@ def test_auto_tile_plan_by_size(ctx):
     ctx.dgemm(A, A, mode=P.MODE_EXACT)             # 441 tiles: 2.98 per SM, one-shot
     assert ctx.last_plan == "dgemm_exact (one-shot)"
     T.cuda.synchronize()
+
+
+# ----------------------------------------------------------------------------- round-2 fixes
+def test_fp32_unaligned_layouts_are_packed_and_bitwise_the_aligned_call(ctx, oracle):
+    # lda / ldb not multiples of 4 floats and misaligned bases: the operands
+    # are packed for the TMA kernel, so the bits equal the dense call's
+    T = torch()
+    big_a = ctx.fill(P.DIST_NORMAL, 5, 301, 1031, dtype=T.float32)
+    big_b = ctx.fill(P.DIST_NORMAL, 6, 1030, 517, dtype=T.float32)
+    A = big_a[1:300, 3:1030]      # lda 1031, base off by 3 floats
+    B = big_b[1:1028, 1:516]      # ldb 517
+    dense = host(ctx.sgemm(A.contiguous(), B.contiguous()))
+    got = host(ctx.sgemm(A, B))
+    assert (got.view(np.int32) == dense.view(np.int32)).all()
+    rows = [0, 150, 298]
+    ref = oracle.matmul_rows(rows, host(A.contiguous()).astype(np.float64),
+                             host(B.contiguous()).astype(np.float64))
+    assert normwise(got[rows].astype(np.float64), ref) <= FP32_TOL
+    assert ctx.last_plan.startswith("sgemm_tma_kernel")
+
+
+def test_graph_keeps_its_own_workspace(ctx, oracle):
+    # a graph whose multiply packs its operands must not
+    # share the context's workspace -- an eager call that regrows it, or runs
+    # meanwhile, must leave the graph's replays correct.
+    T = torch()
+    big = ctx.fill(P.DIST_UNIFORM, 51, 401, 403)
+    A = big[:, 1:400]              # odd leading dimension: packed
+    B = ctx.fill(P.DIST_UNIFORM, 52, 399, 397)
+    C = T.empty((401, 397), dtype=T.float64, device="cuda")
+    want = host(ctx.dgemm(A.contiguous(), B))
+    g = ctx.graph_dgemm(A, B, C)
+    try:
+        g.launch()
+        T.cuda.synchronize()
+        assert (bits(host(C)) == bits(want)).all()
+        # eager calls that need a much bigger packing workspace (regrow)
+        big2 = ctx.fill(P.DIST_UNIFORM, 53, 3001, 3003)
+        ctx.dgemm(big2[:, 1:3002], big2[:3001, 2:3003])
+        T.cuda.synchronize()
+        C.zero_()
+        g.launch()
+        T.cuda.synchronize()
+        assert (bits(host(C)) == bits(want)).all()
+    finally:
+        g.close()
+
+
+def test_host_pipeline_narrow_tail_block_keeps_the_whole_problem_bits(ctx):
+    # m = n = 1060, k = 96 from pinned buffers splits panel 0
+    # into column blocks; a narrow last block must not drop onto the latency
+    # kernel (it is folded into the previous block)
+    T = torch()
+    m = n = 1060
+    k = 96
+    A = ctx.fill(P.DIST_UNIFORM, 61, m, k)
+    B = ctx.fill(P.DIST_UNIFORM, 62, k, n)
+    want = host(ctx.dgemm(A, B))
+    a = T.from_numpy(host(A)).pin_memory().numpy()
+    b = T.from_numpy(host(B)).pin_memory().numpy()
+    c = T.empty((m, n), dtype=T.float64).pin_memory().numpy()
+    got, _ = ctx.matmul_host(a, b, out=c)
+    assert (bits(got) == bits(want)).all()
+
+
+def test_host_and_device_output_checks(ctx):
+    # wrong output buffers are rejected before any write
+    T = torch()
+    a = np.ones((4, 3))
+    b = np.ones((3, 5))
+    with pytest.raises(P.DimensionError):
+        ctx.matmul_host(a, b, out=np.empty((4, 4)))
+    with pytest.raises(P.DomainError):
+        ctx.matmul_host(a, b, out=np.empty((4, 5), dtype=np.float32))
+    with pytest.raises(P.DimensionError):
+        ctx.matmul_host(a, b, out=np.empty((5, 4)).T)
+    A = ctx.fill(P.DIST_UNIFORM, 1, 4, 3)
+    B = ctx.fill(P.DIST_UNIFORM, 2, 3, 5)
+    with pytest.raises(P.DimensionError):
+        ctx.dgemm(A, B, T.empty((3, 5), dtype=T.float64, device="cuda"))
+    with pytest.raises(P.DomainError):
+        ctx.dgemm(A, B, T.empty((4, 5), dtype=T.float32, device="cuda"))
+    with pytest.raises(P.DomainError):
+        ctx.dgemm(A, B, T.empty((4, 5), dtype=T.float64))          # host tensor
+    with pytest.raises(P.DomainError):
+        ctx.graph_dgemm(A, B.float(), T.empty((4, 5), dtype=T.float64, device="cuda"))
+    with pytest.raises(P.DimensionError):
+        ctx.rowblock(4, 5, 3, A, B, T.empty((4, 6), dtype=T.float64, device="cuda"))
+
+
+def test_tuning_knobs_apply_on_a_live_context(ctx):
+    n = 2000
+    A = ctx.fill(P.DIST_UNIFORM, 71, n, n)
+    B = ctx.fill(P.DIST_UNIFORM, 72, n, n)
+    ctx.dgemm(A, B, mode=P.MODE_DMMA)
+    assert "stream-K" in ctx.last_plan
+    ctx.tune("MMWS_GPU_NO_STREAMK", "1")
+    ctx.dgemm(A, B, mode=P.MODE_DMMA)
+    assert "stream-K" not in ctx.last_plan
+    ctx.tune("MMWS_GPU_NO_STREAMK", None)
+    ctx.dgemm(A, B, mode=P.MODE_DMMA)
+    assert "stream-K" in ctx.last_plan
