@@ -314,8 +314,9 @@ int mmws_gpu_rowblock_cost(int64_t m, int64_t n, int64_t k, int nranks, int elem
 /* Whether a row-block round over nranks GPUs is distributed at all (the north
  * star's "used only where N is large enough to amortise the transfers"):
  * *active = nranks when the cost model above, with fixed planning rates
- * (NVLink 600 GB/s per direction, 33 TFLOP/s fp64 / 55 TFLOP/s fp32 per
- * GPU, 60 us of collective latency per round), predicts the distributed round
+ * (NVLink 770 GB/s per direction -- the measured B200 peer copy -- and the
+ * library's measured 36.3 TFLOP/s fp64 / 62 TFLOP/s fp32 per GPU, 60 us of
+ * collective latency per round), predicts the distributed round
  * to beat rank 0 multiplying alone, else 1: rank 0 computes every row and the
  * workers return at once (the reference's idle worker, protocol.hpp:122-123,
  * with no messages at all).  Every rank computes the same answer from its

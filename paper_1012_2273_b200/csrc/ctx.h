@@ -58,6 +58,7 @@ struct mmws_gpu_ctx {
   };
   std::vector<IpcMap> ipc_cache;
   void* ipc_stage = nullptr;  // 256-byte device staging for the handle broadcast / barrier
+  unsigned char* host_stage = nullptr;  // 512 bytes of pinned host memory: its host end
   unsigned char last_handle[80] = {0};  // row-block: handle bytes of the last call
   int last_fused = -1;                  // row-block: agreed fused-gather decision for it
   // streamed host path: [tile order | ready_a | ready_b | done] on the device

@@ -502,7 +502,9 @@ int mmws_gpu_init(int device, mmws_gpu_ctx** out) {
       (e = cudaEventCreate(&ctx->evk0)) != cudaSuccess ||
       (e = cudaEventCreate(&ctx->evk1)) != cudaSuccess ||
       (e = cudaMalloc(&ctx->sink, 4096 * sizeof(double))) != cudaSuccess ||
-      (e = cudaMalloc(&ctx->ipc_stage, 256)) != cudaSuccess) {
+      (e = cudaMalloc(&ctx->ipc_stage, 256)) != cudaSuccess ||
+      (e = cudaHostAlloc(reinterpret_cast<void**>(&ctx->host_stage), 512,
+                         cudaHostAllocDefault)) != cudaSuccess) {
     mmws_gpu_destroy(ctx);
     return cuda_fail(e, "mmws_gpu_init");
   }
@@ -522,6 +524,7 @@ int mmws_gpu_destroy(mmws_gpu_ctx* ctx) {
                   static_cast<void*>(ctx->sink)})
     if (p) cudaFree(p);
   for (void* p : ctx->deferred_free) cudaFree(p);
+  if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
   for (const auto& sp : ctx->sk_spaces) cudaFree(sp.mem);
   staging_destroy(ctx);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);

@@ -337,8 +337,13 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
   mark(ctx, comm, JOINED);
 
   // ---- fused gather set-up (see above)
+  // host ends of the small exchanges live in pinned memory: a copy to or from
+  // pageable memory would block this thread on the comm stream (past the
+  // deadline if a peer is gone)
   unsigned char* stage = static_cast<unsigned char*>(ctx->ipc_stage);
-  unsigned char hbuf[80] = {0};
+  unsigned char* hbuf = ctx->host_stage;
+  int* vote_host = reinterpret_cast<int*>(ctx->host_stage + 128);
+  std::memset(hbuf, 0, 80);
   if (me == 0) {
     hbuf[72] = !ctx->tune.nccl_gather && ipc_export(ctx, C, hbuf) == MMWS_GPU_OK ? 1 : 0;
     if ((e = cudaMemcpyAsync(stage, hbuf, 80, cudaMemcpyHostToDevice, comm)))
@@ -361,14 +366,16 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
   int fused = ctx->last_fused;
   if (fused < 0 || std::memcmp(hbuf, ctx->last_handle, 80) != 0) {  // new handle: vote
     int* vote = reinterpret_cast<int*>(stage + 128);
-    if ((e = cudaMemcpyAsync(vote, &ok_here, sizeof(int), cudaMemcpyHostToDevice, comm)))
+    vote_host[0] = ok_here;
+    if ((e = cudaMemcpyAsync(vote, vote_host, sizeof(int), cudaMemcpyHostToDevice, comm)))
       return cuda_fail(e, "rowblock: vote");
     NCCL_TRY(nccl().AllReduce(vote, vote, 1, ncclInt32, ncclMin, ctx->comm, comm),
              "agree on fused gather");
-    if ((e = cudaMemcpyAsync(&fused, vote, sizeof(int), cudaMemcpyDeviceToHost, comm)))
+    if ((e = cudaMemcpyAsync(vote_host + 1, vote, sizeof(int), cudaMemcpyDeviceToHost, comm)))
       return cuda_fail(e, "rowblock: vote result");
     cudaEventRecord(evHost, comm);
     if (int rc = await(ctx, evHost, "rowblock: agree on the C gather")) return rc;
+    fused = vote_host[1];
     std::memcpy(ctx->last_handle, hbuf, 80);
     ctx->last_fused = fused;
   }
@@ -586,7 +593,8 @@ int comm_create(mmws_gpu_ctx* ctx, int nranks, int rank, const ncclUniqueId& uid
 // cannot name the rank that fell behind.
 int board_setup(mmws_gpu_ctx* ctx) {
   cudaError_t e;
-  unsigned char h[80] = {0};
+  unsigned char* h = ctx->host_stage + 256;  // pinned (see rowblock_enqueue)
+  std::memset(h, 0, 80);
   if (ctx->rank == 0) {
     if ((e = cudaMalloc(&ctx->board, 256 + sizeof(unsigned) * ctx->nranks)) != cudaSuccess ||
         (e = cudaMemset(ctx->board, 0, 256 + sizeof(unsigned) * ctx->nranks)) != cudaSuccess)
