@@ -82,6 +82,10 @@ using Mid = Cfg<128, 64, 32, 32, 5, 1>;    // 8 math warps, 160 KB ring
 using Small8 = Cfg<64, 64, 32, 16, 6, 1>;  // 8 math warps on a 64x64 tile (stream-K, 1 CTA/SM)
 using Tiny = Cfg<32, 32, 16, 16, 4, 6>;    // 4 math warps, 32 KB ring, 6 CTAs/SM
 using Slim = Cfg<32, 64, 16, 32, 4, 4>;    // 4 math warps, 48 KB ring, 4 CTAs/SM
+// Few-tile grids (small N): the K loop of a lone tile is bound by TMA round
+// trips, not the tensor pipe, so these keep most of K in flight at once.
+using TinyDeep = Cfg<32, 32, 16, 16, 12, 2>;  // 4 math warps, 96 KB ring, 2 CTAs/SM
+using Micro = Cfg<16, 16, 8, 16, 12, 4>;      // 2 math warps, 48 KB ring, 4 CTAs/SM
 
 // Poll an arrival flag (written by a cuStreamWriteValue32 behind an H2D copy).
 // A flag that never arrives is a host-side bug; trap after 60 s so the
@@ -470,7 +474,8 @@ cudaError_t launch_dgemm_dmma_stream(const Launch& L, int64_t M, int64_t N, int6
 int dmma_tile_rows(int cfg) {
   switch (cfg) {
     case DMMA_64x64: case DMMA_64x64_W8: return 64;
-    case DMMA_32x32: case DMMA_32x64: return 32;
+    case DMMA_32x32: case DMMA_32x64: case DMMA_32x32_DEEP: return 32;
+    case DMMA_16x16: return 16;
     default: return 128;
   }
 }
@@ -478,14 +483,15 @@ int dmma_tile_rows(int cfg) {
 int dmma_tile_cols(int cfg) {
   switch (cfg) {
     case DMMA_64x64: case DMMA_64x64_W8: case DMMA_128x64: case DMMA_32x64: return 64;
-    case DMMA_32x32: return 32;
+    case DMMA_32x32: case DMMA_32x32_DEEP: return 32;
+    case DMMA_16x16: return 16;
     default: return 128;
   }
 }
 
 const char* dmma_plan_name(int cfg, int launch) {
   // [cfg][launch]: one-shot, stream-K
-  static const char* const names[6][2] = {
+  static const char* const names[8][2] = {
       {"dgemm_dmma_kernel<128x128, 8 math warps, 1 CTA/SM>",
        "dgemm_dmma_kernel<128x128, 8 math warps, stream-K>"},
       {"dgemm_dmma_kernel<64x64, 4 math warps, 3 CTAs/SM>",
@@ -497,8 +503,12 @@ const char* dmma_plan_name(int cfg, int launch) {
       {"dgemm_dmma_kernel<32x32, 4 math warps, 6 CTAs/SM>",
        "dgemm_dmma_kernel<32x32, 4 math warps, stream-K>"},
       {"dgemm_dmma_kernel<32x64, 4 math warps, 4 CTAs/SM>",
-       "dgemm_dmma_kernel<32x64, 4 math warps, stream-K>"}};
-  if (cfg < 0 || cfg > 5 || launch < 0 || launch > 1) return "dgemm_dmma_kernel<?>";
+       "dgemm_dmma_kernel<32x64, 4 math warps, stream-K>"},
+      {"dgemm_dmma_kernel<32x32, 4 math warps, 12 stages, 2 CTAs/SM>",
+       "dgemm_dmma_kernel<32x32, 4 math warps, 12 stages, stream-K>"},
+      {"dgemm_dmma_kernel<16x16, 2 math warps, 12 stages, 4 CTAs/SM>",
+       "dgemm_dmma_kernel<16x16, 2 math warps, 12 stages, stream-K>"}};
+  if (cfg < 0 || cfg > DMMA_16x16 || launch < 0 || launch > 1) return "dgemm_dmma_kernel<?>";
   return names[cfg][launch];
 }
 
@@ -510,6 +520,8 @@ int dmma_ctas_per_sm(int cfg) {
     case DMMA_64x64_W8: return Small8::MINB;
     case DMMA_32x32: return Tiny::MINB;
     case DMMA_32x64: return Slim::MINB;
+    case DMMA_32x32_DEEP: return TinyDeep::MINB;
+    case DMMA_16x16: return Micro::MINB;
     default: return Big::MINB;
   }
 }
@@ -524,6 +536,9 @@ cudaError_t launch_dgemm_dmma_sk(const Launch& L, int cfg, int64_t M, int64_t N,
       return run_sk<Small8>(L, M, N, Kd, A, lda, B, ldb, C, ldc, partial, flags, grid);
     case DMMA_32x32: return run_sk<Tiny>(L, M, N, Kd, A, lda, B, ldb, C, ldc, partial, flags, grid);
     case DMMA_32x64: return run_sk<Slim>(L, M, N, Kd, A, lda, B, ldb, C, ldc, partial, flags, grid);
+    case DMMA_32x32_DEEP:
+      return run_sk<TinyDeep>(L, M, N, Kd, A, lda, B, ldb, C, ldc, partial, flags, grid);
+    case DMMA_16x16: return run_sk<Micro>(L, M, N, Kd, A, lda, B, ldb, C, ldc, partial, flags, grid);
     default: return run_sk<Big>(L, M, N, Kd, A, lda, B, ldb, C, ldc, partial, flags, grid);
   }
 }
@@ -537,6 +552,8 @@ cudaError_t launch_dgemm_dmma(const Launch& L, int cfg, int64_t M, int64_t N, in
     case DMMA_64x64_W8: return run<Small8>(L, M, N, K, A, lda, B, ldb, C, ldc);
     case DMMA_32x32: return run<Tiny>(L, M, N, K, A, lda, B, ldb, C, ldc);
     case DMMA_32x64: return run<Slim>(L, M, N, K, A, lda, B, ldb, C, ldc);
+    case DMMA_32x32_DEEP: return run<TinyDeep>(L, M, N, K, A, lda, B, ldb, C, ldc);
+    case DMMA_16x16: return run<Micro>(L, M, N, K, A, lda, B, ldb, C, ldc);
     default: return run<Big>(L, M, N, K, A, lda, B, ldb, C, ldc);
   }
 }
@@ -548,7 +565,9 @@ cudaError_t preload_dgemm_dmma() {
                          dgemm_dmma_kernel<Mid, 2>,
                          dgemm_dmma_kernel<Small8, 0>, dgemm_dmma_kernel<Small8, 2>,
                          dgemm_dmma_kernel<Tiny, 0>, dgemm_dmma_kernel<Tiny, 2>,
-                         dgemm_dmma_kernel<Slim, 0>, dgemm_dmma_kernel<Slim, 2>);
+                         dgemm_dmma_kernel<Slim, 0>, dgemm_dmma_kernel<Slim, 2>,
+                         dgemm_dmma_kernel<TinyDeep, 0>, dgemm_dmma_kernel<TinyDeep, 2>,
+                         dgemm_dmma_kernel<Micro, 0>, dgemm_dmma_kernel<Micro, 2>);
 }
 
 }  // namespace mmws_impl

@@ -33,6 +33,8 @@ enum DmmaCfg {
   DMMA_64x64_W8 = 3,  // 8 math warps on a 64x64 tile, 1 CTA/SM
   DMMA_32x32 = 4,     // 4 math warps, 6 CTAs/SM
   DMMA_32x64 = 5,     // 4 math warps, 4 CTAs/SM
+  DMMA_32x32_DEEP = 6,  // 4 math warps, 12-stage ring, 2 CTAs/SM (few-tile grids)
+  DMMA_16x16 = 7,       // 2 math warps, 12-stage ring, 4 CTAs/SM (few-tile grids)
 };
 // AUTO takes the 32x32 DFMA latency kernel when n and k are both <= this
 // (a rule on (n, k) only, so row slices get the whole problem's bits).

@@ -267,7 +267,8 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
   if (int rc = pack_operands()) return rc;
   // DMMA tile plan.  Every configuration computes each element as the same
   // DMMA chain in ascending k from +0.0, so the choice never changes the bits.
-  // AUTO: 32x32 tiles, 6 CTAs (24 math warps) per SM below three 128x128
+  // AUTO: 16x16 tiles below one 32x32 tile per SM (below), then
+  // 32x32 tiles, 6 CTAs (24 math warps) per SM below three 128x128
   // tiles per SM; 64x64 tiles, 3 CTAs (12 math warps) per SM up to 64 tiles
   // per SM; 128x128 above.  GPU time per call, back to back
   // (tools/dmma_plan_probe.py, profiles/r01_dmma_plans.jsonl), against the
@@ -280,8 +281,17 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
   // 0.3-0.5 % faster (240.8 vs 241.9 ms) for 2.3x the DRAM reads (116 vs 50
   // GB), so the largest problems keep 128x128 tiles.  Stream-K over small
   // tiles lost to their one-shot launches at every size measured.
+  // Below one 32x32 tile per SM (square N < ~390) AUTO takes 16x16 tiles
+  // (2 math warps, 12-stage ring, 4 CTAs/SM): a lone tile's K loop is bound
+  // by its dependent DMMA chains, so more, smaller tiles finish sooner --
+  // GPU time per call (tools/dmma_plan_probe.py, profiles/r02_small_plans.jsonl)
+  // 32x32 vs 16x16: N=100 5.8 vs 4.1 us, 128 6.1 vs 4.1, 160 6.2 vs 4.4,
+  // 250 8.2 vs 6.2, 300 8.2 vs 7.2; from 400 on 32x32 wins (10.8 vs 12.3).
+  const int64_t tiles32 = ((m + 31) / 32) * ((n + 31) / 32);
   int cfg = DMMA_128x128;
-  if (mode == MMWS_GPU_MODE_DMMA_SMALL || (mode == MMWS_GPU_MODE_AUTO && tiles128 < 3 * G))
+  if (mode == MMWS_GPU_MODE_AUTO && tiles32 < G)
+    cfg = DMMA_16x16;
+  else if (mode == MMWS_GPU_MODE_DMMA_SMALL || (mode == MMWS_GPU_MODE_AUTO && tiles128 < 3 * G))
     cfg = DMMA_32x32;
   else if (mode == MMWS_GPU_MODE_AUTO && tiles128 < 64 * G)
     cfg = DMMA_64x64;
@@ -297,7 +307,7 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
                           ((n + dmma_tile_cols(cfg) - 1) / dmma_tile_cols(cfg));
     // stream-K needs every CTA resident (a CTA may wait on its lower
     // neighbour), a whole tile per CTA, and workspace slots for the grid
-    if (cfg < DMMA_128x128 || cfg > DMMA_32x64 || sk_grid < 0 ||
+    if (cfg < DMMA_128x128 || cfg > DMMA_16x16 || sk_grid < 0 ||
         (sk_grid > 0 && (sk_grid > 4 * G || sk_grid > G * dmma_ctas_per_sm(cfg) || tiles < sk_grid ||
                          static_cast<int64_t>(sk_grid) * dmma_tile_rows(cfg) * dmma_tile_cols(cfg) >
                              G * 128 * 128)))

@@ -195,7 +195,8 @@ def test_every_dmma_tile_plan_gives_the_same_bits(ctx, oracle, monkeypatch, shap
     sms = torch().cuda.get_device_properties(0).multi_processor_count
     tried = 0
     # (tile rows, tile columns, resident CTAs per SM) of each configuration
-    cfgs = [(128, 128, 1), (64, 64, 3), (128, 64, 1), (64, 64, 1), (32, 32, 6), (32, 64, 4)]
+    cfgs = [(128, 128, 1), (64, 64, 3), (128, 64, 1), (64, 64, 1), (32, 32, 6), (32, 64, 4),
+            (32, 32, 2), (16, 16, 4)]
     for cfg, (bm, bn, per_sm) in enumerate(cfgs):
         tiles = -(-m // bm) * -(-n // bn)
         plans = [str(cfg)] + [f"{cfg}s{r}" for r in (1, 2, 3, 4)
@@ -813,14 +814,16 @@ def test_peak_probes_run(ctx):
 
 def test_auto_tile_plan_by_size(ctx):
     # AUTO's plan (mmws_gpu_last_plan): the DFMA latency kernel while n, k <= 96,
-    # 32x32 DMMA tiles below three 128x128 tiles per SM, 64x64 tiles up to 64
-    # per SM, 128x128 above;
+    # 16x16 DMMA tiles below one 32x32 tile per SM, 32x32 tiles below three
+    # 128x128 tiles per SM, 64x64 tiles up to 64 per SM, 128x128 above;
     # MODE_DMMA keeps 128x128 tiles (stream-K from one tile per SM).
     T = torch()
     sms = T.cuda.get_device_properties(0).multi_processor_count
     for (m, n, k), want in [((64, 64, 64), "dgemm_small_kernel<DFMA"),
                             ((96, 96, 96), "dgemm_small_kernel<DFMA"),
-                            ((64, 97, 64), "dgemm_dmma_kernel<32x32"),
+                            ((64, 97, 64), "dgemm_dmma_kernel<16x16"),
+                            ((250, 250, 250), "dgemm_dmma_kernel<16x16"),
+                            ((400, 400, 400), "dgemm_dmma_kernel<32x32"),
                             ((1000, 1000, 1000), "dgemm_dmma_kernel<32x32"),
                             ((128 * 3 * sms, 128, 64), "dgemm_dmma_kernel<64x64"),
                             ((128 * 64 * sms, 128, 16), "dgemm_dmma_kernel<128x128")]:
