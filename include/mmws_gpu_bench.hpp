@@ -249,12 +249,16 @@ inline void emit_csv(const std::vector<BenchRecord>& records, const std::string&
 // ---------------------------------------------------------------- calibration
 // The reference's `bench calibrate` fits tc / tf (seconds per datum moved over
 // its TCP link) for cost_model.hpp.  The GPU row-block round has two rates:
-// the NVLink broadcast bandwidth out of rank 0 and the per-GPU multiply rate
-// (mmws_gpu_rowblock_cost).  Collective when the context has a communicator
-// of more than one rank (every rank must call it); otherwise the link rate is
-// NVLink 5's nominal 900 GB/s per direction and marked as not measured.
+// rank 0's NVLink egress (the B broadcast and the point-to-point A-slices) and
+// the per-GPU multiply rate (mmws_gpu_rowblock_cost).  With a communicator of
+// more than one rank both links are measured (collective: every rank must
+// call it) and the slower one is the model's link rate; a 1-rank world has no
+// link to measure, so the rate is the B200 peer-copy reference of 770 GB/s
+// per direction (B200_PROFILING.md) and marked as not measured in this run.
 struct CostFit {
-  double link_bytes_per_s = 900e9;
+  double link_bytes_per_s = 770e9;
+  double broadcast_bytes_per_s = 0.0;  // measured (world > 1)
+  double p2p_bytes_per_s = 0.0;        // measured (world > 1)
   double gemm_flops_per_s = 0.0;
   bool link_measured = false;
 };
@@ -264,7 +268,11 @@ inline CostFit calibrate(Context& ctx, std::int64_t gemm_n = 4096,
   CostFit fit;
   check(mmws_gpu_gemm_probe(ctx.handle(), gemm_n, MMWS_GPU_MODE_AUTO, 3, &fit.gemm_flops_per_s));
   if (ctx.world_size() > 1) {
-    check(mmws_gpu_link_probe(ctx.handle(), link_bytes, 5, &fit.link_bytes_per_s));
+    check(mmws_gpu_link_probe(ctx.handle(), link_bytes, 5, &fit.broadcast_bytes_per_s));
+    check(mmws_gpu_p2p_probe(ctx.handle(), link_bytes, 5, &fit.p2p_bytes_per_s));
+    fit.link_bytes_per_s = fit.p2p_bytes_per_s > 0.0
+                               ? std::min(fit.broadcast_bytes_per_s, fit.p2p_bytes_per_s)
+                               : fit.broadcast_bytes_per_s;
     fit.link_measured = true;
   }
   return fit;
@@ -418,7 +426,7 @@ inline void emit_plots(const std::vector<BenchRecord>& records, const std::strin
     if (!model.points.empty()) {
       runtime.push_back(std::move(model));
       comment = "cost-model overlay: link=" + plot_detail::num(fit->link_bytes_per_s) +
-                " B/s (" + (fit->link_measured ? "measured" : "nominal") +
+                " B/s (" + (fit->link_measured ? "measured" : "B200 peer-copy reference") +
                 "), gemm=" + plot_detail::num(fit->gemm_flops_per_s) +
                 " FLOP/s; predicted seconds = mmws_gpu_rowblock_cost";
     }

@@ -62,7 +62,7 @@ def test_plots_series_and_cost_overlay(tmp_path):
     for (_, a), (_, b) in zip(s["cost-model"], want):
         assert abs(a - b) <= 1e-5 * b                                  # %.6g in the attribute
     assert s["cost-model#dashed"] and not s["gpu#dashed"]
-    assert "cost-model overlay: link=5e+11 B/s (nominal)" in text
+    assert "cost-model overlay: link=5e+11 B/s (B200 peer-copy reference)" in text
     _, m = _series(d / "mflops.svg")
     assert m["gpu-rowblock"] == [(2048.0, 5.7e6), (4096.0, 1.3e7)] and "cost-model" not in m
     _, sp = _series(d / "speedup.svg")
@@ -97,7 +97,7 @@ def test_cli_sweep_with_gate(tmp_path):
     assert len(lines) == 1 + 12
     models = [ln.split(",")[0] for ln in lines[1:]]
     assert models == ["gpu"] * 4 + ["gpu-exact"] * 4 + ["gpu-rowblock"] * 4
-    assert "calibration: link 9e+11 B/s (nominal NVLink 5), gemm" in r.stdout
+    assert "calibration: link 7.7e+11 B/s (B200 peer-copy reference), gemm" in r.stdout
     _, s = _series(tmp_path / "svg" / "runtime.svg")
     assert [x for x, _ in s["cost-model"]] == [10.0, 100.0, 257.0, 1000.0]
     assert [x for x, _ in s["gpu-rowblock"]] == [10.0, 100.0, 257.0, 1000.0]

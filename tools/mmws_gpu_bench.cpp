@@ -190,7 +190,11 @@ int main(int argc, char** argv) {
     if (calibrate) {
       fit = mmws::gpu::calibrate(ctx);
       std::printf("calibration: link %.6g B/s (%s), gemm %.6g FLOP/s\n", fit->link_bytes_per_s,
-                  fit->link_measured ? "measured" : "nominal NVLink 5", fit->gemm_flops_per_s);
+                  fit->link_measured ? "measured" : "B200 peer-copy reference",
+                  fit->gemm_flops_per_s);
+      if (fit->link_measured)
+        std::printf("calibration: broadcast %.6g B/s, point-to-point %.6g B/s\n",
+                    fit->broadcast_bytes_per_s, fit->p2p_bytes_per_s);
     }
     if (!plots_dir.empty()) mmws::gpu::emit_plots(records, plots_dir, fit);
   } catch (const mmws::gpu::GateError& e) {
