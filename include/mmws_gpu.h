@@ -153,6 +153,20 @@ int mmws_gpu_sgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const flo
                    int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int mode,
                    void* stream);
 
+/* Accumulating multiply, C = Cin + A.B (Cin m x n, leading dimension ldcin;
+ * Cin may be C itself): every element's chain starts from its Cin value
+ * instead of +0.0 and continues exactly as in mmws_gpu_dgemm.  Splitting K
+ * into panels at multiples of 16 (fp64) / 1024 (fp32, the partial-sum chunk)
+ * and chaining the calls (the first from +0.0 via mmws_gpu_dgemm / _sgemm)
+ * therefore gives bitwise the one-call result -- what the row-block workers
+ * use to multiply while B is still arriving.  All modes but OZAKI. */
+int mmws_gpu_dgemm_acc(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
+                       int64_t lda, const double* B, int64_t ldb, const double* Cin,
+                       int64_t ldcin, double* C, int64_t ldc, int mode, void* stream);
+int mmws_gpu_sgemm_acc(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const float* A,
+                       int64_t lda, const float* B, int64_t ldb, const float* Cin, int64_t ldcin,
+                       float* C, int64_t ldc, int mode, void* stream);
+
 /* MMWS_GPU_MODE_OZAKI plan for inner dimension k: number of int8 tensor-core
  * GEMMs (moduli) and the integer bits each row of A / column of B is scaled to
  * (normwise error ~1.4 * 2^-bits for random inputs).  Host-only. */

@@ -39,6 +39,10 @@ SIGNATURES = {
     "mmws_gpu_op_count": (_i, [_i64, _p(_u64)]),
     "mmws_gpu_dgemm": (_i, [_v, _i64, _i64, _i64, _v, _i64, _v, _i64, _v, _i64, _i, _v]),
     "mmws_gpu_sgemm": (_i, [_v, _i64, _i64, _i64, _v, _i64, _v, _i64, _v, _i64, _i, _v]),
+    "mmws_gpu_dgemm_acc": (_i, [_v, _i64, _i64, _i64, _v, _i64, _v, _i64, _v, _i64, _v, _i64, _i,
+                                _v]),
+    "mmws_gpu_sgemm_acc": (_i, [_v, _i64, _i64, _i64, _v, _i64, _v, _i64, _v, _i64, _v, _i64, _i,
+                                _v]),
     "mmws_gpu_matmul_host": (_i, [_v, _i64, _i64, _i64, _v, _v, _v, _i, _p(_d)]),
     "mmws_gpu_matmul_host_f32": (_i, [_v, _i64, _i64, _i64, _v, _v, _v, _i, _p(_d)]),
     "mmws_gpu_fill": (_i, [_v, _i, _u64, _v, _i64, _i64, _i64, _i, _u64, _v]),

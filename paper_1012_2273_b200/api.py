@@ -269,20 +269,36 @@ class Context:
         return int(_lib().mmws_gpu_stream(self._h) or 0)
 
     # -- device-pointer multiply (torch CUDA tensors)
-    def dgemm(self, A, B, C_=None, mode: int = MODE_AUTO, stream=None):
+    def dgemm(self, A, B, C_=None, mode: int = MODE_AUTO, stream=None, accumulate=None):
+        """C_ = A . B; with `accumulate`, C_ = accumulate + A . B continuing its
+        chains (mmws_gpu_dgemm_acc; `accumulate` may be C_ itself)."""
         import torch
         m, n, k = _device_operands(A, B, C_, torch.float64, "dgemm")
         if C_ is None:
             C_ = torch.empty((m, n), dtype=torch.float64, device=A.device)
+        if accumulate is not None:
+            _device_operands(A, B, accumulate, torch.float64, "dgemm")
+            _check(_lib().mmws_gpu_dgemm_acc(self._h, m, n, k, _ptr(A), _ld(A), _ptr(B), _ld(B),
+                                             _ptr(accumulate), _ld(accumulate), _ptr(C_), _ld(C_),
+                                             mode, _stream(stream)))
+            return C_
         _check(_lib().mmws_gpu_dgemm(self._h, m, n, k, _ptr(A), _ld(A), _ptr(B), _ld(B),
                                      _ptr(C_), _ld(C_), mode, _stream(stream)))
         return C_
 
-    def sgemm(self, A, B, C_=None, mode: int = MODE_AUTO, stream=None):
+    def sgemm(self, A, B, C_=None, mode: int = MODE_AUTO, stream=None, accumulate=None):
+        """fp32 C_ = A . B; with `accumulate`, C_ = accumulate + A . B
+        (mmws_gpu_sgemm_acc)."""
         import torch
         m, n, k = _device_operands(A, B, C_, torch.float32, "sgemm")
         if C_ is None:
             C_ = torch.empty((m, n), dtype=torch.float32, device=A.device)
+        if accumulate is not None:
+            _device_operands(A, B, accumulate, torch.float32, "sgemm")
+            _check(_lib().mmws_gpu_sgemm_acc(self._h, m, n, k, _ptr(A), _ld(A), _ptr(B), _ld(B),
+                                             _ptr(accumulate), _ld(accumulate), _ptr(C_), _ld(C_),
+                                             mode, _stream(stream)))
+            return C_
         _check(_lib().mmws_gpu_sgemm(self._h, m, n, k, _ptr(A), _ld(A), _ptr(B), _ld(B),
                                      _ptr(C_), _ld(C_), mode, _stream(stream)))
         return C_

@@ -142,9 +142,11 @@ inline cudaError_t workspace(mmws_gpu_ctx* ctx, size_t bytes, void** out) {
   return e;
 }
 // the fp64 multiply dispatch used by dgemm / host / graph / row-block paths
+// cin (optional): accumulate, C = Cin + A.B continuing Cin's chains (no
+// stream-K; not in MODE_OZAKI).
 int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
                    int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int mode,
-                   cudaStream_t stream);
+                   cudaStream_t stream, const double* cin = nullptr, int64_t ldcin = 0);
 // Host -> device copy of `rows` rows of `width` bytes (row pitches in bytes),
 // queued on s.  Pageable host memory goes through pinned chunks filled by
 // host threads (staging.cu); pinned memory is copied directly.  Returns once
@@ -194,16 +196,17 @@ int host_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A
                   T* C, int mode, double* elapsed_s);
 int sgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const float* A,
                    int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int mode,
-                   cudaStream_t stream);
+                   cudaStream_t stream, const float* cin = nullptr, int64_t ldcin = 0);
 
 // fp64 / fp32 multiply through the matching dispatch
 template <class T>
 int gemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, int64_t lda, const T* B,
-         int64_t ldb, T* C, int64_t ldc, int mode, cudaStream_t s) {
+         int64_t ldb, T* C, int64_t ldc, int mode, cudaStream_t s, const T* cin = nullptr,
+         int64_t ldcin = 0) {
   if constexpr (sizeof(T) == 8)
-    return dgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode, s);
+    return dgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode, s, cin, ldcin);
   else
-    return sgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode, s);
+    return sgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode, s, cin, ldcin);
 }
 
 // at least `need` ordering events (timing disabled) in ctx->pool

@@ -131,9 +131,10 @@ MMWS_DEVICE void set_flag(int* f, int v) {
 template <class K, int MODE>
 __global__ void __launch_bounds__(K::THREADS, K::MINB)
     dgemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA,
-                      const __grid_constant__ CUtensorMap tmB, double* __restrict__ C,
+                      const __grid_constant__ CUtensorMap tmB, double* C,
                       int64_t ldc, int M, int N, int K_, int tiles_m, int tiles_n, int vec_ok,
                       int group, DmmaStream st) {
+  // C may alias st.cin (in-place accumulate), so neither is __restrict__ here
   constexpr bool STREAM = MODE == 1, SK = MODE == 2;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   // 1024-byte aligned ring (128B-swizzle atoms); offsetting the __shared__
@@ -283,6 +284,24 @@ __global__ void __launch_bounds__(K::THREADS, K::MINB)
       for (int b = 0; b < K::NB; ++b)
   #pragma unroll
         for (int e = 0; e < 2; ++e) acc[i][b][e][0] = acc[i][b][e][1] = 0.0;
+    if constexpr (MODE == 0) {
+      if (st.cin) {  // accumulate: continue Cin's chains (the epilogue's layout)
+  #pragma unroll
+        for (int i = 0; i < K::MI; ++i) {
+          const int row = tm * K::BM + wm * K::WM + i * 8 + sig;
+          if (row >= M) continue;
+          const double* crow = st.cin + static_cast<int64_t>(row) * st.ldcin;
+  #pragma unroll
+          for (int b = 0; b < K::NB; ++b) {
+            const int col = tn * K::BN + (wn * K::NB + b) * 16 + 4 * tig;
+            acc[i][b][0][0] = col + 0 < N ? crow[col + 0] : 0.0;
+            acc[i][b][1][0] = col + 1 < N ? crow[col + 1] : 0.0;
+            acc[i][b][0][1] = col + 2 < N ? crow[col + 2] : 0.0;
+            acc[i][b][1][1] = col + 3 < N ? crow[col + 3] : 0.0;
+          }
+        }
+      }
+    }
     if constexpr (SK) {
       if (k0 > 0) {  // continue the lower CTA's accumulators for this tile
         if (threadIdx.x == 0) wait_flag(st.flags + blockIdx.x);
@@ -408,7 +427,8 @@ bool make_map(const Launch& L, CUtensorMap* map, const double* base, int64_t inn
 
 template <class K>
 cudaError_t run(const Launch& L, int64_t M, int64_t N, int64_t Kd, const double* A, int64_t lda,
-                const double* B, int64_t ldb, double* C, int64_t ldc) {
+                const double* B, int64_t ldb, double* C, int64_t ldc, const double* cin,
+                int64_t ldcin) {
   CUtensorMap ta, tb;
   if (!make_map(L, &ta, A, Kd, M, lda, 16, K::BM)) return cudaErrorInvalidValue;
   if (!make_map(L, &tb, B, N, Kd, ldb, 16, 16)) return cudaErrorInvalidValue;
@@ -419,9 +439,12 @@ cudaError_t run(const Launch& L, int64_t M, int64_t N, int64_t Kd, const double*
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int vec_ok = (ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0);
+  DmmaStream st;
+  st.cin = cin;
+  st.ldcin = ldcin;
   dgemm_dmma_kernel<K, 0><<<tiles_m * tiles_n, K::THREADS, smem, L.stream>>>(
       ta, tb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(Kd), tiles_m,
-      tiles_n, vec_ok, raster_group<K>(L), DmmaStream{});
+      tiles_n, vec_ok, raster_group<K>(L), st);
   L.count();
   return cudaGetLastError();
 }
@@ -545,16 +568,16 @@ cudaError_t launch_dgemm_dmma_sk(const Launch& L, int cfg, int64_t M, int64_t N,
 
 cudaError_t launch_dgemm_dmma(const Launch& L, int cfg, int64_t M, int64_t N, int64_t K,
                               const double* A, int64_t lda, const double* B, int64_t ldb,
-                              double* C, int64_t ldc) {
+                              double* C, int64_t ldc, const double* cin, int64_t ldcin) {
   switch (cfg) {
-    case DMMA_64x64: return run<Small>(L, M, N, K, A, lda, B, ldb, C, ldc);
-    case DMMA_128x64: return run<Mid>(L, M, N, K, A, lda, B, ldb, C, ldc);
-    case DMMA_64x64_W8: return run<Small8>(L, M, N, K, A, lda, B, ldb, C, ldc);
-    case DMMA_32x32: return run<Tiny>(L, M, N, K, A, lda, B, ldb, C, ldc);
-    case DMMA_32x64: return run<Slim>(L, M, N, K, A, lda, B, ldb, C, ldc);
-    case DMMA_32x32_DEEP: return run<TinyDeep>(L, M, N, K, A, lda, B, ldb, C, ldc);
-    case DMMA_16x16: return run<Micro>(L, M, N, K, A, lda, B, ldb, C, ldc);
-    default: return run<Big>(L, M, N, K, A, lda, B, ldb, C, ldc);
+    case DMMA_64x64: return run<Small>(L, M, N, K, A, lda, B, ldb, C, ldc, cin, ldcin);
+    case DMMA_128x64: return run<Mid>(L, M, N, K, A, lda, B, ldb, C, ldc, cin, ldcin);
+    case DMMA_64x64_W8: return run<Small8>(L, M, N, K, A, lda, B, ldb, C, ldc, cin, ldcin);
+    case DMMA_32x32: return run<Tiny>(L, M, N, K, A, lda, B, ldb, C, ldc, cin, ldcin);
+    case DMMA_32x64: return run<Slim>(L, M, N, K, A, lda, B, ldb, C, ldc, cin, ldcin);
+    case DMMA_32x32_DEEP: return run<TinyDeep>(L, M, N, K, A, lda, B, ldb, C, ldc, cin, ldcin);
+    case DMMA_16x16: return run<Micro>(L, M, N, K, A, lda, B, ldb, C, ldc, cin, ldcin);
+    default: return run<Big>(L, M, N, K, A, lda, B, ldb, C, ldc, cin, ldcin);
   }
 }
 

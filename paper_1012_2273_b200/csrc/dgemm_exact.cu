@@ -35,8 +35,8 @@ constexpr int SMEM = STAGES * (A_ELEMS + B_ELEMS) * sizeof(double);
 template <bool VA, bool VB>
 __global__ void __launch_bounds__(THREADS, 1)
     dgemm_exact_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
-                       int64_t ldb, double* __restrict__ C, int64_t ldc, int M, int N, int K,
-                       int tiles_m, int tiles_n) {
+                       int64_t ldb, double* C, int64_t ldc, int M, int N, int K,
+                       int tiles_m, int tiles_n, const double* cin, int64_t ldcin) {
   extern __shared__ __align__(16) double smem_d[];
   double* As = smem_d;                       // [STAGES][BM][SLA]
   double* Bs = smem_d + STAGES * A_ELEMS;    // [STAGES][BK][SLB]
@@ -64,6 +64,18 @@ __global__ void __launch_bounds__(THREADS, 1)
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+  if (cin) {  // accumulate: continue Cin's chains (the epilogue's layout; Cin may alias C)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = row0 + ty * 2 + 32 * (i >> 1) + (i & 1);
+      if (r >= M) continue;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int c = col0 + tx * 2 + 32 * (j >> 1) + (j & 1);
+        if (c < N) acc[i][j] = cin[static_cast<int64_t>(r) * ldcin + c];
+      }
+    }
+  }
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
@@ -161,9 +173,10 @@ MMWS_DEVICE void exact_wait_flag(const int* f) {
 template <int TBM, int TBN, bool SK = false>
 __global__ void __launch_bounds__(T_THREADS, ExactTma<TBM, TBN>::MINB)
     dgemm_exact_tma_kernel(const __grid_constant__ CUtensorMap tmA,
-                           const __grid_constant__ CUtensorMap tmB, double* __restrict__ C,
+                           const __grid_constant__ CUtensorMap tmB, double* C,
                            int64_t ldc, int M, int N, int K, int tiles_m, int tiles_n,
-                           double* partial = nullptr, int* flags = nullptr) {
+                           double* partial = nullptr, int* flags = nullptr,
+                           const double* cin = nullptr, int64_t ldcin = 0) {
   using X = ExactTma<TBM, TBN>;
   constexpr int T_A_BYTES = X::A_BYTES, T_STAGE = X::STAGE, TM = X::TM, TN = X::TN;
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -247,6 +260,18 @@ __global__ void __launch_bounds__(T_THREADS, ExactTma<TBM, TBN>::MINB)
     for (int i = 0; i < TM; ++i)
 #pragma unroll
       for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
+    if (!SK && cin) {  // accumulate: continue Cin's chains (epilogue layout)
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        const int r = tm * TBM + ty * 2 + 32 * (i >> 1) + (i & 1);
+        if (r >= M) continue;
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+          const int c = tn * TBN + tx * 2 + 32 * (j >> 1) + (j & 1);
+          if (c < N) acc[i][j] = cin[static_cast<int64_t>(r) * ldcin + c];
+        }
+      }
+    }
     if constexpr (SK) {
       if (k0 > 0) {  // continue the lower CTA's chains for this tile
         if (tid == 0) exact_wait_flag(flags + blockIdx.x);
@@ -341,7 +366,8 @@ bool make_map_f64(const Launch& L, CUtensorMap* map, const double* base, int64_t
 template <int TBM, int TBN, bool SK = false>
 cudaError_t run_exact_tma(const Launch& L, int64_t M, int64_t N, int64_t K, const double* A,
                           int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
-                          double* partial = nullptr, int* flags = nullptr, int grid = 0) {
+                          double* partial = nullptr, int* flags = nullptr, int grid = 0,
+                          const double* cin = nullptr, int64_t ldcin = 0) {
   using X = ExactTma<TBM, TBN>;
   CUtensorMap ta, tb;
   if (!make_map_f64(L, &ta, A, K, M, lda, BK, TBM) || !make_map_f64(L, &tb, B, N, K, ldb, TBN, BK))
@@ -354,7 +380,8 @@ cudaError_t run_exact_tma(const Launch& L, int64_t M, int64_t N, int64_t K, cons
   dgemm_exact_tma_kernel<TBM, TBN, SK><<<SK ? grid : tiles_m * tiles_n, T_THREADS, X::SMEM,
                                          L.stream>>>(ta, tb, C, ldc, static_cast<int>(M),
                                                      static_cast<int>(N), static_cast<int>(K),
-                                                     tiles_m, tiles_n, partial, flags);
+                                                     tiles_m, tiles_n, partial, flags, cin,
+                                                     ldcin);
   L.count();
   return cudaGetLastError();
 }
@@ -377,14 +404,16 @@ cudaError_t launch_dgemm_exact_sk(const Launch& L, int tile, int64_t M, int64_t 
 
 cudaError_t launch_dgemm_exact(const Launch& L, int64_t M, int64_t N, int64_t K, const double* A,
                                int64_t lda, const double* B, int64_t ldb, double* C,
-                               int64_t ldc) {
+                               int64_t ldc, const double* cin, int64_t ldcin) {
   const int tiles_m = static_cast<int>((M + BM - 1) / BM);
   const int tiles_n = static_cast<int>((N + BN - 1) / BN);
   if (exact_tma_ok(lda, ldb, A, B)) {  // TMA can describe both operands
     // 64x64 tiles while 128x128 ones would not give every SM two CTAs
     return tiles_m * tiles_n < 2 * L.num_sms
-               ? run_exact_tma<64, 64>(L, M, N, K, A, lda, B, ldb, C, ldc)
-               : run_exact_tma<128, 128>(L, M, N, K, A, lda, B, ldb, C, ldc);
+               ? run_exact_tma<64, 64>(L, M, N, K, A, lda, B, ldb, C, ldc, nullptr, nullptr, 0,
+                                       cin, ldcin)
+               : run_exact_tma<128, 128>(L, M, N, K, A, lda, B, ldb, C, ldc, nullptr, nullptr, 0,
+                                         cin, ldcin);
   }
   // 16-byte cp.async when a whole chunk is always in or out of the matrix
   const bool va = lda % 2 == 0 && K % 2 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0;
@@ -395,7 +424,8 @@ cudaError_t launch_dgemm_exact(const Launch& L, int64_t M, int64_t N, int64_t K,
   if (e != cudaSuccess) return e;
   kern<<<tiles_m * tiles_n, THREADS, SMEM, L.stream>>>(A, lda, B, ldb, C, ldc,
                                                        static_cast<int>(M), static_cast<int>(N),
-                                                       static_cast<int>(K), tiles_m, tiles_n);
+                                                       static_cast<int>(K), tiles_m, tiles_n,
+                                                       cin, ldcin);
   L.count();
   return cudaGetLastError();
 }

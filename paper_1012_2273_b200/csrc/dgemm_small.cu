@@ -26,8 +26,8 @@ constexpr int T = 32, BK = 32, THREADS = 256;
 template <bool EXACT>
 __global__ void __launch_bounds__(THREADS)
     dgemm_small_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
-                       int64_t ldb, double* __restrict__ C, int64_t ldc, int M, int N, int K,
-                       int tiles_n) {
+                       int64_t ldb, double* C, int64_t ldc, int M, int N, int K,
+                       int tiles_n, const double* cin, int64_t ldcin) {
   __shared__ __align__(16) double As[2][T][BK + 1];  // [row][k], +1 spreads the row starts
   __shared__ __align__(16) double Bs[2][BK][T];      // [k][col]
 
@@ -60,6 +60,15 @@ __global__ void __launch_bounds__(THREADS)
   };
 
   double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  if (cin) {  // accumulate: continue Cin's chains (Cin may alias C)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = row0 + ty * 2 + h, c = col0 + tx * 2 + e;
+        if (r < M && c < N) acc[h][e] = cin[static_cast<int64_t>(r) * ldcin + c];
+      }
+  }
   const int KT = (K + BK - 1) / BK;
   load(0);
   store(0);
@@ -102,13 +111,13 @@ __global__ void __launch_bounds__(THREADS)
 
 cudaError_t launch_dgemm_small(const Launch& L, bool exact, int64_t M, int64_t N, int64_t K,
                                const double* A, int64_t lda, const double* B, int64_t ldb,
-                               double* C, int64_t ldc) {
+                               double* C, int64_t ldc, const double* cin, int64_t ldcin) {
   const int tiles_m = static_cast<int>((M + T - 1) / T);
   const int tiles_n = static_cast<int>((N + T - 1) / T);
   auto kern = exact ? dgemm_small_kernel<true> : dgemm_small_kernel<false>;
   kern<<<tiles_m * tiles_n, THREADS, 0, L.stream>>>(A, lda, B, ldb, C, ldc, static_cast<int>(M),
                                                     static_cast<int>(N), static_cast<int>(K),
-                                                    tiles_n);
+                                                    tiles_n, cin, ldcin);
   L.count();
   return cudaGetLastError();
 }

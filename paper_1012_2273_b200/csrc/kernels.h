@@ -59,6 +59,10 @@ struct DmmaStream {
   // grid + 1 of each (slot b = the tile cut between CTAs b-1 and b)
   double* partial = nullptr;
   int* flags = nullptr;
+  // accumulate (one-shot launches): each tile's accumulators start from
+  // Cin instead of +0.0, so C = Cin + A.B continues Cin's DMMA chains
+  const double* cin = nullptr;
+  int64_t ldcin = 0;
 };
 // fp64 GEMM emulated on the int8 tensor cores (ozaki.cu): plan (moduli s,
 // integer bits t) for inner dimension k, workspace bytes, launch.  `aux` is a
@@ -123,9 +127,13 @@ cudaError_t launch_dgemm_dmma_stream(const Launch& L, int64_t M, int64_t N, int6
 
 // C[M,N] = A[M,K] . B[K,N], row-major, accumulators from +0.0.  The TMA path
 // needs lda, ldb even and A, B 16-byte aligned (the caller packs otherwise).
+// cin (optional): accumulate, C = Cin + A.B with every element's chain
+// continued from Cin (Cin may alias C); splitting K at multiples of 16 and
+// chaining launches gives bitwise the one-launch result.
 cudaError_t launch_dgemm_dmma(const Launch& L, int cfg, int64_t M, int64_t N, int64_t K,
                               const double* A, int64_t lda, const double* B, int64_t ldb,
-                              double* C, int64_t ldc);
+                              double* C, int64_t ldc, const double* cin = nullptr,
+                              int64_t ldcin = 0);
 
 // Exact-order SIMT: per element acc = +0.0; for j ascending acc = (acc + a*b)
 // with separate roundings -- bitwise equal to matmul_seq for every input.
@@ -138,20 +146,26 @@ cudaError_t launch_dgemm_exact_sk(const Launch& L, int tile, int64_t M, int64_t 
                                   double* C, int64_t ldc, double* partial, int* flags, int grid);
 cudaError_t launch_dgemm_exact(const Launch& L, int64_t M, int64_t N, int64_t K,
                                const double* A, int64_t lda, const double* B, int64_t ldb,
-                               double* C, int64_t ldc);
+                               double* C, int64_t ldc, const double* cin = nullptr,
+                               int64_t ldcin = 0);
 
 // Latency path: 32x32 tiles, plain loads, no TMA.  exact: DMUL+DADD chain
 // (bitwise matmul_seq); otherwise one DFMA per step.
 cudaError_t launch_dgemm_small(const Launch& L, bool exact, int64_t M, int64_t N, int64_t K,
                                const double* A, int64_t lda, const double* B, int64_t ldb,
-                               double* C, int64_t ldc);
+                               double* C, int64_t ldc, const double* cin = nullptr,
+                               int64_t ldcin = 0);
 
 // TMA-fed, warp-specialised FFMA2 fp32 GEMM with two-level (chunked)
 // accumulation (needs lda, ldb % 4 == 0 and 16-byte aligned A, B; the caller
 // packs other layouts).
 bool sgemm_tma_supported(int64_t lda, int64_t ldb, const float* A, const float* B);
+// cin (optional): accumulate, C = Cin + A.B -- the running totals start from
+// Cin; splitting K at multiples of 1024 (the partial-sum chunk) and chaining
+// launches gives bitwise the one-launch result.
 cudaError_t launch_sgemm_tma(const Launch& L, int64_t M, int64_t N, int64_t K, const float* A,
-                             int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc);
+                             int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
+                             const float* cin = nullptr, int64_t ldcin = 0);
 
 // Pad/pack src[rows, cols] (ld_src) into dst[rows_p, cols_p] (ld_dst), zero fill.
 cudaError_t launch_pack_f64(const Launch& L, const double* src, int64_t rows, int64_t cols,

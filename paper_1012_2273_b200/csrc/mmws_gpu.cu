@@ -151,8 +151,10 @@ int ozaki_streams(mmws_gpu_ctx* ctx) {
 
 int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
                    int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int mode,
-                   cudaStream_t stream) {
+                   cudaStream_t stream, const double* cin, int64_t ldcin) {
   if (int rc = check_dims(m, n, k, lda, ldb, ldc, A, B, C)) return rc;
+  if (cin && ldcin < n)
+    return fail(MMWS_GPU_ERR_DIMENSION, "matmul accumulate: leading dimension of Cin smaller than n");
   const Launch L = ctx->launch(stream);
   cudaError_t e;
   const int64_t tiles128 = ((m + 127) / 128) * ((n + 127) / 128);
@@ -171,7 +173,7 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(L.stream, &cap);
   const bool sk_ok = cap == cudaStreamCaptureStatusNone && !ctx->server && ctx->allow_streamk &&
-                     !ctx->tune.no_streamk;
+                     !ctx->tune.no_streamk && !cin;
   const bool sk = (mode == MMWS_GPU_MODE_DMMA || mode == MMWS_GPU_MODE_EXACT) && tiles128 >= G &&
                   tiles128 < 32 * G && sk_ok;
   // Exact order below one 128x128 tile per SM: stream-K over 64x64 tiles
@@ -222,7 +224,7 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
     // cp.async kernel for layouts TMA cannot read -- every variant gives
     // matmul_seq's bits
     if (n <= 256 && k <= 256) {
-      e = launch_dgemm_small(L, true, m, n, k, A, lda, B, ldb, C, ldc);
+      e = launch_dgemm_small(L, true, m, n, k, A, lda, B, ldb, C, ldc, cin, ldcin);
       ctx->last_plan = "dgemm_small_kernel<exact, 32x32>";
     } else if (sk || sk64) {
       if (int rc = sk_workspace(ctx, L.stream, &sk_partial, &sk_flags)) return rc;
@@ -232,7 +234,7 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
       ctx->last_plan = sk ? "dgemm_exact_tma_kernel<128x128, stream-K>"
                           : "dgemm_exact_tma_kernel<64x64, stream-K>";
     } else {
-      e = launch_dgemm_exact(L, m, n, k, A, lda, B, ldb, C, ldc);
+      e = launch_dgemm_exact(L, m, n, k, A, lda, B, ldb, C, ldc, cin, ldcin);
       ctx->last_plan = "dgemm_exact (one-shot)";
     }
     return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm exact");
@@ -240,6 +242,7 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
   if (mode == MMWS_GPU_MODE_OZAKI) {
     // fp64 emulated on the int8 tensor cores (ozaki.cu); inputs read with
     // plain loads, so any layout works without packing
+    if (cin) return fail(MMWS_GPU_ERR_DOMAIN, "matmul accumulate: not available in MODE_OZAKI");
     if (k > 131072)
       return fail(MMWS_GPU_ERR_DIMENSION, "dgemm ozaki: k must be <= 131072 (int32 accumulation)");
     void* wsp = nullptr;
@@ -260,7 +263,7 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
     // are faster (GPU time per call: N=128 6.1 vs 8.2 us, 200 6.2 vs 12.3,
     // 256 8.2 vs 13.4; tools/dmma_plan_probe.py); up to 96 it stays, so the
     // latency server (server.cu, N <= 96, same DFMA chain) matches AUTO
-    e = launch_dgemm_small(L, false, m, n, k, A, lda, B, ldb, C, ldc);
+    e = launch_dgemm_small(L, false, m, n, k, A, lda, B, ldb, C, ldc, cin, ldcin);
     ctx->last_plan = "dgemm_small_kernel<DFMA, 32x32>";
     return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm small");
   }
@@ -313,6 +316,8 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
                              G * 128 * 128)))
       return fail(MMWS_GPU_ERR_DOMAIN, std::string("MMWS_GPU_DMMA_PLAN not usable here: ") + plan);
   }
+  if (sk_grid > 0 && cin)
+    return fail(MMWS_GPU_ERR_DOMAIN, "matmul accumulate: stream-K plans do not take Cin");
   if (sk_grid > 0) {
     if (int rc = sk_workspace(ctx, L.stream, &sk_partial, &sk_flags)) return rc;
     e = launch_dgemm_dmma_sk(L, cfg, m, n, k, A, lda, B, ldb, C, ldc, sk_partial, sk_flags,
@@ -320,18 +325,22 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
     ctx->last_plan = dmma_plan_name(cfg, 1);
     return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm stream-K");
   }
-  e = launch_dgemm_dmma(L, cfg, m, n, k, A, lda, B, ldb, C, ldc);
+  e = launch_dgemm_dmma(L, cfg, m, n, k, A, lda, B, ldb, C, ldc, cin, ldcin);
   ctx->last_plan = dmma_plan_name(cfg, 0);
   return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm dmma");
 }
 
 int sgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const float* A,
                    int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int mode,
-                   cudaStream_t stream) {
+                   cudaStream_t stream, const float* cin, int64_t ldcin) {
   if (int rc = check_dims(m, n, k, lda, ldb, ldc, A, B, C)) return rc;
+  if (cin && ldcin < n)
+    return fail(MMWS_GPU_ERR_DIMENSION, "matmul accumulate: leading dimension of Cin smaller than n");
   if (mode != MMWS_GPU_MODE_AUTO && mode != MMWS_GPU_MODE_FFMA && mode != MMWS_GPU_MODE_OZAKI)
     return fail(MMWS_GPU_ERR_DOMAIN, "sgemm: unknown mode " + std::to_string(mode));
   const Launch L = ctx->launch(stream);
+  if (mode == MMWS_GPU_MODE_OZAKI && cin)
+    return fail(MMWS_GPU_ERR_DOMAIN, "matmul accumulate: not available in MODE_OZAKI");
   if (mode == MMWS_GPU_MODE_OZAKI) {  // fp32 through the int8 tensor-core scheme (ozaki.cu)
     if (k > 131072)
       return fail(MMWS_GPU_ERR_DIMENSION, "sgemm ozaki: k must be <= 131072 (int32 accumulation)");
@@ -371,7 +380,7 @@ int sgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const flo
       ldb = ldb_p;
     }
   }
-  e = launch_sgemm_tma(L, m, n, k, A, lda, B, ldb, C, ldc);
+  e = launch_sgemm_tma(L, m, n, k, A, lda, B, ldb, C, ldc, cin, ldcin);
   ctx->last_plan = "sgemm_tma_kernel<128x256, FFMA2>";
   return e == cudaSuccess ? ok() : cuda_fail(e, "sgemm ffma");
 }
@@ -631,6 +640,24 @@ int mmws_gpu_sgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const flo
   MMWS_CTX_GUARD(ctx);
   return sgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode,
                         static_cast<cudaStream_t>(stream));
+}
+
+int mmws_gpu_dgemm_acc(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
+                       int64_t lda, const double* B, int64_t ldb, const double* Cin,
+                       int64_t ldcin, double* C, int64_t ldc, int mode, void* stream) {
+  MMWS_CTX_GUARD(ctx);
+  if (!Cin) return fail(MMWS_GPU_ERR_DOMAIN, "dgemm_acc: null Cin");
+  return dgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode,
+                        static_cast<cudaStream_t>(stream), Cin, ldcin);
+}
+
+int mmws_gpu_sgemm_acc(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const float* A,
+                       int64_t lda, const float* B, int64_t ldb, const float* Cin, int64_t ldcin,
+                       float* C, int64_t ldc, int mode, void* stream) {
+  MMWS_CTX_GUARD(ctx);
+  if (!Cin) return fail(MMWS_GPU_ERR_DOMAIN, "sgemm_acc: null Cin");
+  return sgemm_dispatch(ctx, m, n, k, A, lda, B, ldb, C, ldc, mode,
+                        static_cast<cudaStream_t>(stream), Cin, ldcin);
 }
 
 int mmws_gpu_ozaki_plan(int64_t k, int* moduli, int* bits) {

@@ -63,8 +63,9 @@ constexpr int SMEM = STAGES * STAGE_BYTES + TOT_BYTES + 2 * STAGES * 8 + 128;
 
 __global__ void __launch_bounds__(THREADS, 1)
     sgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA,
-                     const __grid_constant__ CUtensorMap tmB, float* __restrict__ C, int64_t ldc,
-                     int M, int N, int K, int tiles_m, int tiles_n, int vec_c) {
+                     const __grid_constant__ CUtensorMap tmB, float* C, int64_t ldc,
+                     int M, int N, int K, int tiles_m, int tiles_n, int vec_c, const float* cin,
+                     int64_t ldcin) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   float4* tot = reinterpret_cast<float4*>(smem + STAGES * STAGE_BYTES);
@@ -116,6 +117,22 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 #pragma unroll
   for (int q = 0; q < 32; ++q) tot[q * 256 + tid] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (cin) {  // accumulate: the running totals start from Cin (the epilogue's layout)
+#pragma unroll 4
+    for (int q = 0; q < 32; ++q) {
+      const int i = q >> 2, j = q & 3;
+      const int r = tm * BM + row_base + i;
+      if (r >= M) continue;
+      const int col = tn * BN + c * 4 + 64 * j;
+      const float* crow = cin + static_cast<int64_t>(r) * ldcin;
+      float4 t;
+      t.x = col + 0 < N ? crow[col + 0] : 0.f;
+      t.y = col + 1 < N ? crow[col + 1] : 0.f;
+      t.z = col + 2 < N ? crow[col + 2] : 0.f;
+      t.w = col + 3 < N ? crow[col + 3] : 0.f;
+      tot[q * 256 + tid] = t;
+    }
+  }
 
   f32x2 part[8][8];  // [row i][pair p]: columns c*4 + 64*(p>>1) + 2*(p&1) + {0,1}
 #pragma unroll
@@ -217,7 +234,8 @@ bool sgemm_tma_supported(int64_t lda, int64_t ldb, const float* A, const float* 
 }
 
 cudaError_t launch_sgemm_tma(const Launch& L, int64_t M, int64_t N, int64_t K, const float* A,
-                             int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc) {
+                             int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
+                             const float* cin, int64_t ldcin) {
   CUtensorMap ta, tb;
   if (!make_map_f32(L, &ta, A, K, M, lda, BK, BM)) return cudaErrorInvalidValue;
   if (!make_map_f32(L, &tb, B, N, K, ldb, BN, BK)) return cudaErrorInvalidValue;
@@ -229,7 +247,7 @@ cudaError_t launch_sgemm_tma(const Launch& L, int64_t M, int64_t N, int64_t K, c
   const int vec_c = (ldc % 4 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0);
   sgemm_tma_kernel<<<tiles_m * tiles_n, THREADS, SMEM, L.stream>>>(
       ta, tb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), tiles_m,
-      tiles_n, vec_c);
+      tiles_n, vec_c, cin, ldcin);
   L.count();
   return cudaGetLastError();
 }

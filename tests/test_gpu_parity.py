@@ -947,3 +947,57 @@ def test_tuning_knobs_apply_on_a_live_context(ctx):
     ctx.tune("MMWS_GPU_NO_STREAMK", None)
     ctx.dgemm(A, B, mode=P.MODE_DMMA)
     assert "stream-K" in ctx.last_plan
+
+
+@pytest.mark.parametrize("mode,shape,cuts", [
+    (P.MODE_AUTO, (1000, 777, 2048), (512, 1024)),
+    (P.MODE_DMMA, (1000, 777, 2048), (16, 1040)),
+    (P.MODE_DMMA_SMALL, (257, 300, 800), (400,)),
+    (P.MODE_EXACT, (257, 300, 800), (16, 32, 784)),
+    (P.MODE_EXACT, (1500, 1100, 1600), (800,)),
+    (P.MODE_AUTO, (4099, 1000, 4099), (2048,)),
+])
+def test_accumulate_in_k_panels_is_bitwise_one_call(ctx, oracle, mode, shape, cuts):
+    # mmws_gpu_dgemm_acc: C = Cin + A.B continues Cin's chains, so a K split
+    # at multiples of 16 chained through the accumulator reproduces the
+    # one-call bits (what the row-block workers do while B is arriving)
+    T = torch()
+    m, n, k = shape
+    A = ctx.fill(P.DIST_UNIFORM, 81, m, k)
+    B = ctx.fill(P.DIST_UNIFORM, 82, k, n)
+    want = host(ctx.dgemm(A, B, mode=mode))
+    edges = (0,) + tuple(cuts) + (k,)
+    C = T.empty((m, n), dtype=T.float64, device="cuda")
+    ctx.dgemm(A[:, :edges[1]], B[:edges[1]], C, mode=mode)
+    for k0, k1 in zip(edges[1:-1], edges[2:]):
+        ctx.dgemm(A[:, k0:k1], B[k0:k1], C, mode=mode, accumulate=C)   # in place
+    assert (bits(host(C)) == bits(want)).all(), (mode, shape, cuts)
+    # out of place: Cin untouched, C = Cin + A.B
+    Cin = T.empty_like(C)
+    ctx.dgemm(A[:, :edges[-2]], B[:edges[-2]], Cin, mode=mode)
+    keep = host(Cin)
+    C2 = T.full_like(C, float("nan"))
+    ctx.dgemm(A[:, edges[-2]:], B[edges[-2]:], C2, mode=mode, accumulate=Cin)
+    assert (bits(host(C2)) == bits(want)).all()
+    assert (bits(host(Cin)) == bits(keep)).all()
+    if mode == P.MODE_EXACT:
+        rows = [0, m // 2, m - 1]
+        assert (bits(want[rows]) == bits(oracle.matmul_rows(rows, host(A), host(B)))).all()
+
+
+def test_accumulate_fp32_chunks_and_limits(ctx):
+    T = torch()
+    m, n, k = 700, 900, 3072
+    A = ctx.fill(P.DIST_NORMAL, 91, m, k, dtype=T.float32)
+    B = ctx.fill(P.DIST_NORMAL, 92, k, n, dtype=T.float32)
+    want = host(ctx.sgemm(A, B))
+    C = ctx.sgemm(A[:, :1024], B[:1024])
+    ctx.sgemm(A[:, 1024:], B[1024:], C, accumulate=C)       # split at the 1024-k chunk
+    assert (host(C).view(np.int32) == want.view(np.int32)).all()
+    Ad = A.double()
+    Bd = B.double()
+    with pytest.raises(P.DomainError):
+        ctx.dgemm(Ad, Bd, mode=P.MODE_OZAKI, accumulate=T.zeros((m, n), dtype=T.float64,
+                                                                 device="cuda"))
+    with pytest.raises(P.DimensionError):
+        ctx.dgemm(Ad, Bd, accumulate=T.zeros((m - 1, n), dtype=T.float64, device="cuda"))
