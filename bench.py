@@ -432,6 +432,7 @@ def run_ours(args) -> None:
     clocks = sampler.stop() if sampler else None
     plan = ctx.last_plan
     active, gather = ctx.last_round
+    b_panels = ctx.last_b_panels
     per_rank = gather_all([ms, float(launches), sum(kern_ms) / len(kern_ms)])
     ms_max = max(r[0] for r in per_rank)
     launches_total = int(sum(r[1] for r in per_rank))
@@ -544,7 +545,7 @@ def run_ours(args) -> None:
             "data": DATA, "config": workload_config(n, world, args.mode),
             "per_rank_ms_per_step": [r[0] / args.steps for r in per_rank],
             "per_rank_kernel_ms": [r[2] for r in per_rank],
-            "round": {"active_ranks": active, "gather": gather,
+            "round": {"active_ranks": active, "gather": gather, "b_panels": b_panels,
                       "rows_rank0": rows0, "plan_rank0": plan},
             "roofline": {
                 "bound": "tensor", "achieved": achieved, "peak": dmma_peak, "unit": "TFLOP/s",
@@ -684,7 +685,7 @@ def measure_fp32(ctx, P, torch, dist, args, rank, world, local, barrier, gather_
             "warmup": 1, "ms_per_step": ms_max / steps, "dtype": "f32",
             "per_rank_ms_per_step": [r[0] / steps for r in per_rank],
             "round": {"active_ranks": active, "gather": gather, "rows_rank0": rows0,
-                      "plan_rank0": plan},
+                      "b_panels": ctx.last_b_panels, "plan_rank0": plan},
             "roofline": {"bound": "fp32 pipe (FFMA2)", "achieved": achieved, "peak": ffma2_peak,
                          "unit": "TFLOP/s", "frac": achieved / ffma2_peak, "traffic": traffic,
                          "traffic_source": traffic_src, "kernel_ms_avg": kern_ms,

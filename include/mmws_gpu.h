@@ -286,10 +286,12 @@ int mmws_gpu_master_run_host_f32(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_
                                  const float* A, const float* B, float* C, int mode,
                                  double* elapsed_s);
 /* The most recent row-block / master_run call: how many ranks multiplied
- * (1 = rank 0 alone or no communicator) and how C came back: 0 no exchange,
- * 1 fused (worker GEMM epilogues stored into rank 0's C over CUDA IPC),
- * 2 NCCL C-slice messages. */
-int mmws_gpu_last_round(mmws_gpu_ctx* ctx, int* active_ranks, int* gather);
+ * (1 = rank 0 alone or no communicator), how C came back (0 no exchange,
+ * 1 fused: worker GEMM epilogues stored into rank 0's C over CUDA IPC,
+ * 2 NCCL C-slice messages) and in how many k-panels B was broadcast (> 1:
+ * workers multiplied their first rows panel by panel as B landed).  Any
+ * output may be NULL. */
+int mmws_gpu_last_round(mmws_gpu_ctx* ctx, int* active_ranks, int* gather, int* b_panels);
 /* Deadline of one distributed step (communicator bootstrap, a round, a probe):
  * default 30 s (the reference's receive timeout, comm.hpp:144), or
  * MMWS_GPU_TIMEOUT_S at mmws_gpu_init.  When it passes -- or NCCL reports a

@@ -60,7 +60,7 @@ SIGNATURES = {
     "mmws_gpu_gemm_probe": (_i, [_v, _i64, _i, _i, _p(_d)]),
     "mmws_gpu_link_probe": (_i, [_v, _i64, _i, _p(_d)]),
     "mmws_gpu_p2p_probe": (_i, [_v, _i64, _i, _p(_d)]),
-    "mmws_gpu_last_round": (_i, [_v, _p(_i), _p(_i)]),
+    "mmws_gpu_last_round": (_i, [_v, _p(_i), _p(_i), _p(_i)]),
     "mmws_gpu_set_timeout": (_i, [_v, _d]),
     "mmws_gpu_nccl_unique_id": (_i, [_p(C.c_uint8)]),
     "mmws_gpu_comm_init": (_i, [_v, _i, _i, _p(C.c_uint8)]),

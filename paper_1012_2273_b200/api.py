@@ -379,8 +379,15 @@ class Context:
         """(ranks that multiplied, gather) of the latest row-block call;
         gather in {"none", "fused-ipc", "nccl"}."""
         act, g = C.c_int(), C.c_int()
-        _check(_lib().mmws_gpu_last_round(self._h, C.byref(act), C.byref(g)))
+        _check(_lib().mmws_gpu_last_round(self._h, C.byref(act), C.byref(g), None))
         return act.value, {0: "none", 1: "fused-ipc", 2: "nccl"}[g.value]
+
+    @property
+    def last_b_panels(self) -> int:
+        """k-panels B was broadcast in during the latest row-block call."""
+        p = C.c_int()
+        _check(_lib().mmws_gpu_last_round(self._h, None, None, C.byref(p)))
+        return p.value
 
     # -- row-block distribution
     def comm_init(self, nranks: int, rank: int, uid: bytes) -> None:

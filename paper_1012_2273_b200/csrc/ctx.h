@@ -102,7 +102,8 @@ struct mmws_gpu_ctx {
   void* rbA = nullptr;  // worker-side A slice / B copy / C slice
   void* rbB = nullptr;
   void* rbC = nullptr;
-  size_t rbA_bytes = 0, rbB_bytes = 0, rbC_bytes = 0;
+  void* rbAcc = nullptr;  // worker: running accumulators of its first sub-block (B in panels)
+  size_t rbA_bytes = 0, rbB_bytes = 0, rbC_bytes = 0, rbAcc_bytes = 0;
   // failure detection (rowblock.cu): every rank stores its progress through
   // each round into rank 0's board, one word per rank (round * 8 + stage)
   unsigned* board = nullptr;       // rank 0: the board (device memory, IPC-exported)
@@ -111,6 +112,7 @@ struct mmws_gpu_ctx {
   bool comm_failed = false;        // a round timed out / a peer failed: communicator aborted
   int last_gather = 0;             // last round: 0 one GPU, 1 fused IPC stores, 2 NCCL C-slices
   int last_active = 1;             // last round: ranks that multiplied
+  int last_panels = 1;             // last round: B broadcast in this many k-panels
 
   mmws_impl::Launch launch(cudaStream_t s) {
     mmws_impl::Launch L;

@@ -538,7 +538,7 @@ int mmws_gpu_destroy(mmws_gpu_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->comm && nccl().ok) nccl().CommDestroy(ctx->comm);
   for (auto& mp : ctx->ipc_cache) cudaIpcCloseMemHandle(mp.base);
-  for (void* p : {ctx->ws, ctx->dA, ctx->dB, ctx->dC, ctx->rbA, ctx->rbB, ctx->rbC, ctx->sched,
+  for (void* p : {ctx->ws, ctx->dA, ctx->dB, ctx->dC, ctx->rbA, ctx->rbB, ctx->rbC, ctx->rbAcc, ctx->sched,
                   ctx->ipc_stage, static_cast<void*>(ctx->board),
                   static_cast<void*>(ctx->sink)})
     if (p) cudaFree(p);

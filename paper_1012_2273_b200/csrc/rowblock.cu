@@ -193,13 +193,27 @@ int settle(mmws_gpu_ctx* ctx, ncclResult_t r, const char* what) {
 // are needed.  S = 2 for the big configs: each sub-block is a whole number of
 // 128-row bands, so a sub-block launch loses <2% to wave quantisation on 148
 // SMs while half of the C gather hides behind the second multiply.
+//
+// B in k-panels (KP > 1, big rounds): B goes out as KP broadcasts of row
+// panels of B (contiguous in row-major B), after the workers' first A
+// sub-blocks, and a worker multiplies its first sub-block panel by panel as
+// they land -- each launch continuing the previous one's accumulators
+// (mmws_gpu_dgemm_acc semantics: bitwise the one-launch result, panel edges
+// at multiples of 1024 k) -- instead of waiting for all of B (2 GiB at
+// N=16384 fp64: ~3 ms of NVLink before any worker could start).
 struct Schedule {
-  int P = 1, S = 1;
+  int P = 1, S = 1, KP = 1;
   std::vector<int64_t> off, rows;
   std::vector<std::vector<int64_t>> soff, srows;  // [rank][sub-block], offsets within the rank
+  std::vector<int64_t> kb;                        // B panel edges: KP + 1 entries, 0 .. k
 };
 
-Schedule make_schedule(int64_t m, int P) {
+constexpr int64_t PANEL_ELEMS = int64_t{32} << 20;  // 256 MiB of fp64 per B panel
+constexpr int64_t PANEL_QUANTUM = 1024;              // fp32's partial-sum chunk (and 64 fp64 k-tiles)
+constexpr int MAX_PANELS = 8;
+
+// panels: the mode can continue accumulators across launches (all but OZAKI)
+Schedule make_schedule(int64_t m, int64_t n, int64_t k, int P, bool panels) {
   Schedule sc;
   sc.P = P;
   sc.off.resize(P);
@@ -210,6 +224,17 @@ Schedule make_schedule(int64_t m, int P) {
   sc.srows.assign(P, std::vector<int64_t>(sc.S));
   for (int r = 0; r < P; ++r)
     mmws_gpu_split_rows(sc.rows[r], sc.S, sc.soff[r].data(), sc.srows[r].data());
+  sc.kb = {0};
+  const double b_elems = static_cast<double>(k) * n;
+  if (P > 1 && panels && b_elems >= 2.0 * PANEL_ELEMS) {
+    const int want = static_cast<int>(std::min<double>(MAX_PANELS, b_elems / PANEL_ELEMS));
+    for (int j = 1; j < want; ++j) {
+      const int64_t e = (k * j / want) / PANEL_QUANTUM * PANEL_QUANTUM;
+      if (e > sc.kb.back() && e < k) sc.kb.push_back(e);
+    }
+  }
+  sc.kb.push_back(k);
+  sc.KP = static_cast<int>(sc.kb.size()) - 1;
   return sc;
 }
 
@@ -314,20 +339,23 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
     ~NoStreamK() { c->allow_streamk = true; }
   } no_sk{ctx};
   ctx->allow_streamk = false;
-  const Schedule sc = make_schedule(m, P);
-  const int S = sc.S;
+  const Schedule sc = make_schedule(m, n, k, P, mode != MMWS_GPU_MODE_OZAKI);
+  const int S = sc.S, KP = sc.KP;
   const auto& off = sc.off;
   const auto& rows = sc.rows;
   const auto& soff = sc.soff;
   const auto& srows = sc.srows;
+  const auto& kb = sc.kb;
   const ncclDataType_t dt = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
   ++ctx->round;
   ctx->last_active = P;
+  ctx->last_panels = KP;
 
-  if ((e = event_pool(ctx, 2 * S + 5)) != cudaSuccess) return cuda_fail(e, "rowblock: events");
+  if ((e = event_pool(ctx, 2 * S + KP + 4)) != cudaSuccess) return cuda_fail(e, "rowblock: events");
   cudaEvent_t* evA = ctx->pool.data() + 1;
   cudaEvent_t* evC = evA + S;
-  cudaEvent_t evB = evC[S], evStart = evC[S + 1], evJoin = evC[S + 2], evHost = evC[S + 3];
+  cudaEvent_t* evBp = evC + S;  // B panel j has landed
+  cudaEvent_t evStart = evBp[KP], evJoin = evBp[KP + 1], evHost = evBp[KP + 2];
 
   // the exchange starts after everything already queued on the compute stream
   // (e.g. the H2D copies of master_run_host)
@@ -396,13 +424,21 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
     c_loc = fused ? c_peer + off[me] * n : static_cast<T*>(ctx->rbC);
   }
   T* c_dst = c_loc;  // rank 0: C; workers: rank 0's C (fused) or the local slice
+  // worker's running accumulators of its first sub-block while B's panels land
+  T* acc0 = nullptr;
+  if (me != 0 && KP > 1 && srows[me][0] > 0) {
+    if ((e = ensure(ctx, &ctx->rbAcc, &ctx->rbAcc_bytes, sizeof(T) * srows[me][0] * n)) !=
+        cudaSuccess)
+      return cuda_fail(e, "rowblock: worker accumulators");
+    acc0 = static_cast<T*>(ctx->rbAcc);
+  }
 
-  // ---- comm stream, part 1: all of B (protocol.hpp:73), once, as a broadcast ...
-  void* bbuf = as_mut(b_loc);
-  NCCL_TRY(nccl().Broadcast(bbuf, bbuf, k * n, dt, 0, ctx->comm, comm), "broadcast B");
-  cudaEventRecord(evB, comm);
-  // ... then the A-slices (protocol.hpp:70-72), sub-block by sub-block
-  for (int s = 0; s < S; ++s) {
+  // ---- comm stream, part 1: the A-slices (protocol.hpp:70-72) sub-block by
+  // sub-block and all of B (protocol.hpp:73) as KP panel broadcasts.  One
+  // panel: B first (nothing can finish without all of it), then the A
+  // sub-blocks.  Several: the first A sub-blocks, the panels, the other A
+  // sub-blocks -- a worker starts once its first rows and panel 0 are in.
+  auto send_a = [&](int s) -> int {
     NCCL_TRY(nccl().GroupStart(), "ncclGroupStart");
     if (me == 0) {
       for (int r = 1; r < P; ++r)
@@ -415,19 +451,43 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
     }
     NCCL_TRY(nccl().GroupEnd(), "ncclGroupEnd");
     cudaEventRecord(evA[s], comm);
+    return MMWS_GPU_OK;
+  };
+  if (KP > 1)
+    if (int rc = send_a(0)) return rc;
+  for (int j = 0; j < KP; ++j) {
+    T* bp = as_mut(b_loc) + kb[j] * n;
+    NCCL_TRY(nccl().Broadcast(bp, bp, (kb[j + 1] - kb[j]) * n, dt, 0, ctx->comm, comm),
+             "broadcast B");
+    cudaEventRecord(evBp[j], comm);
   }
+  for (int s = KP > 1 ? 1 : 0; s < S; ++s)
+    if (int rc = send_a(s)) return rc;
   mark(ctx, comm, INPUTS);
 
   // ---- compute stream: this rank's rows (worker_run's body, protocol.hpp:132-141)
   cudaEventRecord(ctx->evk0, comp);
-  if (me != 0) cudaStreamWaitEvent(comp, evB, 0);
   for (int s = 0; s < S; ++s) {
     const int64_t r0 = soff[me][s], rs = srows[me][s];
     if (me != 0) cudaStreamWaitEvent(comp, evA[s], 0);
-    if (rs > 0)
-      if (int rc = gemm<T>(ctx, rs, n, k, a_loc + r0 * k, k, b_loc, n, c_dst + r0 * n, n, mode,
-                           comp))
-        return rc;
+    if (me != 0 && s == 0 && KP > 1) {
+      // panel by panel as B lands: launch j continues launch j-1's
+      // accumulators (acc0), the last one stores into the destination
+      for (int j = 0; j < KP; ++j) {
+        cudaStreamWaitEvent(comp, evBp[j], 0);
+        if (rs == 0) continue;
+        T* out = j + 1 < KP ? acc0 : c_dst + r0 * n;
+        if (int rc = gemm<T>(ctx, rs, n, kb[j + 1] - kb[j], a_loc + r0 * k + kb[j], k,
+                             b_loc + kb[j] * n, n, out, n, mode, comp, j ? acc0 : nullptr, n))
+          return rc;
+      }
+    } else {
+      if (me != 0) cudaStreamWaitEvent(comp, evBp[KP - 1], 0);  // all of B
+      if (rs > 0)
+        if (int rc = gemm<T>(ctx, rs, n, k, a_loc + r0 * k, k, b_loc, n, c_dst + r0 * n, n, mode,
+                             comp))
+          return rc;
+    }
     if (s == S - 1) {
       cudaEventRecord(ctx->evk1, comp);
       mark(ctx, comp, MULTIPLIED);  // before evC: the DONE mark below waits on it
@@ -783,10 +843,11 @@ int mmws_gpu_p2p_probe(mmws_gpu_ctx* ctx, int64_t bytes, int iters, double* byte
   return ok();
 }
 
-int mmws_gpu_last_round(mmws_gpu_ctx* ctx, int* active_ranks, int* gather) {
+int mmws_gpu_last_round(mmws_gpu_ctx* ctx, int* active_ranks, int* gather, int* b_panels) {
   if (!ctx) return fail(MMWS_GPU_ERR_STATE, "null mmws_gpu_ctx");
   if (active_ranks) *active_ranks = ctx->last_active;
   if (gather) *gather = ctx->last_gather;
+  if (b_panels) *b_panels = ctx->last_gather ? ctx->last_panels : 1;
   return ok();
 }
 
@@ -804,28 +865,53 @@ int mmws_gpu_rowblock_cost(int64_t m, int64_t n, int64_t k, int nranks, int elem
   // s3.1.1: ((P-1)N^2 + 2N)(tc + tf) datums through the master) for this
   // schedule.  Rank 0's NVLink egress carries B once (broadcast) plus the
   // workers' A rows; its ingress carries the workers' C rows (peer stores).
-  // Time = B broadcast + the largest first A sub-block + the slowest rank's
-  // multiply; the C rows land while tiles finish (fused gather), so there is
-  // no gather tail.  Per-op latencies are ignored (microseconds vs ms).
+  // Time = the slowest rank, a worker's multiplies starting as their inputs
+  // arrive through rank 0's link in issue order (B in panels where the round
+  // uses them); the C rows land while tiles finish (fused gather), so there
+  // is no gather tail.  Per-op latencies are ignored (microseconds vs ms).
   if (m <= 0 || n <= 0 || k <= 0)
     return fail(MMWS_GPU_ERR_DIMENSION, "rowblock_cost: dimensions must be positive");
   if (nranks < 1 || (elem_bytes != 4 && elem_bytes != 8) || !(link_bytes_per_s > 0) ||
       !(gemm_flops_per_s > 0))
     return fail(MMWS_GPU_ERR_DOMAIN, "rowblock_cost: bad nranks / element size / rates");
-  const Schedule sc = make_schedule(m, nranks);
-  const double eb = elem_bytes;
-  int64_t rows_max = 0, a_rows = 0, a0_max = 0;
-  for (int r = 0; r < nranks; ++r) {
-    rows_max = std::max(rows_max, sc.rows[r]);
-    if (r > 0) {
-      a_rows += sc.rows[r];
-      a0_max = std::max(a0_max, sc.srows[r][0]);
-    }
-  }
+  const Schedule sc = make_schedule(m, n, k, nranks, true);
+  const double eb = elem_bytes, link = link_bytes_per_s, rate = gemm_flops_per_s;
+  int64_t a_rows = 0;
+  for (int r = 1; r < nranks; ++r) a_rows += sc.rows[r];
   const double egress = nranks > 1 ? eb * (static_cast<double>(k) * n + static_cast<double>(a_rows) * k) : 0.0;
   const double ingress = nranks > 1 ? eb * static_cast<double>(a_rows) * n : 0.0;
-  double t = 2.0 * static_cast<double>(rows_max) * n * k / gemm_flops_per_s;
-  if (nranks > 1) t += eb * (static_cast<double>(k) * n + static_cast<double>(a0_max) * k) / link_bytes_per_s;
+  // rank 0 alone, then (P > 1) each worker on the arrival times of rank 0's
+  // egress sequence: [A sub-block 0 | B panels | A sub-blocks 1..] or, with
+  // one panel, [B | A sub-blocks] -- rank 0's link carries them one after
+  // another; the C rows land as tiles finish (fused gather)
+  double t = 2.0 * static_cast<double>(sc.rows[0]) * n * k / rate;
+  if (nranks > 1) {
+    auto a_bytes = [&](int s) {
+      double b = 0;
+      for (int r = 1; r < nranks; ++r) b += eb * static_cast<double>(sc.srows[r][s]) * k;
+      return b;
+    };
+    std::vector<double> t_a(sc.S), t_b(sc.KP);
+    double sent = 0;
+    if (sc.KP > 1) t_a[0] = (sent += a_bytes(0)) / link;
+    for (int j = 0; j < sc.KP; ++j)
+      t_b[j] = (sent += eb * static_cast<double>(sc.kb[j + 1] - sc.kb[j]) * n) / link;
+    for (int s = sc.KP > 1 ? 1 : 0; s < sc.S; ++s) t_a[s] = (sent += a_bytes(s)) / link;
+    for (int r = 1; r < nranks; ++r) {
+      double tw = 0;
+      for (int s = 0; s < sc.S; ++s) {
+        const double rs = static_cast<double>(sc.srows[r][s]);
+        if (s == 0 && sc.KP > 1) {
+          tw = std::max(tw, t_a[0]);
+          for (int j = 0; j < sc.KP; ++j)
+            tw = std::max(tw, t_b[j]) + 2.0 * rs * n * (sc.kb[j + 1] - sc.kb[j]) / rate;
+        } else {
+          tw = std::max(tw, std::max(t_a[s], t_b[sc.KP - 1])) + 2.0 * rs * n * k / rate;
+        }
+      }
+      t = std::max(t, tw);
+    }
+  }
   if (seconds) *seconds = t;
   if (root_egress_bytes) *root_egress_bytes = egress;
   if (root_ingress_bytes) *root_ingress_bytes = ingress;
@@ -850,15 +936,19 @@ int mmws_gpu_rowblock_plan(int64_t m, int64_t n, int64_t k, int nranks, int32_t*
   if (m <= 0 || n <= 0 || k <= 0)
     return fail(MMWS_GPU_ERR_DIMENSION, "rowblock_plan: dimensions must be positive");
   if (nranks < 1) return fail(MMWS_GPU_ERR_DOMAIN, "rowblock_plan: nranks must be >= 1");
-  const Schedule sc = make_schedule(m, nranks);
+  const Schedule sc = make_schedule(m, n, k, nranks, true);
   struct E { int32_t peer, tag, kind; int64_t count, row0; int32_t dir; };
   std::vector<E> plan;  // the order rowblock_enqueue issues on rank 0
   if (nranks > 1) {
-    plan.push_back({-1, 1, 1, k * n, -1, 2});
-    for (int s = 0; s < sc.S; ++s)
+    auto sends = [&](int s) {
       for (int r = 1; r < nranks; ++r)
         if (sc.srows[r][s] > 0)
           plan.push_back({r, 1, 1, sc.srows[r][s] * k, sc.off[r] + sc.soff[r][s], 0});
+    };
+    if (sc.KP > 1) sends(0);
+    for (int j = 0; j < sc.KP; ++j)  // B panel j: rows [kb_j, kb_j+1) of B
+      plan.push_back({-1, 1, 1, (sc.kb[j + 1] - sc.kb[j]) * n, sc.KP > 1 ? sc.kb[j] : -1, 2});
+    for (int s = sc.KP > 1 ? 1 : 0; s < sc.S; ++s) sends(s);
     for (int s = 0; s < sc.S; ++s)
       for (int r = 1; r < nranks; ++r)
         if (sc.srows[r][s] > 0)

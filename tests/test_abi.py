@@ -100,11 +100,19 @@ def test_rowblock_plan_shape():
     assert [e["peer"] for e in plan if e["dir"] == "sent"] == [1]
     assert P.rowblock_plan(7, 7, 7, 1) == []
     # N=16384 over 8 GPUs: two sub-blocks per rank; A and C slices tile rows
-    # 2048..16383 exactly once each, B goes out once
+    # 2048..16383 exactly once each; B goes out once, as 8 k-panels (row
+    # panels of B, edges at multiples of 1024) after the first A sub-blocks
     m, n, k, world = 16384, 16384, 16384, 8
     plan = P.rowblock_plan(m, n, k, world)
     rows0 = P.split_rows(m, world)[0][1]
-    assert [e["dir"] for e in plan].count("broadcast") == 1
+    dirs = [e["dir"] for e in plan]
+    first_b = dirs.index("broadcast")
+    assert dirs[:first_b] == ["sent"] * (world - 1)              # A sub-block 0 of every worker
+    panels = [(e["row0"], e["row0"] + e["count"] // n) for e in plan if e["dir"] == "broadcast"]
+    assert len(panels) == 8 and panels[0][0] == 0 and panels[-1][1] == k
+    assert all(a[1] == b[0] for a, b in zip(panels, panels[1:]))
+    assert all(lo % 1024 == 0 for lo, _ in panels)
+    assert dirs[first_b:first_b + 8] == ["broadcast"] * 8
     for d, width in (("sent", k), ("received", n)):
         spans = sorted((e["row0"], e["row0"] + e["count"] // width) for e in plan if e["dir"] == d)
         assert len(spans) == 2 * (world - 1)

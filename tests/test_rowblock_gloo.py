@@ -27,6 +27,14 @@ def _free_port():
     return port
 
 
+def _b_span(e, k, n):
+    """Elements of B a broadcast entry covers: all of it (row0 -1) or the
+    k-panel of rows [row0, row0 + count / n)."""
+    lo = 0 if e["row0"] < 0 else e["row0"] * n
+    assert e["count"] % n == 0 and lo + e["count"] <= k * n
+    return slice(lo, lo + e["count"])
+
+
 def _rank_main(rank, world, port, cases, failures):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -51,9 +59,8 @@ def _rank_main(rank, world, port, cases, failures):
                 if rows:
                     c[off:off + rows] = O.worker_block(a[off:off + rows], b)
                 for e in plan:
-                    if e["dir"] == "broadcast":
-                        assert e["count"] == k * n
-                        dist.broadcast(torch.from_numpy(b), 0)
+                    if e["dir"] == "broadcast":                # B, or one k-panel of it
+                        dist.broadcast(torch.from_numpy(b).reshape(-1)[_b_span(e, k, n)], 0)
                     elif e["dir"] == "sent":               # tag 1: A sub-slice
                         r0, nr = e["row0"], e["count"] // k
                         dist.send(torch.from_numpy(np.ascontiguousarray(a[r0:r0 + nr])), e["peer"])
@@ -73,7 +80,7 @@ def _rank_main(rank, world, port, cases, failures):
                 b = torch.empty((k, n), dtype=torch.float64)
                 for e in plan:
                     if e["dir"] == "broadcast":
-                        dist.broadcast(b, 0)
+                        dist.broadcast(b.reshape(-1)[_b_span(e, k, n)], 0)
                     elif e["peer"] != rank:
                         continue
                     elif e["dir"] == "sent":
@@ -101,11 +108,24 @@ def _run(world, cases):
 ACCEPT = [(n, n, n, 3000 + n, 4000 + n) for n in (1, 2, 3, 4, 8, 16, 33)]
 RECT = [(5, 7, 4, 31, 32), (2, 2, 2, 61, 62), (513, 67, 129, 7, 8)]
 SUBBLOCKS = [(2048 * 5 + 3, 7, 5, 9, 10)]   # >= 1024 rows per rank: two sub-blocks each
+# B big enough to go out in k-panels (>= 64 Mi elements): 2 panels of 1024 rows
+PANELS = [(3, 2048, 32768, 11, 12)]
 
 
 @pytest.mark.parametrize("world", [2, 3, 5])
 def test_rowblock_gloo_bitwise_equals_seq(world):
     assert _run(world, ACCEPT + RECT + SUBBLOCKS) == []
+
+
+def test_rowblock_gloo_b_in_k_panels():
+    # the panel plan (first A sub-blocks, B as k-panels, the other A
+    # sub-blocks, C-slices) replayed by 2 processes; workers multiply only
+    # after every panel landed here (the GPU continues accumulators panel by
+    # panel -- bitwise the same, tests/test_gpu_parity.py accumulate tests)
+    m, k, n = PANELS[0][:3]
+    plan = __import__("paper_1012_2273_b200").rowblock_plan(m, n, k, 2)
+    assert [e["dir"] for e in plan].count("broadcast") == 2
+    assert _run(2, PANELS) == []
 
 
 # ----------------------------------------------------------------------------- fused gather
@@ -165,7 +185,7 @@ def _rank_main_fused(rank, world, port, cases, failures, refuse_rank):
             c_loc = np.zeros((rows, n))
             for e in plan:
                 if e["dir"] == "broadcast":
-                    dist.broadcast(bt, 0)
+                    dist.broadcast(bt.reshape(-1)[_b_span(e, k, n)], 0)
                 elif e["dir"] == "sent":                       # A sub-slices
                     r0, nr = e["row0"], e["count"] // k
                     if rank == 0:
@@ -225,3 +245,7 @@ def _run_fused(world, cases, refuse_rank):
 @pytest.mark.parametrize("world,refuse_rank", [(2, None), (3, None), (5, None), (3, 2)])
 def test_rowblock_gloo_fused_gather_bitwise_equals_seq(world, refuse_rank):
     assert _run_fused(world, ACCEPT[:5] + RECT + SUBBLOCKS, refuse_rank) == []
+
+
+def test_rowblock_gloo_fused_gather_with_b_panels():
+    assert _run_fused(2, PANELS, None) == []
