@@ -131,11 +131,14 @@ MMWS_DEVICE void set_flag(int* f, int v) {
 template <class K, int MODE>
 __global__ void __launch_bounds__(K::THREADS, K::MINB)
     dgemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA,
-                      const __grid_constant__ CUtensorMap tmB, double* C,
+                      const __grid_constant__ CUtensorMap tmB, double* __restrict__ C,
                       int64_t ldc, int M, int N, int K_, int tiles_m, int tiles_n, int vec_ok,
                       int group, DmmaStream st) {
-  // C may alias st.cin (in-place accumulate), so neither is __restrict__ here
-  constexpr bool STREAM = MODE == 1, SK = MODE == 2;
+  // (MODE 3 reads st.cin -- possibly C itself -- only before the K loop and
+  // writes C only after it, behind the pipeline's barriers)
+  // MODE 3 = MODE 0 + accumulate (tiles start from st.cin); a separate
+  // instantiation so the plain one-shot kernel's code is untouched
+  constexpr bool STREAM = MODE == 1, SK = MODE == 2, ACC = MODE == 3;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   // 1024-byte aligned ring (128B-swizzle atoms); offsetting the __shared__
   // array itself keeps the shared address space visible, so fragment fetches
@@ -284,8 +287,8 @@ __global__ void __launch_bounds__(K::THREADS, K::MINB)
       for (int b = 0; b < K::NB; ++b)
   #pragma unroll
         for (int e = 0; e < 2; ++e) acc[i][b][e][0] = acc[i][b][e][1] = 0.0;
-    if constexpr (MODE == 0) {
-      if (st.cin) {  // accumulate: continue Cin's chains (the epilogue's layout)
+    if constexpr (ACC) {
+      {  // accumulate: continue Cin's chains (the epilogue's layout)
   #pragma unroll
         for (int i = 0; i < K::MI; ++i) {
           const int row = tm * K::BM + wm * K::WM + i * 8 + sig;
@@ -294,10 +297,20 @@ __global__ void __launch_bounds__(K::THREADS, K::MINB)
   #pragma unroll
           for (int b = 0; b < K::NB; ++b) {
             const int col = tn * K::BN + (wn * K::NB + b) * 16 + 4 * tig;
-            acc[i][b][0][0] = col + 0 < N ? crow[col + 0] : 0.0;
-            acc[i][b][1][0] = col + 1 < N ? crow[col + 1] : 0.0;
-            acc[i][b][0][1] = col + 2 < N ? crow[col + 2] : 0.0;
-            acc[i][b][1][1] = col + 3 < N ? crow[col + 3] : 0.0;
+            if (vec_ok && col + 3 < N && (st.ldcin & 1) == 0 &&
+                (reinterpret_cast<uintptr_t>(st.cin) & 15) == 0) {
+              const double2 lo = __ldcg(reinterpret_cast<const double2*>(crow + col));
+              const double2 hi = __ldcg(reinterpret_cast<const double2*>(crow + col) + 1);
+              acc[i][b][0][0] = lo.x;
+              acc[i][b][1][0] = lo.y;
+              acc[i][b][0][1] = hi.x;
+              acc[i][b][1][1] = hi.y;
+            } else {
+              acc[i][b][0][0] = col + 0 < N ? crow[col + 0] : 0.0;
+              acc[i][b][1][0] = col + 1 < N ? crow[col + 1] : 0.0;
+              acc[i][b][0][1] = col + 2 < N ? crow[col + 2] : 0.0;
+              acc[i][b][1][1] = col + 3 < N ? crow[col + 3] : 0.0;
+            }
           }
         }
       }
@@ -442,7 +455,14 @@ cudaError_t run(const Launch& L, int64_t M, int64_t N, int64_t Kd, const double*
   DmmaStream st;
   st.cin = cin;
   st.ldcin = ldcin;
-  dgemm_dmma_kernel<K, 0><<<tiles_m * tiles_n, K::THREADS, smem, L.stream>>>(
+  auto kern = dgemm_dmma_kernel<K, 0>;
+  if constexpr (K::MATH_REGS == 0) {  // accumulate: small-register plans only (below)
+    if (cin) kern = dgemm_dmma_kernel<K, 3>;
+  }
+  if (cin && (e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) !=
+                 cudaSuccess)
+    return e;
+  kern<<<tiles_m * tiles_n, K::THREADS, smem, L.stream>>>(
       ta, tb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(Kd), tiles_m,
       tiles_n, vec_ok, raster_group<K>(L), st);
   L.count();
@@ -569,6 +589,10 @@ cudaError_t launch_dgemm_dmma_sk(const Launch& L, int cfg, int64_t M, int64_t N,
 cudaError_t launch_dgemm_dmma(const Launch& L, int cfg, int64_t M, int64_t N, int64_t K,
                               const double* A, int64_t lda, const double* B, int64_t ldb,
                               double* C, int64_t ldc, const double* cin, int64_t ldcin) {
+  // Accumulating launches take the 4-math-warp plans: loading the 8-warp
+  // plans' 64 accumulators per lane from Cin would spill (every plan gives the
+  // same bits, so the choice is free).
+  if (cin && (cfg == DMMA_128x128 || cfg == DMMA_128x64 || cfg == DMMA_64x64_W8)) cfg = DMMA_64x64;
   switch (cfg) {
     case DMMA_64x64: return run<Small>(L, M, N, K, A, lda, B, ldb, C, ldc, cin, ldcin);
     case DMMA_128x64: return run<Mid>(L, M, N, K, A, lda, B, ldb, C, ldc, cin, ldcin);
@@ -590,7 +614,10 @@ cudaError_t preload_dgemm_dmma() {
                          dgemm_dmma_kernel<Tiny, 0>, dgemm_dmma_kernel<Tiny, 2>,
                          dgemm_dmma_kernel<Slim, 0>, dgemm_dmma_kernel<Slim, 2>,
                          dgemm_dmma_kernel<TinyDeep, 0>, dgemm_dmma_kernel<TinyDeep, 2>,
-                         dgemm_dmma_kernel<Micro, 0>, dgemm_dmma_kernel<Micro, 2>);
+                         dgemm_dmma_kernel<Micro, 0>, dgemm_dmma_kernel<Micro, 2>,
+                         dgemm_dmma_kernel<Small, 3>,
+                         dgemm_dmma_kernel<Tiny, 3>, dgemm_dmma_kernel<Slim, 3>,
+                         dgemm_dmma_kernel<TinyDeep, 3>, dgemm_dmma_kernel<Micro, 3>);
 }
 
 }  // namespace mmws_impl

@@ -325,6 +325,8 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
     ctx->last_plan = dmma_plan_name(cfg, 1);
     return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm stream-K");
   }
+  // accumulating launches run on the 4-math-warp plans (dgemm_dmma.cu)
+  if (cin && (cfg == DMMA_128x128 || cfg == DMMA_128x64 || cfg == DMMA_64x64_W8)) cfg = DMMA_64x64;
   e = launch_dgemm_dmma(L, cfg, m, n, k, A, lda, B, ldb, C, ldc, cin, ldcin);
   ctx->last_plan = dmma_plan_name(cfg, 0);
   return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm dmma");
