@@ -506,11 +506,18 @@ def test_rowblock_nccl_path_single_rank(oracle):
         A = c2.fill(P.DIST_UNIFORM, 0, n, n)
         B = c2.fill(P.DIST_UNIFORM, 1, n, n)
         C = T.empty_like(A)
+        rows = [0, 1, 1151, 1152, n - 1]   # both sub-blocks
+        ref_rows = oracle.matmul_rows(rows, host(A), host(B))
         for mode in (P.MODE_AUTO, P.MODE_EXACT):
             el = c2.rowblock(n, n, n, A, B, C, mode=mode)
             assert el > 0
             want = host(c2.dgemm(A, B, mode=mode))
             assert (bits(host(C)) == bits(want)).all()
+            got_rows = host(C)[rows]
+            if mode == P.MODE_EXACT:       # the engine's rows against the CPU oracle
+                assert (bits(got_rows) == bits(ref_rows)).all()
+            else:
+                assert normwise(got_rows, ref_rows) <= FP64_TOL
             c, el = c2.master_run_host(host(A), host(B), mode=mode)
             assert el > 0 and (bits(c) == bits(want)).all()
         # fp32 through the same engine
