@@ -48,6 +48,7 @@ struct mmws_gpu_ctx {
   CUresult (*wait_value)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
   void* server = nullptr;  // latency server state (server.cu), null when not running
   void* stager = nullptr;  // pinned chunk ring + host copy threads (staging.cu), lazy
+  void* tiny_host = nullptr;  // pinned bounce buffer of tiny host-buffer multiplies, lazy
   uint64_t stage_next = 0;  // next pinned chunk (round robin)
   std::vector<void*> deferred_free;  // buffers outgrown while the server ran
   // CUDA IPC (fused C gather of the row-block path)

@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "../../include/mmws_gpu.h"
@@ -286,6 +287,66 @@ int host_multiply_ozaki(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, cons
   return ok();
 }
 
+// Tiny problems (the paper's N = 10 .. ~70): A, B and C fit one small pinned,
+// device-mapped bounce buffer.  A and B are packed into it with host memcpy.
+// When the multiply takes the latency kernel (plain loads: n, k <= 96 in
+// AUTO / EXACT) it reads A and B and writes C through the mapping -- no copy
+// engine at all; otherwise A|B cross PCIe in ONE transfer and C in one D2H,
+// on the same stream as the multiply, with one synchronisation (no
+// driver-staged pageable copies, no cross-stream events: each costs
+// microseconds at this size).  Same kernel, same bits as the other paths.
+constexpr size_t TINY_BYTES = size_t(128) << 10;
+
+template <class T>
+int host_multiply_tiny(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A,
+                       const T* B, T* C, int mode, double* elapsed_s) {
+  const size_t a_b = sizeof(T) * m * k, b_b = sizeof(T) * k * n, c_b = sizeof(T) * m * n;
+  const size_t b_off = (a_b + 255) / 256 * 256;
+  cudaError_t e;
+  if (!ctx->tiny_host &&
+      (e = cudaHostAlloc(&ctx->tiny_host, 2 * TINY_BYTES + 512, cudaHostAllocMapped)) != cudaSuccess) {
+    ctx->tiny_host = nullptr;
+    return cuda_fail(e, "matmul_host: pinned bounce buffer");
+  }
+  char* hin = static_cast<char*>(ctx->tiny_host);
+  char* hout = hin + TINY_BYTES + 256;
+  std::memcpy(hin, A, a_b);
+  std::memcpy(hin + b_off, B, b_b);
+  cudaStream_t s = ctx->stream;
+  const bool zero_copy = sizeof(T) == 8 && n <= AUTO_SMALL_MAX && k <= AUTO_SMALL_MAX &&
+                         (mode == MMWS_GPU_MODE_AUTO || mode == MMWS_GPU_MODE_EXACT);
+  if (zero_copy) {  // the latency kernel reads and writes host memory (UVA mapping)
+    cudaEventRecord(ctx->ev0, s);
+    if (int rc = gemm<T>(ctx, m, n, k, reinterpret_cast<const T*>(hin), k,
+                         reinterpret_cast<const T*>(hin + b_off), n, reinterpret_cast<T*>(hout),
+                         n, mode, s))
+      return rc;
+  } else {
+    if ((e = ensure(ctx, &ctx->dA, &ctx->dA_bytes, b_off + b_b)) != cudaSuccess ||
+        (e = ensure(ctx, &ctx->dC, &ctx->dC_bytes, c_b)) != cudaSuccess)
+      return cuda_fail(e, "matmul_host: device buffers");
+    char* dAB = static_cast<char*>(ctx->dA);
+    cudaEventRecord(ctx->ev0, s);
+    if ((e = cudaMemcpyAsync(dAB, hin, b_off + b_b, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+      return cuda_fail(e, "matmul_host: H2D");
+    if (int rc = gemm<T>(ctx, m, n, k, reinterpret_cast<const T*>(dAB), k,
+                         reinterpret_cast<const T*>(dAB + b_off), n, static_cast<T*>(ctx->dC), n,
+                         mode, s))
+      return rc;
+    if ((e = cudaMemcpyAsync(hout, ctx->dC, c_b, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return cuda_fail(e, "matmul_host: D2H");
+  }
+  cudaEventRecord(ctx->ev1, s);
+  if ((e = cudaEventSynchronize(ctx->ev1)) != cudaSuccess) return cuda_fail(e, "matmul_host: sync");
+  std::memcpy(C, hout, c_b);
+  if (elapsed_s) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    *elapsed_s = ms * 1e-3;
+  }
+  return ok();
+}
+
 }  // namespace
 
 template <class T>
@@ -295,6 +356,8 @@ int host_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A
     return fail(MMWS_GPU_ERR_DIMENSION, "matmul: dimensions must be positive");
   if (!A || !B || !C) return fail(MMWS_GPU_ERR_DOMAIN, "matmul: null host pointer");
   const size_t a_b = sizeof(T) * m * k, b_b = sizeof(T) * k * n, c_b = sizeof(T) * m * n;
+  if (a_b + 256 + b_b <= TINY_BYTES && c_b <= TINY_BYTES)
+    return host_multiply_tiny(ctx, m, n, k, A, B, C, mode, elapsed_s);
   cudaError_t e;
   if ((e = ensure(ctx, &ctx->dA, &ctx->dA_bytes, a_b)) != cudaSuccess ||
       (e = ensure(ctx, &ctx->dB, &ctx->dB_bytes, b_b)) != cudaSuccess ||

@@ -546,6 +546,7 @@ int mmws_gpu_destroy(mmws_gpu_ctx* ctx) {
     if (p) cudaFree(p);
   for (void* p : ctx->deferred_free) cudaFree(p);
   if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
+  if (ctx->tiny_host) cudaFreeHost(ctx->tiny_host);
   for (const auto& sp : ctx->sk_spaces) cudaFree(sp.mem);
   staging_destroy(ctx);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
