@@ -650,7 +650,10 @@ def measure_fp32(ctx, P, torch, dist, args, rank, world, local, barrier, gather_
         B = ctx.fill(P.DIST_NORMAL, 1, n, n, dtype=torch.float32)
         C = torch.empty_like(A)
     torch.cuda.synchronize()
-    ffma2_peak = max(ctx.peak_probe(P.PROBE_FFMA2, 20000) for _ in range(3))
+    ffma2_peak = max(ctx.peak_probe(P.PROBE_FFMA2, 100000) for _ in range(3))
+    # the GEMM's own operand pattern in registers (one fresh register operand
+    # per FFMA2): the ceiling of an FFMA2 GEMM, DESIGN.md s3.4
+    pattern_peak = max(ctx.peak_probe(P.PROBE_FFMA2_OUTER, 20000) for _ in range(3))
 
     def round32():
         ctx.rowblock(n, n, n, A, B, C, mode=P.MODE_FFMA, f32=True)
@@ -692,7 +695,13 @@ def measure_fp32(ctx, P, torch, dist, args, rank, world, local, barrier, gather_
                          "flops_per_launch": 2.0 * rows0 * n * n,
                          "peak_source": "measured live in this run: FFMA2 (fma.rn.f32x2) "
                                         "throughput probe",
-                         "peak_nominal": NOMINAL_FP32_TFLOPS},
+                         "peak_nominal": NOMINAL_FP32_TFLOPS,
+                         "pattern_ceiling": pattern_peak,
+                         "frac_of_pattern_ceiling": achieved / pattern_peak,
+                         "pattern_note": "FFMA2 outer product with a fresh broadcast register "
+                                         "operand per instruction (the kernel's pattern), "
+                                         "registers only, same shape (8 warps/SM, 64 pairs "
+                                         "per lane): mmws_gpu_peak_probe(FFMA2_OUTER)"},
             "accuracy": {"normwise_rel_error": err, "bound": 1e-5, "ok": err <= 1e-5,
                          "rows": rows,
                          "reference": "fp64 product of the widened fp32 rows (torch fp64 on the "

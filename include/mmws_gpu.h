@@ -97,13 +97,16 @@ enum {
   MMWS_GPU_DIST_NORMAL = 3
 };
 
-/* Peak probes (mmws_gpu_peak_probe). */
+/* Peak probes (mmws_gpu_peak_probe).  FFMA2_OUTER is the fp32 GEMM's own
+ * operand pattern (a fresh broadcast register operand per FFMA2) in registers
+ * only -- the ceiling of any FFMA2 GEMM, below the plain FFMA2 peak. */
 enum {
   MMWS_GPU_PROBE_DMMA = 0,
   MMWS_GPU_PROBE_DFMA = 1,
   MMWS_GPU_PROBE_DMUL_DADD = 2,
   MMWS_GPU_PROBE_FFMA = 3,
-  MMWS_GPU_PROBE_FFMA2 = 4
+  MMWS_GPU_PROBE_FFMA2 = 4,
+  MMWS_GPU_PROBE_FFMA2_OUTER = 5
 };
 
 typedef struct mmws_gpu_ctx mmws_gpu_ctx;

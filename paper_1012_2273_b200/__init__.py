@@ -12,4 +12,5 @@ from .api import (Context, DimensionError, DomainError, GpuError, Graph, Protoco
                   split_rows, static_partition)
 from ._abi import (GATHER_FUSED, GATHER_NCCL, GATHER_NONE, DIST_INT8, DIST_NORMAL, DIST_UNIFORM, DIST_UNIT, MODE_AUTO, MODE_DMMA,  # noqa: F401
                    MODE_DMMA_SMALL, MODE_EXACT, MODE_FFMA, MODE_OZAKI, PROBE_DFMA, PROBE_DMMA,
-                   PROBE_DMUL_DADD, PROBE_FFMA, PROBE_FFMA2)
+                   PROBE_DMUL_DADD, PROBE_FFMA, PROBE_FFMA2,
+                   PROBE_FFMA2_OUTER)

@@ -18,7 +18,7 @@ HEADER = os.path.join(os.path.dirname(PKG_DIR), "include", "mmws_gpu.h")
 GATHER_NONE, GATHER_FUSED, GATHER_NCCL = range(3)
 MODE_AUTO, MODE_EXACT, MODE_DMMA, MODE_DMMA_SMALL, MODE_FFMA, MODE_OZAKI = range(6)
 DIST_UNIT, DIST_UNIFORM, DIST_INT8, DIST_NORMAL = range(4)
-PROBE_DMMA, PROBE_DFMA, PROBE_DMUL_DADD, PROBE_FFMA, PROBE_FFMA2 = range(5)
+PROBE_DMMA, PROBE_DFMA, PROBE_DMUL_DADD, PROBE_FFMA, PROBE_FFMA2, PROBE_FFMA2_OUTER = range(6)
 
 _v, _i, _i32, _i64, _u32, _u64 = C.c_void_p, C.c_int, C.c_int32, C.c_int64, C.c_uint32, C.c_uint64
 _p = C.POINTER

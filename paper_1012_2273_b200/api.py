@@ -17,7 +17,8 @@ import numpy as np
 from . import _abi
 from ._abi import (DIST_INT8, DIST_NORMAL, DIST_UNIFORM, DIST_UNIT, MODE_AUTO, MODE_DMMA,  # noqa: F401
                    MODE_DMMA_SMALL, MODE_EXACT, MODE_FFMA, MODE_OZAKI, PROBE_DFMA, PROBE_DMMA,
-                   PROBE_DMUL_DADD, PROBE_FFMA, PROBE_FFMA2)
+                   PROBE_DMUL_DADD, PROBE_FFMA, PROBE_FFMA2,
+                   PROBE_FFMA2_OUTER)
 
 
 # --------------------------------------------------------------------------- errors

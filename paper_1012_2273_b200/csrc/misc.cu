@@ -82,6 +82,45 @@ cudaError_t launch_pack(const Launch& L, const T* src, int64_t rows, int64_t col
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- FFMA2 outer-product probe
+// The fp32 GEMM kernel's operand pattern in registers only (sgemm_tma.cu):
+// 8 warps per SM, 64 accumulator pairs per lane, B pairs reused across 8
+// consecutive FFMA2, the broadcast A scalar fresh from the register file each
+// time.  Its rate is the ceiling of any GEMM built from this pattern (the
+// extra register-file read per FFMA2 is what the plain FFMA2 probe does not
+// pay).
+__global__ void __launch_bounds__(256, 1) ffma2_outer_probe_kernel(int iters, double* sink) {
+  typedef unsigned long long u64;
+  auto pk = [](float a, float b) {
+    u64 r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+  };
+  const float seed = 1.0f + threadIdx.x * 1e-7f;
+  u64 b[8], d[8][8];
+  float ar[8];
+#pragma unroll
+  for (int p = 0; p < 8; ++p) b[p] = pk(seed * (0.5f + p), seed * (1.25f + p) + 0.375f);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    ar[i] = seed * (2.0625f + 0.1875f * i) - 3.0f;  // distinct from every B element
+#pragma unroll
+    for (int p = 0; p < 8; ++p) d[i][p] = 0;
+  }
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        asm volatile("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d[i][p]) : "l"(b[p]), "l"(pk(ar[i], ar[i])));
+  u64 x = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int p = 0; p < 8; ++p) x ^= d[i][p];
+  if (x == 12345ull) sink[threadIdx.x] = static_cast<double>(x);
+}
+
 // ---------------------------------------------------------------- peak probes
 // 0: DMMA.8x8x4 (FP64 tensor)  1: DFMA  2: DMUL+DADD  3: FFMA (fp32)  4: FFMA2 (fp32x2)
 template <int WHICH>
@@ -189,9 +228,13 @@ cudaError_t launch_peak_probe(const Launch& L, int which, int iters, double* sin
       probe_kernel<3><<<blocks, threads, 0, L.stream>>>(iters, sink);
       *flops = thr * 16.0 * iters * 2.0;
       break;
-    default:
+    case 4:
       probe_kernel<4><<<blocks, threads, 0, L.stream>>>(iters, sink);
       *flops = thr * 8.0 * iters * 4.0;  // 8 chains x 2 lanes x 2 flops
+      break;
+    default:  // 5: the fp32 GEMM's FFMA2 operand pattern, one 8-warp CTA per SM
+      ffma2_outer_probe_kernel<<<L.num_sms, 256, 0, L.stream>>>(iters, sink);
+      *flops = static_cast<double>(L.num_sms) * 256 * 64.0 * iters * 4.0;
       break;
   }
   L.count();
@@ -205,7 +248,8 @@ cudaError_t launch_board_mark(const Launch& L, unsigned* word, unsigned value) {
 }
 
 cudaError_t preload_misc() {
-  return preload_kernels(fill_kernel, pack_kernel<double>, pack_kernel<float>, board_mark_kernel, probe_kernel<0>, probe_kernel<1>,
+  return preload_kernels(fill_kernel, pack_kernel<double>, pack_kernel<float>, board_mark_kernel,
+                         ffma2_outer_probe_kernel, probe_kernel<0>, probe_kernel<1>,
                          probe_kernel<2>, probe_kernel<3>, probe_kernel<4>);
 }
 

@@ -796,7 +796,7 @@ int mmws_gpu_ipc_open(mmws_gpu_ctx* ctx, const uint8_t in[72], void** ptr) {
 // ------------------------------------------------------------------ measurement
 int mmws_gpu_peak_probe(mmws_gpu_ctx* ctx, int which, int iters, double* tflops) {
   MMWS_CTX_GUARD(ctx);
-  if (which < 0 || which > 4 || iters < 1 || !tflops)
+  if (which < 0 || which > 5 || iters < 1 || !tflops)
     return fail(MMWS_GPU_ERR_DOMAIN, "peak_probe: bad arguments");
   const Launch L = ctx->launch(nullptr);
   double flops = 0;
