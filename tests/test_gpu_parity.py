@@ -814,9 +814,16 @@ def test_launch_accounting(ctx):
 
 
 def test_peak_probes_run(ctx):
-    for which in (P.PROBE_DMMA, P.PROBE_DFMA, P.PROBE_DMUL_DADD, P.PROBE_FFMA, P.PROBE_FFMA2):
+    for which in (P.PROBE_DMMA, P.PROBE_DFMA, P.PROBE_DMUL_DADD, P.PROBE_FFMA, P.PROBE_FFMA2,
+                  P.PROBE_FFMA2_OUTER):
         tf = ctx.peak_probe(which, 256)
         assert 0.5 < tf < 200, (which, tf)
+    # the GEMM operand pattern cannot beat the plain FFMA2 peak
+    outer = max(ctx.peak_probe(P.PROBE_FFMA2_OUTER, 20000) for _ in range(2))
+    plain = max(ctx.peak_probe(P.PROBE_FFMA2, 100000) for _ in range(2))
+    assert 40 < outer <= plain * 1.02, (outer, plain)
+    with pytest.raises(P.DomainError):
+        ctx.peak_probe(6, 10)
 
 
 def test_auto_tile_plan_by_size(ctx):
