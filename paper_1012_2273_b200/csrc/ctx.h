@@ -110,6 +110,7 @@ struct mmws_gpu_ctx {
   unsigned* board = nullptr;       // rank 0: the board (device memory, IPC-exported)
   unsigned* board_peer = nullptr;  // where this rank's stores go / rank 0's board as seen here
   uint32_t round = 0;              // rounds started on this communicator
+  double round_work_s = 0.0;       // deadline allowance for the current step's own work
   bool comm_failed = false;        // a round timed out / a peer failed: communicator aborted
   int last_gather = 0;             // last round: 0 one GPU, 1 fused IPC stores, 2 NCCL C-slices
   int last_active = 1;             // last round: ranks that multiplied

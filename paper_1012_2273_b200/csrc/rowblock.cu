@@ -146,9 +146,12 @@ int round_failed(mmws_gpu_ctx* ctx, const char* what, ncclResult_t async, bool t
   return fail(!who.empty() || !timed_out ? MMWS_GPU_ERR_PROTOCOL : MMWS_GPU_ERR_TIMEOUT, msg);
 }
 
-// Wait for `ev` with the deadline while watching the communicator.
+// Wait for `ev` with the deadline while watching the communicator.  A round's
+// deadline is the step timeout plus a generous allowance for its own
+// arithmetic (ctx->round_work_s): like the reference's receive timeout, it
+// must not fire on a worker that is merely still multiplying a big block.
 int await(mmws_gpu_ctx* ctx, cudaEvent_t ev, const char* what) {
-  const Deadline dl(ctx->tune.timeout_s);
+  const Deadline dl(ctx->tune.timeout_s + ctx->round_work_s);
   for (int spins = 0;; backoff(spins)) {
     const cudaError_t q = cudaEventQuery(ev);
     if (q == cudaSuccess) return MMWS_GPU_OK;
@@ -350,6 +353,12 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
   ++ctx->round;
   ctx->last_active = P;
   ctx->last_panels = KP;
+  {
+    int64_t rows_max = 0;
+    for (int r = 0; r < P; ++r) rows_max = std::max(rows_max, rows[r]);
+    // twice the slowest rank's multiply at 5 TFLOP/s (well below every mode)
+    ctx->round_work_s = 2.0 * 2.0 * static_cast<double>(rows_max) * n * k / 5e12;
+  }
 
   if ((e = event_pool(ctx, 2 * S + KP + 4)) != cudaSuccess) return cuda_fail(e, "rowblock: events");
   cudaEvent_t* evA = ctx->pool.data() + 1;
@@ -643,6 +652,7 @@ int comm_create(mmws_gpu_ctx* ctx, int nranks, int rank, const ncclUniqueId& uid
   ctx->nranks = nranks;
   ctx->rank = rank;
   ctx->round = 0;
+  ctx->round_work_s = 0.0;
   ctx->comm_failed = false;
   ctx->last_fused = -1;
   return MMWS_GPU_OK;
@@ -790,6 +800,7 @@ int mmws_gpu_link_probe(mmws_gpu_ctx* ctx, int64_t bytes, int iters, double* byt
   if ((e = ensure(ctx, &ctx->rbB, &ctx->rbB_bytes, static_cast<size_t>(bytes))) != cudaSuccess)
     return cuda_fail(e, "link_probe: buffer");
   if ((e = event_pool(ctx, 1)) != cudaSuccess) return cuda_fail(e, "link_probe: events");
+  ctx->round_work_s = static_cast<double>(bytes) * iters / 1e9;  // >= 1 GB/s
   cudaStream_t s = ctx->comm_stream;
   NCCL_TRY(nccl().Broadcast(ctx->rbB, ctx->rbB, bytes, ncclUint8, 0, ctx->comm, s),
            "link_probe warm-up");
@@ -818,6 +829,7 @@ int mmws_gpu_p2p_probe(mmws_gpu_ctx* ctx, int64_t bytes, int iters, double* byte
   if ((e = ensure(ctx, &ctx->rbB, &ctx->rbB_bytes, static_cast<size_t>(bytes))) != cudaSuccess)
     return cuda_fail(e, "p2p_probe: buffer");
   if ((e = event_pool(ctx, 1)) != cudaSuccess) return cuda_fail(e, "p2p_probe: events");
+  ctx->round_work_s = static_cast<double>(bytes) * (iters + 1) * ctx->nranks / 1e9;
   cudaStream_t s = ctx->comm_stream;
   // rank 0 -> rank r, one peer at a time (the A-slice / C-slice link); the
   // slowest peer is reported (rank 0's view; workers report their own link)
