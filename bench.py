@@ -849,8 +849,15 @@ def main() -> None:
         sys.exit(launch_ranks(args))
     if args.dry_run:
         run_dry(args)
-    else:
+        return
+    try:
         run_ours(args)
+    except Exception as exc:  # a failed run still leaves a line saying why
+        if int(os.environ.get("RANK", "0")) == 0:
+            print(json.dumps({"metric": metric_name(), "value": None, "unit": "GFLOP/s",
+                              "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                              "error": f"{type(exc).__name__}: {exc}"}), flush=True)
+        raise
 
 
 if __name__ == "__main__":
