@@ -269,22 +269,43 @@ def free_port() -> int:
 def launch_ranks(args) -> int:
     """One process per GPU (the driver may call plain `python bench.py --gpus N`):
     children get RANK/LOCAL_RANK/WORLD_SIZE/MASTER_ADDR/MASTER_PORT; rank 0's
-    stdout is relayed; any failing rank fails the run."""
+    stdout is relayed; any failing rank fails the run, and -- like the
+    reference's ProcessGroup (launch.hpp:73,113-127) -- the first rank to fail
+    takes the others down instead of leaving them blocked on their peers."""
     port = str(free_port())
+    out = tempfile.TemporaryFile()
     procs = []
     for r in range(args.gpus):
         env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(args.gpus),
                    LOCAL_WORLD_SIZE=str(args.gpus), MASTER_ADDR="127.0.0.1", MASTER_PORT=port)
         procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:],
-                                      env=env,
-                                      stdout=subprocess.PIPE if r == 0 else sys.stderr.fileno()))
-    out, _ = procs[0].communicate()
-    codes = [procs[0].returncode] + [p.wait() for p in procs[1:]]
-    sys.stdout.write(out.decode())
+                                      env=env, stdout=out if r == 0 else sys.stderr.fileno()))
+    failed = None
+    while True:
+        states = [p.poll() for p in procs]  # every rank, every time (no short-circuit)
+        if all(st is not None for st in states):
+            break
+        bad = [r for r, st in enumerate(states) if st not in (None, 0)]
+        if bad and failed is None:
+            failed = bad
+            for p in procs:
+                if p.poll() is None:
+                    p.terminate()
+            deadline = time.time() + 15
+            while any(p.poll() is None for p in procs) and time.time() < deadline:
+                time.sleep(0.1)
+            for p in procs:
+                if p.poll() is None:
+                    p.kill()
+        time.sleep(0.05)
+    codes = [p.wait() for p in procs]
+    out.seek(0)
+    sys.stdout.write(out.read().decode())
     sys.stdout.flush()
     bad = [(r, c) for r, c in enumerate(codes) if c != 0]
     if bad:
-        sys.stderr.write(f"bench.py: rank(s) failed: {bad}\n")
+        sys.stderr.write(f"bench.py: rank(s) failed: {bad}" +
+                         (f" (first: {failed})" if failed else "") + "\n")
         return 1
     return 0
 
@@ -308,6 +329,8 @@ def run_dry(args) -> None:
 
     import paper_1012_2273_b200 as P
     rank, world, _ = world_from_env(args)
+    if os.environ.get("MMWS_BENCH_DRY_FAIL_RANK") == str(rank):  # launcher test: this rank dies
+        sys.exit(3)
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", str(free_port()))
     dist.init_process_group("gloo", rank=rank, world_size=world)

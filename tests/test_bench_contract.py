@@ -65,3 +65,16 @@ def test_world_size_must_match_gpus():
                         "--n", "64", "--steps", "1", "--warmup", "0"],
                        capture_output=True, text=True, cwd=ROOT, env=env, timeout=120)
     assert r.returncode != 0 and "WORLD_SIZE=2" in r.stderr
+
+
+def test_launcher_takes_the_world_down_when_a_rank_fails():
+    """A rank that dies (here rank 2 of 3, on purpose, before the rendezvous)
+    must not leave the others blocked on it: the launcher terminates the rest
+    and exits non-zero."""
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    env["MMWS_BENCH_DRY_FAIL_RANK"] = "2"
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--dry-run", "--gpus", "3",
+                        "--n", "64", "--steps", "1", "--warmup", "0"],
+                       capture_output=True, text=True, cwd=ROOT, env=env, timeout=120)
+    assert r.returncode != 0 and "rank(s) failed" in r.stderr
