@@ -215,8 +215,10 @@ constexpr int64_t PANEL_ELEMS = int64_t{32} << 20;  // 256 MiB of fp64 per B pan
 constexpr int64_t PANEL_QUANTUM = 1024;              // fp32's partial-sum chunk (and 64 fp64 k-tiles)
 constexpr int MAX_PANELS = 8;
 
-// panels: the mode can continue accumulators across launches (all but OZAKI)
-Schedule make_schedule(int64_t m, int64_t n, int64_t k, int P, bool panels) {
+// panels: the mode can continue accumulators across launches (all but OZAKI);
+// host: a master_run round from host memory (B also streams over PCIe into
+// rank 0, so rank 0 takes panels too -- even in a 1-rank world)
+Schedule make_schedule(int64_t m, int64_t n, int64_t k, int P, bool panels, bool host = false) {
   Schedule sc;
   sc.P = P;
   sc.off.resize(P);
@@ -229,7 +231,7 @@ Schedule make_schedule(int64_t m, int64_t n, int64_t k, int P, bool panels) {
     mmws_gpu_split_rows(sc.rows[r], sc.S, sc.soff[r].data(), sc.srows[r].data());
   sc.kb = {0};
   const double b_elems = static_cast<double>(k) * n;
-  if (P > 1 && panels && b_elems >= 2.0 * PANEL_ELEMS) {
+  if ((P > 1 || host) && panels && b_elems >= 2.0 * PANEL_ELEMS) {
     const int want = static_cast<int>(std::min<double>(MAX_PANELS, b_elems / PANEL_ELEMS));
     for (int j = 1; j < want; ++j) {
       const int64_t e = (k * j / want) / PANEL_QUANTUM * PANEL_QUANTUM;
@@ -287,9 +289,20 @@ int rowblock_active(int64_t m, int64_t n, int64_t k, int P, int elem_bytes, int 
 //   * rank 0 multiplies its own rows meanwhile (it holds A and B already).
 // Every launch computes each element with the same kernel and k-order as a
 // 1-GPU launch, so the assembled C is bitwise the 1-GPU result.
+//
+// Host rounds (master_run_host, host = true on every rank): rank 0's A, B
+// are the device staging buffers and hA, hB the caller's host matrices; rank
+// 0 copies each piece over PCIe (copy_in stream) right before the NCCL
+// operation that sends it -- the workers' first A rows, its own rows, the B
+// panels, the workers' other A rows -- so the exchange and the workers start
+// while the rest of A and B is still crossing PCIe, and rank 0 multiplies its
+// own rows panel by panel as B lands, like a worker.  *own_done (rank 0) is
+// recorded once rank 0's own rows of C are final.
 template <class T>
 int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, const T* B,
-                     T* C, int mode, bool bracket, cudaEvent_t* done) {
+                     T* C, int mode, bool bracket, cudaEvent_t* done, bool host = false,
+                     const T* hA = nullptr, const T* hB = nullptr,
+                     cudaEvent_t* own_done = nullptr) {
   if (m <= 0 || n <= 0 || k <= 0)
     return fail(MMWS_GPU_ERR_DIMENSION, "rowblock: dimensions must be positive");
   if (ctx->comm_failed)
@@ -342,8 +355,9 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
     ~NoStreamK() { c->allow_streamk = true; }
   } no_sk{ctx};
   ctx->allow_streamk = false;
-  const Schedule sc = make_schedule(m, n, k, P, mode != MMWS_GPU_MODE_OZAKI);
+  const Schedule sc = make_schedule(m, n, k, P, mode != MMWS_GPU_MODE_OZAKI, host);
   const int S = sc.S, KP = sc.KP;
+  const bool stream_in = me == 0 && hA && hB;  // rank 0 of a host round
   const auto& off = sc.off;
   const auto& rows = sc.rows;
   const auto& soff = sc.soff;
@@ -360,11 +374,16 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
     ctx->round_work_s = 2.0 * 2.0 * static_cast<double>(rows_max) * n * k / 5e12;
   }
 
-  if ((e = event_pool(ctx, 2 * S + KP + 4)) != cudaSuccess) return cuda_fail(e, "rowblock: events");
+  if ((e = event_pool(ctx, 3 * S + 2 * KP + 5)) != cudaSuccess)
+    return cuda_fail(e, "rowblock: events");
   cudaEvent_t* evA = ctx->pool.data() + 1;
   cudaEvent_t* evC = evA + S;
   cudaEvent_t* evBp = evC + S;  // B panel j has landed
   cudaEvent_t evStart = evBp[KP], evJoin = evBp[KP + 1], evHost = evBp[KP + 2];
+  cudaEvent_t* evHA = evBp + KP + 3;  // host round, rank 0: workers' A rows of sub-block s copied in
+  cudaEvent_t* evHB = evHA + S;       // ... B panel j copied in
+  cudaEvent_t evHself = evHB[KP];     // ... rank 0's own rows copied in
+  if (own_done) *own_done = evC[S - 1];
 
   // the exchange starts after everything already queued on the compute stream
   // (e.g. the H2D copies of master_run_host)
@@ -433,9 +452,11 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
     c_loc = fused ? c_peer + off[me] * n : static_cast<T*>(ctx->rbC);
   }
   T* c_dst = c_loc;  // rank 0: C; workers: rank 0's C (fused) or the local slice
-  // worker's running accumulators of its first sub-block while B's panels land
+  // worker's (or a host round's rank 0's) running accumulators of its first
+  // sub-block while B's panels land
+  const bool paneled = KP > 1 && (me != 0 || stream_in);
   T* acc0 = nullptr;
-  if (me != 0 && KP > 1 && srows[me][0] > 0) {
+  if (paneled && srows[me][0] > 0) {
     if ((e = ensure(ctx, &ctx->rbAcc, &ctx->rbAcc_bytes, sizeof(T) * srows[me][0] * n)) !=
         cudaSuccess)
       return cuda_fail(e, "rowblock: worker accumulators");
@@ -447,7 +468,31 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
   // panel: B first (nothing can finish without all of it), then the A
   // sub-blocks.  Several: the first A sub-blocks, the panels, the other A
   // sub-blocks -- a worker starts once its first rows and panel 0 are in.
+  // host round, rank 0: one piece over PCIe, then an event the dependent
+  // NCCL operation (comm stream) or multiply (compute stream) waits on
+  cudaStream_t in = ctx->copy_in;
+  auto h2d_rows = [&](T* dst, const T* src, int64_t r0, int64_t nr, int64_t w) -> cudaError_t {
+    if (nr <= 0) return cudaSuccess;
+    return copy_h2d(ctx, dst + r0 * w, sizeof(T) * w, src + r0 * w, sizeof(T) * w,
+                    sizeof(T) * w, static_cast<size_t>(nr), in);
+  };
+  auto h2d_a = [&](int s) -> int {  // every worker's A rows of sub-block s
+    for (int r = 1; r < P; ++r)
+      if ((e = h2d_rows(as_mut(A), hA, off[r] + soff[r][s], srows[r][s], k)) != cudaSuccess)
+        return cuda_fail(e, "master_run: H2D A");
+    cudaEventRecord(evHA[s], in);
+    cudaStreamWaitEvent(comm, evHA[s], 0);
+    return MMWS_GPU_OK;
+  };
+  auto h2d_self = [&]() -> int {  // rank 0's own rows
+    if ((e = h2d_rows(as_mut(A), hA, 0, rows[0], k)) != cudaSuccess)
+      return cuda_fail(e, "master_run: H2D A");
+    cudaEventRecord(evHself, in);
+    return MMWS_GPU_OK;
+  };
   auto send_a = [&](int s) -> int {
+    if (stream_in)
+      if (int rc = h2d_a(s)) return rc;
     NCCL_TRY(nccl().GroupStart(), "ncclGroupStart");
     if (me == 0) {
       for (int r = 1; r < P; ++r)
@@ -462,10 +507,21 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
     cudaEventRecord(evA[s], comm);
     return MMWS_GPU_OK;
   };
+  if (stream_in && bracket) cudaEventRecord(ctx->ev0, in);
+  if (stream_in && KP == 1)
+    if (int rc = h2d_self()) return rc;
   if (KP > 1)
     if (int rc = send_a(0)) return rc;
+  if (stream_in && KP > 1)
+    if (int rc = h2d_self()) return rc;
   for (int j = 0; j < KP; ++j) {
     T* bp = as_mut(b_loc) + kb[j] * n;
+    if (stream_in) {
+      if ((e = h2d_rows(bp - kb[j] * n, hB, kb[j], kb[j + 1] - kb[j], n)) != cudaSuccess)
+        return cuda_fail(e, "master_run: H2D B");
+      cudaEventRecord(evHB[j], in);
+      cudaStreamWaitEvent(comm, evHB[j], 0);
+    }
     NCCL_TRY(nccl().Broadcast(bp, bp, (kb[j + 1] - kb[j]) * n, dt, 0, ctx->comm, comm),
              "broadcast B");
     cudaEventRecord(evBp[j], comm);
@@ -476,14 +532,21 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
 
   // ---- compute stream: this rank's rows (worker_run's body, protocol.hpp:132-141)
   cudaEventRecord(ctx->evk0, comp);
+  // where this rank's inputs land: workers by NCCL; rank 0 of a host round by
+  // its own H2D copies; rank 0 otherwise already holds them
+  auto wait_b = [&](int j) {
+    if (me != 0) cudaStreamWaitEvent(comp, evBp[j], 0);
+    else if (stream_in) cudaStreamWaitEvent(comp, evHB[j], 0);
+  };
+  if (stream_in) cudaStreamWaitEvent(comp, evHself, 0);
   for (int s = 0; s < S; ++s) {
     const int64_t r0 = soff[me][s], rs = srows[me][s];
     if (me != 0) cudaStreamWaitEvent(comp, evA[s], 0);
-    if (me != 0 && s == 0 && KP > 1) {
+    if (paneled && s == 0) {
       // panel by panel as B lands: launch j continues launch j-1's
       // accumulators (acc0), the last one stores into the destination
       for (int j = 0; j < KP; ++j) {
-        cudaStreamWaitEvent(comp, evBp[j], 0);
+        wait_b(j);
         if (rs == 0) continue;
         T* out = j + 1 < KP ? acc0 : c_dst + r0 * n;
         if (int rc = gemm<T>(ctx, rs, n, kb[j + 1] - kb[j], a_loc + r0 * k + kb[j], k,
@@ -491,7 +554,7 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
           return rc;
       }
     } else {
-      if (me != 0) cudaStreamWaitEvent(comp, evBp[KP - 1], 0);  // all of B
+      wait_b(KP - 1);  // all of B
       if (rs > 0)
         if (int rc = gemm<T>(ctx, rs, n, k, a_loc + r0 * k, k, b_loc, n, c_dst + r0 * n, n, mode,
                              comp))
@@ -572,9 +635,14 @@ template <class T>
 int master_run_host(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, const T* B,
                     T* C, int mode, double* elapsed_s) {
   const bool root = !ctx->comm || ctx->rank == 0;
-  if (!root) return rowblock(ctx, m, n, k, static_cast<const T*>(nullptr),
-                             static_cast<const T*>(nullptr), static_cast<T*>(nullptr), mode,
-                             elapsed_s);
+  if (!root) {  // worker_run: the host round's schedule (B in panels where rank 0 uses them)
+    cudaEvent_t done = nullptr;
+    if (int rc = rowblock_enqueue(ctx, m, n, k, static_cast<const T*>(nullptr),
+                                  static_cast<const T*>(nullptr), static_cast<T*>(nullptr), mode,
+                                  true, &done, true))
+      return rc;
+    return finish(ctx, done, false, elapsed_s);
+  }
   if (ctx->comm_failed)
     return fail(MMWS_GPU_ERR_STATE, "master_run: the communicator was aborted after a failed "
                                     "round; mmws_gpu_comm_destroy + mmws_gpu_comm_init first");
@@ -597,27 +665,32 @@ int master_run_host(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T*
       (e = ensure(ctx, &ctx->dB, &ctx->dB_bytes, b_b)) != cudaSuccess ||
       (e = ensure(ctx, &ctx->dC, &ctx->dC_bytes, c_b)) != cudaSuccess)
     return cuda_fail(e, "master_run: device buffers");
-  cudaStream_t s = ctx->stream;
-  cudaEventRecord(ctx->ev0, s);
-  if ((e = copy_h2d(ctx, ctx->dA, sizeof(T) * k, A, sizeof(T) * k, sizeof(T) * k, m, s)) !=
-          cudaSuccess ||
-      (e = copy_h2d(ctx, ctx->dB, sizeof(T) * n, B, sizeof(T) * n, sizeof(T) * n, k, s)) !=
-          cudaSuccess)
-    return cuda_fail(e, "master_run: H2D");
-  cudaEvent_t done = nullptr;
+  // the engine copies A and B in piece by piece, each right before the
+  // exchange (or rank 0's multiply) that needs it; ev0 precedes the first copy
+  cudaEvent_t done = nullptr, own = nullptr;
   if (int rc = rowblock_enqueue(ctx, m, n, k, static_cast<const T*>(ctx->dA),
                                 static_cast<const T*>(ctx->dB), static_cast<T*>(ctx->dC), mode,
-                                false, &done))
+                                true, &done, true, A, B, &own))
     return rc;
-  // the round must complete (within the deadline) before the copy-out: a
-  // pageable C is pumped by this thread, which would otherwise block on it
+  // copy-out: rank 0's own rows as soon as they are final, the workers' rows
+  // once the round completed (within the deadline: a pageable C is pumped by
+  // this thread, which would otherwise block on an unfinished round)
+  const int64_t rows0 = make_schedule(m, n, k, ctx->nranks, false).rows[0];
+  cudaStream_t out = ctx->copy_out;
+  cudaStreamWaitEvent(out, own, 0);
+  D2hPump pump(ctx, out);
+  if ((e = pump.add(C, sizeof(T) * n, ctx->dC, sizeof(T) * n, sizeof(T) * n, rows0)) !=
+      cudaSuccess)
+    return cuda_fail(e, "master_run: D2H");
   if (int rc = await(ctx, done, "master_run round")) return rc;
-  D2hPump pump(ctx, s);
-  if ((e = pump.add(C, sizeof(T) * n, ctx->dC, sizeof(T) * n, sizeof(T) * n, m)) != cudaSuccess ||
+  cudaStreamWaitEvent(out, done, 0);
+  if ((e = pump.add(C + rows0 * n, sizeof(T) * n, static_cast<T*>(ctx->dC) + rows0 * n,
+                    sizeof(T) * n, sizeof(T) * n, m - rows0)) != cudaSuccess ||
       (e = pump.finish()) != cudaSuccess)
     return cuda_fail(e, "master_run: D2H");
-  cudaEventRecord(ctx->ev1, s);
-  cudaEventRecord(done, s);
+  cudaEventRecord(ctx->ev1, out);
+  cudaEventRecord(done, out);
+  if ((e = cudaStreamSynchronize(out)) != cudaSuccess) return cuda_fail(e, "master_run: sync");
   return finish(ctx, done, true, elapsed_s);
 }
 

@@ -343,3 +343,41 @@ def test_tune_rejects_unknown_knobs(ctx):
     ctx.tune("MMWS_GPU_TIMEOUT_S", "30")
     with pytest.raises(P.DomainError):
         ctx.set_timeout(0)
+
+
+def test_one_rank_host_round_streams_b_in_panels():
+    """master_run from host memory in a 1-rank world with a B big enough for
+    k-panels: rank 0 copies its rows and B's panels in over PCIe piece by
+    piece and multiplies panel by panel as they land (accumulator
+    continuation), its own C rows go back before the round's barrier --
+    bitwise the one-call product, pinned and pageable."""
+    import torch
+    c = P.Context(0)
+    try:
+        c.comm_init(1, 0, P.nccl_unique_id())
+        m, k, n = 1100, 8192, 8192          # B = 64 Mi elements: 2 panels of 4096 rows
+        A = c.fill(P.DIST_UNIFORM, 5, m, k)
+        B = c.fill(P.DIST_UNIFORM, 6, k, n)
+        a, b = A.cpu().numpy(), B.cpu().numpy()
+        for mode in (P.MODE_AUTO, P.MODE_EXACT):
+            want = c.dgemm(A, B, mode=mode).cpu().numpy()
+            got, el = c.master_run_host(a, b, mode=mode)                       # pageable
+            assert el > 0 and c.last_b_panels == 2 and c.last_round == (1, "fused-ipc")
+            assert np.array_equal(got.view(np.int64), want.view(np.int64)), mode
+            ap = torch.from_numpy(a).pin_memory().numpy()
+            bp = torch.from_numpy(b).pin_memory().numpy()
+            cp = torch.empty((m, n), dtype=torch.float64).pin_memory().numpy()
+            got, _ = c.master_run_host(ap, bp, cp, mode=mode)                  # pinned
+            assert np.array_equal(got.view(np.int64), want.view(np.int64)), mode
+        # fp32 through the same host round (panel edges at multiples of 1024)
+        Af, Bf = A.float(), B.float()
+        want = c.sgemm(Af, Bf).cpu().numpy()
+        got, _ = c.master_run_host(Af.cpu().numpy(), Bf.cpu().numpy())
+        assert np.array_equal(got.view(np.int32), want.view(np.int32))
+        # device-resident rounds in a 1-rank world keep B in one piece
+        C = torch.empty((m, n), dtype=torch.float64, device="cuda")
+        c.rowblock(m, n, k, A, B, C)
+        assert c.last_b_panels == 1
+        c.comm_destroy()
+    finally:
+        c.close()
