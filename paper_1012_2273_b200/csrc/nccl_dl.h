@@ -5,9 +5,11 @@
 // older libnccl.so.2 bound first would break the other library's newer
 // symbols.  dlopen("libnccl.so.2") returns whichever copy the process already
 // loaded, or the system one otherwise.  Only the row-block path needs NCCL.
+// Resolved once, on the first row-block / communicator call.
 #pragma once
 
 #include <dlfcn.h>
+#include <cstdlib>
 #include <nccl.h>
 
 #include <mutex>
@@ -37,8 +39,12 @@ inline const NcclApi& nccl() {
   static NcclApi api;
   static std::once_flag once;
   std::call_once(once, [] {
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    // MMWS_GPU_NCCL_LIB (tests only): a stand-in library with the same entry
+    // points, loaded privately -- tests/fake_nccl runs several ranks on one GPU
+    const char* lib = std::getenv("MMWS_GPU_NCCL_LIB");
+    void* h = lib && *lib ? dlopen(lib, RTLD_NOW | RTLD_LOCAL)
+                          : dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h && !(lib && *lib)) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
     if (!h) return;
 #define MMWS_NCCL_SYM(field, name) api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name))
     MMWS_NCCL_SYM(GetUniqueId, "ncclGetUniqueId");

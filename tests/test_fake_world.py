@@ -1,0 +1,200 @@
+"""The row-block master/worker engine with every rank's side executing on the
+GPU -- several processes on ONE B200.
+
+NCCL refuses two ranks on one device, so these tests load a loopback
+stand-in for its entry points (tests/fake_nccl/fake_nccl.cpp, test
+infrastructure only: device-to-device copies between the processes' buffers
+through CUDA IPC, host rendezvous in shared memory) via MMWS_GPU_NCCL_LIB.
+Everything else is the product path: the workers receive their A rows and
+B (in k-panels where the round uses them), multiply panel by panel with
+accumulator continuation, store their C rows straight into rank 0's C
+through the CUDA IPC mapping (fused gather) or send them back (NCCL-style
+gather), mark their progress on rank 0's board, and rank 0 names a worker
+that left (test_protocol.cpp:171-178).  Results must be bitwise rank 0's own
+one-GPU product.  No kernel waits on another process's kernel (the B200
+profiling guide's Xid-109 warning): cross-process ordering is host
+rendezvous plus stream waits on IPC events.
+"""
+import os
+import secrets
+import subprocess
+import time
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def fake_lib(tmp_path_factory):
+    out = tmp_path_factory.mktemp("fake_nccl") / "libfake_nccl.so"
+    subprocess.run(["g++", "-std=c++17", "-O2", "-shared", "-fPIC", "-I/usr/local/cuda/include",
+                    os.path.join(ROOT, "tests", "fake_nccl", "fake_nccl.cpp"), "-o", str(out),
+                    "-L/usr/local/cuda/lib64/stubs", "-lcuda"], check=True)
+    return str(out)
+
+
+def _uid(name: str) -> bytes:
+    raw = name.encode()
+    return raw + b"\0" * (128 - len(raw))
+
+
+def _rank_main(rank, world, lib, name, job, results):
+    os.environ["MMWS_GPU_NCCL_LIB"] = lib
+    import sys
+    sys.path.insert(0, ROOT)
+    import paper_1012_2273_b200 as P
+    ctx = P.Context(0)
+    try:
+        ctx.set_timeout(60)
+        ctx.comm_init(world, rank, _uid(name))
+        out = JOBS[job](P, ctx, rank, world)
+        results.put((rank, "ok", out))
+    except Exception as exc:
+        results.put((rank, "error", f"{type(exc).__name__}: {exc}"))
+    finally:
+        try:
+            ctx.close()
+        except Exception:
+            pass
+
+
+def _run(world, lib, job, timeout=600):
+    import torch.multiprocessing as mp
+    mpc = mp.get_context("spawn")
+    results = mpc.Queue()
+    name = "/mmws_fake_nccl_" + secrets.token_hex(8)
+    procs = [mpc.Process(target=_rank_main, args=(r, world, lib, name, job, results))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    deadline = time.time() + timeout
+    while len(out) < world and time.time() < deadline:
+        try:
+            r, status, val = results.get(timeout=5)
+            out[r] = (status, val)
+        except Exception:
+            if all(not p.is_alive() for p in procs) and results.empty():
+                break
+    for p in procs:
+        p.join(timeout=30)
+        if p.is_alive():
+            p.kill()
+    return out
+
+
+def _ok(out, world):
+    assert len(out) == world, out
+    bad = {r: v for r, v in out.items() if v[0] != "ok"}
+    assert not bad, bad
+    return {r: v[1] for r, v in out.items()}
+
+
+def _same(a, b):
+    import torch
+    return bool(torch.equal(a.view(torch.int64 if a.dtype == torch.float64 else torch.int32),
+                            b.view(torch.int64 if b.dtype == torch.float64 else torch.int32)))
+
+
+# ----------------------------------------------------------------------------- jobs
+CASES = [  # (m, k, n, dtype, mode name): one-piece B with two sub-blocks, B in k-panels
+    (2304, 2304, 2304, "f64", "auto"), (2304, 2304, 2304, "f64", "exact"),
+    (2100, 8192, 8192, "f64", "auto"), (2100, 8192, 8192, "f32", "ffma"),
+]
+
+
+def _job_rounds(P, ctx, rank, world):
+    import torch
+    modes = {"auto": P.MODE_AUTO, "exact": P.MODE_EXACT, "ffma": P.MODE_FFMA}
+    ctx.tune("MMWS_GPU_ROWBLOCK_RANKS", "all")
+    res = []
+    for gather in (None, "1"):
+        ctx.tune("MMWS_GPU_NCCL_GATHER", gather)
+        for (m, k, n, dt, mode_name) in CASES:
+            mode, f32 = modes[mode_name], dt == "f32"
+            tdt = torch.float32 if f32 else torch.float64
+            dist = P.DIST_NORMAL if f32 else P.DIST_UNIFORM
+            if rank == 0:
+                A = ctx.fill(dist, 11, m, k, dtype=tdt)
+                B = ctx.fill(dist, 12, k, n, dtype=tdt)
+                C = torch.full((m, n), float("nan"), dtype=tdt, device="cuda")
+                ctx.rowblock(m, n, k, A, B, C, mode=mode, f32=f32)
+                info = (ctx.last_round, ctx.last_b_panels)
+                want = (ctx.sgemm if f32 else ctx.dgemm)(A, B, mode=mode)
+                torch.cuda.synchronize()
+                res.append((gather, m, k, n, dt, mode_name, info, _same(C, want)))
+                del A, B, C, want
+            else:
+                ctx.rowblock(m, n, k, mode=mode, f32=f32)
+    # master_run from pageable host memory (the e2e entry), B in k-panels
+    ctx.tune("MMWS_GPU_NCCL_GATHER", None)
+    m, k, n = 2100, 8192, 8192
+    if rank == 0:
+        A = ctx.fill(P.DIST_UNIFORM, 21, m, k)
+        B = ctx.fill(P.DIST_UNIFORM, 22, k, n)
+        want = ctx.dgemm(A, B).cpu().numpy()
+        got, el = ctx.master_run_host(A.cpu().numpy(), B.cpu().numpy())
+        res.append(("host", m, k, n, "f64", "auto", (ctx.last_round, ctx.last_b_panels),
+                    bool(np.array_equal(got.view(np.int64), want.view(np.int64))) and el > 0))
+    else:
+        ctx.master_run_host(None, None, None, m=m, n=n, k=k)
+    return res
+
+
+def _job_dead(P, ctx, rank, world):
+    """rank 1 joins, then leaves without serving a round"""
+    import torch
+    if rank == 1:
+        return "left"
+    ctx.tune("MMWS_GPU_ROWBLOCK_RANKS", "all")
+    n = 512
+    A = ctx.fill(P.DIST_UNIFORM, 81, n, n)
+    B = ctx.fill(P.DIST_UNIFORM, 82, n, n)
+    C = torch.empty_like(A)
+    t0 = time.time()
+    try:
+        ctx.rowblock(n, n, n, A, B, C)
+    except (P.ProtocolError, P.TimeoutError) as exc:
+        took = time.time() - t0
+        try:
+            ctx.rowblock(n, n, n, A, B, C)
+            after = "no error"
+        except P.GpuError as e2:
+            after = str(e2)
+        ctx.comm_destroy()
+        ctx.rowblock(n, n, n, A, B, C)   # no communicator: one multiply
+        ok = _same(C, ctx.dgemm(A, B))
+        return {"type": type(exc).__name__, "msg": str(exc), "took": took, "after": after,
+                "recovered": ok}
+    return {"type": None}
+
+
+JOBS = {"rounds": _job_rounds, "dead": _job_dead}
+
+
+# ----------------------------------------------------------------------------- tests
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("world", [2, 3])
+def test_worker_side_executes_bitwise_on_one_gpu(fake_lib, world):
+    res = _ok(_run(world, fake_lib, "rounds"), world)[0]
+    assert len(res) == 2 * len(CASES) + 1
+    for gather, m, k, n, dt, mode, ((active, how), panels), same in res:
+        assert same, (gather, m, k, n, dt, mode)
+        assert active == world
+        if gather != "host":
+            assert how == ("nccl" if gather == "1" else "fused-ipc"), (gather, how)
+        assert panels == (2 if k * n >= 64 * 2 ** 20 else 1), (m, k, n, panels)
+
+
+@pytest.mark.timeout(300)
+def test_dead_worker_named_on_one_gpu(fake_lib):
+    out = _ok(_run(2, fake_lib, "dead", timeout=240), 2)
+    r0 = out[0]
+    assert r0["type"] == "ProtocolError", r0
+    assert "rank 1" in r0["msg"], r0
+    assert r0["took"] < 60, r0
+    assert "destroy" in r0["after"] and r0["recovered"], r0
