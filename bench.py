@@ -387,9 +387,18 @@ def run_ours(args) -> None:
     import paper_1012_2273_b200 as P
 
     rank, world, local = world_from_env(args)
+    # MMWS_BENCH_ONE_GPU_WORLD=1 (tests only): every rank on GPU 0, gloo for
+    # the plumbing, with MMWS_GPU_NCCL_LIB naming tests/fake_nccl -- runs the
+    # N>1 code path of this file on one GPU; its times are not measurements
+    one_gpu = os.environ.get("MMWS_BENCH_ONE_GPU_WORLD") == "1" and world > 1
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     ctx = P.Context(local)
     if world > 1:
         P.bootstrap_comm(ctx)
@@ -406,7 +415,7 @@ def run_ours(args) -> None:
 
     def gather_all(values):
         """[per-rank list of `values`] on every rank."""
-        t = torch.tensor(values, dtype=torch.float64, device="cuda")
+        t = torch.tensor(values, dtype=torch.float64, device="cpu" if one_gpu else "cuda")
         if world == 1:
             return [values]
         out = [torch.empty_like(t) for _ in range(world)]
@@ -563,6 +572,9 @@ def run_ours(args) -> None:
     if root:
         line = {
             "metric": metric_name(), "value": value, "unit": "GFLOP/s", "n_gpus": world,
+            **({"plumbing_test": "MMWS_BENCH_ONE_GPU_WORLD: every rank on one GPU with the "
+                                 "loopback NCCL stand-in -- a code-path test, not a "
+                                 "measurement"} if one_gpu else {}),
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": DATA, "config": workload_config(n, world, args.mode),

@@ -198,3 +198,30 @@ def test_dead_worker_named_on_one_gpu(fake_lib):
     assert "rank 1" in r0["msg"], r0
     assert r0["took"] < 60, r0
     assert "destroy" in r0["after"] and r0["recovered"], r0
+
+
+@pytest.mark.timeout(900)
+def test_bench_multi_rank_line_on_one_gpu(fake_lib):
+    """bench.py's N>1 path (self-launched ranks, the row-block rounds with B in
+    k-panels, link probes, host-round e2e, fp32 rounds, per-rank gathering)
+    on one GPU with the stand-in: one complete JSON line (times meaningless)."""
+    import json
+    import sys
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    env.update(MMWS_GPU_NCCL_LIB=fake_lib, MMWS_BENCH_ONE_GPU_WORLD="1")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--n", "8192",
+                        "--n32", "8192", "--steps", "2", "--warmup", "1", "--steps32", "1",
+                        "--quick"], capture_output=True, text=True, cwd=ROOT, env=env,
+                       timeout=800)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and "plumbing_test" in d and d["value"] > 0
+    assert d["round"]["active_ranks"] == 2 and d["round"]["gather"] == "fused-ipc"
+    assert d["round"]["b_panels"] == 2 and len(d["per_rank_ms_per_step"]) == 2
+    assert d["link"]["broadcast_GBps"] > 0 and d["link"]["p2p_GBps"] > 0
+    assert d["e2e"]["value"] > 0 and d["e2e_pageable"]["value"] > 0
+    assert d["fp32"]["accuracy"]["ok"] and d["fp32"]["round"]["b_panels"] == 2
+    assert d["cpu_baseline"]["cores"] >= 1 and d["gpu_launches"] > 0
