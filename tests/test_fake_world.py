@@ -173,7 +173,51 @@ def _job_dead(P, ctx, rank, world):
     return {"type": None}
 
 
-JOBS = {"rounds": _job_rounds, "dead": _job_dead}
+def _job_ragged(P, ctx, rank, world):
+    """configs[2] over `world` ranks: N=4099 integer inputs, ragged split_rows
+    blocks (513 x 3 + 512 x 5 at 8 ranks), AUTO and EXACT -- sha256 of C
+    against the reference-generated golden; then idle ranks (m < P)."""
+    import hashlib
+    import json
+    import torch
+    ctx.tune("MMWS_GPU_ROWBLOCK_RANKS", "all")
+    out = {}
+    n = 4099
+    for name, mode in (("auto", P.MODE_AUTO), ("exact", P.MODE_EXACT)):
+        if rank == 0:
+            A = ctx.fill(P.DIST_INT8, 0, n, n)
+            B = ctx.fill(P.DIST_INT8, 1, n, n)
+            C = torch.empty_like(A)
+            ctx.rowblock(n, n, n, A, B, C, mode=mode)
+            out[name] = hashlib.sha256(C.cpu().numpy().tobytes()).hexdigest()
+            del A, B, C
+        else:
+            ctx.rowblock(n, n, n, mode=mode)
+    if rank == 0:
+        with open(os.path.join(ROOT, "tests", "golden", "ref_big.json")) as f:
+            out["golden"] = json.load(f)["n4099_int8_sha256"]
+        out["split"] = P.split_rows(n, world)
+    m = world - 2                      # idle ranks: fewer rows than ranks
+    if rank == 0:
+        A = ctx.fill(P.DIST_UNIFORM, 3, m, 33)
+        B = ctx.fill(P.DIST_UNIFORM, 4, 33, 17)
+        C = torch.full((m, 17), float("nan"), dtype=torch.float64, device="cuda")
+        ctx.rowblock(m, 17, 33, A, B, C, mode=P.MODE_EXACT)
+        out["idle"] = _same(C, ctx.dgemm(A, B, mode=P.MODE_EXACT))
+    else:
+        ctx.rowblock(m, 17, 33, mode=P.MODE_EXACT)
+    return out
+
+
+JOBS = {"rounds": _job_rounds, "dead": _job_dead, "ragged": _job_ragged}
+
+
+@pytest.mark.timeout(900)
+def test_ragged_n4099_over_8_ranks_matches_reference_golden(fake_lib):
+    res = _ok(_run(8, fake_lib, "ragged"), 8)[0]
+    assert [r for _, r in res["split"]] == [513] * 3 + [512] * 5
+    assert res["auto"] == res["golden"] and res["exact"] == res["golden"], res
+    assert res["idle"]
 
 
 # ----------------------------------------------------------------------------- tests
