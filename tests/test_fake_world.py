@@ -209,7 +209,40 @@ def _job_ragged(P, ctx, rank, world):
     return out
 
 
-JOBS = {"rounds": _job_rounds, "dead": _job_dead, "ragged": _job_ragged}
+def _job_config3(P, ctx, rank, world):
+    """configs[3] at its real size over `world` ranks (S = 2 sub-blocks, B in
+    8 k-panels): bitwise the one-GPU product, AUTO fp64 and fp32 FFMA."""
+    import torch
+    n = 16384
+    out = {}
+    for f32 in (False, True):
+        mode = P.MODE_FFMA if f32 else P.MODE_AUTO
+        if rank == 0:
+            dt = torch.float32 if f32 else torch.float64
+            dist = P.DIST_NORMAL if f32 else P.DIST_UNIFORM
+            A = ctx.fill(dist, 0, n, n, dtype=dt)
+            B = ctx.fill(dist, 1, n, n, dtype=dt)
+            C = torch.empty_like(A)
+            ctx.rowblock(n, n, n, A, B, C, mode=mode, f32=f32)
+            panels = ctx.last_b_panels
+            want = (ctx.sgemm if f32 else ctx.dgemm)(A, B, mode=mode)
+            out["f32" if f32 else "f64"] = (_same(C, want), panels, ctx.last_round)
+            del A, B, C, want
+            torch.cuda.empty_cache()
+        else:
+            ctx.rowblock(n, n, n, mode=mode, f32=f32)
+    return out
+
+
+JOBS = {"rounds": _job_rounds, "dead": _job_dead, "ragged": _job_ragged, "config3": _job_config3}
+
+
+@pytest.mark.timeout(900)
+def test_config3_at_size_over_8_ranks_bitwise(fake_lib):
+    res = _ok(_run(8, fake_lib, "config3"), 8)[0]
+    for key in ("f64", "f32"):
+        same, panels, (active, gather) = res[key]
+        assert same and panels == 8 and active == 8 and gather == "fused-ipc", (key, res[key])
 
 
 @pytest.mark.timeout(900)
