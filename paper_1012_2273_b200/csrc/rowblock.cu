@@ -9,13 +9,15 @@
 // last receive (protocol.hpp:63,105).
 //
 // Here: every rank derives (offset, rows) from split_rows itself (no
-// metadata messages), the A-slices go out as one grouped ncclSend/ncclRecv
-// batch, B is one ncclBroadcast (NVLink/NVSwitch, not P-1 re-sends), each rank
-// multiplies its slice with the same kernel configuration as a 1-GPU call --
-// per-element arithmetic does not depend on the row offset or the slice
-// height, so P-GPU results are bitwise the 1-GPU results -- and the C-slices
-// come back as one grouped receive batch into C's row blocks on rank 0.  Rank
-// 0 is master AND worker 0 (its GPU would otherwise idle).
+// metadata messages), the A-slices go out as grouped ncclSend/ncclRecv
+// batches, B as ncclBroadcasts (NVLink/NVSwitch, not P-1 re-sends; in
+// k-panels for big rounds, multiplied as they land), each rank multiplies its
+// slice with kernels whose per-element arithmetic does not depend on the row
+// offset, the slice height or a K split -- so P-GPU results are bitwise the
+// 1-GPU results -- and the workers' C rows are stored by their GEMM epilogues
+// straight into rank 0's C (CUDA IPC over NVLink; grouped C-slice messages
+// when the allocation cannot be exported).  Rank 0 is master AND worker 0 (its
+// GPU would otherwise idle).
 //
 // Failure detection (the reference's receive deadline, comm.hpp:144 /
 // net.hpp:116-132, and its dead-worker ProtocolError naming the rank,
@@ -280,12 +282,13 @@ int rowblock_active(int64_t m, int64_t n, int64_t k, int P, int elem_bytes, int 
 //     barrier.  The 80-byte handle is broadcast every call; whether the
 //     mapping works is voted on (allreduce-min) only when the handle changed,
 //     so a steady-state call needs no host round trip on rank 0;
-//   * comm order, identical on every rank: handle, [vote], B (one broadcast --
-//     all of it is needed before any output element can finish), then every
-//     rank's A-slice in S sub-blocks (grouped send/recv); without the fused
-//     gather, per sub-block s the C-slice messages (grouped send/recv into C's
-//     row block on rank 0);
-//   * a worker multiplies sub-block s as soon as B and A sub-block s landed;
+//   * comm order, identical on every rank: handle, [vote], then either B (one
+//     broadcast) and every rank's A-slice in S sub-blocks (grouped send/recv),
+//     or -- B in KP k-panels (Schedule) -- the first A sub-blocks, the B
+//     panels, the other A sub-blocks; without the fused gather, per sub-block
+//     s the C-slice messages (grouped send/recv into C's row block on rank 0);
+//   * a worker multiplies sub-block s as soon as its A rows and B landed (its
+//     first sub-block panel by panel, continuing the accumulators);
 //   * rank 0 multiplies its own rows meanwhile (it holds A and B already).
 // Every launch computes each element with the same kernel and k-order as a
 // 1-GPU launch, so the assembled C is bitwise the 1-GPU result.
