@@ -374,6 +374,11 @@ def test_one_rank_host_round_streams_b_in_panels():
         want = c.sgemm(Af, Bf).cpu().numpy()
         got, _ = c.master_run_host(Af.cpu().numpy(), Bf.cpu().numpy())
         assert np.array_equal(got.view(np.int32), want.view(np.int32))
+        # MODE_OZAKI cannot continue accumulators: its host round keeps B in one piece
+        want = c.dgemm(A, B, mode=P.MODE_OZAKI).cpu().numpy()
+        got, _ = c.master_run_host(a, b, mode=P.MODE_OZAKI)
+        assert c.last_b_panels == 1
+        assert np.array_equal(got.view(np.int64), want.view(np.int64))
         # device-resident rounds in a 1-rank world keep B in one piece
         C = torch.empty((m, n), dtype=torch.float64, device="cuda")
         c.rowblock(m, n, k, A, B, C)
