@@ -102,6 +102,14 @@ static void cpu_checks() {
   const auto id0 = G::share_unique_id(root);
   const auto id1 = G::share_unique_id(worker);
   CHECK(wire.size() == 16 && id0.size() == 128 && id0 == id1);
+  // status codes map to the reference's exception types (error.hpp)
+  CHECK_THROWS_AS(G::check(MMWS_GPU_ERR_TIMEOUT), mmws::TimeoutError);
+  CHECK_THROWS_AS(G::check(MMWS_GPU_ERR_PROTOCOL), mmws::ProtocolError);
+  CHECK_THROWS_AS(G::check(MMWS_GPU_ERR_RANK), mmws::RankError);
+  CHECK_THROWS_AS(G::check(MMWS_GPU_ERR_NCCL), G::GpuError);
+  // the drop-in's master_run defaults to the reference's bitwise contract
+  CHECK(G::contract_mode<MatrixF64>() == G::Mode::exact);
+  CHECK(G::contract_mode<MatrixF32>() == G::Mode::ffma);
 }
 
 static void gpu_checks() {
@@ -131,11 +139,15 @@ static void gpu_checks() {
   CHECK_THROWS_AS(G::matmul_threads(ctx, r23, r22, 2), mmws::DimensionError);
   CHECK_THROWS_AS(G::matmul_threads(ctx, r22, r22, 0), mmws::DomainError);
   CHECK_THROWS_AS(G::matmul_seq(ctx, r23, r22), mmws::DimensionError);
-  // master_run in a one-rank world (rank 0 is master and worker)
+  // master_run in a one-rank world (rank 0 is master and worker); the
+  // default mode keeps the reference's bitwise contract
   const MatrixF64 a = random_matrix(33, 33, 3033), b = random_matrix(33, 33, 4033);
   auto [c, elapsed] = G::master_run(ctx, a, b, G::Mode::exact);
   CHECK(bitwise_equal(c, seq(a, b)));
   CHECK(elapsed > 0.0);
+  auto [c_default, el2] = G::master_run(ctx, random_matrix(130, 257, 5), random_matrix(257, 65, 6));
+  CHECK(bitwise_equal(c_default, seq(random_matrix(130, 257, 5), random_matrix(257, 65, 6))));
+  CHECK(el2 > 0.0);
   CHECK_THROWS_AS(G::worker_run(ctx, 4, 4, 4), mmws::RankError);
   // fp32 configuration type
   MatrixF32 af(3, 2, {1, 2, 3, 4, 5, 6}), bf(2, 2, {1, 0, 0, 1});
