@@ -107,7 +107,75 @@ __global__ void __launch_bounds__(THREADS)
   }
 }
 
+// 16x16 tiles, one output per thread (256 threads): four times the CTAs of
+// the 32x32 kernel for the smallest problems; same per-element chain.
+template <bool EXACT>
+__global__ void __launch_bounds__(THREADS)
+    dgemm_small16_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
+                         int64_t ldb, double* C, int64_t ldc, int M, int N, int K, int tiles_n,
+                         const double* cin, int64_t ldcin) {
+  constexpr int T16 = 16;
+  __shared__ __align__(16) double As[2][T16][BK + 1];  // [row][k]
+  __shared__ __align__(16) double Bs[2][BK][T16 + 1];  // [k][col]
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int row0 = (blockIdx.x / tiles_n) * T16, col0 = (blockIdx.x % tiles_n) * T16;
+  // staging: A as 16 rows x 32 k (2 per thread), B as 32 k x 16 columns (2 per thread)
+  const int ar = tid >> 4, ak = (tid & 15) * 2;
+  const int bk = tid >> 3, bc = (tid & 7) * 2;
+  double ra[2], rb[2];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int r = row0 + ar, k = k0 + ak + j;
+      ra[j] = (r < M && k < K) ? A[static_cast<int64_t>(r) * lda + k] : 0.0;
+      const int kk = k0 + bk, c = col0 + bc + j;
+      rb[j] = (kk < K && c < N) ? B[static_cast<int64_t>(kk) * ldb + c] : 0.0;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      As[buf][ar][ak + j] = ra[j];
+      Bs[buf][bk][bc + j] = rb[j];
+    }
+  };
+  const int r = row0 + ty, c = col0 + tx;
+  double acc = 0.0;
+  if (cin && r < M && c < N) acc = cin[static_cast<int64_t>(r) * ldcin + c];
+  const int KT = (K + BK - 1) / BK;
+  load(0);
+  store(0);
+  __syncthreads();
+  for (int kt = 0; kt < KT; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < KT) load((kt + 1) * BK);
+#pragma unroll 8
+    for (int k = 0; k < BK; ++k) {
+      const double a = As[buf][ty][k], b = Bs[buf][k][tx];
+      if constexpr (EXACT) acc = __dadd_rn(acc, __dmul_rn(a, b));
+      else acc = fma(a, b, acc);
+    }
+    if (kt + 1 < KT) store(buf ^ 1);
+    __syncthreads();
+  }
+  if (r < M && c < N) C[static_cast<int64_t>(r) * ldc + c] = acc;
+}
+
 }  // namespace
+
+cudaError_t launch_dgemm_small16(const Launch& L, bool exact, int64_t M, int64_t N, int64_t K,
+                                 const double* A, int64_t lda, const double* B, int64_t ldb,
+                                 double* C, int64_t ldc, const double* cin, int64_t ldcin) {
+  const int tiles_m = static_cast<int>((M + 15) / 16);
+  const int tiles_n = static_cast<int>((N + 15) / 16);
+  auto kern = exact ? dgemm_small16_kernel<true> : dgemm_small16_kernel<false>;
+  kern<<<tiles_m * tiles_n, THREADS, 0, L.stream>>>(A, lda, B, ldb, C, ldc, static_cast<int>(M),
+                                                    static_cast<int>(N), static_cast<int>(K),
+                                                    tiles_n, cin, ldcin);
+  L.count();
+  return cudaGetLastError();
+}
 
 cudaError_t launch_dgemm_small(const Launch& L, bool exact, int64_t M, int64_t N, int64_t K,
                                const double* A, int64_t lda, const double* B, int64_t ldb,
@@ -123,7 +191,8 @@ cudaError_t launch_dgemm_small(const Launch& L, bool exact, int64_t M, int64_t N
 }
 
 cudaError_t preload_dgemm_small() {
-  return preload_kernels(dgemm_small_kernel<true>, dgemm_small_kernel<false>);
+  return preload_kernels(dgemm_small_kernel<true>, dgemm_small_kernel<false>,
+                         dgemm_small16_kernel<true>, dgemm_small16_kernel<false>);
 }
 
 }  // namespace mmws_impl

@@ -156,6 +156,12 @@ cudaError_t launch_dgemm_small(const Launch& L, bool exact, int64_t M, int64_t N
                                double* C, int64_t ldc, const double* cin = nullptr,
                                int64_t ldcin = 0);
 
+// Same chain on 16x16 tiles, one output per thread (more CTAs for tiny problems).
+cudaError_t launch_dgemm_small16(const Launch& L, bool exact, int64_t M, int64_t N, int64_t K,
+                                 const double* A, int64_t lda, const double* B, int64_t ldb,
+                                 double* C, int64_t ldc, const double* cin = nullptr,
+                                 int64_t ldcin = 0);
+
 // TMA-fed, warp-specialised FFMA2 fp32 GEMM with two-level (chunked)
 // accumulation (needs lda, ldb % 4 == 0 and 16-byte aligned A, B; the caller
 // packs other layouts).

@@ -185,6 +185,12 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
   // vs 262.0, 1400 353.1 vs 405.5; balanced sizes stay one-shot (1300 286.7
   // vs 301.8, 1500 432.1 vs 446.3).
   const int64_t tiles64 = ((m + 63) / 64) * ((n + 63) / 64);
+  // latency kernels (plain loads, one chain per element): 16x16 tiles with
+  // one output per thread while 32x32 tiles would not give every SM one --
+  // 4x the CTAs; device time per call, 32x32 vs 16x16 (round 2): DFMA N=50
+  // 6.2 vs 4.2 us, 64 6.2 vs 4.2, 96 7.0 vs 6.2; exact N=96 7.2 vs 6.2, 128
+  // 8.2 vs 6.2, 160 10.3 vs 8.2, 256 14.4 vs 12.4; same chain, same bits
+  const bool small16 = ((m + 31) / 32) * ((n + 31) / 32) < G;
   const bool sk64 = mode == MMWS_GPU_MODE_EXACT && tiles128 < G && tiles64 >= G && sk_ok &&
                     10 * tiles64 < 9 * (((tiles64 + G - 1) / G) * G);
   // TMA needs 16-byte aligned bases and even row pitches: pack A and/or B into
@@ -224,8 +230,13 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
     // cp.async kernel for layouts TMA cannot read -- every variant gives
     // matmul_seq's bits
     if (n <= 256 && k <= 256) {
-      e = launch_dgemm_small(L, true, m, n, k, A, lda, B, ldb, C, ldc, cin, ldcin);
-      ctx->last_plan = "dgemm_small_kernel<exact, 32x32>";
+      if (small16) {
+        e = launch_dgemm_small16(L, true, m, n, k, A, lda, B, ldb, C, ldc, cin, ldcin);
+        ctx->last_plan = "dgemm_small_kernel<exact, 16x16>";
+      } else {
+        e = launch_dgemm_small(L, true, m, n, k, A, lda, B, ldb, C, ldc, cin, ldcin);
+        ctx->last_plan = "dgemm_small_kernel<exact, 32x32>";
+      }
     } else if (sk || sk64) {
       if (int rc = sk_workspace(ctx, L.stream, &sk_partial, &sk_flags)) return rc;
       if (int rc = pack_operands()) return rc;
@@ -263,8 +274,13 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
     // are faster (GPU time per call: N=128 6.1 vs 8.2 us, 200 6.2 vs 12.3,
     // 256 8.2 vs 13.4; tools/dmma_plan_probe.py); up to 96 it stays, so the
     // latency server (server.cu, N <= 96, same DFMA chain) matches AUTO
-    e = launch_dgemm_small(L, false, m, n, k, A, lda, B, ldb, C, ldc, cin, ldcin);
-    ctx->last_plan = "dgemm_small_kernel<DFMA, 32x32>";
+    if (small16) {
+      e = launch_dgemm_small16(L, false, m, n, k, A, lda, B, ldb, C, ldc, cin, ldcin);
+      ctx->last_plan = "dgemm_small_kernel<DFMA, 16x16>";
+    } else {
+      e = launch_dgemm_small(L, false, m, n, k, A, lda, B, ldb, C, ldc, cin, ldcin);
+      ctx->last_plan = "dgemm_small_kernel<DFMA, 32x32>";
+    }
     return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm small");
   }
   if (int rc = pack_operands()) return rc;
