@@ -234,7 +234,35 @@ def _job_config3(P, ctx, rank, world):
     return out
 
 
-JOBS = {"rounds": _job_rounds, "dead": _job_dead, "ragged": _job_ragged, "config3": _job_config3}
+def _job_slow(P, ctx, rank, world):
+    """test_protocol.cpp:160-168: a worker that stalls before serving is waited
+    for (no false deadline), and the round's result is still exact."""
+    import torch
+    ctx.set_timeout(5)
+    ctx.tune("MMWS_GPU_ROWBLOCK_RANKS", "all")
+    n = 300
+    if rank == 1:
+        time.sleep(3)                   # stalls before the round, within the deadline
+    if rank != 0:
+        ctx.rowblock(n, n, n, mode=P.MODE_EXACT)
+        return None
+    A = ctx.fill(P.DIST_UNIFORM, 71, n, n)
+    B = ctx.fill(P.DIST_UNIFORM, 72, n, n)
+    C = torch.empty_like(A)
+    t0 = time.time()
+    el = ctx.rowblock(n, n, n, A, B, C, mode=P.MODE_EXACT)
+    return {"same": _same(C, ctx.dgemm(A, B, mode=P.MODE_EXACT)), "waited": time.time() - t0,
+            "elapsed": el}
+
+
+JOBS = {"rounds": _job_rounds, "dead": _job_dead, "ragged": _job_ragged, "config3": _job_config3,
+        "slow": _job_slow}
+
+
+@pytest.mark.timeout(300)
+def test_slow_worker_is_waited_for(fake_lib):
+    res = _ok(_run(3, fake_lib, "slow", timeout=240), 3)[0]
+    assert res["same"] and res["waited"] > 2.0 and res["elapsed"] > 0, res
 
 
 @pytest.mark.timeout(900)
