@@ -21,6 +21,7 @@ struct Tuning {
   int rowblock_ranks = 0;       // MMWS_GPU_ROWBLOCK_RANKS: 0 cost model, -1 "all", 1 rank 0 alone
   int server_ctas = 0;          // MMWS_GPU_SERVER_CTAS (0 = default)
   int copy_threads = 0;         // MMWS_GPU_COPY_THREADS (0 = 3/4 of the host cores, <= 12)
+  int host_panels = 0;          // MMWS_GPU_HOST_PANELS: row panels of a host-buffer multiply (0 = built-in)
   double timeout_s = 30.0;      // MMWS_GPU_TIMEOUT_S: deadline of one distributed step
   bool nccl_gather = false;     // MMWS_GPU_NCCL_GATHER: C-slices as NCCL messages, no fused IPC
   static Tuning from_env();

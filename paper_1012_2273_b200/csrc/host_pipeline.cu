@@ -379,20 +379,28 @@ int host_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A
   T* dC = static_cast<T*>(ctx->dC);
   cudaStream_t in = ctx->copy_in, comp = ctx->stream, out = ctx->copy_out;
 
-  // Panels of 1/8 of the rows (multiples of 128) once the problem is big
-  // enough for the overlap to matter; one panel otherwise.  Pinned buffers
-  // pipeline from m*n*k = 1e8 on (host-buffer multiply, min of 25 interleaved
-  // calls: N=750 260.5 vs 292.4 us, 1000 415.2 vs 514.7, 1250 648.5 vs
-  // 818.8); pageable ones only from 2e9, because every panel's copy is
-  // pumped through the pinned staging ring in chunks of its own (N=1000 with
-  // 8 panels: 2.2 ms vs 1.3 ms in one).
+  // Row panels (multiples of 128 rows) once the problem is big enough for the
+  // overlap to matter (m*n*k >= 1e8); one panel otherwise.  Pinned buffers:
+  // 1/8 of the rows (host-buffer multiply, min of 25 interleaved calls: N=750
+  // 260.5 vs 292.4 us in one panel, 1000 415.2 vs 514.7, 1250 648.5 vs
+  // 818.8).  Pageable buffers: every panel's copy is pumped through the
+  // pinned staging ring by the host copy pool in chunks of its own, so fewer,
+  // bigger panels -- 4 below 1.5e9, 2 below 4.5e9, 3 below 1.5e10, 8 above
+  // (min of 20 interleaved calls, tools/host_panels_probe.py, 1 / 2 / 3 / 4 /
+  // 8 panels: N=500 236 / 208 / 207 / 194 / 187 us, 1000 836 / 727 / 719 /
+  // 726 / 715, 1500 2177 / 1356 / 1576 / 1613 / 1622, 1750 2692 / 2281 /
+  // 2087 / 2239 / 2271, 2100 4892 / 3078 / 2668 / 2847 / 3196; the steps
+  // follow how the panels' copies fall into staging chunks).
+  // MMWS_GPU_HOST_PANELS overrides the count; the bits never change.
   const double work = static_cast<double>(m) * n * k;
   const bool pinned = !is_pageable(A) && !is_pageable(C);
-  const double min_work = pinned ? 1.0e8 : 2.0e9;
+  int want = work < 1.0e8 ? 1 : 8;
+  if (!pinned && want > 1) want = work < 1.5e9 ? 4 : work < 4.5e9 ? 2 : work < 1.5e10 ? 3 : 8;
+  if (ctx->tune.host_panels > 0 && work >= 1.0e7) want = ctx->tune.host_panels;
   // small MODE_OZAKI problems would recompute B's residues per launch: one panel
-  const int64_t R = (work < min_work || mode == MMWS_GPU_MODE_OZAKI)
+  const int64_t R = (want <= 1 || mode == MMWS_GPU_MODE_OZAKI)
                         ? m
-                        : std::max<int64_t>(128, ((m + 7) / 8 + 127) / 128 * 128);
+                        : std::max<int64_t>(128, ((m + want - 1) / want + 127) / 128 * 128);
   const int64_t panels = (m + R - 1) / R;
   // column blocks never narrower than 512 unless n itself is: a block then
   // takes the same kernel as the whole problem (see dgemm_dispatch).  A

@@ -50,6 +50,8 @@ bool Tuning::set(const char* name, const char* v) {
     server_ctas = v ? std::atoi(v) : d.server_ctas;
   } else if (!std::strcmp(name, "MMWS_GPU_COPY_THREADS")) {
     copy_threads = v ? std::clamp(std::atoi(v), 1, 64) : d.copy_threads;
+  } else if (!std::strcmp(name, "MMWS_GPU_HOST_PANELS")) {
+    host_panels = v ? std::clamp(std::atoi(v), 0, 64) : d.host_panels;
   } else if (!std::strcmp(name, "MMWS_GPU_TIMEOUT_S")) {
     const double s = v ? std::atof(v) : 0.0;
     timeout_s = s > 0 ? s : d.timeout_s;
@@ -65,7 +67,8 @@ Tuning Tuning::from_env() {
   Tuning t;
   for (const char* name : {"MMWS_GPU_NO_STREAMK", "MMWS_GPU_DMMA_PLAN", "MMWS_GPU_RASTER_GROUP",
                            "MMWS_GPU_PIPELINE_TRACE", "MMWS_GPU_ROWBLOCK_RANKS",
-                           "MMWS_GPU_SERVER_CTAS", "MMWS_GPU_COPY_THREADS", "MMWS_GPU_TIMEOUT_S",
+                           "MMWS_GPU_SERVER_CTAS", "MMWS_GPU_COPY_THREADS", "MMWS_GPU_HOST_PANELS",
+                           "MMWS_GPU_TIMEOUT_S",
                            "MMWS_GPU_NCCL_GATHER"})
     if (const char* v = std::getenv(name)) t.set(name, v);
   return t;

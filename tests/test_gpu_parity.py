@@ -607,8 +607,9 @@ def test_host_entry_matches_device_entry(ctx, oracle):
 
 
 def test_host_entry_pinned_panels_match_pageable_and_device(ctx, oracle):
-    # pinned host buffers take the row-panel pipeline from m*n*k = 1e8 on,
-    # pageable ones from 2e9: same bits either way, and the device entry's
+    # host buffers take the row-panel pipeline from m*n*k = 1e8 on (8 panels
+    # pinned; 4 / 2 / 8 pageable by size): same bits either way, and the
+    # device entry's
     T = torch()
     for (m, k, n) in [(700, 600, 900), (1001, 999, 1003), (333, 2000, 700)]:
         a = oracle.fill(oracle.DIST_UNIFORM, 7, m, k)
@@ -624,6 +625,28 @@ def test_host_entry_pinned_panels_match_pageable_and_device(ctx, oracle):
         ex, _ = ctx.matmul_host(ap, bp, mode=P.MODE_EXACT, out=cp)
         rows = [0, m // 2, m - 1]
         assert (bits(ex[rows]) == bits(oracle.matmul_rows(rows, a, b))).all()
+
+
+def test_host_entry_any_panel_count_gives_the_same_bits(ctx, oracle):
+    # MMWS_GPU_HOST_PANELS forces the row-panel count of a host-buffer
+    # multiply: every count (one panel .. more panels than 128-row bands)
+    # gives the device entry's bits, pageable and pinned, AUTO and EXACT
+    T = torch()
+    m, k, n = 777, 515, 1029
+    a = oracle.fill(oracle.DIST_UNIFORM, 31, m, k)
+    b = oracle.fill(oracle.DIST_UNIFORM, 32, k, n)
+    ap = T.from_numpy(a).pin_memory().numpy()
+    bp = T.from_numpy(b).pin_memory().numpy()
+    try:
+        for mode in (P.MODE_AUTO, P.MODE_EXACT):
+            want = bits(host(ctx.dgemm(dev(a), dev(b), mode=mode)))
+            for panels in ("1", "2", "3", "4", "8", "64"):
+                ctx.tune("MMWS_GPU_HOST_PANELS", panels)
+                for x, y in ((a, b), (ap, bp)):
+                    got, _ = ctx.matmul_host(x, y, mode=mode)
+                    assert (bits(got) == want).all(), (mode, panels, x.flags.c_contiguous)
+    finally:
+        ctx.tune("MMWS_GPU_HOST_PANELS", "0")
 
 
 @pytest.mark.timeout(180, method="thread")
