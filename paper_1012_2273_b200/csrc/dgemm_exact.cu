@@ -136,7 +136,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 // DADD -- no cp.async address arithmetic, no __syncthreads per k-tile.  Stages
 // are released one iteration late (see dgemm_dmma.cu).  Zero-filled TMA
 // out-of-bounds boxes are the (+0)*(+0) padding discussed above.
-// TBM x TBN tiles (128x128, or 64x64 for problems that would leave SMs idle);
+// TBM x TBN tiles (128x128, or 64x64 / 32x32 for problems that would leave
+// SMs idle);
 // each of the 256 math threads owns (TBM/16) x (TBN/16) outputs at rows
 // 2*ty + 32v + h and columns 2*tx + 32v + h.
 constexpr int T_STAGES = 4, T_CONSUMERS = 8, T_THREADS = (T_CONSUMERS + 4) * 32;
@@ -146,7 +147,7 @@ struct ExactTma {
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int SMEM = T_STAGES * STAGE + 2 * T_STAGES * 8 + 128;
   static constexpr int TM = TBM / 16, TN = TBN / 16;  // outputs per thread
-  static constexpr int MINB = TBM == 128 ? 1 : 2;
+  static constexpr int MINB = TBM == 128 ? 1 : TBM == 64 ? 2 : 4;
 };
 
 // SK = true: stream-K with in-order fix-up, exactly as dgemm_dmma.cu's MODE 2
@@ -402,13 +403,33 @@ cudaError_t launch_dgemm_exact_sk(const Launch& L, int tile, int64_t M, int64_t 
                                              grid);
 }
 
+const char* exact_oneshot_plan(const Launch& L, int64_t M, int64_t N, const double* A,
+                               int64_t lda, const double* B, int64_t ldb) {
+  if (!exact_tma_ok(lda, ldb, A, B)) return "dgemm_exact_kernel<128x128, cp.async>";
+  const int64_t tiles64 = ((M + 63) / 64) * ((N + 63) / 64);
+  const int64_t tiles128 = ((M + 127) / 128) * ((N + 127) / 128);
+  if (2 * tiles64 <= L.num_sms) return "dgemm_exact_tma_kernel<32x32>";
+  return tiles128 < 2 * L.num_sms ? "dgemm_exact_tma_kernel<64x64>"
+                                  : "dgemm_exact_tma_kernel<128x128>";
+}
+
 cudaError_t launch_dgemm_exact(const Launch& L, int64_t M, int64_t N, int64_t K, const double* A,
                                int64_t lda, const double* B, int64_t ldb, double* C,
                                int64_t ldc, const double* cin, int64_t ldcin) {
   const int tiles_m = static_cast<int>((M + BM - 1) / BM);
   const int tiles_n = static_cast<int>((N + BN - 1) / BN);
   if (exact_tma_ok(lda, ldb, A, B)) {  // TMA can describe both operands
-    // 64x64 tiles while 128x128 ones would not give every SM two CTAs
+    // 32x32 tiles while 64x64 ones would not give half the SMs one (device
+    // time per call, 64x64 vs 32x32, round 2, tools/exact_plan_probe.py:
+    // N=400 33.7 vs 24.8 us, 500 42.8 vs 32.0, 128x500x500 41.1 vs 20.6,
+    // 128x1000x1000 78.0 vs 38.6, 256x1000x1000 78.7 vs 58.2; from ~100
+    // 64x64 tiles on the bigger tile wins: N=640 52.7 vs 55.4, 700 58.2 vs
+    // 78.7, 256x2000x2000 153.9 vs 211.8), then 64x64 tiles while 128x128
+    // ones would not give every SM two CTAs
+    const int64_t tiles64 = ((M + 63) / 64) * ((N + 63) / 64);
+    if (2 * tiles64 <= L.num_sms)
+      return run_exact_tma<32, 32>(L, M, N, K, A, lda, B, ldb, C, ldc, nullptr, nullptr, 0, cin,
+                                   ldcin);
     return tiles_m * tiles_n < 2 * L.num_sms
                ? run_exact_tma<64, 64>(L, M, N, K, A, lda, B, ldb, C, ldc, nullptr, nullptr, 0,
                                        cin, ldcin)
@@ -431,7 +452,8 @@ cudaError_t launch_dgemm_exact(const Launch& L, int64_t M, int64_t N, int64_t K,
 }
 
 cudaError_t preload_dgemm_exact() {
-  return preload_kernels(dgemm_exact_tma_kernel<64, 64>, dgemm_exact_tma_kernel<128, 128>,
+  return preload_kernels(dgemm_exact_tma_kernel<32, 32>, dgemm_exact_tma_kernel<64, 64>,
+                         dgemm_exact_tma_kernel<128, 128>,
                          dgemm_exact_tma_kernel<128, 128, true>, dgemm_exact_tma_kernel<64, 64, true>,
                          dgemm_exact_kernel<true, true>, dgemm_exact_kernel<true, false>,
                          dgemm_exact_kernel<false, true>, dgemm_exact_kernel<false, false>);

@@ -141,6 +141,9 @@ cudaError_t launch_dgemm_dmma(const Launch& L, int cfg, int64_t M, int64_t N, in
 // matmul_seq); same workspace contract as launch_dgemm_dmma_sk, tiles >= grid.
 // exact_tma_ok: the layout the TMA kernels (and so this one) accept.
 bool exact_tma_ok(int64_t lda, int64_t ldb, const double* A, const double* B);
+// the kernel launch_dgemm_exact picks for these arguments (for last_plan)
+const char* exact_oneshot_plan(const Launch& L, int64_t M, int64_t N, const double* A,
+                               int64_t lda, const double* B, int64_t ldb);
 cudaError_t launch_dgemm_exact_sk(const Launch& L, int tile, int64_t M, int64_t N, int64_t K,
                                   const double* A, int64_t lda, const double* B, int64_t ldb,
                                   double* C, int64_t ldc, double* partial, int* flags, int grid);

@@ -226,13 +226,18 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
   double* sk_partial = nullptr;
   int* sk_flags = nullptr;
   if (mode == MMWS_GPU_MODE_EXACT) {
-    // exact order: the 32x32 latency kernel for tiny problems, the stream-K
-    // form of the 128x128 TMA kernel (operands packed if needed) from one
-    // tile per SM, of the 64x64 one below that where a one-shot launch would
-    // load the SMs unevenly, else the 64x64 / 128x128 TMA kernels or the
-    // cp.async kernel for layouts TMA cannot read -- every variant gives
-    // matmul_seq's bits
-    if (n <= 320 && k <= 320) {  // N=300: 20.8 us vs 26.9 for the 64x64 TMA stream-K
+    // exact order: the latency kernels for tiny problems -- plain loads, any
+    // layout -- up to n, k <= 192 (above that the 32x32 TMA tiles win;
+    // device time per call, latency kernel vs 32x32 TMA, round 2: N=128 6.3
+    // vs 8.3 us, 160 8.3 vs 8.4, 200 12.0 vs 10.4, 300 20.6 vs 14.4) and up
+    // to 320 for layouts TMA cannot read; the stream-K form of the 128x128
+    // TMA kernel (operands packed if needed) from one tile per SM, of the
+    // 64x64 one below that where a one-shot launch would load the SMs
+    // unevenly; else the 32x32 / 64x64 / 128x128 TMA kernels or the cp.async
+    // kernel for layouts TMA cannot read -- every variant gives matmul_seq's
+    // bits
+    if ((n <= 192 && k <= 192) ||
+        (n <= 320 && k <= 320 && !exact_tma_ok(lda, ldb, A, B))) {
       if (small16) {
         e = launch_dgemm_small16(L, true, m, n, k, A, lda, B, ldb, C, ldc, cin, ldcin);
         ctx->last_plan = "dgemm_small_kernel<exact, 16x16>";
@@ -249,7 +254,7 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
                           : "dgemm_exact_tma_kernel<64x64, stream-K>";
     } else {
       e = launch_dgemm_exact(L, m, n, k, A, lda, B, ldb, C, ldc, cin, ldcin);
-      ctx->last_plan = "dgemm_exact (one-shot)";
+      ctx->last_plan = exact_oneshot_plan(L, m, n, A, lda, B, ldb);
     }
     return e == cudaSuccess ? ok() : cuda_fail(e, "dgemm exact");
   }

@@ -880,8 +880,38 @@ def test_auto_tile_plan_by_size(ctx):
     assert ctx.last_plan == "dgemm_exact_tma_kernel<64x64, stream-K>"
     A = T.zeros((1300, 1300), dtype=T.float64, device="cuda")
     ctx.dgemm(A, A, mode=P.MODE_EXACT)             # 441 tiles: 2.98 per SM, one-shot
-    assert ctx.last_plan == "dgemm_exact (one-shot)"
+    assert ctx.last_plan == "dgemm_exact_tma_kernel<64x64>"
+    A = T.zeros((500, 500), dtype=T.float64, device="cuda")
+    ctx.dgemm(A, A, mode=P.MODE_EXACT)             # 64 tiles of 64x64: 32x32 tiles
+    assert ctx.last_plan == "dgemm_exact_tma_kernel<32x32>"
+    A = T.zeros((160, 160), dtype=T.float64, device="cuda")
+    ctx.dgemm(A, A, mode=P.MODE_EXACT)
+    assert ctx.last_plan.startswith("dgemm_small_kernel<exact")
     T.cuda.synchronize()
+
+
+@pytest.mark.parametrize("shape", [(193, 200, 202), (500, 500, 500), (128, 1000, 998),
+                                   (257, 32, 300), (33, 700, 1000), (640, 18, 250)])
+def test_exact_32x32_tma_tiles_are_matmul_seq(ctx, oracle, shape):
+    # the 32x32 exact TMA plan (few-tile problems): ragged M / N edges, K not
+    # a multiple of the 16-wide k-stage; bitwise the reference chain, and
+    # bitwise the other exact kernels (latency kernel / cp.async layout)
+    m, k, n = shape
+    a = oracle.fill(oracle.DIST_UNIFORM, 61, m, k)
+    b = oracle.fill(oracle.DIST_UNIFORM, 62, k, n)
+    got = host(ctx.dgemm(dev(a), dev(b), mode=P.MODE_EXACT))
+    assert ctx.last_plan == "dgemm_exact_tma_kernel<32x32>", (shape, ctx.last_plan)
+    if m * n * k <= 40_000_000:
+        assert oracle.first_difference(got, oracle.matmul_seq(a, b)) is None, shape
+    else:
+        rows = [0, 1, m // 2, m - 1]
+        assert (bits(got[rows]) == bits(oracle.matmul_rows(rows, a, b))).all(), shape
+    # an odd row pitch sends the same problem to the plain-load kernels
+    T = torch()
+    big_a = T.zeros((m, k + 1), dtype=T.float64, device="cuda")
+    big_a[:, :k] = dev(a)
+    other = host(ctx.dgemm(big_a[:, :k], dev(b), mode=P.MODE_EXACT))
+    assert (bits(other) == bits(got)).all(), shape
 
 
 # ----------------------------------------------------------------------------- round-2 fixes
