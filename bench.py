@@ -796,6 +796,11 @@ def measure_sweep(ctx, P, torch, np):
         reps = 20 if n <= 500 else 8
         inner = 20 if n <= 1000 else 3
         t = dev_time(lambda: ctx.dgemm(A, B, C), reps, inner)
+        # EXACT (bitwise matmul_seq): what the C++ drop-in's matmul_seq /
+        # matmul_threads / master_run run by default
+        plan = ctx.last_plan
+        tx = dev_time(lambda: ctx.dgemm(A, B, C, mode=P.MODE_EXACT), reps, inner)
+        plan_x = ctx.last_plan
         g = ctx.graph_dgemm(A, B, C)
         tg = dev_time(lambda: g.launch(), reps, inner)
         tw, tw_med = wall(lambda: ctx.dgemm(A, B, C), reps)
@@ -812,8 +817,10 @@ def measure_sweep(ctx, P, torch, np):
             th.append(time.perf_counter() - t0)
         flops = 2.0 * n ** 3
         byt = 3 * 8.0 * n * n
-        out.append({"n": n, "plan": ctx.last_plan,
+        out.append({"n": n, "plan": plan,
                     "device_us": t * 1e6, "graph_device_us": tg * 1e6,
+                    "exact_plan": plan_x, "exact_device_us": tx * 1e6,
+                    "gflops_exact_device": 2.0 * n ** 3 / tx / 1e9,
                     "launch_wall_us": tw * 1e6, "graph_wall_us": tgw * 1e6,
                     "graph_wall_median_us": tgw_med * 1e6,
                     "host_entry_wall_us": min(th) * 1e6,
