@@ -162,7 +162,11 @@ int mmws_gpu_sgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const flo
  * into panels at multiples of 16 (fp64) / 1024 (fp32, the partial-sum chunk)
  * and chaining the calls (the first from +0.0 via mmws_gpu_dgemm / _sgemm)
  * therefore gives bitwise the one-call result -- what the row-block workers
- * use to multiply while B is still arriving.  All modes but OZAKI. */
+ * use to multiply while B is still arriving -- as long as every call takes
+ * the same kernel family as the one call: always in MODE_DMMA, MODE_DMMA_SMALL
+ * and MODE_EXACT; in MODE_AUTO unless a piece falls under the DFMA latency
+ * kernel's limit (n <= 96 and k <= 96) while the whole does not (or the
+ * reverse).  All modes but OZAKI. */
 int mmws_gpu_dgemm_acc(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
                        int64_t lda, const double* B, int64_t ldb, const double* Cin,
                        int64_t ldcin, double* C, int64_t ldc, int mode, void* stream);

@@ -272,7 +272,9 @@ class Context:
     # -- device-pointer multiply (torch CUDA tensors)
     def dgemm(self, A, B, C_=None, mode: int = MODE_AUTO, stream=None, accumulate=None):
         """C_ = A . B; with `accumulate`, C_ = accumulate + A . B continuing its
-        chains (mmws_gpu_dgemm_acc; `accumulate` may be C_ itself)."""
+        chains (mmws_gpu_dgemm_acc; `accumulate` may be C_ itself; K splits are
+        bitwise the one call when every call takes the same kernel family --
+        see include/mmws_gpu.h)."""
         import torch
         m, n, k = _device_operands(A, B, C_, torch.float64, "dgemm")
         if C_ is None:
