@@ -274,7 +274,10 @@ int mmws_gpu_comm_destroy(mmws_gpu_ctx* ctx);
  * gather), or as NCCL C-slice messages when the allocation cannot be
  * IPC-exported; ranks with rows_r == 0 still take part (protocol.hpp:122-123).  *elapsed_s
  * (rank 0, optional) is first send -> last receive measured on the device
- * (the bracket of protocol.hpp:63,105).  Synchronous on return. */
+ * (the bracket of protocol.hpp:63,105).  Synchronous on return.  The round is
+ * queued on the context stream (mmws_gpu_stream): A and B written on another
+ * stream must be ordered before the call (an event wait on the context
+ * stream, or a synchronisation of the producing stream). */
 int mmws_gpu_rowblock_dgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k,
                             const double* A, const double* B, double* C, int mode,
                             double* elapsed_s);

@@ -415,6 +415,12 @@ class Context:
                                      f"{tuple(C_.shape)} do not match m={m} n={n} k={k}")
             if not (A.is_contiguous() and B.is_contiguous() and C_.is_contiguous()):
                 raise DimensionError("rowblock: A, B and C must be dense (contiguous)")
+        # The round runs on the context's own stream (mmws_gpu.h): order it
+        # after the work already queued on torch's current stream (e.g. the
+        # kernels that produced A and B), as every other call here is.
+        import torch
+        torch.cuda.ExternalStream(self.stream, device=f"cuda:{self.device}").wait_stream(
+            torch.cuda.current_stream(self.device))
         el = C.c_double(0.0)
         fn = _lib().mmws_gpu_rowblock_sgemm if f32 else _lib().mmws_gpu_rowblock_dgemm
         _check(fn(self._h, m, n, k, _ptr(A) if A is not None else None,

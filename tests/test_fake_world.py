@@ -255,8 +255,68 @@ def _job_slow(P, ctx, rank, world):
             "elapsed": el}
 
 
+def _job_random(P, ctx, rank, world):
+    """Seeded random rounds (every rank draws the same sequence): shapes from
+    1 row to B in k-panels, ragged and idle-rank splits, AUTO / EXACT / DMMA
+    fp64 and FFMA fp32, both gathers, device and host entries -- rank 0
+    compares each round with its own one-GPU product, bitwise."""
+    import torch
+    rng = np.random.default_rng(4242)
+    modes = [("auto", P.MODE_AUTO, False), ("exact", P.MODE_EXACT, False),
+             ("dmma", P.MODE_DMMA, False), ("ffma", P.MODE_FFMA, True)]
+    ctx.tune("MMWS_GPU_ROWBLOCK_RANKS", "all")
+    res = []
+    for case in range(24):
+        r = rng.random()
+        if r < 0.3:
+            m, k, n = (int(v) for v in rng.integers(1, 40, size=3))
+        elif r < 0.85:
+            m, k, n = (int(v) for v in rng.integers(40, 1500, size=3))
+        else:  # B in k-panels: k * n >= 64 Mi elements
+            m, k, n = int(rng.integers(600, 2500)), 8192, int(rng.integers(8192, 9000))
+        name, mode, f32 = modes[int(rng.integers(0, len(modes)))]
+        gather = None if rng.random() < 0.6 else "1"
+        host = not f32 and rng.random() < 0.25
+        ctx.tune("MMWS_GPU_NCCL_GATHER", gather)
+        tdt = torch.float32 if f32 else torch.float64
+        dist = P.DIST_NORMAL if f32 else [P.DIST_UNIFORM, P.DIST_INT8][case % 2]
+        if rank == 0:
+            A = ctx.fill(dist, 100 + case, m, k, dtype=tdt)
+            B = ctx.fill(dist, 200 + case, k, n, dtype=tdt)
+            want = (ctx.sgemm if f32 else ctx.dgemm)(A, B, mode=mode)
+            if host:
+                got, _ = ctx.master_run_host(A.cpu().numpy(), B.cpu().numpy(), mode=mode)
+                got = torch.from_numpy(got)
+            else:
+                C = torch.full((m, n), float("nan"), dtype=tdt, device="cuda")
+                ctx.rowblock(m, n, k, A, B, C, mode=mode, f32=f32)
+                got = C.cpu()
+            torch.cuda.synchronize()
+            w = want.cpu()
+            iv = torch.int32 if f32 else torch.int64
+            rows_bad = (got.view(iv) != w.view(iv)).any(dim=1).nonzero().flatten().tolist()
+            same = not rows_bad
+            res.append((case, m, k, n, name, gather, host, ctx.last_round, ctx.last_b_panels,
+                        rows_bad[:3] + ([len(rows_bad)] if rows_bad else []), same))
+            del A, B, want
+        elif host:
+            ctx.master_run_host(None, None, None, mode=mode, m=m, n=n, k=k)
+        else:
+            ctx.rowblock(m, n, k, mode=mode, f32=f32)
+    return res
+
+
 JOBS = {"rounds": _job_rounds, "dead": _job_dead, "ragged": _job_ragged, "config3": _job_config3,
-        "slow": _job_slow}
+        "slow": _job_slow, "random": _job_random}
+
+
+@pytest.mark.timeout(900)
+def test_random_rounds_bitwise_over_3_ranks(fake_lib):
+    res = _ok(_run(3, fake_lib, "random"), 3)[0]
+    assert len(res) == 24
+    bad = [r for r in res if not r[-1]]
+    if bad:
+        pytest.fail(f"rounds differing from the one-GPU product: {bad}")
 
 
 @pytest.mark.timeout(300)

@@ -493,6 +493,23 @@ def test_rowblock_single_rank_entry(ctx, oracle):
     assert oracle.first_difference(host(C), want) is None
 
 
+def test_rowblock_orders_after_the_callers_stream(ctx):
+    # the round runs on the context stream; the Python entry orders it after
+    # torch's current stream, where fill queued A and B behind a long sleep
+    # (found by the randomized one-GPU-world rounds: without the ordering a
+    # round could read its inputs before they were written)
+    T = torch()
+    n = 512
+    for _ in range(2):
+        T.cuda._sleep(100_000_000)                      # ~50 ms on the current stream
+        A = ctx.fill(P.DIST_UNIFORM, 91, n, n)
+        B = ctx.fill(P.DIST_UNIFORM, 92, n, n)
+        C = T.full((n, n), float("nan"), dtype=T.float64, device="cuda")
+        ctx.rowblock(n, n, n, A, B, C)
+        want = ctx.dgemm(A, B)
+        assert (bits(host(C)) == bits(host(want))).all()
+
+
 def test_rowblock_nccl_path_single_rank(oracle):
     # The NCCL engine (dlopen of the process's libnccl, communicator, broadcast,
     # grouped exchanges, two sub-blocks, stream joins) in a 1-rank world -- the
