@@ -71,11 +71,17 @@ struct mmws_gpu_ctx {
   std::mutex mu;
   mmws_impl::Tuning tune;
 
-  // packing / MODE_OZAKI workspace (device), grown on demand.  While a CUDA
-  // graph is built, ws_cur points at that graph's own workspace instead, so a
-  // replay never shares (or outlives) the eager calls' buffer.
-  void* ws = nullptr;
-  size_t ws_bytes = 0;
+  // packing / MODE_OZAKI workspaces (device), one per launch stream, grown on
+  // demand: stream order keeps each one safe, and a call on one stream never
+  // overwrites the workspace a call still running on another stream reads.
+  // While a CUDA graph is built, ws_cur points at that graph's own workspace
+  // instead, so a replay never shares (or outlives) the eager calls' buffers.
+  struct WsSpace {
+    cudaStream_t stream;
+    void* mem;
+    size_t bytes;
+  };
+  std::vector<WsSpace> ws_spaces;
   void** ws_cur = nullptr;
   size_t* ws_cur_bytes = nullptr;
   // stream-K workspaces, one per launch stream (fixed size, never moved):
@@ -137,11 +143,24 @@ int ok();
 // cudaFree (a device-wide synchronisation) would wait for it forever, so the
 // old buffer is parked in deferred_free instead (growth at least doubles).
 cudaError_t ensure(mmws_gpu_ctx* ctx, void** buf, size_t* have, size_t bytes);
-// The current multiply workspace (the context's, or the graph's being built),
-// at least `bytes` long.
-inline cudaError_t workspace(mmws_gpu_ctx* ctx, size_t bytes, void** out) {
-  void** buf = ctx->ws_cur ? ctx->ws_cur : &ctx->ws;
-  size_t* have = ctx->ws_cur ? ctx->ws_cur_bytes : &ctx->ws_bytes;
+// The multiply workspace for work queued on `stream` (NULL: the context
+// stream) -- that stream's own, or the graph's being built -- at least
+// `bytes` long.
+inline cudaError_t workspace(mmws_gpu_ctx* ctx, size_t bytes, void** out, cudaStream_t stream) {
+  void** buf = ctx->ws_cur;
+  size_t* have = ctx->ws_cur_bytes;
+  if (!buf) {
+    const cudaStream_t s = stream ? stream : ctx->stream;
+    mmws_gpu_ctx::WsSpace* sp = nullptr;
+    for (auto& w : ctx->ws_spaces)
+      if (w.stream == s) sp = &w;
+    if (!sp) {
+      ctx->ws_spaces.push_back({s, nullptr, 0});
+      sp = &ctx->ws_spaces.back();
+    }
+    buf = &sp->mem;
+    have = &sp->bytes;
+  }
   const cudaError_t e = ensure(ctx, buf, have, bytes);
   *out = *buf;
   return e;

@@ -233,7 +233,8 @@ int host_multiply_ozaki(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, cons
   const int64_t panels = (m + R - 1) / R;
   const size_t ws = sizeof(T) == 8 ? ozaki_workspace_bytes(R, n, k) : ozaki_workspace_bytes_f32(R, n, k);
   cudaError_t e;
-  if ((e = ensure(ctx, &ctx->ws, &ctx->ws_bytes, ws)) != cudaSuccess)
+  void* wsp = nullptr;
+  if ((e = workspace(ctx, ws, &wsp, ctx->stream)) != cudaSuccess)
     return cuda_fail(e, "matmul ozaki: workspace");
   if ((e = event_pool(ctx, panels * 2 + 1)) != cudaSuccess)
     return cuda_fail(e, "matmul ozaki: events");
@@ -253,7 +254,7 @@ int host_multiply_ozaki(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, cons
   cudaEventRecord(evB, in);
   cudaStreamWaitEvent(comp, evB, 0);
   ctx->last_plan = "ozaki (int8 tcgen05 GEMMs + CRT), B prepared once, A in row panels";
-  if ((e = launch_ozaki_prepare_b(L, n, k, dB, n, ctx->ws)) != cudaSuccess)
+  if ((e = launch_ozaki_prepare_b(L, n, k, dB, n, wsp)) != cudaSuccess)
     return cuda_fail(e, "matmul ozaki: prepare B");
   for (int64_t i = 0; i < panels; ++i) {
     if ((e = copy_h2d(ctx, dA + i * R * k, sizeof(T) * k, A + i * R * k, sizeof(T) * k,
@@ -262,7 +263,7 @@ int host_multiply_ozaki(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, cons
     cudaEventRecord(evA[i], in);
     cudaStreamWaitEvent(comp, evA[i], 0);
     if ((e = launch_ozaki_panel(L, rows_of(i), n, k, dA + i * R * k, k, dC + i * R * n, n,
-                                ctx->ws)) != cudaSuccess)
+                                wsp)) != cudaSuccess)
       return cuda_fail(e, "matmul ozaki: panel");
     cudaEventRecord(evC[i], comp);
   }

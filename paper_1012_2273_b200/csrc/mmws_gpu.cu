@@ -205,7 +205,7 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
     const int64_t lda_p = round_up(k, 8), ldb_p = round_up(n, 8);
     const size_t bytes = sizeof(double) * ((a_ok ? 0 : m * lda_p) + (b_ok ? 0 : k * ldb_p));
     void* wsp = nullptr;
-    cudaError_t pe = workspace(ctx, bytes, &wsp);
+    cudaError_t pe = workspace(ctx, bytes, &wsp, L.stream);
     if (pe != cudaSuccess) return cuda_fail(pe, "dgemm pack workspace");
     double* w = static_cast<double*>(wsp);
     if (!a_ok) {
@@ -265,7 +265,7 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
     if (k > 131072)
       return fail(MMWS_GPU_ERR_DIMENSION, "dgemm ozaki: k must be <= 131072 (int32 accumulation)");
     void* wsp = nullptr;
-    if ((e = workspace(ctx, ozaki_workspace_bytes(m, n, k), &wsp)) != cudaSuccess)
+    if ((e = workspace(ctx, ozaki_workspace_bytes(m, n, k), &wsp, L.stream)) != cudaSuccess)
       return cuda_fail(e, "dgemm ozaki workspace");
     if (int rc = ozaki_streams(ctx)) return rc;
     e = launch_dgemm_ozaki(L, m, n, k, A, lda, B, ldb, C, ldc, wsp, ctx->oz_stream, ctx->oz_ev);
@@ -372,7 +372,7 @@ int sgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const flo
       return fail(MMWS_GPU_ERR_DIMENSION, "sgemm ozaki: k must be <= 131072 (int32 accumulation)");
     cudaError_t e;
     void* wsp = nullptr;
-    if ((e = workspace(ctx, ozaki_workspace_bytes_f32(m, n, k), &wsp)) != cudaSuccess)
+    if ((e = workspace(ctx, ozaki_workspace_bytes_f32(m, n, k), &wsp, L.stream)) != cudaSuccess)
       return cuda_fail(e, "sgemm ozaki workspace");
     if (int rc = ozaki_streams(ctx)) return rc;
     e = launch_sgemm_ozaki(L, m, n, k, A, lda, B, ldb, C, ldc, wsp, ctx->oz_stream, ctx->oz_ev);
@@ -390,7 +390,7 @@ int sgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const flo
     const int64_t lda_p = round_up(k, 4), ldb_p = round_up(n, 4);
     const size_t bytes = sizeof(float) * ((a_aligned ? 0 : m * lda_p) + (b_aligned ? 0 : k * ldb_p));
     void* wsp = nullptr;
-    if ((e = workspace(ctx, bytes, &wsp)) != cudaSuccess) return cuda_fail(e, "sgemm pack workspace");
+    if ((e = workspace(ctx, bytes, &wsp, L.stream)) != cudaSuccess) return cuda_fail(e, "sgemm pack workspace");
     float* w = static_cast<float*>(wsp);
     if (!a_aligned) {
       if ((e = launch_pack_f32(L, A, m, k, lda, w, m, lda_p, lda_p)) != cudaSuccess)
@@ -564,7 +564,9 @@ int mmws_gpu_destroy(mmws_gpu_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->comm && nccl().ok) nccl().CommDestroy(ctx->comm);
   for (auto& mp : ctx->ipc_cache) cudaIpcCloseMemHandle(mp.base);
-  for (void* p : {ctx->ws, ctx->dA, ctx->dB, ctx->dC, ctx->rbA, ctx->rbB, ctx->rbC, ctx->rbAcc, ctx->sched,
+  for (const auto& w : ctx->ws_spaces)
+    if (w.mem) cudaFree(w.mem);
+  for (void* p : {ctx->dA, ctx->dB, ctx->dC, ctx->rbA, ctx->rbB, ctx->rbC, ctx->rbAcc, ctx->sched,
                   ctx->ipc_stage, static_cast<void*>(ctx->board),
                   static_cast<void*>(ctx->sink)})
     if (p) cudaFree(p);

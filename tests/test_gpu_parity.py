@@ -510,6 +510,36 @@ def test_rowblock_orders_after_the_callers_stream(ctx):
         assert (bits(host(C)) == bits(host(want))).all()
 
 
+@pytest.mark.parametrize("mode", ["dmma", "sgemm", "ozaki"])
+def test_calls_on_two_streams_do_not_share_a_workspace(ctx, mode):
+    # Operands TMA cannot read are packed into a workspace, and MODE_OZAKI
+    # keeps its residues in one: a call on stream s2 must not overwrite the
+    # workspace a still-running call on stream s1 reads.  s1: a long
+    # multiply of packed operands; s2: a short sleep, then the same-shaped
+    # multiply of other operands, packed while the first one runs.
+    T = torch()
+    n = 4099 if mode != "ozaki" else 3001
+    dt = T.float32 if mode == "sgemm" else T.float64
+    call = ctx.sgemm if mode == "sgemm" else ctx.dgemm
+    kw = {} if mode == "sgemm" else {"mode": P.MODE_OZAKI if mode == "ozaki" else P.MODE_AUTO}
+    big = [ctx.fill(P.DIST_UNIFORM, 300 + i, n, n + 1, dtype=dt) for i in range(4)]
+    ops = [x[:, 1:] for x in big]                     # misaligned views: packed
+    A1, B1, A2, B2 = ops[0], ops[1][:, :n], ops[2], ops[3][:, :n]
+    want1 = host(call(A1, B1, **kw))
+    want2 = host(call(A2, B2, **kw))
+    s1, s2 = T.cuda.Stream(), T.cuda.Stream()
+    T.cuda.synchronize()
+    for _ in range(3):
+        with T.cuda.stream(s1):
+            C1 = call(A1, B1, **kw)
+        with T.cuda.stream(s2):
+            T.cuda._sleep(2_000_000)                  # ~1 ms: lands mid-multiply on s1
+            C2 = call(A2, B2, **kw)
+        T.cuda.synchronize()
+        assert (bits(host(C1)) == bits(want1)).all(), mode
+        assert (bits(host(C2)) == bits(want2)).all(), mode
+
+
 def test_rowblock_nccl_path_single_rank(oracle):
     # The NCCL engine (dlopen of the process's libnccl, communicator, broadcast,
     # grouped exchanges, two sub-blocks, stream joins) in a 1-rank world -- the
