@@ -540,6 +540,60 @@ def test_calls_on_two_streams_do_not_share_a_workspace(ctx, mode):
         assert (bits(host(C2)) == bits(want2)).all(), mode
 
 
+def test_one_context_from_four_threads(ctx):
+    # The ABI is reentrant per context (a mutex; ctypes drops the GIL): four
+    # threads, each on its own torch stream, mix device multiplies (AUTO,
+    # EXACT, packed views, fp32, OZAKI) and host-buffer multiplies (pageable
+    # and pinned) on one context; every result equals its single-threaded
+    # reference, bitwise.
+    import threading
+    T = torch()
+    rng = np.random.default_rng(77)
+    jobs = []
+    for i in range(24):
+        n = int(rng.integers(40, 700))
+        kind = ["auto", "exact", "packed", "f32", "ozaki", "host", "host_pinned"][i % 7]
+        dt = T.float32 if kind == "f32" else T.float64
+        big = ctx.fill(P.DIST_UNIFORM, 500 + i, n, n + 1, dtype=dt)
+        A = big[:, 1:] if kind == "packed" else big[:, :n].contiguous()
+        B = ctx.fill(P.DIST_UNIFORM, 600 + i, n, n, dtype=dt)
+        jobs.append((kind, A, B))
+
+    def run(kind, A, B):
+        if kind == "f32":
+            return host(ctx.sgemm(A, B))
+        if kind in ("host", "host_pinned"):
+            a, b = host(A), host(B)
+            if kind == "host_pinned":
+                a = T.from_numpy(a).pin_memory().numpy()
+                b = T.from_numpy(b).pin_memory().numpy()
+            return ctx.matmul_host(a, b, mode=P.MODE_EXACT)[0].copy()
+        mode = {"auto": P.MODE_AUTO, "exact": P.MODE_EXACT, "packed": P.MODE_AUTO,
+                "ozaki": P.MODE_OZAKI}[kind]
+        return host(ctx.dgemm(A, B, mode=mode))
+
+    want = [run(*j) for j in jobs]
+    T.cuda.synchronize()
+    errors = []
+
+    def worker(t):
+        s = T.cuda.Stream()
+        with T.cuda.stream(s):
+            for rep in range(3):
+                for i in range(t, len(jobs), 4):
+                    got = run(*jobs[i])
+                    if not (bits(got) == bits(want[i])).all():
+                        errors.append((t, rep, i, jobs[i][0]))
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join(timeout=240)
+    assert not any(th.is_alive() for th in threads)
+    assert not errors, errors
+
+
 def test_rowblock_nccl_path_single_rank(oracle):
     # The NCCL engine (dlopen of the process's libnccl, communicator, broadcast,
     # grouped exchanges, two sub-blocks, stream joins) in a 1-rank world -- the
