@@ -41,6 +41,8 @@ def normwise(x, y):
 
 def dim():
     r = rng.random()
+    if r < 0.01:  # big enough for the streamed host path (>= 2 x 148 tiles of 128 x 128)
+        return int(rng.integers(2200, 3000))
     if r < 0.35:
         return int(rng.integers(1, 65))
     if r < 0.8:
@@ -107,19 +109,23 @@ while time.time() < t_end:
         if same_family and not torch.equal(C.view(torch.int64), one.view(torch.int64)):
             fails.append({"case": case, "what": "accumulate", "shape": [m, k, n], "cut": cut,
                           "mode": mode})
-    # host entries
+    # host entries (matmul_host and the 1-rank master_run_host), fp64 and fp32
     if rng.random() < 0.3:
-        mode = [P.MODE_AUTO, P.MODE_EXACT][int(rng.integers(0, 2))]
-        dev_c = ctx.dgemm(A.contiguous(), B.contiguous(), mode=mode).cpu().numpy()
+        mode = [P.MODE_AUTO, P.MODE_EXACT, P.MODE_DMMA][int(rng.integers(0, 3))]
+        f32 = rng.random() < 0.25
+        x0, y0 = (a.astype(np.float32), b.astype(np.float32)) if f32 else (a, b)
+        xd, yd = torch.from_numpy(x0).cuda(), torch.from_numpy(y0).cuda()
+        dev_c = (ctx.sgemm(xd, yd) if f32 else ctx.dgemm(xd, yd, mode=mode)).cpu().numpy()
         for pinned in (False, True):
-            x, y = a, b
+            x, y = x0, y0
             if pinned:
-                x = torch.from_numpy(a).pin_memory().numpy()
-                y = torch.from_numpy(b).pin_memory().numpy()
-            c, _ = ctx.matmul_host(x, y, mode=mode)
+                x = torch.from_numpy(x0).pin_memory().numpy()
+                y = torch.from_numpy(y0).pin_memory().numpy()
+            entry = "master_run_host" if rng.random() < 0.3 else "matmul_host"
+            c, _ = getattr(ctx, entry)(x, y, mode=P.MODE_FFMA if f32 else mode)
             counts["host_entry_vs_device"] = counts.get("host_entry_vs_device", 0) + 1
             if not (bits(c) == bits(dev_c)).all():
-                fails.append({"case": case, "what": "host_entry", "pinned": pinned,
+                fails.append({"case": case, "what": entry, "pinned": pinned, "f32": f32,
                               "shape": [m, k, n], "mode": mode})
     # graph replay
     if rng.random() < 0.2:
