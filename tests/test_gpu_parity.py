@@ -835,6 +835,32 @@ def test_host_pipeline_bitwise_equals_device(ctx, oracle, shape):
     assert (cf == host(ctx.sgemm(dev(af), dev(bf)))).all()
 
 
+def test_streamed_host_path_random_shapes(ctx):
+    # host_multiply_streamed (one persistent DMMA kernel fed by PCIe bands,
+    # arrival flags, per-row-band copy-out): seeded random shapes with ragged
+    # last bands (m, n not multiples of 256 / 512, k small to large), pageable
+    # and pinned, AUTO and DMMA -- bitwise the device-pointer call
+    T = torch()
+    rng = np.random.default_rng(5150)
+    seen = 0
+    for case in range(10):
+        m = int(rng.integers(2200, 4200))
+        n = int(rng.integers(1100, 2100)) * 2
+        k = int(rng.integers(8, 2100)) * 2
+        A = ctx.fill(P.DIST_UNIFORM, 700 + case, m, k)
+        B = ctx.fill(P.DIST_UNIFORM, 800 + case, k, n)
+        mode = P.MODE_AUTO if case % 2 else P.MODE_DMMA
+        want = bits(host(ctx.dgemm(A, B, mode=mode)))
+        a, b = host(A), host(B)
+        if case % 3 == 0:
+            a = T.from_numpy(a).pin_memory().numpy()
+            b = T.from_numpy(b).pin_memory().numpy()
+        got, el = ctx.matmul_host(a, b, mode=mode)
+        seen += "streamed" in ctx.last_plan
+        assert el > 0 and (bits(got) == want).all(), (m, k, n, mode)
+    assert seen >= 8, seen
+
+
 def test_pageable_host_buffers_bigger_than_the_staging_ring(ctx, oracle):
     # pageable numpy buffers go through the pinned chunk ring (4 x 32 MB):
     # 128 MB operands wrap it several times; fp64 streamed path, fp32 panel
