@@ -57,8 +57,11 @@ struct mmws_gpu_ctx {
   struct IpcMap {
     unsigned char handle[64];
     void* base;
+    bool round_scoped;   // a row-block round's C mapping: closed when evicted
+    uint64_t last_use;
   };
   std::vector<IpcMap> ipc_cache;
+  uint64_t ipc_clock = 0;
   void* ipc_stage = nullptr;  // 256-byte device staging for the handle broadcast / barrier
   unsigned char* host_stage = nullptr;  // 512 bytes of pinned host memory: its host end
   unsigned char last_handle[80] = {0};  // row-block: handle bytes of the last call
@@ -213,7 +216,13 @@ int server_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const do
                     double* elapsed_s);
 // CUDA IPC: 64-byte handle of the allocation holding ptr + 8-byte offset.
 int ipc_export(mmws_gpu_ctx* ctx, const void* ptr, uint8_t out[72]);
-int ipc_open(mmws_gpu_ctx* ctx, const uint8_t in[72], void** ptr);
+// round_scoped: a mapping only a row-block round uses (rank 0's C): at most
+// IPC_ROUND_MAPPINGS of them stay open, least recently used closed first --
+// a caller that gives every round a fresh C allocation would otherwise keep
+// every old one mapped (and its memory alive on rank 0) until the context
+// goes away.  Rounds are synchronous, so no work uses an evicted mapping.
+int ipc_open(mmws_gpu_ctx* ctx, const uint8_t in[72], void** ptr, bool round_scoped = false);
+constexpr int IPC_ROUND_MAPPINGS = 4;
 // Host-buffer multiply with PCIe copies overlapped (host_pipeline.cu).
 template <class T>
 int host_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, const T* B,

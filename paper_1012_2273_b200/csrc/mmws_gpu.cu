@@ -429,15 +429,32 @@ int ipc_export(mmws_gpu_ctx* ctx, const void* ptr, uint8_t out[72]) {
   return ok();
 }
 
-int ipc_open(mmws_gpu_ctx* ctx, const uint8_t in[72], void** ptr) {
+int ipc_open(mmws_gpu_ctx* ctx, const uint8_t in[72], void** ptr, bool round_scoped) {
   if (!in || !ptr) return fail(MMWS_GPU_ERR_DOMAIN, "ipc_open: null argument");
   uint64_t offset = 0;
   std::memcpy(&offset, in + 64, 8);
-  for (const auto& mp : ctx->ipc_cache)
+  ++ctx->ipc_clock;
+  for (auto& mp : ctx->ipc_cache)
     if (std::memcmp(mp.handle, in, 64) == 0) {
+      mp.last_use = ctx->ipc_clock;
+      mp.round_scoped = mp.round_scoped && round_scoped;  // a caller's own mapping stays
       *ptr = static_cast<char*>(mp.base) + offset;
       return ok();
     }
+  if (round_scoped) {  // evict the least recently used round mappings
+    for (;;) {
+      int n = 0;
+      auto lru = ctx->ipc_cache.end();
+      for (auto it = ctx->ipc_cache.begin(); it != ctx->ipc_cache.end(); ++it)
+        if (it->round_scoped) {
+          ++n;
+          if (lru == ctx->ipc_cache.end() || it->last_use < lru->last_use) lru = it;
+        }
+      if (n < IPC_ROUND_MAPPINGS) break;
+      cudaIpcCloseMemHandle(lru->base);
+      ctx->ipc_cache.erase(lru);
+    }
+  }
   cudaIpcMemHandle_t h;
   std::memcpy(&h, in, 64);
   void* base = nullptr;
@@ -446,6 +463,8 @@ int ipc_open(mmws_gpu_ctx* ctx, const uint8_t in[72], void** ptr) {
   mmws_gpu_ctx::IpcMap mp;
   std::memcpy(mp.handle, in, 64);
   mp.base = base;
+  mp.round_scoped = round_scoped;
+  mp.last_use = ctx->ipc_clock;
   ctx->ipc_cache.push_back(mp);
   *ptr = static_cast<char*>(base) + offset;
   return ok();

@@ -419,7 +419,7 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
   int ok_here = hbuf[72] && !ctx->tune.nccl_gather;
   if (me != 0 && ok_here) {
     void* p = nullptr;
-    ok_here = ipc_open(ctx, hbuf, &p) == MMWS_GPU_OK ? 1 : 0;
+    ok_here = ipc_open(ctx, hbuf, &p, /*round_scoped=*/true) == MMWS_GPU_OK ? 1 : 0;
     c_peer = static_cast<T*>(p);
   }
   int fused = ctx->last_fused;

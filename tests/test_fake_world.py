@@ -306,8 +306,47 @@ def _job_random(P, ctx, rank, world):
     return res
 
 
+def _job_fresh_c(P, ctx, rank, world):
+    """Every round gets a freshly allocated C on rank 0 (new IPC handle): the
+    workers map each one for the fused gather and close the least recently
+    used beyond a few, so old C allocations do not stay mapped; results stay
+    bitwise, including a C seen again after its mapping was evicted."""
+    import torch
+    ctx.tune("MMWS_GPU_ROWBLOCK_RANKS", "all")
+    m, n, k = 600, 520, 300
+    out = []
+    keep = None
+    for i in range(9):
+        if rank == 0:
+            A = ctx.fill(P.DIST_UNIFORM, 900 + i, m, k)
+            B = ctx.fill(P.DIST_UNIFORM, 950 + i, k, n)
+            if i == 8:
+                C = keep                                  # an early C again
+            else:
+                C = torch.full((m, n), float("nan"), dtype=torch.float64, device="cuda")
+            ctx.rowblock(m, n, k, A, B, C)
+            out.append((i, ctx.last_round, _same(C, ctx.dgemm(A, B))))
+            if i == 1:
+                keep = C
+            else:
+                del C
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()                      # the next C is a new allocation
+        else:
+            ctx.rowblock(m, n, k)
+    return out
+
+
 JOBS = {"rounds": _job_rounds, "dead": _job_dead, "ragged": _job_ragged, "config3": _job_config3,
-        "slow": _job_slow, "random": _job_random}
+        "slow": _job_slow, "random": _job_random, "fresh_c": _job_fresh_c}
+
+
+@pytest.mark.timeout(600)
+def test_fresh_c_every_round_keeps_few_mappings(fake_lib):
+    res = _ok(_run(3, fake_lib, "fresh_c"), 3)[0]
+    assert len(res) == 9
+    for i, (active, how), same in res:
+        assert same and active == 3 and how == "fused-ipc", (i, active, how)
 
 
 @pytest.mark.timeout(900)
