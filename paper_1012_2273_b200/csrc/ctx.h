@@ -57,7 +57,7 @@ struct mmws_gpu_ctx {
   struct IpcMap {
     unsigned char handle[64];
     void* base;
-    bool round_scoped;   // a row-block round's C mapping: closed when evicted
+    int scope;           // IPC_CALLER / IPC_ROUND / IPC_COMM (ipc_open)
     uint64_t last_use;
   };
   std::vector<IpcMap> ipc_cache;
@@ -216,12 +216,16 @@ int server_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const do
                     double* elapsed_s);
 // CUDA IPC: 64-byte handle of the allocation holding ptr + 8-byte offset.
 int ipc_export(mmws_gpu_ctx* ctx, const void* ptr, uint8_t out[72]);
-// round_scoped: a mapping only a row-block round uses (rank 0's C): at most
-// IPC_ROUND_MAPPINGS of them stay open, least recently used closed first --
-// a caller that gives every round a fresh C allocation would otherwise keep
-// every old one mapped (and its memory alive on rank 0) until the context
-// goes away.  Rounds are synchronous, so no work uses an evicted mapping.
-int ipc_open(mmws_gpu_ctx* ctx, const uint8_t in[72], void** ptr, bool round_scoped = false);
+// Mapping scopes: IPC_CALLER -- mmws_gpu_ipc_open's, open until the context
+// goes away; IPC_ROUND -- rank 0's C as a row-block round maps it: at most
+// IPC_ROUND_MAPPINGS stay open, least recently used closed first (a caller
+// that gives every round a fresh C allocation would otherwise keep every old
+// one mapped, and its memory alive on rank 0; rounds are synchronous, so no
+// work uses an evicted mapping); IPC_COMM -- the progress board.  Round and
+// communicator mappings are closed by mmws_gpu_comm_destroy.
+enum { IPC_CALLER = 0, IPC_ROUND = 1, IPC_COMM = 2 };
+int ipc_open(mmws_gpu_ctx* ctx, const uint8_t in[72], void** ptr, int scope = IPC_CALLER);
+void ipc_close_scoped(mmws_gpu_ctx* ctx);
 constexpr int IPC_ROUND_MAPPINGS = 4;
 // Host-buffer multiply with PCIe copies overlapped (host_pipeline.cu).
 template <class T>

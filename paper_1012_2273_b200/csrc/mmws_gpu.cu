@@ -429,7 +429,18 @@ int ipc_export(mmws_gpu_ctx* ctx, const void* ptr, uint8_t out[72]) {
   return ok();
 }
 
-int ipc_open(mmws_gpu_ctx* ctx, const uint8_t in[72], void** ptr, bool round_scoped) {
+void ipc_close_scoped(mmws_gpu_ctx* ctx) {
+  for (auto it = ctx->ipc_cache.begin(); it != ctx->ipc_cache.end();) {
+    if (it->scope != IPC_CALLER) {
+      cudaIpcCloseMemHandle(it->base);
+      it = ctx->ipc_cache.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+
+int ipc_open(mmws_gpu_ctx* ctx, const uint8_t in[72], void** ptr, int scope) {
   if (!in || !ptr) return fail(MMWS_GPU_ERR_DOMAIN, "ipc_open: null argument");
   uint64_t offset = 0;
   std::memcpy(&offset, in + 64, 8);
@@ -437,16 +448,16 @@ int ipc_open(mmws_gpu_ctx* ctx, const uint8_t in[72], void** ptr, bool round_sco
   for (auto& mp : ctx->ipc_cache)
     if (std::memcmp(mp.handle, in, 64) == 0) {
       mp.last_use = ctx->ipc_clock;
-      mp.round_scoped = mp.round_scoped && round_scoped;  // a caller's own mapping stays
+      if (scope == IPC_CALLER) mp.scope = IPC_CALLER;  // the caller's own mapping stays
       *ptr = static_cast<char*>(mp.base) + offset;
       return ok();
     }
-  if (round_scoped) {  // evict the least recently used round mappings
+  if (scope == IPC_ROUND) {  // evict the least recently used round mappings
     for (;;) {
       int n = 0;
       auto lru = ctx->ipc_cache.end();
       for (auto it = ctx->ipc_cache.begin(); it != ctx->ipc_cache.end(); ++it)
-        if (it->round_scoped) {
+        if (it->scope == IPC_ROUND) {
           ++n;
           if (lru == ctx->ipc_cache.end() || it->last_use < lru->last_use) lru = it;
         }
@@ -463,7 +474,7 @@ int ipc_open(mmws_gpu_ctx* ctx, const uint8_t in[72], void** ptr, bool round_sco
   mmws_gpu_ctx::IpcMap mp;
   std::memcpy(mp.handle, in, 64);
   mp.base = base;
-  mp.round_scoped = round_scoped;
+  mp.scope = scope;
   mp.last_use = ctx->ipc_clock;
   ctx->ipc_cache.push_back(mp);
   *ptr = static_cast<char*>(base) + offset;

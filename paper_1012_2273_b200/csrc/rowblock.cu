@@ -419,7 +419,7 @@ int rowblock_enqueue(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T
   int ok_here = hbuf[72] && !ctx->tune.nccl_gather;
   if (me != 0 && ok_here) {
     void* p = nullptr;
-    ok_here = ipc_open(ctx, hbuf, &p, /*round_scoped=*/true) == MMWS_GPU_OK ? 1 : 0;
+    ok_here = ipc_open(ctx, hbuf, &p, IPC_ROUND) == MMWS_GPU_OK ? 1 : 0;
     c_peer = static_cast<T*>(p);
   }
   int fused = ctx->last_fused;
@@ -761,7 +761,7 @@ int board_setup(mmws_gpu_ctx* ctx) {
   if (int rc = await(ctx, ctx->pool[0], "comm_init: board handle")) return rc;
   if (ctx->rank != 0 && h[72]) {
     void* p = nullptr;
-    if (ipc_open(ctx, h, &p) == MMWS_GPU_OK) ctx->board_peer = static_cast<unsigned*>(p);
+    if (ipc_open(ctx, h, &p, IPC_COMM) == MMWS_GPU_OK) ctx->board_peer = static_cast<unsigned*>(p);
     ok();
   }
   return MMWS_GPU_OK;
@@ -819,6 +819,8 @@ int mmws_gpu_comm_destroy(mmws_gpu_ctx* ctx) {
     ctx->board = nullptr;
   }
   ctx->board_peer = nullptr;
+  ipc_close_scoped(ctx);  // this communicator's C and board mappings
+  std::memset(ctx->last_handle, 0, sizeof ctx->last_handle);
   ctx->comm_failed = false;
   ctx->round = 0;
   ctx->nranks = 1;
