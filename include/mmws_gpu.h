@@ -207,6 +207,10 @@ int mmws_gpu_graph_dgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, con
                          int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                          int mode, mmws_gpu_graph** out);
 int mmws_gpu_graph_launch(mmws_gpu_graph* graph, void* stream);
+/* A graph may outlive its context: mmws_gpu_destroy releases the device
+ * resources of the context's live graphs, after which mmws_gpu_graph_launch
+ * returns MMWS_GPU_ERR_STATE and mmws_gpu_graph_destroy only frees the handle
+ * (which the caller still owns). */
 int mmws_gpu_graph_destroy(mmws_gpu_graph* graph);
 
 /* ---------------------------------------------------------------- latency server (N <= 96) */

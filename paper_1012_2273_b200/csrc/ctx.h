@@ -31,6 +31,8 @@ struct Tuning {
 };
 }  // namespace mmws_impl
 
+struct mmws_gpu_graph;
+
 struct mmws_gpu_ctx {
   int device = 0;
   int num_sms = 0;
@@ -62,6 +64,10 @@ struct mmws_gpu_ctx {
   };
   std::vector<IpcMap> ipc_cache;
   uint64_t ipc_clock = 0;
+  // live graphs: mmws_gpu_destroy releases their device resources and
+  // detaches them, so a graph destroyed (or launched) after its context is
+  // an error, not a use after free
+  std::vector<mmws_gpu_graph*> graphs;
   void* ipc_stage = nullptr;  // 256-byte device staging for the handle broadcast / barrier
   unsigned char* host_stage = nullptr;  // 512 bytes of pinned host memory: its host end
   unsigned char last_handle[80] = {0};  // row-block: handle bytes of the last call

@@ -495,6 +495,23 @@ struct mmws_gpu_graph {
 };
 
 namespace {
+// Device resources of a graph (its context's lock held).
+void graph_release(mmws_gpu_ctx* ctx, mmws_gpu_graph* g) {
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  g->exec = nullptr;
+  g->graph = nullptr;
+  if (g->ws) {
+    // a replay may still be running: free after the context's work, or at
+    // server stop while the latency server holds the device
+    if (ctx->server) ctx->deferred_free.push_back(g->ws);
+    else cudaDeviceSynchronize(), cudaFree(g->ws);
+    g->ws = nullptr;
+  }
+}
+}  // namespace
+
+namespace {
 // The NCCL stream gets the highest priority so its CTAs are scheduled ahead of
 // pending GEMM CTAs whenever an SM frees up -- otherwise the C gather of a
 // finished sub-block would wait for the whole next multiply.
@@ -592,6 +609,11 @@ int mmws_gpu_destroy(mmws_gpu_ctx* ctx) {
   cudaSetDevice(ctx->device);
   server_destroy(ctx);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (mmws_gpu_graph* g : ctx->graphs) {  // detach: the caller still owns the handles
+    graph_release(ctx, g);
+    g->ctx = nullptr;
+  }
+  ctx->graphs.clear();
   if (ctx->comm && nccl().ok) nccl().CommDestroy(ctx->comm);
   for (auto& mp : ctx->ipc_cache) cudaIpcCloseMemHandle(mp.base);
   for (const auto& w : ctx->ws_spaces)
@@ -801,6 +823,7 @@ int mmws_gpu_graph_dgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, con
     delete g;
     return rc ? rc : cuda_fail(e, "graph capture / instantiate");
   }
+  ctx->graphs.push_back(g);
   *out = g;
   return ok();
 }
@@ -808,6 +831,7 @@ int mmws_gpu_graph_dgemm(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, con
 int mmws_gpu_graph_launch(mmws_gpu_graph* g, void* stream) {
   if (!g) return fail(MMWS_GPU_ERR_STATE, "null graph");
   mmws_gpu_ctx* ctx = g->ctx;
+  if (!ctx) return fail(MMWS_GPU_ERR_STATE, "graph_launch: the graph's context was destroyed");
   MMWS_CTX_GUARD(ctx);
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
   cudaError_t e = cudaGraphLaunch(g->exec, s);
@@ -816,18 +840,18 @@ int mmws_gpu_graph_launch(mmws_gpu_graph* g, void* stream) {
   return ok();
 }
 
+
 int mmws_gpu_graph_destroy(mmws_gpu_graph* g) {
   if (!g) return ok();
   mmws_gpu_ctx* ctx = g->ctx;
-  MMWS_CTX_GUARD(ctx);
-  if (g->exec) cudaGraphExecDestroy(g->exec);
-  if (g->graph) cudaGraphDestroy(g->graph);
-  if (g->ws) {
-    // a replay may still be running: free after the context's work, or at
-    // server stop while the latency server holds the device
-    if (ctx->server) ctx->deferred_free.push_back(g->ws);
-    else cudaDeviceSynchronize(), cudaFree(g->ws);
+  if (!ctx) {  // its context was destroyed first: device resources already gone
+    delete g;
+    return ok();
   }
+  MMWS_CTX_GUARD(ctx);
+  graph_release(ctx, g);
+  auto& gs = ctx->graphs;
+  gs.erase(std::remove(gs.begin(), gs.end(), g), gs.end());
   delete g;
   return ok();
 }

@@ -594,6 +594,24 @@ def test_one_context_from_four_threads(ctx):
     assert not errors, errors
 
 
+def test_graph_outliving_its_context_is_an_error_not_a_crash():
+    # mmws_gpu_destroy releases the device resources of the context's live
+    # graphs and detaches them: launching one afterwards is an error, and
+    # destroying it just frees the handle
+    T = torch()
+    c = P.Context(0)
+    A = c.fill(P.DIST_UNIFORM, 1, 100, 100)
+    C_ = T.empty_like(A)
+    g = c.graph_dgemm(A, A, C_)
+    g.launch()
+    T.cuda.synchronize()
+    c.close()
+    with pytest.raises(P.GpuError):
+        g.launch()
+    g.close()
+    g.close()                                          # idempotent
+
+
 def test_rowblock_nccl_path_single_rank(oracle):
     # The NCCL engine (dlopen of the process's libnccl, communicator, broadcast,
     # grouped exchanges, two sub-blocks, stream joins) in a 1-rank world -- the
