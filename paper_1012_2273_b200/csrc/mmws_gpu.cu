@@ -470,6 +470,21 @@ int ipc_open(mmws_gpu_ctx* ctx, const uint8_t in[72], void** ptr, int scope) {
   std::memcpy(&h, in, 64);
   void* base = nullptr;
   cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e == cudaErrorAlreadyMapped && scope != IPC_CALLER) {
+    // The exporter freed an allocation we still map and reallocated at its
+    // address (a fresh C per round): the stale round mappings are idle
+    // (rounds are synchronous) -- close them and map the new one.
+    cudaGetLastError();
+    for (auto it = ctx->ipc_cache.begin(); it != ctx->ipc_cache.end();) {
+      if (it->scope == IPC_ROUND) {
+        cudaIpcCloseMemHandle(it->base);
+        it = ctx->ipc_cache.erase(it);
+      } else {
+        ++it;
+      }
+    }
+    e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+  }
   if (e != cudaSuccess) return cuda_fail(e, "ipc_open: cudaIpcOpenMemHandle");
   mmws_gpu_ctx::IpcMap mp;
   std::memcpy(mp.handle, in, 64);

@@ -61,6 +61,13 @@ struct Comm {
   uint32_t sent[MAXR] = {}, recvd[MAXR] = {}, reductions = 0;
   ncclResult_t async = ncclSuccess;
   std::vector<CUevent> events;  // kept until destroy (peers may still open them)
+  // per-peer rings of interprocess events, reused: message i to / from a peer
+  // uses slot i % RING.  Safe because every send returns only after the
+  // peer has queued its wait on the "ready" event, and the sender queues its
+  // wait on "done" before the next message of the pair is posted (creating
+  // a fresh interprocess event per message ran out after ~6000 of them)
+  static constexpr int RING = 4;
+  CUevent ready_ring[MAXR][RING] = {}, done_ring[MAXR][RING] = {};
   struct Open {
     CUipcMemHandle h;
     CUdeviceptr base;
@@ -87,18 +94,45 @@ size_t type_size(ncclDataType_t t) {
   }
 }
 
+ncclResult_t cu_fail(const char* what, CUresult r, ncclResult_t code) {
+  const char* name = nullptr;
+  cuGetErrorName(r, &name);
+  std::fprintf(stderr, "[fake_nccl] %s failed: %s\n", what, name ? name : "?");
+  return code;
+}
+
 CUevent new_event(Comm* c) {
   CUevent e = nullptr;
-  cuEventCreate(&e, CU_EVENT_INTERPROCESS | CU_EVENT_DISABLE_TIMING);
+  if (CUresult r = cuEventCreate(&e, CU_EVENT_INTERPROCESS | CU_EVENT_DISABLE_TIMING)) {
+    cu_fail("cuEventCreate", r, ncclSystemError);
+    return nullptr;
+  }
   c->events.push_back(e);
   return e;
+}
+
+CUevent ring_event(Comm* c, CUevent* slot) {
+  if (!*slot) *slot = new_event(c);
+  return *slot;
 }
 
 CUdeviceptr open_mem(Comm* c, const CUipcMemHandle& h) {
   for (const auto& o : c->opened)
     if (!std::memcmp(&o.h, &h, sizeof h)) return o.base;
   CUdeviceptr p = 0;
-  if (cuIpcOpenMemHandle(&p, h, CU_IPC_MEM_LAZY_ENABLE_PEER_ACCESS) != CUDA_SUCCESS) return 0;
+  CUresult r = cuIpcOpenMemHandle(&p, h, CU_IPC_MEM_LAZY_ENABLE_PEER_ACCESS);
+  if (r == CUDA_ERROR_ALREADY_MAPPED) {
+    // the peer freed a buffer we still map and reallocated at its address:
+    // drop the cached mappings (after the copies queued from them) and retry
+    cuCtxSynchronize();
+    for (auto& o : c->opened) cuIpcCloseMemHandle(o.base);
+    c->opened.clear();
+    r = cuIpcOpenMemHandle(&p, h, CU_IPC_MEM_LAZY_ENABLE_PEER_ACCESS);
+  }
+  if (r) {
+    cu_fail("cuIpcOpenMemHandle", r, ncclSystemError);
+    return 0;
+  }
   c->opened.push_back({h, p});
   return p;
 }
@@ -114,19 +148,22 @@ ncclResult_t send(Comm* c, const void* buf, size_t bytes, int peer, CUstream s) 
   if (cuMemGetAddressRange(&base, &size, reinterpret_cast<CUdeviceptr>(buf)) != CUDA_SUCCESS)
     return ncclInvalidArgument;
   Msg& m = c->shm->msg[c->rank][peer];
-  if (cuIpcGetMemHandle(&m.mem, base) != CUDA_SUCCESS) return ncclSystemError;
+  if (CUresult r = cuIpcGetMemHandle(&m.mem, base))
+    return cu_fail("cuIpcGetMemHandle", r, ncclSystemError);
   m.off = reinterpret_cast<CUdeviceptr>(buf) - base;
   m.bytes = bytes;
-  CUevent ready = new_event(c);
+  const uint32_t seq = ++c->sent[peer];
+  CUevent ready = ring_event(c, &c->ready_ring[peer][seq % Comm::RING]);
+  if (!ready) return ncclSystemError;
   cuEventRecord(ready, s);
   cuIpcGetEventHandle(&m.ready, ready);
-  const uint32_t seq = ++c->sent[peer];
   m.seq.store(seq, std::memory_order_release);
   // the peer copies out of buf: wait for its copy before buf may change
   Ack& a = c->shm->ack[c->rank][peer];
   if (!wait_for(a.seq, seq)) return fail(c);
   CUevent done = nullptr;
-  if (cuIpcOpenEventHandle(&done, a.done) != CUDA_SUCCESS) return ncclSystemError;
+  if (CUresult r = cuIpcOpenEventHandle(&done, a.done))
+    return cu_fail("cuIpcOpenEventHandle(done)", r, ncclSystemError);
   cuStreamWaitEvent(s, done, 0);
   cuEventDestroy(done);
   return ncclSuccess;
@@ -140,13 +177,15 @@ ncclResult_t recv(Comm* c, void* buf, size_t bytes, int peer, CUstream s) {
   const CUdeviceptr src = open_mem(c, m.mem);
   if (!src) return ncclSystemError;
   CUevent ready = nullptr;
-  if (cuIpcOpenEventHandle(&ready, m.ready) != CUDA_SUCCESS) return ncclSystemError;
+  if (CUresult r = cuIpcOpenEventHandle(&ready, m.ready))
+    return cu_fail("cuIpcOpenEventHandle(ready)", r, ncclSystemError);
   cuStreamWaitEvent(s, ready, 0);
   cuEventDestroy(ready);
-  if (bytes && cuMemcpyDtoDAsync(reinterpret_cast<CUdeviceptr>(buf), src + m.off, bytes, s) !=
-                   CUDA_SUCCESS)
-    return ncclUnhandledCudaError;
-  CUevent done = new_event(c);
+  if (bytes)
+    if (CUresult r = cuMemcpyDtoDAsync(reinterpret_cast<CUdeviceptr>(buf), src + m.off, bytes, s))
+      return cu_fail("cuMemcpyDtoDAsync", r, ncclUnhandledCudaError);
+  CUevent done = ring_event(c, &c->done_ring[peer][seq % Comm::RING]);
+  if (!done) return ncclSystemError;
   cuEventRecord(done, s);
   Ack& a = c->shm->ack[peer][c->rank];
   cuIpcGetEventHandle(&a.done, done);

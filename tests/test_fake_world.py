@@ -261,12 +261,16 @@ def _job_random(P, ctx, rank, world):
     fp64 and FFMA fp32, both gathers, device and host entries -- rank 0
     compares each round with its own one-GPU product, bitwise."""
     import torch
-    rng = np.random.default_rng(4242)
+    # MMWS_FAKE_SOAK=<rounds>:<seed> lengthens it (soak runs, tools/README.md)
+    rounds, seed = 24, 4242
+    if os.environ.get("MMWS_FAKE_SOAK"):
+        rounds, seed = (int(v) for v in os.environ["MMWS_FAKE_SOAK"].split(":"))
+    rng = np.random.default_rng(seed)
     modes = [("auto", P.MODE_AUTO, False), ("exact", P.MODE_EXACT, False),
              ("dmma", P.MODE_DMMA, False), ("ffma", P.MODE_FFMA, True)]
     ctx.tune("MMWS_GPU_ROWBLOCK_RANKS", "all")
     res = []
-    for case in range(24):
+    for case in range(rounds):
         r = rng.random()
         if r < 0.3:
             m, k, n = (int(v) for v in rng.integers(1, 40, size=3))
@@ -325,7 +329,7 @@ def _job_fresh_c(P, ctx, rank, world):
             else:
                 C = torch.full((m, n), float("nan"), dtype=torch.float64, device="cuda")
             ctx.rowblock(m, n, k, A, B, C)
-            out.append((i, ctx.last_round, _same(C, ctx.dgemm(A, B))))
+            out.append((i, ctx.last_round, _same(C, ctx.dgemm(A, B)), C.data_ptr()))
             if i == 1:
                 keep = C
             else:
@@ -345,14 +349,20 @@ JOBS = {"rounds": _job_rounds, "dead": _job_dead, "ragged": _job_ragged, "config
 def test_fresh_c_every_round_keeps_few_mappings(fake_lib):
     res = _ok(_run(3, fake_lib, "fresh_c"), 3)[0]
     assert len(res) == 9
-    for i, (active, how), same in res:
+    for i, (active, how), same, _ in res:
         assert same and active == 3 and how == "fused-ipc", (i, active, how)
+    # the allocator hands the same address to later C's (new allocations,
+    # new IPC handles): the workers' stale mappings of it must not get in
+    # the way (cudaErrorAlreadyMapped -> close the idle round mappings)
+    ptrs = [p for *_, p in res]
+    assert len(set(ptrs)) < len(ptrs), ptrs
 
 
 @pytest.mark.timeout(900)
 def test_random_rounds_bitwise_over_3_ranks(fake_lib):
     res = _ok(_run(3, fake_lib, "random"), 3)[0]
-    assert len(res) == 24
+    assert len(res) == (int(os.environ["MMWS_FAKE_SOAK"].split(":")[0])
+                        if os.environ.get("MMWS_FAKE_SOAK") else 24)
     bad = [r for r in res if not r[-1]]
     if bad:
         pytest.fail(f"rounds differing from the one-GPU product: {bad}")
