@@ -89,8 +89,10 @@ struct mmws_gpu_ctx {
     cudaStream_t stream;
     void* mem;
     size_t bytes;
+    uint64_t last_use;
   };
   std::vector<WsSpace> ws_spaces;
+  uint64_t space_clock = 0;  // LRU clock of the per-stream workspaces
   void** ws_cur = nullptr;
   size_t* ws_cur_bytes = nullptr;
   // stream-K workspaces, one per launch stream (fixed size, never moved):
@@ -98,6 +100,7 @@ struct mmws_gpu_ctx {
   struct SkSpace {
     cudaStream_t stream;
     void* mem;
+    uint64_t last_use;
   };
   std::vector<SkSpace> sk_spaces;
   bool allow_streamk = true;  // false while a row-block round overlaps NCCL with multiplies
@@ -155,6 +158,24 @@ cudaError_t ensure(mmws_gpu_ctx* ctx, void** buf, size_t* have, size_t bytes);
 // The multiply workspace for work queued on `stream` (NULL: the context
 // stream) -- that stream's own, or the graph's being built -- at least
 // `bytes` long.
+// At most MAX_STREAM_SPACES per-stream workspaces of each kind are kept: a
+// caller cycling through many streams would otherwise keep one per stream
+// alive.  Over the cap the least recently used one is freed after a device
+// synchronisation (not while the latency server holds the device -- its
+// kernel never ends -- then the list just grows).
+constexpr size_t MAX_STREAM_SPACES = 16;
+template <class V>
+void trim_stream_spaces(mmws_gpu_ctx* ctx, V& spaces) {
+  while (spaces.size() >= MAX_STREAM_SPACES && !ctx->server) {
+    auto lru = spaces.begin();
+    for (auto it = spaces.begin(); it != spaces.end(); ++it)
+      if (it->last_use < lru->last_use) lru = it;
+    cudaDeviceSynchronize();
+    if (lru->mem) cudaFree(lru->mem);
+    spaces.erase(lru);
+  }
+}
+
 inline cudaError_t workspace(mmws_gpu_ctx* ctx, size_t bytes, void** out, cudaStream_t stream) {
   void** buf = ctx->ws_cur;
   size_t* have = ctx->ws_cur_bytes;
@@ -164,9 +185,11 @@ inline cudaError_t workspace(mmws_gpu_ctx* ctx, size_t bytes, void** out, cudaSt
     for (auto& w : ctx->ws_spaces)
       if (w.stream == s) sp = &w;
     if (!sp) {
-      ctx->ws_spaces.push_back({s, nullptr, 0});
+      trim_stream_spaces(ctx, ctx->ws_spaces);
+      ctx->ws_spaces.push_back({s, nullptr, 0, 0});
       sp = &ctx->ws_spaces.back();
     }
+    sp->last_use = ++ctx->space_clock;
     buf = &sp->mem;
     have = &sp->bytes;
   }

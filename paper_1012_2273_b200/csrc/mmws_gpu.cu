@@ -110,10 +110,10 @@ int check_dims(int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb, int64_
 }
 }  // namespace
 
-// The stream-K workspace of a launch stream: (num_sms + 1) accumulator slots
-// of 128 x 128 doubles and their flags, allocated (flags zeroed on the
-// stream) on first use and kept for the context's lifetime -- fixed size, so
-// a pointer baked into a launch never goes stale.
+// The stream-K workspace of a launch stream: allocated (flags zeroed on the
+// stream) on first use and kept while the stream is among the 16 most
+// recently used (trim_stream_spaces) -- fixed size, never moved; graphs never
+// use stream-K, so no pointer to it is baked into a replay.
 // Stream-K workspace of one stream: the flags of up to 4 persistent CTAs per SM
 // (zeroed once; every launch leaves them zero), then accumulator slots --
 // (grid + 1) slots of BM x BN doubles, at most (num_sms + 1) x 128 x 128.
@@ -121,9 +121,13 @@ int sk_workspace(mmws_gpu_ctx* ctx, cudaStream_t stream, double** partial, int**
   const size_t flag_bytes = round_up(sizeof(int) * (4 * static_cast<size_t>(ctx->num_sms) + 1), 4096);
   const size_t part_bytes = sizeof(double) * 128 * 128 * (static_cast<size_t>(ctx->num_sms) + 1);
   void* mem = nullptr;
-  for (const auto& sp : ctx->sk_spaces)
-    if (sp.stream == stream) mem = sp.mem;
+  for (auto& sp : ctx->sk_spaces)
+    if (sp.stream == stream) {
+      mem = sp.mem;
+      sp.last_use = ++ctx->space_clock;
+    }
   if (!mem) {
+    trim_stream_spaces(ctx, ctx->sk_spaces);
     cudaError_t e;
     if ((e = cudaMalloc(&mem, flag_bytes + part_bytes)) != cudaSuccess)
       return cuda_fail(e, "stream-K workspace");
@@ -131,7 +135,7 @@ int sk_workspace(mmws_gpu_ctx* ctx, cudaStream_t stream, double** partial, int**
       cudaFree(mem);
       return cuda_fail(e, "stream-K workspace");
     }
-    ctx->sk_spaces.push_back({stream, mem});
+    ctx->sk_spaces.push_back({stream, mem, ++ctx->space_clock});
   }
   *flags = static_cast<int*>(mem);
   *partial = reinterpret_cast<double*>(static_cast<char*>(mem) + flag_bytes);

@@ -540,6 +540,26 @@ def test_calls_on_two_streams_do_not_share_a_workspace(ctx, mode):
         assert (bits(host(C2)) == bits(want2)).all(), mode
 
 
+def test_many_streams_keep_a_bounded_set_of_workspaces(ctx):
+    # per-stream workspaces (packing, stream-K) are capped: cycling through
+    # more streams than the cap frees the least recently used ones (after a
+    # device synchronisation) -- results unchanged
+    T = torch()
+    n = 2051                                          # odd: packed operands
+    big = ctx.fill(P.DIST_UNIFORM, 41, n, n + 1)
+    A, B = big[:, 1:], big[:, :n]
+    want = bits(host(ctx.dgemm(A, B, mode=P.MODE_DMMA)))   # stream-K + packing
+    streams = [T.cuda.Stream() for _ in range(40)]
+    for rep in range(2):
+        outs = []
+        for s in streams:
+            with T.cuda.stream(s):
+                outs.append(ctx.dgemm(A, B, mode=P.MODE_DMMA))
+        T.cuda.synchronize()
+        for o in outs:
+            assert (bits(host(o)) == want).all()
+
+
 def test_one_context_from_four_threads(ctx):
     # The ABI is reentrant per context (a mutex; ctypes drops the GIL): four
     # threads, each on its own torch stream, mix device multiplies (AUTO,
