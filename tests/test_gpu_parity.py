@@ -264,7 +264,7 @@ def test_random_shapes_and_strides(ctx, oracle, seed):
 # ----------------------------------------------------------------------------- fp64 on the int8 tensor cores
 @pytest.mark.parametrize("shape", [(1, 1, 1), (7, 3, 5), (128, 128, 128), (129, 1000, 131),
                                    (300, 17, 257), (1000, 37, 999), (513, 260, 1030),
-                                   (2048, 2048, 2048)])
+                                   (2048, 2048, 2048), (64, 131072, 64), (1, 131072, 1)])
 def test_ozaki_mode_accuracy_and_integer_exactness(ctx, oracle, shape):
     m, k, n = shape
     a = oracle.fill(oracle.DIST_UNIFORM, 51, m, k)
