@@ -115,6 +115,26 @@ def test_exact_mode_bitwise_equals_matmul_seq(ctx, oracle, shape):
     assert oracle.first_difference(got, want) is None
 
 
+@pytest.mark.parametrize("shape", [(4, 1_000_000, 4), (3, 500_001, 130), (1_000_003, 16, 97),
+                                   (7, 97, 300_001)])
+def test_extreme_aspect_ratios_bit_exact(ctx, oracle, shape):
+    # very long K (one tile, a million-step chain), very tall A, very wide B:
+    # integer inputs, so every mode must reproduce the oracle's sampled rows
+    # bitwise (fp32 too while the partial sums stay below 2^24)
+    m, k, n = shape
+    a = oracle.fill(oracle.DIST_INT8, 1, m, k)
+    b = oracle.fill(oracle.DIST_INT8, 2, k, n)
+    rows = sorted({0, m // 2, m - 1})
+    want = oracle.matmul_rows(rows, a, b)
+    A, B = dev(a), dev(b)
+    for mode in (P.MODE_AUTO, P.MODE_DMMA, P.MODE_EXACT):
+        got = host(ctx.dgemm(A, B, mode=mode))[rows]
+        assert (bits(got) == bits(want)).all(), (shape, mode)
+    af, bf = a.astype(np.float32), b.astype(np.float32)
+    gf = host(ctx.sgemm(dev(af), dev(bf)))[rows].astype(np.float64)
+    assert normwise(gf, oracle.matmul_rows(rows, af, bf)) <= FP32_TOL, shape
+
+
 def test_exact_mode_signed_zeros_and_specials(ctx, oracle):
     # -0 handling: acc starts at +0, so all-zero rows give +0 (matrix.hpp:120)
     a = np.array([[-0.0, 0.0], [1e308, 1e308], [1.0, -1.0]])
