@@ -439,3 +439,26 @@ def test_bench_multi_rank_line_on_one_gpu(fake_lib):
     assert d["e2e"]["value"] > 0 and d["e2e_pageable"]["value"] > 0
     assert d["fp32"]["accuracy"]["ok"] and d["fp32"]["round"]["b_panels"] == 2
     assert d["cpu_baseline"]["cores"] >= 1 and d["gpu_launches"] > 0
+
+
+@pytest.mark.timeout(600)
+def test_cpp_dropin_master_worker_over_3_processes(fake_lib):
+    """The C++ drop-in end to end over 3 processes on one GPU: the reference's
+    own launcher starts the workers (launch_with_master / connect_from_env),
+    mmws::gpu::comm_init_from ships the NCCL id over its Communicator, and
+    master_run / worker_run run the rounds; the harness gates every record
+    against mmws::matmul_seq (tools/cpp_world_rehearsal.sh)."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "mmws_gpu_bench_ref")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/mmws_gpu_bench_ref not built (needs the reference headers)")
+    env = dict(os.environ, MMWS_GPU_NCCL_LIB=fake_lib, MMWS_BENCH_ONE_GPU_WORLD="1",
+               MMWS_GPU_ROWBLOCK_RANKS="all")
+    r = subprocess.run([exe, "--gpus", "3", "--dims", "1,10,500,2000,4099",
+                        "--models", "gpu-rowblock", "--repeats", "2"],
+                       capture_output=True, text=True, env=env, timeout=500)
+    assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-2000:])
+    rows = [ln.split() for ln in r.stdout.splitlines() if ln.startswith("gpu-rowblock")]
+    assert [int(x[1]) for x in rows] == [1, 10, 500, 2000, 4099], r.stdout
+    for x in rows:
+        assert int(x[2]) == 3 and float(x[5]) <= 1e-12, x
+

@@ -67,7 +67,9 @@ int usage() {
 // records (run_suite order: per N, `repeats` timed rounds), as worker_run.
 int run_worker(const mmws::gpu::BenchConfig& config, bool calibrate) {
   mmws::Communicator comm = mmws::connect_from_env();
-  mmws::gpu::Context ctx(comm.my_rank());
+  // one process per GPU; MMWS_BENCH_ONE_GPU_WORLD=1 (tests: every rank on GPU
+  // 0 with the loopback NCCL stand-in, MMWS_GPU_NCCL_LIB) keeps them on one
+  mmws::gpu::Context ctx(std::getenv("MMWS_BENCH_ONE_GPU_WORLD") ? 0 : comm.my_rank());
   mmws::gpu::comm_init_from(ctx, comm);
   bool rowblock = false;
   for (auto m : config.models) rowblock = rowblock || m == mmws::gpu::GpuModel::gpu_rowblock;
