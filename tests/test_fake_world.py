@@ -360,7 +360,8 @@ def test_fresh_c_every_round_keeps_few_mappings(fake_lib):
 
 @pytest.mark.timeout(900)
 def test_random_rounds_bitwise_over_3_ranks(fake_lib):
-    res = _ok(_run(3, fake_lib, "random"), 3)[0]
+    world = int(os.environ.get("MMWS_FAKE_SOAK_WORLD", "3"))  # soak runs: other worlds
+    res = _ok(_run(world, fake_lib, "random"), world)[0]
     assert len(res) == (int(os.environ["MMWS_FAKE_SOAK"].split(":")[0])
                         if os.environ.get("MMWS_FAKE_SOAK") else 24)
     bad = [r for r in res if not r[-1]]
