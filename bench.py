@@ -708,6 +708,46 @@ def measure_fp32(ctx, P, torch, dist, args, rank, world, local, barrier, gather_
     kern_ms = sum(kern) / len(kern)
     achieved = 2.0 * rows0 * n * n / (kern_ms / 1e3) / 1e12
     traffic, traffic_src = profiled_traffic(n, rows0, plan, "f32")
+
+    # e2e through the host entry, as for the headline: master_run with pinned
+    # host fp32 matrices (H2D of A and B, the round, D2H of C inside the
+    # bracket), rank 0's host wall clock, max over ranks
+    e2e = None
+    if not args.quick:
+        hA = hB = hC = None
+        if root:
+            hA = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
+            hB = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
+            hC = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
+            hA.copy_(A)
+            hB.copy_(B)
+            hA, hB, hC = hA.numpy(), hB.numpy(), hC.numpy()
+
+        def host_round32():
+            if root:
+                ctx.master_run_host(hA, hB, hC, mode=P.MODE_FFMA)
+            else:
+                ctx.master_run_host(None, None, None, mode=P.MODE_FFMA, m=n, n=n, k=n, f32=True)
+
+        host_round32()  # warm-up
+        barrier()
+        walls = []
+        for _ in range(2):
+            t0 = time.perf_counter()
+            host_round32()
+            walls.append(time.perf_counter() - t0)
+        barrier()
+        e2e_s = max(r[0] for r in gather_all([sum(walls) / len(walls)]))
+        same = None
+        if root:  # the host entry's C is the device round's C, bitwise
+            same = bool(torch.equal(torch.from_numpy(hC).view(torch.int32),
+                                    C.cpu().view(torch.int32)))
+        e2e = {"value": 2.0 * n ** 3 / e2e_s / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": 2 * 4 * n * n, "d2h_bytes_per_step": 4 * n * n,
+               "seconds_per_step": e2e_s, "bitwise_equal_device_round": same,
+               "entry": "mmws_gpu_master_run_host_f32 (C ABI), pinned host A/B/C, MODE_FFMA, "
+                        "rank 0 host wall clock (perf_counter) per call, max over ranks"}
+        del hA, hB, hC
     out = None
     if root:
         rows = sorted({0, 1, n // 3, n // 2, (2 * n) // 3, n - 2, n - 1, 12345 % n})
@@ -743,6 +783,7 @@ def measure_fp32(ctx, P, torch, dist, args, rank, world, local, barrier, gather_
                                       "GPU, checker only); tests pin the same rows against the "
                                       "CPU oracle"},
             "clocks": clocks,
+            "e2e": e2e,
         }
     del A, B, C
     torch.cuda.empty_cache()
