@@ -155,9 +155,6 @@ int ok();
 // cudaFree (a device-wide synchronisation) would wait for it forever, so the
 // old buffer is parked in deferred_free instead (growth at least doubles).
 cudaError_t ensure(mmws_gpu_ctx* ctx, void** buf, size_t* have, size_t bytes);
-// The multiply workspace for work queued on `stream` (NULL: the context
-// stream) -- that stream's own, or the graph's being built -- at least
-// `bytes` long.
 // At most MAX_STREAM_SPACES per-stream workspaces of each kind are kept: a
 // caller cycling through many streams would otherwise keep one per stream
 // alive.  Over the cap the least recently used one is freed after a device
@@ -176,6 +173,9 @@ void trim_stream_spaces(mmws_gpu_ctx* ctx, V& spaces) {
   }
 }
 
+// The multiply workspace for work queued on `stream` (NULL: the context
+// stream) -- that stream's own, or the graph's being built -- at least
+// `bytes` long.
 inline cudaError_t workspace(mmws_gpu_ctx* ctx, size_t bytes, void** out, cudaStream_t stream) {
   void** buf = ctx->ws_cur;
   size_t* have = ctx->ws_cur_bytes;
