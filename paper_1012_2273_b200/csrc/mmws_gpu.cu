@@ -110,13 +110,12 @@ int check_dims(int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb, int64_
 }
 }  // namespace
 
-// The stream-K workspace of a launch stream: allocated (flags zeroed on the
-// stream) on first use and kept while the stream is among the 16 most
-// recently used (trim_stream_spaces) -- fixed size, never moved; graphs never
-// use stream-K, so no pointer to it is baked into a replay.
-// Stream-K workspace of one stream: the flags of up to 4 persistent CTAs per SM
-// (zeroed once; every launch leaves them zero), then accumulator slots --
-// (grid + 1) slots of BM x BN doubles, at most (num_sms + 1) x 128 x 128.
+// The stream-K workspace of a launch stream: the flags of up to 4 persistent
+// CTAs per SM (zeroed once on the stream; every launch leaves them zero), then
+// accumulator slots -- (grid + 1) slots of BM x BN doubles, at most
+// (num_sms + 1) x 128 x 128.  Allocated on first use and kept while the stream
+// is among the 16 most recently used (trim_stream_spaces); fixed size, never
+// moved, and graphs never use stream-K, so no replay holds a pointer to it.
 int sk_workspace(mmws_gpu_ctx* ctx, cudaStream_t stream, double** partial, int** flags) {
   const size_t flag_bytes = round_up(sizeof(int) * (4 * static_cast<size_t>(ctx->num_sms) + 1), 4096);
   const size_t part_bytes = sizeof(double) * 128 * 128 * (static_cast<size_t>(ctx->num_sms) + 1);
@@ -528,9 +527,7 @@ void graph_release(mmws_gpu_ctx* ctx, mmws_gpu_graph* g) {
     g->ws = nullptr;
   }
 }
-}  // namespace
 
-namespace {
 // The NCCL stream gets the highest priority so its CTAs are scheduled ahead of
 // pending GEMM CTAs whenever an SM frees up -- otherwise the C gather of a
 // finished sub-block would wait for the whole next multiply.
