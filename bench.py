@@ -870,6 +870,30 @@ def measure_sweep(ctx, P, torch, np):
                     "gflops_host_entry": flops / min(th) / 1e9,
                     "hbm_GBps_device": byt / t / 1e9, "hbm_frac": byt / t / 1e9 / hbm})
         del A, B, C
+    # the resident latency server (N <= 96): host-buffer calls without a
+    # launch or a copy engine (mmws_gpu_server_dgemm); it holds SMs, so it
+    # runs last and is stopped again
+    torch.cuda.synchronize()
+    ctx.server_start()
+    try:
+        for rec in out:
+            n = rec["n"]
+            if n > 96:
+                continue
+            a = np.random.default_rng(n).uniform(-1, 1, (n, n))
+            b = np.random.default_rng(n + 1).uniform(-1, 1, (n, n))
+            c = np.empty_like(a)
+            for _ in range(50):
+                ctx.server_matmul(a, b, out=c)
+            ts = []
+            for _ in range(500):
+                t0 = time.perf_counter()
+                ctx.server_matmul(a, b, out=c)
+                ts.append(time.perf_counter() - t0)
+            rec["server_wall_us"] = min(ts) * 1e6
+            rec["server_wall_median_us"] = statistics.median(ts) * 1e6
+    finally:
+        ctx.server_stop()
     return out
 
 
