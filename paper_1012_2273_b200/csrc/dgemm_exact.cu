@@ -140,14 +140,24 @@ __global__ void __launch_bounds__(THREADS, 1)
 // SMs idle);
 // each of the 256 math threads owns (TBM/16) x (TBN/16) outputs at rows
 // 2*ty + 32v + h and columns 2*tx + 32v + h.
-constexpr int T_STAGES = 4, T_CONSUMERS = 8, T_THREADS = (T_CONSUMERS + 4) * 32;
-template <int TBM, int TBN>
+// CONS math warps (8, or 4 for the 32x32 tile): 16 x (2*CONS) math threads,
+// rows 2*ty + RP*v + h with the row period RP = 4*CONS.  The 32x32 tile
+// runs 4 math warps with 4 x 2 outputs per thread (64 registers, 4 CTAs/SM):
+// fewer LDS per DMUL+DADD than 8 warps with 2 x 2 -- device time per call
+// (round 2, tools/exact_plan_probe.py) N=256 12.4 -> 10.4 us, 300 14.4 ->
+// 12.4, 400 24.7 -> 21.3, 500 32.1 -> 26.8; on the 64x64 tile 4 warps lose
+// (N=640 52.7 vs 55.1, 1000 stream-K 140.1 vs 148.4).
+constexpr int T_STAGES = 4;
+template <int TBM, int TBN, int CONS = 8>
 struct ExactTma {
   static constexpr int A_BYTES = TBM * BK * 8, B_BYTES = BK * TBN * 8;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int SMEM = T_STAGES * STAGE + 2 * T_STAGES * 8 + 128;
-  static constexpr int TM = TBM / 16, TN = TBN / 16;  // outputs per thread
+  static constexpr int RP = 4 * CONS;                        // row period
+  static constexpr int TM = 2 * TBM / RP, TN = TBN / 16;     // outputs per thread
+  static constexpr int THREADS = (CONS + 4) * 32;
   static constexpr int MINB = TBM == 128 ? 1 : TBM == 64 ? 2 : 4;
+  static_assert(TBM % RP == 0, "row period");
 };
 
 // SK = true: stream-K with in-order fix-up, exactly as dgemm_dmma.cu's MODE 2
@@ -171,15 +181,16 @@ MMWS_DEVICE void exact_wait_flag(const int* f) {
   }
 }
 
-template <int TBM, int TBN, bool SK = false>
-__global__ void __launch_bounds__(T_THREADS, ExactTma<TBM, TBN>::MINB)
+template <int TBM, int TBN, bool SK = false, int CONS = 8>
+__global__ void __launch_bounds__(ExactTma<TBM, TBN, CONS>::THREADS, ExactTma<TBM, TBN, CONS>::MINB)
     dgemm_exact_tma_kernel(const __grid_constant__ CUtensorMap tmA,
                            const __grid_constant__ CUtensorMap tmB, double* C,
                            int64_t ldc, int M, int N, int K, int tiles_m, int tiles_n,
                            double* partial = nullptr, int* flags = nullptr,
                            const double* cin = nullptr, int64_t ldcin = 0) {
-  using X = ExactTma<TBM, TBN>;
+  using X = ExactTma<TBM, TBN, CONS>;
   constexpr int T_A_BYTES = X::A_BYTES, T_STAGE = X::STAGE, TM = X::TM, TN = X::TN;
+  constexpr int RP = X::RP, T_CONSUMERS = CONS;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + T_STAGES * T_STAGE);
@@ -264,7 +275,7 @@ __global__ void __launch_bounds__(T_THREADS, ExactTma<TBM, TBN>::MINB)
     if (!SK && cin) {  // accumulate: continue Cin's chains (epilogue layout)
 #pragma unroll
       for (int i = 0; i < TM; ++i) {
-        const int r = tm * TBM + ty * 2 + 32 * (i >> 1) + (i & 1);
+        const int r = tm * TBM + ty * 2 + RP * (i >> 1) + (i & 1);
         if (r >= M) continue;
 #pragma unroll
         for (int j = 0; j < TN; ++j) {
@@ -301,7 +312,7 @@ __global__ void __launch_bounds__(T_THREADS, ExactTma<TBM, TBN>::MINB)
 #pragma unroll
         for (int i = 0; i < TM; ++i)
           a2[i] =
-              *reinterpret_cast<const double2*>(as + (ty * 2 + 32 * (i >> 1) + (i & 1)) * BK + k);
+              *reinterpret_cast<const double2*>(as + (ty * 2 + RP * (i >> 1) + (i & 1)) * BK + k);
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk) {
           double b[TN];
@@ -339,7 +350,7 @@ __global__ void __launch_bounds__(T_THREADS, ExactTma<TBM, TBN>::MINB)
     }
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
-      const int r = tm * TBM + ty * 2 + 32 * (i >> 1) + (i & 1);
+      const int r = tm * TBM + ty * 2 + RP * (i >> 1) + (i & 1);
       if (r >= M) continue;
       double* crow = C + static_cast<int64_t>(r) * ldc;
 #pragma unroll
@@ -364,22 +375,22 @@ bool make_map_f64(const Launch& L, CUtensorMap* map, const double* base, int64_t
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int TBM, int TBN, bool SK = false>
+template <int TBM, int TBN, bool SK = false, int CONS = 8>
 cudaError_t run_exact_tma(const Launch& L, int64_t M, int64_t N, int64_t K, const double* A,
                           int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                           double* partial = nullptr, int* flags = nullptr, int grid = 0,
                           const double* cin = nullptr, int64_t ldcin = 0) {
-  using X = ExactTma<TBM, TBN>;
+  using X = ExactTma<TBM, TBN, CONS>;
   CUtensorMap ta, tb;
   if (!make_map_f64(L, &ta, A, K, M, lda, BK, TBM) || !make_map_f64(L, &tb, B, N, K, ldb, TBN, BK))
     return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(dgemm_exact_tma_kernel<TBM, TBN, SK>,
+  cudaError_t e = cudaFuncSetAttribute(dgemm_exact_tma_kernel<TBM, TBN, SK, CONS>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, X::SMEM);
   if (e != cudaSuccess) return e;
   const int tiles_m = static_cast<int>((M + TBM - 1) / TBM);
   const int tiles_n = static_cast<int>((N + TBN - 1) / TBN);
-  dgemm_exact_tma_kernel<TBM, TBN, SK><<<SK ? grid : tiles_m * tiles_n, T_THREADS, X::SMEM,
-                                         L.stream>>>(ta, tb, C, ldc, static_cast<int>(M),
+  dgemm_exact_tma_kernel<TBM, TBN, SK, CONS><<<SK ? grid : tiles_m * tiles_n, X::THREADS,
+                                               X::SMEM, L.stream>>>(ta, tb, C, ldc, static_cast<int>(M),
                                                      static_cast<int>(N), static_cast<int>(K),
                                                      tiles_m, tiles_n, partial, flags, cin,
                                                      ldcin);
@@ -408,7 +419,7 @@ const char* exact_oneshot_plan(const Launch& L, int64_t M, int64_t N, const doub
   if (!exact_tma_ok(lda, ldb, A, B)) return "dgemm_exact_kernel<128x128, cp.async>";
   const int64_t tiles64 = ((M + 63) / 64) * ((N + 63) / 64);
   const int64_t tiles128 = ((M + 127) / 128) * ((N + 127) / 128);
-  if (2 * tiles64 <= L.num_sms) return "dgemm_exact_tma_kernel<32x32>";
+  if (2 * tiles64 <= L.num_sms) return "dgemm_exact_tma_kernel<32x32>";  // 4 math warps
   return tiles128 < 2 * L.num_sms ? "dgemm_exact_tma_kernel<64x64>"
                                   : "dgemm_exact_tma_kernel<128x128>";
 }
@@ -427,9 +438,9 @@ cudaError_t launch_dgemm_exact(const Launch& L, int64_t M, int64_t N, int64_t K,
     // 78.7, 256x2000x2000 153.9 vs 211.8), then 64x64 tiles while 128x128
     // ones would not give every SM two CTAs
     const int64_t tiles64 = ((M + 63) / 64) * ((N + 63) / 64);
-    if (2 * tiles64 <= L.num_sms)
-      return run_exact_tma<32, 32>(L, M, N, K, A, lda, B, ldb, C, ldc, nullptr, nullptr, 0, cin,
-                                   ldcin);
+    if (2 * tiles64 <= L.num_sms)  // 4 math warps, 4 x 2 outputs each (see ExactTma)
+      return run_exact_tma<32, 32, false, 4>(L, M, N, K, A, lda, B, ldb, C, ldc, nullptr, nullptr,
+                                             0, cin, ldcin);
     return tiles_m * tiles_n < 2 * L.num_sms
                ? run_exact_tma<64, 64>(L, M, N, K, A, lda, B, ldb, C, ldc, nullptr, nullptr, 0,
                                        cin, ldcin)
@@ -452,7 +463,7 @@ cudaError_t launch_dgemm_exact(const Launch& L, int64_t M, int64_t N, int64_t K,
 }
 
 cudaError_t preload_dgemm_exact() {
-  return preload_kernels(dgemm_exact_tma_kernel<32, 32>, dgemm_exact_tma_kernel<64, 64>,
+  return preload_kernels(dgemm_exact_tma_kernel<32, 32, false, 4>, dgemm_exact_tma_kernel<64, 64>,
                          dgemm_exact_tma_kernel<128, 128>,
                          dgemm_exact_tma_kernel<128, 128, true>, dgemm_exact_tma_kernel<64, 64, true>,
                          dgemm_exact_kernel<true, true>, dgemm_exact_kernel<true, false>,

@@ -232,7 +232,8 @@ int dgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
     // exact order: the latency kernels for tiny problems -- plain loads, any
     // layout -- up to n, k <= 192 (above that the 32x32 TMA tiles win;
     // device time per call, latency kernel vs 32x32 TMA, round 2: N=128 6.3
-    // vs 8.3 us, 160 8.3 vs 8.4, 200 12.0 vs 10.4, 300 20.6 vs 14.4) and up
+    // vs 7.1 us, 160 8.2 vs 8.3, 192 8.3 vs 8.5, 200 12.0 vs 10.3, 300 20.6
+    // vs 12.4) and up
     // to 320 for layouts TMA cannot read; the stream-K form of the 128x128
     // TMA kernel (operands packed if needed) from one tile per SM, of the
     // 64x64 one below that where a one-shot launch would load the SMs
