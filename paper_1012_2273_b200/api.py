@@ -175,9 +175,10 @@ def _ld(t) -> int:
     return t.stride(0)
 
 
-def _device_operands(A, B, C_, dtype, who: str):
+def _device_operands(A, B, C_, dtype, who: str, device: Optional[int] = None):
     """Shapes (m, n, k) of C_ = A . B on the device; every tensor must be a
-    2-D CUDA tensor of `dtype`, and C_ (if given) at least m x n."""
+    2-D CUDA tensor of `dtype` on the context's device, and C_ (if given) at
+    least m x n."""
     for name, t in (("A", A), ("B", B), ("C", C_)):
         if t is None:
             continue
@@ -185,6 +186,8 @@ def _device_operands(A, B, C_, dtype, who: str):
             raise DomainError(f"{who}: {name} must be {dtype}, got {t.dtype}")
         if not t.is_cuda:
             raise DomainError(f"{who}: {name} must be a CUDA tensor")
+        if device is not None and t.device.index != device:
+            raise DomainError(f"{who}: {name} is on {t.device}, the context on cuda:{device}")
         if t.dim() != 2:
             raise DimensionError(f"{who}: {name} must be 2-D, got {t.dim()}-D")
     m, k = A.shape
@@ -287,11 +290,11 @@ class Context:
         bitwise the one call when every call takes the same kernel family --
         see include/mmws_gpu.h)."""
         import torch
-        m, n, k = _device_operands(A, B, C_, torch.float64, "dgemm")
+        m, n, k = _device_operands(A, B, C_, torch.float64, "dgemm", self.device)
         if C_ is None:
             C_ = torch.empty((m, n), dtype=torch.float64, device=A.device)
         if accumulate is not None:
-            _device_operands(A, B, accumulate, torch.float64, "dgemm")
+            _device_operands(A, B, accumulate, torch.float64, "dgemm", self.device)
             _check(_lib().mmws_gpu_dgemm_acc(self._h, m, n, k, _ptr(A), _ld(A), _ptr(B), _ld(B),
                                              _ptr(accumulate), _ld(accumulate), _ptr(C_), _ld(C_),
                                              mode, _stream(stream)))
@@ -304,11 +307,11 @@ class Context:
         """fp32 C_ = A . B; with `accumulate`, C_ = accumulate + A . B
         (mmws_gpu_sgemm_acc)."""
         import torch
-        m, n, k = _device_operands(A, B, C_, torch.float32, "sgemm")
+        m, n, k = _device_operands(A, B, C_, torch.float32, "sgemm", self.device)
         if C_ is None:
             C_ = torch.empty((m, n), dtype=torch.float32, device=A.device)
         if accumulate is not None:
-            _device_operands(A, B, accumulate, torch.float32, "sgemm")
+            _device_operands(A, B, accumulate, torch.float32, "sgemm", self.device)
             _check(_lib().mmws_gpu_sgemm_acc(self._h, m, n, k, _ptr(A), _ld(A), _ptr(B), _ld(B),
                                              _ptr(accumulate), _ld(accumulate), _ptr(C_), _ld(C_),
                                              mode, _stream(stream)))
@@ -342,6 +345,15 @@ class Context:
              out=None, stream=None):
         import torch
         dtype = dtype or torch.float64
+        if dtype not in (torch.float64, torch.float32):
+            raise DomainError(f"fill: dtype must be float64 or float32, got {dtype}")
+        if out is not None:
+            if out.dtype not in (torch.float64, torch.float32):
+                raise DomainError(f"fill: out must be float64 or float32, got {out.dtype}")
+            if not out.is_cuda or out.device.index != self.device:
+                raise DomainError(f"fill: out is on {out.device}, the context on cuda:{self.device}")
+            if out.dim() != 2 or out.shape[0] < rows or out.shape[1] < cols:
+                raise DimensionError(f"fill: out is {tuple(out.shape)}, needs at least ({rows}, {cols})")
         t = out if out is not None else torch.empty((rows, cols), dtype=dtype,
                                                     device=f"cuda:{self.device}")
         _check(_lib().mmws_gpu_fill(self._h, dist, seed, _ptr(t), rows, cols, _ld(t),
@@ -353,7 +365,7 @@ class Context:
         import torch
         if C_ is None:
             raise DomainError("graph_dgemm: C must be given (the graph writes into it on every replay)")
-        m, n, k = _device_operands(A, B, C_, torch.float64, "graph_dgemm")
+        m, n, k = _device_operands(A, B, C_, torch.float64, "graph_dgemm", self.device)
         g = C.c_void_p()
         _check(_lib().mmws_gpu_graph_dgemm(self._h, m, n, k, _ptr(A), _ld(A), _ptr(B), _ld(B),
                                            _ptr(C_), _ld(C_), mode, C.byref(g)))
@@ -420,7 +432,7 @@ class Context:
             if A is None or B is None or C_ is None:
                 raise DomainError("rowblock: rank 0 passes A, B and C")
             dt = torch.float32 if f32 else torch.float64
-            _device_operands(A, B, C_, dt, "rowblock")
+            _device_operands(A, B, C_, dt, "rowblock", self.device)
             if tuple(A.shape) != (m, k) or tuple(B.shape) != (k, n) or tuple(C_.shape) != (m, n):
                 raise DimensionError(f"rowblock: shapes {tuple(A.shape)} x {tuple(B.shape)} -> "
                                      f"{tuple(C_.shape)} do not match m={m} n={n} k={k}")
@@ -446,6 +458,10 @@ def _master_run_host(self, a=None, b=None, out=None, mode: int = MODE_AUTO, m=No
     arrays, pinned for full PCIe bandwidth); other ranks pass nothing but the
     shape.  Returns (C or None, elapsed_s)."""
     if a is not None:
+        if b is None:
+            raise DomainError("master_run: rank 0 passes both A and B")
+        if a.ndim != 2 or b.ndim != 2:
+            raise DimensionError("master_run expects 2-D matrices")
         if a.shape[1] != b.shape[0]:
             raise DimensionError(f"master_run: inner dimensions disagree, {a.shape[1]} vs {b.shape[0]}")
         m, k = a.shape
@@ -457,6 +473,8 @@ def _master_run_host(self, a=None, b=None, out=None, mode: int = MODE_AUTO, m=No
         for x in (a, b):
             if not x.flags["C_CONTIGUOUS"]:
                 raise DimensionError("master_run: host matrices must be C-contiguous")
+    elif m is None or n is None or k is None:
+        raise DomainError("master_run: a worker rank passes the shape (m, n, k)")
     el = C.c_double()
     fn = _lib().mmws_gpu_master_run_host_f32 if f32 else _lib().mmws_gpu_master_run_host
     ptr = (lambda x: x.ctypes.data if x is not None else None)

@@ -267,3 +267,40 @@ def test_python_output_buffer_checks_without_a_gpu():
         api._device_operands(a, b, None, torch.float64, "t")
     with pytest.raises(P.DomainError):
         api._device_operands(a.float(), b, None, torch.float64, "t")
+
+
+def test_device_operand_checks_name_the_context_device():
+    # operands on another GPU than the context's would be read through UVA by
+    # the kernels (an illegal address without peer access): refused up front
+    import torch
+
+    from paper_1012_2273_b200 import api
+
+    class FakeCuda:
+        def __init__(self, shape, index):
+            self.shape, self.dtype, self.is_cuda = shape, torch.float64, True
+            self.device = torch.device("cuda", index)
+
+        def dim(self):
+            return 2
+
+    a, b = FakeCuda((3, 2), 1), FakeCuda((2, 4), 1)
+    assert api._device_operands(a, b, None, torch.float64, "t", 1) == (3, 4, 2)
+    with pytest.raises(P.DomainError, match="cuda:1.*cuda:0"):
+        api._device_operands(a, b, None, torch.float64, "t", 0)
+
+
+def test_master_run_host_argument_checks_without_a_gpu():
+    import numpy as np
+
+    from paper_1012_2273_b200 import api
+
+    class Ctx:  # the checks run before the C ABI is reached
+        _h = None
+
+    with pytest.raises(P.DomainError):
+        api._master_run_host(Ctx(), np.zeros((2, 2)))
+    with pytest.raises(P.DimensionError):
+        api._master_run_host(Ctx(), np.zeros(4), np.zeros((2, 2)))
+    with pytest.raises(P.DomainError):
+        api._master_run_host(Ctx(), m=4, n=None, k=4)
