@@ -452,6 +452,7 @@ def run_ours(args) -> None:
     def round64():
         ctx.rowblock(n, n, n, A, B, C, mode=mode)
 
+    barrier()
     for _ in range(args.warmup):
         round64()
     barrier()
@@ -509,6 +510,9 @@ def run_ours(args) -> None:
             ctx.master_run_host(None, None, None, mode=mode, m=n, n=n, k=n)
 
     def e2e_wall(a, b, c, steps):
+        # workers wait for rank 0's host-side preparation here (torch's own
+        # collective timeout), not inside the round's 30 s deadline
+        barrier()
         host_round(a, b, c)  # warm-up (staging buffers, IPC mappings)
         barrier()
         walls = []
@@ -693,6 +697,7 @@ def measure_fp32(ctx, P, torch, dist, args, rank, world, local, barrier, gather_
     def round32():
         ctx.rowblock(n, n, n, A, B, C, mode=P.MODE_FFMA, f32=True)
 
+    barrier()
     round32()  # warm-up
     sampler = ClockSampler(local) if root else None
     if sampler:
@@ -729,6 +734,7 @@ def measure_fp32(ctx, P, torch, dist, args, rank, world, local, barrier, gather_
             else:
                 ctx.master_run_host(None, None, None, mode=P.MODE_FFMA, m=n, n=n, k=n, f32=True)
 
+        barrier()  # rank 0 pinned 3 x 4 GiB meanwhile: outside the round's deadline
         host_round32()  # warm-up
         barrier()
         walls = []
