@@ -690,8 +690,9 @@ def measure_fp32(ctx, P, torch, dist, args, rank, world, local, barrier, gather_
         C = torch.empty_like(A)
     torch.cuda.synchronize()
     ffma2_peak = max(ctx.peak_probe(P.PROBE_FFMA2, 100000) for _ in range(3))
-    # the GEMM's own operand pattern in registers (one fresh register operand
-    # per FFMA2): the ceiling of an FFMA2 GEMM, DESIGN.md s3.4
+    # the outer-product operand pattern in registers (one fresh register
+    # operand per FFMA2): one register-only loop of it, not a ceiling -- the
+    # rate depends on where ptxas puts the operands
     pattern_peak = max(ctx.peak_probe(P.PROBE_FFMA2_OUTER, 20000) for _ in range(3))
 
     def round32():
@@ -777,12 +778,16 @@ def measure_fp32(ctx, P, torch, dist, args, rank, world, local, barrier, gather_
                          "peak_source": "measured live in this run: FFMA2 (fma.rn.f32x2) "
                                         "throughput probe",
                          "peak_nominal": NOMINAL_FP32_TFLOPS,
-                         "pattern_ceiling": pattern_peak,
-                         "frac_of_pattern_ceiling": achieved / pattern_peak,
-                         "pattern_note": "FFMA2 outer product with a fresh broadcast register "
-                                         "operand per instruction (the kernel's pattern), "
-                                         "registers only, same shape (8 warps/SM, 64 pairs "
-                                         "per lane): mmws_gpu_peak_probe(FFMA2_OUTER)"},
+                         "pattern_probe": pattern_peak,
+                         "pattern_note": "register-only FFMA2 outer-product loop at the kernel's "
+                                         "shape (8 warps/SM, 64 pairs per lane, one fresh "
+                                         "broadcast operand per instruction): "
+                                         "mmws_gpu_peak_probe(FFMA2_OUTER); not a ceiling -- "
+                                         "such loops measure 62-71 TFLOP/s depending on the "
+                                         "register assignment (profiles/r02_ffma2_shape_probe.txt)"
+                                         ", and the kernel with A staged k-major beats this one",
+                         "transpose_pass": "A is transposed once per launch (HBM-bound, 0.17% of "
+                                           "the multiply at N=32768) inside the timed region"},
             "accuracy": {"normwise_rel_error": err, "bound": 1e-5, "ok": err <= 1e-5,
                          "rows": rows,
                          "reference": "fp64 product of the widened fp32 rows (torch fp64 on the "

@@ -131,7 +131,8 @@ void* mmws_gpu_stream(mmws_gpu_ctx* ctx);
  * NULL or "": the default).  Knobs: MMWS_GPU_NO_STREAMK, MMWS_GPU_DMMA_PLAN,
  * MMWS_GPU_RASTER_GROUP, MMWS_GPU_PIPELINE_TRACE, MMWS_GPU_ROWBLOCK_RANKS
  * (all | 1), MMWS_GPU_SERVER_CTAS, MMWS_GPU_COPY_THREADS, MMWS_GPU_TIMEOUT_S,
- * MMWS_GPU_NCCL_GATHER (C-slices as NCCL messages instead of fused stores). */
+ * MMWS_GPU_NCCL_GATHER (C-slices as NCCL messages instead of fused stores),
+ * MMWS_GPU_SGEMM_AT (0 | 1: fp32 A staged as it lies | transposed, k-major). */
 int mmws_gpu_tune(mmws_gpu_ctx* ctx, const char* knob, const char* value);
 
 /* ---------------------------------------------------------------- host-only helpers */

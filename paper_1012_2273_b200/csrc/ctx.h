@@ -24,6 +24,7 @@ struct Tuning {
   int host_panels = 0;          // MMWS_GPU_HOST_PANELS: row panels of a host-buffer multiply (0 = built-in)
   double timeout_s = 30.0;      // MMWS_GPU_TIMEOUT_S: deadline of one distributed step
   bool nccl_gather = false;     // MMWS_GPU_NCCL_GATHER: C-slices as NCCL messages, no fused IPC
+  int sgemm_at = -1;            // MMWS_GPU_SGEMM_AT: fp32 A staged k-major; -1 by size, 0 never, 1 always
   static Tuning from_env();
   // Set one knob by its environment name (value NULL: back to the default);
   // false for an unknown name.

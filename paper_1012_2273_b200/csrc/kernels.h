@@ -172,9 +172,15 @@ bool sgemm_tma_supported(int64_t lda, int64_t ldb, const float* A, const float* 
 // cin (optional): accumulate, C = Cin + A.B -- the running totals start from
 // Cin; splitting K at multiples of 1024 (the partial-sum chunk) and chaining
 // launches gives bitwise the one-launch result.
+// a_transposed: A points at A^T ([K][M], pitch lda >= M, lda % 4 == 0) and is
+// staged k-major.
 cudaError_t launch_sgemm_tma(const Launch& L, int64_t M, int64_t N, int64_t K, const float* A,
                              int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
-                             const float* cin = nullptr, int64_t ldcin = 0);
+                             const float* cin = nullptr, int64_t ldcin = 0,
+                             bool a_transposed = false);
+// dst[cols][rows] (pitch ld_dst) = src[rows][cols] (pitch ld_src, any alignment).
+cudaError_t launch_transpose_f32(const Launch& L, const float* src, int64_t rows, int64_t cols,
+                                 int64_t ld_src, float* dst, int64_t ld_dst);
 
 // Pad/pack src[rows, cols] (ld_src) into dst[rows_p, cols_p] (ld_dst), zero fill.
 cudaError_t launch_pack_f64(const Launch& L, const double* src, int64_t rows, int64_t cols,

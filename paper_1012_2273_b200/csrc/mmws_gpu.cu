@@ -57,6 +57,8 @@ bool Tuning::set(const char* name, const char* v) {
     timeout_s = s > 0 ? s : d.timeout_s;
   } else if (!std::strcmp(name, "MMWS_GPU_NCCL_GATHER")) {
     nccl_gather = v != nullptr;
+  } else if (!std::strcmp(name, "MMWS_GPU_SGEMM_AT")) {
+    sgemm_at = v ? (std::atoi(v) != 0 ? 1 : 0) : d.sgemm_at;
   } else {
     return false;
   }
@@ -68,8 +70,7 @@ Tuning Tuning::from_env() {
   for (const char* name : {"MMWS_GPU_NO_STREAMK", "MMWS_GPU_DMMA_PLAN", "MMWS_GPU_RASTER_GROUP",
                            "MMWS_GPU_PIPELINE_TRACE", "MMWS_GPU_ROWBLOCK_RANKS",
                            "MMWS_GPU_SERVER_CTAS", "MMWS_GPU_COPY_THREADS", "MMWS_GPU_HOST_PANELS",
-                           "MMWS_GPU_TIMEOUT_S",
-                           "MMWS_GPU_NCCL_GATHER"})
+                           "MMWS_GPU_TIMEOUT_S", "MMWS_GPU_NCCL_GATHER", "MMWS_GPU_SGEMM_AT"})
     if (const char* v = std::getenv(name)) t.set(name, v);
   return t;
 }
@@ -387,16 +388,31 @@ int sgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const flo
   // floats: other layouts are packed once into the workspace (one HBM-bound
   // pass, zero padding never read), so every layout runs the same kernel --
   // and gets the same bits.
+  //
+  // Wide problems take A transposed: one more HBM-bound pass writes A^T into
+  // the workspace (any layout of A), and the kernel stages A k-major, which
+  // keeps every row's A scalar in one register bank (sgemm_tma.cu; +6 % FFMA2
+  // rate).  The pass costs 8mk bytes against 2mnk flops, ~40/n of the
+  // multiply: taken from n = 2048.  Same FFMA chain per element either way,
+  // so the same bits.
   cudaError_t e;
-  const bool a_aligned = lda % 4 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0;
+  const bool a_t = ctx->tune.sgemm_at < 0 ? n >= 2048 && m >= 128 : ctx->tune.sgemm_at == 1;
+  const bool a_aligned = a_t || (lda % 4 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0);
   const bool b_aligned = ldb % 4 == 0 && reinterpret_cast<uintptr_t>(B) % 16 == 0;
-  if (!a_aligned || !b_aligned) {
-    const int64_t lda_p = round_up(k, 4), ldb_p = round_up(n, 4);
-    const size_t bytes = sizeof(float) * ((a_aligned ? 0 : m * lda_p) + (b_aligned ? 0 : k * ldb_p));
+  if (a_t || !a_aligned || !b_aligned) {
+    const int64_t lda_p = round_up(k, 4), ldb_p = round_up(n, 4), ldat = round_up(m, 4);
+    const size_t bytes = sizeof(float) * ((a_t ? k * ldat : a_aligned ? 0 : m * lda_p) +
+                                          (b_aligned ? 0 : k * ldb_p));
     void* wsp = nullptr;
     if ((e = workspace(ctx, bytes, &wsp, L.stream)) != cudaSuccess) return cuda_fail(e, "sgemm pack workspace");
     float* w = static_cast<float*>(wsp);
-    if (!a_aligned) {
+    if (a_t) {
+      if ((e = launch_transpose_f32(L, A, m, k, lda, w, ldat)) != cudaSuccess)
+        return cuda_fail(e, "sgemm transpose A");
+      A = w;
+      lda = ldat;
+      w += k * ldat;
+    } else if (!a_aligned) {
       if ((e = launch_pack_f32(L, A, m, k, lda, w, m, lda_p, lda_p)) != cudaSuccess)
         return cuda_fail(e, "sgemm pack A");
       A = w;
@@ -410,8 +426,8 @@ int sgemm_dispatch(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const flo
       ldb = ldb_p;
     }
   }
-  e = launch_sgemm_tma(L, m, n, k, A, lda, B, ldb, C, ldc, cin, ldcin);
-  ctx->last_plan = "sgemm_tma_kernel<128x256, FFMA2>";
+  e = launch_sgemm_tma(L, m, n, k, A, lda, B, ldb, C, ldc, cin, ldcin, a_t);
+  ctx->last_plan = a_t ? "sgemm_tma_kernel<128x256, FFMA2, A k-major>" : "sgemm_tma_kernel<128x256, FFMA2>";
   return e == cudaSuccess ? ok() : cuda_fail(e, "sgemm ffma");
 }
 

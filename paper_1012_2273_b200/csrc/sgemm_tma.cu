@@ -25,11 +25,19 @@
 //     barrier), the ptxas-proof ordering dgemm_dmma.cu documents.
 // Operand pattern: every FFMA2 reads its accumulator pair and the broadcast A
 // scalar from the register file (the B pair comes from the operand reuse
-// cache); a register-only loop of exactly this pattern peaks at ~63 TFLOP/s
-// on B200 against ~69.5 when the scalar is a uniform register
-// (tools/ffma2_uniform_probe.cu, profiles/r02_ffma2_uniform_probe.txt) -- the
-// kernel runs at ~99% of its pattern's ceiling.  Layouts TMA cannot read are
-// packed by the caller (mmws_gpu.cu), so every layout takes this kernel.
+// cache).  How fast that issues depends on where the operands sit in the
+// register file: register-only loops of this outer product measure 56-71
+// TFLOP/s on B200 depending on the block shape and ptxas' assignment
+// (tools/ffma2_shape_probe.cu), and with the operands fed by LDS.128 the
+// row-major A stage -- a float4 holds four k of one row, so a row's scalar
+// changes register bank with k -- costs 64.3 against 68.6 TFLOP/s for a
+// k-major stage, where a float4 holds four rows of one k and each row's scalar
+// keeps its register (tools/ffma2_lds_probe.cu, profiles/r02_ffma2_lds_probe.txt).
+// Hence the AT instance: wide problems transpose A once (transpose_f32_kernel,
+// HBM-bound, 0.17 % of the multiply at N=32768) and TMA stages A^T tiles;
+// N=16384 65.0 vs 62.3 TFLOP/s, same bits (profiles/r02_sgemm_k_major.txt).
+// Layouts TMA cannot read are packed by the caller (mmws_gpu.cu), so every
+// layout takes this kernel.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -61,6 +69,11 @@ constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TOT_BYTES = CONSUMERS * 32 * 128 * 4;  // 128 floats per math lane
 constexpr int SMEM = STAGES * STAGE_BYTES + TOT_BYTES + 2 * STAGES * 8 + 128;
 
+// AT: tmA describes A transposed ([K][M], made by transpose_f32_kernel), so a
+// stage holds A k-major ([16 k][128 rows]) and one LDS.128 brings four rows of
+// one k -- a row's A scalar then sits in the same register bank for every k
+// (see the header); otherwise A is staged as it lies ([128 rows][16 k]).
+template <bool AT>
 __global__ void __launch_bounds__(THREADS, 1)
     sgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB, float* C, int64_t ldc,
@@ -102,7 +115,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
         uint8_t* sa = smem + s * STAGE_BYTES;
         mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-        tma_load_2d(sa, &tmA, &full[s], kt * BK, tm * BM);
+        if (AT) tma_load_2d(sa, &tmA, &full[s], tm * BM, kt * BK);
+        else tma_load_2d(sa, &tmA, &full[s], kt * BK, tm * BM);
         tma_load_2d(sa + A_BYTES, &tmB, &full[s], tn * BN, kt * BK);
       }
     }
@@ -152,11 +166,18 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
     for (int k4 = 0; k4 < BK; k4 += 4) {
       float4 a4[8];
+      if (!AT) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        a4[i] = *reinterpret_cast<const float4*>(as + (row_base + i) * BK + k4);
+        for (int i = 0; i < 8; ++i)
+          a4[i] = *reinterpret_cast<const float4*>(as + (row_base + i) * BK + k4);
+      }
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
+        float4 at[2];  // AT: rows row_base .. +7 at k = k4 + kk
+        if (AT) {
+          at[0] = *reinterpret_cast<const float4*>(as + (k4 + kk) * BM + row_base);
+          at[1] = *reinterpret_cast<const float4*>(as + (k4 + kk) * BM + row_base + 4);
+        }
         f32x2 b2[8];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -167,7 +188,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         f32x2 aa[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float a = kk == 0 ? a4[i].x : kk == 1 ? a4[i].y : kk == 2 ? a4[i].z : a4[i].w;
+          float a;
+          if (AT) {
+            const float4 t = at[i >> 2];
+            a = (i & 3) == 0 ? t.x : (i & 3) == 1 ? t.y : (i & 3) == 2 ? t.z : t.w;
+          } else {
+            a = kk == 0 ? a4[i].x : kk == 1 ? a4[i].y : kk == 2 ? a4[i].z : a4[i].w;
+          }
           aa[i] = pack2(a, a);
         }
         // B pair outer, A inner: consecutive FFMA2s share the B pair (operand
@@ -175,7 +202,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int p = 0; p < 8; ++p)
 #pragma unroll
-          for (int i = 0; i < 8; ++i) ffma2(part[i][p], aa[i], b2[p]);
+          for (int i = 0; i < 8; ++i) ffma2(part[i][p], b2[p], aa[i]);
       }
     }
     if ((kt % KC_STAGES) == KC_STAGES - 1 || kt + 1 == KT) {
@@ -213,6 +240,28 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// A [rows][cols] (pitch ld_src, any alignment) -> dst [cols][rows] (pitch
+// ld_dst): one HBM-bound pass, 32x32 tiles through shared memory so both sides
+// are coalesced.
+__global__ void __launch_bounds__(256)
+    transpose_f32_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, int64_t ld_src,
+                         float* __restrict__ dst, int64_t ld_dst) {
+  __shared__ float tile[32][33];
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 32, r0 = static_cast<int64_t>(blockIdx.y) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < 32; j += 8) {
+    const int64_t r = r0 + ty + j, c = c0 + tx;
+    tile[ty + j][tx] = r < rows && c < cols ? src[r * ld_src + c] : 0.f;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 32; j += 8) {
+    const int64_t c = c0 + ty + j, r = r0 + tx;
+    if (c < cols && r < rows) dst[c * ld_dst + r] = tile[tx][ty + j];
+  }
+}
+
 bool make_map_f32(const Launch& L, CUtensorMap* map, const float* base, int64_t inner,
                   int64_t outer, int64_t ld, int box_inner, int box_outer) {
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
@@ -233,25 +282,38 @@ bool sgemm_tma_supported(int64_t lda, int64_t ldb, const float* A, const float* 
          reinterpret_cast<uintptr_t>(B) % 16 == 0;
 }
 
+cudaError_t launch_transpose_f32(const Launch& L, const float* src, int64_t rows, int64_t cols,
+                                 int64_t ld_src, float* dst, int64_t ld_dst) {
+  const dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
+  transpose_f32_kernel<<<grid, 256, 0, L.stream>>>(src, rows, cols, ld_src, dst, ld_dst);
+  L.count();
+  return cudaGetLastError();
+}
+
+// a_transposed: A points at A transposed ([K][M], pitch lda >= M)
 cudaError_t launch_sgemm_tma(const Launch& L, int64_t M, int64_t N, int64_t K, const float* A,
                              int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
-                             const float* cin, int64_t ldcin) {
+                             const float* cin, int64_t ldcin, bool a_transposed) {
   CUtensorMap ta, tb;
-  if (!make_map_f32(L, &ta, A, K, M, lda, BK, BM)) return cudaErrorInvalidValue;
+  if (a_transposed ? !make_map_f32(L, &ta, A, M, K, lda, BM, BK)
+                   : !make_map_f32(L, &ta, A, K, M, lda, BK, BM))
+    return cudaErrorInvalidValue;
   if (!make_map_f32(L, &tb, B, N, K, ldb, BN, BK)) return cudaErrorInvalidValue;
-  cudaError_t e =
-      cudaFuncSetAttribute(sgemm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  auto kern = a_transposed ? sgemm_tma_kernel<true> : sgemm_tma_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
   if (e != cudaSuccess) return e;
   const int tiles_m = static_cast<int>((M + BM - 1) / BM);
   const int tiles_n = static_cast<int>((N + BN - 1) / BN);
   const int vec_c = (ldc % 4 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0);
-  sgemm_tma_kernel<<<tiles_m * tiles_n, THREADS, SMEM, L.stream>>>(
+  kern<<<tiles_m * tiles_n, THREADS, SMEM, L.stream>>>(
       ta, tb, C, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), tiles_m,
       tiles_n, vec_c, cin, ldcin);
   L.count();
   return cudaGetLastError();
 }
 
-cudaError_t preload_sgemm_tma() { return preload_kernels(sgemm_tma_kernel); }
+cudaError_t preload_sgemm_tma() {
+  return preload_kernels(sgemm_tma_kernel<false>, sgemm_tma_kernel<true>, transpose_f32_kernel);
+}
 
 }  // namespace mmws_impl

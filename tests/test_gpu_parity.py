@@ -1118,6 +1118,44 @@ def test_fp32_unaligned_layouts_are_packed_and_bitwise_the_aligned_call(ctx, ora
     assert ctx.last_plan.startswith("sgemm_tma_kernel")
 
 
+def test_fp32_k_major_staging_is_bitwise_the_row_major_kernel(ctx, oracle):
+    # wide fp32 problems transpose A first and stage it k-major (sgemm_tma.cu):
+    # same FFMA chain per element, so the same bits as the kernel that stages A
+    # as it lies -- ragged shapes, unaligned / strided A, accumulate
+    T = torch()
+    rng = np.random.default_rng(77)
+    shapes = [(128, 16, 2048), (129, 1025, 2049), (333, 3001, 2307), (1, 7, 5), (700, 2048, 2560)]
+    try:
+        for m, k, n in shapes:
+            big_a = ctx.fill(P.DIST_NORMAL, 11 + m, m + 2, k + 5, dtype=T.float32)
+            B = ctx.fill(P.DIST_NORMAL, 12 + m, k, n, dtype=T.float32)
+            for A in (big_a[1:m + 1, 3:k + 3], big_a[:m, :k].contiguous()):
+                ctx.tune("MMWS_GPU_SGEMM_AT", "0")
+                want = ctx.sgemm(A, B)
+                assert "k-major" not in ctx.last_plan
+                ctx.tune("MMWS_GPU_SGEMM_AT", "1")
+                got = ctx.sgemm(A, B)
+                assert "k-major" in ctx.last_plan
+                assert bool((got.view(T.int32) == want.view(T.int32)).all()), (m, k, n)
+                if k > 1024:  # accumulate continuation at the 1024-k chunk
+                    C = ctx.sgemm(A[:, :1024], B[:1024])
+                    ctx.sgemm(A[:, 1024:], B[1024:], C, accumulate=C)
+                    assert bool((C.view(T.int32) == want.view(T.int32)).all()), (m, k, n)
+        # the size rule: from n = 2048 (and at least one 128-row tile)
+        ctx.tune("MMWS_GPU_SGEMM_AT", None)
+        A = ctx.fill(P.DIST_NORMAL, 1, 256, 64, dtype=T.float32)
+        for n, want_at in ((2047, False), (2048, True)):
+            ctx.sgemm(A, ctx.fill(P.DIST_NORMAL, 2, 64, n, dtype=T.float32))
+            assert ("k-major" in ctx.last_plan) == want_at, (n, ctx.last_plan)
+        rows = [0, 127, 255]
+        Bn = ctx.fill(P.DIST_NORMAL, 2, 64, 2048, dtype=T.float32)
+        got = host(ctx.sgemm(A, Bn))
+        ref = oracle.matmul_rows(rows, host(A).astype(np.float64), host(Bn).astype(np.float64))
+        assert normwise(got[rows].astype(np.float64), ref) <= FP32_TOL
+    finally:
+        ctx.tune("MMWS_GPU_SGEMM_AT", None)
+
+
 def test_graph_keeps_its_own_workspace(ctx, oracle):
     # a graph whose multiply packs its operands must not
     # share the context's workspace -- an eager call that regrows it, or runs
