@@ -249,10 +249,10 @@ Schedule make_schedule(int64_t m, int64_t n, int64_t k, int P, bool panels, bool
 // the same decision without exchanging anything): the measured B200 peer
 // copy bandwidth per direction (B200_PROFILING.md: 770 GB/s) and the
 // measured 1-GPU multiply rates of this library (DMMA 36.3
-// TFLOP/s at N=16384, FFMA2 65.5 TFLOP/s at N=32768), 60 us of collective
+// TFLOP/s at N=16384, FFMA2 67 TFLOP/s at N=32768), 60 us of collective
 // latency per round.
 constexpr double PLAN_LINK_BPS = 770e9;
-constexpr double PLAN_FP64_FLOPS = 36.3e12, PLAN_FP32_FLOPS = 65.5e12;
+constexpr double PLAN_FP64_FLOPS = 36.3e12, PLAN_FP32_FLOPS = 67e12;
 constexpr double PLAN_ROUND_LATENCY_S = 60e-6;
 
 // force: 0 cost model, -1 every rank, 1 rank 0 alone (MMWS_GPU_ROWBLOCK_RANKS)

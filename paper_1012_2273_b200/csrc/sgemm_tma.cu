@@ -16,7 +16,7 @@
 // Structure (like the DMMA kernel, so the math warps do nothing but LDS +
 // FFMA2):
 //   * a producer warpgroup (one elected lane) streams A[128 x 16] and
-//     B[16 x 256] k-slices with TMA into a 4-stage mbarrier ring and gives its
+//     B[16 x 256] k-slices with TMA into a 3-stage mbarrier ring and gives its
 //     registers to the math warps (setmaxnreg 40 / 232);
 //   * 8 math warps, each lane owning 8 rows x 16 columns (64 packed fp32 pairs)
 //     -- 64 FFMA2 per k against 6 LDS.128 (A as 4-k vectors of one row,
@@ -35,7 +35,8 @@
 // keeps its register (tools/ffma2_lds_probe.cu, profiles/r02_ffma2_lds_probe.txt).
 // Hence the AT instance: wide problems transpose A once (transpose_f32_kernel,
 // HBM-bound, 0.17 % of the multiply at N=32768) and TMA stages A^T tiles;
-// N=16384 65.0 vs 62.3 TFLOP/s, same bits (profiles/r02_sgemm_k_major.txt).
+// N=16384 65.0 vs 62.3 TFLOP/s, same bits (profiles/r02_sgemm_k_major.txt);
+// 66.4 with the 3-stage ring.
 // Layouts TMA cannot read are packed by the caller (mmws_gpu.cu), so every
 // layout takes this kernel.
 #include "common.cuh"
@@ -61,9 +62,19 @@ __device__ __forceinline__ void ffma2(f32x2& d, f32x2 a, f32x2 b) {
   asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
 }
 
-constexpr int BM = 128, BN = 256, BK = 16, STAGES = 4, CONSUMERS = 8;
+// k per stage and ring depth (build-time, for tuning runs: make EXTRA=-D...).
+// The ring depth is not a limit (2, 3 and 4 stages of 16 k: 66.0 / 67.2 / 66.0
+// TFLOP/s at N=32768; 8-k stages lose 8 %: profiles/r02_sgemm_ring_geometry.txt);
+// 3 stages is the instance ptxas schedules best.
+#ifndef MMWS_SGEMM_BK
+#define MMWS_SGEMM_BK 16
+#endif
+#ifndef MMWS_SGEMM_STAGES
+#define MMWS_SGEMM_STAGES 3
+#endif
+constexpr int BM = 128, BN = 256, BK = MMWS_SGEMM_BK, STAGES = MMWS_SGEMM_STAGES, CONSUMERS = 8;
 constexpr int THREADS = (CONSUMERS + 4) * 32;
-constexpr int KC_STAGES = 64;  // partial-sum chunk = 64 stages = 1024 k
+constexpr int KC_STAGES = 1024 / BK;  // partial-sum chunk = 1024 k
 constexpr int A_BYTES = BM * BK * 4, B_BYTES = BK * BN * 4;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TOT_BYTES = CONSUMERS * 32 * 128 * 4;  // 128 floats per math lane
