@@ -147,7 +147,10 @@ __global__ void __launch_bounds__(THREADS, 1)
 // (round 2, tools/exact_plan_probe.py) N=256 12.4 -> 10.4 us, 300 14.4 ->
 // 12.4, 400 24.7 -> 21.3, 500 32.1 -> 26.8; on the 64x64 tile 4 warps lose
 // (N=640 52.7 vs 55.1, 1000 stream-K 140.1 vs 148.4).
-constexpr int T_STAGES = 4;
+#ifndef MMWS_EXACT_STAGES  // ring depth of the TMA variant (build-time, for tuning runs)
+#define MMWS_EXACT_STAGES 4
+#endif
+constexpr int T_STAGES = MMWS_EXACT_STAGES;
 template <int TBM, int TBN, int CONS = 8>
 struct ExactTma {
   static constexpr int A_BYTES = TBM * BK * 8, B_BYTES = BK * TBN * 8;
