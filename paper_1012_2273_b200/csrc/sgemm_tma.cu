@@ -258,7 +258,9 @@ __global__ void __launch_bounds__(256)
     transpose_f32_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, int64_t ld_src,
                          float* __restrict__ dst, int64_t ld_dst) {
   __shared__ float tile[32][33];
-  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 32, r0 = static_cast<int64_t>(blockIdx.y) * 32;
+  // 1-D grid (no 65535 limit on either dimension), column tiles fastest
+  const int64_t tiles_c = (cols + 31) / 32;
+  const int64_t c0 = (blockIdx.x % tiles_c) * 32, r0 = (blockIdx.x / tiles_c) * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
 #pragma unroll
   for (int j = 0; j < 32; j += 8) {
@@ -295,8 +297,10 @@ bool sgemm_tma_supported(int64_t lda, int64_t ldb, const float* A, const float* 
 
 cudaError_t launch_transpose_f32(const Launch& L, const float* src, int64_t rows, int64_t cols,
                                  int64_t ld_src, float* dst, int64_t ld_dst) {
-  const dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
-  transpose_f32_kernel<<<grid, 256, 0, L.stream>>>(src, rows, cols, ld_src, dst, ld_dst);
+  const int64_t tiles = ((cols + 31) / 32) * ((rows + 31) / 32);
+  if (tiles > 0x7fffffffLL) return cudaErrorInvalidValue;
+  transpose_f32_kernel<<<static_cast<unsigned>(tiles), 256, 0, L.stream>>>(src, rows, cols, ld_src,
+                                                                          dst, ld_dst);
   L.count();
   return cudaGetLastError();
 }

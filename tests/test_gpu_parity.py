@@ -1141,6 +1141,17 @@ def test_fp32_k_major_staging_is_bitwise_the_row_major_kernel(ctx, oracle):
                     C = ctx.sgemm(A[:, :1024], B[:1024])
                     ctx.sgemm(A[:, 1024:], B[1024:], C, accumulate=C)
                     assert bool((C.view(T.int32) == want.view(T.int32)).all()), (m, k, n)
+        # more than 65535 * 32 rows: the transposition runs on a 1-D grid
+        m, k, n = 2_200_000, 4, 2048
+        A = ctx.fill(P.DIST_NORMAL, 3, m, k, dtype=T.float32)
+        B = ctx.fill(P.DIST_NORMAL, 4, k, n, dtype=T.float32)
+        ctx.tune("MMWS_GPU_SGEMM_AT", "0")
+        want = ctx.sgemm(A, B)
+        ctx.tune("MMWS_GPU_SGEMM_AT", "1")
+        got = ctx.sgemm(A, B)
+        assert bool(T.equal(got.view(T.int32), want.view(T.int32)))
+        del want, got, A, B
+        T.cuda.empty_cache()
         # the size rule: from n = 2048 (and at least one 128-row tile)
         ctx.tune("MMWS_GPU_SGEMM_AT", None)
         A = ctx.fill(P.DIST_NORMAL, 1, 256, 64, dtype=T.float32)
