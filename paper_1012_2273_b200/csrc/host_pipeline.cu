@@ -382,7 +382,7 @@ int host_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A
 
   // Row panels (multiples of 128 rows) once the problem is big enough for the
   // overlap to matter (m*n*k >= 1e8); one panel otherwise.  Pinned buffers:
-  // 1/8 of the rows (host-buffer multiply, min of 25 interleaved calls: N=750
+  // 1/8 of the rows, 1/16 from m*n*k = 1e13 (host-buffer multiply, min of 25 interleaved calls: N=750
   // 260.5 vs 292.4 us in one panel, 1000 415.2 vs 514.7, 1250 648.5 vs
   // 818.8).  Pageable buffers: every panel's copy is pumped through the
   // pinned staging ring by the host copy pool in chunks of its own, so fewer,
@@ -395,7 +395,7 @@ int host_multiply(mmws_gpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A
   // MMWS_GPU_HOST_PANELS overrides the count; the bits never change.
   const double work = static_cast<double>(m) * n * k;
   const bool pinned = !is_pageable(A) && !is_pageable(C);
-  int want = work < 1.0e8 ? 1 : 8;
+  int want = work < 1.0e8 ? 1 : work < 1.0e13 ? 8 : 16;  // fp32 N=32768: 1085 vs 1106 ms (tools/f32_host_panels_probe.py)
   if (!pinned && want > 1) want = work < 1.5e9 ? 4 : work < 4.5e9 ? 2 : work < 1.5e10 ? 3 : 8;
   if (ctx->tune.host_panels > 0 && work >= 1.0e7) want = ctx->tune.host_panels;
   // small MODE_OZAKI problems would recompute B's residues per launch: one panel
