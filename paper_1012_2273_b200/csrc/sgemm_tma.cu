@@ -66,6 +66,9 @@ __device__ __forceinline__ void ffma2(f32x2& d, f32x2 a, f32x2 b) {
 // The ring depth is not a limit (2, 3 and 4 stages of 16 k: 66.0 / 67.2 / 66.0
 // TFLOP/s at N=32768; 8-k stages lose 8 %: profiles/r02_sgemm_ring_geometry.txt);
 // 3 stages is the instance ptxas schedules best.
+#ifndef MMWS_SGEMM_GROUP
+#define MMWS_SGEMM_GROUP 8
+#endif
 #ifndef MMWS_SGEMM_BK
 #define MMWS_SGEMM_BK 16
 #endif
@@ -97,7 +100,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* empty = full + STAGES;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int GROUP = 8;
+  constexpr int GROUP = MMWS_SGEMM_GROUP;  // tile rows per raster group
   const int tile = blockIdx.x;
   const int per_group = GROUP * tiles_n;
   const int first_m = (tile / per_group) * GROUP;
