@@ -1,6 +1,6 @@
 """Time-boxed randomized parity sweep against the CPU oracle (test
 infrastructure, like tests/): random shapes (1..1600, skewed small), padded /
-odd row pitches, every fp64 mode, fp32, accumulate in k-panels, host-buffer
+odd row pitches, every fp64 mode, fp32 (both A stagings), accumulate in k-panels, host-buffer
 entries (pageable and pinned) and graph replay; uniform, integer and normal
 inputs.  EXACT and integer inputs must be bitwise matmul_seq; tensor modes
 <= 1e-12 normwise (OZAKI <= 1e-13 on sampled rows), fp32 <= 1e-5.  Prints one
@@ -141,7 +141,18 @@ while time.time() < t_end:
     # fp32
     af, bf = a.astype(np.float32), b.astype(np.float32)
     Af, Bf = padded(af, pa, torch.float32), padded(bf, pb, torch.float32)
-    gotf = ctx.sgemm(Af, Bf).cpu().numpy().astype(np.float64)
+    # A staged as it lies / transposed and staged k-major (default: by size):
+    # the same bits either way
+    ctx.tune("MMWS_GPU_SGEMM_AT", "1")
+    got_at = ctx.sgemm(Af, Bf)
+    ctx.tune("MMWS_GPU_SGEMM_AT", "0")
+    got_rm = ctx.sgemm(Af, Bf)
+    ctx.tune("MMWS_GPU_SGEMM_AT", None)
+    counts["sgemm_k_major_bitwise"] = counts.get("sgemm_k_major_bitwise", 0) + 1
+    if not bool(torch.equal(got_at.view(torch.int32), got_rm.view(torch.int32))):
+        fails.append({"case": case, "what": "sgemm k-major vs row-major", "shape": [m, k, n],
+                      "pads": [pa, pb]})
+    gotf = (got_at if case % 2 else ctx.sgemm(Af, Bf)).cpu().numpy().astype(np.float64)
     wantf = O.matmul_rows(rows, af, bf)
     counts["sgemm"] = counts.get("sgemm", 0) + 1
     g = gotf[rows]
