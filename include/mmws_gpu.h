@@ -99,7 +99,8 @@ enum {
 
 /* Peak probes (mmws_gpu_peak_probe).  FFMA2_OUTER is the fp32 GEMM's own
  * operand pattern (a fresh broadcast register operand per FFMA2) in registers
- * only -- the ceiling of any FFMA2 GEMM, below the plain FFMA2 peak. */
+ * only -- one such loop, below the plain FFMA2 peak; not a ceiling (its rate
+ * depends on the register assignment). */
 enum {
   MMWS_GPU_PROBE_DMMA = 0,
   MMWS_GPU_PROBE_DFMA = 1,

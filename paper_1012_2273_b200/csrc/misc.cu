@@ -86,9 +86,9 @@ cudaError_t launch_pack(const Launch& L, const T* src, int64_t rows, int64_t col
 // The fp32 GEMM kernel's operand pattern in registers only (sgemm_tma.cu):
 // 8 warps per SM, 64 accumulator pairs per lane, B pairs reused across 8
 // consecutive FFMA2, the broadcast A scalar fresh from the register file each
-// time.  Its rate is the ceiling of any GEMM built from this pattern (the
-// extra register-file read per FFMA2 is what the plain FFMA2 probe does not
-// pay).
+// time.  One loop of that pattern, not a ceiling: such loops measure 56-71
+// TFLOP/s depending on block shape and register assignment, and the kernel
+// with A staged k-major runs above this one.
 __global__ void __launch_bounds__(256, 1) ffma2_outer_probe_kernel(int iters, double* sink) {
   typedef unsigned long long u64;
   auto pk = [](float a, float b) {
