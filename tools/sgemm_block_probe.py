@@ -1,6 +1,7 @@
-"""fp32 kernel per-lane block shapes (MMWS_GPU_SGEMM_AT = 0: A staged as it lies, 1: A transposed first and
-staged k-major): rate at the given N and a sha256 of a ragged product
-(both must give the same bits).  Run once per value of the knob.
+"""fp32 kernel with A staged as it lies (MMWS_GPU_SGEMM_AT=0) or transposed and
+staged k-major (=1; unset: the size rule): rate at the given N and a sha256 of
+two ragged products (both stagings, and any rebuild with other ring geometries,
+must give the same bits).  Run once per value of the knob.
 Usage: MMWS_GPU_SGEMM_AT=1 python tools/sgemm_block_probe.py [N ...]"""
 import hashlib
 import os
